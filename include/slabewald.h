@@ -1,0 +1,138 @@
+/*
+ * slabewald.h — C-ABI of the B200-native doubly periodic spectral Ewald
+ * solver (arXiv 2101.07088), libslabewald_cuda.so.
+ *
+ * The reference has no FFI: its boundary is the Python class API
+ *   SlabSolver(system, params, threads=1, refine=1)      slab.py:197
+ *   SlabSolver.solve(positions=None, need_energy=True, need_forces=True,
+ *                    need_potential=True, subtract_self=False,
+ *                    include_correction=True, force_general=False)
+ *                                                         slab.py:259-261
+ *   near_field_sum(...)                                   slab.py:184-191
+ *   build_partition(...)                                  slab.py:51-82
+ * Each entry point below replaces the compute behind one of those calls; the
+ * Python package paper_2101_07088_b200 (slab.py) binds them with ctypes and
+ * keeps the reference's signatures, exceptions and diagnostics keys.
+ *
+ * Conventions: plain pointers and sizes only.  "host" buffers are caller
+ * owned and only read/written during the call; "device" buffers are device
+ * pointers on the plan's device.  Positions are [n][3] row-major doubles,
+ * fields [n][3].  A plan is not thread safe: one call at a time.  All calls
+ * return SE_OK or an error code; se_last_error() gives the message.
+ */
+#ifndef SLABEWALD_H
+#define SLABEWALD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error codes -> Python exception (slab.py maps them) */
+#define SE_OK          0
+#define SE_ERR_VALUE   1  /* ValueError (bad input, point outside z domain) */
+#define SE_ERR_FLOAT   2  /* FloatingPointError (non-finite mismatch, k=0)  */
+#define SE_ERR_LINALG  3  /* numpy.linalg.LinAlgError (Schur conditioning)  */
+#define SE_ERR_CUDA    4  /* RuntimeError (CUDA / cuFFT failure)            */
+#define SE_ERR_MEMORY  5  /* MemoryError (device allocation)                */
+
+/* solve flags (defaults of SlabSolver.solve are ENERGY|FORCES|POTENTIAL|CORRECTION) */
+#define SE_NEED_ENERGY     (1u << 0)
+#define SE_NEED_FORCES     (1u << 1)
+#define SE_NEED_POTENTIAL  (1u << 2)
+#define SE_SUBTRACT_SELF   (1u << 3)
+#define SE_CORRECTION      (1u << 4)
+#define SE_FORCE_GENERAL   (1u << 5)
+#define SE_TIMINGS         (1u << 6)   /* fill se_diag.t_ms (adds syncs) */
+
+/* Solver parameters: the geometry plus the EwaldParams fields the device
+ * path needs (params.py:28-50). */
+typedef struct {
+    double Lx, Ly, H, eps, eps_b, eps_t;
+    double g_w, xi, g_t, H_E, r_nf, r_cut, k_max, z0, z1;
+    double xi_is_inf;          /* 1.0 when xi == inf (no near field) */
+    int32_t Nx, Ny, Nz, refine;
+} se_params;
+
+/* Diagnostics of one solve (slab.py:275,332,384-385 keys + timings). */
+typedef struct {
+    double ai1, ai2, discrepancy, B_i;
+    double A_i, A_b, A_t, psi_i_bottom, psi_i_top, psi_b_bottom, psi_t_top;
+    double U_wall;             /* wall-charge energy part of U (0 if sigma=0) */
+    int32_t warn_discrepancy;  /* 1 when 1e-3 < discrepancy <= 1e-2 */
+    int32_t n_sources;         /* spread sources (charges + images) */
+    int64_t n_pairs;           /* near-field pairs evaluated for the charges */
+    int64_t n_launches;        /* own kernels launched by this call */
+    double t_ms[16];           /* stage timings when SE_TIMINGS */
+} se_diag;
+
+typedef struct se_plan se_plan;
+
+/* SlabSolver.__init__ (slab.py:197-233).  Host arrays computed by the
+ * Python planner exactly as the reference does (bit-identical constants):
+ *   z_nodes[Nz]  ascending Chebyshev points   (chebyshev.py:14-19)
+ *   cc_w[Nz]     Clenshaw-Curtis weights      (chebyshev.py:22-43)
+ *   t_wall0[Nz], t_wallH[Nz]  T_n(z=0), T_n(z=H) (slab.py:214-222)
+ *   kx[Nx], ky[Ny]            fft-ordered wavenumbers (chebyshev.py:98-102)
+ *   sigma_b, sigma_t          [Nx][Ny] wall charge samples or NULL (zero)
+ * device: CUDA ordinal.  Factorises the per-|k| BVPs on the device; an
+ * ill-conditioned Schur block returns SE_ERR_LINALG (bvp.py:187-192). */
+int se_plan_create(const se_params* params, const double* z_nodes,
+                   const double* cc_w, const double* t_wall0,
+                   const double* t_wallH, const double* kx, const double* ky,
+                   const double* sigma_b, const double* sigma_t, int device,
+                   se_plan** out);
+
+void se_plan_destroy(se_plan* plan);
+
+/* Bind the charges (system.charges, slab.py:274).  host q[n]. */
+int se_set_charges(se_plan* plan, const double* q, int64_t n);
+
+/* SlabSolver.solve with host buffers (positions in, results out):
+ * pos[n][3] -> phi_bar[n], E_bar[n][3] (may be NULL without FORCES), U. */
+int se_solve(se_plan* plan, const double* pos, int64_t n, uint32_t flags,
+             double* phi_bar, double* E_bar, double* U, se_diag* diag);
+
+/* Same with device-resident positions and outputs (no host copies; the
+ * stream is synchronised before return). */
+int se_solve_device(se_plan* plan, const double* d_pos, int64_t n,
+                    uint32_t flags, double* d_phi_bar, double* d_E_bar,
+                    double* U, se_diag* diag);
+
+/* near_field_sum (slab.py:184-191): sources = pos[n] with charges q[n]
+ * (plus the mirrored layers of the geometry in params), evaluated at
+ * eval_pos[ne].  kind 0 = "avg" (r_cut), 1 = "point" (r_nf).  Host buffers.
+ * E may be NULL when need_field == 0.  No plan needed (grid fields of
+ * params are ignored). */
+int se_near_field(const se_params* params, int device, const double* pos,
+                  const double* q, int64_t n, const double* eval_pos,
+                  int64_t ne, int kind, int need_field, int subtract_unsplit,
+                  double* phi, double* E);
+
+/* build_partition (slab.py:51-82).  Host in/out; index arrays int64, sized
+ * by the caller for the worst case (n over/far, 2n images).  Counts out. */
+int se_build_partition(const se_params* params, int device, const double* pos,
+                       const double* q, int64_t n, int64_t* n_over,
+                       int64_t* over, int64_t* n_far, int64_t* far,
+                       int64_t* n_img, double* img_pos, double* img_str,
+                       int64_t* img_src, int32_t* img_wall);
+
+/* Stage buffers of the last solve, for parity tests (host copy):
+ * 0 rho[Nz][2][Nx][Ny] (slot 0 = over, 1 = in), 1 psi coefficients
+ * [Nz][2][Nx][Ny/2+1] complex (slot 0 = psi_o, 1 = psi_i) — only when the
+ * plan was created with SE_KEEP_STAGES=1 in the environment, 2 field grids
+ * [Nz][4][Nx][Ny] (inverse xy FFTs of psi, i kx psi, i ky psi, dpsi/dz
+ * before the signs and the k = 0 A_i terms), 3 mismatch fields
+ * [4][Nx][Ny/2+1] complex (phi_b, e_b, phi_t, e_t), 4 far-field interpolation
+ * sums [4][N], 5 near-field sums [4][N].
+ * Returns the byte size when host == NULL. */
+int64_t se_debug_fetch(se_plan* plan, int which, void* host, int64_t nbytes);
+
+const char* se_last_error(void);
+const char* se_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLABEWALD_H */

@@ -1,0 +1,51 @@
+"""Build libslabewald_cuda.so in-tree with nvcc for sm_100a.
+
+Used by ``__graft_entry__.build()``, the tests and ``python -m
+paper_2101_07088_b200._build``.  The library links cuFFT dynamically with an
+rpath to the CUDA toolkit in this image (the GPU box runs the same image).
+"""
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libslabewald_cuda.so")
+SOURCES = ["se_api.cu", "se_grid.cu", "se_spectral.cu", "se_near.cu"]
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _stale():
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    deps.append(os.path.join(os.path.dirname(HERE), "include", "slabewald.h"))
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force=False, verbose=False):
+    """Compile the CUDA library if a source is newer than the .so."""
+    if not force and not _stale():
+        return LIB
+    cmd = [NVCC, "-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
+           "-shared", "-Xptxas", "-v" if verbose else "-O3",
+           "-o", LIB + ".tmp"]
+    cmd += [os.path.join(CSRC, f) for f in SOURCES]
+    cmd += ["-L" + os.path.join(CUDA_HOME, "lib64"), "-lcufft",
+            "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64")]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libslabewald_cuda.so")
+    if verbose:
+        sys.stderr.write(res.stderr)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,143 @@
+"""ctypes binding of libslabewald_cuda.so (include/slabewald.h).
+
+The library is built in-tree (``_build.py``); there is no fallback: if it
+cannot be loaded the solver raises.  Structures mirror the C declarations
+field for field.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libslabewald_cuda.so")
+
+SE_OK = 0
+SE_ERR_VALUE, SE_ERR_FLOAT, SE_ERR_LINALG, SE_ERR_CUDA, SE_ERR_MEMORY = \
+    1, 2, 3, 4, 5
+
+NEED_ENERGY = 1 << 0
+NEED_FORCES = 1 << 1
+NEED_POTENTIAL = 1 << 2
+SUBTRACT_SELF = 1 << 3
+CORRECTION = 1 << 4
+FORCE_GENERAL = 1 << 5
+TIMINGS = 1 << 6
+
+#: every entry point declared in include/slabewald.h
+EXPORTS = ("se_plan_create", "se_plan_destroy", "se_set_charges", "se_solve",
+           "se_solve_device", "se_near_field", "se_build_partition",
+           "se_debug_fetch", "se_last_error", "se_version")
+
+
+class SeParams(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in (
+        "Lx", "Ly", "H", "eps", "eps_b", "eps_t", "g_w", "xi", "g_t", "H_E",
+        "r_nf", "r_cut", "k_max", "z0", "z1", "xi_is_inf")] + \
+        [(n, ctypes.c_int32) for n in ("Nx", "Ny", "Nz", "refine")]
+
+
+class SeDiag(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in (
+        "ai1", "ai2", "discrepancy", "B_i", "A_i", "A_b", "A_t",
+        "psi_i_bottom", "psi_i_top", "psi_b_bottom", "psi_t_top",
+        "U_wall")] + [
+        ("warn_discrepancy", ctypes.c_int32), ("n_sources", ctypes.c_int32),
+        ("n_pairs", ctypes.c_int64), ("n_launches", ctypes.c_int64),
+        ("t_ms", ctypes.c_double * 16)]
+
+
+_P = ctypes.c_void_p
+_D = ctypes.POINTER(ctypes.c_double)
+_I64 = ctypes.c_int64
+_I64P = ctypes.POINTER(ctypes.c_int64)
+_I32P = ctypes.POINTER(ctypes.c_int32)
+
+_lib = None
+
+
+def load():
+    """Load (once) and return the library; raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            "libslabewald_cuda.so is not built (%s); run "
+            "`python -m paper_2101_07088_b200._build`" % LIB_PATH)
+    lib = ctypes.CDLL(LIB_PATH)
+    lib.se_plan_create.argtypes = [ctypes.POINTER(SeParams), _D, _D, _D, _D,
+                                   _D, _D, _D, _D, ctypes.c_int,
+                                   ctypes.POINTER(_P)]
+    lib.se_plan_create.restype = ctypes.c_int
+    lib.se_plan_destroy.argtypes = [_P]
+    lib.se_plan_destroy.restype = None
+    lib.se_set_charges.argtypes = [_P, _D, _I64]
+    lib.se_set_charges.restype = ctypes.c_int
+    lib.se_solve.argtypes = [_P, _D, _I64, ctypes.c_uint32, _D, _D, _D,
+                             ctypes.POINTER(SeDiag)]
+    lib.se_solve.restype = ctypes.c_int
+    lib.se_solve_device.argtypes = [_P, ctypes.c_void_p, _I64,
+                                    ctypes.c_uint32, ctypes.c_void_p,
+                                    ctypes.c_void_p, _D,
+                                    ctypes.POINTER(SeDiag)]
+    lib.se_solve_device.restype = ctypes.c_int
+    lib.se_near_field.argtypes = [ctypes.POINTER(SeParams), ctypes.c_int, _D,
+                                  _D, _I64, _D, _I64, ctypes.c_int,
+                                  ctypes.c_int, ctypes.c_int, _D, _D]
+    lib.se_near_field.restype = ctypes.c_int
+    lib.se_build_partition.argtypes = [ctypes.POINTER(SeParams), ctypes.c_int,
+                                       _D, _D, _I64, _I64P, _I64P, _I64P,
+                                       _I64P, _I64P, _D, _D, _I64P, _I32P]
+    lib.se_build_partition.restype = ctypes.c_int
+    lib.se_debug_fetch.argtypes = [_P, ctypes.c_int, ctypes.c_void_p, _I64]
+    lib.se_debug_fetch.restype = ctypes.c_int64
+    lib.se_last_error.argtypes = []
+    lib.se_last_error.restype = ctypes.c_char_p
+    lib.se_version.argtypes = []
+    lib.se_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def check(code):
+    """Map a library error code to the reference's exception type."""
+    if code == SE_OK:
+        return
+    msg = load().se_last_error().decode()
+    if code == SE_ERR_VALUE:
+        raise ValueError(msg)
+    if code == SE_ERR_FLOAT:
+        raise FloatingPointError(msg)
+    if code == SE_ERR_LINALG:
+        raise np.linalg.LinAlgError(msg)
+    if code == SE_ERR_MEMORY:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def dptr(a):
+    """double* of a C-contiguous float64 array (or None)."""
+    if a is None:
+        return None
+    return a.ctypes.data_as(_D)
+
+
+def as_f64(a, shape=None):
+    out = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None:
+        out = out.reshape(shape)
+    return out
+
+
+def params_struct(geometry, params, refine=1):
+    xi_inf = bool(np.isinf(params.xi))
+    return SeParams(
+        Lx=geometry.Lx, Ly=geometry.Ly, H=geometry.H, eps=geometry.eps,
+        eps_b=geometry.eps_b, eps_t=geometry.eps_t, g_w=params.g_w,
+        xi=float(params.xi), g_t=params.g_t, H_E=params.H_E,
+        r_nf=params.r_nf, r_cut=params.r_cut, k_max=params.k_max,
+        z0=params.z0, z1=params.z1, xi_is_inf=1.0 if xi_inf else 0.0,
+        Nx=int(params.Nx), Ny=int(params.Ny), Nz=int(params.Nz),
+        refine=int(refine))

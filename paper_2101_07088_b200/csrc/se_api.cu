@@ -1,0 +1,581 @@
+// C-ABI of libslabewald_cuda.so: plan lifetime and the solve orchestration.
+//
+// Reference: SlabSolver.__init__ (slab.py:197-233) and SlabSolver.solve
+// (slab.py:259-394); near_field_sum (slab.py:184-191); build_partition
+// (slab.py:51-82).  See include/slabewald.h for the contract.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "se_internal.cuh"
+
+namespace se {
+
+static thread_local std::string g_error;
+
+void dfree(Plan* p, void* ptr) {
+    if (!ptr) return;
+    for (auto& b : p->owned)
+        if (b.p == ptr) {
+            cudaFree(ptr);
+            b.p = nullptr;
+            return;
+        }
+}
+
+namespace {
+
+__global__ void scale_complex(cufftDoubleComplex* a, int64_t n, double s) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) { a[i].x *= s; a[i].y *= s; }
+}
+
+__global__ void gauge_kernel(double* scal) {
+    // B_i = -(far0 + near0)                                  slab.py:380-383
+    scal[1] = -(scal[4] + scal[5]);
+}
+
+int fail(const Error& e) {
+    g_error = e.what();
+    return e.code;
+}
+
+void make_plan2d(cufftHandle* h, int nx, int ny, int nyh, cufftType type,
+                 int64_t idist, int64_t odist, int batch, cudaStream_t s) {
+    int real_embed[2] = {nx, ny};
+    int cplx_embed[2] = {nx, nyh};
+    int* in_e = (type == CUFFT_D2Z) ? real_embed : cplx_embed;
+    int* out_e = (type == CUFFT_D2Z) ? cplx_embed : real_embed;
+    SE_CUFFT(cufftCreate(h));
+    size_t ws = 0;
+    long long nn[2] = {nx, ny}, ie[2] = {in_e[0], in_e[1]}, oe[2] = {out_e[0], out_e[1]};
+    SE_CUFFT(cufftMakePlanMany64(*h, 2, nn, ie, 1, idist, oe, 1, odist, type, batch, &ws));
+    SE_CUFFT(cufftSetStream(*h, s));
+}
+
+void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
+                double* d_phi_out, double* d_E_out, double* U, se_diag* diag) {
+    p->launches = 0;
+    if (n != p->N)
+        throw Error(SE_ERR_VALUE, "positions and charges disagree on N");
+    const se_params& P = p->P;
+    const bool xi_inf = P.xi_is_inf != 0.0;
+    const bool forces = flags & SE_NEED_FORCES;
+    const bool potential = flags & SE_NEED_POTENTIAL;
+    const bool energy = flags & SE_NEED_ENERGY;
+    const bool corr = flags & SE_CORRECTION;
+    const bool jumps = P.eps_b != P.eps || P.eps_t != P.eps || (flags & SE_FORCE_GENERAL);
+    const bool two = corr && jumps;
+    const int mode = two ? 0 : (corr ? 1 : 2);
+    const bool near_empty = (n == 0) || xi_inf;
+    if (!near_empty && P.r_cut >= 0.5 * std::min(P.Lx, P.Ly))
+        throw Error(SE_ERR_VALUE, "near-field cutoff exceeds half the periodic box");
+    cudaStream_t s = p->stream;
+    SE_CUDA(cudaMemsetAsync(p->d_flags, 0, sizeof(int), s));
+    SE_CUDA(cudaMemsetAsync(p->d_scal, 0, 8 * sizeof(double), s));
+    SE_CUDA(cudaMemsetAsync(p->d_count, 0, sizeof(int64_t), s));
+
+    cudaEvent_t ev[12];
+    const bool timed = flags & SE_TIMINGS;
+    if (timed) for (auto& e : ev) SE_CUDA(cudaEventCreate(&e));
+    int ne = 0;
+    auto mark = [&]() { if (timed) SE_CUDA(cudaEventRecord(ev[ne++], s)); };
+
+    mark();
+    // ---- far field: spread, transforms, mode BVPs, correction, inverse
+    build_sources(p, d_pos, n, two);
+    mark();
+    spread(p, two);
+    mark();
+    forward_transforms(p, two);
+    mark();
+    bvp_solve(p, two, mode, corr);
+    mark();
+    inverse_transforms(p, forces, corr);
+    mark();
+    interp_charges(p, n, forces);
+    mark();
+    // ---- near field
+    const double eps = P.eps, inv4pie = 1.0 / (4.0 * M_PI * eps);
+    const double two_sqrtpi = 2.0 / std::sqrt(M_PI);
+    NearKernel kavg{}, kpt{};
+    if (!xi_inf) {
+        kavg.c1 = 2.0 * P.g_w;
+        kavg.c2 = std::sqrt(4.0 * P.g_w * P.g_w + 1.0 / (P.xi * P.xi));
+        kavg.inv4pie = inv4pie;
+        kavg.radius = P.r_cut;
+        kavg.self_value = (flags & SE_SUBTRACT_SELF)
+                              ? -two_sqrtpi / kavg.c2 / (4.0 * M_PI * eps)
+                              : two_sqrtpi * (0.5 / P.g_w - 1.0 / kavg.c2) / (4.0 * M_PI * eps);
+        kavg.kind = 0;
+        kavg.need_field = forces ? 1 : 0;
+        kpt.c1 = std::sqrt(2.0) * P.g_w;
+        kpt.c2 = std::sqrt(2.0 * P.g_w * P.g_w + 1.0 / (P.xi * P.xi));
+        kpt.inv4pie = inv4pie;
+        kpt.radius = P.r_nf;
+        kpt.point0 = (two_sqrtpi / kpt.c1 - two_sqrtpi / kpt.c2) / (4.0 * M_PI * eps);
+        kpt.kind = 1;
+        kpt.need_field = 0;
+    }
+    if (!near_empty) {
+        build_cells(p, d_pos, p->d_q, n);
+        near_eval(p, d_pos, p->d_tgt, n, kavg, p->d_near, p->d_count);
+    } else {
+        SE_CUDA(cudaMemsetAsync(p->d_near, 0, sizeof(double) * 4 * (size_t)std::max<int64_t>(n, 1), s));
+    }
+    mark();
+    // ---- gauge: pointwise potential vanishes at the origin
+    if (potential && !xi_inf) {
+        const double w = 0.5 / P.xi;
+        const double rad = (P.H_E / P.g_t) * w;
+        interp_points(p, p->d_origin, 1, w, rad, p->d_scal + 4);
+        if (!near_empty) near_eval(p, p->d_origin, nullptr, 1, kpt, p->d_scal + 5, nullptr);
+        gauge_kernel<<<1, 1, 0, s>>>(p->d_scal);
+        SE_LAUNCHED(p);
+    }
+    // ---- combine, energy
+    double self_inf = 0.0;
+    if (xi_inf) self_inf = -two_sqrtpi / (2.0 * P.g_w) / (4.0 * M_PI * eps);
+    if (n > 0) finalize(p, n, flags, self_inf, d_phi_out, d_E_out);
+    if (energy && !p->sigma_zero) {
+        if (xi_inf) throw Error(SE_ERR_VALUE, "wall-charge energy needs a finite xi");
+        if (near_empty && n == 0) {
+            // near field of no sources is zero; wall_energy handles cl.n == 0
+            p->cl.n = 0;
+        }
+        wall_energy(p, kpt);
+    }
+    mark();
+    // ---- results
+    double scal[8], k0[16];
+    int hflags = 0;
+    int64_t npairs = 0;
+    SE_CUDA(cudaMemcpyAsync(scal, p->d_scal, sizeof(scal), cudaMemcpyDeviceToHost, s));
+    SE_CUDA(cudaMemcpyAsync(k0, p->d_k0, sizeof(k0), cudaMemcpyDeviceToHost, s));
+    SE_CUDA(cudaMemcpyAsync(&hflags, p->d_flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SE_CUDA(cudaMemcpyAsync(&npairs, p->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SE_CUDA(cudaStreamSynchronize(s));
+    if (hflags & FLAG_Z_OUTSIDE) throw Error(SE_ERR_VALUE, "point outside the extended z domain");
+    if (hflags & FLAG_NONFINITE) throw Error(SE_ERR_FLOAT, "non-finite mismatch field");
+    if (hflags & FLAG_K0_FAIL) {
+        char buf[160];
+        snprintf(buf, sizeof buf,
+                 "k=0 coefficient mismatch %.2e: system not electroneutral or under-resolved",
+                 k0[2]);
+        throw Error(SE_ERR_FLOAT, buf);
+    }
+    if (U) *U = energy ? (n > 0 ? scal[2] : 0.0) + (p->sigma_zero ? 0.0 : scal[3]) : 0.0;
+    if (diag) {
+        diag->ai1 = k0[0]; diag->ai2 = k0[1]; diag->discrepancy = k0[2];
+        diag->A_i = k0[3]; diag->A_b = k0[4]; diag->A_t = k0[5];
+        diag->psi_i_bottom = k0[6]; diag->psi_i_top = k0[7];
+        diag->psi_b_bottom = k0[8]; diag->psi_t_top = k0[9];
+        diag->B_i = (potential && !xi_inf) ? scal[1] : 0.0;
+        diag->U_wall = p->sigma_zero ? 0.0 : scal[3];
+        diag->warn_discrepancy = (hflags & FLAG_K0_WARN) ? 1 : 0;
+        diag->n_sources = (int32_t)p->ss.S;
+        diag->n_pairs = npairs;
+        diag->n_launches = p->launches;
+        for (int i = 0; i < 16; ++i) diag->t_ms[i] = 0.0;
+        if (timed) {
+            for (int i = 0; i + 1 < ne && i < 16; ++i) {
+                float ms = 0;
+                SE_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+                diag->t_ms[i] = ms;
+            }
+        }
+    }
+    if (timed) for (auto& e : ev) cudaEventDestroy(e);
+}
+
+void ensure_charges(Plan* p, int64_t n) {
+    if (n <= p->q_cap && p->d_q) return;
+    void* olds[] = {p->d_q, p->d_pos, p->d_phi, p->d_E, p->d_far, p->d_near};
+    for (void* o : olds) dfree(p, o);
+    int64_t cap = std::max<int64_t>(n, 1);
+    p->d_q = dalloc<double>(p, cap);
+    p->d_pos = dalloc<double>(p, 3 * cap);
+    p->d_phi = dalloc<double>(p, cap);
+    p->d_E = dalloc<double>(p, 3 * cap);
+    p->d_far = dalloc<double>(p, 4 * cap);
+    p->d_near = dalloc<double>(p, 4 * cap);
+    p->q_cap = cap;
+}
+
+}  // namespace
+}  // namespace se
+
+using namespace se;
+
+extern "C" {
+
+const char* se_last_error(void) { return g_error.c_str(); }
+const char* se_version(void) { return "slabewald-b200 0.1.0 (sm_100a)"; }
+
+int se_plan_create(const se_params* params, const double* z_nodes, const double* cc_w,
+                   const double* t_wall0, const double* t_wallH, const double* kx,
+                   const double* ky, const double* sigma_b, const double* sigma_t,
+                   int device, se_plan** out) {
+    Plan* p = nullptr;
+    try {
+        if (!params || !out) throw Error(SE_ERR_VALUE, "null argument");
+        p = new Plan();
+        p->P = *params;
+        const se_params& P = p->P;
+        if (P.Nx < 1 || P.Ny < 1 || P.Nz < 3)
+            throw Error(SE_ERR_VALUE, "grid must have Nx, Ny >= 1 and Nz >= 3");
+        p->dev = device;
+        SE_CUDA(cudaSetDevice(device));
+        SE_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+        p->Nx = P.Nx; p->Ny = P.Ny; p->Nz = P.Nz;
+        p->Nyh = P.Ny / 2 + 1;
+        p->N2 = 2 * (P.Nz - 1);
+        p->M = (int64_t)p->Nx * p->Nyh;
+        p->NXY = (int64_t)p->Nx * p->Ny;
+        p->G = p->NXY * p->Nz;
+        p->hx = P.Lx / P.Nx;                   // gridops.py:54-55
+        p->hy = P.Ly / P.Ny;
+        p->rad = P.H_E;
+        p->rad_keep = P.H_E + 1e-12 * P.H_E;    // gridops.py:25
+        p->width = P.g_t;
+        p->norm = std::sqrt(2.0 * M_PI * (P.g_t * P.g_t));
+        p->mx = (int)std::floor(P.H_E / p->hx + 1e-12);
+        p->my = (int)std::floor(P.H_E / p->hy + 1e-12);
+        if (p->mx > MAX_M || p->my > MAX_M)
+            throw Error(SE_ERR_VALUE, "Gaussian support wider than the tile kernels handle");
+        const int nz = P.Nz;
+        p->z.assign(z_nodes, z_nodes + nz);
+        p->wcc.assign(cc_w, cc_w + nz);
+        p->tw0.assign(t_wall0, t_wall0 + nz);
+        p->twH.assign(t_wallH, t_wallH + nz);
+        p->kx.assign(kx, kx + p->Nx);
+        p->ky.assign(ky, ky + p->Ny);
+        // widest z stencil: nodes within any window of length 2 H_E (+1 slack)
+        int wz = 1;
+        for (int i = 0, j = 0; i < nz; ++i) {
+            while (j < nz && p->z[j] - p->z[i] <= 2.0 * P.H_E) ++j;
+            wz = std::max(wz, j - i);
+        }
+        p->wz_max = std::min(wz + 1, nz);
+        // correction window (dpsolver.py:106): z in [-H_E, H + H_E]
+        const double zlo = -P.H_E, zhi = P.H + P.H_E;
+        p->win0 = nz; p->win1 = 0;
+        for (int j = 0; j < nz; ++j)
+            if (p->z[j] >= zlo && p->z[j] <= zhi) { p->win0 = std::min(p->win0, j); p->win1 = j + 1; }
+        if (p->win1 <= p->win0) p->win0 = p->win1 = 0;
+        // per-mode |k| on the half spectrum, distinct values, selection
+        std::vector<double> kmag(p->M);
+        std::vector<unsigned char> sel(p->M);
+        std::vector<double> uniq;
+        for (int ix = 0; ix < p->Nx; ++ix)
+            for (int iy = 0; iy < p->Nyh; ++iy) {
+                double k = std::hypot(p->kx[ix], p->ky[iy]);   // dpsolver.py:38
+                int64_t m = (int64_t)ix * p->Nyh + iy;
+                kmag[m] = k;
+                sel[m] = (k > 0.0 && k <= P.k_max) ? 1 : 0;     // dpsolver.py:105
+                if (k > 0.0) uniq.push_back(k);
+            }
+        std::sort(uniq.begin(), uniq.end());
+        uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+        std::vector<int> kidx(p->M);
+        for (int64_t m = 0; m < p->M; ++m)
+            kidx[m] = kmag[m] > 0.0
+                          ? (int)(std::lower_bound(uniq.begin(), uniq.end(), kmag[m]) - uniq.begin())
+                          : -1;
+        p->n_uniq = (int)uniq.size();
+        auto up = [&](const std::vector<double>& h) {
+            double* d = dalloc<double>(p, h.size());
+            SE_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+            return d;
+        };
+        p->d_z = up(p->z); p->d_wcc = up(p->wcc); p->d_tw0 = up(p->tw0); p->d_twH = up(p->twH);
+        p->d_kx = up(p->kx); p->d_ky = up(p->ky); p->d_kmag = up(kmag);
+        p->d_kuniq = up(uniq.empty() ? std::vector<double>{0.0} : uniq);
+        p->d_kidx = dalloc<int>(p, p->M);
+        SE_CUDA(cudaMemcpy(p->d_kidx, kidx.data(), p->M * sizeof(int), cudaMemcpyHostToDevice));
+        p->d_sel = dalloc<unsigned char>(p, p->M);
+        SE_CUDA(cudaMemcpy(p->d_sel, sel.data(), p->M, cudaMemcpyHostToDevice));
+        factor_bvp(p);
+
+        // buffers
+        p->d_rho = dalloc<double>(p, 2 * (size_t)p->G);
+        SE_CUDA(cudaMemset(p->d_rho, 0, 2 * (size_t)p->G * sizeof(double)));
+        p->d_ext = dalloc<cufftDoubleComplex>(p, (size_t)p->N2 * 2 * p->M);
+        p->d_spec = dalloc<cufftDoubleComplex>(p, (size_t)nz * 4 * p->M);
+        p->d_fields = dalloc<double>(p, 4 * (size_t)p->G);
+        p->d_scr = dalloc<cufftDoubleComplex>(p, 3 * (size_t)nz * p->M);
+        p->d_mom = dalloc<cufftDoubleComplex>(p, 2 * (size_t)p->M);
+        p->d_mism = dalloc<cufftDoubleComplex>(p, 4 * (size_t)p->M);
+        const char* keep = std::getenv("SE_KEEP_STAGES");
+        p->keep_stages = keep && keep[0] == '1';
+        if (p->keep_stages) p->d_keep = dalloc<cufftDoubleComplex>(p, (size_t)nz * 2 * p->M);
+        p->d_k0 = dalloc<double>(p, 16);
+        p->d_scal = dalloc<double>(p, 8);
+        p->d_flags = dalloc<int>(p, 1);
+        p->d_count = dalloc<int64_t>(p, 1);
+        p->d_partial = dalloc<double>(p, 1024);
+        p->d_mm = dalloc<double>(p, 256);
+        p->d_origin = dalloc<double>(p, 3);
+        SE_CUDA(cudaMemset(p->d_origin, 0, 3 * sizeof(double)));
+        SE_CUDA(cudaMemset(p->d_k0, 0, 16 * sizeof(double)));
+
+        // wall charge: samples and their normalised half spectra (slab.py:209-213)
+        p->sigma_zero = (sigma_b == nullptr && sigma_t == nullptr);
+        p->d_sigb = dalloc<double>(p, 2 * (size_t)p->NXY);
+        p->d_sigt = p->d_sigb + p->NXY;
+        p->d_sbh = dalloc<cufftDoubleComplex>(p, 2 * (size_t)p->M);
+        p->d_sth = p->d_sbh + p->M;
+        double sscale = 0.0;
+        if (p->sigma_zero) {
+            SE_CUDA(cudaMemset(p->d_sigb, 0, 2 * p->NXY * sizeof(double)));
+            SE_CUDA(cudaMemset(p->d_sbh, 0, 2 * p->M * sizeof(cufftDoubleComplex)));
+        } else {
+            std::vector<double> zeros(p->NXY, 0.0);
+            const double* sb = sigma_b ? sigma_b : zeros.data();
+            const double* st = sigma_t ? sigma_t : zeros.data();
+            SE_CUDA(cudaMemcpy(p->d_sigb, sb, p->NXY * sizeof(double), cudaMemcpyHostToDevice));
+            SE_CUDA(cudaMemcpy(p->d_sigt, st, p->NXY * sizeof(double), cudaMemcpyHostToDevice));
+            double ab = 0, at = 0;
+            for (int64_t i = 0; i < p->NXY; ++i) { ab += std::fabs(sb[i]); at += std::fabs(st[i]); }
+            sscale = ab / p->NXY + at / p->NXY;
+            make_plan2d(&p->fft_sig, p->Nx, p->Ny, p->Nyh, CUFFT_D2Z, p->NXY, p->M, 2, p->stream);
+            SE_CUFFT(cufftExecD2Z(p->fft_sig, p->d_sigb, p->d_sbh));
+            scale_complex<<<(unsigned)((2 * p->M + 255) / 256), 256, 0, p->stream>>>(
+                p->d_sbh, 2 * p->M, 1.0 / (double)p->NXY);
+            SE_LAUNCHED(p);
+        }
+        p->sigma_scale = sscale;
+
+        // cuFFT plans
+        make_plan2d(&p->fft_fwd2, p->Nx, p->Ny, p->Nyh, CUFFT_D2Z, p->NXY, p->M, 2 * nz, p->stream);
+        make_plan2d(&p->fft_inv4, p->Nx, p->Ny, p->Nyh, CUFFT_Z2D, p->M, p->NXY, 4 * nz, p->stream);
+        make_plan2d(&p->fft_inv1, p->Nx, p->Ny, p->Nyh, CUFFT_Z2D, 4 * p->M, 4 * p->NXY, nz, p->stream);
+        {
+            long long n1[1] = {p->N2}, emb[1] = {p->N2};
+            size_t ws = 0;
+            SE_CUFFT(cufftCreate(&p->fft_z));
+            SE_CUFFT(cufftMakePlanMany64(p->fft_z, 1, n1, emb, 2 * p->M, 1, emb, 2 * p->M, 1,
+                                         CUFFT_Z2Z, 2 * p->M, &ws));
+            SE_CUFFT(cufftSetStream(p->fft_z, p->stream));
+        }
+        SE_CUDA(cudaStreamSynchronize(p->stream));
+        *out = reinterpret_cast<se_plan*>(p);
+        return SE_OK;
+    } catch (const Error& e) {
+        if (p) se_plan_destroy(reinterpret_cast<se_plan*>(p));
+        return fail(e);
+    } catch (const std::exception& e) {
+        if (p) se_plan_destroy(reinterpret_cast<se_plan*>(p));
+        return fail(Error(SE_ERR_CUDA, e.what()));
+    }
+}
+
+void se_plan_destroy(se_plan* plan) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p) return;
+    cudaSetDevice(p->dev);
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    cufftHandle hs[] = {p->fft_fwd2, p->fft_fwd1, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig};
+    for (auto h : hs) if (h) cufftDestroy(h);
+    for (auto& b : p->owned) if (b.p) cudaFree(b.p);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    delete p;
+}
+
+int se_set_charges(se_plan* plan, const double* q, int64_t n) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        if (n < 0) throw Error(SE_ERR_VALUE, "negative charge count");
+        SE_CUDA(cudaSetDevice(p->dev));
+        ensure_charges(p, n);
+        if (n > 0)
+            SE_CUDA(cudaMemcpy(p->d_q, q, n * sizeof(double), cudaMemcpyHostToDevice));
+        p->N = n;
+        double aq = 0;
+        for (int64_t i = 0; i < n; ++i) aq += std::fabs(q[i]);
+        p->k0_scale = (aq / (p->P.Lx * p->P.Ly) + p->sigma_scale) / p->P.eps;   // slab.py:231-233
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_solve(se_plan* plan, const double* pos, int64_t n, uint32_t flags, double* phi_bar,
+             double* E_bar, double* U, se_diag* diag) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        SE_CUDA(cudaSetDevice(p->dev));
+        if (n != p->N) throw Error(SE_ERR_VALUE, "positions and charges disagree on N");
+        if (n > 0)
+            SE_CUDA(cudaMemcpyAsync(p->d_pos, pos, 3 * n * sizeof(double),
+                                    cudaMemcpyHostToDevice, p->stream));
+        solve_core(p, p->d_pos, n, flags, p->d_phi, p->d_E, U, diag);
+        if (n > 0) {
+            if (phi_bar)
+                SE_CUDA(cudaMemcpyAsync(phi_bar, p->d_phi, n * sizeof(double),
+                                        cudaMemcpyDeviceToHost, p->stream));
+            if (E_bar && (flags & SE_NEED_FORCES))
+                SE_CUDA(cudaMemcpyAsync(E_bar, p->d_E, 3 * n * sizeof(double),
+                                        cudaMemcpyDeviceToHost, p->stream));
+            SE_CUDA(cudaStreamSynchronize(p->stream));
+        }
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_solve_device(se_plan* plan, const double* d_pos, int64_t n, uint32_t flags,
+                    double* d_phi_bar, double* d_E_bar, double* U, se_diag* diag) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        SE_CUDA(cudaSetDevice(p->dev));
+        solve_core(p, d_pos, n, flags, d_phi_bar ? d_phi_bar : p->d_phi,
+                   d_E_bar ? d_E_bar : p->d_E, U, diag);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+// light-weight plan for the plan-free entry points (no grids, no FFTs)
+static Plan* light_plan(const se_params* params, int device) {
+    if (!params) throw Error(SE_ERR_VALUE, "null params");
+    Plan* p = new Plan();
+    p->P = *params;
+    p->dev = device;
+    SE_CUDA(cudaSetDevice(device));
+    SE_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    return p;
+}
+
+struct PlanGuard {
+    Plan* p;
+    ~PlanGuard() { if (p) se_plan_destroy(reinterpret_cast<se_plan*>(p)); }
+};
+
+int se_near_field(const se_params* params, int device, const double* pos, const double* q,
+                  int64_t n, const double* eval_pos, int64_t ne, int kind, int need_field,
+                  int subtract_unsplit, double* phi, double* E) {
+    try {
+        Plan* p = light_plan(params, device);
+        PlanGuard pg{p};
+        const se_params& P = p->P;
+        p->launches = 0;
+        bool empty = n == 0 || P.xi_is_inf != 0.0;
+        std::fill(phi, phi + ne, 0.0);
+        if (E && need_field) std::fill(E, E + 3 * ne, 0.0);
+        if (empty || ne == 0) return SE_OK;
+        if (P.r_cut >= 0.5 * std::min(P.Lx, P.Ly))
+            throw Error(SE_ERR_VALUE, "near-field cutoff exceeds half the periodic box");
+        double *d_pos = nullptr, *d_q = nullptr, *d_ev = nullptr, *d_out = nullptr;
+        SE_CUDA(cudaMalloc(&d_pos, 3 * n * sizeof(double)));
+        SE_CUDA(cudaMalloc(&d_q, n * sizeof(double)));
+        SE_CUDA(cudaMalloc(&d_ev, 3 * ne * sizeof(double)));
+        SE_CUDA(cudaMalloc(&d_out, 4 * ne * sizeof(double)));
+        struct Guard { void* a[4]; ~Guard() { for (void* x : a) cudaFree(x); } } g{{d_pos, d_q, d_ev, d_out}};
+        SE_CUDA(cudaMemcpy(d_pos, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice));
+        SE_CUDA(cudaMemcpy(d_q, q, n * sizeof(double), cudaMemcpyHostToDevice));
+        SE_CUDA(cudaMemcpy(d_ev, eval_pos, 3 * ne * sizeof(double), cudaMemcpyHostToDevice));
+        const double eps = P.eps, two_sqrtpi = 2.0 / std::sqrt(M_PI);
+        NearKernel k{};
+        k.inv4pie = 1.0 / (4.0 * M_PI * eps);
+        k.kind = kind;
+        k.need_field = need_field ? 1 : 0;
+        if (kind == 0) {
+            k.c1 = 2.0 * P.g_w;
+            k.c2 = std::sqrt(4.0 * P.g_w * P.g_w + 1.0 / (P.xi * P.xi));
+            k.radius = P.r_cut;
+            k.self_value = subtract_unsplit ? -two_sqrtpi / k.c2 / (4.0 * M_PI * eps)
+                                            : two_sqrtpi * (0.5 / P.g_w - 1.0 / k.c2) / (4.0 * M_PI * eps);
+        } else {
+            k.c1 = std::sqrt(2.0) * P.g_w;
+            k.c2 = std::sqrt(2.0 * P.g_w * P.g_w + 1.0 / (P.xi * P.xi));
+            k.radius = P.r_nf;
+            k.point0 = (two_sqrtpi / k.c1 - two_sqrtpi / k.c2) / (4.0 * M_PI * eps);
+        }
+        build_cells(p, d_pos, d_q, n);
+        near_eval(p, d_ev, nullptr, ne, k, d_out, nullptr);
+        std::vector<double> h(4 * ne);
+        SE_CUDA(cudaMemcpyAsync(h.data(), d_out, (need_field ? 4 : 1) * ne * sizeof(double),
+                                cudaMemcpyDeviceToHost, p->stream));
+        SE_CUDA(cudaStreamSynchronize(p->stream));
+        std::copy(h.begin(), h.begin() + ne, phi);
+        if (E && need_field)
+            for (int64_t i = 0; i < ne; ++i)
+                for (int c = 0; c < 3; ++c) E[3 * i + c] = h[(c + 1) * ne + i];
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_build_partition(const se_params* params, int device, const double* pos,
+                       const double* q, int64_t n, int64_t* n_over, int64_t* over,
+                       int64_t* n_far, int64_t* far, int64_t* n_img, double* img_pos,
+                       double* img_str, int64_t* img_src, int32_t* img_wall) {
+    try {
+        *n_over = *n_far = *n_img = 0;
+        if (n == 0) return SE_OK;
+        Plan* p = light_plan(params, device);
+        PlanGuard pg{p};
+        ensure_charges(p, n);
+        SE_CUDA(cudaMemcpy(p->d_pos, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice));
+        SE_CUDA(cudaMemcpy(p->d_q, q, n * sizeof(double), cudaMemcpyHostToDevice));
+        partition_sources(p, p->d_pos, n);
+        std::vector<int> cls(3 * n);
+        std::vector<double4> src(3 * n);
+        SE_CUDA(cudaMemcpyAsync(cls.data(), p->d_src_cls, 3 * n * sizeof(int),
+                                cudaMemcpyDeviceToHost, p->stream));
+        SE_CUDA(cudaMemcpyAsync(src.data(), p->d_src, 3 * n * sizeof(double4),
+                                cudaMemcpyDeviceToHost, p->stream));
+        SE_CUDA(cudaStreamSynchronize(p->stream));
+        int64_t no = 0, nf = 0, ni = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            if (cls[3 * i] == 0) over[no++] = i; else far[nf++] = i;
+        }
+        for (int64_t k = 0; k < no; ++k) {            // slab.py:66-78 loop order
+            int64_t i = over[k];
+            for (int w = 0; w < 2; ++w) {
+                if (cls[3 * i + 1 + w] < 0) continue;
+                double4 v = src[3 * i + 1 + w];
+                img_pos[3 * ni] = v.x; img_pos[3 * ni + 1] = v.y; img_pos[3 * ni + 2] = v.z;
+                img_str[ni] = v.w; img_src[ni] = i; img_wall[ni] = w;
+                ++ni;
+            }
+        }
+        *n_over = no; *n_far = nf; *n_img = ni;
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int64_t se_debug_fetch(se_plan* plan, int which, void* host, int64_t nbytes) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p) return -1;
+    const void* src = nullptr;
+    int64_t size = 0;
+    switch (which) {
+        case 0: src = p->d_rho; size = 2 * p->G * sizeof(double); break;
+        case 1: src = p->d_keep; size = p->keep_stages ? p->Nz * 2 * p->M * 16 : 0; break;
+        case 2: src = p->d_fields; size = 4 * p->G * sizeof(double); break;
+        case 3: src = p->d_mism; size = 4 * p->M * 16; break;
+        case 4: src = p->d_far; size = 4 * p->N * sizeof(double); break;
+        case 5: src = p->d_near; size = 4 * p->N * sizeof(double); break;
+        default: return -1;
+    }
+    if (!host) return size;
+    if (nbytes < size || !src) return -1;
+    cudaSetDevice(p->dev);
+    if (cudaMemcpy(host, src, size, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return size;
+}
+
+}  // extern "C"

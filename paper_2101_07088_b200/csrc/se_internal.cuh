@@ -1,0 +1,272 @@
+// Internal declarations of libslabewald_cuda.so (sm_100a).
+//
+// Data layout in HBM (z slowest, SURVEY.md section 7 "design decisions"):
+//   rho    [Nz][2][Nx][Ny]        real spread grids, slot 0 = rho_over,
+//                                 slot 1 = rho_in            (slab.py:282-289)
+//   ext    [2N][2][Nx][Ny/2+1]    complex, N = Nz-1: even extension in z of
+//                                 the xy half spectra; a batched length-2N
+//                                 FFT along z turns it into the DCT-I
+//                                 (cheb_transform / cheb_inverse,
+//                                 chebyshev.py:46-65)
+//   spec4  [Nz][4][Nx][Ny/2+1]    psi, ikx psi, iky psi, dpsi/dz mode values
+//   fields [Nz][4][Nx][Ny]        real field grids after the inverse xy FFT
+// Sources for spreading are sorted by (xy bin, class, first z node) so one
+// CTA finds every source touching its grid tile by binary search.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/slabewald.h"
+
+namespace se {
+
+// ----------------------------------------------------------------------------
+// errors
+// ----------------------------------------------------------------------------
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define SE_CUDA(call)                                                        \
+    do {                                                                     \
+        cudaError_t e_ = (call);                                             \
+        if (e_ != cudaSuccess)                                               \
+            throw ::se::Error(e_ == cudaErrorMemoryAllocation ? SE_ERR_MEMORY \
+                                                               : SE_ERR_CUDA, \
+                              std::string(#call) + ": " +                    \
+                                  cudaGetErrorString(e_));                   \
+    } while (0)
+
+#define SE_CUFFT(call)                                                       \
+    do {                                                                     \
+        cufftResult r_ = (call);                                             \
+        if (r_ != CUFFT_SUCCESS)                                             \
+            throw ::se::Error(SE_ERR_CUDA, std::string(#call) +              \
+                                               ": cufft error " +            \
+                                               std::to_string((int)r_));     \
+    } while (0)
+
+#define SE_LAUNCHED(plan)                                                    \
+    do {                                                                     \
+        (plan)->launches++;                                                  \
+        cudaError_t e_ = cudaGetLastError();                                 \
+        if (e_ != cudaSuccess)                                               \
+            throw ::se::Error(SE_ERR_CUDA, std::string("launch: ") +         \
+                                               cudaGetErrorString(e_));      \
+    } while (0)
+
+// device-side error flags (checked after the stream is synchronised)
+enum : int {
+    FLAG_Z_OUTSIDE = 1,      // gridops.py:87-88,119-120  ValueError
+    FLAG_NONFINITE = 2,      // dpsolver.py:83-86        FloatingPointError
+    FLAG_K0_FAIL = 4,        // dpsolver.py:208-211      FloatingPointError
+    FLAG_K0_WARN = 8,        // dpsolver.py:212-213      warning
+};
+
+// ----------------------------------------------------------------------------
+// spread / interpolation tiling
+// ----------------------------------------------------------------------------
+constexpr int TILE = 8;          // xy tile = 8 x 8 grid columns (one bin)
+constexpr int SPREAD_TZ = 32;    // z nodes per spread CTA (4 groups of 8)
+constexpr int INTERP_TZ = 16;    // z nodes per interp CTA (4 groups of 4)
+constexpr int CHUNK = 64;        // sources staged in shared memory at a time
+constexpr int MAX_M = 24;        // max xy stencil half width supported
+
+// Per-source stencil tables, structure of arrays over the sorted sources.
+struct Stencils {
+    int64_t S = 0;               // number of sources (table stride)
+    int mx = 0, my = 0;          // x / y half widths (gridops.py:20)
+    int wz = 0;                  // z table width (max nodes per stencil)
+    int* j0x = nullptr;          // floor(x / hx)
+    int* j0y = nullptr;
+    int* lo = nullptr;           // first z node
+    double* q = nullptr;         // strength
+    double* wx = nullptr;        // [(2mx+1)][S] Gaussian weights * keep
+    double* wy = nullptr;
+    double* wzt = nullptr;       // [wz][S]
+    int* owner = nullptr;        // charge index of the source, -1 for images
+};
+
+// Sorted source set with segment offsets per (bin, class).
+struct SourceSet {
+    int64_t S = 0;
+    int nbx = 0, nby = 0;        // bins along x, y
+    int64_t* seg = nullptr;      // [nbx*nby*2 + 1] start offsets
+    Stencils st;
+};
+
+// ----------------------------------------------------------------------------
+// near field cell list
+// ----------------------------------------------------------------------------
+struct CellList {
+    int ncx = 0, ncy = 0, ncz = 0;
+    double csx = 0, csy = 0, csz = 0, zlo = 0;
+    int64_t n = 0;
+    int* start = nullptr;        // [ncells + 1]
+    double4* src = nullptr;      // sorted sources (x, y, z, q) original coords
+    float4* srcf = nullptr;      // wrapped fp32 copy for the pre-test
+    int* orig = nullptr;         // sorted -> original source index
+};
+
+// ----------------------------------------------------------------------------
+// the plan
+// ----------------------------------------------------------------------------
+struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+struct Plan {
+    se_params P{};
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+
+    // grid
+    int Nx = 0, Ny = 0, Nz = 0, Nyh = 0, N2 = 0;
+    int64_t M = 0, NXY = 0, G = 0;
+    double hx = 0, hy = 0;
+    int mx = 0, my = 0;          // spread/interp stencil half widths
+    int wz_max = 0;              // max z stencil width
+    double rad = 0, rad_keep = 0, width = 0, norm = 0;   // spread kernel
+    bool jumps = false, sigma_zero = true;
+
+    // host copies of constants
+    std::vector<double> z, wcc, tw0, twH, kx, ky;
+
+    // device constants
+    double *d_z = nullptr, *d_wcc = nullptr, *d_tw0 = nullptr, *d_twH = nullptr;
+    double *d_kx = nullptr, *d_ky = nullptr;
+    int* d_kidx = nullptr;                // mode -> unique |k| row (-1: k = 0)
+    double* d_kmag = nullptr;             // |k| per half-spectrum mode
+    unsigned char* d_sel = nullptr;       // correction mode mask (0 < k <= k_max)
+    double* d_kuniq = nullptr;            // distinct |k| > 0
+    double* d_maps = nullptr;             // integration maps + column sums [9][Nz]
+    int win0 = 0, win1 = 0;               // correction node window [win0, win1)
+    int n_uniq = 0;
+    double* d_fac = nullptr;              // BVP factors [n_uniq][FAC_ROWS][Nz]
+    double* d_sinv = nullptr;             // [n_uniq][4]
+    double* d_kappa = nullptr;            // [n_uniq]
+    cufftDoubleComplex *d_sbh = nullptr, *d_sth = nullptr;  // sigma hats
+    double *d_sigb = nullptr, *d_sigt = nullptr;            // sigma samples
+    double k0_scale = 0;
+    double sigma_scale = 0;               // mean|sigma_b| + mean|sigma_t|
+
+    // charges and per-solve buffers
+    int64_t N = 0, q_cap = 0;
+    double* d_q = nullptr;
+    double* d_pos = nullptr;              // [N][3]
+    double* d_phi = nullptr;              // [N]
+    double* d_E = nullptr;                // [N][3]
+    double* d_far = nullptr;              // [4][N] interp sums
+    double* d_near = nullptr;             // [4][N] near sums
+    double* d_scal = nullptr;             // device scalars (A_i, B_i, U, ...)
+    int* d_flags = nullptr;
+    double* d_k0 = nullptr;               // k=0 outputs [16]
+
+    // sources
+    double4* d_src = nullptr;             // unsorted spread sources
+    int* d_src_cls = nullptr;             // class (0 over, 1 far/image)
+    int* d_src_owner = nullptr;
+    int64_t src_cap = 0;
+    uint32_t* d_keys = nullptr;
+    uint32_t* d_keys2 = nullptr;
+    int* d_perm = nullptr;
+    int* d_perm2 = nullptr;
+    void* d_cub = nullptr;
+    size_t cub_bytes = 0;
+    SourceSet ss;
+
+    // near field
+    CellList cl;
+    int64_t cl_cap = 0;
+    uint32_t* d_ckeys = nullptr;
+    uint32_t* d_ckeys2 = nullptr;
+    int* d_cperm = nullptr;
+    int* d_cperm2 = nullptr;
+    int* d_tgt = nullptr;                 // charge targets in cell order
+    uint32_t* d_tkeys = nullptr;
+    uint32_t* d_tkeys2 = nullptr;
+    int* d_tperm = nullptr;
+    double4* d_near_src = nullptr;        // unsorted near-field sources
+    void* d_near_cub = nullptr;
+    size_t near_cub_bytes = 0;
+    int64_t cell_cap = 0;
+    double* d_mm = nullptr;               // z-range partials
+    int64_t* d_count = nullptr;
+    double* d_partial = nullptr;          // reduction partials
+    double* d_origin = nullptr;           // (0, 0, 0)
+    double *d_wall_pts = nullptr, *d_wall_far = nullptr, *d_wall_near = nullptr;
+
+    // grids
+    double* d_rho = nullptr;              // [Nz][2][Nx][Ny]
+    cufftDoubleComplex* d_ext = nullptr;  // [2N][2][M]
+    cufftDoubleComplex* d_spec = nullptr; // [Nz][4][M]
+    double* d_fields = nullptr;           // [Nz][4][Nx][Ny]
+    cufftDoubleComplex* d_scr = nullptr;  // BVP scratch [3][Nz][M]
+    bool keep_stages = false;
+    cufftDoubleComplex* d_keep = nullptr; // [Nz][2][M] psi coefficients (debug)
+    cufftDoubleComplex* d_mom = nullptr;  // [M][2] correction moments / den
+    cufftDoubleComplex* d_mism = nullptr; // [4][M] mismatch (debug)
+
+    cufftHandle fft_fwd2 = 0, fft_fwd1 = 0, fft_z = 0, fft_inv4 = 0,
+                fft_inv1 = 0, fft_sig = 0;
+    void* fft_work = nullptr;
+
+    std::vector<Buf> owned;
+};
+
+// factor table rows per unique |k| (see se_spectral.cu)
+constexpr int FAC_CP = 0, FAC_INV = 1, FAC_AINVB = 2, FAC_C0 = 3, FAC_C1 = 4;
+constexpr int FAC_ROWS = 5;
+
+void dfree(Plan* p, void* ptr);
+
+// allocation helper (tracked, freed by the plan)
+template <class T>
+T* dalloc(Plan* p, size_t count) {
+    void* ptr = nullptr;
+    size_t bytes = count * sizeof(T);
+    if (bytes == 0) bytes = 16;
+    SE_CUDA(cudaMalloc(&ptr, bytes));
+    p->owned.push_back({ptr, bytes});
+    return static_cast<T*>(ptr);
+}
+
+// --- se_grid.cu ---
+void build_sources(Plan* p, const double* d_pos, int64_t n, bool two_grids);
+void partition_sources(Plan* p, const double* d_pos, int64_t n);
+void spread(Plan* p, bool two_grids);
+void interp_charges(Plan* p, int64_t n, bool forces);
+void interp_points(Plan* p, const double* d_pts, int64_t npts, double width,
+                   double radius, double* d_out);
+void ensure_sources(Plan* p, int64_t cap);
+
+// --- se_spectral.cu ---
+void factor_bvp(Plan* p);
+void forward_transforms(Plan* p, bool two_grids);
+void bvp_solve(Plan* p, bool two_grids, int mode, bool correction);
+void inverse_transforms(Plan* p, bool forces, bool correction);
+
+// --- se_near.cu ---
+struct NearKernel {
+    double c1, c2, inv4pie, radius, self_value, point0;
+    int kind;            // 0 avg, 1 point
+    int need_field;
+};
+void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n);
+void near_eval(Plan* p, const double* d_eval, const int* d_eval_order,
+               int64_t ne, const NearKernel& k, double* d_out4,
+               int64_t* d_npairs);
+void finalize(Plan* p, int64_t n, uint32_t flags, double self_inf_value,
+              double* d_phi, double* d_E);
+void wall_energy(Plan* p, const NearKernel& kpoint);
+
+}  // namespace se

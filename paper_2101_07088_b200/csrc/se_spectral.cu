@@ -1,0 +1,565 @@
+// Fourier x Chebyshev transforms and the per-mode boundary value problems.
+//
+// Reference: SlabSolver._forward / _modes_to_grid (slab.py:240-251),
+// cheb_transform / cheb_inverse / cheb_derivative (chebyshev.py:46-79),
+// DtnSolver.solve (dpsolver.py:47-71) -> BvpFactor (bvp.py:142-278),
+// solve_k0_dirichlet (bvp.py:281-296), the mismatch assembly
+// (slab.py:302-318), HarmonicCorrection (dpsolver.py:89-155) and the k = 0
+// combination (slab.py:397-445, dpsolver.py:166-218).
+//
+// B200 design.  The xy transforms are batched cuFFT D2Z / C2R over the
+// Chebyshev planes of the z-slowest layout.  The DCT-I along z (Nz = 258 at
+// the north-star size, 2(Nz-1) = 2*257: Bluestein-hostile for a hand radix
+// kernel) is one batched length-2(Nz-1) Z2Z FFT over the even extension,
+// strided across modes so every transform reads coalesced rows.  The BVP is
+// one thread per (kx, ky) mode of the half spectrum: sweeps along z touch
+// row n of all modes together, so every global access is coalesced across
+// the warp; factors are precomputed per distinct |k| at plan time.  The
+// mismatch, harmonic-correction moments and the k = 0 combination are fused
+// into the same kernel (a mode needs only its own wall values), and the
+// correction values themselves are evaluated on the fly while assembling
+// the four spectral fields, so no (mode x node) correction table is stored.
+#include <cmath>
+
+#include "se_internal.cuh"
+
+namespace se {
+
+namespace {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 cfma(double s, double2 a, double2 acc) {
+    return make_double2(fma(s, a.x, acc.x), fma(s, a.y, acc.y));
+}
+
+// k-independent integration maps (bvp.py:21-54) and BC column sums
+// (bvp.py:104-121), uploaded once.
+struct Maps {
+    const double *e_lo, *e_hi, *q_lo, *q_dg, *q_hi;   // [Nz]
+    const double *ue, *uq, *ve, *vq;                  // [Nz]
+};
+
+// ---------------------------------------------------------------------------
+// per-|k| factorisation                                    bvp.py:145-198
+// ---------------------------------------------------------------------------
+struct FactorArgs {
+    Maps mp; int Nz; int n_uniq; double half;
+    const double* kuniq; double* fac; double* sinv; double* kappa;
+    int* bad;
+};
+
+__global__ void factor_kernel(FactorArgs a) {
+    int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= a.n_uniq) return;
+    const int n = a.Nz;
+    const double kap = a.kuniq[u] * a.half;
+    const double k2 = kap * kap;
+    a.kappa[u] = kap;
+    double* cp = a.fac + ((int64_t)u * FAC_ROWS + FAC_CP) * n;
+    double* inv = a.fac + ((int64_t)u * FAC_ROWS + FAC_INV) * n;
+    double* aib = a.fac + ((int64_t)u * FAC_ROWS + FAC_AINVB) * n;
+    double* c0 = a.fac + ((int64_t)u * FAC_ROWS + FAC_C0) * n;
+    double* c1 = a.fac + ((int64_t)u * FAC_ROWS + FAC_C1) * n;
+    // Thomas factorisation of each parity chain (rows m = 2j + par)
+    for (int par = 0; par < 2; ++par) {
+        double cprev = 0.0;
+        for (int m = par; m < n; m += 2) {
+            double dg = 1.0 - k2 * a.mp.q_dg[m];
+            double lo = -k2 * a.mp.q_lo[m];
+            double up = -k2 * a.mp.q_hi[m];
+            double den = (m == par) ? dg : dg - lo * cprev;
+            double iv = 1.0 / den;
+            inv[m] = iv;
+            double c = (m + 2 < n) ? up * iv : 0.0;
+            cp[m] = c;
+            cprev = c;
+        }
+        // A^{-1} B column: rhs = -kappa^2 at the chain's first row
+        double dprev = 0.0;
+        for (int m = par; m < n; m += 2) {
+            double lo = -k2 * a.mp.q_lo[m];
+            double r = (m == par) ? -k2 : 0.0;
+            double d = (m == par) ? r * inv[m] : (r - lo * dprev) * inv[m];
+            aib[m] = d;
+            dprev = d;
+        }
+        int last = par + 2 * ((n - 1 - par) / 2);
+        for (int m = last - 2; m >= par; m -= 2) aib[m] -= cp[m] * aib[m + 2];
+    }
+    // BC rows C and the Schur complement S = C A^{-1} B - D
+    double s00 = 0, s01 = 0, s10 = 0, s11 = 0;
+    for (int m = 0; m < n; ++m) {
+        double r0 = a.mp.ue[m] + kap * a.mp.uq[m];
+        double r1 = a.mp.ve[m] - kap * a.mp.vq[m];
+        c0[m] = r0;
+        c1[m] = r1;
+        if ((m & 1) == 0) { s00 += r0 * aib[m]; s10 += r1 * aib[m]; }
+        else { s01 += r0 * aib[m]; s11 += r1 * aib[m]; }
+    }
+    s00 -= kap; s01 -= 1.0 + kap; s10 -= -kap; s11 -= 1.0 + kap;
+    double det = s00 * s11 - s01 * s10;
+    double scale = fabs(s00) + fabs(s01) + fabs(s10) + fabs(s11);
+    if (fabs(det) * 1e12 < scale * scale) atomicAdd(a.bad, 1);
+    a.sinv[4 * u + 0] = s11 / det;
+    a.sinv[4 * u + 1] = -s01 / det;
+    a.sinv[4 * u + 2] = -s10 / det;
+    a.sinv[4 * u + 3] = s00 / det;
+}
+
+// ---------------------------------------------------------------------------
+// even extension in z: ext[2N - j] = ext[j], j = 1..N-1
+// ---------------------------------------------------------------------------
+__global__ void mirror_kernel(double2* ext, int N, int64_t row) {
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t total = (int64_t)(N - 1) * row;
+    if (e >= total) return;
+    int64_t j = 1 + e / row, c = e % row;
+    ext[(2 * N - j) * row + c] = ext[j * row + c];
+}
+
+// ---------------------------------------------------------------------------
+// the per-mode solve
+// ---------------------------------------------------------------------------
+struct BvpArgs {
+    Maps mp;
+    int Nz, Nx, Nyh; int64_t M;
+    double half, eps, eps_b, eps_t, cb, ct, z0, z1, k_max, k0_scale;
+    int refine, two, mode;       // mode 0 jump, 1 plain+sigma, 2 plain
+    int correction;              // compute correction moments
+    const int* kidx; const double* kmag; const unsigned char* sel;
+    const double* fac; const double* sinv; const double* kappa;
+    const double* tw0; const double* twH;
+    const double2* sbh; const double2* sth;
+    double2* ext;                // [2N][2][M] in: raw DCT, out: iDCT inputs
+    double2* scrF; double2* scrA; double2* scrB;   // [Nz][M] each
+    double inv_nxy;
+    double2* mom;                // [M][2]  M_b/den, M_t/den
+    double2* mism;               // [4][M] (debug, may be null)
+    double2* keep;               // [Nz][2][M] psi coefficients (debug, may be null)
+    double* k0out;               // [16]
+    double* scal;                // scal[0] = A_i
+    int* flags;
+    double rb, rt, H;
+};
+
+// Solve one grid of one mode (column m, grid slot g of ext).  Returns the
+// wall values wv = {y(0), y(H), y'(0), y'(H)} and ends = {y'(z0), y'(z1)}.
+// With emit, writes the iDCT inputs of y (slot 0) and y' (slot 1), i.e. the
+// coefficients with the interior halved, mirrored to rows 2N - k.
+// Scratch columns (stride M): F = f_sc, A = y'' (ypp), B = Thomas d / x.
+__device__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
+                           double2 ends[2], bool emit) {
+    const int n = a.Nz, N = n - 1;
+    const int64_t M = a.M, RS = 2 * M;           // ext row stride
+    const double2* raw = a.ext + g * M + m;
+    double2* F = a.scrF + m;
+    double2* A = a.scrA + m;
+    double2* B = a.scrB + m;
+    const double* q_lo = a.mp.q_lo; const double* q_dg = a.mp.q_dg; const double* q_hi = a.mp.q_hi;
+    const double* e_lo = a.mp.e_lo; const double* e_hi = a.mp.e_hi;
+    // f_sc = -(Chebyshev coefficient of rho_hat) / eps * half^2, where the
+    // coefficient is (-1)^n FFT(ext)_n / (2N) * (2 if interior) / (Nx Ny)
+    const double base = -(a.half * a.half) / (a.eps * 2.0 * N) * a.inv_nxy;
+    auto fsc_at = [&](int k) -> double2 {
+        double s = base * (((k & 1) ? -1.0 : 1.0) * ((k > 0 && k < N) ? 2.0 : 1.0));
+        return cscale(raw[(int64_t)k * RS], s);
+    };
+    const int u = a.kidx[m];
+    double2 c0v = make_double2(0, 0), c1v = make_double2(0, 0);
+    if (u < 0) {
+        // ---- k = 0: y'' = f, y(z0) = y(z1) = 0              bvp.py:281-296
+        for (int k = 0; k < n; ++k) A[(int64_t)k * M] = fsc_at(k);
+        double2 P = make_double2(0, 0), Qs = make_double2(0, 0);
+        for (int k = 1; k < n; ++k) {
+            double2 y = cscale(A[(int64_t)k * M], q_dg[k]);
+            if (k >= 2) y = cadd(y, cscale(A[(int64_t)(k - 2) * M], q_lo[k]));
+            if (k + 2 < n) y = cadd(y, cscale(A[(int64_t)(k + 2) * M], q_hi[k]));
+            P = cadd(P, y);
+            Qs = (k & 1) ? csub(Qs, y) : cadd(Qs, y);
+        }
+        c0v = cscale(cadd(P, Qs), -0.5);
+        c1v = cscale(csub(Qs, P), 0.5);
+    } else {
+        const double* cp = a.fac + ((int64_t)u * FAC_ROWS + FAC_CP) * n;
+        const double* iv = a.fac + ((int64_t)u * FAC_ROWS + FAC_INV) * n;
+        const double* aib = a.fac + ((int64_t)u * FAC_ROWS + FAC_AINVB) * n;
+        const double* cr0 = a.fac + ((int64_t)u * FAC_ROWS + FAC_C0) * n;
+        const double* cr1 = a.fac + ((int64_t)u * FAC_ROWS + FAC_C1) * n;
+        const double kap = a.kappa[u], k2 = kap * kap;
+        const double S00 = a.sinv[4 * u], S01 = a.sinv[4 * u + 1];
+        const double S10 = a.sinv[4 * u + 2], S11 = a.sinv[4 * u + 3];
+
+        // forward sweep (both parity chains interleaved): d_k = (r_k - lo_k d_{k-2}) / den_k
+        // backward sweep: x_k = d_k - cp_k x_{k+2}; Schur rhs C.x     bvp.py:76-90,216-227
+        auto descend = [&](double2& s0, double2& s1) {
+            double2 xp1 = make_double2(0, 0), xp2 = make_double2(0, 0);
+            s0 = make_double2(0, 0); s1 = make_double2(0, 0);
+            for (int k = n - 1; k >= 0; --k) {
+                double2 d = B[(int64_t)k * M];
+                double2 x = (k + 2 < n) ? cfma(-cp[k], xp2, d) : d;
+                B[(int64_t)k * M] = x;
+                s0 = cfma(cr0[k], x, s0);
+                s1 = cfma(cr1[k], x, s1);
+                xp2 = xp1; xp1 = x;
+            }
+        };
+        {
+            double2 dm1 = make_double2(0, 0), dm2 = make_double2(0, 0);
+            for (int k = 0; k < n; ++k) {
+                double2 r = fsc_at(k);
+                F[(int64_t)k * M] = r;
+                double2 d = (k < 2) ? cscale(r, iv[k])
+                                    : cscale(cfma(k2 * q_lo[k], dm2, r), iv[k]);
+                B[(int64_t)k * M] = d;
+                dm2 = dm1; dm1 = d;
+            }
+        }
+        double2 s0, s1;
+        descend(s0, s1);                       // rhs2 = bc = 0
+        c0v = make_double2(S00 * s0.x + S01 * s1.x, S00 * s0.y + S01 * s1.y);
+        c1v = make_double2(S10 * s0.x + S11 * s1.x, S10 * s0.y + S11 * s1.y);
+        for (int k = 0; k < n; ++k)
+            A[(int64_t)k * M] = cfma(-aib[k], (k & 1) ? c1v : c0v, B[(int64_t)k * M]);
+
+        for (int it = 0; it < a.refine; ++it) {     // bvp.py:229-246,268-273
+            double2 yq_sum = make_double2(0, 0), yq_sgn = make_double2(0, 0);
+            double2 ye_sum = make_double2(0, 0), ye_sgn = make_double2(0, 0);
+            double2 ym2 = make_double2(0, 0), ym1 = make_double2(0, 0);
+            double2 y0 = A[0];
+            double2 yp1 = (n > 1) ? A[M] : make_double2(0, 0);
+            double2 dm1 = make_double2(0, 0), dm2 = make_double2(0, 0);
+            for (int k = 0; k < n; ++k) {
+                double2 yp2 = (k + 2 < n) ? A[(int64_t)(k + 2) * M] : make_double2(0, 0);
+                double2 yq = make_double2(0, 0), ye = make_double2(0, 0);
+                if (k > 0) {
+                    yq = cscale(y0, q_dg[k]);
+                    if (k >= 2) yq = cadd(yq, cscale(ym2, q_lo[k]));
+                    if (k + 2 < n) yq = cadd(yq, cscale(yp2, q_hi[k]));
+                    ye = cscale(ym1, e_lo[k]);
+                    if (k + 1 < n) ye = cadd(ye, cscale(yp1, e_hi[k]));
+                }
+                double2 r = csub(F[(int64_t)k * M], csub(y0, cscale(yq, k2)));
+                if (k == 0) r = cadd(r, cscale(c0v, k2));
+                if (k == 1) r = cadd(r, cscale(c1v, k2));
+                yq_sum = cadd(yq_sum, yq); ye_sum = cadd(ye_sum, ye);
+                if (k & 1) { yq_sgn = csub(yq_sgn, yq); ye_sgn = csub(ye_sgn, ye); }
+                else { yq_sgn = cadd(yq_sgn, yq); ye_sgn = cadd(ye_sgn, ye); }
+                double2 d = (k < 2) ? cscale(r, iv[k])
+                                    : cscale(cfma(k2 * q_lo[k], dm2, r), iv[k]);
+                B[(int64_t)k * M] = d;
+                dm2 = dm1; dm1 = d;
+                ym2 = ym1; ym1 = y0; y0 = yp1; yp1 = yp2;
+            }
+            // r2 = bc - (C ypp + D c) with bc = 0
+            double2 r20 = cscale(cadd(cadd(ye_sum, cscale(yq_sum, kap)),
+                                      cadd(cscale(c0v, kap), cscale(c1v, 1.0 + kap))), -1.0);
+            double2 r21 = cscale(cadd(csub(ye_sgn, cscale(yq_sgn, kap)),
+                                      cadd(cscale(c0v, -kap), cscale(c1v, 1.0 + kap))), -1.0);
+            double2 t0, t1;
+            descend(t0, t1);
+            t0 = csub(t0, r20); t1 = csub(t1, r21);
+            double2 dc0 = make_double2(S00 * t0.x + S01 * t1.x, S00 * t0.y + S01 * t1.y);
+            double2 dc1 = make_double2(S10 * t0.x + S11 * t1.x, S10 * t0.y + S11 * t1.y);
+            for (int k = 0; k < n; ++k) {
+                double2 dy = cfma(-aib[k], (k & 1) ? dc1 : dc0, B[(int64_t)k * M]);
+                A[(int64_t)k * M] = cadd(A[(int64_t)k * M], dy);
+            }
+            c0v = cadd(c0v, dc0);
+            c1v = cadd(c1v, dc1);
+        }
+    }
+    // ---- y = Q ypp + c0 T0 + c1 T1; derivative (downward recurrence,
+    // chebyshev.py:68-79), wall values, iDCT inputs
+    const double dscale = 2.0 / (a.z1 - a.z0);
+    double2 w_y0 = make_double2(0, 0), w_yH = make_double2(0, 0);
+    double2 w_d0 = make_double2(0, 0), w_dH = make_double2(0, 0);
+    double2 d_sum = make_double2(0, 0), d_sgn = make_double2(0, 0);
+    double2 bp1 = make_double2(0, 0), bp2 = make_double2(0, 0);   // b_{k+1}, b_{k+2}
+    double2 ynext = make_double2(0, 0);                              // y_{k+1}
+    double2* out_y = a.ext + 0 * M + m;
+    double2* out_d = a.ext + 1 * M + m;
+    // sliding window of ypp: a_{k-2}, a_k, a_{k+2}
+    double2 ap2 = make_double2(0, 0), ap1 = make_double2(0, 0);
+    double2 a0 = A[(int64_t)(n - 1) * M];
+    double2 am1 = (n >= 2) ? A[(int64_t)(n - 2) * M] : make_double2(0, 0);
+    for (int k = n - 1; k >= 0; --k) {
+        double2 am2 = (k >= 2) ? A[(int64_t)(k - 2) * M] : make_double2(0, 0);
+        double2 y = make_double2(0, 0);
+        if (k > 0) {
+            y = cscale(a0, q_dg[k]);
+            if (k >= 2) y = cadd(y, cscale(am2, q_lo[k]));
+            if (k + 2 < n) y = cadd(y, cscale(ap2, q_hi[k]));
+        }
+        if (k == 0) y = cadd(y, c0v);
+        if (k == 1) y = cadd(y, c1v);
+        double2 b;
+        if (k == n - 1) b = make_double2(0, 0);
+        else if (k == n - 2) b = cscale(ynext, 2.0 * (n - 1));
+        else b = cadd(bp2, cscale(ynext, 2.0 * (k + 1)));
+        double2 bs = cscale((k == 0) ? cscale(b, 0.5) : b, dscale);
+        w_y0 = cfma(a.tw0[k], y, w_y0);
+        w_yH = cfma(a.twH[k], y, w_yH);
+        w_d0 = cfma(a.tw0[k], bs, w_d0);
+        w_dH = cfma(a.twH[k], bs, w_dH);
+        d_sum = cadd(d_sum, bs);
+        d_sgn = (k & 1) ? csub(d_sgn, bs) : cadd(d_sgn, bs);
+        if (a.keep) a.keep[((int64_t)k * 2 + g) * M + m] = y;
+        if (emit) {
+            double hw = (k > 0 && k < N) ? 0.5 : 1.0;
+            double2 xy = cscale(y, hw), xd = cscale(bs, hw);
+            out_y[(int64_t)k * RS] = xy;
+            out_d[(int64_t)k * RS] = xd;
+            if (k > 0 && k < N) {
+                out_y[(int64_t)(2 * N - k) * RS] = xy;
+                out_d[(int64_t)(2 * N - k) * RS] = xd;
+            }
+        }
+        bp2 = bp1; bp1 = b; ynext = y;
+        ap2 = ap1; ap1 = a0; a0 = am1; am1 = am2;
+    }
+    wv[0] = w_y0; wv[1] = w_yH; wv[2] = w_d0; wv[3] = w_dH;
+    ends[0] = d_sgn; ends[1] = d_sum;
+}
+
+__device__ __forceinline__ bool finite2(double2 v) { return isfinite(v.x) && isfinite(v.y); }
+
+__global__ void bvp_kernel(BvpArgs a) {
+    int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (m >= a.M) return;
+    double2 wo[4], wi[4], eo[2], ei[2];
+    // the in-slab grid's raw data lives in slot 1, the over grid in slot 0;
+    // the over grid is solved first so its slot can be reused for output
+    if (a.two) solve_mode(a, m, 0, wo, eo, false);
+    solve_mode(a, m, 1, wi, ei, true);
+
+    double2 sb = a.sbh[m], st = a.sth[m];
+    double2 phib, eb, phit, et;
+    if (a.mode == 0) {                                   // slab.py:306-316
+        phib = csub(wi[0], cscale(wo[0], a.cb));
+        eb = cadd(csub(cscale(wi[2], a.eps), cscale(wo[2], a.eps_b * a.cb)), sb);
+        phit = csub(wi[1], cscale(wo[1], a.ct));
+        et = csub(csub(cscale(wi[3], a.eps), cscale(wo[3], a.eps_t * a.ct)), st);
+    } else {                                             // slab.py:322-324
+        phib = make_double2(0, 0); eb = sb;
+        phit = make_double2(0, 0); et = cscale(st, -1.0);
+    }
+    if (a.mism) {
+        a.mism[m] = phib; a.mism[a.M + m] = eb;
+        a.mism[2 * a.M + m] = phit; a.mism[3 * a.M + m] = et;
+    }
+    if (a.correction) {
+        if (!(finite2(phib) && finite2(eb) && finite2(phit) && finite2(et)))
+            atomicOr(a.flags, FLAG_NONFINITE);
+        double2 mb = make_double2(0, 0), mt = make_double2(0, 0);
+        if (a.sel[m]) {                                  // dpsolver.py:131-138
+            double k = a.kmag[m];
+            mb = cscale(csub(eb, cscale(phib, a.eps_b * k)), 1.0 / a.eps);
+            mt = cscale(cadd(cscale(phit, a.eps_t * k), et), 1.0 / a.eps);
+            double den = k * ((1.0 + a.rb) * (1.0 + a.rt)
+                              - (1.0 - a.rb) * (1.0 - a.rt) * exp(-2.0 * k * a.H));
+            mb = cscale(mb, 1.0 / den);
+            mt = cscale(mt, 1.0 / den);
+        }
+        a.mom[2 * m] = mb;
+        a.mom[2 * m + 1] = mt;
+    }
+    if (a.kidx[m] >= 0) return;
+    // ---- k = 0 linear modes                       slab.py:400-445, dpsolver.py:189-218
+    double* o = a.k0out;
+    double ai1, ai2, A_b, A_t, pib = wi[0].x, pit = wi[1].x, pbb, ptt;
+    int check = 0;
+    if (a.mode == 0) {
+        A_b = -(a.cb * eo[0].x);
+        A_t = -(a.ct * eo[1].x);
+        ai1 = (a.eps_b * (a.cb * wo[2].x + A_b) - a.eps * wi[2].x - sb.x) / a.eps;
+        ai2 = (a.eps_t * (a.ct * wo[3].x + A_t) - a.eps * wi[3].x + st.x) / a.eps;
+        pbb = a.cb * wo[0].x;
+        ptt = a.ct * wo[1].x;
+        check = 1;
+    } else {
+        double s0b = (a.mode == 1) ? sb.x : 0.0, s0t = (a.mode == 1) ? st.x : 0.0;
+        ai1 = -ei[0].x - s0b / a.eps;
+        ai2 = -ei[1].x + s0t / a.eps;
+        A_b = ai1; A_t = ai2;
+        pbb = pib; ptt = pit;
+    }
+    double ref = fmax(fmax(fabs(ai1), fabs(ai2)), fabs(a.k0_scale));
+    double disc = ref > 0 ? fabs(ai1 - ai2) / ref : 0.0;
+    if (check && disc > 1e-2) atomicOr(a.flags, FLAG_K0_FAIL);
+    else if (check && disc > 1e-3) atomicOr(a.flags, FLAG_K0_WARN);
+    double A_i = 0.5 * (ai1 + ai2);
+    o[0] = ai1; o[1] = ai2; o[2] = disc; o[3] = A_i; o[4] = A_b; o[5] = A_t;
+    o[6] = pib; o[7] = pit; o[8] = pbb; o[9] = ptt;
+    a.scal[0] = A_i;
+}
+
+// ---------------------------------------------------------------------------
+// assemble the spectral fields at the nodes: values + correction, and the
+// ik multipliers (Nyquist zeroed)                       slab.py:223-230,335-353
+// ---------------------------------------------------------------------------
+struct AsmArgs {
+    const double2* ext; double2* spec; const double2* mom;
+    const double* kx; const double* ky; const double* kmag; const unsigned char* sel;
+    const double* z; int Nz, Nx, Ny, Nyh; int64_t M;
+    int w0, w1;                  // correction window [w0, w1)
+    int corr, forces;
+    double rb, rt, H;
+};
+
+__global__ void assemble_kernel(AsmArgs a) {
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= (int64_t)a.Nz * a.M) return;
+    int j = (int)(e / a.M);
+    int64_t m = e % a.M;
+    const int N = a.Nz - 1;
+    const int64_t RS = 2 * a.M;
+    // iDCT output row r holds the node cos(pi r / N), i.e. ascending index N - r
+    double2 v = a.ext[(int64_t)(N - j) * RS + m];
+    double2 d = a.ext[(int64_t)(N - j) * RS + a.M + m];
+    if (a.corr && a.sel[m] && j >= a.w0 && j < a.w1) {
+        double k = a.kmag[m], z = a.z[j];
+        double e1 = exp(-k * z), e2 = exp(k * (z - a.H));
+        double e3 = exp(-k * (a.H + z)), e4 = exp(k * (z - 2.0 * a.H));
+        double pb = (a.rt + 1.0) * e1 - (a.rt - 1.0) * e4;
+        double pt = -(a.rb + 1.0) * e2 + (a.rb - 1.0) * e3;
+        double db = -k * ((a.rt + 1.0) * e1 + (a.rt - 1.0) * e4);
+        double dt = -k * ((a.rb + 1.0) * e2 + (a.rb - 1.0) * e3);
+        double2 mb = a.mom[2 * m], mt = a.mom[2 * m + 1];
+        v = cadd(v, cadd(cscale(mb, pb), cscale(mt, pt)));
+        d = cadd(d, cadd(cscale(mb, db), cscale(mt, dt)));
+    }
+    double2* out = a.spec + (int64_t)j * 4 * a.M + m;
+    out[0] = v;
+    if (a.forces) {
+        int ix = (int)(m / a.Nyh), iy = (int)(m % a.Nyh);
+        double ikx = (a.Nx % 2 == 0 && ix == a.Nx / 2) ? 0.0 : a.kx[ix];
+        double iky = (a.Ny % 2 == 0 && iy == a.Ny / 2) ? 0.0 : a.ky[iy];
+        out[a.M] = make_double2(-ikx * v.y, ikx * v.x);        // i kx v
+        out[2 * a.M] = make_double2(-iky * v.y, iky * v.x);    // i ky v
+        out[3 * a.M] = d;
+    }
+}
+
+Maps maps_of(Plan* p, const double* base) {
+    const int n = p->Nz;
+    Maps mp;
+    mp.e_lo = base; mp.e_hi = base + n; mp.q_lo = base + 2 * n;
+    mp.q_dg = base + 3 * n; mp.q_hi = base + 4 * n;
+    mp.ue = base + 5 * n; mp.uq = base + 6 * n; mp.ve = base + 7 * n; mp.vq = base + 8 * n;
+    return mp;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+void factor_bvp(Plan* p) {
+    const int n = p->Nz;
+    // integration maps (bvp.py:21-54) and BC column sums (bvp.py:110-121)
+    std::vector<double> h(9 * (size_t)n, 0.0);
+    double *e_lo = &h[0], *e_hi = &h[n], *q_lo = &h[2 * n], *q_dg = &h[3 * n], *q_hi = &h[4 * n];
+    if (n > 1) { e_lo[1] = 1.0; e_hi[1] = -0.5; q_dg[1] = -0.125; q_hi[1] = 0.125; }
+    if (n > 2) { e_lo[2] = 0.25; e_hi[2] = -0.25; q_lo[2] = 0.25; q_dg[2] = -1.0 / 6.0; q_hi[2] = 1.0 / 24.0; }
+    for (int m = 3; m < n; ++m) {
+        e_lo[m] = 0.5 / m;
+        e_hi[m] = -0.5 / m;
+        q_lo[m] = 1.0 / (4.0 * m * (m - 1));
+        q_dg[m] = -0.5 / ((double)m * m - 1.0);
+        q_hi[m] = 1.0 / (4.0 * m * (m + 1));
+    }
+    auto colsums = [&](const std::vector<double>& w, double* ue, double* uq) {
+        for (int j = 0; j < n - 1; ++j) ue[j] += w[j + 1] * e_lo[j + 1];
+        for (int j = 1; j < n; ++j) ue[j] += w[j - 1] * e_hi[j - 1];
+        for (int j = 0; j < n - 2; ++j) uq[j] += w[j + 2] * q_lo[j + 2];
+        for (int j = 0; j < n; ++j) uq[j] += w[j] * q_dg[j];
+        for (int j = 2; j < n; ++j) uq[j] += w[j - 2] * q_hi[j - 2];
+    };
+    std::vector<double> ones(n, 1.0), sgn(n);
+    for (int j = 0; j < n; ++j) sgn[j] = (j % 2 == 0) ? 1.0 : -1.0;
+    colsums(ones, &h[5 * n], &h[6 * n]);
+    colsums(sgn, &h[7 * n], &h[8 * n]);
+    p->d_maps = dalloc<double>(p, h.size());
+    SE_CUDA(cudaMemcpy(p->d_maps, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+    const int nu = std::max(p->n_uniq, 1);
+    p->d_fac = dalloc<double>(p, (size_t)nu * FAC_ROWS * n);
+    p->d_sinv = dalloc<double>(p, 4 * (size_t)nu);
+    p->d_kappa = dalloc<double>(p, (size_t)nu);
+    int* d_bad = dalloc<int>(p, 1);
+    SE_CUDA(cudaMemset(d_bad, 0, sizeof(int)));
+    if (p->n_uniq > 0) {
+        FactorArgs a{maps_of(p, p->d_maps), n, p->n_uniq, 0.5 * (p->P.z1 - p->P.z0),
+                     p->d_kuniq, p->d_fac, p->d_sinv, p->d_kappa, d_bad};
+        factor_kernel<<<(p->n_uniq + 127) / 128, 128, 0, p->stream>>>(a);
+        SE_LAUNCHED(p);
+    }
+    int bad = 0;
+    SE_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    SE_CUDA(cudaStreamSynchronize(p->stream));
+    if (bad) throw Error(SE_ERR_LINALG, "ill-conditioned Schur block in the mode BVP factorisation");
+}
+
+void forward_transforms(Plan* p, bool two_grids) {
+    (void)two_grids;
+    SE_CUFFT(cufftExecD2Z(p->fft_fwd2, p->d_rho, p->d_ext));
+    const int N = p->Nz - 1;
+    const int64_t row = 2 * p->M;
+    int64_t total = (int64_t)(N - 1) * row;
+    if (total > 0) {
+        mirror_kernel<<<(unsigned)((total + 255) / 256), 256, 0, p->stream>>>(
+            reinterpret_cast<double2*>(p->d_ext), N, row);
+        SE_LAUNCHED(p);
+    }
+    SE_CUFFT(cufftExecZ2Z(p->fft_z, p->d_ext, p->d_ext, CUFFT_FORWARD));
+}
+
+void bvp_solve(Plan* p, bool two_grids, int mode, bool correction) {
+    BvpArgs a{};
+    a.mp = maps_of(p, p->d_maps);
+    a.Nz = p->Nz; a.Nx = p->Nx; a.Nyh = p->Nyh; a.M = p->M;
+    a.half = 0.5 * (p->P.z1 - p->P.z0);
+    a.eps = p->P.eps; a.eps_b = p->P.eps_b; a.eps_t = p->P.eps_t;
+    a.cb = 2.0 * p->P.eps / (p->P.eps_b + p->P.eps);
+    a.ct = 2.0 * p->P.eps / (p->P.eps_t + p->P.eps);
+    a.z0 = p->P.z0; a.z1 = p->P.z1; a.k_max = p->P.k_max; a.k0_scale = p->k0_scale;
+    a.refine = p->P.refine; a.two = two_grids ? 1 : 0; a.mode = mode;
+    a.correction = correction ? 1 : 0;
+    a.kidx = p->d_kidx; a.kmag = p->d_kmag; a.sel = p->d_sel;
+    a.fac = p->d_fac; a.sinv = p->d_sinv; a.kappa = p->d_kappa;
+    a.tw0 = p->d_tw0; a.twH = p->d_twH;
+    a.sbh = reinterpret_cast<const double2*>(p->d_sbh);
+    a.sth = reinterpret_cast<const double2*>(p->d_sth);
+    a.ext = reinterpret_cast<double2*>(p->d_ext);
+    a.scrF = reinterpret_cast<double2*>(p->d_scr);
+    a.scrA = a.scrF + (int64_t)p->Nz * p->M;
+    a.scrB = a.scrA + (int64_t)p->Nz * p->M;
+    a.inv_nxy = 1.0 / (double)p->NXY;
+    a.mom = reinterpret_cast<double2*>(p->d_mom);
+    a.mism = reinterpret_cast<double2*>(p->d_mism);
+    a.keep = p->keep_stages ? reinterpret_cast<double2*>(p->d_keep) : nullptr;
+    a.k0out = p->d_k0; a.scal = p->d_scal; a.flags = p->d_flags;
+    a.rb = p->P.eps_b / p->P.eps; a.rt = p->P.eps_t / p->P.eps; a.H = p->P.H;
+    bvp_kernel<<<(unsigned)((p->M + 127) / 128), 128, 0, p->stream>>>(a);
+    SE_LAUNCHED(p);
+}
+
+void inverse_transforms(Plan* p, bool forces, bool correction) {
+    SE_CUFFT(cufftExecZ2Z(p->fft_z, p->d_ext, p->d_ext, CUFFT_FORWARD));
+    AsmArgs a{};
+    a.ext = reinterpret_cast<const double2*>(p->d_ext);
+    a.spec = reinterpret_cast<double2*>(p->d_spec);
+    a.mom = reinterpret_cast<const double2*>(p->d_mom);
+    a.kx = p->d_kx; a.ky = p->d_ky; a.kmag = p->d_kmag; a.sel = p->d_sel;
+    a.z = p->d_z; a.Nz = p->Nz; a.Nx = p->Nx; a.Ny = p->Ny; a.Nyh = p->Nyh; a.M = p->M;
+    a.w0 = p->win0; a.w1 = p->win1; a.corr = correction ? 1 : 0; a.forces = forces ? 1 : 0;
+    a.rb = p->P.eps_b / p->P.eps; a.rt = p->P.eps_t / p->P.eps; a.H = p->P.H;
+    int64_t total = (int64_t)p->Nz * p->M;
+    assemble_kernel<<<(unsigned)((total + 255) / 256), 256, 0, p->stream>>>(a);
+    SE_LAUNCHED(p);
+    if (forces) SE_CUFFT(cufftExecZ2D(p->fft_inv4, p->d_spec, p->d_fields));
+    else SE_CUFFT(cufftExecZ2D(p->fft_inv1, p->d_spec, p->d_fields));
+}
+
+}  // namespace se

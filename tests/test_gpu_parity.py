@@ -1,0 +1,123 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle and
+the reference-generated golden fixtures.
+
+Tolerances (north star): stencil / partition / pair membership bit-exact;
+phi, E and U within 1e-10 relative L2 in fp64.  Per-stage buffers are
+compared at 1e-11 (differences are summation order and erf/exp ulps only).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+os.environ.setdefault("SE_KEEP_STAGES", "1")
+
+from oracle import slab_oracle as O                              # noqa: E402
+from paper_2101_07088_b200 import workloads as W                 # noqa: E402
+from paper_2101_07088_b200.geometry import (ChargeSystem,        # noqa: E402
+                                            SlabGeometry, SurfaceCharge)
+from paper_2101_07088_b200.params import plan_grid               # noqa: E402
+from _golden import rel_l2, solves, stages                       # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+STAGE_TOL = 1e-11
+
+
+def _solver(system, params, refine=1):
+    from paper_2101_07088_b200.slab import SlabSolver
+    return SlabSolver(system, params, refine=refine)
+
+
+def _compare(res, ref, forces=True, tol=TOL):
+    phi, E, U, diag = ref
+    assert rel_l2(res.phi_bar, phi) < tol, rel_l2(res.phi_bar, phi)
+    if forces:
+        assert rel_l2(res.E_bar, E) < tol, rel_l2(res.E_bar, E)
+    assert abs(res.U - U) <= tol * max(1.0, abs(U)), (res.U, U)
+    assert abs(res.diagnostics["B_i"] - diag["B_i"]) <= tol * max(
+        1.0, abs(diag["B_i"]))
+
+
+def _tiny():
+    g = stages()
+    geo = SlabGeometry(1.5, 1.5, 1.0, 1.0, 0.05, 0.02)
+    system = ChargeSystem(geo, g["positions"], g["charges"], 0.03)
+    params = plan_grid(geo, 0.03, 1e-4, Nxy=24)
+    return g, system, params
+
+
+def test_stages_tiny_against_oracle():
+    g, system, params = _tiny()
+    solver = _solver(system, params)
+    res = solver.solve()
+    cap = {}
+    ref = O.OracleSlabSolver(system, params).solve(capture=cap)
+    nx, ny, nz = params.Nx, params.Ny, params.Nz
+    nyh = ny // 2 + 1
+    rho = solver.debug_fetch(0).reshape(nz, 2, nx, ny).transpose(1, 2, 3, 0)
+    assert rel_l2(rho[0], cap["rho_over"]) < STAGE_TOL
+    assert rel_l2(rho[1], cap["rho_in"]) < STAGE_TOL
+    keep = solver.debug_fetch(1).view(np.complex128).reshape(nz, 2, nx, nyh)
+    psi = keep.transpose(1, 2, 3, 0)
+    assert rel_l2(psi[0], cap["psi_o"][:, :nyh]) < STAGE_TOL
+    assert rel_l2(psi[1], cap["psi_i"][:, :nyh]) < STAGE_TOL
+    mism = solver.debug_fetch(3).view(np.complex128).reshape(4, nx, nyh)
+    for i, key in enumerate(("phi_b", "e_b", "phi_t", "e_t")):
+        assert rel_l2(mism[i], cap["mismatch"][key][:, :nyh]) < STAGE_TOL
+    fields = solver.debug_fetch(2).reshape(nz, 4, nx, ny).transpose(1, 2, 3, 0)
+    A_i = cap["k0"]["A_i"]
+    z = O.cheb_nodes(nz, params.z0, params.z1)
+    ref_f = cap["fields"]
+    assert rel_l2(fields[0] + A_i * z, ref_f[0]) < STAGE_TOL
+    assert rel_l2(-fields[1], ref_f[1]) < STAGE_TOL
+    assert rel_l2(-fields[2], ref_f[2]) < STAGE_TOL
+    assert rel_l2(-(fields[3] + A_i), ref_f[3]) < STAGE_TOL
+    _compare(res, ref)
+    # and against the reference fixture itself
+    assert rel_l2(res.phi_bar, g["phi"]) < TOL
+    assert rel_l2(res.E_bar, g["E"]) < TOL
+
+
+def test_partition_bit_exact():
+    from paper_2101_07088_b200.slab import build_partition
+    g, system, params = _tiny()
+    part = build_partition(system.positions, system.charges, system.geometry,
+                           params)
+    assert np.array_equal(part.over, g["over"])
+    assert np.array_equal(part.far, g["far_idx"])
+    assert np.array_equal(part.image_source, g["img_src"])
+    assert np.array_equal(part.image_wall, g["img_wall"])
+    assert np.array_equal(part.image_positions, g["img_pos"])
+    assert np.array_equal(part.image_strengths, g["img_str"])
+
+
+def test_partition_c3_bit_exact(golden_dir):
+    from paper_2101_07088_b200.slab import build_partition
+    gp = np.load(os.path.join(golden_dir, "partition_c3.npz"))
+    system, params = W.build("c3")
+    part = build_partition(system.positions, system.charges, system.geometry,
+                           params)
+    assert np.array_equal(part.over, gp["over"])
+    assert np.array_equal(part.image_source, gp["img_src"])
+    assert np.array_equal(part.image_wall, gp["img_wall"])
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "c3"])
+def test_workloads_against_golden(case):
+    gold = solves()[case]
+    system, params = W.build(case)
+    res = _solver(system, params).solve()
+    ref = (gold["phi"], gold["E"], float(gold["U"]), {"B_i": float(gold["B_i"])})
+    _compare(res, ref)
+    assert abs(res.diagnostics["k0"].A_i - gold["A_i"]) <= 1e-9 * max(
+        1.0, abs(gold["A_i"]))
+
+
+@pytest.mark.parametrize("case", ["c2", "c3"])
+def test_workloads_against_oracle(case):
+    system, params = W.build(case, N=4096 if case == "c3" else None)
+    res = _solver(system, params).solve()
+    _compare(res, O.oracle_solve(system, params))
