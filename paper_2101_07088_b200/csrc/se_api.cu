@@ -122,7 +122,7 @@ void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
     }
     if (!near_empty) {
         build_cells(p, d_pos, p->d_q, n);
-        near_eval(p, d_pos, p->d_tgt, n, kavg, p->d_near, p->d_count);
+        near_eval(p, d_pos, nullptr, n, kavg, p->d_near, p->d_count);
     } else {
         SE_CUDA(cudaMemsetAsync(p->d_near, 0, sizeof(double) * 4 * (size_t)std::max<int64_t>(n, 1), s));
     }

@@ -142,7 +142,7 @@ __global__ void stencil_kernel(StencilArgs a) {
     if ((a.keys[i] >> a.zbits) >= a.invalid_major) return;
     int s = a.perm[i];
     double4 v = a.src[s];
-    const int64_t S = a.st.S;
+    double* rec = a.st.rec + i * a.st.rs;
     // x axis: j0 = floor(x/h); delta = x - (j0+off)*h; keep |delta| <= r(1+1e-12)
     long long jx = (long long)floor(v.x / a.hx);
     for (int o = 0; o <= 2 * a.mx; ++o) {
@@ -153,8 +153,9 @@ __global__ void stencil_kernel(StencilArgs a) {
             double t = d / a.width;
             wt = exp(-0.5 * (t * t)) / a.norm;
         }
-        a.st.wx[o * S + i] = wt;
+        rec[o] = wt;
     }
+    rec += 2 * a.mx + 1;
     long long jy = (long long)floor(v.y / a.hy);
     for (int o = 0; o <= 2 * a.my; ++o) {
         double yj = __dmul_rn((double)(jy + o - a.my), a.hy);
@@ -164,8 +165,9 @@ __global__ void stencil_kernel(StencilArgs a) {
             double t = d / a.width;
             wt = exp(-0.5 * (t * t)) / a.norm;
         }
-        a.st.wy[o * S + i] = wt;
+        rec[o] = wt;
     }
+    rec += 2 * a.my + 1;
     // z axis: nodes in [searchsorted(z-r, left), searchsorted(z+r, right))
     int lo = lower_bound_d(a.znodes, a.Nz, __dsub_rn(v.z, a.rad));
     int hi = upper_bound_d(a.znodes, a.Nz, __dadd_rn(v.z, a.rad));
@@ -179,11 +181,12 @@ __global__ void stencil_kernel(StencilArgs a) {
                 wt = exp(-0.5 * (u * u)) / a.norm;
             }
         }
-        a.st.wzt[t * S + i] = wt;
+        rec[t] = wt;
     }
     a.st.j0x[i] = (int)jx;
     a.st.j0y[i] = (int)jy;
     a.st.lo[i] = lo;
+    a.st.hi[i] = hi < lo + a.wz ? hi : lo + a.wz;
     a.st.q[i] = v.w;
     a.st.owner[i] = a.owner_in[s];
 }
@@ -200,11 +203,12 @@ struct TileArgs {
 
 constexpr int MAX_BINS = 49;     // (2*3+1)^2
 
-// Build the list of candidate (bin, class) source ranges for the tile.
+// Candidate (bin, class) source ranges of the tile: sources are sorted by
+// first z node within each segment, so those that can reach nodes
+// [k0, k0 + TZ) form one contiguous range per bin (two binary searches).
 template <int TZ>
 __device__ void tile_ranges(const TileArgs& a, int bx, int by, int k0, int cls,
                             int* s_lo, int* s_len, int* s_nr, int* s_total) {
-    // bins along x / y (deduplicated when the ring wraps onto itself)
     int nxb = (2 * a.Rx + 1 >= a.nbx) ? a.nbx : 2 * a.Rx + 1;
     int nyb = (2 * a.Ry + 1 >= a.nby) ? a.nby : 2 * a.Ry + 1;
     int nr = nxb * nyb;
@@ -215,7 +219,6 @@ __device__ void tile_ranges(const TileArgs& a, int bx, int by, int k0, int cls,
         int byy = (nyb == a.nby) ? iy : pmod(by - a.Ry + iy, a.nby);
         int sg = (byy * a.nbx + bxx) * 2 + cls;
         int64_t b = a.seg[sg], e = a.seg[sg + 1];
-        // sources sorted by first node lo: keep lo in [k0 - wz + 1, k0 + TZ - 1]
         int want_lo = k0 - a.st.wz + 1, want_hi = k0 + TZ - 1;
         int64_t l = b, h = e;
         while (l < h) { int64_t mid = (l + h) >> 1; if (a.st.lo[mid] < want_lo) l = mid + 1; else h = mid; }
@@ -244,24 +247,130 @@ __device__ __forceinline__ int map_candidate(int idx, const int* s_lo,
     return -1;
 }
 
-// x (or y) weights of source i at the TILE columns starting at g0.
-__device__ __forceinline__ unsigned axis_tile_weights(
-        const double* w, int64_t S, int64_t i, int j0, int m, int n, int g0,
-        double scale, double* out) {
+__device__ __forceinline__ int imod(int a, int n) { int r = a % n; return r < 0 ? r + n : r; }
+
+// 8-byte asynchronous global -> shared copy (LDGSTS) and its completion wait
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// Shared-memory staging of up to CAP sources that touch the CTA tile.
+// Rows are per source so the compute loop reads a source's weights with
+// broadcast (vector) loads; the fill maps consecutive threads to consecutive
+// addresses both in shared memory and in the AoS stencil records.
+template <int TZ, int CAP, bool OWNER>
+struct Stage {
+    double wx[CAP][TILE];
+    double wy[CAP][TILE];
+    double wz[CAP][TZ];
+    double q[CAP];
+    int idx[CAP], lo[CAP], ox[CAP], oy[CAP];
+    unsigned xm[CAP], zm[CAP];
+    int own[OWNER ? CAP : 1];
+    int wcount[8];
+};
+
+// Mask of the TILE columns g0.. lying in the periodic stencil j0-m..j0+m;
+// *o0 returns the stencil offset of column g0.
+__device__ __forceinline__ unsigned axis_mask(int j0, int m, int n, int g0, int* o0) {
+    int o = imod(g0 - j0 + m, n);
+    *o0 = o;
     unsigned mask = 0;
 #pragma unroll
     for (int c = 0; c < TILE; ++c) {
-        int g = g0 + c;
-        double acc = 0.0;
-        if (g < n) {
-            int o = pmod((long long)g - j0 + m, n);
-            for (; o <= 2 * m; o += n) acc += w[o * S + i];
-        }
-        acc *= scale;
-        out[c] = acc;
-        if (acc != 0.0) mask |= 1u << c;
+        if (g0 + c < n && o <= 2 * m) mask |= 1u << c;
+        if (++o == n) o = 0;
     }
     return mask;
+}
+
+// One staging round: candidates [cursor, cursor + CAP) are tested against
+// the tile, the touching ones are compacted (warp ballots + block prefix)
+// and their tile-restricted weights staged.  Returns the staged count.
+template <int TZ, int NG, int CAP, bool OWNER, bool FOLD_Q>
+__device__ int stage_round(Stage<TZ, CAP, OWNER>& sm, const TileArgs& A, int cursor,
+                           int total, const int* s_lo, const int* s_len, int nr,
+                           int gx0, int gy0, int k0) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    constexpr int NW = CAP / 32;
+    bool touch = false;
+    int i = -1, lo = 0, ox = 0, oy = 0, own = 0;
+    unsigned xm = 0, zm = 0;
+    if (t < CAP && cursor + t < total) {
+        i = map_candidate(cursor + t, s_lo, s_len, nr);
+        if (OWNER && i >= 0) { own = A.st.owner[i]; if (own < 0) i = -1; }
+        if (i >= 0) {
+            lo = A.st.lo[i];
+            const int hi = A.st.hi[i];
+            xm = axis_mask(A.st.j0x[i], A.st.mx, A.Nx, gx0, &ox);
+            const unsigned ym = axis_mask(A.st.j0y[i], A.st.my, A.Ny, gy0, &oy);
+            constexpr int per = TZ / NG;
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                const int a0 = k0 + g * per, a1 = a0 + per;
+                if (lo < a1 && hi > a0) zm |= 1u << g;
+            }
+            touch = xm && ym && zm;
+        }
+    }
+    unsigned b = 0;
+    if (warp < NW) {
+        b = __ballot_sync(0xffffffffu, touch);
+        if (lane == 0) sm.wcount[warp] = __popc(b);
+    }
+    __syncthreads();
+    int base = 0, n = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        const int c = sm.wcount[w];
+        if (w < warp) base += c;
+        n += c;
+    }
+    if (touch) {
+        const int sl = base + __popc(b & ((1u << lane) - 1u));
+        sm.idx[sl] = i; sm.lo[sl] = lo; sm.ox[sl] = ox; sm.oy[sl] = oy;
+        sm.xm[sl] = xm; sm.zm[sl] = zm;
+        sm.q[sl] = FOLD_Q ? A.st.q[i] : 1.0;
+        if (OWNER) sm.own[OWNER ? sl : 0] = own;
+    }
+    __syncthreads();
+    const int rs = A.st.rs, mx = A.st.mx, my = A.st.my;
+    const int yoff = 2 * mx + 1, zoff = yoff + 2 * my + 1;
+    const bool simple = A.Nx >= 2 * mx + 1 && A.Ny >= 2 * my + 1;
+    // x / y weights: one stencil offset per column when the grid is wider
+    // than the stencil (async copies); otherwise sum the wrapped offsets
+    for (int e = threadIdx.x; e < n * TILE; e += blockDim.x) {
+        const int sl = e / TILE, c = e % TILE;
+        const double* rec = A.st.rec + (int64_t)sm.idx[sl] * rs;
+        int ox = sm.ox[sl] + c; if (ox >= A.Nx) ox -= A.Nx;
+        int oy = sm.oy[sl] + c; if (oy >= A.Ny) oy -= A.Ny;
+        const bool inx = gx0 + c < A.Nx, iny = gy0 + c < A.Ny;
+        if (simple) {
+            if (inx && ox <= 2 * mx) cp_async8(&sm.wx[sl][c], rec + ox); else sm.wx[sl][c] = 0.0;
+            if (iny && oy <= 2 * my) cp_async8(&sm.wy[sl][c], rec + yoff + oy); else sm.wy[sl][c] = 0.0;
+        } else {
+            double wxv = 0.0, wyv = 0.0;
+            if (inx) for (; ox <= 2 * mx; ox += A.Nx) wxv += rec[ox];
+            if (iny) for (; oy <= 2 * my; oy += A.Ny) wyv += rec[yoff + oy];
+            sm.wx[sl][c] = wxv;
+            sm.wy[sl][c] = wyv;
+        }
+    }
+    for (int e = threadIdx.x; e < n * TZ; e += blockDim.x) {
+        const int sl = e / TZ, r = e % TZ;
+        const int k = k0 + r, tt = k - sm.lo[sl];
+        if (tt >= 0 && tt < A.st.wz && k < A.Nz)
+            cp_async8(&sm.wz[sl][r], A.st.rec + (int64_t)sm.idx[sl] * rs + zoff + tt);
+        else
+            sm.wz[sl][r] = 0.0;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    return n;
 }
 
 // ---------------------------------------------------------------------------
@@ -273,23 +382,24 @@ struct SpreadArgs {
     int two;                     // slot 0 (over) as well as slot 1 (in)
 };
 
-__global__ void __launch_bounds__(256) spread_kernel(SpreadArgs a) {
+constexpr int SPREAD_CAP = 256;
+constexpr int INTERP_CAP = 128;
+using SpreadStage = Stage<SPREAD_TZ, SPREAD_CAP, false>;
+
+__global__ void __launch_bounds__(256, 2) spread_kernel(SpreadArgs a) {
     constexpr int TZ = SPREAD_TZ;       // 32 nodes = 4 groups of 8
-    __shared__ double s_wx[CHUNK][TILE];
-    __shared__ double s_wy[CHUNK][TILE];
-    __shared__ double s_wz[CHUNK][TZ];
-    __shared__ unsigned s_xm[CHUNK], s_ym[CHUNK], s_zm[2][CHUNK];
+    extern __shared__ __align__(16) unsigned char dsm[];
+    SpreadStage& sm = *reinterpret_cast<SpreadStage*>(dsm);
     __shared__ int s_lo[MAX_BINS], s_len[MAX_BINS], s_nr, s_total;
 
     const TileArgs& A = a.t;
     const int bx = blockIdx.x, by = blockIdx.y, k0 = blockIdx.z * TZ;
     const int gx0 = bx * TILE, gy0 = by * TILE;
-    const int t = threadIdx.x;
-    const int col = t & 63, tx = col >> 3, ty = col & 7, zg = t >> 6;
-    const int warp = t >> 5;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    // warp w: x columns 4(w&1)..+4, all 8 y columns, z group w>>1
+    const int tx = 4 * (warp & 1) + (lane >> 3), ty = lane & 7, zg = warp >> 1;
     const unsigned wxbits = 0xFu << (4 * (warp & 1));
     const unsigned wzbit = 1u << zg;
-    const int64_t S = A.st.S;
 
     double acc[8];
 #pragma unroll
@@ -299,53 +409,29 @@ __global__ void __launch_bounds__(256) spread_kernel(SpreadArgs a) {
     for (int cls = a.two ? 0 : 1; cls < 2; ++cls) {
         tile_ranges<TZ>(A, bx, by, k0, cls, s_lo, s_len, &s_nr, &s_total);
         const int total = s_total, nr = s_nr;
-        for (int base = 0; base < total; base += CHUNK) {
-            // ---- stage CHUNK sources: 4 parts (x, y, z lo half, z hi half)
-            const int slot = t & (CHUNK - 1), part = t >> 6;
-            const int idx = base + slot;
-            int i = (idx < total) ? map_candidate(idx, s_lo, s_len, nr) : -1;
-            if (part == 0) {
-                unsigned m = 0;
-                if (i >= 0) m = axis_tile_weights(A.st.wx, S, i, A.st.j0x[i], A.st.mx,
-                                                  A.Nx, gx0, A.st.q[i], s_wx[slot]);
-                else for (int c = 0; c < TILE; ++c) s_wx[slot][c] = 0.0;
-                s_xm[slot] = m;
-            } else if (part == 1) {
-                unsigned m = 0;
-                if (i >= 0) m = axis_tile_weights(A.st.wy, S, i, A.st.j0y[i], A.st.my,
-                                                  A.Ny, gy0, 1.0, s_wy[slot]);
-                else for (int c = 0; c < TILE; ++c) s_wy[slot][c] = 0.0;
-                s_ym[slot] = m;
-            } else {
-                const int h = part - 2;            // nodes k0 + 16h .. +16
-                unsigned m = 0;
-                int lo = (i >= 0) ? A.st.lo[i] : 0;
-#pragma unroll 4
-                for (int r = 0; r < 16; ++r) {
-                    int k = k0 + 16 * h + r;
-                    int tt = k - lo;
-                    double w = 0.0;
-                    if (i >= 0 && tt >= 0 && tt < A.st.wz && k < A.Nz)
-                        w = A.st.wzt[tt * S + i];
-                    s_wz[slot][16 * h + r] = w;
-                    if (w != 0.0) m |= 1u << ((16 * h + r) >> 3);
-                }
-                s_zm[h][slot] = m;
-            }
-            __syncthreads();
-            // ---- accumulate
-            const int nloc = min(CHUNK, total - base);
-            for (int s = 0; s < nloc; ++s) {
-                if ((s_xm[s] & wxbits) && ((s_zm[0][s] | s_zm[1][s]) & wzbit) && s_ym[s]) {
-                    const double cxy = s_wx[s][tx] * s_wy[s][ty];
-                    const double* wz = &s_wz[s][8 * zg];
+        for (int cursor = 0; cursor < total; cursor += SPREAD_CAP) {
+            const int n = stage_round<TZ, 4, SPREAD_CAP, false, true>(
+                sm, A, cursor, total, s_lo, s_len, nr, gx0, gy0, k0);
+            for (int w0 = 0; w0 < n; w0 += 32) {
+                const int s0 = w0 + lane;
+                const bool act = s0 < n && (sm.xm[s0] & wxbits) && (sm.zm[s0] & wzbit);
+                unsigned m = __ballot_sync(0xffffffffu, act);
+                while (m) {
+                    const int s = w0 + __ffs(m) - 1;
+                    m &= m - 1;
+                    const double cxy = (sm.q[s] * sm.wx[s][tx]) * sm.wy[s][ty];
+                    const double2* wz = reinterpret_cast<const double2*>(&sm.wz[s][8 * zg]);
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) acc[r] = fma(cxy, wz[r], acc[r]);
+                    for (int r = 0; r < 4; ++r) {
+                        const double2 w2 = wz[r];
+                        acc[2 * r] = fma(cxy, w2.x, acc[2 * r]);
+                        acc[2 * r + 1] = fma(cxy, w2.y, acc[2 * r + 1]);
+                    }
                 }
             }
             __syncthreads();
         }
-        // ---- store this class's running sum (slot 0 after class 0, 1 after 1)
+        // store this class's running sum (slot 0 after class 0, slot 1 after 1)
         if (gx < A.Nx && gy < A.Ny) {
             double* base_ptr = a.rho + (int64_t)(cls) * A.NXY + (int64_t)gx * A.Ny + gy;
 #pragma unroll
@@ -354,7 +440,6 @@ __global__ void __launch_bounds__(256) spread_kernel(SpreadArgs a) {
                 if (k < A.Nz) base_ptr[(int64_t)k * 2 * A.NXY] = acc[r];
             }
         }
-        __syncthreads();
     }
 }
 
@@ -371,26 +456,64 @@ struct InterpArgs {
     int nf;                      // 1 (potential only) or 4
 };
 
+// Butterfly transpose-reduction across the warp: lane l starts with 32
+// partial values v[0..31] and ends with the warp total of value index l.
+__device__ __forceinline__ double warp_transpose_reduce32(double (&v)[32], int lane) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const bool up = lane & 16;
+        const double send = up ? v[j] : v[j + 16], keep = up ? v[j + 16] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const bool up = lane & 8;
+        const double send = up ? v[j] : v[j + 8], keep = up ? v[j + 8] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const bool up = lane & 4;
+        const double send = up ? v[j] : v[j + 4], keep = up ? v[j + 4] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const bool up = lane & 2;
+        const double send = up ? v[j] : v[j + 2], keep = up ? v[j + 2] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    {
+        const bool up = lane & 1;
+        const double send = up ? v[0] : v[1], keep = up ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+    return v[0];
+}
+
+template <int NF>
+struct InterpSmem {
+    Stage<INTERP_TZ, INTERP_CAP, true> st;
+    double red[8][INTERP_CAP][NF];      // per-warp totals
+    unsigned done[8][INTERP_CAP / 32];  // which (warp, slot) entries are valid
+};
+
 template <int NF>
 __global__ void __launch_bounds__(256) interp_kernel(InterpArgs a) {
     constexpr int TZ = INTERP_TZ;       // 16 nodes = 4 groups of 4
-    __shared__ double s_wx[CHUNK][TILE];
-    __shared__ double s_wy[CHUNK][TILE];
-    __shared__ double s_wz[CHUNK][TZ];
-    __shared__ unsigned s_xm[CHUNK], s_ym[CHUNK], s_zm[CHUNK];
-    __shared__ int s_own[CHUNK];
-    __shared__ double s_red[8][CHUNK][NF];
+    constexpr int NB = 32 / NF;         // sources per transpose-reduce batch
+    extern __shared__ __align__(16) unsigned char dsm[];
+    InterpSmem<NF>& S = *reinterpret_cast<InterpSmem<NF>*>(dsm);
+    auto& sm = S.st;
     __shared__ int s_lo[MAX_BINS], s_len[MAX_BINS], s_nr, s_total;
 
     const TileArgs& A = a.t;
     const int bx = blockIdx.x, by = blockIdx.y, k0 = blockIdx.z * TZ;
     const int gx0 = bx * TILE, gy0 = by * TILE;
-    const int t = threadIdx.x;
-    const int col = t & 63, tx = col >> 3, ty = col & 7, zg = t >> 6;
-    const int warp = t >> 5, lane = t & 31;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int tx = 4 * (warp & 1) + (lane >> 3), ty = lane & 7, zg = warp >> 1;
     const unsigned wxbits = 0xFu << (4 * (warp & 1));
     const unsigned wzbit = 1u << zg;
-    const int64_t S = A.st.S;
     const int gx = gx0 + tx, gy = gy0 + ty;
     const double A_i = a.scal[0];
 
@@ -417,78 +540,59 @@ __global__ void __launch_bounds__(256) interp_kernel(InterpArgs a) {
     for (int cls = 0; cls < 2; ++cls) {
         tile_ranges<TZ>(A, bx, by, k0, cls, s_lo, s_len, &s_nr, &s_total);
         const int total = s_total, nr = s_nr;
-        for (int base = 0; base < total; base += CHUNK) {
-            const int slot = t & (CHUNK - 1), part = t >> 6;
-            const int idx = base + slot;
-            int i = (idx < total) ? map_candidate(idx, s_lo, s_len, nr) : -1;
-            int own = (i >= 0) ? A.st.owner[i] : -1;
-            if (own < 0) i = -1;                       // images are not targets
-            if (part == 0) {
-                unsigned m = 0;
-                if (i >= 0) m = axis_tile_weights(A.st.wx, S, i, A.st.j0x[i], A.st.mx,
-                                                  A.Nx, gx0, 1.0, s_wx[slot]);
-                else for (int c = 0; c < TILE; ++c) s_wx[slot][c] = 0.0;
-                s_xm[slot] = m;
-                s_own[slot] = own;
-            } else if (part == 1) {
-                unsigned m = 0;
-                if (i >= 0) m = axis_tile_weights(A.st.wy, S, i, A.st.j0y[i], A.st.my,
-                                                  A.Ny, gy0, 1.0, s_wy[slot]);
-                else for (int c = 0; c < TILE; ++c) s_wy[slot][c] = 0.0;
-                s_ym[slot] = m;
-            } else if (part == 2) {
-                unsigned m = 0;
-                int lo = (i >= 0) ? A.st.lo[i] : 0;
+        for (int cursor = 0; cursor < total; cursor += INTERP_CAP) {
+            const int n = stage_round<TZ, 4, INTERP_CAP, true, false>(
+                sm, A, cursor, total, s_lo, s_len, nr, gx0, gy0, k0);
+            for (int w0 = 0; w0 < INTERP_CAP; w0 += 32) {
+                const int s0 = w0 + lane;
+                const bool act = s0 < n && (sm.xm[s0] & wxbits) && (sm.zm[s0] & wzbit);
+                unsigned m = __ballot_sync(0xffffffffu, act);
+                if (lane == 0) S.done[warp][w0 >> 5] = m;
+                while (m) {
+                    double v[32];
+                    int first = w0 + __ffs(m) - 1;   // batch slots are first.. in mask order
+                    unsigned mb = m;
 #pragma unroll
-                for (int r = 0; r < TZ; ++r) {
-                    int k = k0 + r;
-                    int tt = k - lo;
-                    double w = 0.0;
-                    if (i >= 0 && tt >= 0 && tt < A.st.wz && k < A.Nz)
-                        w = A.st.wzt[tt * S + i];
-                    s_wz[slot][r] = w;
-                    if (w != 0.0) m |= 1u << (r >> 2);
-                }
-                s_zm[slot] = m;
-            }
-            // zero the per-warp reduction slots
-            for (int e = t; e < 8 * CHUNK * NF; e += 256) (&s_red[0][0][0])[e] = 0.0;
-            __syncthreads();
-            const int nloc = min(CHUNK, total - base);
-            for (int s = 0; s < nloc; ++s) {
-                if ((s_xm[s] & wxbits) && (s_zm[s] & wzbit) && s_ym[s]) {
-                    const double wxy = s_wx[s][tx] * s_wy[s][ty];
-                    const double* wz = &s_wz[s][4 * zg];
-                    double part_c[NF];
+                    for (int b = 0; b < NB; ++b) {
+                        if (mb) {
+                            const int s = w0 + __ffs(mb) - 1;
+                            mb &= mb - 1;
+                            const double wxy = sm.wx[s][tx] * sm.wy[s][ty];
+                            const double2* wz = reinterpret_cast<const double2*>(&sm.wz[s][4 * zg]);
+                            const double2 w01 = wz[0], w23 = wz[1];
 #pragma unroll
-                    for (int c = 0; c < NF; ++c) {
-                        double v = 0.0;
+                            for (int c = 0; c < NF; ++c) {
+                                double u = w01.x * F[c][0];
+                                u = fma(w01.y, F[c][1], u);
+                                u = fma(w23.x, F[c][2], u);
+                                u = fma(w23.y, F[c][3], u);
+                                v[b * NF + c] = u * wxy;
+                            }
+                        } else {
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) v = fma(wz[r], F[c][r], v);
-                        part_c[c] = v * wxy;
+                            for (int c = 0; c < NF; ++c) v[b * NF + c] = 0.0;
+                        }
                     }
-#pragma unroll
-                    for (int c = 0; c < NF; ++c) {
-#pragma unroll
-                        for (int off = 16; off > 0; off >>= 1)
-                            part_c[c] += __shfl_xor_sync(0xffffffffu, part_c[c], off);
-                    }
-                    if (lane == 0) {
-#pragma unroll
-                        for (int c = 0; c < NF; ++c) s_red[warp][s][c] = part_c[c];
-                    }
+                    (void)first;
+                    const double tot = warp_transpose_reduce32(v, lane);
+                    // lane l holds batch entry l / NF, field l % NF: find its slot
+                    unsigned mm = m;
+                    const int want = lane / NF;
+                    for (int b = 0; b < want && mm; ++b) mm &= mm - 1;
+                    if (mm) S.red[warp][w0 + __ffs(mm) - 1][lane % NF] = tot;
+                    m = mb;
                 }
             }
             __syncthreads();
-            // combine the 8 warps and push one atomic per (source, field)
-            for (int e = t; e < CHUNK * NF; e += 256) {
-                int s = e / NF, c = e % NF;
-                if (s < nloc && s_own[s] >= 0) {
-                    double v = 0.0;
+            // combine the warps that touched each staged source; one atomic per field
+            for (int e = t; e < n * NF; e += blockDim.x) {
+                const int s = e / NF, c = e % NF;
+                const unsigned bit = 1u << (s & 31);
+                double v = 0.0;
 #pragma unroll
-                    for (int w = 0; w < 8; ++w) v += s_red[w][s][c];
-                    if (v != 0.0) atomicAdd(&a.out[(int64_t)c * a.N + s_own[s]], v);
-                }
+                for (int w = 0; w < 8; ++w)
+                    if (S.done[w][s >> 5] & bit) v += S.red[w][s][c];
+                if (v != 0.0) atomicAdd(&a.out[(int64_t)c * a.N + sm.own[s]], v);
             }
             __syncthreads();
         }
@@ -563,7 +667,7 @@ void ensure_sources(Plan* p, int64_t n) {
     Stencils& st = p->ss.st;
     void* olds[] = {p->d_src, p->d_src_cls, p->d_src_owner, p->d_keys,
                     p->d_keys2, p->d_perm, p->d_perm2, p->d_cub, st.j0x,
-                    st.j0y, st.lo, st.q, st.wx, st.wy, st.wzt, st.owner};
+                    st.j0y, st.lo, st.hi, st.q, st.rec, st.owner};
     for (void* o : olds) dfree(p, o);
     p->d_src = dalloc<double4>(p, cap);
     p->d_src_cls = dalloc<int>(p, cap);
@@ -587,9 +691,10 @@ void ensure_sources(Plan* p, int64_t n) {
     st.j0y = dalloc<int>(p, cap);
     st.lo = dalloc<int>(p, cap);
     st.q = dalloc<double>(p, cap);
-    st.wx = dalloc<double>(p, (size_t)(2 * p->mx + 1) * cap);
-    st.wy = dalloc<double>(p, (size_t)(2 * p->my + 1) * cap);
-    st.wzt = dalloc<double>(p, (size_t)p->wz_max * cap);
+    st.hi = dalloc<int>(p, cap);
+    st.rs = (2 * p->mx + 1) + (2 * p->my + 1) + p->wz_max;
+    st.rs += st.rs & 1;
+    st.rec = dalloc<double>(p, (size_t)st.rs * cap);
     st.owner = dalloc<int>(p, cap);
     p->src_cap = cap;
 }
@@ -677,7 +782,13 @@ static TileArgs tile_args(Plan* p) {
 void spread(Plan* p, bool two_grids) {
     SpreadArgs a{tile_args(p), p->d_rho, two_grids ? 1 : 0};
     dim3 grid(p->ss.nbx, p->ss.nby, (p->Nz + SPREAD_TZ - 1) / SPREAD_TZ);
-    spread_kernel<<<grid, 256, 0, p->stream>>>(a);
+    const int smem = (int)sizeof(SpreadStage);
+    static bool attr = false;
+    if (!attr) {
+        SE_CUDA(cudaFuncSetAttribute(spread_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    spread_kernel<<<grid, 256, smem, p->stream>>>(a);
     SE_LAUNCHED(p);
 }
 
@@ -687,8 +798,16 @@ void interp_charges(Plan* p, int64_t n, bool forces) {
     InterpArgs a{tile_args(p), p->d_fields, p->d_z, p->d_wcc, p->d_scal, p->d_far,
                  n, forces ? 4 : 1};
     dim3 grid(p->ss.nbx, p->ss.nby, (p->Nz + INTERP_TZ - 1) / INTERP_TZ);
-    if (forces) interp_kernel<4><<<grid, 256, 0, p->stream>>>(a);
-    else interp_kernel<1><<<grid, 256, 0, p->stream>>>(a);
+    static bool attr = false;
+    if (!attr) {
+        SE_CUDA(cudaFuncSetAttribute(interp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(InterpSmem<4>)));
+        SE_CUDA(cudaFuncSetAttribute(interp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(InterpSmem<1>)));
+        attr = true;
+    }
+    if (forces) interp_kernel<4><<<grid, 256, sizeof(InterpSmem<4>), p->stream>>>(a);
+    else interp_kernel<1><<<grid, 256, sizeof(InterpSmem<1>), p->stream>>>(a);
     SE_LAUNCHED(p);
 }
 

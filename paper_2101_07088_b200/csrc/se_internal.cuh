@@ -87,10 +87,10 @@ struct Stencils {
     int* j0x = nullptr;          // floor(x / hx)
     int* j0y = nullptr;
     int* lo = nullptr;           // first z node
+    int* hi = nullptr;           // one past the last z node
     double* q = nullptr;         // strength
-    double* wx = nullptr;        // [(2mx+1)][S] Gaussian weights * keep
-    double* wy = nullptr;
-    double* wzt = nullptr;       // [wz][S]
+    int rs = 0;                  // record stride (doubles)
+    double* rec = nullptr;       // [S][rs]: wx[2mx+1] | wy[2my+1] | wz[wz]
     int* owner = nullptr;        // charge index of the source, -1 for images
 };
 
@@ -121,6 +121,17 @@ struct CellList {
 struct Buf {
     void* p = nullptr;
     size_t bytes = 0;
+};
+
+// scratch of near_eval: evaluation points sorted by cell, one-cell warp tasks
+struct NearScratch {
+    int64_t pcap = 0, ccap = 0, tcap = 0;
+    uint32_t *keys = nullptr, *keys2 = nullptr;
+    int *perm = nullptr, *order = nullptr, *pstart = nullptr, *pend = nullptr;
+    int *tcount = nullptr, *toff = nullptr;
+    int2* tasks = nullptr;
+    void* cub = nullptr;
+    size_t cub_bytes = 0;
 };
 
 struct Plan {
@@ -186,6 +197,7 @@ struct Plan {
 
     // near field
     CellList cl;
+    NearScratch ns;
     int64_t cl_cap = 0;
     uint32_t* d_ckeys = nullptr;
     uint32_t* d_ckeys2 = nullptr;

@@ -20,40 +20,18 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <type_traits>
 
 #include "se_internal.cuh"
+#include "se_erf_table.inc"
 
 namespace se {
 
 namespace {
 
 constexpr double TWO_OVER_SQRTPI = 1.1283791670955126;   // 2/sqrt(pi)
-constexpr int QN = 16;                                    // per-thread queue
 
 __device__ __forceinline__ int pmod_i(int a, int n) { int r = a % n; return r < 0 ? r + n : r; }
-
-// erf(r/c)/r and its r-derivative for one width c       kernels.py:38-72
-struct ErfPair { double v, d; };
-
-__device__ __forceinline__ ErfPair erf_terms(double r, double c, double inv_c,
-                                             bool need_d) {
-    ErfPair o;
-    if (r < 1e-10 * c) o.v = TWO_OVER_SQRTPI / c;
-    else o.v = erf(r / c) / r;
-    o.d = 0.0;
-    if (need_d) {
-        if (r < 1e-2 * c) {
-            double x = r / c, u = x * x;
-            o.d = TWO_OVER_SQRTPI / (c * c) * x *
-                  (-2.0 / 3.0 + u * (2.0 / 5.0 + u * (-1.0 / 7.0 + u / 27.0)));
-        } else {
-            double x = r / c;
-            o.d = TWO_OVER_SQRTPI * exp(-x * x) / (c * r) - erf(x) / (r * r);
-        }
-    }
-    (void)inv_c;
-    return o;
-}
 
 // ---------------------------------------------------------------------------
 // cell list
@@ -149,115 +127,316 @@ __global__ void cell_fill_kernel(const uint32_t* keys, const int* perm, int64_t 
 // ---------------------------------------------------------------------------
 struct NearArgs {
     const double* eval; const int* order; int64_t ne;
+    const int2* tasks; int64_t ntask; const int* ntask_dev; const int* pt_end;
     CellGeo g; const int* start; const double4* src; const float4* srcf;
-    double radius, c1, c2, inv4pie, self_value, point0;
+    double r2max;                 // largest r2 with sqrt(r2) <= r_query
+    double c1, c2, ic1, ic2, inv4pie, self_value, point0;
     int kind, need_field;
     float r2f;                    // fp32 pre-test bound (with margin)
+    float r2close;                // fp32 bound below which a pair may need the
+                                  // general (close) path
     float Lxf, Lyf, iLxf, iLyf;
     double* out; int64_t out_stride;   // out[c * stride + i]
     int64_t* npairs;
 };
 
-__device__ __forceinline__ void pair_terms(const NearArgs& a, double r,
-                                           double& g, double& coef) {
-    if (r == 0.0) {                              // slab.py:161-171,176
+constexpr int NB_THREADS = 128;
+constexpr int NQ = 48;            // per-lane far-pair queue (shared memory)
+constexpr int NQC = 12;           // per-lane close-pair queue
+
+// erf / erfc / exp(-x^2) of one argument.  erfc = exp(-x^2) erfcx(x) with
+// erfcx from the piecewise polynomial table (tools/gen_erfcx.py, ~2e-15
+// relative); a Maclaurin series below 0.5.  One exp serves both the
+// potential and the field.
+__device__ __forceinline__ void erf_erfc(double x, const double* tab, double& erf_v,
+                                         double& erfc_v, double& e) {
+    e = exp(-x * x);
+    if (x < SE_ERFCX_X0) {
+        const double u = x * x;
+        // erf(x) = 2/sqrt(pi) sum_n (-1)^n x^(2n+1) / (n! (2n+1))
+        double s = 1.0 / (479001600.0 * 25.0);
+        s = fma(s, u, -1.0 / (39916800.0 * 23.0));
+        s = fma(s, u, 1.0 / (3628800.0 * 21.0));
+        s = fma(s, u, -1.0 / (362880.0 * 19.0));
+        s = fma(s, u, 1.0 / (40320.0 * 17.0));
+        s = fma(s, u, -1.0 / (5040.0 * 15.0));
+        s = fma(s, u, 1.0 / (720.0 * 13.0));
+        s = fma(s, u, -1.0 / (120.0 * 11.0));
+        s = fma(s, u, 1.0 / (24.0 * 9.0));
+        s = fma(s, u, -1.0 / (6.0 * 7.0));
+        s = fma(s, u, 1.0 / (2.0 * 5.0));
+        s = fma(s, u, -1.0 / 3.0);
+        s = fma(s, u, 1.0);
+        erf_v = TWO_OVER_SQRTPI * x * s;
+        erfc_v = 1.0 - erf_v;
+    } else if (x < SE_ERFCX_X0 + SE_ERFCX_NP * SE_ERFCX_W) {
+        const int p = (int)((x - SE_ERFCX_X0) * (1.0 / SE_ERFCX_W));
+        const double t = (x - (SE_ERFCX_X0 + (p + 0.5) * SE_ERFCX_W)) * (2.0 / SE_ERFCX_W);
+        const double* c = tab + p * (SE_ERFCX_DEG + 1);
+        double acc = c[SE_ERFCX_DEG];
+#pragma unroll
+        for (int j = SE_ERFCX_DEG - 1; j >= 0; --j) acc = fma(acc, t, c[j]);
+        erfc_v = e * acc;
+        erf_v = 1.0 - erfc_v;
+    } else {
+        erfc_v = 0.0;
+        erf_v = 1.0;
+    }
+}
+
+// Near kernel between two widths (erf(r/c1) - erf(r/c2)) / (4 pi eps r) and
+// its radial derivative over r (kernels.py:38-113, slab.py:162-177).
+// FAR: r > 6.5 c1 and r >= 0.01 c2, where erf(r/c1) == 1 in fp64 and
+// exp(-(r/c1)^2) is below 1e-17 of the kernel: erfc-only form.
+template <bool FAR>
+__device__ __forceinline__ void pair_terms(const NearArgs& a, const double* tab,
+                                           double r2, double& g, double& coef) {
+    const bool nd = a.need_field;
+    if (!FAR && r2 == 0.0) {                     // slab.py:161-171,176
         g = (a.kind == 0) ? a.self_value : a.point0;
         coef = 0.0;
         return;
     }
-    ErfPair t1 = erf_terms(r, a.c1, 0.0, a.need_field);
-    ErfPair t2 = erf_terms(r, a.c2, 0.0, a.need_field);
-    g = (t1.v - t2.v) * a.inv4pie;
-    coef = a.need_field ? -((t1.d - t2.d) * a.inv4pie) / r : 0.0;
+    const double rinv = rsqrt(r2);
+    const double r = r2 * rinv;
+    const double x2 = r * a.ic2;
+    double E2, C2, e2;
+    erf_erfc(x2, tab, E2, C2, e2);
+    if (FAR || (r > 6.5 * a.c1 && r >= 1e-2 * a.c2)) {
+        g = C2 * rinv * a.inv4pie;
+        coef = 0.0;
+        if (nd) {
+            const double dd = -(C2 * rinv + TWO_OVER_SQRTPI * e2 * a.ic2) * rinv;
+            coef = -(dd * a.inv4pie) * rinv;
+        }
+        return;
+    }
+    double E1 = 1.0, C1 = 0.0, e1 = 0.0;
+    const double x1 = r * a.ic1;
+    if (r <= 6.5 * a.c1) erf_erfc(x1, tab, E1, C1, e1);
+    const double v1 = (r < 1e-10 * a.c1) ? TWO_OVER_SQRTPI * a.ic1 : E1 * rinv;
+    const double v2 = (r < 1e-10 * a.c2) ? TWO_OVER_SQRTPI * a.ic2 : E2 * rinv;
+    g = (v1 - v2) * a.inv4pie;
+    coef = 0.0;
+    if (!nd) return;
+    auto series = [](double x, double ic) {
+        double u = x * x;
+        return TWO_OVER_SQRTPI * (ic * ic) * x *
+               (-2.0 / 3.0 + u * (2.0 / 5.0 + u * (-1.0 / 7.0 + u / 27.0)));
+    };
+    double d1, d2;
+    if (r > 6.5 * a.c1) d1 = -rinv * rinv;
+    else if (r < 1e-2 * a.c1) d1 = series(x1, a.ic1);
+    else d1 = TWO_OVER_SQRTPI * e1 * a.ic1 * rinv - v1 * rinv;
+    if (r < 1e-2 * a.c2) d2 = series(x2, a.ic2);
+    else d2 = TWO_OVER_SQRTPI * e2 * a.ic2 * rinv - v2 * rinv;
+    coef = -((d1 - d2) * a.inv4pie) * rinv;
 }
 
-__global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
-    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    bool live = t < a.ne;
-    int64_t i = live ? (a.order ? a.order[t] : t) : 0;
+// exact displacement and squared distance, reference operation order
+//   d = p - s; d_xy -= L * round(d_xy / L); r2 = (dx^2 + dy^2) + dz^2
+__device__ __forceinline__ double min_image(double d, double L) {
+    if (fabs(d) <= 0.25 * L) return d;           // round(d/L) == 0 exactly
+    return __dsub_rn(d, __dmul_rn(L, rint(d / L)));
+}
+
+// Butterfly transpose-reduction across the warp: lane l starts with 32
+// partial values v[0..31] and ends with the warp total of value index l.
+__device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) {
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1) {
+        const bool up = lane & w;
+#pragma unroll
+        for (int j = 0; j < w; ++j) {
+            const double send = up ? v[j] : v[j + w], keep = up ? v[j + w] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+        }
+    }
+    return v[0];
+}
+
+// One warp per task; a task is up to 32 evaluation points of ONE cell, so
+// the neighbour cells and the candidate stream are warp-uniform and every
+// candidate load is a broadcast.  Lane = evaluation point.  Candidates are
+// drawn round-robin, 4 at a time, from all neighbour cells so every lane's
+// hit rate is the same over any window (hits from a single neighbour cell are
+// strongly clustered on the lanes near it); each lane queues its hits and the
+// warp drains the queues together, every lane evaluating its own pairs.
+constexpr int MAXNB = 27;
+
+template <bool WRAP_ALL>
+__global__ void __launch_bounds__(NB_THREADS, 4) near_kernel(NearArgs a) {
+    constexpr int W = NB_THREADS / 32;
+    __shared__ int lf[W][NQ][32];           // far-pair queues (lane-strided)
+    __shared__ int lc[W][NQC][32];          // close-pair queues
+    __shared__ int cb[W][MAXNB], ce[W][MAXNB];
+    __shared__ float csx[W][MAXNB], csy[W][MAXNB];
+    __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1)];
+    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+    for (int e = tid; e < SE_ERFCX_NP * (SE_ERFCX_DEG + 1); e += blockDim.x)
+        tab[e] = (&se_erfcx_tab[0][0])[e];
+    __syncthreads();
+    const int64_t task = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
+    if (task >= a.ntask || task >= *a.ntask_dev) return;
+    const int2 tk = a.tasks[task];                 // (cell, first sorted point)
+    const int cell = tk.x;
+    const int64_t slot = (int64_t)tk.y + lane;
+    const bool live = slot < a.pt_end[cell];
+    const int64_t i = live ? a.order[slot] : 0;
     double px = 0, py = 0, pz = 0;
     if (live) { px = a.eval[3 * i]; py = a.eval[3 * i + 1]; pz = a.eval[3 * i + 2]; }
-    int cx = 0, cy = 0, cz = 0;
-    cell_of(a.g, px, py, pz, &cx, &cy, &cz);
+    const int cx = cell % a.g.ncx, cy = (cell / a.g.ncx) % a.g.ncy, cz = cell / (a.g.ncx * a.g.ncy);
     const float pxf = (float)wrap(px, a.g.Lx), pyf = (float)wrap(py, a.g.Ly);
     const float pzf = (float)(pz - a.g.zlo);
     const double Lx = a.g.Lx, Ly = a.g.Ly;
+    const float r2f = live ? a.r2f : -1.0f;         // dead lanes never queue
+    const bool nd = a.need_field;
+
+    // neighbour cells: lane k sets up cell k.  A dimension with fewer than 3
+    // cells is walked completely (no duplicates) and wrapped per candidate.
+    const bool wx = a.g.ncx < 3, wy = a.g.ncy < 3;
+    const int nxr = wx ? a.g.ncx : 3, nyr = wy ? a.g.ncy : 3;
+    const int nnb = nxr * nyr * 3;
+    if (lane < nnb) {
+        const int k = lane;
+        const int dxi = k % nxr, dyi = (k / nxr) % nyr, dzi = k / (nxr * nyr);
+        const int zc = cz + dzi - 1;
+        int b = 0, e = 0;
+        float sx = 0.f, sy = 0.f;
+        if (zc >= 0 && zc < a.g.ncz) {
+            int yc = wy ? dyi : cy + dyi - 1, xc = wx ? dxi : cx + dxi - 1;
+            if (!wy) {
+                if (yc < 0) { yc += a.g.ncy; sy = -a.Lyf; } else if (yc >= a.g.ncy) { yc -= a.g.ncy; sy = a.Lyf; }
+            }
+            if (!wx) {
+                if (xc < 0) { xc += a.g.ncx; sx = -a.Lxf; } else if (xc >= a.g.ncx) { xc -= a.g.ncx; sx = a.Lxf; }
+            }
+            const int c = (zc * a.g.ncy + yc) * a.g.ncx + xc;
+            b = a.start[c];
+            e = a.start[c + 1];
+        }
+        cb[wib][k] = b; ce[wib][k] = e; csx[wib][k] = sx; csy[wib][k] = sy;
+    }
+    __syncwarp();
 
     double phi = 0, ex = 0, ey = 0, ez = 0;
-    int64_t count = 0;
-    int queue[QN];
-    int qn = 0;
+    int count = 0, qn = 0, qc = 0;
 
-    auto drain = [&]() {
-        for (int e = 0; e < qn; ++e) {
-            double4 s = a.src[queue[e]];
-            double dx = __dsub_rn(px, s.x), dy = __dsub_rn(py, s.y), dz = __dsub_rn(pz, s.z);
-            dx = __dsub_rn(dx, __dmul_rn(Lx, rint(dx / Lx)));
-            dy = __dsub_rn(dy, __dmul_rn(Ly, rint(dy / Ly)));
-            double r = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
-                                      __dmul_rn(dz, dz)));
+    auto one = [&](int j, auto far_tag) {
+        constexpr bool FAR = decltype(far_tag)::value;
+        const double4 sv = a.src[j];
+        const double dx = min_image(__dsub_rn(px, sv.x), Lx);
+        const double dy = min_image(__dsub_rn(py, sv.y), Ly);
+        const double dz = __dsub_rn(pz, sv.z);
+        const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                    __dmul_rn(dz, dz));
+        if (r2 <= a.r2max) {                   // == sqrt(r2) <= r_query
             double g, coef;
-            pair_terms(a, r, g, coef);
-            phi += s.w * g;
-            if (a.need_field) {
-                double cq = coef * s.w;
-                ex += cq * dx; ey += cq * dy; ez += cq * dz;
+            pair_terms<FAR>(a, tab, r2, g, coef);
+            phi = fma(sv.w, g, phi);
+            if (nd) {
+                const double cq = coef * sv.w;
+                ex = fma(cq, dx, ex); ey = fma(cq, dy, ey); ez = fma(cq, dz, ez);
             }
+            ++count;
         }
-        count += qn;
-        qn = 0;
     };
 
-    const int xs = (a.g.ncx >= 3) ? -1 : 0, xe = (a.g.ncx >= 3) ? 1 : a.g.ncx - 1;
-    const int ys = (a.g.ncy >= 3) ? -1 : 0, ye = (a.g.ncy >= 3) ? 1 : a.g.ncy - 1;
-    for (int dzc = -1; dzc <= 1; ++dzc) {
-        int zc = cz + dzc;
-        if (zc < 0 || zc >= a.g.ncz) continue;
-        for (int dyc = ys; dyc <= ye; ++dyc) {
-            int yc = (a.g.ncy >= 3) ? pmod_i(cy + dyc, a.g.ncy) : dyc;
-            for (int dxc = xs; dxc <= xe; ++dxc) {
-                int xc = (a.g.ncx >= 3) ? pmod_i(cx + dxc, a.g.ncx) : dxc;
-                int c = (zc * a.g.ncy + yc) * a.g.ncx + xc;
-                int b = a.start[c], e = a.start[c + 1];
-                for (int j = b; j < e; ++j) {
-                    bool hit = false;
-                    if (live) {
-                        float4 f = a.srcf[j];
-                        float dx = pxf - f.x, dy = pyf - f.y, dz = pzf - f.z;
-                        dx -= a.Lxf * rintf(dx * a.iLxf);
-                        dy -= a.Lyf * rintf(dy * a.iLyf);
-                        float r2 = dx * dx + dy * dy + dz * dz;
-                        if (r2 <= a.r2f) {
-                            double4 s = a.src[j];
-                            double ddx = __dsub_rn(px, s.x), ddy = __dsub_rn(py, s.y);
-                            double ddz = __dsub_rn(pz, s.z);
-                            ddx = __dsub_rn(ddx, __dmul_rn(Lx, rint(ddx / Lx)));
-                            ddy = __dsub_rn(ddy, __dmul_rn(Ly, rint(ddy / Ly)));
-                            double r = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(ddx, ddx),
-                                                                __dmul_rn(ddy, ddy)),
-                                                      __dmul_rn(ddz, ddz)));
-                            hit = r <= a.radius;
-                        }
+    for (;;) {
+        // -------- scan: round-robin over the neighbour cells, 4 candidates each
+        bool left = false;
+        for (int k = 0; k < nnb; ++k) {
+            const int b = cb[wib][k], e = ce[wib][k];
+            if (b >= e) continue;
+            left = true;
+            const int take = min(4, e - b);
+            const float qx = pxf - csx[wib][k], qy = pyf - csy[wib][k];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (u < take) {
+                    const float4 f = a.srcf[b + u];
+                    float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
+                    if (WRAP_ALL) {
+                        if (wx) dx -= a.Lxf * rintf(dx * a.iLxf);
+                        if (wy) dy -= a.Lyf * rintf(dy * a.iLyf);
                     }
-                    if (hit) queue[qn++] = j;
-                    if (__any_sync(__activemask(), qn == QN)) drain();
+                    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                    if (r2 <= r2f) {
+                        if (r2 > a.r2close) lf[wib][qn++][lane] = b + u;
+                        else lc[wib][qc++][lane] = b + u;
+                    }
                 }
             }
+            __syncwarp();
+            if (lane == 0) cb[wib][k] = b + take;
+            __syncwarp();
+            if (__any_sync(0xffffffffu, qn > NQ - 4 || qc > NQC - 4)) break;
         }
+        // -------- drain: every lane evaluates its own queued pairs
+        const bool fin = !__any_sync(0xffffffffu, left);
+        if (fin || __any_sync(0xffffffffu, qn > NQ - 4)) {
+            const int mx = __reduce_max_sync(0xffffffffu, qn);
+#pragma unroll 1
+            for (int e = 0; e < mx; e += 2) {
+                if (e < qn) one(lf[wib][e][lane], std::true_type{});
+                if (e + 1 < qn) one(lf[wib][e + 1][lane], std::true_type{});
+            }
+            qn = 0;
+        }
+        if (fin || __any_sync(0xffffffffu, qc > NQC - 4)) {
+            const int mx = __reduce_max_sync(0xffffffffu, qc);
+#pragma unroll 1
+            for (int e = 0; e < mx; ++e)
+                if (e < qc) one(lc[wib][e][lane], std::false_type{});
+            qc = 0;
+        }
+        if (fin) break;
     }
-    drain();
     if (live) {
         a.out[i] = phi;
-        if (a.need_field) {
+        if (nd) {
             a.out[a.out_stride + i] = ex;
             a.out[2 * a.out_stride + i] = ey;
             a.out[3 * a.out_stride + i] = ez;
         }
     }
-    // pair count (diagnostic)
-    unsigned long long c = live ? (unsigned long long)count : 0ull;
-    for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(__activemask(), c, off);
-    if ((threadIdx.x & 31) == 0 && a.npairs) atomicAdd((unsigned long long*)a.npairs, c);
+    unsigned long long cnt = (unsigned long long)count;
+    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    if (lane == 0 && a.npairs) atomicAdd((unsigned long long*)a.npairs, cnt);
+}
+
+// point tasks: per cell, ceil(count/32) warps
+__global__ void task_count_kernel(const int* pt_start, int ncell, int* ntask) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncell) return;
+    ntask[c] = (pt_start[c + 1] - pt_start[c] + 31) >> 5;
+}
+
+__global__ void task_fill_kernel(const int* pt_start, const int* toff, int ncell, int2* tasks,
+                                 int* pt_end) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncell) return;
+    int b = pt_start[c], e = pt_start[c + 1];
+    pt_end[c] = e;
+    int o = toff[c];
+    for (int f = b; f < e; f += 32) tasks[o++] = make_int2(c, f);
+}
+
+__global__ void point_starts_kernel(const uint32_t* keys, int64_t n, int ncell, int* start) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i > n) return;
+    int cur = (i < n) ? (int)keys[i] : ncell;
+    int prev = (i == 0) ? -1 : (int)keys[i - 1];
+    for (int c = prev + 1; c <= cur; ++c) start[c] = (int)i;
+}
+
+__global__ void point_keys_kernel(const double* pts, int64_t n, CellGeo g, uint32_t* keys,
+                                  int* perm) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int cx, cy, cz;
+    keys[i] = (uint32_t)cell_of(g, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], &cx, &cy, &cz);
+    perm[i] = (int)i;
 }
 
 // ---------------------------------------------------------------------------
@@ -404,14 +583,17 @@ void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n) {
         p->d_ckeys2, p->d_cperm2, ns, (int)ncell, p->d_near_src, g, cl.start, cl.src,
         cl.srcf, cl.orig);
     SE_LAUNCHED(p);
-    // charge targets in cell order (coherent warps)
-    cell_keys_kernel<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(
-        p->d_near_src, n, g, p->d_tkeys, p->d_tperm);
-    SE_LAUNCHED(p);
-    bytes = p->near_cub_bytes;
-    SE_CUDA(cub::DeviceRadixSort::SortPairs(p->d_near_cub, bytes, p->d_tkeys, p->d_tkeys2,
-                                            p->d_tperm, p->d_tgt, (int)n, 0, end_bit,
-                                            p->stream));
+}
+
+static double r2_threshold(double radius) {
+    // largest double t with sqrt(t) <= radius (IEEE sqrt on host == device)
+    double t = radius * radius;
+    while (std::sqrt(t) > radius) t = std::nextafter(t, -INFINITY);
+    for (;;) {
+        double u = std::nextafter(t, INFINITY);
+        if (std::sqrt(u) <= radius) t = u; else break;
+    }
+    return t;
 }
 
 void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
@@ -421,11 +603,16 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     a.eval = d_eval; a.order = d_order; a.ne = ne;
     a.g = cell_geo(p);
     a.start = p->cl.start; a.src = p->cl.src; a.srcf = p->cl.srcf;
-    a.radius = k.radius; a.c1 = k.c1; a.c2 = k.c2; a.inv4pie = k.inv4pie;
+    a.r2max = r2_threshold(k.radius);
+    a.c1 = k.c1; a.c2 = k.c2; a.ic1 = 1.0 / k.c1; a.ic2 = 1.0 / k.c2;
+    a.inv4pie = k.inv4pie;
     a.self_value = k.self_value; a.point0 = k.point0;
     a.kind = k.kind; a.need_field = k.need_field;
-    double rr = k.radius * (1.0 + 1e-4) + 1e-6 * (p->P.Lx + p->P.Ly + p->P.H);
+    double rr = k.radius * (1.0 + 1e-5) + 4e-7 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(p->cl.zlo));
     a.r2f = (float)(rr * rr);
+    // close path needed below max(6.5 c1, 0.01 c2) (+margin for fp32 error)
+    double rcl = std::max(6.5 * k.c1, 1e-2 * k.c2) * (1.0 + 1e-4) + 1e-6 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(p->cl.zlo));
+    a.r2close = (float)(rcl * rcl);
     a.Lxf = (float)p->P.Lx; a.Lyf = (float)p->P.Ly;
     a.iLxf = (float)(1.0 / p->P.Lx); a.iLyf = (float)(1.0 / p->P.Ly);
     a.out = d_out4; a.out_stride = ne;
@@ -435,7 +622,66 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
                                 p->stream));
         return;
     }
-    near_kernel<<<(unsigned)((ne + 127) / 128), 128, 0, p->stream>>>(a);
+    // sort the evaluation points by cell and cut them into one-cell warp tasks
+    const int ncell = p->cl.ncx * p->cl.ncy * p->cl.ncz;
+    NearScratch& ns = p->ns;
+    const int64_t tcap = ne / 32 + ncell + 1;
+    if (ne > ns.pcap || ncell + 1 > ns.ccap || tcap > ns.tcap) {
+        void* olds[] = {ns.keys, ns.keys2, ns.perm, ns.order, ns.pstart, ns.pend, ns.tcount,
+                        ns.toff, ns.tasks, ns.cub};
+        for (void* o : olds) dfree(p, o);
+        ns.pcap = std::max<int64_t>(ne, ns.pcap);
+        ns.ccap = std::max<int64_t>(ncell + 1, ns.ccap);
+        ns.tcap = std::max<int64_t>(tcap, ns.tcap);
+        ns.keys = dalloc<uint32_t>(p, ns.pcap);
+        ns.keys2 = dalloc<uint32_t>(p, ns.pcap);
+        ns.perm = dalloc<int>(p, ns.pcap);
+        ns.order = dalloc<int>(p, ns.pcap);
+        ns.pstart = dalloc<int>(p, ns.ccap + 1);
+        ns.pend = dalloc<int>(p, ns.ccap);
+        ns.tcount = dalloc<int>(p, ns.ccap + 1);
+        ns.toff = dalloc<int>(p, ns.ccap + 1);
+        ns.tasks = dalloc<int2>(p, ns.tcap);
+        size_t b1 = 0, b2 = 0;
+        SE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                                (int*)nullptr, (int*)nullptr, (int)ns.pcap, 0, 32,
+                                                p->stream));
+        SE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b2, (int*)nullptr, (int*)nullptr,
+                                              (int)ns.ccap + 1, p->stream));
+        ns.cub_bytes = std::max(b1, b2);
+        ns.cub = dalloc<char>(p, ns.cub_bytes);
+    }
+    CellGeo g = cell_geo(p);
+    point_keys_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, p->stream>>>(d_eval, ne, g, ns.keys,
+                                                                             ns.perm);
+    SE_LAUNCHED(p);
+    int end_bit = 1;
+    while (end_bit < 32 && ((uint64_t)ncell >> end_bit) != 0) ++end_bit;
+    size_t bytes = ns.cub_bytes;
+    SE_CUDA(cub::DeviceRadixSort::SortPairs(ns.cub, bytes, ns.keys, ns.keys2, ns.perm, ns.order,
+                                            (int)ne, 0, end_bit, p->stream));
+    point_starts_kernel<<<(unsigned)((ne + 1 + 255) / 256), 256, 0, p->stream>>>(ns.keys2, ne,
+                                                                                  ncell, ns.pstart);
+    SE_LAUNCHED(p);
+    task_count_kernel<<<(ncell + 255) / 256, 256, 0, p->stream>>>(ns.pstart, ncell, ns.tcount);
+    SE_LAUNCHED(p);
+    SE_CUDA(cudaMemsetAsync(ns.tcount + ncell, 0, sizeof(int), p->stream));
+    bytes = ns.cub_bytes;
+    SE_CUDA(cub::DeviceScan::ExclusiveSum(ns.cub, bytes, ns.tcount, ns.toff, ncell + 1,
+                                          p->stream));
+    task_fill_kernel<<<(ncell + 255) / 256, 256, 0, p->stream>>>(ns.pstart, ns.toff, ncell,
+                                                                 ns.tasks, ns.pend);
+    SE_LAUNCHED(p);
+    a.order = ns.order;
+    a.tasks = ns.tasks;
+    a.pt_end = ns.pend;
+    a.ntask_dev = ns.toff + ncell;
+    a.ntask = tcap;
+    const unsigned nblk = (unsigned)((tcap * 32 + NB_THREADS - 1) / NB_THREADS);
+    if (p->cl.ncx >= 3 && p->cl.ncy >= 3)
+        near_kernel<false><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+    else
+        near_kernel<true><<<nblk, NB_THREADS, 0, p->stream>>>(a);   // a dimension of <= 2 cells
     SE_LAUNCHED(p);
 }
 
