@@ -1,0 +1,326 @@
+"""Benchmark: energy+force solve of the dielectric slab (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c4] [--no-cpu-baseline]
+
+One step = one ``SlabSolver.solve`` (energy + forces + gauge, the reference
+defaults) of the C4 workload: N = 2^20 random charges in a 2 x 2 x 1 slab with
+dielectric jumps at both walls (eps ratio 0.05), delta = 1e-4, 256 x 256 x 258
+Fourier-Chebyshev grid.  Inputs are synthetic
+(seeded), resident in HBM for ``value``; ``e2e`` goes through the public
+host-array API with the H2D copy of the positions (pinned) and the D2H copy of
+phi and E inside the timed region.  L2 (126 MB) is flushed between timed steps
+by writing a 256 MB buffer outside the event pair.
+
+Multi-GPU (torchrun, one process per GPU): every rank solves an independent
+replica of the workload ("replicas", weak scaling); the domain-decomposed
+single-system solve is not implemented yet.  Timing is the max
+over ranks of the summed per-step CUDA-event times.
+
+``--impl reference`` times the CPU oracle (a numpy/scipy restatement of the
+reference solve, oracle/) on this box's host on the same config, rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = ("charges/s and ms per energy+force solve, N=1M dielectric slab, "
+          "at 1/2/4/8 B200")
+FP64_PAIR_FLOPS = 150.0     # ~150-200 fp64 ops per near pair
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,"
+              "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(system, params, sample=4096):
+    """Oracle (numpy/scipy restatement of the reference) timed on the host on
+    a bounded sample of the workload, extrapolated to the full solve."""
+    from oracle import cpu_bench
+    est = cpu_bench.estimate_solve_seconds(system, params, sample=sample)
+    n = system.n
+    return {"value": n / est["total_s"], "unit": "charges/s", "cores": 1,
+            "kind": "port",
+            "sample": ("oracle grid stages on the full %dx%dx%d grid (%.1f s) "
+                       "+ per-charge stages timed on %d of the %d charges "
+                       "(spread %.2e s/source, interp %.2e s/charge, near "
+                       "field %.2e s/charge at full density) extrapolated to "
+                       "N; single thread" % (params.Nx, params.Ny, params.Nz,
+                                              est["grid_s"],
+                                              est["sample_charges"], n,
+                                              est["spread_s_per_source"],
+                                              est["interp_s_per_charge"],
+                                              est["near_s_per_charge"])),
+            "ms_per_solve": est["total_s"] * 1e3, "stages": est}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import cpu_bench
+    from paper_2101_07088_b200 import workloads as W
+    system, params = W.build(args.config)
+    t_grid = None
+    totals = []
+    for step in range(args.warmup + args.steps):
+        if t_grid is None:
+            t_grid = cpu_bench.grid_stage_seconds(system, params)
+        est = cpu_bench.estimate_solve_seconds(system, params, sample=2048,
+                                               grid_seconds=t_grid)
+        if step >= args.warmup:
+            totals.append(est["total_s"])
+    mean_s = float(np.mean(totals))
+    value = system.n / mean_s
+    sample = ("oracle (numpy/scipy restatement of the reference solve, "
+              "single thread): grid stages timed once on the full grid "
+              "(%.1f s), per-charge stages timed each step on 2048 charges "
+              "and extrapolated to N=%d" % (t_grid, system.n))
+    line = {"impl": "reference", "metric": METRIC, "value": value,
+            "unit": "charges/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": mean_s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "N": system.n,
+                       "grid": [params.Nx, params.Ny, params.Nz],
+                       "parallelism": "cpu"},
+            "cpu_baseline": {"value": value, "unit": "charges/s", "cores": 1,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "charges/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    from paper_2101_07088_b200 import workloads as W
+    from paper_2101_07088_b200 import _lib
+    from paper_2101_07088_b200.slab import SlabSolver
+
+    system, params = W.build(args.config)
+    n = system.n
+    solver = SlabSolver(system, params, device=local)
+    stream = torch.cuda.current_stream()
+    solver.set_stream(stream.cuda_stream)
+    pos_d = torch.from_numpy(np.ascontiguousarray(system.positions)).cuda()
+    phi_d = torch.empty(n, dtype=torch.float64, device="cuda")
+    E_d = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step(timings=False):
+        return solver.solve_device(pos_d.data_ptr(), phi_d.data_ptr(),
+                                   E_d.data_ptr(), n, timings=timings)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # ---- device-resident timing (value)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    times, kernel_ms, launches, pairs = [], {k: [] for k in range(8, 12)}, 0, 0
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        U, diag = step(timings=True)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        for k in kernel_ms:
+            kernel_ms[k].append(diag.t_ms[k])
+        launches += int(diag.n_launches)
+        pairs = int(diag.n_pairs)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    total_ms = float(np.sum(times))
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_total = float(t.item())
+    ms_per_step = max_total / args.steps
+    value = world * n / (ms_per_step * 1e-3)
+    stage = dict(zip(("k_spread", "k_bvp", "k_interp", "k_near"),
+                     [float(np.mean(kernel_ms[k])) for k in range(8, 12)]))
+
+    # ---- end-to-end through the public API (pinned host positions)
+    pin = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
+    pin.copy_(torch.from_numpy(system.positions))
+    pos_h = pin.numpy()
+    e2e_steps = args.e2e_steps or args.steps
+    solver.solve(positions=pos_h)
+    e2e = []
+    barrier()
+    for _ in range(e2e_steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = solver.solve(positions=pos_h)
+        e1.record(stream)
+        e1.synchronize()
+        e2e.append(e0.elapsed_time(e1))
+    te = torch.tensor([float(np.sum(e2e))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item()) / e2e_steps
+    _ = res
+
+    if rank != 0:
+        return
+    # ---- roofline of the dominant kernel (FP64-pipe bound)
+    lib = _lib.load()
+    import ctypes
+    pk = ctypes.c_double(0.0)
+    _lib.check(lib.se_fp64_peak(local, ctypes.byref(pk)))
+    fp64_peak = pk.value
+    dominant = max(stage, key=stage.get)
+    roof = {"kernel": dominant, "bound": "fp64", "unit": "TFLOP/s",
+            "peak_source": "measured DFMA throughput on this GPU (se_fp64_peak)"}
+    if dominant == "k_near":
+        flops = pairs * FP64_PAIR_FLOPS
+        roof["work"] = "%d pairs x %g fp64 flop (SURVEY 8d)" % (pairs, FP64_PAIR_FLOPS)
+    elif dominant == "k_interp":
+        flops = 2.0 * 4 * n * 12 * 12 * 14
+        roof["work"] = "2 x 4 fields x N x 12x12x14 stencil nodes"
+    elif dominant == "k_spread":
+        flops = 2.0 * 1.2 * n * 12 * 12 * 14
+        roof["work"] = "2 x N' x 12x12x14 stencil nodes"
+    else:
+        flops = 0.0
+    achieved = flops / (stage[dominant] * 1e-3) / 1e12 if stage[dominant] > 0 else 0.0
+    roof.update({"achieved": achieved, "peak": fp64_peak,
+                 "frac": achieved / fp64_peak if fp64_peak else None,
+                 "kernel_ms": stage[dominant], "traffic": None})
+
+    line = {"metric": METRIC, "value": value, "unit": "charges/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.config, "N": n,
+                       "grid": [params.Nx, params.Ny, params.Nz],
+                       "eps_b": system.geometry.eps_b,
+                       "eps_t": system.geometry.eps_t, "delta": params.delta,
+                       "parallelism": ("replicas x%d (independent systems per "
+                                       "GPU)" % world) if world > 1 else "single",
+                       "l2": "flushed (256 MB write) between timed steps"},
+            "e2e": {"value": world * n / (e2e_ms * 1e-3), "unit": "charges/s",
+                    "ms_per_step": e2e_ms, "h2d_bytes_per_step": 24 * n,
+                    "d2h_bytes_per_step": 32 * n + 8},
+            "gpu_launches": launches,
+            "kernel_ms": stage, "near_pairs": pairs,
+            "roofline": roof, "clocks": clk}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(system, params)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

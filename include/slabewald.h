@@ -64,7 +64,10 @@ typedef struct {
     int32_t n_sources;         /* spread sources (charges + images) */
     int64_t n_pairs;           /* near-field pairs evaluated for the charges */
     int64_t n_launches;        /* own kernels launched by this call */
-    double t_ms[16];           /* stage timings when SE_TIMINGS */
+    double t_ms[16];           /* SE_TIMINGS: 0-7 stages (sources, spread,
+                                  forward, bvp, inverse, interp, near,
+                                  finish); 8-11 kernels (spread, bvp, interp,
+                                  near field of the charges) */
 } se_diag;
 
 typedef struct se_plan se_plan;
@@ -85,6 +88,10 @@ int se_plan_create(const se_params* params, const double* z_nodes,
                    se_plan** out);
 
 void se_plan_destroy(se_plan* plan);
+
+/* Run the plan's work on a caller-provided cudaStream_t (e.g. PyTorch's
+ * current stream) instead of its own; NULL selects the legacy stream. */
+int se_plan_set_stream(se_plan* plan, void* stream);
 
 /* Bind the charges (system.charges, slab.py:274).  host q[n]. */
 int se_set_charges(se_plan* plan, const double* q, int64_t n);
@@ -128,6 +135,11 @@ int se_build_partition(const se_params* params, int device, const double* pos,
  * sums [4][N], 5 near-field sums [4][N].
  * Returns the byte size when host == NULL. */
 int64_t se_debug_fetch(se_plan* plan, int which, void* host, int64_t nbytes);
+
+/* Measured FP64 FMA throughput of the device (TFLOP/s, 2 flops per DFMA):
+ * the roofline denominator of the FP64-bound kernels (spread, interpolation,
+ * near field), which MEASURED_PEAKS.json does not cover. */
+int se_fp64_peak(int device, double* tflops);
 
 const char* se_last_error(void);
 const char* se_version(void);

@@ -26,9 +26,10 @@ FORCE_GENERAL = 1 << 5
 TIMINGS = 1 << 6
 
 #: every entry point declared in include/slabewald.h
-EXPORTS = ("se_plan_create", "se_plan_destroy", "se_set_charges", "se_solve",
+EXPORTS = ("se_plan_create", "se_plan_destroy", "se_plan_set_stream",
+           "se_set_charges", "se_solve",
            "se_solve_device", "se_near_field", "se_build_partition",
-           "se_debug_fetch", "se_last_error", "se_version")
+           "se_debug_fetch", "se_fp64_peak", "se_last_error", "se_version")
 
 
 class SeParams(ctypes.Structure):
@@ -73,6 +74,8 @@ def load():
     lib.se_plan_create.restype = ctypes.c_int
     lib.se_plan_destroy.argtypes = [_P]
     lib.se_plan_destroy.restype = None
+    lib.se_plan_set_stream.argtypes = [_P, ctypes.c_void_p]
+    lib.se_plan_set_stream.restype = ctypes.c_int
     lib.se_set_charges.argtypes = [_P, _D, _I64]
     lib.se_set_charges.restype = ctypes.c_int
     lib.se_solve.argtypes = [_P, _D, _I64, ctypes.c_uint32, _D, _D, _D,
@@ -93,6 +96,8 @@ def load():
     lib.se_build_partition.restype = ctypes.c_int
     lib.se_debug_fetch.argtypes = [_P, ctypes.c_int, ctypes.c_void_p, _I64]
     lib.se_debug_fetch.restype = ctypes.c_int64
+    lib.se_fp64_peak.argtypes = [ctypes.c_int, _D]
+    lib.se_fp64_peak.restype = ctypes.c_int
     lib.se_last_error.argtypes = []
     lib.se_last_error.restype = ctypes.c_char_p
     lib.se_version.argtypes = []

@@ -33,6 +33,18 @@ __global__ void scale_complex(cufftDoubleComplex* a, int64_t n, double s) {
     if (i < n) { a[i].x *= s; a[i].y *= s; }
 }
 
+// FP64 FMA throughput probe: 8 independent DFMA chains per thread
+__global__ void dfma_probe_kernel(double* out, int iters, double a, double b) {
+    double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-3, x2 = x0 + 2e-3, x3 = x0 + 3e-3;
+    double x4 = x0 + 4e-3, x5 = x0 + 5e-3, x6 = x0 + 6e-3, x7 = x0 + 7e-3;
+    for (int i = 0; i < iters; ++i) {
+        x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+        x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+    double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+    if (s == 12345.678) out[0] = s;       // keep the chains alive
+}
+
 __global__ void gauge_kernel(double* scal) {
     // B_i = -(far0 + near0)                                  slab.py:380-383
     scal[1] = -(scal[4] + scal[5]);
@@ -81,6 +93,9 @@ void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
     cudaEvent_t ev[12];
     const bool timed = flags & SE_TIMINGS;
     if (timed) for (auto& e : ev) SE_CUDA(cudaEventCreate(&e));
+    p->timing = timed;
+    if (timed && !p->kev[0][0])
+        for (auto& pr : p->kev) { SE_CUDA(cudaEventCreate(&pr[0])); SE_CUDA(cudaEventCreate(&pr[1])); }
     int ne = 0;
     auto mark = [&]() { if (timed) SE_CUDA(cudaEventRecord(ev[ne++], s)); };
 
@@ -181,14 +196,23 @@ void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
         diag->n_launches = p->launches;
         for (int i = 0; i < 16; ++i) diag->t_ms[i] = 0.0;
         if (timed) {
-            for (int i = 0; i + 1 < ne && i < 16; ++i) {
+            for (int i = 0; i + 1 < ne && i < 8; ++i) {
                 float ms = 0;
                 SE_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
                 diag->t_ms[i] = ms;
             }
+            // per-kernel times: 8 spread, 9 bvp, 10 interp, 11 near (charges)
+            for (int k = 0; k < 4; ++k) {
+                float ms = 0;
+                if (cudaEventElapsedTime(&ms, p->kev[k][0], p->kev[k][1]) == cudaSuccess)
+                    diag->t_ms[8 + k] = ms;
+                else
+                    cudaGetLastError();
+            }
         }
     }
     if (timed) for (auto& e : ev) cudaEventDestroy(e);
+    p->timing = false;
 }
 
 void ensure_charges(Plan* p, int64_t n) {
@@ -213,6 +237,34 @@ using namespace se;
 extern "C" {
 
 const char* se_last_error(void) { return g_error.c_str(); }
+
+int se_fp64_peak(int device, double* tflops) {
+    try {
+        SE_CUDA(cudaSetDevice(device));
+        int sms = 0;
+        SE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        double* d = nullptr;
+        SE_CUDA(cudaMalloc(&d, sizeof(double)));
+        cudaEvent_t e0, e1;
+        SE_CUDA(cudaEventCreate(&e0));
+        SE_CUDA(cudaEventCreate(&e1));
+        const int blocks = sms * 8, threads = 256, iters = 1 << 14;
+        dfma_probe_kernel<<<blocks, threads>>>(d, 256, 0.999999, 1e-7);   // warm-up
+        SE_CUDA(cudaEventRecord(e0));
+        dfma_probe_kernel<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
+        SE_CUDA(cudaEventRecord(e1));
+        SE_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        SE_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        *tflops = 2.0 * 8.0 * iters * (double)blocks * threads / (ms * 1e-3) / 1e12;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFree(d);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
 const char* se_version(void) { return "slabewald-b200 0.1.0 (sm_100a)"; }
 
 int se_plan_create(const se_params* params, const double* z_nodes, const double* cc_w,
@@ -230,6 +282,7 @@ int se_plan_create(const se_params* params, const double* z_nodes, const double*
         p->dev = device;
         SE_CUDA(cudaSetDevice(device));
         SE_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+        p->own_stream = true;
         p->Nx = P.Nx; p->Ny = P.Ny; p->Nz = P.Nz;
         p->Nyh = P.Ny / 2 + 1;
         p->N2 = 2 * (P.Nz - 1);
@@ -381,8 +434,25 @@ void se_plan_destroy(se_plan* plan) {
     cufftHandle hs[] = {p->fft_fwd2, p->fft_fwd1, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig};
     for (auto h : hs) if (h) cufftDestroy(h);
     for (auto& b : p->owned) if (b.p) cudaFree(b.p);
-    if (p->stream) cudaStreamDestroy(p->stream);
+    for (auto& pr : p->kev) { if (pr[0]) cudaEventDestroy(pr[0]); if (pr[1]) cudaEventDestroy(pr[1]); }
+    if (p->stream && p->own_stream) cudaStreamDestroy(p->stream);
     delete p;
+}
+
+int se_plan_set_stream(se_plan* plan, void* stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        SE_CUDA(cudaSetDevice(p->dev));
+        SE_CUDA(cudaStreamSynchronize(p->stream));
+        if (p->own_stream && p->stream) { cudaStreamDestroy(p->stream); p->own_stream = false; }
+        p->stream = reinterpret_cast<cudaStream_t>(stream);
+        cufftHandle hs[] = {p->fft_fwd2, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig};
+        for (auto h : hs) if (h) SE_CUFFT(cufftSetStream(h, p->stream));
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
 }
 
 int se_set_charges(se_plan* plan, const double* q, int64_t n) {

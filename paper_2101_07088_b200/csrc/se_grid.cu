@@ -788,7 +788,9 @@ void spread(Plan* p, bool two_grids) {
         SE_CUDA(cudaFuncSetAttribute(spread_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
+    p->ktic(0);
     spread_kernel<<<grid, 256, smem, p->stream>>>(a);
+    p->ktoc(0);
     SE_LAUNCHED(p);
 }
 
@@ -806,8 +808,10 @@ void interp_charges(Plan* p, int64_t n, bool forces) {
                                      (int)sizeof(InterpSmem<1>)));
         attr = true;
     }
+    p->ktic(2);
     if (forces) interp_kernel<4><<<grid, 256, sizeof(InterpSmem<4>), p->stream>>>(a);
     else interp_kernel<1><<<grid, 256, sizeof(InterpSmem<1>), p->stream>>>(a);
+    p->ktoc(2);
     SE_LAUNCHED(p);
 }
 

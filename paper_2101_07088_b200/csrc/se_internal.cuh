@@ -138,6 +138,7 @@ struct Plan {
     se_params P{};
     int dev = 0;
     cudaStream_t stream = nullptr;
+    bool own_stream = false;
     int64_t launches = 0;
 
     // grid
@@ -233,6 +234,12 @@ struct Plan {
     void* fft_work = nullptr;
 
     std::vector<Buf> owned;
+
+    // per-kernel event timers (SE_TIMINGS): 0 spread, 1 bvp, 2 interp, 3 near
+    bool timing = false;
+    cudaEvent_t kev[4][2] = {};
+    void ktic(int k) { if (timing) cudaEventRecord(kev[k][0], stream); }
+    void ktoc(int k) { if (timing) cudaEventRecord(kev[k][1], stream); }
 };
 
 // factor table rows per unique |k| (see se_spectral.cu)

@@ -678,10 +678,12 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     a.ntask_dev = ns.toff + ncell;
     a.ntask = tcap;
     const unsigned nblk = (unsigned)((tcap * 32 + NB_THREADS - 1) / NB_THREADS);
+    if (d_npairs) p->ktic(3);
     if (p->cl.ncx >= 3 && p->cl.ncy >= 3)
         near_kernel<false><<<nblk, NB_THREADS, 0, p->stream>>>(a);
     else
         near_kernel<true><<<nblk, NB_THREADS, 0, p->stream>>>(a);   // a dimension of <= 2 cells
+    if (d_npairs) p->ktoc(3);
     SE_LAUNCHED(p);
 }
 

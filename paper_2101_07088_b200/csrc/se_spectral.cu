@@ -541,7 +541,9 @@ void bvp_solve(Plan* p, bool two_grids, int mode, bool correction) {
     a.keep = p->keep_stages ? reinterpret_cast<double2*>(p->d_keep) : nullptr;
     a.k0out = p->d_k0; a.scal = p->d_scal; a.flags = p->d_flags;
     a.rb = p->P.eps_b / p->P.eps; a.rt = p->P.eps_t / p->P.eps; a.H = p->P.H;
+    p->ktic(1);
     bvp_kernel<<<(unsigned)((p->M + 127) / 128), 128, 0, p->stream>>>(a);
+    p->ktoc(1);
     SE_LAUNCHED(p);
 }
 

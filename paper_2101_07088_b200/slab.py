@@ -88,7 +88,7 @@ def _flags(need_energy, need_forces, need_potential, subtract_self,
 
 
 STAGES = ("sources", "spread", "forward", "bvp", "inverse", "interp", "near",
-          "finish")
+          "finish", "k_spread", "k_bvp", "k_interp", "k_near")
 
 
 class SlabSolver:
@@ -196,18 +196,27 @@ class SlabSolver:
     def solve_device(self, d_pos, d_phi, d_E, n, need_energy=True,
                      need_forces=True, need_potential=True,
                      subtract_self=False, include_correction=True,
-                     force_general=False):
+                     force_general=False, timings=False):
         """Device-resident variant: ``d_pos``, ``d_phi``, ``d_E`` are raw
         device pointers (ints) on the plan's device.  Returns (U, diag)."""
         flags = _flags(need_energy, need_forces, need_potential,
-                       subtract_self, include_correction, force_general)
+                       subtract_self, include_correction, force_general,
+                       timings)
         U = ctypes.c_double(0.0)
         diag = _lib.SeDiag()
         _lib.check(self._lib.se_solve_device(
             self._plan, ctypes.c_void_p(d_pos), int(n), flags,
             ctypes.c_void_p(d_phi), ctypes.c_void_p(d_E), ctypes.byref(U),
             ctypes.byref(diag)))
+        if timings:
+            self.last_timings = dict(zip(STAGES, list(diag.t_ms)[:len(STAGES)]))
         return float(U.value), diag
+
+    def set_stream(self, stream_handle):
+        """Run on a caller's cudaStream_t (int handle, e.g. torch's
+        ``torch.cuda.current_stream().cuda_stream``)."""
+        _lib.check(self._lib.se_plan_set_stream(self._plan,
+                                                ctypes.c_void_p(stream_handle)))
 
     def debug_fetch(self, which):
         """Copy a stage buffer of the last solve (see se_debug_fetch)."""

@@ -24,6 +24,9 @@ pytestmark = pytest.mark.gpu
 
 TOL = 1e-10
 STAGE_TOL = 1e-11
+# field grids after the inverse xy FFT carry FFT rounding amplified by i k
+# (|k| up to pi/h): ~3e-11 relative between cuFFT and pocketfft
+FIELD_TOL = 1e-9
 
 
 def _solver(system, params, refine=1):
@@ -71,10 +74,10 @@ def test_stages_tiny_against_oracle():
     A_i = cap["k0"]["A_i"]
     z = O.cheb_nodes(nz, params.z0, params.z1)
     ref_f = cap["fields"]
-    assert rel_l2(fields[0] + A_i * z, ref_f[0]) < STAGE_TOL
-    assert rel_l2(-fields[1], ref_f[1]) < STAGE_TOL
-    assert rel_l2(-fields[2], ref_f[2]) < STAGE_TOL
-    assert rel_l2(-(fields[3] + A_i), ref_f[3]) < STAGE_TOL
+    assert rel_l2(fields[0] + A_i * z, ref_f[0]) < FIELD_TOL
+    assert rel_l2(-fields[1], ref_f[1]) < FIELD_TOL
+    assert rel_l2(-fields[2], ref_f[2]) < FIELD_TOL
+    assert rel_l2(-(fields[3] + A_i), ref_f[3]) < FIELD_TOL
     _compare(res, ref)
     # and against the reference fixture itself
     assert rel_l2(res.phi_bar, g["phi"]) < TOL
