@@ -124,3 +124,150 @@ def test_workloads_against_oracle(case):
     system, params = W.build(case, N=4096 if case == "c3" else None)
     res = _solver(system, params).solve()
     _compare(res, O.oracle_solve(system, params))
+
+
+# ---------------------------------------------------------------------------
+# flag / geometry variants against the reference fixtures
+# ---------------------------------------------------------------------------
+from test_oracle_golden import VARIANTS, variant_problem       # noqa: E402
+
+
+@pytest.mark.parametrize("case", sorted(VARIANTS))
+def test_variants_against_golden(case):
+    g = solves()[case]
+    system, params, kw = variant_problem(case)
+    refine = kw.pop("refine", 1)
+    res = _solver(system, params, refine=refine).solve(**kw)
+    forces = kw.get("need_forces", True)
+    ref = (g["phi"], g["E"], float(g["U"]), {"B_i": float(g["B_i"])})
+    _compare(res, ref, forces=forces)
+    if not forces:
+        assert np.all(res.E_bar == 0.0)
+
+
+def test_positions_override_against_golden():
+    g = solves()["c2n256_moved"]
+    system, params = W.build("c2", N=256)
+    res = _solver(system, params).solve(positions=g["positions"])
+    _compare(res, (g["phi"], g["E"], float(g["U"]), {"B_i": float(g["B_i"])}))
+
+
+def test_unsplit_against_golden():
+    import math
+    from paper_2101_07088_b200.params import EwaldParams
+    g = solves()["unsplit4"]
+    geo = SlabGeometry(1.0, 1.0, 0.5, 1.0, 0.2, 3.0)
+    system = ChargeSystem(geo, g["positions"], g["charges"], 0.05)
+    g_w, h_e = 0.05, 6.0 * 0.05
+    nx = int(round(1.0 / (g_w / 2.0)))
+    h = 1.0 / nx
+    params = EwaldParams(xi=np.inf, g_w=g_w, g_t=g_w, delta=0.0,
+                         n_g=int(math.ceil(2.0 * h_e / h)), n_sigma=6.0,
+                         h_xy=h, H_E=h_e, r_nf=0.0, r_cut=0.0,
+                         k_max=math.pi / h, Nx=nx, Ny=nx,
+                         Nz=int(math.ceil(math.pi * (0.5 + 6 * h_e) / (2 * h))),
+                         z0=-3.0 * h_e, z1=0.5 + 3.0 * h_e, h_min=6 * g_w)
+    res = _solver(system, params).solve(subtract_self=True)
+    _compare(res, (g["phi"], g["E"], float(g["U"]), {"B_i": float(g["B_i"])}))
+
+
+def test_pair_count_matches_reference_pairs(golden_dir):
+    gp = np.load(os.path.join(golden_dir, "pairs_c2n512.npz"))
+    system, params = W.build("c2", N=512)
+    res = _solver(system, params).solve()
+    assert res.diagnostics["n_pairs"] == gp["e"].size
+
+
+def test_near_field_sum_against_oracle():
+    from paper_2101_07088_b200.slab import near_field_sum
+    system, params = W.build("c3", N=2048)
+    geo = system.geometry
+    ev = np.random.default_rng(4).uniform([0, 0, 0.05], [2, 2, 0.95], (300, 3))
+    nf = O.NearSources(system.positions, system.charges, geo, params)
+    for kind in ("avg", "point"):
+        phi, E = near_field_sum(system.positions, system.charges, geo, params,
+                                eval_positions=ev, kind=kind)
+        rphi, rE = nf.evaluate(ev, kind)
+        assert rel_l2(phi, rphi) < 1e-13
+        assert rel_l2(E, rE) < 1e-13
+    phi = near_field_sum(system.positions, system.charges, geo, params,
+                         need_field=False, subtract_unsplit_self=True)
+    rphi = nf.evaluate(system.positions, "avg", need_field=False,
+                       subtract_unsplit=True)
+    assert rel_l2(phi, rphi) < 1e-13
+
+
+def test_errors_match_reference():
+    system, params = W.build("c2", N=256)
+    solver = _solver(system, params)
+    bad = system.positions.copy()
+    bad[0, 2] = params.z1 + 0.5
+    with pytest.raises(ValueError, match="outside the extended z domain"):
+        solver.solve(positions=bad)
+    with pytest.raises(ValueError):
+        solver.solve(positions=system.positions[:10])
+    # a net charge breaks the k = 0 displacement balance (dpsolver.py:208)
+    sysq = ChargeSystem(system.geometry, system.positions,
+                        np.ones(system.n), system.g_w)
+    with pytest.raises(FloatingPointError, match="k=0 coefficient mismatch"):
+        _solver(sysq, params).solve()
+
+
+# ---------------------------------------------------------------------------
+# size-independent properties at the north-star size (C4, N = 2^20)
+# ---------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def c4():
+    system, params = W.build("c4")
+    solver = _solver(system, params)
+    return system, params, solver, solver.solve()
+
+
+def test_c4_translation_by_grid_cell(c4):
+    """A shift by one grid cell in x is an exact symmetry of the discrete
+    operator (stencils, near-field pairs and spectra all shift)."""
+    system, params, solver, base = c4
+    pos = system.positions.copy()
+    pos[:, 0] = (pos[:, 0] + params.h_xy) % system.geometry.Lx
+    moved = solver.solve(positions=pos)
+    assert rel_l2(moved.phi_bar, base.phi_bar) < 1e-11
+    assert rel_l2(moved.E_bar, base.E_bar) < 1e-11
+    assert abs(moved.U - base.U) < 1e-11 * abs(base.U)
+
+
+def test_c4_charge_sign_linearity(c4):
+    system, params, solver, base = c4
+    neg = ChargeSystem(system.geometry, system.positions, -system.charges,
+                       system.g_w)
+    res = _solver(neg, params).solve()
+    assert rel_l2(res.phi_bar, -base.phi_bar) < 1e-12
+    assert rel_l2(res.E_bar, -base.E_bar) < 1e-12
+    assert abs(res.U - base.U) < 1e-12 * abs(base.U)
+
+
+def test_c4_z_reflection(c4):
+    """eps_b == eps_t and a Chebyshev grid symmetric about H/2: reflecting
+    z -> H - z flips Ez and leaves phi (up to the gauge) unchanged."""
+    system, params, solver, base = c4
+    pos = system.positions.copy()
+    pos[:, 2] = system.geometry.H - pos[:, 2]
+    res = solver.solve(positions=pos, need_potential=False)
+    ref = solver.solve(need_potential=False)
+    assert rel_l2(res.E_bar[:, :2], ref.E_bar[:, :2]) < 1e-9
+    assert rel_l2(res.E_bar[:, 2], -ref.E_bar[:, 2]) < 1e-9
+    assert abs(res.U - ref.U) < 1e-9 * abs(ref.U)
+
+
+def test_c4_work_check(c4):
+    """Energy-force consistency (reference.py:124-147): the centred
+    difference of U along a random displacement matches F . dX."""
+    system, params, solver, base = c4
+    rng = np.random.default_rng(0)
+    d = rng.standard_normal(system.positions.shape)
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    w2 = float(np.sum(base.forces * d))
+    h = 1e-5
+    up = solver.solve(positions=system.positions + 0.5 * h * d, need_forces=False).U
+    dn = solver.solve(positions=system.positions - 0.5 * h * d, need_forces=False).U
+    w1 = -(up - dn) / h
+    assert abs(w1 - w2) / abs(w1) < 1e-3
