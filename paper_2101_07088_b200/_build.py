@@ -35,7 +35,7 @@ def build(force=False, verbose=False):
            "-shared", "-Xptxas", "-v" if verbose else "-O3",
            "-o", LIB + ".tmp"]
     cmd += [os.path.join(CSRC, f) for f in SOURCES]
-    cmd += ["-L" + os.path.join(CUDA_HOME, "lib64"), "-lcufft",
+    cmd += ["-L" + os.path.join(CUDA_HOME, "lib64"), "-lcufft", "-lcublas",
             "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

@@ -100,6 +100,7 @@ void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
     auto mark = [&]() { if (timed) SE_CUDA(cudaEventRecord(ev[ne++], s)); };
 
     mark();
+    p->d_pos_cur = d_pos;
     // ---- far field: spread, transforms, mode BVPs, correction, inverse
     build_sources(p, d_pos, n, two);
     mark();
@@ -356,7 +357,8 @@ int se_plan_create(const se_params* params, const double* z_nodes, const double*
         // buffers
         p->d_rho = dalloc<double>(p, 2 * (size_t)p->G);
         SE_CUDA(cudaMemset(p->d_rho, 0, 2 * (size_t)p->G * sizeof(double)));
-        p->d_ext = dalloc<cufftDoubleComplex>(p, (size_t)p->N2 * 2 * p->M);
+        p->d_ext = dalloc<cufftDoubleComplex>(p, (size_t)nz * 2 * p->M);
+        p->d_hat = dalloc<cufftDoubleComplex>(p, (size_t)nz * 2 * p->M);
         p->d_spec = dalloc<cufftDoubleComplex>(p, (size_t)nz * 4 * p->M);
         p->d_fields = dalloc<double>(p, 4 * (size_t)p->G);
         p->d_scr = dalloc<cufftDoubleComplex>(p, 3 * (size_t)nz * p->M);
@@ -406,14 +408,9 @@ int se_plan_create(const se_params* params, const double* z_nodes, const double*
         make_plan2d(&p->fft_fwd2, p->Nx, p->Ny, p->Nyh, CUFFT_D2Z, p->NXY, p->M, 2 * nz, p->stream);
         make_plan2d(&p->fft_inv4, p->Nx, p->Ny, p->Nyh, CUFFT_Z2D, p->M, p->NXY, 4 * nz, p->stream);
         make_plan2d(&p->fft_inv1, p->Nx, p->Ny, p->Nyh, CUFFT_Z2D, 4 * p->M, 4 * p->NXY, nz, p->stream);
-        {
-            long long n1[1] = {p->N2}, emb[1] = {p->N2};
-            size_t ws = 0;
-            SE_CUFFT(cufftCreate(&p->fft_z));
-            SE_CUFFT(cufftMakePlanMany64(p->fft_z, 1, n1, emb, 2 * p->M, 1, emb, 2 * p->M, 1,
-                                         CUFFT_Z2Z, 2 * p->M, &ws));
-            SE_CUFFT(cufftSetStream(p->fft_z, p->stream));
-        }
+        SE_CUBLAS(cublasCreate(&p->blas));
+        SE_CUBLAS(cublasSetStream(p->blas, p->stream));
+        SE_CUBLAS(cublasSetMathMode(p->blas, CUBLAS_DEFAULT_MATH));
         SE_CUDA(cudaStreamSynchronize(p->stream));
         *out = reinterpret_cast<se_plan*>(p);
         return SE_OK;
@@ -433,6 +430,7 @@ void se_plan_destroy(se_plan* plan) {
     if (p->stream) cudaStreamSynchronize(p->stream);
     cufftHandle hs[] = {p->fft_fwd2, p->fft_fwd1, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig};
     for (auto h : hs) if (h) cufftDestroy(h);
+    if (p->blas) cublasDestroy(p->blas);
     for (auto& b : p->owned) if (b.p) cudaFree(b.p);
     for (auto& pr : p->kev) { if (pr[0]) cudaEventDestroy(pr[0]); if (pr[1]) cudaEventDestroy(pr[1]); }
     if (p->stream && p->own_stream) cudaStreamDestroy(p->stream);
@@ -449,6 +447,7 @@ int se_plan_set_stream(se_plan* plan, void* stream) {
         p->stream = reinterpret_cast<cudaStream_t>(stream);
         cufftHandle hs[] = {p->fft_fwd2, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig};
         for (auto h : hs) if (h) SE_CUFFT(cufftSetStream(h, p->stream));
+        if (p->blas) SE_CUBLAS(cublasSetStream(p->blas, p->stream));
         return SE_OK;
     } catch (const Error& e) {
         return fail(e);

@@ -199,6 +199,8 @@ struct TileArgs {
     const int64_t* seg; int nbx, nby;
     int Nx, Ny, Nz; int64_t NXY;
     int Rx, Ry;                  // neighbour bin radius
+    int TZ;                      // z nodes per tile of the calling kernel
+    int SX, SY, SZ;              // interp partial slots per dimension
 };
 
 constexpr int MAX_BINS = 49;     // (2*3+1)^2
@@ -271,6 +273,7 @@ struct Stage {
     int idx[CAP], lo[CAP], ox[CAP], oy[CAP];
     unsigned xm[CAP], zm[CAP];
     int own[OWNER ? CAP : 1];
+    int pslot[OWNER ? CAP : 1];     // interp: slot of this tile among the charge's tiles
     int wcount[8];
 };
 
@@ -335,7 +338,16 @@ __device__ int stage_round(Stage<TZ, CAP, OWNER>& sm, const TileArgs& A, int cur
         sm.idx[sl] = i; sm.lo[sl] = lo; sm.ox[sl] = ox; sm.oy[sl] = oy;
         sm.xm[sl] = xm; sm.zm[sl] = zm;
         sm.q[sl] = FOLD_Q ? A.st.q[i] : 1.0;
-        if (OWNER) sm.own[OWNER ? sl : 0] = own;
+        if (OWNER) {
+            sm.own[OWNER ? sl : 0] = own;
+            // tile offsets from the charge's first tile in x, y, z
+            const int fx = imod(A.st.j0x[i] - A.st.mx, A.Nx) / TILE;
+            const int fy = imod(A.st.j0y[i] - A.st.my, A.Ny) / TILE;
+            const int fz = lo / TZ;
+            const int sx = imod(gx0 / TILE - fx, A.nbx), sy = imod(gy0 / TILE - fy, A.nby);
+            const int sz = k0 / TZ - fz;
+            sm.pslot[OWNER ? sl : 0] = (sz * A.SY + sy) * A.SX + sx;
+        }
     }
     __syncthreads();
     const int rs = A.st.rs, mx = A.st.mx, my = A.st.my;
@@ -454,6 +466,7 @@ struct InterpArgs {
     double* out;                 // [4][N] raw sums
     int64_t N;
     int nf;                      // 1 (potential only) or 4
+    double* part;                // [SX*SY*SZ][nf][N] per-tile partial sums
 };
 
 // Butterfly transpose-reduction across the warp: lane l starts with 32
@@ -584,7 +597,8 @@ __global__ void __launch_bounds__(256) interp_kernel(InterpArgs a) {
                 }
             }
             __syncthreads();
-            // combine the warps that touched each staged source; one atomic per field
+            // combine the warps that touched each staged source and store the
+            // tile's partial sum in the charge's slot for this tile (no atomics)
             for (int e = t; e < n * NF; e += blockDim.x) {
                 const int s = e / NF, c = e % NF;
                 const unsigned bit = 1u << (s & 31);
@@ -592,11 +606,51 @@ __global__ void __launch_bounds__(256) interp_kernel(InterpArgs a) {
 #pragma unroll
                 for (int w = 0; w < 8; ++w)
                     if (S.done[w][s >> 5] & bit) v += S.red[w][s][c];
-                if (v != 0.0) atomicAdd(&a.out[(int64_t)c * a.N + sm.own[s]], v);
+                a.part[((int64_t)sm.pslot[s] * NF + c) * a.N + sm.own[s]] = v;
             }
             __syncthreads();
         }
     }
+}
+
+// per-charge sum of its tile partials: the touched tiles are exactly the
+// tiles intersecting the charge's stencil box (same test as the staging)
+struct PartArgs {
+    const double* part; double* out; int64_t N; int nf;
+    const int* j0x; const int* j0y; const int* lo; const int* hi; const int* perm_inv;
+    int mx, my, Nx, Ny, TZ, SX, SY;
+};
+
+__global__ void interp_reduce_kernel(PartArgs a, const double* pos, const double* znodes,
+                                     int Nz, double hx, double hy, double rad) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= a.N) return;
+    const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
+    const int jx = (int)floor(x / hx), jy = (int)floor(y / hy);
+    const int lo = lower_bound_d(znodes, Nz, __dsub_rn(z, rad));
+    const int hi = upper_bound_d(znodes, Nz, __dadd_rn(z, rad));
+    const int fx = imod(jx - a.mx, a.Nx), fy = imod(jy - a.my, a.Ny);
+    // tiles touched along x: those containing columns fx .. fx + 2mx (mod Nx)
+    auto ntiles = [](int f, int w, int n) {
+        int first = f / TILE, cnt = 0;
+        for (int c = 0; c < w; ++c) {                 // distinct tiles in order
+            int g = f + c; if (g >= n) g -= n;
+            int t = g / TILE;
+            int off = t - first; if (off < 0) off += (n + TILE - 1) / TILE;
+            if (off + 1 > cnt) cnt = off + 1;
+        }
+        return cnt;
+    };
+    const int nx = ntiles(fx, 2 * a.mx + 1, a.Nx), ny = ntiles(fy, 2 * a.my + 1, a.Ny);
+    const int nz = (hi > lo) ? (hi - 1) / a.TZ - lo / a.TZ + 1 : 0;
+    double acc[4] = {0, 0, 0, 0};
+    for (int sz = 0; sz < nz; ++sz)
+        for (int sy = 0; sy < ny; ++sy)
+            for (int sx = 0; sx < nx; ++sx) {
+                const int64_t sl = (int64_t)(sz * a.SY + sy) * a.SX + sx;
+                for (int c = 0; c < a.nf; ++c) acc[c] += a.part[(sl * a.nf + c) * a.N + i];
+            }
+    for (int c = 0; c < a.nf; ++c) a.out[(int64_t)c * a.N + i] = acc[c];
 }
 
 // ---------------------------------------------------------------------------
@@ -797,8 +851,20 @@ void spread(Plan* p, bool two_grids) {
 void interp_charges(Plan* p, int64_t n, bool forces) {
     SE_CUDA(cudaMemsetAsync(p->d_far, 0, sizeof(double) * 4 * (size_t)n, p->stream));
     if (n == 0) return;
-    InterpArgs a{tile_args(p), p->d_fields, p->d_z, p->d_wcc, p->d_scal, p->d_far,
-                 n, forces ? 4 : 1};
+    TileArgs ta = tile_args(p);
+    ta.TZ = INTERP_TZ;
+    ta.SX = (2 * p->mx + 1 + TILE - 2) / TILE + 1 + ((p->Nx % TILE) ? 1 : 0);
+    ta.SY = (2 * p->my + 1 + TILE - 2) / TILE + 1 + ((p->Ny % TILE) ? 1 : 0);
+    ta.SZ = (p->wz_max + INTERP_TZ - 2) / INTERP_TZ + 1;
+    const int nf = forces ? 4 : 1;
+    const int64_t need = (int64_t)ta.SX * ta.SY * ta.SZ * nf * n;
+    if (need > p->part_cap) {
+        dfree(p, p->d_part);
+        p->d_part = dalloc<double>(p, need);
+        p->part_cap = need;
+    }
+    InterpArgs a{ta, p->d_fields, p->d_z, p->d_wcc, p->d_scal, p->d_far,
+                 n, nf, p->d_part};
     dim3 grid(p->ss.nbx, p->ss.nby, (p->Nz + INTERP_TZ - 1) / INTERP_TZ);
     static bool attr = false;
     if (!attr) {
@@ -811,6 +877,11 @@ void interp_charges(Plan* p, int64_t n, bool forces) {
     p->ktic(2);
     if (forces) interp_kernel<4><<<grid, 256, sizeof(InterpSmem<4>), p->stream>>>(a);
     else interp_kernel<1><<<grid, 256, sizeof(InterpSmem<1>), p->stream>>>(a);
+    SE_LAUNCHED(p);
+    PartArgs pa{p->d_part, p->d_far, n, nf, nullptr, nullptr, nullptr, nullptr, nullptr,
+                p->mx, p->my, p->Nx, p->Ny, INTERP_TZ, ta.SX, ta.SY};
+    interp_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(
+        pa, p->d_pos_cur, p->d_z, p->Nz, p->hx, p->hy, p->rad);
     p->ktoc(2);
     SE_LAUNCHED(p);
 }

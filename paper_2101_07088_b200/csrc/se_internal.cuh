@@ -16,6 +16,7 @@
 
 #include <cuda_runtime.h>
 #include <cufft.h>
+#include <cublas_v2.h>
 
 #include <cstdint>
 #include <stdexcept>
@@ -51,6 +52,15 @@ struct Error : std::runtime_error {
             throw ::se::Error(SE_ERR_CUDA, std::string(#call) +              \
                                                ": cufft error " +            \
                                                std::to_string((int)r_));     \
+    } while (0)
+
+#define SE_CUBLAS(call)                                                      \
+    do {                                                                     \
+        cublasStatus_t s_ = (call);                                          \
+        if (s_ != CUBLAS_STATUS_SUCCESS)                                     \
+            throw ::se::Error(SE_ERR_CUDA, std::string(#call) +              \
+                                               ": cublas error " +           \
+                                               std::to_string((int)s_));     \
     } while (0)
 
 #define SE_LAUNCHED(plan)                                                    \
@@ -123,6 +133,12 @@ struct Buf {
     size_t bytes = 0;
 };
 
+// near-field pair lists (scan -> eval), point-major
+struct NearLists {
+    int64_t cap_far_total = 0, cap_close_total = 0, ncap = 0;
+    int *far = nullptr, *close = nullptr, *cfar = nullptr, *cclose = nullptr, *ovf = nullptr;
+};
+
 // scratch of near_eval: evaluation points sorted by cell, one-cell warp tasks
 struct NearScratch {
     int64_t pcap = 0, ccap = 0, tcap = 0;
@@ -178,6 +194,9 @@ struct Plan {
     double* d_phi = nullptr;              // [N]
     double* d_E = nullptr;                // [N][3]
     double* d_far = nullptr;              // [4][N] interp sums
+    double* d_part = nullptr;             // interp per-tile partials
+    int64_t part_cap = 0;
+    const double* d_pos_cur = nullptr;    // positions of the solve in flight
     double* d_near = nullptr;             // [4][N] near sums
     double* d_scal = nullptr;             // device scalars (A_i, B_i, U, ...)
     int* d_flags = nullptr;
@@ -199,6 +218,7 @@ struct Plan {
     // near field
     CellList cl;
     NearScratch ns;
+    NearLists nl;
     int64_t cl_cap = 0;
     uint32_t* d_ckeys = nullptr;
     uint32_t* d_ckeys2 = nullptr;
@@ -220,7 +240,10 @@ struct Plan {
 
     // grids
     double* d_rho = nullptr;              // [Nz][2][Nx][Ny]
-    cufftDoubleComplex* d_ext = nullptr;  // [2N][2][M]
+    cufftDoubleComplex* d_ext = nullptr;  // [Nz][2][M] Chebyshev coefficients
+    cufftDoubleComplex* d_hat = nullptr;  // [Nz][2][M] xy spectra / iDCT values
+    double *d_dct_fwd = nullptr, *d_dct_inv = nullptr;   // [Nz][Nz] column-major
+    cublasHandle_t blas = nullptr;
     cufftDoubleComplex* d_spec = nullptr; // [Nz][4][M]
     double* d_fields = nullptr;           // [Nz][4][Nx][Ny]
     cufftDoubleComplex* d_scr = nullptr;  // BVP scratch [3][Nz][M]

@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstdio>
 #include <type_traits>
 
 #include "se_internal.cuh"
@@ -138,11 +139,48 @@ struct NearArgs {
     float Lxf, Lyf, iLxf, iLyf;
     double* out; int64_t out_stride;   // out[c * stride + i]
     int64_t* npairs;
+    void* stats;
+    int* list_far; int* list_close; int64_t cap_far, cap_close;
+    int* cnt_far; int* cnt_close; int* overflow;
 };
 
 constexpr int NB_THREADS = 128;
 constexpr int NQ = 48;            // per-lane far-pair queue (shared memory)
 constexpr int NQC = 12;           // per-lane close-pair queue
+
+// exp(-u) for 0 <= u <= 700 without the special-case paths of libm exp:
+// Cody-Waite reduction by ln2, degree-11 Taylor polynomial on |r| <= ln2/2,
+// scaling by 2^n through the exponent bits.  ~1 ulp.
+__device__ __forceinline__ double exp_neg(double u) {
+    const double v = -u;
+    const double n = rint(v * 1.4426950408889634);
+    double r = fma(n, -6.93147180369123816490e-01, v);   // ln2 hi
+    r = fma(n, -1.90821492927058770002e-10, r);          // ln2 lo
+    double p = 2.5052108385441720e-08;                   // 1/11!
+    p = fma(p, r, 2.7557319223985893e-07);
+    p = fma(p, r, 2.7557319223985888e-06);
+    p = fma(p, r, 2.4801587301587302e-05);
+    p = fma(p, r, 1.9841269841269841e-04);
+    p = fma(p, r, 1.3888888888888889e-03);
+    p = fma(p, r, 8.3333333333333332e-03);
+    p = fma(p, r, 4.1666666666666664e-02);
+    p = fma(p, r, 1.6666666666666666e-01);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    const long long bits = (long long)(1023 + (int)n) << 52;
+    return p * __longlong_as_double(bits);
+}
+
+// 1/sqrt(x) for normal positive x: hardware approximation + 2 Newton steps
+__device__ __forceinline__ double rsqrt_pos(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double h = 0.5 * x;
+    y = y * fma(-h * y, y, 1.5);
+    y = y * fma(-h * y, y, 1.5);
+    return y;
+}
 
 // erf / erfc / exp(-x^2) of one argument.  erfc = exp(-x^2) erfcx(x) with
 // erfcx from the piecewise polynomial table (tools/gen_erfcx.py, ~2e-15
@@ -150,7 +188,7 @@ constexpr int NQC = 12;           // per-lane close-pair queue
 // potential and the field.
 __device__ __forceinline__ void erf_erfc(double x, const double* tab, double& erf_v,
                                          double& erfc_v, double& e) {
-    e = exp(-x * x);
+    e = exp_neg(fmin(x * x, 700.0));
     if (x < SE_ERFCX_X0) {
         const double u = x * x;
         // erf(x) = 2/sqrt(pi) sum_n (-1)^n x^(2n+1) / (n! (2n+1))
@@ -197,7 +235,7 @@ __device__ __forceinline__ void pair_terms(const NearArgs& a, const double* tab,
         coef = 0.0;
         return;
     }
-    const double rinv = rsqrt(r2);
+    const double rinv = (FAR || r2 > 1e-280) ? rsqrt_pos(r2) : rsqrt(r2);
     const double r = r2 * rinv;
     const double x2 = r * a.ic2;
     double E2, C2, e2;
@@ -233,6 +271,10 @@ __device__ __forceinline__ void pair_terms(const NearArgs& a, const double* tab,
     coef = -((d1 - d2) * a.inv4pie) * rinv;
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" :: "l"(p));
+}
+
 // exact displacement and squared distance, reference operation order
 //   d = p - s; d_xy -= L * round(d_xy / L); r2 = (dx^2 + dy^2) + dz^2
 __device__ __forceinline__ double min_image(double d, double L) {
@@ -255,146 +297,169 @@ __device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) 
     return v[0];
 }
 
-// One warp per task; a task is up to 32 evaluation points of ONE cell, so
-// the neighbour cells and the candidate stream are warp-uniform and every
-// candidate load is a broadcast.  Lane = evaluation point.  Candidates are
-// drawn round-robin, 4 at a time, from all neighbour cells so every lane's
-// hit rate is the same over any window (hits from a single neighbour cell are
-// strongly clustered on the lanes near it); each lane queues its hits and the
-// warp drains the queues together, every lane evaluating its own pairs.
+// ---------------------------------------------------------------------------
+// two-phase near field
+//  scan: one warp per task (<= 32 evaluation points of ONE cell; lane = point).
+//        The 27 neighbour cells are walked round-robin, 4 candidates per cell
+//        per visit, with an fp32 pre-test; survivors are appended to the
+//        point's far / close list in HBM (point-major, contiguous per lane).
+//  eval: one thread per evaluation point walks its own lists: exact fp64
+//        membership test and the erf kernels.  Lists have nearly equal
+//        lengths across a warp (same cell), so the evaluation is dense.
+// ---------------------------------------------------------------------------
 constexpr int MAXNB = 27;
+constexpr int SCAN_Q = 16;                  // per-lane staging before a flush
 
-template <bool WRAP_ALL>
-__global__ void __launch_bounds__(NB_THREADS, 4) near_kernel(NearArgs a) {
+__global__ void __launch_bounds__(NB_THREADS) near_scan_kernel(NearArgs a) {
     constexpr int W = NB_THREADS / 32;
-    __shared__ int lf[W][NQ][32];           // far-pair queues (lane-strided)
-    __shared__ int lc[W][NQC][32];          // close-pair queues
-    __shared__ int cb[W][MAXNB], ce[W][MAXNB];
-    __shared__ float csx[W][MAXNB], csy[W][MAXNB];
-    __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1)];
+    __shared__ int qf[W][SCAN_Q + 4][32];
+    __shared__ int qcl[W][SCAN_Q + 4][32];
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+    const int64_t task = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
+    if (task >= a.ntask || task >= *a.ntask_dev) return;
+    const int2 tk = a.tasks[task];
+    const int cell = tk.x;
+    const int64_t slot = (int64_t)tk.y + lane;
+    const bool live = slot < a.pt_end[cell];
+    const int64_t i = live ? a.order[slot] : 0;
+    float pxf = 0.f, pyf = 0.f, pzf = 0.f;
+    if (live) {
+        pxf = (float)wrap(a.eval[3 * i], a.g.Lx);
+        pyf = (float)wrap(a.eval[3 * i + 1], a.g.Ly);
+        pzf = (float)(a.eval[3 * i + 2] - a.g.zlo);
+    }
+    const int cx = cell % a.g.ncx, cy = (cell / a.g.ncx) % a.g.ncy, cz = cell / (a.g.ncx * a.g.ncy);
+    const float r2f = live ? a.r2f : -1.0f;
+    const float r2c = a.r2close;
+    const bool wx = a.g.ncx < 3, wy = a.g.ncy < 3;
+    const int nxr = wx ? a.g.ncx : 3, nyr = wy ? a.g.ncy : 3;
+    int* lfar = a.list_far + (int64_t)(slot < a.ne ? slot : 0) * a.cap_far;
+    int* lcls = a.list_close + (int64_t)(slot < a.ne ? slot : 0) * a.cap_close;
+    int nf = 0, nc = 0, qn = 0, qc = 0;
+    bool overflow = false;
+    // warp-wide flush of whole groups of 4 (16-byte stores, lists stay aligned)
+    auto flush = [&](int (*q)[32], int& cnt, int& n, int* list, int cap, bool all) {
+        const int m = all ? cnt : (cnt & ~3);
+        if (n + m + 4 > cap) { overflow = true; cnt = 0; return; }
+        for (int e = 0; e < m; e += 4) {
+            int4 v;
+            v.x = q[e][lane];
+            v.y = e + 1 < m ? q[e + 1][lane] : -1;
+            v.z = e + 2 < m ? q[e + 2][lane] : -1;
+            v.w = e + 3 < m ? q[e + 3][lane] : -1;
+            *reinterpret_cast<int4*>(list + n + e) = v;
+        }
+        n += (m + 3) & ~3;
+        for (int e = m; e < cnt; ++e) q[e - m][lane] = q[e][lane];
+        cnt -= m;
+    };
+    for (int dzi = 0; dzi < 3; ++dzi) {
+        const int zc = cz + dzi - 1;
+        if (zc < 0 || zc >= a.g.ncz) continue;
+        for (int dyi = 0; dyi < nyr; ++dyi) {
+            int yc = wy ? dyi : cy + dyi - 1;
+            float sy = 0.f;
+            if (!wy) {
+                if (yc < 0) { yc += a.g.ncy; sy = -a.Lyf; } else if (yc >= a.g.ncy) { yc -= a.g.ncy; sy = a.Lyf; }
+            }
+            // the three x-neighbours of a row are contiguous in the sort order
+            // unless the row wraps: walk them cell by cell
+            for (int dxi = 0; dxi < nxr; ++dxi) {
+                int xc = wx ? dxi : cx + dxi - 1;
+                float sx = 0.f;
+                if (!wx) {
+                    if (xc < 0) { xc += a.g.ncx; sx = -a.Lxf; } else if (xc >= a.g.ncx) { xc -= a.g.ncx; sx = a.Lxf; }
+                }
+                const int c = (zc * a.g.ncy + yc) * a.g.ncx + xc;
+                const int b = a.start[c], e = a.start[c + 1];
+                const float qx = pxf - sx, qy = pyf - sy;
+                int j = b;
+                for (; j < e; j += 4) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (j + u < e) {
+                            const float4 f = a.srcf[j + u];
+                            float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
+                            if (wx) dx -= a.Lxf * rintf(dx * a.iLxf);
+                            if (wy) dy -= a.Lyf * rintf(dy * a.iLyf);
+                            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                            if (r2 <= r2f) {
+                                if (r2 > r2c) qf[wib][qn++][lane] = j + u;
+                                else qcl[wib][qc++][lane] = j + u;
+                            }
+                        }
+                    }
+                    if (__any_sync(0xffffffffu, qn >= SCAN_Q)) flush(qf[wib], qn, nf, lfar, a.cap_far, false);
+                    if (__any_sync(0xffffffffu, qc >= SCAN_Q)) flush(qcl[wib], qc, nc, lcls, a.cap_close, false);
+                }
+            }
+        }
+    }
+    flush(qf[wib], qn, nf, lfar, a.cap_far, true);
+    flush(qcl[wib], qc, nc, lcls, a.cap_close, true);
+    if (live) {
+        a.cnt_far[slot] = nf;
+        a.cnt_close[slot] = nc;
+    }
+    if (overflow) atomicOr(a.overflow, 1);
+}
+
+template <bool FAR>
+__device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, const int* list,
+                                          int n, double px, double py, double pz, double& phi,
+                                          double& ex, double& ey, double& ez, int& count) {
+    const double Lx = a.g.Lx, Ly = a.g.Ly;
+    const bool nd = a.need_field;
+    for (int k = 0; k < n; k += 4) {
+        const int4 j4 = *reinterpret_cast<const int4*>(list + k);
+        const int jj[4] = {j4.x, j4.y, j4.z, j4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (jj[u] >= 0) {
+                const double4 sv = a.src[jj[u]];
+                const double dx = min_image(__dsub_rn(px, sv.x), Lx);
+                const double dy = min_image(__dsub_rn(py, sv.y), Ly);
+                const double dz = __dsub_rn(pz, sv.z);
+                const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                            __dmul_rn(dz, dz));
+                if (r2 <= a.r2max) {           // == sqrt(r2) <= r_query
+                    double g, coef;
+                    pair_terms<FAR>(a, tab, r2, g, coef);
+                    phi = fma(sv.w, g, phi);
+                    if (nd) {
+                        const double cq = coef * sv.w;
+                        ex = fma(cq, dx, ex); ey = fma(cq, dy, ey); ez = fma(cq, dz, ez);
+                    }
+                    ++count;
+                }
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(NB_THREADS, 6) near_eval_kernel(NearArgs a) {
+    __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1)];
+    const int tid = threadIdx.x, lane = tid & 31;
     for (int e = tid; e < SE_ERFCX_NP * (SE_ERFCX_DEG + 1); e += blockDim.x)
         tab[e] = (&se_erfcx_tab[0][0])[e];
     __syncthreads();
     const int64_t task = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
     if (task >= a.ntask || task >= *a.ntask_dev) return;
-    const int2 tk = a.tasks[task];                 // (cell, first sorted point)
-    const int cell = tk.x;
+    const int2 tk = a.tasks[task];
     const int64_t slot = (int64_t)tk.y + lane;
-    const bool live = slot < a.pt_end[cell];
-    const int64_t i = live ? a.order[slot] : 0;
-    double px = 0, py = 0, pz = 0;
-    if (live) { px = a.eval[3 * i]; py = a.eval[3 * i + 1]; pz = a.eval[3 * i + 2]; }
-    const int cx = cell % a.g.ncx, cy = (cell / a.g.ncx) % a.g.ncy, cz = cell / (a.g.ncx * a.g.ncy);
-    const float pxf = (float)wrap(px, a.g.Lx), pyf = (float)wrap(py, a.g.Ly);
-    const float pzf = (float)(pz - a.g.zlo);
-    const double Lx = a.g.Lx, Ly = a.g.Ly;
-    const float r2f = live ? a.r2f : -1.0f;         // dead lanes never queue
-    const bool nd = a.need_field;
-
-    // neighbour cells: lane k sets up cell k.  A dimension with fewer than 3
-    // cells is walked completely (no duplicates) and wrapped per candidate.
-    const bool wx = a.g.ncx < 3, wy = a.g.ncy < 3;
-    const int nxr = wx ? a.g.ncx : 3, nyr = wy ? a.g.ncy : 3;
-    const int nnb = nxr * nyr * 3;
-    if (lane < nnb) {
-        const int k = lane;
-        const int dxi = k % nxr, dyi = (k / nxr) % nyr, dzi = k / (nxr * nyr);
-        const int zc = cz + dzi - 1;
-        int b = 0, e = 0;
-        float sx = 0.f, sy = 0.f;
-        if (zc >= 0 && zc < a.g.ncz) {
-            int yc = wy ? dyi : cy + dyi - 1, xc = wx ? dxi : cx + dxi - 1;
-            if (!wy) {
-                if (yc < 0) { yc += a.g.ncy; sy = -a.Lyf; } else if (yc >= a.g.ncy) { yc -= a.g.ncy; sy = a.Lyf; }
-            }
-            if (!wx) {
-                if (xc < 0) { xc += a.g.ncx; sx = -a.Lxf; } else if (xc >= a.g.ncx) { xc -= a.g.ncx; sx = a.Lxf; }
-            }
-            const int c = (zc * a.g.ncy + yc) * a.g.ncx + xc;
-            b = a.start[c];
-            e = a.start[c + 1];
-        }
-        cb[wib][k] = b; ce[wib][k] = e; csx[wib][k] = sx; csy[wib][k] = sy;
-    }
-    __syncwarp();
-
+    const bool live = slot < a.pt_end[tk.x];
     double phi = 0, ex = 0, ey = 0, ez = 0;
-    int count = 0, qn = 0, qc = 0;
-
-    auto one = [&](int j, auto far_tag) {
-        constexpr bool FAR = decltype(far_tag)::value;
-        const double4 sv = a.src[j];
-        const double dx = min_image(__dsub_rn(px, sv.x), Lx);
-        const double dy = min_image(__dsub_rn(py, sv.y), Ly);
-        const double dz = __dsub_rn(pz, sv.z);
-        const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
-                                    __dmul_rn(dz, dz));
-        if (r2 <= a.r2max) {                   // == sqrt(r2) <= r_query
-            double g, coef;
-            pair_terms<FAR>(a, tab, r2, g, coef);
-            phi = fma(sv.w, g, phi);
-            if (nd) {
-                const double cq = coef * sv.w;
-                ex = fma(cq, dx, ex); ey = fma(cq, dy, ey); ez = fma(cq, dz, ez);
-            }
-            ++count;
-        }
-    };
-
-    for (;;) {
-        // -------- scan: round-robin over the neighbour cells, 4 candidates each
-        bool left = false;
-        for (int k = 0; k < nnb; ++k) {
-            const int b = cb[wib][k], e = ce[wib][k];
-            if (b >= e) continue;
-            left = true;
-            const int take = min(4, e - b);
-            const float qx = pxf - csx[wib][k], qy = pyf - csy[wib][k];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (u < take) {
-                    const float4 f = a.srcf[b + u];
-                    float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
-                    if (WRAP_ALL) {
-                        if (wx) dx -= a.Lxf * rintf(dx * a.iLxf);
-                        if (wy) dy -= a.Lyf * rintf(dy * a.iLyf);
-                    }
-                    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                    if (r2 <= r2f) {
-                        if (r2 > a.r2close) lf[wib][qn++][lane] = b + u;
-                        else lc[wib][qc++][lane] = b + u;
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) cb[wib][k] = b + take;
-            __syncwarp();
-            if (__any_sync(0xffffffffu, qn > NQ - 4 || qc > NQC - 4)) break;
-        }
-        // -------- drain: every lane evaluates its own queued pairs
-        const bool fin = !__any_sync(0xffffffffu, left);
-        if (fin || __any_sync(0xffffffffu, qn > NQ - 4)) {
-            const int mx = __reduce_max_sync(0xffffffffu, qn);
-#pragma unroll 1
-            for (int e = 0; e < mx; e += 2) {
-                if (e < qn) one(lf[wib][e][lane], std::true_type{});
-                if (e + 1 < qn) one(lf[wib][e + 1][lane], std::true_type{});
-            }
-            qn = 0;
-        }
-        if (fin || __any_sync(0xffffffffu, qc > NQC - 4)) {
-            const int mx = __reduce_max_sync(0xffffffffu, qc);
-#pragma unroll 1
-            for (int e = 0; e < mx; ++e)
-                if (e < qc) one(lc[wib][e][lane], std::false_type{});
-            qc = 0;
-        }
-        if (fin) break;
-    }
+    int count = 0;
+    int64_t i = 0;
     if (live) {
+        i = a.order[slot];
+        const double px = a.eval[3 * i], py = a.eval[3 * i + 1], pz = a.eval[3 * i + 2];
+        eval_list<true>(a, tab, a.list_far + slot * a.cap_far, a.cnt_far[slot], px, py, pz,
+                        phi, ex, ey, ez, count);
+        eval_list<false>(a, tab, a.list_close + slot * a.cap_close, a.cnt_close[slot], px, py,
+                         pz, phi, ex, ey, ez, count);
         a.out[i] = phi;
-        if (nd) {
+        if (a.need_field) {
             a.out[a.out_stride + i] = ex;
             a.out[2 * a.out_stride + i] = ey;
             a.out[3 * a.out_stride + i] = ez;
@@ -678,11 +743,46 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     a.ntask_dev = ns.toff + ncell;
     a.ntask = tcap;
     const unsigned nblk = (unsigned)((tcap * 32 + NB_THREADS - 1) / NB_THREADS);
-    if (d_npairs) p->ktic(3);
-    if (p->cl.ncx >= 3 && p->cl.ncy >= 3)
-        near_kernel<false><<<nblk, NB_THREADS, 0, p->stream>>>(a);
-    else
-        near_kernel<true><<<nblk, NB_THREADS, 0, p->stream>>>(a);   // a dimension of <= 2 cells
+    // pair-list capacities from the expected neighbour count (+ margin);
+    // an overflow doubles them and reruns the scan
+    const double vol_cell = p->cl.csx * p->cl.csy * p->cl.csz;
+    const double dens = (double)p->cl.n / ((double)ncell * vol_cell);
+    const double ball = 4.0 / 3.0 * M_PI * std::pow(k.radius, 3.0);
+    const double rclose = std::sqrt((double)a.r2close);
+    const double ballc = 4.0 / 3.0 * M_PI * std::pow(std::min(rclose, k.radius), 3.0);
+    NearLists& L = p->nl;
+    int64_t want_far = (int64_t)(1.6 * dens * ball + 64), want_close = (int64_t)(2.0 * dens * ballc + 64);
+    want_far = (want_far + 15) & ~15LL;
+    want_close = (want_close + 15) & ~15LL;
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        if (ne * want_far > L.cap_far_total || ne * want_close > L.cap_close_total || ne > L.ncap) {
+            void* olds[] = {L.far, L.close, L.cfar, L.cclose, L.ovf};
+            for (void* o : olds) dfree(p, o);
+            L.cap_far_total = std::max<int64_t>(ne * want_far, L.cap_far_total);
+            L.cap_close_total = std::max<int64_t>(ne * want_close, L.cap_close_total);
+            L.ncap = std::max<int64_t>(ne, L.ncap);
+            L.far = dalloc<int>(p, L.cap_far_total);
+            L.close = dalloc<int>(p, L.cap_close_total);
+            L.cfar = dalloc<int>(p, L.ncap);
+            L.cclose = dalloc<int>(p, L.ncap);
+            L.ovf = dalloc<int>(p, 1);
+        }
+        a.list_far = L.far; a.list_close = L.close;
+        a.cap_far = want_far; a.cap_close = want_close;
+        a.cnt_far = L.cfar; a.cnt_close = L.cclose; a.overflow = L.ovf;
+        SE_CUDA(cudaMemsetAsync(L.ovf, 0, sizeof(int), p->stream));
+        if (d_npairs) p->ktic(3);
+        near_scan_kernel<<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        SE_LAUNCHED(p);
+        int ovf = 0;
+        SE_CUDA(cudaMemcpyAsync(&ovf, L.ovf, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+        SE_CUDA(cudaStreamSynchronize(p->stream));
+        if (!ovf) break;
+        if (attempt == 3) throw Error(SE_ERR_CUDA, "near-field pair list overflow");
+        want_far *= 2;
+        want_close *= 2;
+    }
+    near_eval_kernel<<<nblk, NB_THREADS, 0, p->stream>>>(a);
     if (d_npairs) p->ktoc(3);
     SE_LAUNCHED(p);
 }

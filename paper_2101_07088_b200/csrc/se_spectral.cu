@@ -151,21 +151,18 @@ struct BvpArgs {
 // Scratch columns (stride M): F = f_sc, A = y'' (ypp), B = Thomas d / x.
 __device__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
                            double2 ends[2], bool emit) {
-    const int n = a.Nz, N = n - 1;
-    const int64_t M = a.M, RS = 2 * M;           // ext row stride
+    const int n = a.Nz;
+    const int64_t M = a.M, RS = 2 * M;           // row stride of [Nz][2][M]
     const double2* raw = a.ext + g * M + m;
     double2* F = a.scrF + m;
     double2* A = a.scrA + m;
     double2* B = a.scrB + m;
     const double* q_lo = a.mp.q_lo; const double* q_dg = a.mp.q_dg; const double* q_hi = a.mp.q_hi;
     const double* e_lo = a.mp.e_lo; const double* e_hi = a.mp.e_hi;
-    // f_sc = -(Chebyshev coefficient of rho_hat) / eps * half^2, where the
-    // coefficient is (-1)^n FFT(ext)_n / (2N) * (2 if interior) / (Nx Ny)
-    const double base = -(a.half * a.half) / (a.eps * 2.0 * N) * a.inv_nxy;
-    auto fsc_at = [&](int k) -> double2 {
-        double s = base * (((k & 1) ? -1.0 : 1.0) * ((k > 0 && k < N) ? 2.0 : 1.0));
-        return cscale(raw[(int64_t)k * RS], s);
-    };
+    // f_sc = -(Chebyshev coefficient of rho_hat) / eps * half^2; the DCT-I
+    // GEMM produced the coefficients of the unnormalised xy spectrum
+    const double base = -(a.half * a.half) / a.eps * a.inv_nxy;
+    auto fsc_at = [&](int k) -> double2 { return cscale(raw[(int64_t)k * RS], base); };
     const int u = a.kidx[m];
     double2 c0v = make_double2(0, 0), c1v = make_double2(0, 0);
     if (u < 0) {
@@ -306,15 +303,9 @@ __device__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
         d_sum = cadd(d_sum, bs);
         d_sgn = (k & 1) ? csub(d_sgn, bs) : cadd(d_sgn, bs);
         if (a.keep) a.keep[((int64_t)k * 2 + g) * M + m] = y;
-        if (emit) {
-            double hw = (k > 0 && k < N) ? 0.5 : 1.0;
-            double2 xy = cscale(y, hw), xd = cscale(bs, hw);
-            out_y[(int64_t)k * RS] = xy;
-            out_d[(int64_t)k * RS] = xd;
-            if (k > 0 && k < N) {
-                out_y[(int64_t)(2 * N - k) * RS] = xy;
-                out_d[(int64_t)(2 * N - k) * RS] = xd;
-            }
+        if (emit) {                             // coefficients for the iDCT GEMM
+            out_y[(int64_t)k * RS] = y;
+            out_d[(int64_t)k * RS] = bs;
         }
         bp2 = bp1; bp1 = b; ynext = y;
         ap2 = ap1; ap1 = a0; a0 = am1; am1 = am2;
@@ -413,11 +404,10 @@ __global__ void assemble_kernel(AsmArgs a) {
     if (e >= (int64_t)a.Nz * a.M) return;
     int j = (int)(e / a.M);
     int64_t m = e % a.M;
-    const int N = a.Nz - 1;
     const int64_t RS = 2 * a.M;
-    // iDCT output row r holds the node cos(pi r / N), i.e. ascending index N - r
-    double2 v = a.ext[(int64_t)(N - j) * RS + m];
-    double2 d = a.ext[(int64_t)(N - j) * RS + a.M + m];
+    // iDCT GEMM output: row j = value at ascending Chebyshev node j
+    double2 v = a.ext[(int64_t)j * RS + m];
+    double2 d = a.ext[(int64_t)j * RS + a.M + m];
     if (a.corr && a.sel[m] && j >= a.w0 && j < a.w1) {
         double k = a.kmag[m], z = a.z[j];
         double e1 = exp(-k * z), e2 = exp(k * (z - a.H));
@@ -483,6 +473,28 @@ void factor_bvp(Plan* p) {
     colsums(sgn, &h[7 * n], &h[8 * n]);
     p->d_maps = dalloc<double>(p, h.size());
     SE_CUDA(cudaMemcpy(p->d_maps, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+    // DCT-I matrices (column-major), chebyshev.py:46-65 with the node flip:
+    //  a_n = w_n/(2N) sum_j g_j cos(pi n (N-j)/N) v_j,  g = 1 at the ends else 2,
+    //        w_n = 2 for interior n else 1
+    //  v_j = sum_n cos(pi n (N-j)/N) a_n
+    {
+        const int N = n - 1;
+        std::vector<double> F((size_t)n * n), I((size_t)n * n);
+        for (int r = 0; r < n; ++r)
+            for (int c = 0; c < n; ++c) {
+                const long long nm = (long long)r * (N - c) % (2 * N);
+                const double cs = std::cos(M_PI * (double)nm / N);
+                const double g = (c == 0 || c == N) ? 1.0 : 2.0;
+                const double w = (r == 0 || r == N) ? 1.0 : 2.0;
+                F[(size_t)r + (size_t)c * n] = w / (2.0 * N) * g * cs;      // a = F v
+                const long long nm2 = (long long)c * (N - r) % (2 * N);
+                I[(size_t)r + (size_t)c * n] = std::cos(M_PI * (double)nm2 / N);  // v = I a
+            }
+        p->d_dct_fwd = dalloc<double>(p, F.size());
+        p->d_dct_inv = dalloc<double>(p, I.size());
+        SE_CUDA(cudaMemcpy(p->d_dct_fwd, F.data(), F.size() * sizeof(double), cudaMemcpyHostToDevice));
+        SE_CUDA(cudaMemcpy(p->d_dct_inv, I.data(), I.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
     const int nu = std::max(p->n_uniq, 1);
     p->d_fac = dalloc<double>(p, (size_t)nu * FAC_ROWS * n);
     p->d_sinv = dalloc<double>(p, 4 * (size_t)nu);
@@ -501,18 +513,22 @@ void factor_bvp(Plan* p) {
     if (bad) throw Error(SE_ERR_LINALG, "ill-conditioned Schur block in the mode BVP factorisation");
 }
 
+// z transforms as one DGEMM over all modes of both grids (W = 4M doubles per
+// row): the DCT-I of length Nz = 258 is 2*257 in FFT terms (Bluestein in
+// cuFFT); as a 258 x 258 matrix it runs on the FP64 tensor pipe.
+static void z_gemm(Plan* p, const double* Dcol, const double* in, double* out) {
+    const int64_t W = 4 * p->M;
+    const double one = 1.0, zero = 0.0;
+    // row-major [Nz][W] == column-major (W x Nz): out^T = in^T * D^T
+    SE_CUBLAS(cublasDgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_T, (int)W, p->Nz, p->Nz, &one, in,
+                          (int)W, Dcol, p->Nz, &zero, out, (int)W));
+}
+
 void forward_transforms(Plan* p, bool two_grids) {
     (void)two_grids;
-    SE_CUFFT(cufftExecD2Z(p->fft_fwd2, p->d_rho, p->d_ext));
-    const int N = p->Nz - 1;
-    const int64_t row = 2 * p->M;
-    int64_t total = (int64_t)(N - 1) * row;
-    if (total > 0) {
-        mirror_kernel<<<(unsigned)((total + 255) / 256), 256, 0, p->stream>>>(
-            reinterpret_cast<double2*>(p->d_ext), N, row);
-        SE_LAUNCHED(p);
-    }
-    SE_CUFFT(cufftExecZ2Z(p->fft_z, p->d_ext, p->d_ext, CUFFT_FORWARD));
+    SE_CUFFT(cufftExecD2Z(p->fft_fwd2, p->d_rho, p->d_hat));
+    z_gemm(p, p->d_dct_fwd, reinterpret_cast<const double*>(p->d_hat),
+           reinterpret_cast<double*>(p->d_ext));
 }
 
 void bvp_solve(Plan* p, bool two_grids, int mode, bool correction) {
@@ -548,9 +564,10 @@ void bvp_solve(Plan* p, bool two_grids, int mode, bool correction) {
 }
 
 void inverse_transforms(Plan* p, bool forces, bool correction) {
-    SE_CUFFT(cufftExecZ2Z(p->fft_z, p->d_ext, p->d_ext, CUFFT_FORWARD));
+    z_gemm(p, p->d_dct_inv, reinterpret_cast<const double*>(p->d_ext),
+           reinterpret_cast<double*>(p->d_hat));
     AsmArgs a{};
-    a.ext = reinterpret_cast<const double2*>(p->d_ext);
+    a.ext = reinterpret_cast<const double2*>(p->d_hat);
     a.spec = reinterpret_cast<double2*>(p->d_spec);
     a.mom = reinterpret_cast<const double2*>(p->d_mom);
     a.kx = p->d_kx; a.ky = p->d_ky; a.kmag = p->d_kmag; a.sel = p->d_sel;
