@@ -361,7 +361,7 @@ int se_plan_create(const se_params* params, const double* z_nodes, const double*
         p->d_hat = dalloc<cufftDoubleComplex>(p, (size_t)nz * 2 * p->M);
         p->d_spec = dalloc<cufftDoubleComplex>(p, (size_t)nz * 4 * p->M);
         p->d_fields = dalloc<double>(p, 4 * (size_t)p->G);
-        p->d_scr = dalloc<cufftDoubleComplex>(p, 3 * (size_t)nz * p->M);
+        p->d_scr = dalloc<cufftDoubleComplex>(p, 6 * (size_t)nz * p->M);
         p->d_mom = dalloc<cufftDoubleComplex>(p, 2 * (size_t)p->M);
         p->d_mism = dalloc<cufftDoubleComplex>(p, 4 * (size_t)p->M);
         const char* keep = std::getenv("SE_KEEP_STAGES");

@@ -149,16 +149,20 @@ struct BvpArgs {
 // With emit, writes the iDCT inputs of y (slot 0) and y' (slot 1), i.e. the
 // coefficients with the interior halved, mirrored to rows 2N - k.
 // Scratch columns (stride M): F = f_sc, A = y'' (ypp), B = Thomas d / x.
-__device__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
-                           double2 ends[2], bool emit) {
+__device__ __forceinline__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
+                                           double2 ends[2], bool emit) {
     const int n = a.Nz;
     const int64_t M = a.M, RS = 2 * M;           // row stride of [Nz][2][M]
-    const double2* raw = a.ext + g * M + m;
-    double2* F = a.scrF + m;
-    double2* A = a.scrA + m;
-    double2* B = a.scrB + m;
-    const double* q_lo = a.mp.q_lo; const double* q_dg = a.mp.q_dg; const double* q_hi = a.mp.q_hi;
-    const double* e_lo = a.mp.e_lo; const double* e_hi = a.mp.e_hi;
+    const double2* __restrict__ raw = a.ext + g * M + m;
+    // scratch columns: [Nz][2][M], this grid's column (row stride 2M)
+    double2* __restrict__ F = a.scrF + g * M + m;
+    double2* __restrict__ A = a.scrA + g * M + m;
+    double2* __restrict__ B = a.scrB + g * M + m;
+    const double* __restrict__ q_lo = a.mp.q_lo;
+    const double* __restrict__ q_dg = a.mp.q_dg;
+    const double* __restrict__ q_hi = a.mp.q_hi;
+    const double* __restrict__ e_lo = a.mp.e_lo;
+    const double* __restrict__ e_hi = a.mp.e_hi;
     // f_sc = -(Chebyshev coefficient of rho_hat) / eps * half^2; the DCT-I
     // GEMM produced the coefficients of the unnormalised xy spectrum
     const double base = -(a.half * a.half) / a.eps * a.inv_nxy;
@@ -167,23 +171,23 @@ __device__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
     double2 c0v = make_double2(0, 0), c1v = make_double2(0, 0);
     if (u < 0) {
         // ---- k = 0: y'' = f, y(z0) = y(z1) = 0              bvp.py:281-296
-        for (int k = 0; k < n; ++k) A[(int64_t)k * M] = fsc_at(k);
+        for (int k = 0; k < n; ++k) A[(int64_t)k * RS] = fsc_at(k);
         double2 P = make_double2(0, 0), Qs = make_double2(0, 0);
         for (int k = 1; k < n; ++k) {
-            double2 y = cscale(A[(int64_t)k * M], q_dg[k]);
-            if (k >= 2) y = cadd(y, cscale(A[(int64_t)(k - 2) * M], q_lo[k]));
-            if (k + 2 < n) y = cadd(y, cscale(A[(int64_t)(k + 2) * M], q_hi[k]));
+            double2 y = cscale(A[(int64_t)k * RS], q_dg[k]);
+            if (k >= 2) y = cadd(y, cscale(A[(int64_t)(k - 2) * RS], q_lo[k]));
+            if (k + 2 < n) y = cadd(y, cscale(A[(int64_t)(k + 2) * RS], q_hi[k]));
             P = cadd(P, y);
             Qs = (k & 1) ? csub(Qs, y) : cadd(Qs, y);
         }
         c0v = cscale(cadd(P, Qs), -0.5);
         c1v = cscale(csub(Qs, P), 0.5);
     } else {
-        const double* cp = a.fac + ((int64_t)u * FAC_ROWS + FAC_CP) * n;
-        const double* iv = a.fac + ((int64_t)u * FAC_ROWS + FAC_INV) * n;
-        const double* aib = a.fac + ((int64_t)u * FAC_ROWS + FAC_AINVB) * n;
-        const double* cr0 = a.fac + ((int64_t)u * FAC_ROWS + FAC_C0) * n;
-        const double* cr1 = a.fac + ((int64_t)u * FAC_ROWS + FAC_C1) * n;
+        const double* __restrict__ cp = a.fac + ((int64_t)u * FAC_ROWS + FAC_CP) * n;
+        const double* __restrict__ iv = a.fac + ((int64_t)u * FAC_ROWS + FAC_INV) * n;
+        const double* __restrict__ aib = a.fac + ((int64_t)u * FAC_ROWS + FAC_AINVB) * n;
+        const double* __restrict__ cr0 = a.fac + ((int64_t)u * FAC_ROWS + FAC_C0) * n;
+        const double* __restrict__ cr1 = a.fac + ((int64_t)u * FAC_ROWS + FAC_C1) * n;
         const double kap = a.kappa[u], k2 = kap * kap;
         const double S00 = a.sinv[4 * u], S01 = a.sinv[4 * u + 1];
         const double S10 = a.sinv[4 * u + 2], S11 = a.sinv[4 * u + 3];
@@ -193,10 +197,11 @@ __device__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
         auto descend = [&](double2& s0, double2& s1) {
             double2 xp1 = make_double2(0, 0), xp2 = make_double2(0, 0);
             s0 = make_double2(0, 0); s1 = make_double2(0, 0);
+#pragma unroll 8
             for (int k = n - 1; k >= 0; --k) {
-                double2 d = B[(int64_t)k * M];
+                double2 d = B[(int64_t)k * RS];
                 double2 x = (k + 2 < n) ? cfma(-cp[k], xp2, d) : d;
-                B[(int64_t)k * M] = x;
+                B[(int64_t)k * RS] = x;
                 s0 = cfma(cr0[k], x, s0);
                 s1 = cfma(cr1[k], x, s1);
                 xp2 = xp1; xp1 = x;
@@ -204,12 +209,13 @@ __device__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
         };
         {
             double2 dm1 = make_double2(0, 0), dm2 = make_double2(0, 0);
+#pragma unroll 8
             for (int k = 0; k < n; ++k) {
                 double2 r = fsc_at(k);
-                F[(int64_t)k * M] = r;
+                F[(int64_t)k * RS] = r;
                 double2 d = (k < 2) ? cscale(r, iv[k])
                                     : cscale(cfma(k2 * q_lo[k], dm2, r), iv[k]);
-                B[(int64_t)k * M] = d;
+                B[(int64_t)k * RS] = d;
                 dm2 = dm1; dm1 = d;
             }
         }
@@ -217,18 +223,20 @@ __device__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
         descend(s0, s1);                       // rhs2 = bc = 0
         c0v = make_double2(S00 * s0.x + S01 * s1.x, S00 * s0.y + S01 * s1.y);
         c1v = make_double2(S10 * s0.x + S11 * s1.x, S10 * s0.y + S11 * s1.y);
+#pragma unroll 8
         for (int k = 0; k < n; ++k)
-            A[(int64_t)k * M] = cfma(-aib[k], (k & 1) ? c1v : c0v, B[(int64_t)k * M]);
+            A[(int64_t)k * RS] = cfma(-aib[k], (k & 1) ? c1v : c0v, B[(int64_t)k * RS]);
 
         for (int it = 0; it < a.refine; ++it) {     // bvp.py:229-246,268-273
             double2 yq_sum = make_double2(0, 0), yq_sgn = make_double2(0, 0);
             double2 ye_sum = make_double2(0, 0), ye_sgn = make_double2(0, 0);
             double2 ym2 = make_double2(0, 0), ym1 = make_double2(0, 0);
             double2 y0 = A[0];
-            double2 yp1 = (n > 1) ? A[M] : make_double2(0, 0);
+            double2 yp1 = (n > 1) ? A[RS] : make_double2(0, 0);
             double2 dm1 = make_double2(0, 0), dm2 = make_double2(0, 0);
+#pragma unroll 8
             for (int k = 0; k < n; ++k) {
-                double2 yp2 = (k + 2 < n) ? A[(int64_t)(k + 2) * M] : make_double2(0, 0);
+                double2 yp2 = (k + 2 < n) ? A[(int64_t)(k + 2) * RS] : make_double2(0, 0);
                 double2 yq = make_double2(0, 0), ye = make_double2(0, 0);
                 if (k > 0) {
                     yq = cscale(y0, q_dg[k]);
@@ -237,7 +245,7 @@ __device__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
                     ye = cscale(ym1, e_lo[k]);
                     if (k + 1 < n) ye = cadd(ye, cscale(yp1, e_hi[k]));
                 }
-                double2 r = csub(F[(int64_t)k * M], csub(y0, cscale(yq, k2)));
+                double2 r = csub(F[(int64_t)k * RS], csub(y0, cscale(yq, k2)));
                 if (k == 0) r = cadd(r, cscale(c0v, k2));
                 if (k == 1) r = cadd(r, cscale(c1v, k2));
                 yq_sum = cadd(yq_sum, yq); ye_sum = cadd(ye_sum, ye);
@@ -245,7 +253,7 @@ __device__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
                 else { yq_sgn = cadd(yq_sgn, yq); ye_sgn = cadd(ye_sgn, ye); }
                 double2 d = (k < 2) ? cscale(r, iv[k])
                                     : cscale(cfma(k2 * q_lo[k], dm2, r), iv[k]);
-                B[(int64_t)k * M] = d;
+                B[(int64_t)k * RS] = d;
                 dm2 = dm1; dm1 = d;
                 ym2 = ym1; ym1 = y0; y0 = yp1; yp1 = yp2;
             }
@@ -259,9 +267,10 @@ __device__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
             t0 = csub(t0, r20); t1 = csub(t1, r21);
             double2 dc0 = make_double2(S00 * t0.x + S01 * t1.x, S00 * t0.y + S01 * t1.y);
             double2 dc1 = make_double2(S10 * t0.x + S11 * t1.x, S10 * t0.y + S11 * t1.y);
+#pragma unroll 8
             for (int k = 0; k < n; ++k) {
-                double2 dy = cfma(-aib[k], (k & 1) ? dc1 : dc0, B[(int64_t)k * M]);
-                A[(int64_t)k * M] = cadd(A[(int64_t)k * M], dy);
+                double2 dy = cfma(-aib[k], (k & 1) ? dc1 : dc0, B[(int64_t)k * RS]);
+                A[(int64_t)k * RS] = cadd(A[(int64_t)k * RS], dy);
             }
             c0v = cadd(c0v, dc0);
             c1v = cadd(c1v, dc1);
@@ -279,10 +288,11 @@ __device__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
     double2* out_d = a.ext + 1 * M + m;
     // sliding window of ypp: a_{k-2}, a_k, a_{k+2}
     double2 ap2 = make_double2(0, 0), ap1 = make_double2(0, 0);
-    double2 a0 = A[(int64_t)(n - 1) * M];
-    double2 am1 = (n >= 2) ? A[(int64_t)(n - 2) * M] : make_double2(0, 0);
+    double2 a0 = A[(int64_t)(n - 1) * RS];
+    double2 am1 = (n >= 2) ? A[(int64_t)(n - 2) * RS] : make_double2(0, 0);
+#pragma unroll 8
     for (int k = n - 1; k >= 0; --k) {
-        double2 am2 = (k >= 2) ? A[(int64_t)(k - 2) * M] : make_double2(0, 0);
+        double2 am2 = (k >= 2) ? A[(int64_t)(k - 2) * RS] : make_double2(0, 0);
         double2 y = make_double2(0, 0);
         if (k > 0) {
             y = cscale(a0, q_dg[k]);
@@ -316,15 +326,31 @@ __device__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
 
 __device__ __forceinline__ bool finite2(double2 v) { return isfinite(v.x) && isfinite(v.y); }
 
-__global__ void bvp_kernel(BvpArgs a) {
-    int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (m >= a.M) return;
-    double2 wo[4], wi[4], eo[2], ei[2];
-    // the in-slab grid's raw data lives in slot 1, the over grid in slot 0;
-    // the over grid is solved first so its slot can be reused for output
-    if (a.two) solve_mode(a, m, 0, wo, eo, false);
-    solve_mode(a, m, 1, wi, ei, true);
-
+__global__ void __launch_bounds__(64) bvp_kernel(BvpArgs a) {
+    // lane pair (2m, 2m+1) = (over grid, in-slab grid) of mode m
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int g = (int)(tid & 1);
+    const int64_t mm = tid >> 1;
+    const bool valid = mm < a.M;
+    const int64_t m = valid ? mm : a.M - 1;
+    double2 w[4], e[2];
+    for (int q = 0; q < 4; ++q) w[q] = make_double2(0, 0);
+    e[0] = e[1] = make_double2(0, 0);
+    if (valid && (a.two || g == 1)) solve_mode(a, m, g, w, e, g == 1);
+    double2 wo[4], eo[2], wi[4], ei[2];
+    for (int q = 0; q < 4; ++q) {
+        double2 o;
+        o.x = __shfl_xor_sync(0xffffffffu, w[q].x, 1);
+        o.y = __shfl_xor_sync(0xffffffffu, w[q].y, 1);
+        wo[q] = o; wi[q] = w[q];
+    }
+    for (int q = 0; q < 2; ++q) {
+        double2 o;
+        o.x = __shfl_xor_sync(0xffffffffu, e[q].x, 1);
+        o.y = __shfl_xor_sync(0xffffffffu, e[q].y, 1);
+        eo[q] = o; ei[q] = e[q];
+    }
+    if (!valid || g == 0) return;
     double2 sb = a.sbh[m], st = a.sth[m];
     double2 phib, eb, phit, et;
     if (a.mode == 0) {                                   // slab.py:306-316
@@ -549,8 +575,8 @@ void bvp_solve(Plan* p, bool two_grids, int mode, bool correction) {
     a.sth = reinterpret_cast<const double2*>(p->d_sth);
     a.ext = reinterpret_cast<double2*>(p->d_ext);
     a.scrF = reinterpret_cast<double2*>(p->d_scr);
-    a.scrA = a.scrF + (int64_t)p->Nz * p->M;
-    a.scrB = a.scrA + (int64_t)p->Nz * p->M;
+    a.scrA = a.scrF + (int64_t)p->Nz * 2 * p->M;
+    a.scrB = a.scrA + (int64_t)p->Nz * 2 * p->M;
     a.inv_nxy = 1.0 / (double)p->NXY;
     a.mom = reinterpret_cast<double2*>(p->d_mom);
     a.mism = reinterpret_cast<double2*>(p->d_mism);
@@ -558,7 +584,7 @@ void bvp_solve(Plan* p, bool two_grids, int mode, bool correction) {
     a.k0out = p->d_k0; a.scal = p->d_scal; a.flags = p->d_flags;
     a.rb = p->P.eps_b / p->P.eps; a.rt = p->P.eps_t / p->P.eps; a.H = p->P.H;
     p->ktic(1);
-    bvp_kernel<<<(unsigned)((p->M + 127) / 128), 128, 0, p->stream>>>(a);
+    bvp_kernel<<<(unsigned)((2 * p->M + 63) / 64), 64, 0, p->stream>>>(a);
     p->ktoc(1);
     SE_LAUNCHED(p);
 }
