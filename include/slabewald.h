@@ -107,6 +107,22 @@ int se_solve_device(se_plan* plan, const double* d_pos, int64_t n,
                     uint32_t flags, double* d_phi_bar, double* d_E_bar,
                     double* U, se_diag* diag);
 
+/* Sharded solve (one rank per GPU, charges split by index): the same solve
+ * in three phases.  Phase 1 spreads the charges first..first+count-1 (and
+ * their images) into the plan's grids and returns the grid buffer
+ * (device, rho_len doubles) for the caller to SUM over ranks in place
+ * (e.g. an NCCL all-reduce on the plan's stream).  Phase 2 runs the grid
+ * pipeline on the summed grids.  Phase 3 interpolates and evaluates the near
+ * field (sources: all n_all charges) for this rank's charges, writes
+ * d_phi[count], d_E[count][3] (device) and this rank's part of U (the
+ * ranks' parts sum to U). */
+int se_shard_spread(se_plan* plan, const double* d_pos_all, int64_t n_all,
+                    int64_t first, int64_t count, uint32_t flags,
+                    double** d_rho, int64_t* rho_len);
+int se_shard_fields(se_plan* plan);
+int se_shard_charges(se_plan* plan, const double* d_pos_all, double* d_phi,
+                     double* d_E, double* U_part, se_diag* diag);
+
 /* near_field_sum (slab.py:184-191): sources = pos[n] with charges q[n]
  * (plus the mirrored layers of the geometry in params), evaluated at
  * eval_pos[ne].  kind 0 = "avg" (r_cut), 1 = "point" (r_nf).  Host buffers.

@@ -712,18 +712,21 @@ class OracleSlabSolver:
         return self.grid.interpolate(field, pts, w, rad, rad)
 
     # -- solve ---------------------------------------------------------
-    def solve(self, positions=None, need_energy=True, need_forces=True,
-              need_potential=True, subtract_self=False,
-              include_correction=True, force_general=False, capture=None):
-        geo, par = self.system.geometry, self.params
-        pos = self.system.positions if positions is None else \
-            np.atleast_2d(np.asarray(positions, dtype=float))
-        q = self.system.charges
-        cap = capture if capture is not None else {}
+    # The solve is written as three phases so a sharded host (charges split
+    # by index across ranks, grids summed between phases 1 and 2) can drive
+    # it; ``solve`` runs them back to back (reference slab.py:259-394).
+    def _two_grids(self, include_correction, force_general):
+        geo = self.system.geometry
         jumps = geo.eps_b != geo.eps or geo.eps_t != geo.eps or force_general
-        nz = par.Nz
+        return include_correction and jumps
 
-        if include_correction and jumps:
+    def spread_phase(self, pos, q, include_correction=True,
+                     force_general=False, cap=None):
+        """Grids of the charges ``pos, q`` (slab.py:280-297): stacked
+        (rho_over, rho_in) with jumps + correction, else (rho,)."""
+        geo, par = self.system.geometry, self.params
+        cap = cap if cap is not None else {}
+        if self._two_grids(include_correction, force_general):
             part = partition(pos, q, geo, par)
             cap["partition"] = part
             rho_o = self._spread(pos[part["over"]], q[part["over"]])
@@ -731,20 +734,31 @@ class OracleSlabSolver:
             xq = np.concatenate([q[part["far"]], part["image_strengths"]])
             rho_i = rho_o + self._spread(xp, xq)
             cap["rho_over"], cap["rho_in"] = rho_o, rho_i
-            both = self.modes.solve(np.stack([self._forward(rho_o),
-                                              self._forward(rho_i)]),
+            return np.stack([rho_o, rho_i])
+        rho = self._spread(pos, q)
+        cap["rho_in"] = rho
+        return rho[None]
+
+    def field_phase(self, rho, need_forces=True, include_correction=True,
+                    force_general=False, cap=None):
+        """Mode solves, correction, k = 0 and the field grids from the
+        (summed) grids (slab.py:298-352)."""
+        geo, par = self.system.geometry, self.params
+        cap = cap if cap is not None else {}
+        two = self._two_grids(include_correction, force_general)
+        if two:
+            both = self.modes.solve(np.stack([self._forward(rho[0]),
+                                              self._forward(rho[1])]),
                                     self.refine)
             psi_o, psi_i = both[0], both[1]
         else:
-            rho = self._spread(pos, q)
-            cap["rho_in"] = rho
             psi_o = None
-            psi_i = self.modes.solve(self._forward(rho), self.refine)
+            psi_i = self.modes.solve(self._forward(rho[0]), self.refine)
         cap["psi_i"], cap["psi_o"] = psi_i, psi_o
         dpsi_i = cheb_deriv(psi_i, par.z0, par.z1)
 
         T0, TH = self.t_wall[0.0], self.t_wall[geo.H]
-        if include_correction and jumps:
+        if two:
             dpsi_o = cheb_deriv(psi_o, par.z0, par.z1)
             cb, ct = geo.exterior_factor_bottom(), geo.exterior_factor_top()
             mism = {
@@ -785,21 +799,37 @@ class OracleSlabSolver:
             fields.append(-(self._to_grid(dz) + k0["A_i"]))
         stack = np.stack(fields)
         cap["fields"] = stack
+        return {"k0": k0, "psi_vals": psi_vals, "fields": stack}
 
-        far = self.grid.interpolate(stack, pos, par.g_t, par.H_E, par.H_E)
+    def charge_phase(self, state, pos, q, first=0, count=None,
+                     need_energy=True, need_forces=True, need_potential=True,
+                     subtract_self=False, cap=None):
+        """Interpolation, near field, gauge and energy at the charges
+        ``first .. first+count-1`` with every charge as a near-field source
+        (slab.py:354-391).  Returns (phi, E, U_part, diag); the parts of U
+        over a partition of the charges sum to U (the wall-charge energy is
+        added by the part holding charge 0)."""
+        geo, par = self.system.geometry, self.params
+        cap = cap if cap is not None else {}
+        n = pos.shape[0]
+        count = n - first if count is None else count
+        own = slice(first, first + count)
+        k0, psi_vals, stack = state["k0"], state["psi_vals"], state["fields"]
+        pe, qe = pos[own], q[own]
+        far = self.grid.interpolate(stack, pe, par.g_t, par.H_E, par.H_E)
         nf = NearSources(pos, q, geo, par)
         if need_forces:
-            phi_near, e_near = nf.evaluate(pos, "avg",
+            phi_near, e_near = nf.evaluate(pe, "avg",
                                            subtract_unsplit=subtract_self)
             e_bar = far[1:4].T + e_near
         else:
-            phi_near = nf.evaluate(pos, "avg", need_field=False,
+            phi_near = nf.evaluate(pe, "avg", need_field=False,
                                    subtract_unsplit=subtract_self)
             e_near = None
-            e_bar = np.zeros((pos.shape[0], 3))
+            e_bar = np.zeros((pe.shape[0], 3))
         cap["phi_far"], cap["phi_near"], cap["e_near"] = far[0], phi_near, e_near
         if subtract_self and np.isinf(par.xi):
-            phi_near = phi_near + q * self_avg(par.g_w, np.inf, geo.eps, True)
+            phi_near = phi_near + qe * self_avg(par.g_w, np.inf, geo.eps, True)
         phi_bar = far[0] + phi_near
 
         b_i = 0.0
@@ -812,13 +842,27 @@ class OracleSlabSolver:
 
         U = 0.0
         if need_energy:
-            U = 0.5 * float(np.dot(q, phi_bar))
-            if not self.system.surface.is_zero:
+            U = 0.5 * float(np.dot(qe, phi_bar))
+            if not self.system.surface.is_zero and first == 0:
                 U += self._wall_energy(nf, psi_vals, b_i)
         diag = {"charges": q, "ai1": k0["ai1"], "ai2": k0["ai2"],
                 "ai_discrepancy": k0["discrepancy"], "B_i": b_i, "k0": k0,
                 "constraints": par.constraints}
         return phi_bar, e_bar, U, diag
+
+    def solve(self, positions=None, need_energy=True, need_forces=True,
+              need_potential=True, subtract_self=False,
+              include_correction=True, force_general=False, capture=None):
+        pos = self.system.positions if positions is None else \
+            np.atleast_2d(np.asarray(positions, dtype=float))
+        q = self.system.charges
+        cap = capture if capture is not None else {}
+        rho = self.spread_phase(pos, q, include_correction, force_general, cap)
+        state = self.field_phase(rho, need_forces, include_correction,
+                                 force_general, cap)
+        return self.charge_phase(state, pos, q, 0, pos.shape[0], need_energy,
+                                 need_forces, need_potential, subtract_self,
+                                 cap)
 
     def _wall_energy(self, nf, psi_vals, b_i):
         geo = self.system.geometry

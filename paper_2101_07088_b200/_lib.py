@@ -29,7 +29,8 @@ TIMINGS = 1 << 6
 EXPORTS = ("se_plan_create", "se_plan_destroy", "se_plan_set_stream",
            "se_set_charges", "se_solve",
            "se_solve_device", "se_near_field", "se_build_partition",
-           "se_debug_fetch", "se_fp64_peak", "se_last_error", "se_version")
+           "se_debug_fetch", "se_fp64_peak", "se_last_error", "se_version",
+           "se_shard_spread", "se_shard_fields", "se_shard_charges")
 
 
 class SeParams(ctypes.Structure):
@@ -96,6 +97,15 @@ def load():
     lib.se_build_partition.restype = ctypes.c_int
     lib.se_debug_fetch.argtypes = [_P, ctypes.c_int, ctypes.c_void_p, _I64]
     lib.se_debug_fetch.restype = ctypes.c_int64
+    lib.se_shard_spread.argtypes = [_P, ctypes.c_void_p, _I64, _I64, _I64,
+                                    ctypes.c_uint32,
+                                    ctypes.POINTER(ctypes.c_void_p), _I64P]
+    lib.se_shard_spread.restype = ctypes.c_int
+    lib.se_shard_fields.argtypes = [_P]
+    lib.se_shard_fields.restype = ctypes.c_int
+    lib.se_shard_charges.argtypes = [_P, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_void_p, _D, ctypes.POINTER(SeDiag)]
+    lib.se_shard_charges.restype = ctypes.c_int
     lib.se_fp64_peak.argtypes = [ctypes.c_int, _D]
     lib.se_fp64_peak.restype = ctypes.c_int
     lib.se_last_error.argtypes = []

@@ -68,104 +68,140 @@ void make_plan2d(cufftHandle* h, int nx, int ny, int nyh, cufftType type,
     SE_CUFFT(cufftSetStream(*h, s));
 }
 
-void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
-                double* d_phi_out, double* d_E_out, double* U, se_diag* diag) {
+// ---------------------------------------------------------------------------
+// the solve in three phases; the single-GPU solve runs them back to back and a
+// sharded solve (charges split by index across ranks) runs them with a sum of
+// the spread grids over ranks between phase 1 and phase 2.
+// ---------------------------------------------------------------------------
+static void mark(Plan* p, Solve& S) {
+    if (S.timed) SE_CUDA(cudaEventRecord(S.ev[S.ne++], p->stream));
+}
+
+static Solve& current(Plan* p) { return p->solve; }
+
+void phase_spread(Plan* p, const double* d_pos, int64_t n_all, int64_t first, int64_t count,
+                  uint32_t flags) {
     p->launches = 0;
-    if (n != p->N)
+    if (n_all != p->N)
         throw Error(SE_ERR_VALUE, "positions and charges disagree on N");
+    if (first < 0 || count < 0 || first + count > n_all)
+        throw Error(SE_ERR_VALUE, "shard range outside the charge set");
     const se_params& P = p->P;
-    const bool xi_inf = P.xi_is_inf != 0.0;
-    const bool forces = flags & SE_NEED_FORCES;
-    const bool potential = flags & SE_NEED_POTENTIAL;
-    const bool energy = flags & SE_NEED_ENERGY;
-    const bool corr = flags & SE_CORRECTION;
+    Solve& S = current(p);
+    S.phase = 0;
+    S.flags = flags;
+    S.n_all = n_all; S.first = first; S.count = count;
+    S.xi_inf = P.xi_is_inf != 0.0;
+    S.forces = flags & SE_NEED_FORCES;
+    S.potential = flags & SE_NEED_POTENTIAL;
+    S.energy = flags & SE_NEED_ENERGY;
+    S.corr = flags & SE_CORRECTION;
     const bool jumps = P.eps_b != P.eps || P.eps_t != P.eps || (flags & SE_FORCE_GENERAL);
-    const bool two = corr && jumps;
-    const int mode = two ? 0 : (corr ? 1 : 2);
-    const bool near_empty = (n == 0) || xi_inf;
-    if (!near_empty && P.r_cut >= 0.5 * std::min(P.Lx, P.Ly))
+    S.two = S.corr && jumps;
+    S.mode = S.two ? 0 : (S.corr ? 1 : 2);
+    S.near_empty = (n_all == 0) || S.xi_inf;
+    if (!S.near_empty && P.r_cut >= 0.5 * std::min(P.Lx, P.Ly))
         throw Error(SE_ERR_VALUE, "near-field cutoff exceeds half the periodic box");
     cudaStream_t s = p->stream;
     SE_CUDA(cudaMemsetAsync(p->d_flags, 0, sizeof(int), s));
     SE_CUDA(cudaMemsetAsync(p->d_scal, 0, 8 * sizeof(double), s));
     SE_CUDA(cudaMemsetAsync(p->d_count, 0, sizeof(int64_t), s));
-
-    cudaEvent_t ev[12];
-    const bool timed = flags & SE_TIMINGS;
-    if (timed) for (auto& e : ev) SE_CUDA(cudaEventCreate(&e));
-    p->timing = timed;
-    if (timed && !p->kev[0][0])
+    S.timed = flags & SE_TIMINGS;
+    S.ne = 0;
+    if (S.timed) for (auto& e : S.ev) SE_CUDA(cudaEventCreate(&e));
+    p->timing = S.timed;
+    if (S.timed && !p->kev[0][0])
         for (auto& pr : p->kev) { SE_CUDA(cudaEventCreate(&pr[0])); SE_CUDA(cudaEventCreate(&pr[1])); }
-    int ne = 0;
-    auto mark = [&]() { if (timed) SE_CUDA(cudaEventRecord(ev[ne++], s)); };
-
-    mark();
+    mark(p, S);
     p->d_pos_cur = d_pos;
-    // ---- far field: spread, transforms, mode BVPs, correction, inverse
-    build_sources(p, d_pos, n, two);
-    mark();
-    spread(p, two);
-    mark();
-    forward_transforms(p, two);
-    mark();
-    bvp_solve(p, two, mode, corr);
-    mark();
-    inverse_transforms(p, forces, corr);
-    mark();
-    interp_charges(p, n, forces);
-    mark();
-    // ---- near field
+    build_sources(p, d_pos, first, count, S.two);
+    mark(p, S);
+    spread(p, S.two);
+    mark(p, S);
+    S.phase = 1;
+}
+
+void phase_fields(Plan* p) {
+    Solve& S = current(p);
+    if (S.phase != 1) throw Error(SE_ERR_CUDA, "se_shard_fields before se_shard_spread");
+    forward_transforms(p, S.two);
+    mark(p, S);
+    bvp_solve(p, S.two, S.mode, S.corr);
+    mark(p, S);
+    inverse_transforms(p, S.forces, S.corr);
+    mark(p, S);
+    S.phase = 2;
+}
+
+static NearKernel kernel_of(const se_params& P, int kind, bool field, bool sub_unsplit) {
     const double eps = P.eps, inv4pie = 1.0 / (4.0 * M_PI * eps);
     const double two_sqrtpi = 2.0 / std::sqrt(M_PI);
+    NearKernel k{};
+    k.inv4pie = inv4pie;
+    k.kind = kind;
+    k.need_field = field ? 1 : 0;
+    if (kind == 0) {                                        // kernels.py:90-125
+        k.c1 = 2.0 * P.g_w;
+        k.c2 = std::sqrt(4.0 * P.g_w * P.g_w + 1.0 / (P.xi * P.xi));
+        k.radius = P.r_cut;
+        k.self_value = sub_unsplit ? -two_sqrtpi / k.c2 / (4.0 * M_PI * eps)
+                                   : two_sqrtpi * (0.5 / P.g_w - 1.0 / k.c2) / (4.0 * M_PI * eps);
+    } else {                                                // kernels.py:83-87
+        k.c1 = std::sqrt(2.0) * P.g_w;
+        k.c2 = std::sqrt(2.0 * P.g_w * P.g_w + 1.0 / (P.xi * P.xi));
+        k.radius = P.r_nf;
+        k.point0 = (two_sqrtpi / k.c1 - two_sqrtpi / k.c2) / (4.0 * M_PI * eps);
+    }
+    return k;
+}
+
+void phase_charges(Plan* p, const double* d_pos, double* d_phi_out, double* d_E_out) {
+    Solve& S = current(p);
+    if (S.phase != 2) throw Error(SE_ERR_CUDA, "se_shard_charges before se_shard_fields");
+    if (d_pos != p->d_pos_cur) throw Error(SE_ERR_VALUE, "positions changed between phases");
+    S.phase = 0;
+    const se_params& P = p->P;
+    cudaStream_t s = p->stream;
+    const int64_t n = S.n_all, first = S.first, count = S.count;
+    interp_charges(p, n, first, count, S.forces);
+    mark(p, S);
     NearKernel kavg{}, kpt{};
-    if (!xi_inf) {
-        kavg.c1 = 2.0 * P.g_w;
-        kavg.c2 = std::sqrt(4.0 * P.g_w * P.g_w + 1.0 / (P.xi * P.xi));
-        kavg.inv4pie = inv4pie;
-        kavg.radius = P.r_cut;
-        kavg.self_value = (flags & SE_SUBTRACT_SELF)
-                              ? -two_sqrtpi / kavg.c2 / (4.0 * M_PI * eps)
-                              : two_sqrtpi * (0.5 / P.g_w - 1.0 / kavg.c2) / (4.0 * M_PI * eps);
-        kavg.kind = 0;
-        kavg.need_field = forces ? 1 : 0;
-        kpt.c1 = std::sqrt(2.0) * P.g_w;
-        kpt.c2 = std::sqrt(2.0 * P.g_w * P.g_w + 1.0 / (P.xi * P.xi));
-        kpt.inv4pie = inv4pie;
-        kpt.radius = P.r_nf;
-        kpt.point0 = (two_sqrtpi / kpt.c1 - two_sqrtpi / kpt.c2) / (4.0 * M_PI * eps);
-        kpt.kind = 1;
-        kpt.need_field = 0;
+    if (!S.xi_inf) {
+        kavg = kernel_of(P, 0, S.forces, S.flags & SE_SUBTRACT_SELF);
+        kpt = kernel_of(P, 1, false, false);
     }
-    if (!near_empty) {
-        build_cells(p, d_pos, p->d_q, n);
-        near_eval(p, d_pos, nullptr, n, kavg, p->d_near, p->d_count);
+    if (!S.near_empty) {
+        build_cells(p, d_pos, p->d_q, n);                 // sources: every charge
+        near_eval(p, d_pos + 3 * first, nullptr, count, kavg, p->d_near, p->d_count);
     } else {
-        SE_CUDA(cudaMemsetAsync(p->d_near, 0, sizeof(double) * 4 * (size_t)std::max<int64_t>(n, 1), s));
+        SE_CUDA(cudaMemsetAsync(p->d_near, 0, sizeof(double) * 4 * (size_t)std::max<int64_t>(count, 1), s));
     }
-    mark();
-    // ---- gauge: pointwise potential vanishes at the origin
-    if (potential && !xi_inf) {
+    mark(p, S);
+    // gauge: pointwise potential vanishes at the origin      slab.py:377-384
+    if (S.potential && !S.xi_inf) {
         const double w = 0.5 / P.xi;
         const double rad = (P.H_E / P.g_t) * w;
         interp_points(p, p->d_origin, 1, w, rad, p->d_scal + 4);
-        if (!near_empty) near_eval(p, p->d_origin, nullptr, 1, kpt, p->d_scal + 5, nullptr);
+        if (!S.near_empty) near_eval(p, p->d_origin, nullptr, 1, kpt, p->d_scal + 5, nullptr);
         gauge_kernel<<<1, 1, 0, s>>>(p->d_scal);
         SE_LAUNCHED(p);
     }
-    // ---- combine, energy
+    const double two_sqrtpi = 2.0 / std::sqrt(M_PI);
     double self_inf = 0.0;
-    if (xi_inf) self_inf = -two_sqrtpi / (2.0 * P.g_w) / (4.0 * M_PI * eps);
-    if (n > 0) finalize(p, n, flags, self_inf, d_phi_out, d_E_out);
-    if (energy && !p->sigma_zero) {
-        if (xi_inf) throw Error(SE_ERR_VALUE, "wall-charge energy needs a finite xi");
-        if (near_empty && n == 0) {
-            // near field of no sources is zero; wall_energy handles cl.n == 0
-            p->cl.n = 0;
-        }
+    if (S.xi_inf) self_inf = -two_sqrtpi / (2.0 * P.g_w) / (4.0 * M_PI * P.eps);
+    if (count > 0) finalize(p, first, count, S.flags, self_inf, d_phi_out, d_E_out);
+    // the wall-charge energy is global: the shard holding charge 0 adds it
+    if (S.energy && !p->sigma_zero && first == 0) {
+        if (S.xi_inf) throw Error(SE_ERR_VALUE, "wall-charge energy needs a finite xi");
+        if (S.near_empty) p->cl.n = 0;
         wall_energy(p, kpt);
     }
-    mark();
-    // ---- results
+    mark(p, S);
+}
+
+void phase_results(Plan* p, double* U, se_diag* diag) {
+    Solve& S = current(p);
+    cudaStream_t s = p->stream;
     double scal[8], k0[16];
     int hflags = 0;
     int64_t npairs = 0;
@@ -174,6 +210,7 @@ void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
     SE_CUDA(cudaMemcpyAsync(&hflags, p->d_flags, sizeof(int), cudaMemcpyDeviceToHost, s));
     SE_CUDA(cudaMemcpyAsync(&npairs, p->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     SE_CUDA(cudaStreamSynchronize(s));
+    p->timing = false;
     if (hflags & FLAG_Z_OUTSIDE) throw Error(SE_ERR_VALUE, "point outside the extended z domain");
     if (hflags & FLAG_NONFINITE) throw Error(SE_ERR_FLOAT, "non-finite mismatch field");
     if (hflags & FLAG_K0_FAIL) {
@@ -183,26 +220,26 @@ void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
                  k0[2]);
         throw Error(SE_ERR_FLOAT, buf);
     }
-    if (U) *U = energy ? (n > 0 ? scal[2] : 0.0) + (p->sigma_zero ? 0.0 : scal[3]) : 0.0;
+    const bool wall = !p->sigma_zero && S.first == 0;
+    if (U) *U = S.energy ? (S.count > 0 ? scal[2] : 0.0) + (wall ? scal[3] : 0.0) : 0.0;
     if (diag) {
         diag->ai1 = k0[0]; diag->ai2 = k0[1]; diag->discrepancy = k0[2];
         diag->A_i = k0[3]; diag->A_b = k0[4]; diag->A_t = k0[5];
         diag->psi_i_bottom = k0[6]; diag->psi_i_top = k0[7];
         diag->psi_b_bottom = k0[8]; diag->psi_t_top = k0[9];
-        diag->B_i = (potential && !xi_inf) ? scal[1] : 0.0;
-        diag->U_wall = p->sigma_zero ? 0.0 : scal[3];
+        diag->B_i = (S.potential && !S.xi_inf) ? scal[1] : 0.0;
+        diag->U_wall = wall ? scal[3] : 0.0;
         diag->warn_discrepancy = (hflags & FLAG_K0_WARN) ? 1 : 0;
         diag->n_sources = (int32_t)p->ss.S;
         diag->n_pairs = npairs;
         diag->n_launches = p->launches;
         for (int i = 0; i < 16; ++i) diag->t_ms[i] = 0.0;
-        if (timed) {
-            for (int i = 0; i + 1 < ne && i < 8; ++i) {
+        if (S.timed) {
+            for (int i = 0; i + 1 < S.ne && i < 8; ++i) {
                 float ms = 0;
-                SE_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+                SE_CUDA(cudaEventElapsedTime(&ms, S.ev[i], S.ev[i + 1]));
                 diag->t_ms[i] = ms;
             }
-            // per-kernel times: 8 spread, 9 bvp, 10 interp, 11 near (charges)
             for (int k = 0; k < 4; ++k) {
                 float ms = 0;
                 if (cudaEventElapsedTime(&ms, p->kev[k][0], p->kev[k][1]) == cudaSuccess)
@@ -212,8 +249,16 @@ void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
             }
         }
     }
-    if (timed) for (auto& e : ev) cudaEventDestroy(e);
-    p->timing = false;
+    if (S.timed) for (auto& e : S.ev) cudaEventDestroy(e);
+    S.timed = false;
+}
+
+void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
+                double* d_phi_out, double* d_E_out, double* U, se_diag* diag) {
+    phase_spread(p, d_pos, n, 0, n, flags);
+    phase_fields(p);
+    phase_charges(p, d_pos, d_phi_out, d_E_out);
+    phase_results(p, U, diag);
 }
 
 void ensure_charges(Plan* p, int64_t n) {
@@ -528,6 +573,47 @@ struct PlanGuard {
     Plan* p;
     ~PlanGuard() { if (p) se_plan_destroy(reinterpret_cast<se_plan*>(p)); }
 };
+
+int se_shard_spread(se_plan* plan, const double* d_pos_all, int64_t n_all, int64_t first,
+                    int64_t count, uint32_t flags, double** d_rho, int64_t* rho_len) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        SE_CUDA(cudaSetDevice(p->dev));
+        phase_spread(p, d_pos_all, n_all, first, count, flags);
+        if (d_rho) *d_rho = p->d_rho;
+        if (rho_len) *rho_len = 2 * p->G;
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_shard_fields(se_plan* plan) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        SE_CUDA(cudaSetDevice(p->dev));
+        phase_fields(p);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_shard_charges(se_plan* plan, const double* d_pos_all, double* d_phi, double* d_E,
+                     double* U_part, se_diag* diag) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        SE_CUDA(cudaSetDevice(p->dev));
+        phase_charges(p, d_pos_all, d_phi, d_E);
+        phase_results(p, U_part, diag);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
 
 int se_near_field(const se_params* params, int device, const double* pos, const double* q,
                   int64_t n, const double* eval_pos, int64_t ne, int kind, int need_field,

@@ -57,17 +57,18 @@ __device__ __forceinline__ int pmod(long long a, int n) {
 // first images of near-wall charges (class 1)         slab.py:51-82,280-289
 // ---------------------------------------------------------------------------
 struct SrcArgs {
-    const double* pos; const double* q; int64_t n;
+    const double* pos; const double* q; int64_t n; int64_t first;   // charges first..first+n
     double H, two_HE, fb, ft; int two_grids;
     double4* src; int* cls; int* owner;
 };
 
 __global__ void make_sources_kernel(SrcArgs a) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= a.n) return;
+    int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (li >= a.n) return;
+    const int64_t i = a.first + li;                    // global charge index
     double x = a.pos[3 * i], y = a.pos[3 * i + 1], z = a.pos[3 * i + 2];
     double qi = a.q[i];
-    int64_t base = 3 * i;
+    int64_t base = 3 * li;
     if (!a.two_grids) {
         a.src[base] = make_double4(x, y, z, qi);
         a.cls[base] = 1; a.owner[base] = (int)i;
@@ -622,9 +623,11 @@ struct PartArgs {
 };
 
 __global__ void interp_reduce_kernel(PartArgs a, const double* pos, const double* znodes,
-                                     int Nz, double hx, double hy, double rad) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= a.N) return;
+                                     int Nz, double hx, double hy, double rad, int64_t first,
+                                     int64_t count) {
+    int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (li >= count) return;
+    const int64_t i = first + li;
     const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
     const int jx = (int)floor(x / hx), jy = (int)floor(y / hy);
     const int lo = lower_bound_d(znodes, Nz, __dsub_rn(z, rad));
@@ -753,9 +756,10 @@ void ensure_sources(Plan* p, int64_t n) {
     p->src_cap = cap;
 }
 
-static void launch_make_sources(Plan* p, const double* d_pos, int64_t n, bool two_grids) {
+static void launch_make_sources(Plan* p, const double* d_pos, int64_t n, bool two_grids,
+                                int64_t first = 0) {
     const int TB = 256;
-    SrcArgs sa{d_pos, p->d_q, n, p->P.H, 2.0 * p->P.H_E,
+    SrcArgs sa{d_pos, p->d_q, n, first, p->P.H, 2.0 * p->P.H_E,
                -(p->P.eps_b - p->P.eps) / (p->P.eps_b + p->P.eps),
                -(p->P.eps_t - p->P.eps) / (p->P.eps_t + p->P.eps),
                two_grids ? 1 : 0, p->d_src, p->d_src_cls, p->d_src_owner};
@@ -778,11 +782,11 @@ void partition_sources(Plan* p, const double* d_pos, int64_t n) {
     launch_make_sources(p, d_pos, n, true);
 }
 
-void build_sources(Plan* p, const double* d_pos, int64_t n, bool two_grids) {
+void build_sources(Plan* p, const double* d_pos, int64_t first, int64_t n, bool two_grids) {
     ensure_sources(p, n);
     const int64_t total = 3 * n;
     const int TB = 256;
-    launch_make_sources(p, d_pos, n, two_grids);
+    launch_make_sources(p, d_pos, n, two_grids, first);
     SourceSet& ss = p->ss;
     ss.nbx = (p->Nx + TILE - 1) / TILE;
     ss.nby = (p->Ny + TILE - 1) / TILE;
@@ -848,9 +852,9 @@ void spread(Plan* p, bool two_grids) {
     SE_LAUNCHED(p);
 }
 
-void interp_charges(Plan* p, int64_t n, bool forces) {
+void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool forces) {
     SE_CUDA(cudaMemsetAsync(p->d_far, 0, sizeof(double) * 4 * (size_t)n, p->stream));
-    if (n == 0) return;
+    if (count == 0) return;
     TileArgs ta = tile_args(p);
     ta.TZ = INTERP_TZ;
     ta.SX = (2 * p->mx + 1 + TILE - 2) / TILE + 1 + ((p->Nx % TILE) ? 1 : 0);
@@ -880,8 +884,8 @@ void interp_charges(Plan* p, int64_t n, bool forces) {
     SE_LAUNCHED(p);
     PartArgs pa{p->d_part, p->d_far, n, nf, nullptr, nullptr, nullptr, nullptr, nullptr,
                 p->mx, p->my, p->Nx, p->Ny, INTERP_TZ, ta.SX, ta.SY};
-    interp_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(
-        pa, p->d_pos_cur, p->d_z, p->Nz, p->hx, p->hy, p->rad);
+    interp_reduce_kernel<<<(unsigned)((count + 255) / 256), 256, 0, p->stream>>>(
+        pa, p->d_pos_cur, p->d_z, p->Nz, p->hx, p->hy, p->rad, first, count);
     p->ktoc(2);
     SE_LAUNCHED(p);
 }

@@ -150,8 +150,22 @@ struct NearScratch {
     size_t cub_bytes = 0;
 };
 
+// state of one solve between its phases (se_api.cu)
+struct Solve {
+    uint32_t flags = 0;
+    bool xi_inf = false, forces = false, potential = false, energy = false, corr = false,
+         two = false, near_empty = true;
+    int mode = 0;
+    int64_t n_all = 0, first = 0, count = 0;
+    cudaEvent_t ev[12] = {};
+    int ne = 0;
+    bool timed = false;
+    int phase = 0;                // 0 idle, 1 spread done, 2 fields done
+};
+
 struct Plan {
     se_params P{};
+    Solve solve;
     int dev = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -283,10 +297,10 @@ T* dalloc(Plan* p, size_t count) {
 }
 
 // --- se_grid.cu ---
-void build_sources(Plan* p, const double* d_pos, int64_t n, bool two_grids);
+void build_sources(Plan* p, const double* d_pos, int64_t first, int64_t n, bool two_grids);
 void partition_sources(Plan* p, const double* d_pos, int64_t n);
 void spread(Plan* p, bool two_grids);
-void interp_charges(Plan* p, int64_t n, bool forces);
+void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool forces);
 void interp_points(Plan* p, const double* d_pts, int64_t npts, double width,
                    double radius, double* d_out);
 void ensure_sources(Plan* p, int64_t cap);
@@ -307,7 +321,7 @@ void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n);
 void near_eval(Plan* p, const double* d_eval, const int* d_eval_order,
                int64_t ne, const NearKernel& k, double* d_out4,
                int64_t* d_npairs);
-void finalize(Plan* p, int64_t n, uint32_t flags, double self_inf_value,
+void finalize(Plan* p, int64_t first, int64_t count, uint32_t flags, double self_inf_value,
               double* d_phi, double* d_E);
 void wall_energy(Plan* p, const NearKernel& kpoint);
 

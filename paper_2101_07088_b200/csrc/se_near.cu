@@ -509,6 +509,7 @@ __global__ void point_keys_kernel(const double* pts, int64_t n, CellGeo g, uint3
 // ---------------------------------------------------------------------------
 struct FinArgs {
     const double* far; const double* near; const double* q; int64_t n;
+    int64_t first, nfar;          // own charges first..first+n; far has stride nfar
     double cell; int forces, potential, self_inf; double self_inf_value;
     const double* scal;           // scal[1] = B_i
     double* phi; double* E; double* partial;
@@ -521,16 +522,17 @@ __global__ void finalize_kernel(FinArgs a) {
     double b_i = a.potential ? a.scal[1] : 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
          i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t gi = a.first + i;
         double phi_near = a.near[i];
-        if (a.self_inf) phi_near = phi_near + a.q[i] * a.self_inf_value;
-        double phi = (a.cell * a.far[i] + phi_near) + b_i;
+        if (a.self_inf) phi_near = phi_near + a.q[gi] * a.self_inf_value;
+        double phi = (a.cell * a.far[gi] + phi_near) + b_i;
         a.phi[i] = phi;
         if (a.forces) {
-            a.E[3 * i] = -(a.cell * a.far[a.n + i]) + a.near[a.n + i];
-            a.E[3 * i + 1] = -(a.cell * a.far[2 * a.n + i]) + a.near[2 * a.n + i];
-            a.E[3 * i + 2] = -(a.cell * a.far[3 * a.n + i]) + a.near[3 * a.n + i];
+            a.E[3 * i] = -(a.cell * a.far[a.nfar + gi]) + a.near[a.n + i];
+            a.E[3 * i + 1] = -(a.cell * a.far[2 * a.nfar + gi]) + a.near[2 * a.n + i];
+            a.E[3 * i + 2] = -(a.cell * a.far[3 * a.nfar + gi]) + a.near[3 * a.n + i];
         }
-        acc += a.q[i] * phi;
+        acc += a.q[gi] * phi;
     }
     red[threadIdx.x] = acc;
     __syncthreads();
@@ -787,11 +789,12 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     SE_LAUNCHED(p);
 }
 
-void finalize(Plan* p, int64_t n, uint32_t flags, double self_inf_value,
+void finalize(Plan* p, int64_t first, int64_t count, uint32_t flags, double self_inf_value,
               double* d_phi, double* d_E) {
     const int nblk = 592;
     FinArgs a{};
-    a.far = p->d_far; a.near = p->d_near; a.q = p->d_q; a.n = n;
+    a.far = p->d_far; a.near = p->d_near; a.q = p->d_q; a.n = count;
+    a.first = first; a.nfar = p->N;
     a.cell = p->hx * p->hy;
     a.forces = (flags & SE_NEED_FORCES) ? 1 : 0;
     a.potential = (flags & SE_NEED_POTENTIAL) && !(p->P.xi_is_inf != 0.0);

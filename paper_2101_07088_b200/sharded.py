@@ -1,0 +1,190 @@
+"""One system solved on several GPUs (one process per GPU).
+
+The charges are split by index into contiguous shards, one per rank
+(SURVEY.md section 8e, step 1).  Each rank
+
+1. spreads its own charges (and their first images) into a full copy of the
+   grids (``se_shard_spread``),
+2. sums the grids over ranks in place (``torch.distributed.all_reduce``, NCCL
+   over NVLink on the solver's stream),
+3. runs the grid pipeline -- xy FFTs, z DCT-I, mode BVPs, correction, inverse
+   transforms -- on the summed grids (``se_shard_fields``; replicated, it is
+   a small share of the solve),
+4. interpolates the fields and evaluates the near field at its own charges,
+   with every charge as a near-field source (``se_shard_charges``),
+
+then the parts of the energy are summed (all-reduce of one double) and, for
+the host API, potentials and fields are gathered to every rank.  Spreading is
+linear in the charges and the per-charge stages are independent, so the
+result equals the single-GPU solve up to the order of the grid sums.
+
+The host logic here is backend-neutral: ``ShardedSlabSolver`` drives an
+engine with the three phases.  The product engine is ``CudaShardEngine``
+(the C-ABI in include/slabewald.h); the CPU tests drive the same host logic
+over ``gloo`` with a checker engine built on the test oracle.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .slab import STAGES, SlabSolver, SolveResult, _flags
+
+
+def shard_range(n, rank, world):
+    """Contiguous index range [first, first + count) of ``rank``."""
+    first = (n * rank) // world
+    last = (n * (rank + 1)) // world
+    return first, last - first
+
+
+class _DeviceArray:
+    """Zero-copy view of a library-owned device buffer for torch."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {
+            "shape": (int(n),), "typestr": "<f8", "data": (int(ptr), False),
+            "version": 3, "strides": None}
+
+
+class CudaShardEngine:
+    """The three solve phases of one rank on its GPU (se_shard_*)."""
+
+    def __init__(self, system, params, refine=1, device=0):
+        self.device = torch.device("cuda", device)
+        self.solver = SlabSolver(system, params, refine=refine, device=device)
+        self.solver.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+        self._lib = self.solver._lib
+
+    def positions(self, positions):
+        if isinstance(positions, torch.Tensor):
+            pos = positions.to(torch.float64)
+        else:
+            pos = torch.as_tensor(np.ascontiguousarray(positions,
+                                                       dtype=np.float64))
+        return pos.to(self.device, non_blocking=True).contiguous()
+
+    def spread(self, pos_all, first, count, flags):
+        ptr = ctypes.c_void_p()
+        size = ctypes.c_int64()
+        _lib.check(self._lib.se_shard_spread(
+            self.solver._plan, ctypes.c_void_p(pos_all.data_ptr()),
+            pos_all.shape[0], first, count, flags, ctypes.byref(ptr),
+            ctypes.byref(size)))
+        return torch.as_tensor(_DeviceArray(ptr.value, size.value),
+                               device=self.device)
+
+    def fields(self):
+        _lib.check(self._lib.se_shard_fields(self.solver._plan))
+
+    def charges(self, pos_all, count, need_forces):
+        phi = torch.empty(count, dtype=torch.float64, device=self.device)
+        E = torch.zeros((count, 3), dtype=torch.float64, device=self.device)
+        U = ctypes.c_double(0.0)
+        diag = _lib.SeDiag()
+        _lib.check(self._lib.se_shard_charges(
+            self.solver._plan, ctypes.c_void_p(pos_all.data_ptr()),
+            ctypes.c_void_p(phi.data_ptr()),
+            ctypes.c_void_p(E.data_ptr() if need_forces else 0),
+            ctypes.byref(U), ctypes.byref(diag)))
+        return phi, E, float(U.value), diag
+
+    def diagnostics(self, diag):
+        return self.solver._diagnostics(diag)
+
+    def close(self):
+        self.solver.close()
+
+
+class ShardedSlabSolver:
+    """``SlabSolver`` API over a process group: every rank constructs it with
+    the same system; ``solve`` returns the full result on every rank."""
+
+    def __init__(self, system, params, threads=1, refine=1, group=None,
+                 device=None, engine=None):
+        if not dist.is_initialized():
+            raise RuntimeError("ShardedSlabSolver needs torch.distributed "
+                               "initialised (one process per GPU)")
+        self.system, self.params = system, params
+        self.threads = threads
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        n = system.charges.size
+        self.first, self.count = shard_range(n, self.rank, self.world)
+        self.counts = [shard_range(n, r, self.world)[1]
+                       for r in range(self.world)]
+        if engine is None:
+            if device is None:
+                device = torch.cuda.current_device()
+            engine = CudaShardEngine(system, params, refine, device)
+        self.engine = engine
+        self.last_timings = None
+
+    def close(self):
+        self.engine.close()
+
+    def solve_shard(self, pos_all, need_energy=True, need_forces=True,
+                    need_potential=True, subtract_self=False,
+                    include_correction=True, force_general=False,
+                    timings=False):
+        """The sharded solve on engine-resident positions of ALL charges.
+        Returns (phi, E, U, diag) with phi, E for this rank's charges
+        ``first .. first+count-1`` and U the total energy."""
+        flags = _flags(need_energy, need_forces, need_potential,
+                       subtract_self, include_correction, force_general,
+                       timings)
+        rho = self.engine.spread(pos_all, self.first, self.count, flags)
+        if self.world > 1:
+            dist.all_reduce(rho, group=self.group)
+        self.engine.fields()
+        phi, E, u_part, diag = self.engine.charges(pos_all, self.count,
+                                                   need_forces)
+        U = u_part
+        if self.world > 1:
+            u = torch.tensor([u_part], dtype=torch.float64, device=phi.device)
+            dist.all_reduce(u, group=self.group)
+            U = float(u.item())
+        if timings and hasattr(diag, "t_ms"):
+            self.last_timings = dict(zip(STAGES, list(diag.t_ms)[:len(STAGES)]))
+        return phi, E, U, diag
+
+    def _gather(self, local, width):
+        if self.world == 1:
+            return local
+        cap = max(self.counts)
+        buf = torch.zeros((cap, width), dtype=local.dtype, device=local.device)
+        buf[:local.shape[0]] = local.reshape(-1, width)
+        parts = [torch.empty_like(buf) for _ in range(self.world)]
+        dist.all_gather(parts, buf, group=self.group)
+        return torch.cat([p[:c] for p, c in zip(parts, self.counts)])
+
+    def solve(self, positions=None, need_energy=True, need_forces=True,
+              need_potential=True, subtract_self=False,
+              include_correction=True, force_general=False, timings=False):
+        """Same call and result as ``SlabSolver.solve`` (reference
+        slab.py:259-394), computed across the group."""
+        pos = self.system.positions if positions is None else positions
+        pos = np.atleast_2d(np.asarray(pos, dtype=float))
+        if pos.ndim != 2 or (pos.size and pos.shape[1] != 3):
+            raise ValueError("positions must be (N, 3)")
+        if pos.shape[0] != self.system.charges.size:
+            raise ValueError("positions and charges disagree on N")
+        pos_all = self.engine.positions(pos)
+        phi, E, U, diag = self.solve_shard(
+            pos_all, need_energy, need_forces, need_potential, subtract_self,
+            include_correction, force_general, timings)
+        phi_all = self._gather(phi.reshape(-1, 1), 1).reshape(-1)
+        E_all = self._gather(E, 3) if need_forces else \
+            torch.zeros((pos.shape[0], 3), dtype=torch.float64)
+        out = self.engine.diagnostics(diag)
+        if timings and self.last_timings is not None:
+            out["timings_ms"] = self.last_timings
+        return SolveResult(phi_bar=phi_all.cpu().numpy(),
+                           E_bar=E_all.cpu().numpy(), U=U, diagnostics=out)
+
+
+__all__ = ["ShardedSlabSolver", "CudaShardEngine", "shard_range"]

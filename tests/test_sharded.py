@@ -1,0 +1,90 @@
+"""Sharded solve (charges split by index across ranks, grids all-reduced):
+the host logic of ``ShardedSlabSolver`` on CPU over ``gloo`` with
+world_size 2 and 3, each rank's phases computed by the oracle engine.  The
+result must equal the unsharded solve (and the reference's golden output)
+up to the summation order of the grids.  The GPU engine is covered by
+``test_gpu_parity.py::test_sharded_single_rank``."""
+
+import os
+import pickle
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from _golden import rel_l2, solves
+from paper_2101_07088_b200.sharded import ShardedSlabSolver, shard_range
+
+CASES = ["c2n256", "c2n256_noforce", "c2n256_nocorr", "c3n256_gauss_sigma"]
+TOL = 1e-12
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, cases, outdir):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    for p in (here, os.path.dirname(here)):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    from _oracle_engine import OracleShardEngine
+    from test_oracle_golden import variant_problem
+    dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % port,
+                            rank=rank, world_size=world)
+    try:
+        out = {}
+        for case in cases:
+            system, params, kw = variant_problem(case)
+            refine = kw.pop("refine", 1)
+            eng = OracleShardEngine(system, params, refine=refine)
+            solver = ShardedSlabSolver(system, params, engine=eng)
+            res = solver.solve(**kw)
+            out[case] = (res.phi_bar, res.E_bar, res.U,
+                         res.diagnostics["B_i"], solver.first, solver.count)
+        with open(os.path.join(outdir, "rank%d.pkl" % rank), "wb") as f:
+            pickle.dump(out, f)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_ranges_cover():
+    for n in (0, 1, 5, 256, 1 << 20):
+        for w in (1, 2, 3, 8):
+            got = [shard_range(n, r, w) for r in range(w)]
+            assert got[0][0] == 0
+            for (f0, c0), (f1, _) in zip(got, got[1:]):
+                assert f0 + c0 == f1
+            assert got[-1][0] + got[-1][1] == n
+            assert max(c for _, c in got) - min(c for _, c in got) <= 1
+
+
+@pytest.mark.parametrize("world,cases", [(2, CASES),
+                                         (3, ["c3n256_gauss_sigma"])])
+def test_sharded_matches_golden(tmp_path, world, cases):
+    mp.spawn(_worker, args=(world, _free_port(), cases, str(tmp_path)),
+             nprocs=world, join=True)
+    gold = solves()
+    ranks = []
+    for r in range(world):
+        with open(tmp_path / ("rank%d.pkl" % r), "rb") as f:
+            ranks.append(pickle.load(f))
+    for case in cases:
+        g = gold[case]
+        phi0, E0, U0, B0, _, _ = ranks[0][case]
+        assert rel_l2(phi0, g["phi"]) < TOL, case
+        if "noforce" not in case:
+            assert rel_l2(E0, g["E"]) < TOL, case
+        assert abs(U0 - g["U"]) <= TOL * max(1.0, abs(g["U"])), case
+        assert abs(B0 - g["B_i"]) <= TOL * max(1.0, abs(g["B_i"])), case
+        # every rank returns the same gathered result and the same energy
+        for r in range(1, world):
+            phi, E, U, B, first, count = ranks[r][case]
+            assert np.array_equal(phi, phi0) and np.array_equal(E, E0)
+            assert U == U0 and B == B0
+        assert sum(ranks[r][case][5] for r in range(world)) == phi0.size
