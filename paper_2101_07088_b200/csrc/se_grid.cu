@@ -265,7 +265,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // Rows are per source so the compute loop reads a source's weights with
 // broadcast (vector) loads; the fill maps consecutive threads to consecutive
 // addresses both in shared memory and in the AoS stencil records.
-template <int TZ, int CAP, bool OWNER>
+template <int TZ, int CAP>
 struct Stage {
     double wx[CAP][TILE];
     double wy[CAP][TILE];
@@ -273,8 +273,6 @@ struct Stage {
     double q[CAP];
     int idx[CAP], lo[CAP], ox[CAP], oy[CAP];
     unsigned xm[CAP], zm[CAP];
-    int own[OWNER ? CAP : 1];
-    int pslot[OWNER ? CAP : 1];     // interp: slot of this tile among the charge's tiles
     int wcount[8];
 };
 
@@ -295,18 +293,17 @@ __device__ __forceinline__ unsigned axis_mask(int j0, int m, int n, int g0, int*
 // One staging round: candidates [cursor, cursor + CAP) are tested against
 // the tile, the touching ones are compacted (warp ballots + block prefix)
 // and their tile-restricted weights staged.  Returns the staged count.
-template <int TZ, int NG, int CAP, bool OWNER, bool FOLD_Q>
-__device__ int stage_round(Stage<TZ, CAP, OWNER>& sm, const TileArgs& A, int cursor,
+template <int TZ, int NG, int CAP, bool FOLD_Q>
+__device__ int stage_round(Stage<TZ, CAP>& sm, const TileArgs& A, int cursor,
                            int total, const int* s_lo, const int* s_len, int nr,
                            int gx0, int gy0, int k0) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     constexpr int NW = CAP / 32;
     bool touch = false;
-    int i = -1, lo = 0, ox = 0, oy = 0, own = 0;
+    int i = -1, lo = 0, ox = 0, oy = 0;
     unsigned xm = 0, zm = 0;
     if (t < CAP && cursor + t < total) {
         i = map_candidate(cursor + t, s_lo, s_len, nr);
-        if (OWNER && i >= 0) { own = A.st.owner[i]; if (own < 0) i = -1; }
         if (i >= 0) {
             lo = A.st.lo[i];
             const int hi = A.st.hi[i];
@@ -339,16 +336,6 @@ __device__ int stage_round(Stage<TZ, CAP, OWNER>& sm, const TileArgs& A, int cur
         sm.idx[sl] = i; sm.lo[sl] = lo; sm.ox[sl] = ox; sm.oy[sl] = oy;
         sm.xm[sl] = xm; sm.zm[sl] = zm;
         sm.q[sl] = FOLD_Q ? A.st.q[i] : 1.0;
-        if (OWNER) {
-            sm.own[OWNER ? sl : 0] = own;
-            // tile offsets from the charge's first tile in x, y, z
-            const int fx = imod(A.st.j0x[i] - A.st.mx, A.Nx) / TILE;
-            const int fy = imod(A.st.j0y[i] - A.st.my, A.Ny) / TILE;
-            const int fz = lo / TZ;
-            const int sx = imod(gx0 / TILE - fx, A.nbx), sy = imod(gy0 / TILE - fy, A.nby);
-            const int sz = k0 / TZ - fz;
-            sm.pslot[OWNER ? sl : 0] = (sz * A.SY + sy) * A.SX + sx;
-        }
     }
     __syncthreads();
     const int rs = A.st.rs, mx = A.st.mx, my = A.st.my;
@@ -396,8 +383,7 @@ struct SpreadArgs {
 };
 
 constexpr int SPREAD_CAP = 256;
-constexpr int INTERP_CAP = 128;
-using SpreadStage = Stage<SPREAD_TZ, SPREAD_CAP, false>;
+using SpreadStage = Stage<SPREAD_TZ, SPREAD_CAP>;
 
 __global__ void __launch_bounds__(256, 2) spread_kernel(SpreadArgs a) {
     constexpr int TZ = SPREAD_TZ;       // 32 nodes = 4 groups of 8
@@ -423,7 +409,7 @@ __global__ void __launch_bounds__(256, 2) spread_kernel(SpreadArgs a) {
         tile_ranges<TZ>(A, bx, by, k0, cls, s_lo, s_len, &s_nr, &s_total);
         const int total = s_total, nr = s_nr;
         for (int cursor = 0; cursor < total; cursor += SPREAD_CAP) {
-            const int n = stage_round<TZ, 4, SPREAD_CAP, false, true>(
+            const int n = stage_round<TZ, 4, SPREAD_CAP, true>(
                 sm, A, cursor, total, s_lo, s_len, nr, gx0, gy0, k0);
             for (int w0 = 0; w0 < n; w0 += 32) {
                 const int s0 = w0 + lane;
@@ -457,203 +443,236 @@ __global__ void __launch_bounds__(256, 2) spread_kernel(SpreadArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// interpolation of the field stack at the charges (adjoint)   gridops.py:105-133
+// interpolation of the field stack at the charges         gridops.py:105-133
+//
+// Charge-stationary: the charges are sorted by (4x4-column xy bin, first z
+// node) and cut into groups of IG consecutive charges of one bin.  One warp
+// owns a group: its window is the union of the group's stencils (at most
+// (3 + 2 mx + 1) x (3 + 2 my + 1) columns x the union z range), each lane
+// walks window columns and for every z node loads the NF field values once
+// and applies them to all IG charges (IG x NF FMAs per NF loads).  Weights
+// are recomputed in the reference's operation order (bit-identical to the
+// spread's stencils).  The k = 0 linear terms (psi + A_i z, dpsi/dz + A_i)
+// are separable and added analytically.  The per-charge sums are reduced
+// across the warp and written once: no atomics, no partial buffers.
 // ---------------------------------------------------------------------------
-struct InterpArgs {
-    TileArgs t;
-    const double* fields;        // [Nz][4][Nx][Ny]
-    const double* znodes; const double* wcc;
-    const double* scal;          // scal[0] = A_i
-    double* out;                 // [4][N] raw sums
-    int64_t N;
-    int nf;                      // 1 (potential only) or 4
-    double* part;                // [SX*SY*SZ][nf][N] per-tile partial sums
+constexpr int IG = 4;            // charges per warp group
+constexpr int IBIN = 4;          // xy bin width (columns)
+constexpr int IZC = 32;          // z nodes per weight-table chunk
+constexpr int IWARPS = 8;
+
+struct ChargeKeyArgs {
+    const double* pos; int64_t first, count;
+    const double* znodes; int Nz; double hx, hy, rad; int Nx, Ny, nbx; int zbits;
+    uint32_t* keys; int* perm;
 };
 
-// Butterfly transpose-reduction across the warp: lane l starts with 32
-// partial values v[0..31] and ends with the warp total of value index l.
-__device__ __forceinline__ double warp_transpose_reduce32(double (&v)[32], int lane) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const bool up = lane & 16;
-        const double send = up ? v[j] : v[j + 16], keep = up ? v[j + 16] : v[j];
-        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const bool up = lane & 8;
-        const double send = up ? v[j] : v[j + 8], keep = up ? v[j + 8] : v[j];
-        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const bool up = lane & 4;
-        const double send = up ? v[j] : v[j + 4], keep = up ? v[j + 4] : v[j];
-        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const bool up = lane & 2;
-        const double send = up ? v[j] : v[j + 2], keep = up ? v[j + 2] : v[j];
-        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    }
-    {
-        const bool up = lane & 1;
-        const double send = up ? v[0] : v[1], keep = up ? v[1] : v[0];
-        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-    }
-    return v[0];
+__global__ void charge_keys_kernel(ChargeKeyArgs a) {
+    int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (li >= a.count) return;
+    const int64_t i = a.first + li;
+    const double x = a.pos[3 * i], y = a.pos[3 * i + 1], z = a.pos[3 * i + 2];
+    const int cx = pmod((long long)floor(x / a.hx), a.Nx);
+    const int cy = pmod((long long)floor(y / a.hy), a.Ny);
+    const uint32_t bin = (uint32_t)((cy / IBIN) * a.nbx + cx / IBIN);
+    const int lo = lower_bound_d(a.znodes, a.Nz, __dsub_rn(z, a.rad));
+    a.keys[li] = (bin << a.zbits) | (uint32_t)lo;
+    a.perm[li] = (int)i;
 }
 
-template <int NF>
-struct InterpSmem {
-    Stage<INTERP_TZ, INTERP_CAP, true> st;
-    double red[8][INTERP_CAP][NF];      // per-warp totals
-    unsigned done[8][INTERP_CAP / 32];  // which (warp, slot) entries are valid
+// groups of <= IG consecutive sorted charges within each bin: one block,
+// each thread a contiguous run of bins, block-wide exclusive scan
+__global__ void __launch_bounds__(1024) charge_groups_kernel(const int64_t* seg, int nbins,
+                                                            int2* groups, int* ngroups) {
+    typedef cub::BlockScan<int, 1024> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    const int per = (nbins + 1023) / 1024;
+    const int b0 = threadIdx.x * per, b1 = min(nbins, b0 + per);
+    int mine = 0;
+    for (int b = b0; b < b1; ++b) mine += (int)((seg[b + 1] - seg[b] + IG - 1) / IG);
+    int off = 0, total = 0;
+    Scan(tmp).ExclusiveSum(mine, off, total);
+    for (int b = b0; b < b1; ++b) {
+        const int64_t s0 = seg[b], n = seg[b + 1] - s0;
+        for (int64_t j = 0; j < n; j += IG)
+            groups[off++] = make_int2((int)(s0 + j), (int)(n - j < IG ? n - j : IG));
+    }
+    if (threadIdx.x == 0) *ngroups = total;
+}
+
+struct InterpArgs {
+    const double* fields;        // [Nz][4][Nx][Ny]
+    const double* pos; const double* znodes; const double* wcc;
+    const double* scal;          // scal[0] = A_i
+    const int* perm; const int2* groups; const int* ngroups;
+    int Nx, Ny, Nz; int64_t NXY;
+    double hx, hy, rad, rad_keep, width, norm; int mx, my;
+    double* out; int64_t N;      // [NF][N] raw sums (global charge index)
+};
+
+struct GroupInfo {
+    double x[IG], y[IG], z[IG];
+    long long jx[IG], jy[IG];
+    int jxw[IG], jyw[IG], lo[IG], hi[IG], idx[IG];
 };
 
 template <int NF>
-__global__ void __launch_bounds__(256) interp_kernel(InterpArgs a) {
-    constexpr int TZ = INTERP_TZ;       // 16 nodes = 4 groups of 4
-    constexpr int NB = 32 / NF;         // sources per transpose-reduce batch
-    extern __shared__ __align__(16) unsigned char dsm[];
-    InterpSmem<NF>& S = *reinterpret_cast<InterpSmem<NF>*>(dsm);
-    auto& sm = S.st;
-    __shared__ int s_lo[MAX_BINS], s_len[MAX_BINS], s_nr, s_total;
-
-    const TileArgs& A = a.t;
-    const int bx = blockIdx.x, by = blockIdx.y, k0 = blockIdx.z * TZ;
-    const int gx0 = bx * TILE, gy0 = by * TILE;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int tx = 4 * (warp & 1) + (lane >> 3), ty = lane & 7, zg = warp >> 1;
-    const unsigned wxbits = 0xFu << (4 * (warp & 1));
-    const unsigned wzbit = 1u << zg;
-    const int gx = gx0 + tx, gy = gy0 + ty;
-    const double A_i = a.scal[0];
-
-    // field values of this thread's column x 4 nodes, CC-weighted, with the
-    // k = 0 linear terms folded in (psi + A_i z, dpsi + A_i; slab.py:340-352)
-    double F[NF][4];
+__global__ void __launch_bounds__(IWARPS * 32) interp_kernel(InterpArgs a) {
+    extern __shared__ __align__(16) double ism[];
+    __shared__ GroupInfo ginfo[IWARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = blockIdx.x * IWARPS + warp;
+    if (g >= *a.ngroups) return;
+    const int SX = 2 * a.mx + 1, SY = 2 * a.my + 1;
+    double* swx = ism + (size_t)warp * IG * (SX + SY + IZC);
+    double* swy = swx + IG * SX;
+    double* swz = swy + IG * SY;
+    GroupInfo& gi = ginfo[warp];
+    const int2 gr = a.groups[g];
+    const int cnt = gr.y;
+    if (lane < IG) {
+        int i = -1, lo = 0, hi = 0, jxw = 0, jyw = 0;
+        long long jx = 0, jy = 0;
+        double x = 0, y = 0, z = 0;
+        if (lane < cnt) {
+            i = a.perm[gr.x + lane];
+            x = a.pos[3 * i]; y = a.pos[3 * i + 1]; z = a.pos[3 * i + 2];
+            jx = (long long)floor(x / a.hx);
+            jy = (long long)floor(y / a.hy);
+            jxw = pmod(jx, a.Nx); jyw = pmod(jy, a.Ny);
+            lo = lower_bound_d(a.znodes, a.Nz, __dsub_rn(z, a.rad));
+            hi = upper_bound_d(a.znodes, a.Nz, __dadd_rn(z, a.rad));
+        }
+        gi.x[lane] = x; gi.y[lane] = y; gi.z[lane] = z;
+        gi.jx[lane] = jx; gi.jy[lane] = jy; gi.jxw[lane] = jxw; gi.jyw[lane] = jyw;
+        gi.lo[lane] = lo; gi.hi[lane] = hi; gi.idx[lane] = i;
+    }
+    __syncwarp();
+    int jxw[IG], jyw[IG];
+    int xmin = 1 << 30, xmax = -1, ymin = 1 << 30, ymax = -1, zlo = 1 << 30, zhi = 0;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        int k = k0 + 4 * zg + r;
-        bool ok = (k < A.Nz) && (gx < A.Nx) && (gy < A.Ny);
-        double wq = ok ? a.wcc[k] : 0.0;
-#pragma unroll
-        for (int c = 0; c < NF; ++c) {
-            double v = 0.0;
-            if (ok) {
-                v = a.fields[((int64_t)k * 4 + c) * A.NXY + (int64_t)gx * A.Ny + gy];
-                if (c == 0) v = v + A_i * a.znodes[k];
-                if (c == 3) v = v + A_i;
-            }
-            F[c][r] = v * wq;
+    for (int m = 0; m < IG; ++m) {
+        jxw[m] = gi.jxw[m]; jyw[m] = gi.jyw[m];
+        if (m < cnt) {
+            xmin = min(xmin, jxw[m]); xmax = max(xmax, jxw[m]);
+            ymin = min(ymin, jyw[m]); ymax = max(ymax, jyw[m]);
+            zlo = min(zlo, gi.lo[m]); zhi = max(zhi, gi.hi[m]);
         }
     }
-
-    for (int cls = 0; cls < 2; ++cls) {
-        tile_ranges<TZ>(A, bx, by, k0, cls, s_lo, s_len, &s_nr, &s_total);
-        const int total = s_total, nr = s_nr;
-        for (int cursor = 0; cursor < total; cursor += INTERP_CAP) {
-            const int n = stage_round<TZ, 4, INTERP_CAP, true, false>(
-                sm, A, cursor, total, s_lo, s_len, nr, gx0, gy0, k0);
-            for (int w0 = 0; w0 < INTERP_CAP; w0 += 32) {
-                const int s0 = w0 + lane;
-                const bool act = s0 < n && (sm.xm[s0] & wxbits) && (sm.zm[s0] & wzbit);
-                unsigned m = __ballot_sync(0xffffffffu, act);
-                if (lane == 0) S.done[warp][w0 >> 5] = m;
-                while (m) {
-                    double v[32];
-                    int first = w0 + __ffs(m) - 1;   // batch slots are first.. in mask order
-                    unsigned mb = m;
+    // x / y weights: offsets o = 0 .. 2m of each charge (gridops.py:20-25)
+    for (int e = lane; e < IG * SX; e += 32) {
+        const int m = e / SX, o = e - m * SX;
+        double wt = 0.0;
+        if (m < cnt) {
+            const double xj = __dmul_rn((double)(gi.jx[m] + o - a.mx), a.hx);
+            const double d = __dsub_rn(gi.x[m], xj);
+            if (fabs(d) <= a.rad_keep) { const double t = d / a.width; wt = exp(-0.5 * (t * t)) / a.norm; }
+        }
+        swx[e] = wt;
+    }
+    for (int e = lane; e < IG * SY; e += 32) {
+        const int m = e / SY, o = e - m * SY;
+        double wt = 0.0;
+        if (m < cnt) {
+            const double yj = __dmul_rn((double)(gi.jy[m] + o - a.my), a.hy);
+            const double d = __dsub_rn(gi.y[m], yj);
+            if (fabs(d) <= a.rad_keep) { const double t = d / a.width; wt = exp(-0.5 * (t * t)) / a.norm; }
+        }
+        swy[e] = wt;
+    }
+    __syncwarp();
+    // separable sums for the k = 0 linear terms (lane m: charge m)
+    double sx = 0.0, sy = 0.0, sz0 = 0.0, sz1 = 0.0;
+    if (lane < IG) {
+        for (int o = 0; o < SX; ++o) sx += swx[lane * SX + o];
+        for (int o = 0; o < SY; ++o) sy += swy[lane * SY + o];
+    }
+    double acc[IG][NF];
 #pragma unroll
-                    for (int b = 0; b < NB; ++b) {
-                        if (mb) {
-                            const int s = w0 + __ffs(mb) - 1;
-                            mb &= mb - 1;
-                            const double wxy = sm.wx[s][tx] * sm.wy[s][ty];
-                            const double2* wz = reinterpret_cast<const double2*>(&sm.wz[s][4 * zg]);
-                            const double2 w01 = wz[0], w23 = wz[1];
+    for (int m = 0; m < IG; ++m)
 #pragma unroll
-                            for (int c = 0; c < NF; ++c) {
-                                double u = w01.x * F[c][0];
-                                u = fma(w01.y, F[c][1], u);
-                                u = fma(w23.x, F[c][2], u);
-                                u = fma(w23.y, F[c][3], u);
-                                v[b * NF + c] = u * wxy;
-                            }
-                        } else {
+        for (int c = 0; c < NF; ++c) acc[m][c] = 0.0;
+    const int Wx = xmax - xmin + SX, Wy = ymax - ymin + SY;
+    const int64_t zstride = 4 * a.NXY;
+    for (int zc = zlo; zc < zhi; zc += IZC) {
+        const int nz = min(IZC, zhi - zc);
+        __syncwarp();
+        // z weights x Clenshaw-Curtis weights (gridops.py:29-39, 128-129)
+        for (int e = lane; e < IG * IZC; e += 32) {
+            const int m = e / IZC, r = e - m * IZC, k = zc + r;
+            double wt = 0.0;
+            if (m < cnt && k >= gi.lo[m] && k < gi.hi[m] && k < a.Nz) {
+                const double d = __dsub_rn(gi.z[m], a.znodes[k]);
+                if (fabs(d) <= a.rad) { const double u = d / a.width; wt = exp(-0.5 * (u * u)) / a.norm; }
+                wt = wt * a.wcc[k];
+            }
+            swz[e] = wt;
+        }
+        __syncwarp();
+        if (lane < IG) {
+            for (int r = 0; r < nz; ++r) {
+                const double w = swz[lane * IZC + r];
+                sz1 += w;
+                sz0 += w * a.znodes[zc + r];
+            }
+        }
+        for (int p = lane; p < Wx * Wy; p += 32) {
+            const int ux = p / Wy, uy = p - ux * Wy;
+            double wxy[IG];
+            bool any = false;
 #pragma unroll
-                            for (int c = 0; c < NF; ++c) v[b * NF + c] = 0.0;
-                        }
-                    }
-                    (void)first;
-                    const double tot = warp_transpose_reduce32(v, lane);
-                    // lane l holds batch entry l / NF, field l % NF: find its slot
-                    unsigned mm = m;
-                    const int want = lane / NF;
-                    for (int b = 0; b < want && mm; ++b) mm &= mm - 1;
-                    if (mm) S.red[warp][w0 + __ffs(mm) - 1][lane % NF] = tot;
-                    m = mb;
+            for (int m = 0; m < IG; ++m) {
+                const int ox = xmin + ux - jxw[m], oy = ymin + uy - jyw[m];
+                double w = 0.0;
+                if (m < cnt && ox >= 0 && ox < SX && oy >= 0 && oy < SY)
+                    w = swx[m * SX + ox] * swy[m * SY + oy];
+                wxy[m] = w;
+                any |= (w != 0.0);
+            }
+            if (!any) continue;
+            int gx = xmin - a.mx + ux, gy = ymin - a.my + uy;
+            gx %= a.Nx; if (gx < 0) gx += a.Nx;
+            gy %= a.Ny; if (gy < 0) gy += a.Ny;
+            const double* F = a.fields + (int64_t)zc * zstride + (int64_t)gx * a.Ny + gy;
+#pragma unroll 2
+            for (int r = 0; r < nz; ++r) {
+                double f[NF];
+#pragma unroll
+                for (int c = 0; c < NF; ++c) f[c] = __ldg(F + (int64_t)r * zstride + c * a.NXY);
+#pragma unroll
+                for (int m = 0; m < IG; ++m) {
+                    const double W = wxy[m] * swz[m * IZC + r];
+#pragma unroll
+                    for (int c = 0; c < NF; ++c) acc[m][c] = fma(W, f[c], acc[m][c]);
                 }
             }
-            __syncthreads();
-            // combine the warps that touched each staged source and store the
-            // tile's partial sum in the charge's slot for this tile (no atomics)
-            for (int e = t; e < n * NF; e += blockDim.x) {
-                const int s = e / NF, c = e % NF;
-                const unsigned bit = 1u << (s & 31);
-                double v = 0.0;
-#pragma unroll
-                for (int w = 0; w < 8; ++w)
-                    if (S.done[w][s >> 5] & bit) v += S.red[w][s][c];
-                a.part[((int64_t)sm.pslot[s] * NF + c) * a.N + sm.own[s]] = v;
-            }
-            __syncthreads();
         }
     }
-}
-
-// per-charge sum of its tile partials: the touched tiles are exactly the
-// tiles intersecting the charge's stencil box (same test as the staging)
-struct PartArgs {
-    const double* part; double* out; int64_t N; int nf;
-    const int* j0x; const int* j0y; const int* lo; const int* hi; const int* perm_inv;
-    int mx, my, Nx, Ny, TZ, SX, SY;
-};
-
-__global__ void interp_reduce_kernel(PartArgs a, const double* pos, const double* znodes,
-                                     int Nz, double hx, double hy, double rad, int64_t first,
-                                     int64_t count) {
-    int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (li >= count) return;
-    const int64_t i = first + li;
-    const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
-    const int jx = (int)floor(x / hx), jy = (int)floor(y / hy);
-    const int lo = lower_bound_d(znodes, Nz, __dsub_rn(z, rad));
-    const int hi = upper_bound_d(znodes, Nz, __dadd_rn(z, rad));
-    const int fx = imod(jx - a.mx, a.Nx), fy = imod(jy - a.my, a.Ny);
-    // tiles touched along x: those containing columns fx .. fx + 2mx (mod Nx)
-    auto ntiles = [](int f, int w, int n) {
-        int first = f / TILE, cnt = 0;
-        for (int c = 0; c < w; ++c) {                 // distinct tiles in order
-            int g = f + c; if (g >= n) g -= n;
-            int t = g / TILE;
-            int off = t - first; if (off < 0) off += (n + TILE - 1) / TILE;
-            if (off + 1 > cnt) cnt = off + 1;
+    // warp sums; lane m * NF + c ends up holding (m, c)
+    double mine = 0.0;
+#pragma unroll
+    for (int m = 0; m < IG; ++m)
+#pragma unroll
+        for (int c = 0; c < NF; ++c) {
+            double v = acc[m][c];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == m * NF + c) mine = v;
         }
-        return cnt;
-    };
-    const int nx = ntiles(fx, 2 * a.mx + 1, a.Nx), ny = ntiles(fy, 2 * a.my + 1, a.Ny);
-    const int nz = (hi > lo) ? (hi - 1) / a.TZ - lo / a.TZ + 1 : 0;
-    double acc[4] = {0, 0, 0, 0};
-    for (int sz = 0; sz < nz; ++sz)
-        for (int sy = 0; sy < ny; ++sy)
-            for (int sx = 0; sx < nx; ++sx) {
-                const int64_t sl = (int64_t)(sz * a.SY + sy) * a.SX + sx;
-                for (int c = 0; c < a.nf; ++c) acc[c] += a.part[(sl * a.nf + c) * a.N + i];
-            }
-    for (int c = 0; c < a.nf; ++c) a.out[(int64_t)c * a.N + i] = acc[c];
+    // analytic k = 0 terms: sum_nodes W * (A_i z) and W * A_i
+    const double A_i = a.scal[0];
+    const int src = lane / NF;
+    const double Sx = __shfl_sync(0xffffffffu, sx, src & (IG - 1));
+    const double Sy = __shfl_sync(0xffffffffu, sy, src & (IG - 1));
+    const double Sz0 = __shfl_sync(0xffffffffu, sz0, src & (IG - 1));
+    const double Sz1 = __shfl_sync(0xffffffffu, sz1, src & (IG - 1));
+    if (lane < IG * NF && src < cnt) {
+        const int c = lane - src * NF;
+        double v = mine;
+        if (c == 0) v += A_i * ((Sx * Sy) * Sz0);
+        if (c == 3) v += A_i * ((Sx * Sy) * Sz1);
+        a.out[(int64_t)c * a.N + gi.idx[src]] = v;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -853,39 +872,50 @@ void spread(Plan* p, bool two_grids) {
 }
 
 void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool forces) {
-    SE_CUDA(cudaMemsetAsync(p->d_far, 0, sizeof(double) * 4 * (size_t)n, p->stream));
     if (count == 0) return;
-    TileArgs ta = tile_args(p);
-    ta.TZ = INTERP_TZ;
-    ta.SX = (2 * p->mx + 1 + TILE - 2) / TILE + 1 + ((p->Nx % TILE) ? 1 : 0);
-    ta.SY = (2 * p->my + 1 + TILE - 2) / TILE + 1 + ((p->Ny % TILE) ? 1 : 0);
-    ta.SZ = (p->wz_max + INTERP_TZ - 2) / INTERP_TZ + 1;
-    const int nf = forces ? 4 : 1;
-    const int64_t need = (int64_t)ta.SX * ta.SY * ta.SZ * nf * n;
-    if (need > p->part_cap) {
-        dfree(p, p->d_part);
-        p->d_part = dalloc<double>(p, need);
-        p->part_cap = need;
-    }
-    InterpArgs a{ta, p->d_fields, p->d_z, p->d_wcc, p->d_scal, p->d_far,
-                 n, nf, p->d_part};
-    dim3 grid(p->ss.nbx, p->ss.nby, (p->Nz + INTERP_TZ - 1) / INTERP_TZ);
-    static bool attr = false;
-    if (!attr) {
-        SE_CUDA(cudaFuncSetAttribute(interp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(InterpSmem<4>)));
-        SE_CUDA(cudaFuncSetAttribute(interp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(InterpSmem<1>)));
-        attr = true;
+    const int TB = 256;
+    const int nbx = (p->Nx + IBIN - 1) / IBIN, nby = (p->Ny + IBIN - 1) / IBIN;
+    const int nbins = nbx * nby;
+    const int zb = zbits_for(p->Nz);
+    int end_bit = zb;
+    while (end_bit < 32 && ((uint64_t)nbins >> (end_bit - zb)) != 0) ++end_bit;
+    if (((uint64_t)nbins << zb) >> 32)
+        throw Error(SE_ERR_VALUE, "grid too large for the interpolation sort keys");
+    ensure_sources(p, n);               // key / permutation / sort scratch (>= 3n)
+    const int64_t gcap = count / IG + nbins + 1;
+    if (nbins + 1 > p->iseg_cap || gcap > p->igroup_cap) {
+        dfree(p, p->d_iseg); dfree(p, p->d_igroups); dfree(p, p->d_ingroups);
+        p->d_iseg = dalloc<int64_t>(p, nbins + 1);
+        p->d_igroups = dalloc<int2>(p, gcap);
+        p->d_ingroups = dalloc<int>(p, 1);
+        p->iseg_cap = nbins + 1;
+        p->igroup_cap = gcap;
     }
     p->ktic(2);
-    if (forces) interp_kernel<4><<<grid, 256, sizeof(InterpSmem<4>), p->stream>>>(a);
-    else interp_kernel<1><<<grid, 256, sizeof(InterpSmem<1>), p->stream>>>(a);
+    ChargeKeyArgs ka{p->d_pos_cur, first, count, p->d_z, p->Nz, p->hx, p->hy, p->rad,
+                     p->Nx, p->Ny, nbx, zb, p->d_keys, p->d_perm};
+    charge_keys_kernel<<<(unsigned)((count + TB - 1) / TB), TB, 0, p->stream>>>(ka);
     SE_LAUNCHED(p);
-    PartArgs pa{p->d_part, p->d_far, n, nf, nullptr, nullptr, nullptr, nullptr, nullptr,
-                p->mx, p->my, p->Nx, p->Ny, INTERP_TZ, ta.SX, ta.SY};
-    interp_reduce_kernel<<<(unsigned)((count + 255) / 256), 256, 0, p->stream>>>(
-        pa, p->d_pos_cur, p->d_z, p->Nz, p->hx, p->hy, p->rad, first, count);
+    size_t bytes = p->cub_bytes;
+    SE_CUDA(cub::DeviceRadixSort::SortPairs(p->d_cub, bytes, p->d_keys, p->d_keys2,
+                                            p->d_perm, p->d_perm2, (int)count, 0, end_bit,
+                                            p->stream));
+    segment_offsets_kernel<<<(unsigned)((count + 1 + TB - 1) / TB), TB, 0, p->stream>>>(
+        p->d_keys2, count, zb, nbins, p->d_iseg);
+    SE_LAUNCHED(p);
+    charge_groups_kernel<<<1, 1024, 0, p->stream>>>(p->d_iseg, nbins, p->d_igroups,
+                                                    p->d_ingroups);
+    SE_LAUNCHED(p);
+    InterpArgs a{p->d_fields, p->d_pos_cur, p->d_z, p->d_wcc, p->d_scal, p->d_perm2,
+                 p->d_igroups, p->d_ingroups, p->Nx, p->Ny, p->Nz, p->NXY, p->hx, p->hy,
+                 p->rad, p->rad_keep, p->width, p->norm, p->mx, p->my, p->d_far, n};
+    const int smem = IWARPS * IG * (2 * p->mx + 1 + 2 * p->my + 1 + IZC) * (int)sizeof(double);
+    if (smem > 200 * 1024) throw Error(SE_ERR_VALUE, "stencil too wide for the interpolation");
+    SE_CUDA(cudaFuncSetAttribute(interp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SE_CUDA(cudaFuncSetAttribute(interp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const unsigned blocks = (unsigned)((gcap + IWARPS - 1) / IWARPS);
+    if (forces) interp_kernel<4><<<blocks, IWARPS * 32, smem, p->stream>>>(a);
+    else interp_kernel<1><<<blocks, IWARPS * 32, smem, p->stream>>>(a);
     p->ktoc(2);
     SE_LAUNCHED(p);
 }

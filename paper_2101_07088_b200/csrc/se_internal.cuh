@@ -208,8 +208,10 @@ struct Plan {
     double* d_phi = nullptr;              // [N]
     double* d_E = nullptr;                // [N][3]
     double* d_far = nullptr;              // [4][N] interp sums
-    double* d_part = nullptr;             // interp per-tile partials
-    int64_t part_cap = 0;
+    int64_t* d_iseg = nullptr;            // interp: sorted charges per 4x4 bin
+    int2* d_igroups = nullptr;            // interp: (first sorted index, count)
+    int* d_ingroups = nullptr;
+    int64_t iseg_cap = 0, igroup_cap = 0;
     const double* d_pos_cur = nullptr;    // positions of the solve in flight
     double* d_near = nullptr;             // [4][N] near sums
     double* d_scal = nullptr;             // device scalars (A_i, B_i, U, ...)
