@@ -37,6 +37,7 @@ __device__ __forceinline__ int pmod_i(int a, int n) { int r = a % n; return r < 
 // ---------------------------------------------------------------------------
 // cell list
 // ---------------------------------------------------------------------------
+// xy columns of width >= r/2 (r = max query radius), z bins of ~r/8
 struct CellGeo {
     int ncx, ncy, ncz;
     double csx, csy, csz, zlo, Lx, Ly;
@@ -47,6 +48,7 @@ __device__ __forceinline__ double wrap(double x, double L) {
     return (w >= L) ? 0.0 : w;
 }
 
+// cell = (xy column, z bin); a column's z bins are contiguous in the sort
 __device__ __forceinline__ int cell_of(const CellGeo& g, double x, double y, double z,
                                        int* cx, int* cy, int* cz) {
     int ix = (int)(wrap(x, g.Lx) / g.csx); if (ix >= g.ncx) ix = g.ncx - 1;
@@ -54,7 +56,7 @@ __device__ __forceinline__ int cell_of(const CellGeo& g, double x, double y, dou
     double fz = floor((z - g.zlo) / g.csz);
     int iz = fz < 0 ? 0 : (fz >= g.ncz ? g.ncz - 1 : (int)fz);
     *cx = ix; *cy = iy; *cz = iz;
-    return (iz * g.ncy + iy) * g.ncx + ix;
+    return (iy * g.ncx + ix) * g.ncz + iz;
 }
 
 struct SrcBuild {
@@ -137,6 +139,7 @@ struct NearArgs {
     float r2close;                // fp32 bound below which a pair may need the
                                   // general (close) path
     float Lxf, Lyf, iLxf, iLyf;
+    float zmarg;                  // fp32 z-window margin
     double* out; int64_t out_stride;   // out[c * stride + i]
     int64_t* npairs;
     void* stats;
@@ -310,6 +313,43 @@ __device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) 
 constexpr int MAXNB = 27;
 constexpr int SCAN_Q = 16;                  // per-lane staging before a flush
 
+// Neighbour columns of a target column and the candidate range of one lane
+// in one of them: columns whose xy distance to the target exceeds the query
+// radius are skipped, and the z window is the chord sqrt(r^2 - d_xy^2).
+struct ColumnWalk {
+    int nxr, nyr;          // columns visited per axis (5, or all when fewer)
+    bool allx, ally;
+};
+
+__device__ __forceinline__ ColumnWalk column_walk(const CellGeo& g) {
+    ColumnWalk w;
+    w.allx = g.ncx < 5; w.ally = g.ncy < 5;
+    w.nxr = w.allx ? g.ncx : 5; w.nyr = w.ally ? g.ncy : 5;
+    return w;
+}
+
+// neighbour column (i) of target column c along one axis: wrapped index, the
+// shift that brings its sources next to the target, and the fp32 distance
+// from the target coordinate p to the column's interval
+__device__ __forceinline__ void column_axis(int c, int i, bool all, int n, float cs, float L,
+                                           float p, int* idx, float* shift, float* dist) {
+    if (all) {                         // every column once, periodic distance
+        *idx = i; *shift = 0.f;
+        const float lo = i * cs, hi = lo + cs;
+        float d = fmaxf(0.f, fmaxf(lo - p, p - hi));
+        d = fminf(d, fmaxf(0.f, fmaxf(lo + L - p, p - (hi + L))));
+        d = fminf(d, fmaxf(0.f, fmaxf(lo - L - p, p - (hi - L))));
+        *dist = d;
+        return;
+    }
+    const int u = c + i - 2;
+    int w = u; float sh = 0.f;
+    if (w < 0) { w += n; sh = -L; } else if (w >= n) { w -= n; sh = L; }
+    *idx = w; *shift = sh;
+    const float lo = u * cs, hi = lo + cs;
+    *dist = fmaxf(0.f, fmaxf(lo - p, p - hi));
+}
+
 __global__ void __launch_bounds__(NB_THREADS) near_scan_kernel(NearArgs a) {
     constexpr int W = NB_THREADS / 32;
     __shared__ int qf[W][SCAN_Q + 4][32];
@@ -318,9 +358,9 @@ __global__ void __launch_bounds__(NB_THREADS) near_scan_kernel(NearArgs a) {
     const int64_t task = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
     if (task >= a.ntask || task >= *a.ntask_dev) return;
     const int2 tk = a.tasks[task];
-    const int cell = tk.x;
+    const int col = tk.x;
     const int64_t slot = (int64_t)tk.y + lane;
-    const bool live = slot < a.pt_end[cell];
+    const bool live = slot < a.pt_end[col];
     const int64_t i = live ? a.order[slot] : 0;
     float pxf = 0.f, pyf = 0.f, pzf = 0.f;
     if (live) {
@@ -328,11 +368,11 @@ __global__ void __launch_bounds__(NB_THREADS) near_scan_kernel(NearArgs a) {
         pyf = (float)wrap(a.eval[3 * i + 1], a.g.Ly);
         pzf = (float)(a.eval[3 * i + 2] - a.g.zlo);
     }
-    const int cx = cell % a.g.ncx, cy = (cell / a.g.ncx) % a.g.ncy, cz = cell / (a.g.ncx * a.g.ncy);
-    const float r2f = live ? a.r2f : -1.0f;
-    const float r2c = a.r2close;
-    const bool wx = a.g.ncx < 3, wy = a.g.ncy < 3;
-    const int nxr = wx ? a.g.ncx : 3, nyr = wy ? a.g.ncy : 3;
+    const int cx = col % a.g.ncx, cy = col / a.g.ncx;
+    const ColumnWalk cw = column_walk(a.g);
+    const float r2f = a.r2f, r2c = a.r2close;
+    const float csxf = (float)a.g.csx, csyf = (float)a.g.csy, icsz = (float)(1.0 / a.g.csz);
+    const int nzb = a.g.ncz;
     int* lfar = a.list_far + (int64_t)(slot < a.ne ? slot : 0) * a.cap_far;
     int* lcls = a.list_close + (int64_t)(slot < a.ne ? slot : 0) * a.cap_close;
     int nf = 0, nc = 0, qn = 0, qc = 0;
@@ -353,45 +393,43 @@ __global__ void __launch_bounds__(NB_THREADS) near_scan_kernel(NearArgs a) {
         for (int e = m; e < cnt; ++e) q[e - m][lane] = q[e][lane];
         cnt -= m;
     };
-    for (int dzi = 0; dzi < 3; ++dzi) {
-        const int zc = cz + dzi - 1;
-        if (zc < 0 || zc >= a.g.ncz) continue;
-        for (int dyi = 0; dyi < nyr; ++dyi) {
-            int yc = wy ? dyi : cy + dyi - 1;
-            float sy = 0.f;
-            if (!wy) {
-                if (yc < 0) { yc += a.g.ncy; sy = -a.Lyf; } else if (yc >= a.g.ncy) { yc -= a.g.ncy; sy = a.Lyf; }
+    for (int iy = 0; iy < cw.nyr; ++iy) {
+        int yc; float sy, dyd;
+        column_axis(cy, iy, cw.ally, a.g.ncy, csyf, a.Lyf, pyf, &yc, &sy, &dyd);
+        for (int ix = 0; ix < cw.nxr; ++ix) {
+            int xc; float sx, dxd;
+            column_axis(cx, ix, cw.allx, a.g.ncx, csxf, a.Lxf, pxf, &xc, &sx, &dxd);
+            const float d2 = fmaf(dxd, dxd, dyd * dyd);
+            int j = 0, e = 0;
+            if (live && d2 <= r2f) {
+                const float hz = sqrtf(r2f - d2) * 1.0001f + a.zmarg;
+                const int z0 = max(0, min(nzb - 1, (int)floorf((pzf - hz) * icsz)));
+                const int z1 = max(0, min(nzb - 1, (int)floorf((pzf + hz) * icsz)));
+                const int base = (yc * a.g.ncx + xc) * nzb;
+                j = a.start[base + z0];
+                e = a.start[base + z1 + 1];
             }
-            // the three x-neighbours of a row are contiguous in the sort order
-            // unless the row wraps: walk them cell by cell
-            for (int dxi = 0; dxi < nxr; ++dxi) {
-                int xc = wx ? dxi : cx + dxi - 1;
-                float sx = 0.f;
-                if (!wx) {
-                    if (xc < 0) { xc += a.g.ncx; sx = -a.Lxf; } else if (xc >= a.g.ncx) { xc -= a.g.ncx; sx = a.Lxf; }
-                }
-                const int c = (zc * a.g.ncy + yc) * a.g.ncx + xc;
-                const int b = a.start[c], e = a.start[c + 1];
-                const float qx = pxf - sx, qy = pyf - sy;
-                int j = b;
-                for (; j < e; j += 4) {
+            if (!__any_sync(0xffffffffu, j < e)) continue;
+            const float qx = pxf - sx, qy = pyf - sy;
+            for (;;) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        if (j + u < e) {
-                            const float4 f = a.srcf[j + u];
-                            float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
-                            if (wx) dx -= a.Lxf * rintf(dx * a.iLxf);
-                            if (wy) dy -= a.Lyf * rintf(dy * a.iLyf);
-                            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                            if (r2 <= r2f) {
-                                if (r2 > r2c) qf[wib][qn++][lane] = j + u;
-                                else qcl[wib][qc++][lane] = j + u;
-                            }
+                for (int u = 0; u < 4; ++u) {
+                    if (j + u < e) {
+                        const float4 f = a.srcf[j + u];
+                        float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
+                        if (cw.allx) dx -= a.Lxf * rintf(dx * a.iLxf);
+                        if (cw.ally) dy -= a.Lyf * rintf(dy * a.iLyf);
+                        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                        if (r2 <= r2f) {
+                            if (r2 > r2c) qf[wib][qn++][lane] = j + u;
+                            else qcl[wib][qc++][lane] = j + u;
                         }
                     }
-                    if (__any_sync(0xffffffffu, qn >= SCAN_Q)) flush(qf[wib], qn, nf, lfar, a.cap_far, false);
-                    if (__any_sync(0xffffffffu, qc >= SCAN_Q)) flush(qcl[wib], qc, nc, lcls, a.cap_close, false);
                 }
+                j += 4;
+                if (__any_sync(0xffffffffu, qn >= SCAN_Q)) flush(qf[wib], qn, nf, lfar, a.cap_far, false);
+                if (__any_sync(0xffffffffu, qc >= SCAN_Q)) flush(qcl[wib], qc, nc, lcls, a.cap_close, false);
+                if (!__any_sync(0xffffffffu, j < e)) break;
             }
         }
     }
@@ -470,18 +508,105 @@ __global__ void __launch_bounds__(NB_THREADS, 6) near_eval_kernel(NearArgs a) {
     if (lane == 0 && a.npairs) atomicAdd((unsigned long long*)a.npairs, cnt);
 }
 
-// point tasks: per cell, ceil(count/32) warps
-__global__ void task_count_kernel(const int* pt_start, int ncell, int* ntask) {
-    int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncell) return;
-    ntask[c] = (pt_start[c + 1] - pt_start[c] + 31) >> 5;
+// A few evaluation points (the gauge origin): one CTA per point, the threads
+// stride over the 27 neighbour cells' sources with the exact test and the
+// general kernel, then a block reduction.  Avoids the sort / task / list
+// machinery whose single-warp scan is latency-bound for one point.
+constexpr int FEW_POINTS = 64;
+
+__global__ void __launch_bounds__(256) near_few_kernel(NearArgs a) {
+    __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1)];
+    __shared__ double red[4][8];
+    __shared__ unsigned long long redc[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < SE_ERFCX_NP * (SE_ERFCX_DEG + 1); e += blockDim.x)
+        tab[e] = (&se_erfcx_tab[0][0])[e];
+    __syncthreads();
+    const int64_t i = blockIdx.x;
+    const double px = a.eval[3 * i], py = a.eval[3 * i + 1], pz = a.eval[3 * i + 2];
+    int cx, cy, cz;
+    cell_of(a.g, px, py, pz, &cx, &cy, &cz);
+    const ColumnWalk cw = column_walk(a.g);
+    const float pxf = (float)wrap(px, a.g.Lx), pyf = (float)wrap(py, a.g.Ly);
+    const float pzf = (float)(pz - a.g.zlo);
+    const float csxf = (float)a.g.csx, csyf = (float)a.g.csy, icsz = (float)(1.0 / a.g.csz);
+    double phi = 0, ex = 0, ey = 0, ez = 0;
+    unsigned long long count = 0;
+    const double Lx = a.g.Lx, Ly = a.g.Ly;
+    for (int iy = 0; iy < cw.nyr; ++iy) {
+        int yc; float sy, dyd;
+        column_axis(cy, iy, cw.ally, a.g.ncy, csyf, a.Lyf, pyf, &yc, &sy, &dyd);
+        for (int ix = 0; ix < cw.nxr; ++ix) {
+            int xc; float sx, dxd;
+            column_axis(cx, ix, cw.allx, a.g.ncx, csxf, a.Lxf, pxf, &xc, &sx, &dxd);
+            const float d2 = fmaf(dxd, dxd, dyd * dyd);
+            if (d2 > a.r2f) continue;
+            const float hz = sqrtf(a.r2f - d2) * 1.0001f + a.zmarg;
+            const int z0 = max(0, min(a.g.ncz - 1, (int)floorf((pzf - hz) * icsz)));
+            const int z1 = max(0, min(a.g.ncz - 1, (int)floorf((pzf + hz) * icsz)));
+            const int base = (yc * a.g.ncx + xc) * a.g.ncz;
+            for (int j = a.start[base + z0] + tid; j < a.start[base + z1 + 1]; j += blockDim.x) {
+                const double4 sv = a.src[j];
+                const double dx = min_image(__dsub_rn(px, sv.x), Lx);
+                const double dy = min_image(__dsub_rn(py, sv.y), Ly);
+                const double dz = __dsub_rn(pz, sv.z);
+                const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                            __dmul_rn(dz, dz));
+                if (r2 <= a.r2max) {
+                    double g, coef;
+                    pair_terms<false>(a, tab, r2, g, coef);
+                    phi = fma(sv.w, g, phi);
+                    if (a.need_field) {
+                        const double cq = coef * sv.w;
+                        ex = fma(cq, dx, ex); ey = fma(cq, dy, ey); ez = fma(cq, dz, ez);
+                    }
+                    ++count;
+                }
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        phi += __shfl_xor_sync(0xffffffffu, phi, o);
+        ex += __shfl_xor_sync(0xffffffffu, ex, o);
+        ey += __shfl_xor_sync(0xffffffffu, ey, o);
+        ez += __shfl_xor_sync(0xffffffffu, ez, o);
+        count += __shfl_xor_sync(0xffffffffu, count, o);
+    }
+    if (lane == 0) {
+        red[0][warp] = phi; red[1][warp] = ex; red[2][warp] = ey; red[3][warp] = ez;
+        redc[warp] = count;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double v[4] = {0, 0, 0, 0};
+        unsigned long long cnt = 0;
+        for (int w = 0; w < 8; ++w) {
+            for (int c = 0; c < 4; ++c) v[c] += red[c][w];
+            cnt += redc[w];
+        }
+        a.out[i] = v[0];
+        if (a.need_field) {
+            a.out[a.out_stride + i] = v[1];
+            a.out[2 * a.out_stride + i] = v[2];
+            a.out[3 * a.out_stride + i] = v[3];
+        }
+        if (a.npairs) atomicAdd((unsigned long long*)a.npairs, cnt);
+    }
 }
 
-__global__ void task_fill_kernel(const int* pt_start, const int* toff, int ncell, int2* tasks,
-                                 int* pt_end) {
+// point tasks: per xy column, ceil(count/32) warps (points sorted by z
+// within the column, so a warp's z windows overlap)
+__global__ void task_count_kernel(const int* pt_start, int ncol, int nzb, int* ntask) {
     int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncell) return;
-    int b = pt_start[c], e = pt_start[c + 1];
+    if (c >= ncol) return;
+    ntask[c] = (pt_start[(c + 1) * nzb] - pt_start[c * nzb] + 31) >> 5;
+}
+
+__global__ void task_fill_kernel(const int* pt_start, const int* toff, int ncol, int nzb,
+                                 int2* tasks, int* pt_end) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncol) return;
+    int b = pt_start[c * nzb], e = pt_start[(c + 1) * nzb];
     pt_end[c] = e;
     int o = toff[c];
     for (int f = b; f < e; f += 32) tasks[o++] = make_int2(c, f);
@@ -620,14 +745,16 @@ void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n) {
     SE_CUDA(cudaStreamSynchronize(p->stream));
     double zmin = 1e300, zmax = -1e300;
     for (int b = 0; b < nblk; ++b) { zmin = std::min(zmin, mm[2 * b]); zmax = std::max(zmax, mm[2 * b + 1]); }
+    // xy columns >= rc/2 wide (the 5 x 5 neighbour columns cover rc), z bins
+    // ~rc/8 high (the z window of a column is cut to whole bins)
     const double rc = std::max(p->P.r_cut, p->P.r_nf);
-    cl.ncx = std::max(1, (int)std::floor(p->P.Lx / rc));
-    cl.ncy = std::max(1, (int)std::floor(p->P.Ly / rc));
+    cl.ncx = std::max(1, (int)std::floor(p->P.Lx / (0.5 * rc)));
+    cl.ncy = std::max(1, (int)std::floor(p->P.Ly / (0.5 * rc)));
     cl.csx = p->P.Lx / cl.ncx;
     cl.csy = p->P.Ly / cl.ncy;
     cl.zlo = zmin - rc;
     double zspan = (zmax + rc) - cl.zlo;
-    cl.ncz = std::max(1, (int)std::floor(zspan / rc));
+    cl.ncz = std::max(1, (int)std::floor(zspan / (0.125 * rc)));
     cl.csz = zspan / cl.ncz;
     int64_t ncell = (int64_t)cl.ncx * cl.ncy * cl.ncz;
     if (ncell > (1 << 26)) throw Error(SE_ERR_VALUE, "near-field cell grid too large");
@@ -682,6 +809,7 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     a.r2close = (float)(rcl * rcl);
     a.Lxf = (float)p->P.Lx; a.Lyf = (float)p->P.Ly;
     a.iLxf = (float)(1.0 / p->P.Lx); a.iLyf = (float)(1.0 / p->P.Ly);
+    a.zmarg = (float)(1e-6 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(p->cl.zlo)));
     a.out = d_out4; a.out_stride = ne;
     a.npairs = d_npairs;
     if (p->cl.n == 0) {
@@ -689,10 +817,16 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
                                 p->stream));
         return;
     }
+    if (ne <= FEW_POINTS) {
+        near_few_kernel<<<(unsigned)ne, 256, 0, p->stream>>>(a);
+        SE_LAUNCHED(p);
+        return;
+    }
     // sort the evaluation points by cell and cut them into one-cell warp tasks
     const int ncell = p->cl.ncx * p->cl.ncy * p->cl.ncz;
+    const int ncol = p->cl.ncx * p->cl.ncy;
     NearScratch& ns = p->ns;
-    const int64_t tcap = ne / 32 + ncell + 1;
+    const int64_t tcap = ne / 32 + ncol + 1;
     if (ne > ns.pcap || ncell + 1 > ns.ccap || tcap > ns.tcap) {
         void* olds[] = {ns.keys, ns.keys2, ns.perm, ns.order, ns.pstart, ns.pend, ns.tcount,
                         ns.toff, ns.tasks, ns.cub};
@@ -730,19 +864,20 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     point_starts_kernel<<<(unsigned)((ne + 1 + 255) / 256), 256, 0, p->stream>>>(ns.keys2, ne,
                                                                                   ncell, ns.pstart);
     SE_LAUNCHED(p);
-    task_count_kernel<<<(ncell + 255) / 256, 256, 0, p->stream>>>(ns.pstart, ncell, ns.tcount);
+    const int nzb = p->cl.ncz;
+    task_count_kernel<<<(ncol + 255) / 256, 256, 0, p->stream>>>(ns.pstart, ncol, nzb, ns.tcount);
     SE_LAUNCHED(p);
-    SE_CUDA(cudaMemsetAsync(ns.tcount + ncell, 0, sizeof(int), p->stream));
+    SE_CUDA(cudaMemsetAsync(ns.tcount + ncol, 0, sizeof(int), p->stream));
     bytes = ns.cub_bytes;
-    SE_CUDA(cub::DeviceScan::ExclusiveSum(ns.cub, bytes, ns.tcount, ns.toff, ncell + 1,
+    SE_CUDA(cub::DeviceScan::ExclusiveSum(ns.cub, bytes, ns.tcount, ns.toff, ncol + 1,
                                           p->stream));
-    task_fill_kernel<<<(ncell + 255) / 256, 256, 0, p->stream>>>(ns.pstart, ns.toff, ncell,
-                                                                 ns.tasks, ns.pend);
+    task_fill_kernel<<<(ncol + 255) / 256, 256, 0, p->stream>>>(ns.pstart, ns.toff, ncol, nzb,
+                                                                ns.tasks, ns.pend);
     SE_LAUNCHED(p);
     a.order = ns.order;
     a.tasks = ns.tasks;
     a.pt_end = ns.pend;
-    a.ntask_dev = ns.toff + ncell;
+    a.ntask_dev = ns.toff + ncol;
     a.ntask = tcap;
     const unsigned nblk = (unsigned)((tcap * 32 + NB_THREADS - 1) / NB_THREADS);
     // pair-list capacities from the expected neighbour count (+ margin);
