@@ -137,59 +137,62 @@ struct StencilArgs {
     Stencils st;
 };
 
-__global__ void stencil_kernel(StencilArgs a) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= a.total) return;
-    if ((a.keys[i] >> a.zbits) >= a.invalid_major) return;
-    int s = a.perm[i];
-    double4 v = a.src[s];
-    double* rec = a.st.rec + i * a.st.rs;
-    // x axis: j0 = floor(x/h); delta = x - (j0+off)*h; keep |delta| <= r(1+1e-12)
-    long long jx = (long long)floor(v.x / a.hx);
-    for (int o = 0; o <= 2 * a.mx; ++o) {
-        double xj = __dmul_rn((double)(jx + o - a.mx), a.hx);
-        double d = __dsub_rn(v.x, xj);
-        double wt = 0.0;
-        if (fabs(d) <= a.rad_keep) {
-            double t = d / a.width;
-            wt = exp(-0.5 * (t * t)) / a.norm;
-        }
-        rec[o] = wt;
-    }
-    rec += 2 * a.mx + 1;
-    long long jy = (long long)floor(v.y / a.hy);
-    for (int o = 0; o <= 2 * a.my; ++o) {
-        double yj = __dmul_rn((double)(jy + o - a.my), a.hy);
-        double d = __dsub_rn(v.y, yj);
-        double wt = 0.0;
-        if (fabs(d) <= a.rad_keep) {
-            double t = d / a.width;
-            wt = exp(-0.5 * (t * t)) / a.norm;
-        }
-        rec[o] = wt;
-    }
-    rec += 2 * a.my + 1;
-    // z axis: nodes in [searchsorted(z-r, left), searchsorted(z+r, right))
-    int lo = lower_bound_d(a.znodes, a.Nz, __dsub_rn(v.z, a.rad));
-    int hi = upper_bound_d(a.znodes, a.Nz, __dadd_rn(v.z, a.rad));
-    for (int t = 0; t < a.wz; ++t) {
-        int k = lo + t;
-        double wt = 0.0;
-        if (k < hi && k < a.Nz) {
-            double d = __dsub_rn(v.z, a.znodes[k]);
-            if (fabs(d) <= a.rad) {
-                double u = d / a.width;
-                wt = exp(-0.5 * (u * u)) / a.norm;
+// One thread per source; the block's records (contiguous in the sorted
+// order) are assembled in shared memory and written out coalesced.
+constexpr int STENCIL_TB = 64;
+
+__global__ void __launch_bounds__(STENCIL_TB) stencil_kernel(StencilArgs a) {
+    extern __shared__ double srec[];             // [STENCIL_TB][rs + 1]
+    const int t = threadIdx.x;
+    const int64_t i0 = blockIdx.x * (int64_t)STENCIL_TB;
+    const int64_t i = i0 + t;
+    const int rs = a.st.rs, ld = rs + 1;
+    const int nblk = (int)(a.total - i0 < STENCIL_TB ? a.total - i0 : STENCIL_TB);
+    double* my = srec + t * ld;
+    if (t < nblk) {
+        for (int e = 0; e < rs; ++e) my[e] = 0.0;
+        if ((a.keys[i] >> a.zbits) < a.invalid_major) {
+            const int s = a.perm[i];
+            const double4 v = a.src[s];
+            // x axis: j0 = floor(x/h); delta = x - (j0+off)*h; keep |delta| <= r(1+1e-12)
+            const long long jx = (long long)floor(v.x / a.hx);
+            for (int o = 0; o <= 2 * a.mx; ++o) {
+                const double xj = __dmul_rn((double)(jx + o - a.mx), a.hx);
+                const double d = __dsub_rn(v.x, xj);
+                if (fabs(d) <= a.rad_keep) { const double u = d / a.width; my[o] = exp(-0.5 * (u * u)) / a.norm; }
             }
+            double* ry = my + 2 * a.mx + 1;
+            const long long jy = (long long)floor(v.y / a.hy);
+            for (int o = 0; o <= 2 * a.my; ++o) {
+                const double yj = __dmul_rn((double)(jy + o - a.my), a.hy);
+                const double d = __dsub_rn(v.y, yj);
+                if (fabs(d) <= a.rad_keep) { const double u = d / a.width; ry[o] = exp(-0.5 * (u * u)) / a.norm; }
+            }
+            double* rz = ry + 2 * a.my + 1;
+            // z axis: nodes in [searchsorted(z-r, left), searchsorted(z+r, right))
+            const int lo = lower_bound_d(a.znodes, a.Nz, __dsub_rn(v.z, a.rad));
+            const int hi = upper_bound_d(a.znodes, a.Nz, __dadd_rn(v.z, a.rad));
+            for (int tt = 0; tt < a.wz; ++tt) {
+                const int k = lo + tt;
+                if (k < hi && k < a.Nz) {
+                    const double d = __dsub_rn(v.z, a.znodes[k]);
+                    if (fabs(d) <= a.rad) { const double u = d / a.width; rz[tt] = exp(-0.5 * (u * u)) / a.norm; }
+                }
+            }
+            a.st.j0x[i] = (int)jx;
+            a.st.j0y[i] = (int)jy;
+            a.st.lo[i] = lo;
+            a.st.hi[i] = hi < lo + a.wz ? hi : lo + a.wz;
+            a.st.q[i] = v.w;
+            a.st.owner[i] = a.owner_in[s];
         }
-        rec[t] = wt;
     }
-    a.st.j0x[i] = (int)jx;
-    a.st.j0y[i] = (int)jy;
-    a.st.lo[i] = lo;
-    a.st.hi[i] = hi < lo + a.wz ? hi : lo + a.wz;
-    a.st.q[i] = v.w;
-    a.st.owner[i] = a.owner_in[s];
+    __syncthreads();
+    double* out = a.st.rec + i0 * rs;
+    for (int e = t; e < nblk * rs; e += STENCIL_TB) {
+        const int r = e / rs, c = e - r * rs;
+        out[e] = srec[r * ld + c];
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -456,7 +459,7 @@ __global__ void __launch_bounds__(256, 2) spread_kernel(SpreadArgs a) {
 // are separable and added analytically.  The per-charge sums are reduced
 // across the warp and written once: no atomics, no partial buffers.
 // ---------------------------------------------------------------------------
-constexpr int IG = 4;            // charges per warp group
+constexpr int IG_MAX = 8;        // charges per warp group (template IG <= IG_MAX)
 constexpr int IBIN = 4;          // xy bin width (columns)
 constexpr int IZC = 32;          // z nodes per weight-table chunk
 constexpr int IWARPS = 8;
@@ -483,7 +486,7 @@ __global__ void charge_keys_kernel(ChargeKeyArgs a) {
 // groups of <= IG consecutive sorted charges within each bin: one block,
 // each thread a contiguous run of bins, block-wide exclusive scan
 __global__ void __launch_bounds__(1024) charge_groups_kernel(const int64_t* seg, int nbins,
-                                                            int2* groups, int* ngroups) {
+                                                            int IG, int2* groups, int* ngroups) {
     typedef cub::BlockScan<int, 1024> Scan;
     __shared__ typename Scan::TempStorage tmp;
     const int per = (nbins + 1023) / 1024;
@@ -511,13 +514,13 @@ struct InterpArgs {
 };
 
 struct GroupInfo {
-    double x[IG], y[IG], z[IG];
-    long long jx[IG], jy[IG];
-    int jxw[IG], jyw[IG], lo[IG], hi[IG], idx[IG];
+    double x[IG_MAX], y[IG_MAX], z[IG_MAX];
+    long long jx[IG_MAX], jy[IG_MAX];
+    int jxw[IG_MAX], jyw[IG_MAX], lo[IG_MAX], hi[IG_MAX], idx[IG_MAX];
 };
 
-template <int NF>
-__global__ void __launch_bounds__(IWARPS * 32) interp_kernel(InterpArgs a) {
+template <int NF, int IG, int MINB>
+__global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgs a) {
     extern __shared__ __align__(16) double ism[];
     __shared__ GroupInfo ginfo[IWARPS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -662,10 +665,10 @@ __global__ void __launch_bounds__(IWARPS * 32) interp_kernel(InterpArgs a) {
     // analytic k = 0 terms: sum_nodes W * (A_i z) and W * A_i
     const double A_i = a.scal[0];
     const int src = lane / NF;
-    const double Sx = __shfl_sync(0xffffffffu, sx, src & (IG - 1));
-    const double Sy = __shfl_sync(0xffffffffu, sy, src & (IG - 1));
-    const double Sz0 = __shfl_sync(0xffffffffu, sz0, src & (IG - 1));
-    const double Sz1 = __shfl_sync(0xffffffffu, sz1, src & (IG - 1));
+    const double Sx = __shfl_sync(0xffffffffu, sx, src % IG);
+    const double Sy = __shfl_sync(0xffffffffu, sy, src % IG);
+    const double Sz0 = __shfl_sync(0xffffffffu, sz0, src % IG);
+    const double Sz1 = __shfl_sync(0xffffffffu, sz1, src % IG);
     if (lane < IG * NF && src < cnt) {
         const int c = lane - src * NF;
         double v = mine;
@@ -837,7 +840,11 @@ void build_sources(Plan* p, const double* d_pos, int64_t first, int64_t n, bool 
         StencilArgs sta{p->d_src, p->d_src_owner, p->d_perm2, keys2, (uint32_t)nseg,
                         zb, total, p->d_z, p->Nz, p->hx, p->hy, p->rad,
                         p->rad_keep, p->width, p->norm, p->mx, p->my, p->wz_max, st};
-        stencil_kernel<<<(unsigned)((total + TB - 1) / TB), TB, 0, p->stream>>>(sta);
+        const int smem = STENCIL_TB * (st.rs + 1) * (int)sizeof(double);
+        if (smem > 48 * 1024)
+            SE_CUDA(cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        stencil_kernel<<<(unsigned)((total + STENCIL_TB - 1) / STENCIL_TB), STENCIL_TB, smem,
+                         p->stream>>>(sta);
         SE_LAUNCHED(p);
     }
 }
@@ -882,7 +889,13 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
     if (((uint64_t)nbins << zb) >> 32)
         throw Error(SE_ERR_VALUE, "grid too large for the interpolation sort keys");
     ensure_sources(p, n);               // key / permutation / sort scratch (>= 3n)
-    const int64_t gcap = count / IG + nbins + 1;
+    static const int ig_env = [] {
+        const char* e = getenv("SE_INTERP_IG");
+        return e ? atoi(e) : 4;
+    }();
+    const int IG = (ig_env == 8) ? 8 : (ig_env == 5 ? 5 : 4);   // 5: IG 4, 3 blocks / SM
+    const int ig = IG == 5 ? 4 : IG;
+    const int64_t gcap = count / ig + nbins + 1;
     if (nbins + 1 > p->iseg_cap || gcap > p->igroup_cap) {
         dfree(p, p->d_iseg); dfree(p, p->d_igroups); dfree(p, p->d_ingroups);
         p->d_iseg = dalloc<int64_t>(p, nbins + 1);
@@ -903,19 +916,22 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
     segment_offsets_kernel<<<(unsigned)((count + 1 + TB - 1) / TB), TB, 0, p->stream>>>(
         p->d_keys2, count, zb, nbins, p->d_iseg);
     SE_LAUNCHED(p);
-    charge_groups_kernel<<<1, 1024, 0, p->stream>>>(p->d_iseg, nbins, p->d_igroups,
+    charge_groups_kernel<<<1, 1024, 0, p->stream>>>(p->d_iseg, nbins, ig, p->d_igroups,
                                                     p->d_ingroups);
     SE_LAUNCHED(p);
     InterpArgs a{p->d_fields, p->d_pos_cur, p->d_z, p->d_wcc, p->d_scal, p->d_perm2,
                  p->d_igroups, p->d_ingroups, p->Nx, p->Ny, p->Nz, p->NXY, p->hx, p->hy,
                  p->rad, p->rad_keep, p->width, p->norm, p->mx, p->my, p->d_far, n};
-    const int smem = IWARPS * IG * (2 * p->mx + 1 + 2 * p->my + 1 + IZC) * (int)sizeof(double);
+    const int smem = IWARPS * ig * (2 * p->mx + 1 + 2 * p->my + 1 + IZC) * (int)sizeof(double);
     if (smem > 200 * 1024) throw Error(SE_ERR_VALUE, "stencil too wide for the interpolation");
-    SE_CUDA(cudaFuncSetAttribute(interp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SE_CUDA(cudaFuncSetAttribute(interp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const unsigned blocks = (unsigned)((gcap + IWARPS - 1) / IWARPS);
-    if (forces) interp_kernel<4><<<blocks, IWARPS * 32, smem, p->stream>>>(a);
-    else interp_kernel<1><<<blocks, IWARPS * 32, smem, p->stream>>>(a);
+    auto go = [&](auto kern) {
+        SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        kern<<<blocks, IWARPS * 32, smem, p->stream>>>(a);
+    };
+    if (IG == 8) { if (forces) go(interp_kernel<4, 8, 1>); else go(interp_kernel<1, 8, 1>); }
+    else if (IG == 5) { if (forces) go(interp_kernel<4, 4, 3>); else go(interp_kernel<1, 4, 3>); }
+    else { if (forces) go(interp_kernel<4, 4, 1>); else go(interp_kernel<1, 4, 1>); }
     p->ktoc(2);
     SE_LAUNCHED(p);
 }

@@ -1,5 +1,5 @@
-"""Summarise an ncu --page source csv (cuda,sass): per-CUDA-line stall
-samples and executed instructions (top N)."""
+"""Per-CUDA-line stall samples and executed warp instructions from
+`ncu -i REP -k KERNEL --page source --csv --print-source cuda,sass`."""
 import csv
 import sys
 from collections import defaultdict
@@ -7,29 +7,25 @@ from collections import defaultdict
 path = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 rows = list(csv.reader(open(path)))
-hdr_i = next(i for i, r in enumerate(rows) if len(r) > 5 and r[0] == "Line No")
+hdr_i = next(i for i, r in enumerate(rows) if r and r[0] == "Line No")
 h = rows[hdr_i]
-src_lines = {}
-samp = defaultdict(float)
-inst = defaultdict(float)
+i_samp = h.index("Warp Stall Sampling (All Samples)")
+i_inst = h.index("Instructions Executed")
+samp, inst, src = defaultdict(float), defaultdict(float), {}
 cur = None
 for r in rows[hdr_i + 1:]:
-    if len(r) < 8:
+    if len(r) <= i_inst:
         continue
-    if r[0] and r[0].isdigit():
+    if r[0] and r[0].isdigit() and r[2] == "-":      # CUDA line summary row
         cur = int(r[0])
-        src_lines[cur] = r[1]
-    try:
-        s = float(r[4] or 0)
-        n = float(r[7] or 0)
-    except ValueError:
-        continue
-    if cur is not None:
-        samp[cur] += s
-        inst[cur] += n
-tot_s = sum(samp.values()) or 1
-tot_i = sum(inst.values()) or 1
-print("total samples %.0f  instructions %.3g" % (tot_s, tot_i))
-for ln, s in sorted(samp.items(), key=lambda x: -x[1])[:top]:
-    print("%5d  %5.1f%% samp  %5.1f%% inst  %s" % (ln, 100 * s / tot_s,
-          100 * inst[ln] / tot_i, src_lines.get(ln, "")[:90]))
+        src[cur] = r[1]
+        try:
+            samp[cur] += float(r[i_samp] or 0)
+            inst[cur] += float(r[i_inst] or 0)
+        except ValueError:
+            pass
+ts, ti = sum(samp.values()) or 1, sum(inst.values()) or 1
+print("total samples %.0f, warp instructions %.3e" % (ts, ti))
+for ln in sorted(samp, key=lambda k: -samp[k])[:top]:
+    print("%5d %5.1f%% samp %5.1f%% inst  %s" % (ln, 100 * samp[ln] / ts,
+                                               100 * inst[ln] / ti, src[ln][:90]))
