@@ -192,40 +192,88 @@ __device__ __forceinline__ void solve_mode(const BvpArgs& a, int64_t m, int g, d
         const double S00 = a.sinv[4 * u], S01 = a.sinv[4 * u + 1];
         const double S10 = a.sinv[4 * u + 2], S11 = a.sinv[4 * u + 3];
 
+        // Every sweep runs in chunks of CH rows: the chunk's loads (scratch
+        // rows, per-|k| factor rows) are issued together before its
+        // recurrence steps, so CH loads are in flight per thread instead of
+        // one (the stores of a chunk would otherwise serialise the loads of
+        // the next row through possible aliasing).
+        constexpr int CH = 4;
         // forward sweep (both parity chains interleaved): d_k = (r_k - lo_k d_{k-2}) / den_k
         // backward sweep: x_k = d_k - cp_k x_{k+2}; Schur rhs C.x     bvp.py:76-90,216-227
         auto descend = [&](double2& s0, double2& s1) {
             double2 xp1 = make_double2(0, 0), xp2 = make_double2(0, 0);
             s0 = make_double2(0, 0); s1 = make_double2(0, 0);
-#pragma unroll 8
-            for (int k = n - 1; k >= 0; --k) {
-                double2 d = B[(int64_t)k * RS];
-                double2 x = (k + 2 < n) ? cfma(-cp[k], xp2, d) : d;
-                B[(int64_t)k * RS] = x;
-                s0 = cfma(cr0[k], x, s0);
-                s1 = cfma(cr1[k], x, s1);
-                xp2 = xp1; xp1 = x;
+            for (int k0 = n - 1; k0 >= 0; k0 -= CH) {
+                double2 dv[CH]; double cpv[CH], c0r[CH], c1r[CH];
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int k = k0 - j;
+                    if (k >= 0) { dv[j] = B[(int64_t)k * RS]; cpv[j] = cp[k]; c0r[j] = cr0[k]; c1r[j] = cr1[k]; }
+                }
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int k = k0 - j;
+                    if (k >= 0) {
+                        const double2 x = (k + 2 < n) ? cfma(-cpv[j], xp2, dv[j]) : dv[j];
+                        B[(int64_t)k * RS] = x;
+                        s0 = cfma(c0r[j], x, s0);
+                        s1 = cfma(c1r[j], x, s1);
+                        xp2 = xp1; xp1 = x;
+                    }
+                }
+            }
+        };
+        // y'' = x - A^{-1}B c  (A += dy when accumulate)
+        auto update_a = [&](double2 v0, double2 v1, bool accumulate) {
+            for (int k0 = 0; k0 < n; k0 += CH) {
+                double2 bv[CH], av[CH]; double ab[CH];
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int k = k0 + j;
+                    if (k < n) {
+                        bv[j] = B[(int64_t)k * RS]; ab[j] = aib[k];
+                        if (accumulate) av[j] = A[(int64_t)k * RS];
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int k = k0 + j;
+                    if (k < n) {
+                        double2 y = cfma(-ab[j], (k & 1) ? v1 : v0, bv[j]);
+                        if (accumulate) y = cadd(av[j], y);
+                        A[(int64_t)k * RS] = y;
+                    }
+                }
             }
         };
         {
             double2 dm1 = make_double2(0, 0), dm2 = make_double2(0, 0);
-#pragma unroll 8
-            for (int k = 0; k < n; ++k) {
-                double2 r = fsc_at(k);
-                F[(int64_t)k * RS] = r;
-                double2 d = (k < 2) ? cscale(r, iv[k])
-                                    : cscale(cfma(k2 * q_lo[k], dm2, r), iv[k]);
-                B[(int64_t)k * RS] = d;
-                dm2 = dm1; dm1 = d;
+            for (int k0 = 0; k0 < n; k0 += CH) {
+                double2 rv[CH]; double ivv[CH];
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int k = k0 + j;
+                    if (k < n) { rv[j] = fsc_at(k); ivv[j] = iv[k]; }
+                }
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int k = k0 + j;
+                    if (k < n) {
+                        const double2 r = rv[j];
+                        F[(int64_t)k * RS] = r;
+                        const double2 d = (k < 2) ? cscale(r, ivv[j])
+                                                  : cscale(cfma(k2 * q_lo[k], dm2, r), ivv[j]);
+                        B[(int64_t)k * RS] = d;
+                        dm2 = dm1; dm1 = d;
+                    }
+                }
             }
         }
         double2 s0, s1;
         descend(s0, s1);                       // rhs2 = bc = 0
         c0v = make_double2(S00 * s0.x + S01 * s1.x, S00 * s0.y + S01 * s1.y);
         c1v = make_double2(S10 * s0.x + S11 * s1.x, S10 * s0.y + S11 * s1.y);
-#pragma unroll 8
-        for (int k = 0; k < n; ++k)
-            A[(int64_t)k * RS] = cfma(-aib[k], (k & 1) ? c1v : c0v, B[(int64_t)k * RS]);
+        update_a(c0v, c1v, false);
 
         for (int it = 0; it < a.refine; ++it) {     // bvp.py:229-246,268-273
             double2 yq_sum = make_double2(0, 0), yq_sgn = make_double2(0, 0);
@@ -234,28 +282,43 @@ __device__ __forceinline__ void solve_mode(const BvpArgs& a, int64_t m, int g, d
             double2 y0 = A[0];
             double2 yp1 = (n > 1) ? A[RS] : make_double2(0, 0);
             double2 dm1 = make_double2(0, 0), dm2 = make_double2(0, 0);
-#pragma unroll 8
-            for (int k = 0; k < n; ++k) {
-                double2 yp2 = (k + 2 < n) ? A[(int64_t)(k + 2) * RS] : make_double2(0, 0);
-                double2 yq = make_double2(0, 0), ye = make_double2(0, 0);
-                if (k > 0) {
-                    yq = cscale(y0, q_dg[k]);
-                    if (k >= 2) yq = cadd(yq, cscale(ym2, q_lo[k]));
-                    if (k + 2 < n) yq = cadd(yq, cscale(yp2, q_hi[k]));
-                    ye = cscale(ym1, e_lo[k]);
-                    if (k + 1 < n) ye = cadd(ye, cscale(yp1, e_hi[k]));
+            for (int k0 = 0; k0 < n; k0 += CH) {
+                double2 ap[CH], fv[CH]; double ivv[CH];
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int k = k0 + j;
+                    if (k < n) {
+                        ap[j] = (k + 2 < n) ? A[(int64_t)(k + 2) * RS] : make_double2(0, 0);
+                        fv[j] = F[(int64_t)k * RS];
+                        ivv[j] = iv[k];
+                    }
                 }
-                double2 r = csub(F[(int64_t)k * RS], csub(y0, cscale(yq, k2)));
-                if (k == 0) r = cadd(r, cscale(c0v, k2));
-                if (k == 1) r = cadd(r, cscale(c1v, k2));
-                yq_sum = cadd(yq_sum, yq); ye_sum = cadd(ye_sum, ye);
-                if (k & 1) { yq_sgn = csub(yq_sgn, yq); ye_sgn = csub(ye_sgn, ye); }
-                else { yq_sgn = cadd(yq_sgn, yq); ye_sgn = cadd(ye_sgn, ye); }
-                double2 d = (k < 2) ? cscale(r, iv[k])
-                                    : cscale(cfma(k2 * q_lo[k], dm2, r), iv[k]);
-                B[(int64_t)k * RS] = d;
-                dm2 = dm1; dm1 = d;
-                ym2 = ym1; ym1 = y0; y0 = yp1; yp1 = yp2;
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int k = k0 + j;
+                    if (k < n) {
+                        const double2 yp2 = ap[j];
+                        double2 yq = make_double2(0, 0), ye = make_double2(0, 0);
+                        if (k > 0) {
+                            yq = cscale(y0, q_dg[k]);
+                            if (k >= 2) yq = cadd(yq, cscale(ym2, q_lo[k]));
+                            if (k + 2 < n) yq = cadd(yq, cscale(yp2, q_hi[k]));
+                            ye = cscale(ym1, e_lo[k]);
+                            if (k + 1 < n) ye = cadd(ye, cscale(yp1, e_hi[k]));
+                        }
+                        double2 r = csub(fv[j], csub(y0, cscale(yq, k2)));
+                        if (k == 0) r = cadd(r, cscale(c0v, k2));
+                        if (k == 1) r = cadd(r, cscale(c1v, k2));
+                        yq_sum = cadd(yq_sum, yq); ye_sum = cadd(ye_sum, ye);
+                        if (k & 1) { yq_sgn = csub(yq_sgn, yq); ye_sgn = csub(ye_sgn, ye); }
+                        else { yq_sgn = cadd(yq_sgn, yq); ye_sgn = cadd(ye_sgn, ye); }
+                        const double2 d = (k < 2) ? cscale(r, ivv[j])
+                                                  : cscale(cfma(k2 * q_lo[k], dm2, r), ivv[j]);
+                        B[(int64_t)k * RS] = d;
+                        dm2 = dm1; dm1 = d;
+                        ym2 = ym1; ym1 = y0; y0 = yp1; yp1 = yp2;
+                    }
+                }
             }
             // r2 = bc - (C ypp + D c) with bc = 0
             double2 r20 = cscale(cadd(cadd(ye_sum, cscale(yq_sum, kap)),
@@ -267,11 +330,7 @@ __device__ __forceinline__ void solve_mode(const BvpArgs& a, int64_t m, int g, d
             t0 = csub(t0, r20); t1 = csub(t1, r21);
             double2 dc0 = make_double2(S00 * t0.x + S01 * t1.x, S00 * t0.y + S01 * t1.y);
             double2 dc1 = make_double2(S10 * t0.x + S11 * t1.x, S10 * t0.y + S11 * t1.y);
-#pragma unroll 8
-            for (int k = 0; k < n; ++k) {
-                double2 dy = cfma(-aib[k], (k & 1) ? dc1 : dc0, B[(int64_t)k * RS]);
-                A[(int64_t)k * RS] = cadd(A[(int64_t)k * RS], dy);
-            }
+            update_a(dc0, dc1, true);
             c0v = cadd(c0v, dc0);
             c1v = cadd(c1v, dc1);
         }
@@ -286,39 +345,50 @@ __device__ __forceinline__ void solve_mode(const BvpArgs& a, int64_t m, int g, d
     double2 ynext = make_double2(0, 0);                              // y_{k+1}
     double2* out_y = a.ext + 0 * M + m;
     double2* out_d = a.ext + 1 * M + m;
-    // sliding window of ypp: a_{k-2}, a_k, a_{k+2}
+    // sliding window of ypp: a_{k-2}, a_k, a_{k+2} (loads a chunk ahead)
+    constexpr int CHF = 8;
     double2 ap2 = make_double2(0, 0), ap1 = make_double2(0, 0);
     double2 a0 = A[(int64_t)(n - 1) * RS];
     double2 am1 = (n >= 2) ? A[(int64_t)(n - 2) * RS] : make_double2(0, 0);
-#pragma unroll 8
-    for (int k = n - 1; k >= 0; --k) {
-        double2 am2 = (k >= 2) ? A[(int64_t)(k - 2) * RS] : make_double2(0, 0);
-        double2 y = make_double2(0, 0);
-        if (k > 0) {
-            y = cscale(a0, q_dg[k]);
-            if (k >= 2) y = cadd(y, cscale(am2, q_lo[k]));
-            if (k + 2 < n) y = cadd(y, cscale(ap2, q_hi[k]));
+    for (int k0 = n - 1; k0 >= 0; k0 -= CHF) {
+        double2 amv[CHF];
+#pragma unroll
+        for (int j = 0; j < CHF; ++j) {
+            const int k = k0 - j;
+            amv[j] = (k >= 2) ? A[(int64_t)(k - 2) * RS] : make_double2(0, 0);
         }
-        if (k == 0) y = cadd(y, c0v);
-        if (k == 1) y = cadd(y, c1v);
-        double2 b;
-        if (k == n - 1) b = make_double2(0, 0);
-        else if (k == n - 2) b = cscale(ynext, 2.0 * (n - 1));
-        else b = cadd(bp2, cscale(ynext, 2.0 * (k + 1)));
-        double2 bs = cscale((k == 0) ? cscale(b, 0.5) : b, dscale);
-        w_y0 = cfma(a.tw0[k], y, w_y0);
-        w_yH = cfma(a.twH[k], y, w_yH);
-        w_d0 = cfma(a.tw0[k], bs, w_d0);
-        w_dH = cfma(a.twH[k], bs, w_dH);
-        d_sum = cadd(d_sum, bs);
-        d_sgn = (k & 1) ? csub(d_sgn, bs) : cadd(d_sgn, bs);
-        if (a.keep) a.keep[((int64_t)k * 2 + g) * M + m] = y;
-        if (emit) {                             // coefficients for the iDCT GEMM
-            out_y[(int64_t)k * RS] = y;
-            out_d[(int64_t)k * RS] = bs;
+#pragma unroll
+        for (int j = 0; j < CHF; ++j) {
+            const int k = k0 - j;
+            if (k < 0) break;
+            const double2 am2 = amv[j];
+            double2 y = make_double2(0, 0);
+            if (k > 0) {
+                y = cscale(a0, q_dg[k]);
+                if (k >= 2) y = cadd(y, cscale(am2, q_lo[k]));
+                if (k + 2 < n) y = cadd(y, cscale(ap2, q_hi[k]));
+            }
+            if (k == 0) y = cadd(y, c0v);
+            if (k == 1) y = cadd(y, c1v);
+            double2 b;
+            if (k == n - 1) b = make_double2(0, 0);
+            else if (k == n - 2) b = cscale(ynext, 2.0 * (n - 1));
+            else b = cadd(bp2, cscale(ynext, 2.0 * (k + 1)));
+            const double2 bs = cscale((k == 0) ? cscale(b, 0.5) : b, dscale);
+            w_y0 = cfma(a.tw0[k], y, w_y0);
+            w_yH = cfma(a.twH[k], y, w_yH);
+            w_d0 = cfma(a.tw0[k], bs, w_d0);
+            w_dH = cfma(a.twH[k], bs, w_dH);
+            d_sum = cadd(d_sum, bs);
+            d_sgn = (k & 1) ? csub(d_sgn, bs) : cadd(d_sgn, bs);
+            if (a.keep) a.keep[((int64_t)k * 2 + g) * M + m] = y;
+            if (emit) {                             // coefficients for the iDCT GEMM
+                out_y[(int64_t)k * RS] = y;
+                out_d[(int64_t)k * RS] = bs;
+            }
+            bp2 = bp1; bp1 = b; ynext = y;
+            ap2 = ap1; ap1 = a0; a0 = am1; am1 = am2;
         }
-        bp2 = bp1; bp1 = b; ynext = y;
-        ap2 = ap1; ap1 = a0; a0 = am1; am1 = am2;
     }
     wv[0] = w_y0; wv[1] = w_yH; wv[2] = w_d0; wv[3] = w_dH;
     ends[0] = d_sgn; ends[1] = d_sum;
