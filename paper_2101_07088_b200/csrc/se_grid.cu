@@ -189,7 +189,13 @@ __global__ void __launch_bounds__(STENCIL_TB) stencil_kernel(StencilArgs a) {
     }
     __syncthreads();
     double* out = a.st.rec + i0 * rs;
-    for (int e = t; e < nblk * rs; e += STENCIL_TB) {
+    // rows of invalid slots (sorted to the end) are never read: skip them
+    __shared__ int nvalid;
+    if (t == 0) nvalid = 0;
+    __syncthreads();
+    if (t < nblk && (a.keys[i] >> a.zbits) < a.invalid_major) atomicMax(&nvalid, t + 1);
+    __syncthreads();
+    for (int e = t; e < nvalid * rs; e += STENCIL_TB) {
         const int r = e / rs, c = e - r * rs;
         out[e] = srec[r * ld + c];
     }
@@ -483,24 +489,23 @@ __global__ void charge_keys_kernel(ChargeKeyArgs a) {
     a.perm[li] = (int)i;
 }
 
-// groups of <= IG consecutive sorted charges within each bin: one block,
-// each thread a contiguous run of bins, block-wide exclusive scan
-__global__ void __launch_bounds__(1024) charge_groups_kernel(const int64_t* seg, int nbins,
-                                                            int IG, int2* groups, int* ngroups) {
-    typedef cub::BlockScan<int, 1024> Scan;
-    __shared__ typename Scan::TempStorage tmp;
-    const int per = (nbins + 1023) / 1024;
-    const int b0 = threadIdx.x * per, b1 = min(nbins, b0 + per);
-    int mine = 0;
-    for (int b = b0; b < b1; ++b) mine += (int)((seg[b + 1] - seg[b] + IG - 1) / IG);
-    int off = 0, total = 0;
-    Scan(tmp).ExclusiveSum(mine, off, total);
-    for (int b = b0; b < b1; ++b) {
-        const int64_t s0 = seg[b], n = seg[b + 1] - s0;
-        for (int64_t j = 0; j < n; j += IG)
-            groups[off++] = make_int2((int)(s0 + j), (int)(n - j < IG ? n - j : IG));
-    }
-    if (threadIdx.x == 0) *ngroups = total;
+// groups of <= IG consecutive sorted charges within each bin: per-bin
+// counts, an exclusive scan (cub), then one thread per bin writes its groups
+__global__ void group_count_kernel(const int64_t* seg, int nbins, int IG, int* cnt) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nbins) return;
+    cnt[b] = (b < nbins) ? (int)((seg[b + 1] - seg[b] + IG - 1) / IG) : 0;
+}
+
+__global__ void group_fill_kernel(const int64_t* seg, const int* off, int nbins, int IG,
+                                  int2* groups, int* ngroups) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b == nbins) *ngroups = off[nbins];
+    if (b >= nbins) return;
+    const int64_t s0 = seg[b], n = seg[b + 1] - s0;
+    int o = off[b];
+    for (int64_t j = 0; j < n; j += IG)
+        groups[o++] = make_int2((int)(s0 + j), (int)(n - j < IG ? n - j : IG));
 }
 
 struct InterpArgs {
@@ -898,7 +903,9 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
     const int64_t gcap = count / ig + nbins + 1;
     if (nbins + 1 > p->iseg_cap || gcap > p->igroup_cap) {
         dfree(p, p->d_iseg); dfree(p, p->d_igroups); dfree(p, p->d_ingroups);
+        dfree(p, p->d_gcnt);
         p->d_iseg = dalloc<int64_t>(p, nbins + 1);
+        p->d_gcnt = dalloc<int>(p, 2 * (nbins + 1));
         p->d_igroups = dalloc<int2>(p, gcap);
         p->d_ingroups = dalloc<int>(p, 1);
         p->iseg_cap = nbins + 1;
@@ -916,8 +923,22 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
     segment_offsets_kernel<<<(unsigned)((count + 1 + TB - 1) / TB), TB, 0, p->stream>>>(
         p->d_keys2, count, zb, nbins, p->d_iseg);
     SE_LAUNCHED(p);
-    charge_groups_kernel<<<1, 1024, 0, p->stream>>>(p->d_iseg, nbins, ig, p->d_igroups,
-                                                    p->d_ingroups);
+    group_count_kernel<<<(nbins + 1 + TB - 1) / TB, TB, 0, p->stream>>>(p->d_iseg, nbins, ig,
+                                                                       p->d_gcnt);
+    SE_LAUNCHED(p);
+    size_t sbytes = 0;
+    SE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sbytes, p->d_gcnt, p->d_gcnt + nbins + 1,
+                                          nbins + 1, p->stream));
+    if (sbytes > p->gscan_bytes) {
+        dfree(p, p->d_gscan);
+        p->d_gscan = dalloc<char>(p, sbytes);
+        p->gscan_bytes = sbytes;
+    }
+    sbytes = p->gscan_bytes;
+    SE_CUDA(cub::DeviceScan::ExclusiveSum(p->d_gscan, sbytes, p->d_gcnt, p->d_gcnt + nbins + 1,
+                                          nbins + 1, p->stream));
+    group_fill_kernel<<<(nbins + 1 + TB - 1) / TB, TB, 0, p->stream>>>(
+        p->d_iseg, p->d_gcnt + nbins + 1, nbins, ig, p->d_igroups, p->d_ingroups);
     SE_LAUNCHED(p);
     InterpArgs a{p->d_fields, p->d_pos_cur, p->d_z, p->d_wcc, p->d_scal, p->d_perm2,
                  p->d_igroups, p->d_ingroups, p->Nx, p->Ny, p->Nz, p->NXY, p->hx, p->hy,

@@ -211,6 +211,9 @@ struct Plan {
     int64_t* d_iseg = nullptr;            // interp: sorted charges per 4x4 bin
     int2* d_igroups = nullptr;            // interp: (first sorted index, count)
     int* d_ingroups = nullptr;
+    int* d_gcnt = nullptr;                // interp: groups per bin, offsets
+    void* d_gscan = nullptr;              // interp: scan scratch
+    size_t gscan_bytes = 0;
     int64_t iseg_cap = 0, igroup_cap = 0;
     const double* d_pos_cur = nullptr;    // positions of the solve in flight
     double* d_near = nullptr;             // [4][N] near sums
