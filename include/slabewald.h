@@ -67,7 +67,8 @@ typedef struct {
     double t_ms[16];           /* SE_TIMINGS: 0-7 stages (sources, spread,
                                   forward, bvp, inverse, interp, near,
                                   finish); 8-11 kernels (spread, bvp, interp,
-                                  near field of the charges) */
+                                  near field of the charges: scan + eval);
+                                  12 near scan kernel, 13 near eval kernel */
 } se_diag;
 
 typedef struct se_plan se_plan;

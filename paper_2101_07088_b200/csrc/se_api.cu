@@ -240,7 +240,7 @@ void phase_results(Plan* p, double* U, se_diag* diag) {
                 SE_CUDA(cudaEventElapsedTime(&ms, S.ev[i], S.ev[i + 1]));
                 diag->t_ms[i] = ms;
             }
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < 6; ++k) {
                 float ms = 0;
                 if (cudaEventElapsedTime(&ms, p->kev[k][0], p->kev[k][1]) == cudaSuccess)
                     diag->t_ms[8 + k] = ms;

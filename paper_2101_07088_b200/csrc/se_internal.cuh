@@ -277,9 +277,10 @@ struct Plan {
 
     std::vector<Buf> owned;
 
-    // per-kernel event timers (SE_TIMINGS): 0 spread, 1 bvp, 2 interp, 3 near
+    // per-kernel event timers (SE_TIMINGS): 0 spread, 1 bvp, 2 interp, 3 near,
+    // 4 near scan, 5 near eval
     bool timing = false;
-    cudaEvent_t kev[4][2] = {};
+    cudaEvent_t kev[6][2] = {};
     void ktic(int k) { if (timing) cudaEventRecord(kev[k][0], stream); }
     void ktoc(int k) { if (timing) cudaEventRecord(kev[k][1], stream); }
 };

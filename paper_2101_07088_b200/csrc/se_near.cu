@@ -908,8 +908,9 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         a.cap_far = want_far; a.cap_close = want_close;
         a.cnt_far = L.cfar; a.cnt_close = L.cclose; a.overflow = L.ovf;
         SE_CUDA(cudaMemsetAsync(L.ovf, 0, sizeof(int), p->stream));
-        if (d_npairs) p->ktic(3);
+        if (d_npairs) { p->ktic(3); p->ktic(4); }
         near_scan_kernel<<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        if (d_npairs) p->ktoc(4);
         SE_LAUNCHED(p);
         int ovf = 0;
         SE_CUDA(cudaMemcpyAsync(&ovf, L.ovf, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
@@ -919,8 +920,9 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         want_far *= 2;
         want_close *= 2;
     }
+    if (d_npairs) p->ktic(5);
     near_eval_kernel<<<nblk, NB_THREADS, 0, p->stream>>>(a);
-    if (d_npairs) p->ktoc(3);
+    if (d_npairs) { p->ktoc(5); p->ktoc(3); }
     SE_LAUNCHED(p);
 }
 

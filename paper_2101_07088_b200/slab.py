@@ -88,7 +88,8 @@ def _flags(need_energy, need_forces, need_potential, subtract_self,
 
 
 STAGES = ("sources", "spread", "forward", "bvp", "inverse", "interp", "near",
-          "finish", "k_spread", "k_bvp", "k_interp", "k_near")
+          "finish", "k_spread", "k_bvp", "k_interp", "k_near", "k_near_scan",
+          "k_near_eval")
 
 
 class SlabSolver:
