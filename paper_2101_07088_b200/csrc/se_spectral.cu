@@ -501,9 +501,17 @@ __global__ void assemble_kernel(AsmArgs a) {
     int j = (int)(e / a.M);
     int64_t m = e % a.M;
     const int64_t RS = 2 * a.M;
-    // iDCT GEMM output: row j = value at ascending Chebyshev node j
-    double2 v = a.ext[(int64_t)j * RS + m];
-    double2 d = a.ext[(int64_t)j * RS + a.M + m];
+    // iDCT halves: value at node j = E_j + O_j, at node N - j = E_j - O_j
+    const int Pe = (a.Nz + 1) / 2, Po = a.Nz / 2;
+    const int r = (j < Pe) ? j : a.Nz - 1 - j;
+    const double2* E = a.ext + (int64_t)r * RS + m;
+    double2 v = E[0], d = E[a.M];
+    if (r < Po) {
+        const double2* O = a.ext + (int64_t)(Pe + r) * RS + m;
+        const double2 ov = O[0], od = O[a.M];
+        v = (j < Pe) ? cadd(v, ov) : csub(v, ov);
+        d = (j < Pe) ? cadd(d, od) : csub(d, od);
+    }
     if (a.corr && a.sel[m] && j >= a.w0 && j < a.w1) {
         double k = a.kmag[m], z = a.z[j];
         double e1 = exp(-k * z), e2 = exp(k * (z - a.H));
@@ -569,23 +577,37 @@ void factor_bvp(Plan* p) {
     colsums(sgn, &h[7 * n], &h[8 * n]);
     p->d_maps = dalloc<double>(p, h.size());
     SE_CUDA(cudaMemcpy(p->d_maps, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
-    // DCT-I matrices (column-major), chebyshev.py:46-65 with the node flip:
+    // DCT-I matrices, chebyshev.py:46-65 with the node flip:
     //  a_n = w_n/(2N) sum_j g_j cos(pi n (N-j)/N) v_j,  g = 1 at the ends else 2,
     //        w_n = 2 for interior n else 1
     //  v_j = sum_n cos(pi n (N-j)/N) a_n
+    // Both are split by the node reflection j -> N - j (F[n][N-j] = (-1)^n
+    // F[n][j], I[N-j][n] = (-1)^n I[j][n]): even / odd coefficient rows
+    // need only the symmetric / antisymmetric node combinations, so each
+    // transform is two GEMMs of half the order (half the flops).
     {
         const int N = n - 1;
-        std::vector<double> F((size_t)n * n), I((size_t)n * n);
-        for (int r = 0; r < n; ++r)
-            for (int c = 0; c < n; ++c) {
-                const long long nm = (long long)r * (N - c) % (2 * N);
-                const double cs = std::cos(M_PI * (double)nm / N);
-                const double g = (c == 0 || c == N) ? 1.0 : 2.0;
-                const double w = (r == 0 || r == N) ? 1.0 : 2.0;
-                F[(size_t)r + (size_t)c * n] = w / (2.0 * N) * g * cs;      // a = F v
-                const long long nm2 = (long long)c * (N - r) % (2 * N);
-                I[(size_t)r + (size_t)c * n] = std::cos(M_PI * (double)nm2 / N);  // v = I a
-            }
+        const int Pe = (n + 1) / 2, Po = n / 2;
+        auto Fv = [&](int r, int c) {
+            const long long nm = (long long)r * (N - c) % (2 * N);
+            const double g = (c == 0 || c == N) ? 1.0 : 2.0;
+            const double w = (r == 0 || r == N) ? 1.0 : 2.0;
+            return w / (2.0 * N) * g * std::cos(M_PI * (double)nm / N);
+        };
+        auto Iv = [&](int r, int c) {
+            const long long nm = (long long)c * (N - r) % (2 * N);
+            return std::cos(M_PI * (double)nm / N);
+        };
+        // column-major: FEE (Pe x Pe), FOO (Po x Po), IEE (Pe x Pe), IOO (Po x Po)
+        std::vector<double> F((size_t)Pe * Pe + (size_t)Po * Po), I(F.size());
+        for (int i = 0; i < Pe; ++i)
+            for (int c = 0; c < Pe; ++c) F[(size_t)i + (size_t)c * Pe] = Fv(2 * i, c);
+        for (int i = 0; i < Po; ++i)
+            for (int c = 0; c < Po; ++c) F[(size_t)Pe * Pe + i + (size_t)c * Po] = Fv(2 * i + 1, c);
+        for (int r = 0; r < Pe; ++r)
+            for (int i = 0; i < Pe; ++i) I[(size_t)r + (size_t)i * Pe] = Iv(r, 2 * i);
+        for (int r = 0; r < Po; ++r)
+            for (int i = 0; i < Po; ++i) I[(size_t)Pe * Pe + r + (size_t)i * Po] = Iv(r, 2 * i + 1);
         p->d_dct_fwd = dalloc<double>(p, F.size());
         p->d_dct_inv = dalloc<double>(p, I.size());
         SE_CUDA(cudaMemcpy(p->d_dct_fwd, F.data(), F.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -612,19 +634,48 @@ void factor_bvp(Plan* p) {
 // z transforms as one DGEMM over all modes of both grids (W = 4M doubles per
 // row): the DCT-I of length Nz = 258 is 2*257 in FFT terms (Bluestein in
 // cuFFT); as a 258 x 258 matrix it runs on the FP64 tensor pipe.
-static void z_gemm(Plan* p, const double* Dcol, const double* in, double* out) {
+// out (W x cols, ldo) = in (W x k, ldi) * D^T with D (cols x k) column-major;
+// W x k column-major == row-major [k][W] (z-slowest rows)
+static void z_gemm(Plan* p, const double* D, int cols, int k, const double* in, int64_t ldi,
+                   double* out, int64_t ldo) {
     const int64_t W = 4 * p->M;
     const double one = 1.0, zero = 0.0;
-    // row-major [Nz][W] == column-major (W x Nz): out^T = in^T * D^T
-    SE_CUBLAS(cublasDgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_T, (int)W, p->Nz, p->Nz, &one, in,
-                          (int)W, Dcol, p->Nz, &zero, out, (int)W));
+    SE_CUBLAS(cublasDgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_T, (int)W, cols, k, &one, in, (int)ldi,
+                          D, cols, &zero, out, (int)ldo));
+}
+
+// symmetric / antisymmetric node combinations for the forward DCT:
+// s_c = v_c + v_{N-c}, d_c = v_c - v_{N-c} (c < n/2); s_h = v_h (odd n)
+__global__ void fold_kernel(const double* v, int n, int64_t W, double* s, double* d) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int Pe = (n + 1) / 2, Po = n / 2;
+    if (e >= (int64_t)Pe * W) return;
+    const int c = (int)(e / W);
+    const int64_t w = e - (int64_t)c * W;
+    const double a = v[(int64_t)c * W + w];
+    if (c < Po) {
+        const double b = v[(int64_t)(n - 1 - c) * W + w];
+        s[e] = a + b;
+        d[e] = a - b;
+    } else {
+        s[e] = a;
+    }
 }
 
 void forward_transforms(Plan* p, bool two_grids) {
     (void)two_grids;
     SE_CUFFT(cufftExecD2Z(p->fft_fwd2, p->d_rho, p->d_hat));
-    z_gemm(p, p->d_dct_fwd, reinterpret_cast<const double*>(p->d_hat),
-           reinterpret_cast<double*>(p->d_ext));
+    const int n = p->Nz, Pe = (n + 1) / 2, Po = n / 2;
+    const int64_t W = 4 * p->M;
+    double* S = reinterpret_cast<double*>(p->d_scr);   // BVP scratch, free here
+    double* D = S + (int64_t)Pe * W;
+    fold_kernel<<<(unsigned)(((int64_t)Pe * W + 255) / 256), 256, 0, p->stream>>>(
+        reinterpret_cast<const double*>(p->d_hat), n, W, S, D);
+    SE_LAUNCHED(p);
+    double* ext = reinterpret_cast<double*>(p->d_ext);
+    z_gemm(p, p->d_dct_fwd, Pe, Pe, S, W, ext, 2 * W);                     // even rows
+    if (Po > 0)
+        z_gemm(p, p->d_dct_fwd + (size_t)Pe * Pe, Po, Po, D, W, ext + W, 2 * W);   // odd rows
 }
 
 void bvp_solve(Plan* p, bool two_grids, int mode, bool correction) {
@@ -660,8 +711,14 @@ void bvp_solve(Plan* p, bool two_grids, int mode, bool correction) {
 }
 
 void inverse_transforms(Plan* p, bool forces, bool correction) {
-    z_gemm(p, p->d_dct_inv, reinterpret_cast<const double*>(p->d_ext),
-           reinterpret_cast<double*>(p->d_hat));
+    // E (rows 0..Pe-1) from the even coefficients, O (rows Pe..) from the odd
+    const int n = p->Nz, Pe = (n + 1) / 2, Po = n / 2;
+    const int64_t W = 4 * p->M;
+    const double* ext = reinterpret_cast<const double*>(p->d_ext);
+    double* hat = reinterpret_cast<double*>(p->d_hat);
+    z_gemm(p, p->d_dct_inv, Pe, Pe, ext, 2 * W, hat, W);
+    if (Po > 0)
+        z_gemm(p, p->d_dct_inv + (size_t)Pe * Pe, Po, Po, ext + W, 2 * W, hat + (int64_t)Pe * W, W);
     AsmArgs a{};
     a.ext = reinterpret_cast<const double2*>(p->d_hat);
     a.spec = reinterpret_cast<double2*>(p->d_spec);
