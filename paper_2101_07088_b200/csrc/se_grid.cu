@@ -391,13 +391,14 @@ struct SpreadArgs {
     int two;                     // slot 0 (over) as well as slot 1 (in)
 };
 
-constexpr int SPREAD_CAP = 256;
-using SpreadStage = Stage<SPREAD_TZ, SPREAD_CAP>;
-
-__global__ void __launch_bounds__(256, 2) spread_kernel(SpreadArgs a) {
-    constexpr int TZ = SPREAD_TZ;       // 32 nodes = 4 groups of 8
+// TZ nodes per tile in z (TZ/8 z groups of 8), 8 TZ threads, CAP staged
+// sources per round, MINB resident CTAs per SM (the barrier-heavy staging
+// needs several independent CTAs per SM to keep the FMA pipe fed).
+template <int TZ, int CAP, int MINB>
+__global__ void __launch_bounds__(8 * TZ, MINB) spread_kernel(SpreadArgs a) {
+    constexpr int NG = TZ / 8;
     extern __shared__ __align__(16) unsigned char dsm[];
-    SpreadStage& sm = *reinterpret_cast<SpreadStage*>(dsm);
+    Stage<TZ, CAP>& sm = *reinterpret_cast<Stage<TZ, CAP>*>(dsm);
     __shared__ int s_lo[MAX_BINS], s_len[MAX_BINS], s_nr, s_total;
 
     const TileArgs& A = a.t;
@@ -417,8 +418,8 @@ __global__ void __launch_bounds__(256, 2) spread_kernel(SpreadArgs a) {
     for (int cls = a.two ? 0 : 1; cls < 2; ++cls) {
         tile_ranges<TZ>(A, bx, by, k0, cls, s_lo, s_len, &s_nr, &s_total);
         const int total = s_total, nr = s_nr;
-        for (int cursor = 0; cursor < total; cursor += SPREAD_CAP) {
-            const int n = stage_round<TZ, 4, SPREAD_CAP, true>(
+        for (int cursor = 0; cursor < total; cursor += CAP) {
+            const int n = stage_round<TZ, NG, CAP, true>(
                 sm, A, cursor, total, s_lo, s_len, nr, gx0, gy0, k0);
             for (int w0 = 0; w0 < n; w0 += 32) {
                 const int s0 = w0 + lane;
@@ -524,7 +525,7 @@ struct GroupInfo {
     int jxw[IG_MAX], jyw[IG_MAX], lo[IG_MAX], hi[IG_MAX], idx[IG_MAX];
 };
 
-template <int NF, int IG, int MINB>
+template <int NF, int IG, int MINB, int UNR>
 __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgs a) {
     extern __shared__ __align__(16) double ism[];
     __shared__ GroupInfo ginfo[IWARPS];
@@ -642,7 +643,7 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgs a)
             gx %= a.Nx; if (gx < 0) gx += a.Nx;
             gy %= a.Ny; if (gy < 0) gy += a.Ny;
             const double* F = a.fields + (int64_t)zc * zstride + (int64_t)gx * a.Ny + gy;
-#pragma unroll 2
+#pragma unroll UNR
             for (int r = 0; r < nz; ++r) {
                 double f[NF];
 #pragma unroll
@@ -868,17 +869,21 @@ static TileArgs tile_args(Plan* p) {
     return t;
 }
 
+template <int TZ, int CAP, int MINB>
+static void launch_spread(Plan* p, const SpreadArgs& a) {
+    dim3 grid(p->ss.nbx, p->ss.nby, (p->Nz + TZ - 1) / TZ);
+    const int smem = (int)sizeof(Stage<TZ, CAP>);
+    SE_CUDA(cudaFuncSetAttribute(spread_kernel<TZ, CAP, MINB>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    spread_kernel<TZ, CAP, MINB><<<grid, 8 * TZ, smem, p->stream>>>(a);
+}
+
 void spread(Plan* p, bool two_grids) {
     SpreadArgs a{tile_args(p), p->d_rho, two_grids ? 1 : 0};
-    dim3 grid(p->ss.nbx, p->ss.nby, (p->Nz + SPREAD_TZ - 1) / SPREAD_TZ);
-    const int smem = (int)sizeof(SpreadStage);
-    static bool attr = false;
-    if (!attr) {
-        SE_CUDA(cudaFuncSetAttribute(spread_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
+    // 16-node tiles, 64 staged sources per round, 5 CTAs (20 warps) per SM:
+    // measured best among (TZ, CAP, CTAs/SM) in {16,32} x {32..256} x {2..8}
     p->ktic(0);
-    spread_kernel<<<grid, 256, smem, p->stream>>>(a);
+    launch_spread<16, 64, 5>(p, a);
     p->ktoc(0);
     SE_LAUNCHED(p);
 }
@@ -894,12 +899,7 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
     if (((uint64_t)nbins << zb) >> 32)
         throw Error(SE_ERR_VALUE, "grid too large for the interpolation sort keys");
     ensure_sources(p, n);               // key / permutation / sort scratch (>= 3n)
-    static const int ig_env = [] {
-        const char* e = getenv("SE_INTERP_IG");
-        return e ? atoi(e) : 4;
-    }();
-    const int IG = (ig_env == 8) ? 8 : (ig_env == 5 ? 5 : 4);   // 5: IG 4, 3 blocks / SM
-    const int ig = IG == 5 ? 4 : IG;
+    const int ig = 4;                   // charges per group (measured best of 2, 3, 4, 8)
     const int64_t gcap = count / ig + nbins + 1;
     if (nbins + 1 > p->iseg_cap || gcap > p->igroup_cap) {
         dfree(p, p->d_iseg); dfree(p, p->d_igroups); dfree(p, p->d_ingroups);
@@ -950,9 +950,8 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
         SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         kern<<<blocks, IWARPS * 32, smem, p->stream>>>(a);
     };
-    if (IG == 8) { if (forces) go(interp_kernel<4, 8, 1>); else go(interp_kernel<1, 8, 1>); }
-    else if (IG == 5) { if (forces) go(interp_kernel<4, 4, 3>); else go(interp_kernel<1, 4, 3>); }
-    else { if (forces) go(interp_kernel<4, 4, 1>); else go(interp_kernel<1, 4, 1>); }
+    if (forces) go(interp_kernel<4, 4, 1, 2>);
+    else go(interp_kernel<1, 4, 1, 2>);
     p->ktoc(2);
     SE_LAUNCHED(p);
 }

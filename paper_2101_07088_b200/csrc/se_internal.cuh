@@ -84,7 +84,6 @@ enum : int {
 // spread / interpolation tiling
 // ----------------------------------------------------------------------------
 constexpr int TILE = 8;          // xy tile = 8 x 8 grid columns (one bin)
-constexpr int SPREAD_TZ = 32;    // z nodes per spread CTA (4 groups of 8)
 constexpr int INTERP_TZ = 16;    // z nodes per interp CTA (4 groups of 4)
 constexpr int CHUNK = 64;        // sources staged in shared memory at a time
 constexpr int MAX_M = 24;        // max xy stencil half width supported
