@@ -492,12 +492,18 @@ __device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, 
     }
 }
 
-__global__ void __launch_bounds__(NB_THREADS, 6) near_eval_kernel(NearArgs a) {
+// Evaluation of one list kind per launch: the far lists (the bulk; erfc-only
+// kernel, small register footprint, high occupancy) write the sums, the close
+// lists (general kernel) add to them.
+template <bool FAR, int MINB>
+__global__ void __launch_bounds__(NB_THREADS, MINB) near_eval_kernel(NearArgs a) {
     __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1)];
     const int tid = threadIdx.x, lane = tid & 31;
-    for (int e = tid; e < SE_ERFCX_NP * (SE_ERFCX_DEG + 1); e += blockDim.x)
-        tab[e] = (&se_erfcx_tab[0][0])[e];
-    __syncthreads();
+    if (!FAR || !a.use_poly) {
+        for (int e = tid; e < SE_ERFCX_NP * (SE_ERFCX_DEG + 1); e += blockDim.x)
+            tab[e] = (&se_erfcx_tab[0][0])[e];
+        __syncthreads();
+    }
     const int64_t task = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
     if (task >= a.ntask || task >= *a.ntask_dev) return;
     const int2 tk = a.tasks[task];
@@ -509,20 +515,31 @@ __global__ void __launch_bounds__(NB_THREADS, 6) near_eval_kernel(NearArgs a) {
     if (live) {
         i = a.order[slot];
         const double px = a.eval[3 * i], py = a.eval[3 * i + 1], pz = a.eval[3 * i + 2];
-        eval_list<true>(a, tab, a.list_far + slot * a.cap_far, a.cnt_far[slot], px, py, pz,
-                        phi, ex, ey, ez, count);
-        eval_list<false>(a, tab, a.list_close + slot * a.cap_close, a.cnt_close[slot], px, py,
-                         pz, phi, ex, ey, ez, count);
-        a.out[i] = phi;
-        if (a.need_field) {
-            a.out[a.out_stride + i] = ex;
-            a.out[2 * a.out_stride + i] = ey;
-            a.out[3 * a.out_stride + i] = ez;
+        if (FAR)
+            eval_list<true>(a, tab, a.list_far + slot * a.cap_far, a.cnt_far[slot], px, py, pz,
+                            phi, ex, ey, ez, count);
+        else
+            eval_list<false>(a, tab, a.list_close + slot * a.cap_close, a.cnt_close[slot], px,
+                             py, pz, phi, ex, ey, ez, count);
+        if (FAR) {
+            a.out[i] = phi;
+            if (a.need_field) {
+                a.out[a.out_stride + i] = ex;
+                a.out[2 * a.out_stride + i] = ey;
+                a.out[3 * a.out_stride + i] = ez;
+            }
+        } else {
+            a.out[i] += phi;
+            if (a.need_field) {
+                a.out[a.out_stride + i] += ex;
+                a.out[2 * a.out_stride + i] += ey;
+                a.out[3 * a.out_stride + i] += ez;
+            }
         }
     }
     unsigned long long cnt = (unsigned long long)count;
     for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
-    if (lane == 0 && a.npairs) atomicAdd((unsigned long long*)a.npairs, cnt);
+    if (lane == 0 && a.npairs && cnt) atomicAdd((unsigned long long*)a.npairs, cnt);
 }
 
 // A few evaluation points (the gauge origin): one CTA per point, the threads
@@ -983,7 +1000,9 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         want_close *= 2;
     }
     if (d_npairs) p->ktic(5);
-    near_eval_kernel<<<nblk, NB_THREADS, 0, p->stream>>>(a);
+    near_eval_kernel<true, 8><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+    SE_LAUNCHED(p);
+    near_eval_kernel<false, 6><<<nblk, NB_THREADS, 0, p->stream>>>(a);
     if (d_npairs) { p->ktoc(5); p->ktoc(3); }
     SE_LAUNCHED(p);
 }
