@@ -329,6 +329,7 @@ __device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) 
 // ---------------------------------------------------------------------------
 constexpr int MAXNB = 27;
 constexpr int SCAN_Q = 16;                  // per-lane staging before a flush
+constexpr int SCAN_STAGE = 128;             // staged candidates per warp
 
 // Neighbour columns of a target column and the candidate range of one lane
 // in one of them: columns whose xy distance to the target exceeds the query
@@ -367,10 +368,11 @@ __device__ __forceinline__ void column_axis(int c, int i, bool all, int n, float
     *dist = fmaxf(0.f, fmaxf(lo - p, p - hi));
 }
 
-__global__ void __launch_bounds__(NB_THREADS) near_scan_kernel(NearArgs a) {
+__global__ void __launch_bounds__(NB_THREADS, 10) near_scan_kernel(NearArgs a) {
     constexpr int W = NB_THREADS / 32;
     __shared__ int qf[W][SCAN_Q + 4][32];
     __shared__ int qcl[W][SCAN_Q + 4][32];
+    __shared__ float4 stage[W][SCAN_STAGE];
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
     const int64_t task = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
     if (task >= a.ntask || task >= *a.ntask_dev) return;
@@ -428,25 +430,40 @@ __global__ void __launch_bounds__(NB_THREADS) near_scan_kernel(NearArgs a) {
             }
             if (!__any_sync(0xffffffffu, j < e)) continue;
             const float qx = pxf - sx, qy = pyf - sy;
-            for (;;) {
+            // the union of the lanes' windows is staged through shared memory
+            // in coalesced chunks; each lane tests its own part from there
+            int umin = (j < e) ? j : 0x7fffffff, umax = (j < e) ? e : 0;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (j + u < e) {
-                        const float4 f = a.srcf[j + u];
-                        float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
-                        if (cw.allx) dx -= a.Lxf * rintf(dx * a.iLxf);
-                        if (cw.ally) dy -= a.Lyf * rintf(dy * a.iLyf);
-                        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                        if (r2 <= r2f) {
-                            if (r2 > r2c) qf[wib][qn++][lane] = j + u;
-                            else qcl[wib][qc++][lane] = j + u;
+            for (int o = 16; o > 0; o >>= 1) {
+                umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, o));
+                umax = max(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+            }
+            for (int c0 = umin; c0 < umax; c0 += SCAN_STAGE) {
+                const int c1 = min(umax, c0 + SCAN_STAGE);
+                __syncwarp();
+                for (int q = c0 + lane; q < c1; q += 32) stage[wib][q - c0] = a.srcf[q];
+                __syncwarp();
+                int jj = max(j, c0);
+                const int ee = min(e, c1);
+                while (__any_sync(0xffffffffu, jj < ee)) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (jj + u < ee) {
+                            const float4 f = stage[wib][jj + u - c0];
+                            float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
+                            if (cw.allx) dx -= a.Lxf * rintf(dx * a.iLxf);
+                            if (cw.ally) dy -= a.Lyf * rintf(dy * a.iLyf);
+                            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                            if (r2 <= r2f) {
+                                if (r2 > r2c) qf[wib][qn++][lane] = jj + u;
+                                else qcl[wib][qc++][lane] = jj + u;
+                            }
                         }
                     }
+                    jj += 4;
+                    if (__any_sync(0xffffffffu, qn >= SCAN_Q)) flush(qf[wib], qn, nf, lfar, a.cap_far, false);
+                    if (__any_sync(0xffffffffu, qc >= SCAN_Q)) flush(qcl[wib], qc, nc, lcls, a.cap_close, false);
                 }
-                j += 4;
-                if (__any_sync(0xffffffffu, qn >= SCAN_Q)) flush(qf[wib], qn, nf, lfar, a.cap_far, false);
-                if (__any_sync(0xffffffffu, qc >= SCAN_Q)) flush(qcl[wib], qc, nc, lcls, a.cap_close, false);
-                if (!__any_sync(0xffffffffu, j < e)) break;
             }
         }
     }
