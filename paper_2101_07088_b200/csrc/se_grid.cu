@@ -6,15 +6,14 @@
 //
 // B200 design.  fp64 shared-memory atomics are CAS loops on sm_100a and
 // global fp64 atomics cost ~1 op/clk/SM, so the spread is a GATHER: each CTA
-// owns an 8x8-column x 32-node tile of the output grid in registers (one
-// column x 8 nodes per thread) and streams every source whose stencil
-// touches the tile through shared memory, 64 at a time.  The tensor-product
-// weights are staged as 8 x-, 8 y- and 32 z-weights per source; a warp skips
-// a source whose stencil misses the warp's 4x8-column x 8-node sub-tile
-// (uniform branch), so the FMA pipe only sees sources that touch it.  No
-// atomics, deterministic order, coalesced stores.  The interpolation is the
-// adjoint on the same tiling (4 fields x 4 nodes per thread in registers,
-// warp-shuffle reduction, one global atomic per source and tile).
+// owns an 8x8-column x 16-node tile of the output grid in registers (two
+// columns x 8 nodes per lane, one warp per 8-node z group) and streams every
+// source whose stencil touches the tile through shared memory, 64 at a time
+// (candidates from the neighbour bins, compacted with warp ballots, weights
+// staged with cp.async).  No atomics, deterministic order.  The
+// interpolation is charge-stationary instead: warps own groups of 4 charges
+// of one 4x4-column bin and walk the union of their stencils, loading each
+// field node once for the group; the weights are recomputed exactly.
 //
 // Stencil membership is computed with the reference's exact operation order
 // (no FMA contraction: __dmul_rn / __dsub_rn) so the set of grid nodes each
@@ -390,67 +389,6 @@ struct SpreadArgs {
     double* rho;                 // [Nz][2][Nx][Ny]
     int two;                     // slot 0 (over) as well as slot 1 (in)
 };
-
-// TZ nodes per tile in z (TZ/8 z groups of 8), 8 TZ threads, CAP staged
-// sources per round, MINB resident CTAs per SM (the barrier-heavy staging
-// needs several independent CTAs per SM to keep the FMA pipe fed).
-template <int TZ, int CAP, int MINB>
-__global__ void __launch_bounds__(8 * TZ, MINB) spread_kernel(SpreadArgs a) {
-    constexpr int NG = TZ / 8;
-    extern __shared__ __align__(16) unsigned char dsm[];
-    Stage<TZ, CAP>& sm = *reinterpret_cast<Stage<TZ, CAP>*>(dsm);
-    __shared__ int s_lo[MAX_BINS], s_len[MAX_BINS], s_nr, s_total;
-
-    const TileArgs& A = a.t;
-    const int bx = blockIdx.x, by = blockIdx.y, k0 = blockIdx.z * TZ;
-    const int gx0 = bx * TILE, gy0 = by * TILE;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    // warp w: x columns 4(w&1)..+4, all 8 y columns, z group w>>1
-    const int tx = 4 * (warp & 1) + (lane >> 3), ty = lane & 7, zg = warp >> 1;
-    const unsigned wxbits = 0xFu << (4 * (warp & 1));
-    const unsigned wzbit = 1u << zg;
-
-    double acc[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) acc[r] = 0.0;
-
-    const int gx = gx0 + tx, gy = gy0 + ty;
-    for (int cls = a.two ? 0 : 1; cls < 2; ++cls) {
-        tile_ranges<TZ>(A, bx, by, k0, cls, s_lo, s_len, &s_nr, &s_total);
-        const int total = s_total, nr = s_nr;
-        for (int cursor = 0; cursor < total; cursor += CAP) {
-            const int n = stage_round<TZ, NG, CAP, true>(
-                sm, A, cursor, total, s_lo, s_len, nr, gx0, gy0, k0);
-            for (int w0 = 0; w0 < n; w0 += 32) {
-                const int s0 = w0 + lane;
-                const bool act = s0 < n && (sm.xm[s0] & wxbits) && (sm.zm[s0] & wzbit);
-                unsigned m = __ballot_sync(0xffffffffu, act);
-                while (m) {
-                    const int s = w0 + __ffs(m) - 1;
-                    m &= m - 1;
-                    const double cxy = (sm.q[s] * sm.wx[s][tx]) * sm.wy[s][ty];
-                    const double2* wz = reinterpret_cast<const double2*>(&sm.wz[s][8 * zg]);
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        const double2 w2 = wz[r];
-                        acc[2 * r] = fma(cxy, w2.x, acc[2 * r]);
-                        acc[2 * r + 1] = fma(cxy, w2.y, acc[2 * r + 1]);
-                    }
-                }
-            }
-            __syncthreads();
-        }
-        // store this class's running sum (slot 0 after class 0, slot 1 after 1)
-        if (gx < A.Nx && gy < A.Ny) {
-            double* base_ptr = a.rho + (int64_t)(cls) * A.NXY + (int64_t)gx * A.Ny + gy;
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                int k = k0 + 8 * zg + r;
-                if (k < A.Nz) base_ptr[(int64_t)k * 2 * A.NXY] = acc[r];
-            }
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // interpolation of the field stack at the charges         gridops.py:105-133
@@ -869,21 +807,91 @@ static TileArgs tile_args(Plan* p) {
     return t;
 }
 
+// One warp per 8-node z group covers all 8x8 columns of the tile, each lane
+// two y columns (ty, ty + 4) x 8 nodes, so a staged source costs one
+// z-weight fetch per 16 FMAs.  Several small CTAs per SM keep the FMA pipe
+// busy while others wait at their staging barriers.
 template <int TZ, int CAP, int MINB>
-static void launch_spread(Plan* p, const SpreadArgs& a) {
+__global__ void __launch_bounds__(4 * TZ, MINB) spread_wide_kernel(SpreadArgs a) {
+    constexpr int NG = TZ / 8;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    Stage<TZ, CAP>& sm = *reinterpret_cast<Stage<TZ, CAP>*>(dsm);
+    __shared__ int s_lo[MAX_BINS], s_len[MAX_BINS], s_nr, s_total;
+
+    const TileArgs& A = a.t;
+    const int bx = blockIdx.x, by = blockIdx.y, k0 = blockIdx.z * TZ;
+    const int gx0 = bx * TILE, gy0 = by * TILE;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int tx = lane >> 2, ty = lane & 3, zg = warp;
+    const unsigned wzbit = 1u << zg;
+
+    double acc[2][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) { acc[0][r] = 0.0; acc[1][r] = 0.0; }
+
+    const int gx = gx0 + tx;
+    for (int cls = a.two ? 0 : 1; cls < 2; ++cls) {
+        tile_ranges<TZ>(A, bx, by, k0, cls, s_lo, s_len, &s_nr, &s_total);
+        const int total = s_total, nr = s_nr;
+        for (int cursor = 0; cursor < total; cursor += CAP) {
+            const int n = stage_round<TZ, NG, CAP, true>(
+                sm, A, cursor, total, s_lo, s_len, nr, gx0, gy0, k0);
+            for (int w0 = 0; w0 < n; w0 += 32) {
+                const int s0 = w0 + lane;
+                const bool act = s0 < n && (sm.zm[s0] & wzbit);
+                unsigned m = __ballot_sync(0xffffffffu, act);
+                while (m) {
+                    const int s = w0 + __ffs(m) - 1;
+                    m &= m - 1;
+                    const double qx = sm.q[s] * sm.wx[s][tx];
+                    const double c0 = qx * sm.wy[s][ty], c1 = qx * sm.wy[s][ty + 4];
+                    const double2* wz = reinterpret_cast<const double2*>(&sm.wz[s][8 * zg]);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const double2 w2 = wz[r];
+                        acc[0][2 * r] = fma(c0, w2.x, acc[0][2 * r]);
+                        acc[0][2 * r + 1] = fma(c0, w2.y, acc[0][2 * r + 1]);
+                        acc[1][2 * r] = fma(c1, w2.x, acc[1][2 * r]);
+                        acc[1][2 * r + 1] = fma(c1, w2.y, acc[1][2 * r + 1]);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        // store this class's running sum (slot 0 after class 0, slot 1 after 1)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int gy = gy0 + ty + 4 * h;
+            if (gx < A.Nx && gy < A.Ny) {
+                double* base_ptr = a.rho + (int64_t)(cls) * A.NXY + (int64_t)gx * A.Ny + gy;
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int k = k0 + 8 * zg + r;
+                    if (k < A.Nz) base_ptr[(int64_t)k * 2 * A.NXY] = acc[h][r];
+                }
+            }
+        }
+    }
+}
+
+template <int TZ, int CAP, int MINB>
+static void launch_spread_wide(Plan* p, const SpreadArgs& a) {
     dim3 grid(p->ss.nbx, p->ss.nby, (p->Nz + TZ - 1) / TZ);
     const int smem = (int)sizeof(Stage<TZ, CAP>);
-    SE_CUDA(cudaFuncSetAttribute(spread_kernel<TZ, CAP, MINB>,
+    SE_CUDA(cudaFuncSetAttribute(spread_wide_kernel<TZ, CAP, MINB>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    spread_kernel<TZ, CAP, MINB><<<grid, 8 * TZ, smem, p->stream>>>(a);
+    spread_wide_kernel<TZ, CAP, MINB><<<grid, 4 * TZ, smem, p->stream>>>(a);
 }
+
 
 void spread(Plan* p, bool two_grids) {
     SpreadArgs a{tile_args(p), p->d_rho, two_grids ? 1 : 0};
-    // 16-node tiles, 64 staged sources per round, 5 CTAs (20 warps) per SM:
-    // measured best among (TZ, CAP, CTAs/SM) in {16,32} x {32..256} x {2..8}
+    // 8x8-column x 16-node tiles, 2 warps (one per 8-node z group, two y
+    // columns per lane), 64 staged sources per round, 10 CTAs per SM:
+    // measured best among tile heights {16, 32}, rounds {32..256}, lane
+    // shapes {1, 2} columns and 2..16 CTAs per SM
     p->ktic(0);
-    launch_spread<16, 64, 5>(p, a);
+    launch_spread_wide<16, 64, 10>(p, a);
     p->ktoc(0);
     SE_LAUNCHED(p);
 }
