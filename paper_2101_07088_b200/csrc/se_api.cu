@@ -171,7 +171,7 @@ void phase_charges(Plan* p, const double* d_pos, double* d_phi_out, double* d_E_
         kpt = kernel_of(P, 1, false, false);
     }
     if (!S.near_empty) {
-        build_cells(p, d_pos, p->d_q, n);                 // sources: every charge
+        build_cells(p, d_pos, p->d_q, n, true);           // sources: every charge
         near_eval(p, d_pos + 3 * first, nullptr, count, kavg, p->d_near, p->d_count);
     } else {
         SE_CUDA(cudaMemsetAsync(p->d_near, 0, sizeof(double) * 4 * (size_t)std::max<int64_t>(count, 1), s));
@@ -655,7 +655,7 @@ int se_near_field(const se_params* params, int device, const double* pos, const 
             k.radius = P.r_nf;
             k.point0 = (two_sqrtpi / k.c1 - two_sqrtpi / k.c2) / (4.0 * M_PI * eps);
         }
-        build_cells(p, d_pos, d_q, n);
+        build_cells(p, d_pos, d_q, n, false);
         near_eval(p, d_ev, nullptr, ne, k, d_out, nullptr);
         std::vector<double> h(4 * ne);
         SE_CUDA(cudaMemcpyAsync(h.data(), d_out, (need_field ? 4 : 1) * ne * sizeof(double),

@@ -132,7 +132,7 @@ struct StencilArgs {
     const double4* src; const int* owner_in; const int* perm;
     const uint32_t* keys; uint32_t invalid_major; int zbits; int64_t total;
     const double* znodes; int Nz;
-    double hx, hy, rad, rad_keep, width, norm; int mx, my, wz;
+    double hx, hy, rad, rad_keep, inv_width, inv_norm; int mx, my, wz;
     Stencils st;
 };
 
@@ -158,14 +158,14 @@ __global__ void __launch_bounds__(STENCIL_TB) stencil_kernel(StencilArgs a) {
             for (int o = 0; o <= 2 * a.mx; ++o) {
                 const double xj = __dmul_rn((double)(jx + o - a.mx), a.hx);
                 const double d = __dsub_rn(v.x, xj);
-                if (fabs(d) <= a.rad_keep) { const double u = d / a.width; my[o] = exp(-0.5 * (u * u)) / a.norm; }
+                if (fabs(d) <= a.rad_keep) my[o] = gauss_w(d, a.inv_width, a.inv_norm);
             }
             double* ry = my + 2 * a.mx + 1;
             const long long jy = (long long)floor(v.y / a.hy);
             for (int o = 0; o <= 2 * a.my; ++o) {
                 const double yj = __dmul_rn((double)(jy + o - a.my), a.hy);
                 const double d = __dsub_rn(v.y, yj);
-                if (fabs(d) <= a.rad_keep) { const double u = d / a.width; ry[o] = exp(-0.5 * (u * u)) / a.norm; }
+                if (fabs(d) <= a.rad_keep) ry[o] = gauss_w(d, a.inv_width, a.inv_norm);
             }
             double* rz = ry + 2 * a.my + 1;
             // z axis: nodes in [searchsorted(z-r, left), searchsorted(z+r, right))
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(STENCIL_TB) stencil_kernel(StencilArgs a) {
                 const int k = lo + tt;
                 if (k < hi && k < a.Nz) {
                     const double d = __dsub_rn(v.z, a.znodes[k]);
-                    if (fabs(d) <= a.rad) { const double u = d / a.width; rz[tt] = exp(-0.5 * (u * u)) / a.norm; }
+                    if (fabs(d) <= a.rad) rz[tt] = gauss_w(d, a.inv_width, a.inv_norm);
                 }
             }
             a.st.j0x[i] = (int)jx;
@@ -453,7 +453,7 @@ struct InterpArgs {
     const double* scal;          // scal[0] = A_i
     const int* perm; const int2* groups; const int* ngroups;
     int Nx, Ny, Nz; int64_t NXY;
-    double hx, hy, rad, rad_keep, width, norm; int mx, my;
+    double hx, hy, rad, rad_keep, inv_width, inv_norm; int mx, my;
     double* out; int64_t N;      // [NF][N] raw sums (global charge index)
 };
 
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgs a)
         if (m < cnt) {
             const double xj = __dmul_rn((double)(gi.jx[m] + o - a.mx), a.hx);
             const double d = __dsub_rn(gi.x[m], xj);
-            if (fabs(d) <= a.rad_keep) { const double t = d / a.width; wt = exp(-0.5 * (t * t)) / a.norm; }
+            if (fabs(d) <= a.rad_keep) wt = gauss_w(d, a.inv_width, a.inv_norm);
         }
         swx[e] = wt;
     }
@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgs a)
         if (m < cnt) {
             const double yj = __dmul_rn((double)(gi.jy[m] + o - a.my), a.hy);
             const double d = __dsub_rn(gi.y[m], yj);
-            if (fabs(d) <= a.rad_keep) { const double t = d / a.width; wt = exp(-0.5 * (t * t)) / a.norm; }
+            if (fabs(d) <= a.rad_keep) wt = gauss_w(d, a.inv_width, a.inv_norm);
         }
         swy[e] = wt;
     }
@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgs a)
             double wt = 0.0;
             if (m < cnt && k >= gi.lo[m] && k < gi.hi[m] && k < a.Nz) {
                 const double d = __dsub_rn(gi.z[m], a.znodes[k]);
-                if (fabs(d) <= a.rad) { const double u = d / a.width; wt = exp(-0.5 * (u * u)) / a.norm; }
+                if (fabs(d) <= a.rad) wt = gauss_w(d, a.inv_width, a.inv_norm);
                 wt = wt * a.wcc[k];
             }
             swz[e] = wt;
@@ -783,7 +783,7 @@ void build_sources(Plan* p, const double* d_pos, int64_t first, int64_t n, bool 
     if (total > 0) {
         StencilArgs sta{p->d_src, p->d_src_owner, p->d_perm2, keys2, (uint32_t)nseg,
                         zb, total, p->d_z, p->Nz, p->hx, p->hy, p->rad,
-                        p->rad_keep, p->width, p->norm, p->mx, p->my, p->wz_max, st};
+                        p->rad_keep, 1.0 / p->width, 1.0 / p->norm, p->mx, p->my, p->wz_max, st};
         const int smem = STENCIL_TB * (st.rs + 1) * (int)sizeof(double);
         if (smem > 48 * 1024)
             SE_CUDA(cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -950,7 +950,7 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
     SE_LAUNCHED(p);
     InterpArgs a{p->d_fields, p->d_pos_cur, p->d_z, p->d_wcc, p->d_scal, p->d_perm2,
                  p->d_igroups, p->d_ingroups, p->Nx, p->Ny, p->Nz, p->NXY, p->hx, p->hy,
-                 p->rad, p->rad_keep, p->width, p->norm, p->mx, p->my, p->d_far, n};
+                 p->rad, p->rad_keep, 1.0 / p->width, 1.0 / p->norm, p->mx, p->my, p->d_far, n};
     const int smem = IWARPS * ig * (2 * p->mx + 1 + 2 * p->my + 1 + IZC) * (int)sizeof(double);
     if (smem > 200 * 1024) throw Error(SE_ERR_VALUE, "stencil too wide for the interpolation");
     const unsigned blocks = (unsigned)((gcap + IWARPS - 1) / IWARPS);

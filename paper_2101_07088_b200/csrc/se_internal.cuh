@@ -162,6 +162,37 @@ struct Solve {
     int phase = 0;                // 0 idle, 1 spread done, 2 fields done
 };
 
+// exp(-u) for 0 <= u <= 700 without the special-case paths of libm exp:
+// Cody-Waite reduction by ln2, degree-11 Taylor polynomial on |r| <= ln2/2,
+// scaling by 2^n through the exponent bits.  ~1 ulp.
+__device__ __forceinline__ double exp_neg(double u) {
+    const double v = -u;
+    const double n = rint(v * 1.4426950408889634);
+    double r = fma(n, -6.93147180369123816490e-01, v);   // ln2 hi
+    r = fma(n, -1.90821492927058770002e-10, r);          // ln2 lo
+    double p = 2.5052108385441720e-08;                   // 1/11!
+    p = fma(p, r, 2.7557319223985893e-07);
+    p = fma(p, r, 2.7557319223985888e-06);
+    p = fma(p, r, 2.4801587301587302e-05);
+    p = fma(p, r, 1.9841269841269841e-04);
+    p = fma(p, r, 1.3888888888888889e-03);
+    p = fma(p, r, 8.3333333333333332e-03);
+    p = fma(p, r, 4.1666666666666664e-02);
+    p = fma(p, r, 1.6666666666666666e-01);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    const long long bits = (long long)(1023 + (int)n) << 52;
+    return p * __longlong_as_double(bits);
+}
+
+// Gaussian stencil weight exp(-(d/w)^2 / 2) / norm with the reciprocals
+// precomputed (within 2 ulp of the reference's exp(-0.5 (d/w)^2) / norm)
+__device__ __forceinline__ double gauss_w(double d, double inv_width, double inv_norm) {
+    const double u = d * inv_width;
+    return exp_neg(0.5 * (u * u)) * inv_norm;
+}
+
 struct Plan {
     se_params P{};
     Solve solve;
@@ -322,7 +353,7 @@ struct NearKernel {
     int kind;            // 0 avg, 1 point
     int need_field;
 };
-void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n);
+void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, bool in_domain);
 void near_eval(Plan* p, const double* d_eval, const int* d_eval_order,
                int64_t ne, const NearKernel& k, double* d_out4,
                int64_t* d_npairs);

@@ -158,30 +158,6 @@ constexpr int FAR_DEG = 18;
 constexpr int NQ = 48;            // per-lane far-pair queue (shared memory)
 constexpr int NQC = 12;           // per-lane close-pair queue
 
-// exp(-u) for 0 <= u <= 700 without the special-case paths of libm exp:
-// Cody-Waite reduction by ln2, degree-11 Taylor polynomial on |r| <= ln2/2,
-// scaling by 2^n through the exponent bits.  ~1 ulp.
-__device__ __forceinline__ double exp_neg(double u) {
-    const double v = -u;
-    const double n = rint(v * 1.4426950408889634);
-    double r = fma(n, -6.93147180369123816490e-01, v);   // ln2 hi
-    r = fma(n, -1.90821492927058770002e-10, r);          // ln2 lo
-    double p = 2.5052108385441720e-08;                   // 1/11!
-    p = fma(p, r, 2.7557319223985893e-07);
-    p = fma(p, r, 2.7557319223985888e-06);
-    p = fma(p, r, 2.4801587301587302e-05);
-    p = fma(p, r, 1.9841269841269841e-04);
-    p = fma(p, r, 1.3888888888888889e-03);
-    p = fma(p, r, 8.3333333333333332e-03);
-    p = fma(p, r, 4.1666666666666664e-02);
-    p = fma(p, r, 1.6666666666666666e-01);
-    p = fma(p, r, 0.5);
-    p = fma(p, r, 1.0);
-    p = fma(p, r, 1.0);
-    const long long bits = (long long)(1023 + (int)n) << 52;
-    return p * __longlong_as_double(bits);
-}
-
 // 1/sqrt(x) for normal positive x: hardware approximation + 2 Newton steps
 __device__ __forceinline__ double rsqrt_pos(double x) {
     double y;
@@ -746,7 +722,7 @@ static CellGeo cell_geo(const Plan* p) {
     return g;
 }
 
-void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n) {
+void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, bool in_domain) {
     const double eps = p->P.eps;
     const double fb = -(p->P.eps_b - eps) / (p->P.eps_b + eps);
     const double ft = -(p->P.eps_t - eps) / (p->P.eps_t + eps);
@@ -785,19 +761,25 @@ void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n) {
     SrcBuild sb{d_pos, d_q, n, p->P.H, fb, ft, nb, nt, p->d_near_src, ns};
     make_near_sources<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(sb);
     SE_LAUNCHED(p);
-    // z extent of the sources (one small device->host read)
-    int nblk = 64;
-    if (!p->d_mm) p->d_mm = dalloc<double>(p, 256);
-    zrange_kernel<<<nblk, 256, 0, p->stream>>>(p->d_near_src, ns, p->d_mm);
-    SE_LAUNCHED(p);
-    std::vector<double> mm(2 * nblk);
-    SE_CUDA(cudaMemcpyAsync(mm.data(), p->d_mm, sizeof(double) * 2 * nblk,
-                            cudaMemcpyDeviceToHost, p->stream));
-    SE_CUDA(cudaStreamSynchronize(p->stream));
     double zmin = 1e300, zmax = -1e300;
-    for (int b = 0; b < nblk; ++b) { zmin = std::min(zmin, mm[2 * b]); zmax = std::max(zmax, mm[2 * b + 1]); }
-    // xy columns >= rc/2 wide (the 5 x 5 neighbour columns cover rc), z bins
-    // ~rc/8 high (the z window of a column is cut to whole bins)
+    if (in_domain) {
+        // charges lie in the extended domain [z0, z1] (checked by the spread),
+        // the mirror layers in its reflections: no device round trip
+        zmin = p->P.z0; zmax = p->P.z1;
+        if (nb) zmin = std::min(zmin, -p->P.z1);
+        if (nt) zmax = std::max(zmax, 2.0 * p->P.H - p->P.z0);
+    } else {
+        // z extent of the sources (one small device->host read)
+        int nblk = 64;
+        if (!p->d_mm) p->d_mm = dalloc<double>(p, 256);
+        zrange_kernel<<<nblk, 256, 0, p->stream>>>(p->d_near_src, ns, p->d_mm);
+        SE_LAUNCHED(p);
+        std::vector<double> mm(2 * nblk);
+        SE_CUDA(cudaMemcpyAsync(mm.data(), p->d_mm, sizeof(double) * 2 * nblk,
+                                cudaMemcpyDeviceToHost, p->stream));
+        SE_CUDA(cudaStreamSynchronize(p->stream));
+        for (int b = 0; b < nblk; ++b) { zmin = std::min(zmin, mm[2 * b]); zmax = std::max(zmax, mm[2 * b + 1]); }
+    }
     const double rc = std::max(p->P.r_cut, p->P.r_nf);
     cl.ncx = std::max(1, (int)std::floor(p->P.Lx / (0.5 * rc)));
     cl.ncy = std::max(1, (int)std::floor(p->P.Ly / (0.5 * rc)));
