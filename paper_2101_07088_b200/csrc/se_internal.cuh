@@ -139,6 +139,13 @@ struct NearLists {
 };
 
 // scratch of near_eval: evaluation points sorted by cell, one-cell warp tasks
+// cached close-pair kernel table (se_near.cu)
+struct CloseFit {
+    bool valid = false, ok = false;
+    double c1 = 0, c2 = 0, inv4pie = 0, rhi = 0, w = 0;
+    double* dev = nullptr;
+};
+
 struct NearScratch {
     int64_t pcap = 0, ccap = 0, tcap = 0;
     uint32_t *keys = nullptr, *keys2 = nullptr;
@@ -268,6 +275,7 @@ struct Plan {
     CellList cl;
     NearScratch ns;
     NearLists nl;
+    CloseFit close_fit[2];
     int64_t cl_cap = 0;
     uint32_t* d_ckeys = nullptr;
     uint32_t* d_ckeys2 = nullptr;

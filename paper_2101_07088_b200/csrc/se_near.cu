@@ -146,6 +146,10 @@ struct NearArgs {
     int use_poly;
     double pmid, pinvh;
     double pc[19];
+    // close pairs: g(r) and coef(r) as CL_P piecewise degree-CL_D polynomials
+    // in r on [0, CL_P cl_w) (table staged in shared memory by the close
+    // launch); use_ctab = 0 evaluates the erf formulas
+    const double* ctab; int use_ctab; double cl_w, cl_iw;
     double* out; int64_t out_stride;   // out[c * stride + i]
     int64_t* npairs;
     void* stats;
@@ -155,6 +159,8 @@ struct NearArgs {
 
 constexpr int NB_THREADS = 128;
 constexpr int FAR_DEG = 18;
+constexpr int CL_P = 32, CL_D = 12;             // close-pair table: pieces, degree
+constexpr int CL_TAB = 2 * CL_P * (CL_D + 1);
 constexpr int NQ = 48;            // per-lane far-pair queue (shared memory)
 constexpr int NQC = 12;           // per-lane close-pair queue
 
@@ -223,6 +229,20 @@ __device__ __forceinline__ void pair_terms(const NearArgs& a, const double* tab,
     }
     const double rinv = (FAR || r2 > 1e-280) ? rsqrt_pos(r2) : rsqrt(r2);
     const double r = r2 * rinv;
+    if (!FAR && a.use_ctab) {
+        const double* ct = tab + SE_ERFCX_NP * (SE_ERFCX_DEG + 1);
+        int pc = (int)(r * a.cl_iw);
+        pc = pc < CL_P - 1 ? pc : CL_P - 1;
+        const double t = (r - (pc + 0.5) * a.cl_w) * (2.0 * a.cl_iw);
+        const double* cg = ct + pc * (CL_D + 1);
+        const double* cc = ct + (CL_P + pc) * (CL_D + 1);
+        double gv = cg[CL_D], cv = cc[CL_D];
+#pragma unroll
+        for (int j = CL_D - 1; j >= 0; --j) { gv = fma(gv, t, cg[j]); cv = fma(cv, t, cc[j]); }
+        g = gv;
+        coef = nd ? cv : 0.0;
+        return;
+    }
     const double x2 = r * a.ic2;
     double E2, C2, e2;
     if (FAR && a.use_poly) {
@@ -490,11 +510,14 @@ __device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, 
 // lists (general kernel) add to them.
 template <bool FAR, int MINB>
 __global__ void __launch_bounds__(NB_THREADS, MINB) near_eval_kernel(NearArgs a) {
-    __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1)];
+    __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + (FAR ? 0 : CL_TAB)];
     const int tid = threadIdx.x, lane = tid & 31;
     if (!FAR || !a.use_poly) {
         for (int e = tid; e < SE_ERFCX_NP * (SE_ERFCX_DEG + 1); e += blockDim.x)
             tab[e] = (&se_erfcx_tab[0][0])[e];
+        if (!FAR && a.use_ctab)
+            for (int e = tid; e < CL_TAB; e += blockDim.x)
+                tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + e] = a.ctab[e];
         __syncthreads();
     }
     const int64_t task = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
@@ -852,6 +875,84 @@ static bool fit_far_poly(double xa, double xb, double* mid, double* inv_half, do
     return true;
 }
 
+// The general near kernel on the host (same formulas as pair_terms<false>,
+// libm erf / exp): g(r) and coef(r) = -g'(r)/r, r > 0.
+static void kernel_host(const NearKernel& k, double r, double* g, double* coef) {
+    const double ic1 = 1.0 / k.c1, ic2 = 1.0 / k.c2, ts = 2.0 / std::sqrt(M_PI);
+    const double x1 = r * ic1, x2 = r * ic2;
+    const double E1 = (r <= 6.5 * k.c1) ? std::erf(x1) : 1.0, E2 = std::erf(x2);
+    const double e1 = std::exp(-x1 * x1), e2 = std::exp(-x2 * x2);
+    const double v1 = (r < 1e-10 * k.c1) ? ts * ic1 : E1 / r;
+    const double v2 = (r < 1e-10 * k.c2) ? ts * ic2 : E2 / r;
+    *g = (v1 - v2) * k.inv4pie;
+    auto series = [&](double x, double ic) {
+        const double u = x * x;
+        return ts * (ic * ic) * x * (-2.0 / 3.0 + u * (2.0 / 5.0 + u * (-1.0 / 7.0 + u / 27.0)));
+    };
+    double d1, d2;
+    if (r > 6.5 * k.c1) d1 = -1.0 / (r * r);
+    else if (r < 1e-2 * k.c1) d1 = series(x1, ic1);
+    else d1 = ts * e1 * ic1 / r - v1 / r;
+    if (r < 1e-2 * k.c2) d2 = series(x2, ic2);
+    else d2 = ts * e2 * ic2 / r - v2 / r;
+    *coef = -((d1 - d2) * k.inv4pie) / r;
+}
+
+// Piecewise Chebyshev fit of g and coef on [0, rhi]: CL_P pieces, degree
+// CL_D, monomial in the local variable t in [-1, 1].  Accepted when the error
+// at 33 points per piece is below 1e-13 (g) / 1e-11 (coef) of the largest
+// value.
+static bool fit_close_table(const NearKernel& k, double rhi, std::vector<double>& tab,
+                            double* w_out) {
+    const int n = CL_D + 1;
+    const double w = rhi / CL_P;
+    tab.assign(CL_TAB, 0.0);
+    double gmax = 0, cmax = 0, gerr = 0, cerr = 0;
+    std::vector<double> fg(n), fc(n), c(n), mono(n);
+    for (int pc = 0; pc < CL_P; ++pc) {
+        const double mid = (pc + 0.5) * w, h = 0.5 * w;
+        for (int q = 0; q < n; ++q) {
+            const double r = mid + h * std::cos(M_PI * (q + 0.5) / n);
+            kernel_host(k, r, &fg[q], &fc[q]);
+        }
+        for (int f = 0; f < 2; ++f) {
+            const std::vector<double>& fv = f ? fc : fg;
+            for (int j = 0; j < n; ++j) {
+                double acc = 0;
+                for (int q = 0; q < n; ++q) acc += fv[q] * std::cos(M_PI * j * (q + 0.5) / n);
+                c[j] = acc * (j == 0 ? 1.0 : 2.0) / n;
+            }
+            std::vector<double> tp(n, 0.0), tc(n, 0.0), tn(n, 0.0);
+            std::fill(mono.begin(), mono.end(), 0.0);
+            tp[0] = 1.0; mono[0] += c[0];
+            if (n > 1) { tc[1] = 1.0; mono[1] += c[1]; }
+            for (int j = 2; j < n; ++j) {
+                for (int i2 = 0; i2 < n; ++i2) tn[i2] = (i2 > 0 ? 2.0 * tc[i2 - 1] : 0.0) - tp[i2];
+                for (int i2 = 0; i2 < n; ++i2) mono[i2] += c[j] * tn[i2];
+                tp = tc; tc = tn;
+            }
+            for (int i2 = 0; i2 < n; ++i2) tab[(f * CL_P + pc) * n + i2] = mono[i2];
+        }
+        for (int q = 0; q <= 32; ++q) {
+            const double t = -1.0 + 2.0 * q / 32.0, r = mid + h * t;
+            if (r <= 0) continue;
+            double gx, cx;
+            kernel_host(k, r, &gx, &cx);
+            double ga = tab[(0 * CL_P + pc) * n + n - 1], ca = tab[(1 * CL_P + pc) * n + n - 1];
+            for (int j = n - 2; j >= 0; --j) {
+                ga = std::fma(ga, t, tab[(0 * CL_P + pc) * n + j]);
+                ca = std::fma(ca, t, tab[(1 * CL_P + pc) * n + j]);
+            }
+            gmax = std::max(gmax, std::fabs(gx)); cmax = std::max(cmax, std::fabs(cx));
+            gerr = std::max(gerr, std::fabs(ga - gx)); cerr = std::max(cerr, std::fabs(ca - cx));
+        }
+    }
+    *w_out = w;
+    // the formulas themselves carry ~1e-12 relative noise in coef where the
+    // derivative switches from its series to the closed form (cancellation)
+    return gerr <= 1e-13 * gmax && cerr <= 1e-11 * cmax;
+}
+
 static double r2_threshold(double radius) {
     // largest double t with sqrt(t) <= radius (IEEE sqrt on host == device)
     double t = radius * radius;
@@ -866,6 +967,7 @@ static double r2_threshold(double radius) {
 void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
                const NearKernel& k, double* d_out4, int64_t* d_npairs) {
     if (ne == 0) return;
+    bool close_ok = false;
     NearArgs a{};
     a.eval = d_eval; a.order = d_order; a.ne = ne;
     a.g = cell_geo(p);
@@ -880,6 +982,24 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     // close path needed below max(6.5 c1, 0.01 c2) (+margin for fp32 error)
     double rcl = std::max(6.5 * k.c1, 1e-2 * k.c2) * (1.0 + 1e-4) + 1e-6 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(p->cl.zlo));
     a.r2close = (float)(rcl * rcl);
+    {
+        // close-pair table, cached per kernel (rebuilt when the kernel changes)
+        const double rhi = rcl * 1.001;
+        CloseFit& cf = p->close_fit[k.kind ? 1 : 0];
+        if (!cf.valid || cf.c1 != k.c1 || cf.c2 != k.c2 || cf.inv4pie != k.inv4pie ||
+            cf.rhi != rhi) {
+            std::vector<double> h;
+            double w = 0;
+            cf.ok = fit_close_table(k, rhi, h, &w);
+            if (!cf.dev) cf.dev = dalloc<double>(p, CL_TAB);
+            SE_CUDA(cudaMemcpy(cf.dev, h.data(), sizeof(double) * CL_TAB, cudaMemcpyHostToDevice));
+            cf.c1 = k.c1; cf.c2 = k.c2; cf.inv4pie = k.inv4pie; cf.rhi = rhi; cf.w = w;
+            cf.valid = true;
+        }
+        a.ctab = cf.dev; a.use_ctab = 0;          // enabled for the close launch only
+        a.cl_w = cf.w; a.cl_iw = 1.0 / cf.w;
+        close_ok = cf.ok;
+    }
     {
         const double r_far = std::max(6.5 * k.c1, 1e-2 * k.c2);
         const double xa = r_far / k.c2 * (1.0 - 1e-6), xb = k.radius / k.c2 * (1.0 + 1e-6);
@@ -1001,7 +1121,9 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     if (d_npairs) p->ktic(5);
     near_eval_kernel<true, 8><<<nblk, NB_THREADS, 0, p->stream>>>(a);
     SE_LAUNCHED(p);
-    near_eval_kernel<false, 6><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+    NearArgs ac = a;
+    ac.use_ctab = close_ok ? 1 : 0;
+    near_eval_kernel<false, 6><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
     if (d_npairs) { p->ktoc(5); p->ktoc(3); }
     SE_LAUNCHED(p);
 }
