@@ -45,6 +45,10 @@ extern "C" {
 #define SE_CORRECTION      (1u << 4)
 #define SE_FORCE_GENERAL   (1u << 5)
 #define SE_TIMINGS         (1u << 6)   /* fill se_diag.t_ms (adds syncs) */
+#define SE_FP32            (1u << 7)   /* fp32 mode: near-field pair kernels in
+                                          single precision (pair membership stays
+                                          the exact fp64 test); results within
+                                          the run's Ewald tolerance */
 
 /* Solver parameters: the geometry plus the EwaldParams fields the device
  * path needs (params.py:28-50). */

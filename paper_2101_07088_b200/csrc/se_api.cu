@@ -168,6 +168,7 @@ void phase_charges(Plan* p, const double* d_pos, double* d_phi_out, double* d_E_
     NearKernel kavg{}, kpt{};
     if (!S.xi_inf) {
         kavg = kernel_of(P, 0, S.forces, S.flags & SE_SUBTRACT_SELF);
+        kavg.fp32 = (S.flags & SE_FP32) ? 1 : 0;
         kpt = kernel_of(P, 1, false, false);
     }
     if (!S.near_empty) {

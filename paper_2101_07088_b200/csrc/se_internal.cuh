@@ -360,6 +360,7 @@ struct NearKernel {
     double c1, c2, inv4pie, radius, self_value, point0;
     int kind;            // 0 avg, 1 point
     int need_field;
+    int fp32;            // far pairs in single precision (SE_FP32)
 };
 void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, bool in_domain);
 void near_eval(Plan* p, const double* d_eval, const int* d_eval_order,

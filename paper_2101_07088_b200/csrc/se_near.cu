@@ -218,10 +218,23 @@ __device__ __forceinline__ void erf_erfc(double x, const double* tab, double& er
 // its radial derivative over r (kernels.py:38-113, slab.py:162-177).
 // FAR: r > 6.5 c1 and r >= 0.01 c2, where erf(r/c1) == 1 in fp64 and
 // exp(-(r/c1)^2) is below 1e-17 of the kernel: erfc-only form.
-template <bool FAR>
+template <bool FAR, bool F32 = false>
 __device__ __forceinline__ void pair_terms(const NearArgs& a, const double* tab,
                                            double r2, double& g, double& coef) {
     const bool nd = a.need_field;
+    if (FAR && F32) {
+        // fp32 mode: the far kernel in single precision (erfcf, __expf);
+        // ~1e-6 relative per pair, far inside the Ewald tolerance
+        const float sr = (float)r2;
+        const float ri = rsqrtf(sr);
+        const float x = sr * ri * (float)a.ic2;
+        const float C = erfcf(x);
+        const float e = __expf(-x * x);
+        const float i4 = (float)a.inv4pie;
+        g = (double)(C * ri * i4);
+        coef = nd ? (double)((C * ri + 1.1283792f * e * (float)a.ic2) * (ri * ri) * i4) : 0.0;
+        return;
+    }
     if (!FAR && r2 == 0.0) {                     // slab.py:161-171,176
         g = (a.kind == 0) ? a.self_value : a.point0;
         coef = 0.0;
@@ -472,7 +485,7 @@ __global__ void __launch_bounds__(NB_THREADS, 10) near_scan_kernel(NearArgs a) {
     if (overflow) atomicOr(a.overflow, 1);
 }
 
-template <bool FAR>
+template <bool FAR, bool F32 = false>
 __device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, const int* list,
                                           int n, double px, double py, double pz, double& phi,
                                           double& ex, double& ey, double& ez, int& count) {
@@ -492,7 +505,7 @@ __device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, 
                                             __dmul_rn(dz, dz));
                 if (r2 <= a.r2max) {           // == sqrt(r2) <= r_query
                     double g, coef;
-                    pair_terms<FAR>(a, tab, r2, g, coef);
+                    pair_terms<FAR, F32>(a, tab, r2, g, coef);
                     phi = fma(sv.w, g, phi);
                     if (nd) {
                         const double cq = coef * sv.w;
@@ -508,7 +521,7 @@ __device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, 
 // Evaluation of one list kind per launch: the far lists (the bulk; erfc-only
 // kernel, small register footprint, high occupancy) write the sums, the close
 // lists (general kernel) add to them.
-template <bool FAR, int MINB>
+template <bool FAR, int MINB, bool F32 = false>
 __global__ void __launch_bounds__(NB_THREADS, MINB) near_eval_kernel(NearArgs a) {
     __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + (FAR ? 0 : CL_TAB)];
     const int tid = threadIdx.x, lane = tid & 31;
@@ -532,7 +545,7 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_eval_kernel(NearArgs a)
         i = a.order[slot];
         const double px = a.eval[3 * i], py = a.eval[3 * i + 1], pz = a.eval[3 * i + 2];
         if (FAR)
-            eval_list<true>(a, tab, a.list_far + slot * a.cap_far, a.cnt_far[slot], px, py, pz,
+            eval_list<true, F32>(a, tab, a.list_far + slot * a.cap_far, a.cnt_far[slot], px, py, pz,
                             phi, ex, ey, ez, count);
         else
             eval_list<false>(a, tab, a.list_close + slot * a.cap_close, a.cnt_close[slot], px,
@@ -1119,7 +1132,8 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         want_close *= 2;
     }
     if (d_npairs) p->ktic(5);
-    near_eval_kernel<true, 8><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+    if (k.fp32) near_eval_kernel<true, 8, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+    else near_eval_kernel<true, 8><<<nblk, NB_THREADS, 0, p->stream>>>(a);
     SE_LAUNCHED(p);
     NearArgs ac = a;
     ac.use_ctab = close_ok ? 1 : 0;

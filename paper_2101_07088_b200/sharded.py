@@ -53,9 +53,10 @@ class _DeviceArray:
 class CudaShardEngine:
     """The three solve phases of one rank on its GPU (se_shard_*)."""
 
-    def __init__(self, system, params, refine=1, device=0):
+    def __init__(self, system, params, refine=1, device=0, precision="fp64"):
         self.device = torch.device("cuda", device)
-        self.solver = SlabSolver(system, params, refine=refine, device=device)
+        self.solver = SlabSolver(system, params, refine=refine, device=device,
+                                 precision=precision)
         self.solver.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
         self._lib = self.solver._lib
 
@@ -104,7 +105,7 @@ class ShardedSlabSolver:
     the same system; ``solve`` returns the full result on every rank."""
 
     def __init__(self, system, params, threads=1, refine=1, group=None,
-                 device=None, engine=None):
+                 device=None, engine=None, precision="fp64"):
         if not dist.is_initialized():
             raise RuntimeError("ShardedSlabSolver needs torch.distributed "
                                "initialised (one process per GPU)")
@@ -120,8 +121,9 @@ class ShardedSlabSolver:
         if engine is None:
             if device is None:
                 device = torch.cuda.current_device()
-            engine = CudaShardEngine(system, params, refine, device)
+            engine = CudaShardEngine(system, params, refine, device, precision)
         self.engine = engine
+        self.precision = precision
         self.last_timings = None
 
     def close(self):
@@ -136,7 +138,7 @@ class ShardedSlabSolver:
         ``first .. first+count-1`` and U the total energy."""
         flags = _flags(need_energy, need_forces, need_potential,
                        subtract_self, include_correction, force_general,
-                       timings)
+                       timings, self.precision == "fp32")
         rho = self.engine.spread(pos_all, self.first, self.count, flags)
         if self.world > 1:
             dist.all_reduce(rho, group=self.group)

@@ -68,8 +68,10 @@ class SolveResult:
 
 
 def _flags(need_energy, need_forces, need_potential, subtract_self,
-           include_correction, force_general, timings=False):
+           include_correction, force_general, timings=False, fp32=False):
     f = 0
+    if fp32:
+        f |= _lib.FP32
     if need_energy:
         f |= _lib.NEED_ENERGY
     if need_forces:
@@ -92,11 +94,22 @@ STAGES = ("sources", "spread", "forward", "bvp", "inverse", "interp", "near",
           "k_near_eval")
 
 
+PRECISIONS = ("fp64", "fp32")
+
+
 class SlabSolver:
     """Reusable GPU solver: grids, BVP factorisations and wall data live in
-    a device plan created here (reference slab.py:194-233)."""
+    a device plan created here (reference slab.py:194-233).
 
-    def __init__(self, system, params, threads=1, refine=1, device=0):
+    ``precision="fp32"`` (not in the reference) evaluates the near-field pair
+    kernels in single precision; pair membership stays the exact fp64 test
+    and the results stay within the run's Ewald tolerance."""
+
+    def __init__(self, system, params, threads=1, refine=1, device=0,
+                 precision="fp64"):
+        if precision not in PRECISIONS:
+            raise ValueError("precision must be one of %s" % (PRECISIONS,))
+        self.precision = precision
         self.system = system
         self.params = params
         self.threads = threads
@@ -178,7 +191,7 @@ class SlabSolver:
         n = pos.shape[0]
         flags = _flags(need_energy, need_forces, need_potential,
                        subtract_self, include_correction, force_general,
-                       timings)
+                       timings, self.precision == "fp32")
         phi = np.empty(n)
         E = np.zeros((n, 3))
         U = ctypes.c_double(0.0)
@@ -202,7 +215,7 @@ class SlabSolver:
         device pointers (ints) on the plan's device.  Returns (U, diag)."""
         flags = _flags(need_energy, need_forces, need_potential,
                        subtract_self, include_correction, force_general,
-                       timings)
+                       timings, self.precision == "fp32")
         U = ctypes.c_double(0.0)
         diag = _lib.SeDiag()
         _lib.check(self._lib.se_solve_device(

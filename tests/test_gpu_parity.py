@@ -368,3 +368,30 @@ def test_shard_phase_order():
             ctypes.byref(size)))
     res = solver.solve()                  # a full solve still works after
     assert np.all(np.isfinite(res.phi_bar))
+
+
+# ---------------------------------------------------------------------------
+# fp32 mode (SE_FP32): near-field pair kernels in single precision; the pair
+# set is still the exact fp64 one, results within the Ewald tolerance delta
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("case", ["c2n256", "c3n256_gauss_sigma"])
+def test_fp32_mode_within_tolerance(case):
+    from paper_2101_07088_b200.slab import SlabSolver
+    from test_oracle_golden import variant_problem
+    system, params, kw = variant_problem(case)
+    kw.pop("refine", None)
+    g = solves()[case]
+    res = SlabSolver(system, params, precision="fp32").solve(**kw)
+    delta = params.delta
+    assert rel_l2(res.phi_bar, g["phi"]) < delta
+    assert rel_l2(res.E_bar, g["E"]) < delta
+    assert abs(res.U - g["U"]) <= delta * abs(g["U"])
+    ref64 = SlabSolver(system, params).solve(**kw)
+    assert res.diagnostics["n_pairs"] == ref64.diagnostics["n_pairs"]
+
+
+def test_fp32_mode_rejects_unknown_precision():
+    from paper_2101_07088_b200.slab import SlabSolver
+    system, params = W.build("c2", N=64)
+    with pytest.raises(ValueError):
+        SlabSolver(system, params, precision="bf16")
