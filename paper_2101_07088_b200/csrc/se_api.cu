@@ -214,6 +214,8 @@ void phase_results(Plan* p, double* U, se_diag* diag) {
     p->timing = false;
     if (hflags & FLAG_Z_OUTSIDE) throw Error(SE_ERR_VALUE, "point outside the extended z domain");
     if (hflags & FLAG_NONFINITE) throw Error(SE_ERR_FLOAT, "non-finite mismatch field");
+    if (hflags & FLAG_NEAR_BND)
+        throw Error(SE_ERR_CUDA, "too many near-field pairs at the exact cutoff distance");
     if (hflags & FLAG_K0_FAIL) {
         char buf[160];
         snprintf(buf, sizeof buf,
@@ -567,6 +569,9 @@ static Plan* light_plan(const se_params* params, int device) {
     p->dev = device;
     SE_CUDA(cudaSetDevice(device));
     SE_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    p->own_stream = true;
+    p->d_flags = dalloc<int>(p, 1);
+    SE_CUDA(cudaMemset(p->d_flags, 0, sizeof(int)));
     return p;
 }
 
@@ -659,9 +664,14 @@ int se_near_field(const se_params* params, int device, const double* pos, const 
         build_cells(p, d_pos, d_q, n, false);
         near_eval(p, d_ev, nullptr, ne, k, d_out, nullptr);
         std::vector<double> h(4 * ne);
+        int hflags = 0;
         SE_CUDA(cudaMemcpyAsync(h.data(), d_out, (need_field ? 4 : 1) * ne * sizeof(double),
                                 cudaMemcpyDeviceToHost, p->stream));
+        SE_CUDA(cudaMemcpyAsync(&hflags, p->d_flags, sizeof(int), cudaMemcpyDeviceToHost,
+                                p->stream));
         SE_CUDA(cudaStreamSynchronize(p->stream));
+        if (hflags & FLAG_NEAR_BND)
+            throw Error(SE_ERR_CUDA, "too many near-field pairs at the exact cutoff distance");
         std::copy(h.begin(), h.begin() + ne, phi);
         if (E && need_field)
             for (int64_t i = 0; i < ne; ++i)

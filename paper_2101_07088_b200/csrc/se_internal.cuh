@@ -78,6 +78,7 @@ enum : int {
     FLAG_NONFINITE = 2,      // dpsolver.py:83-86        FloatingPointError
     FLAG_K0_FAIL = 4,        // dpsolver.py:208-211      FloatingPointError
     FLAG_K0_WARN = 8,        // dpsolver.py:212-213      warning
+    FLAG_NEAR_BND = 16,      // boundary-pair buffer overflow (RuntimeError)
 };
 
 // ----------------------------------------------------------------------------
@@ -276,6 +277,9 @@ struct Plan {
     NearScratch ns;
     NearLists nl;
     CloseFit close_fit[2];
+    int2* d_bnd = nullptr;                // near pairs within ulps of the cutoff
+    int* d_bnd_cnt = nullptr;
+    int64_t bnd_cap = 0;
     int64_t cl_cap = 0;
     uint32_t* d_ckeys = nullptr;
     uint32_t* d_ckeys2 = nullptr;

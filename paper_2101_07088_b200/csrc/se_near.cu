@@ -98,6 +98,13 @@ __global__ void zrange_kernel(const double4* s, int64_t ns, double* mm) {
     }
 }
 
+// the reference's tree z origin: min(source z) - r_cut - 1 (slab.py:120)
+__global__ void zmin_kernel(const double* mm, int nblk, double r_cut, double* zmin) {
+    double lo = 1e300;
+    for (int b = 0; b < nblk; ++b) lo = fmin(lo, mm[2 * b]);
+    *zmin = __dsub_rn(__dsub_rn(lo, r_cut), 1.0);
+}
+
 __global__ void cell_keys_kernel(const double4* s, int64_t ns, CellGeo g,
                                  uint32_t* keys, int* perm) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -133,6 +140,11 @@ struct NearArgs {
     const int2* tasks; int64_t ntask; const int* ntask_dev; const int* pt_end;
     CellGeo g; const int* start; const double4* src; const float4* srcf;
     double r2max;                 // largest r2 with sqrt(r2) <= r_query
+    // the reference's KD-tree pre-test (slab.py:120-135, scipy cKDTree on
+    // (x mod Lx, y mod Ly, z - zmin), squared distance <= r*r) decides only
+    // within a few ulps of the cutoff: pairs with r2 >= win_lo repeat it
+    double rr, win_lo, lzbox; const double* zmin;
+    int2* bnd; int* bnd_cnt; int bnd_cap; int* flags;   // deferred boundary pairs
     double c1, c2, ic1, ic2, inv4pie, self_value, point0;
     int kind, need_field;
     float r2f;                    // fp32 pre-test bound (with margin)
@@ -311,6 +323,36 @@ __device__ __forceinline__ double min_image(double d, double L) {
     return __dsub_rn(d, __dmul_rn(L, rint(d / L)));
 }
 
+// numpy's float remainder (npy_divmod): fmod, moved into [0, L) for L > 0
+__device__ __forceinline__ double np_mod(double x, double L) {
+    double m = fmod(x, L);
+    if (m != 0.0) { if (m < 0.0) m = __dadd_rn(m, L); }
+    else m = 0.0;
+    return m;
+}
+
+__device__ __forceinline__ double box_wrap(double d, double L) {
+    const double h = 0.5 * L;
+    if (d > h) return __dsub_rn(d, L);
+    if (d < -h) return __dadd_rn(d, L);
+    return d;
+}
+
+// The reference's KD-tree test for one pair: coordinates shifted as in
+// NearField._shift (slab.py:126-131), periodic differences, squared
+// distance summed in dimension order, compared with fl(r*r).
+__device__ __noinline__ bool tree_keep_s(double Lx, double Ly, double lz, double zm, double rr,
+                                         double px, double py, double pz, double sx, double sy,
+                                         double sz) {
+    const double dx = box_wrap(__dsub_rn(np_mod(px, Lx), np_mod(sx, Lx)), Lx);
+    const double dy = box_wrap(__dsub_rn(np_mod(py, Ly), np_mod(sy, Ly)), Ly);
+    const double dz = box_wrap(__dsub_rn(__dsub_rn(pz, zm), __dsub_rn(sz, zm)), lz);
+    const double s2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    return s2 <= rr;
+}
+#define tree_keep(a, px, py, pz, sx, sy, sz) \
+    tree_keep_s((a).g.Lx, (a).g.Ly, (a).lzbox, *(a).zmin, (a).rr, px, py, pz, sx, sy, sz)
+
 // Butterfly transpose-reduction across the warp: lane l starts with 32
 // partial values v[0..31] and ends with the warp total of value index l.
 __device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) {
@@ -485,10 +527,19 @@ __global__ void __launch_bounds__(NB_THREADS, 10) near_scan_kernel(NearArgs a) {
     if (overflow) atomicOr(a.overflow, 1);
 }
 
+// pairs within ulps of the cutoff need the reference's KD-tree test too:
+// they are queued and settled by near_boundary_kernel (rare)
+__device__ __forceinline__ void defer_pair(const NearArgs& a, int64_t i, int j) {
+    const int slot = atomicAdd(a.bnd_cnt, 1);
+    if (slot < a.bnd_cap) a.bnd[slot] = make_int2((int)i, j);
+    else atomicOr(a.flags, FLAG_NEAR_BND);
+}
+
 template <bool FAR, bool F32 = false>
 __device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, const int* list,
-                                          int n, double px, double py, double pz, double& phi,
-                                          double& ex, double& ey, double& ez, int& count) {
+                                          int n, double px, double py, double pz, int64_t self_i,
+                                          double& phi, double& ex, double& ey, double& ez,
+                                          int& count) {
     const double Lx = a.g.Lx, Ly = a.g.Ly;
     const bool nd = a.need_field;
     for (int k = 0; k < n; k += 4) {
@@ -503,7 +554,9 @@ __device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, 
                 const double dz = __dsub_rn(pz, sv.z);
                 const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
                                             __dmul_rn(dz, dz));
-                if (r2 <= a.r2max) {           // == sqrt(r2) <= r_query
+                if (r2 >= a.win_lo && r2 <= a.r2max) {
+                    defer_pair(a, self_i, jj[u]);      // decided by near_boundary_kernel
+                } else if (r2 <= a.r2max) {            // == sqrt(r2) <= r_query
                     double g, coef;
                     pair_terms<FAR, F32>(a, tab, r2, g, coef);
                     phi = fma(sv.w, g, phi);
@@ -546,10 +599,10 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_eval_kernel(NearArgs a)
         const double px = a.eval[3 * i], py = a.eval[3 * i + 1], pz = a.eval[3 * i + 2];
         if (FAR)
             eval_list<true, F32>(a, tab, a.list_far + slot * a.cap_far, a.cnt_far[slot], px, py, pz,
-                            phi, ex, ey, ez, count);
+                                 i, phi, ex, ey, ez, count);
         else
             eval_list<false>(a, tab, a.list_close + slot * a.cap_close, a.cnt_close[slot], px,
-                             py, pz, phi, ex, ey, ez, count);
+                             py, pz, i, phi, ex, ey, ez, count);
         if (FAR) {
             a.out[i] = phi;
             if (a.need_field) {
@@ -615,7 +668,9 @@ __global__ void __launch_bounds__(256) near_few_kernel(NearArgs a) {
                 const double dz = __dsub_rn(pz, sv.z);
                 const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
                                             __dmul_rn(dz, dz));
-                if (r2 <= a.r2max) {
+                if (r2 >= a.win_lo && r2 <= a.r2max) {
+                    defer_pair(a, i, j);
+                } else if (r2 <= a.r2max) {
                     double g, coef;
                     pair_terms<false>(a, tab, r2, g, coef);
                     phi = fma(sv.w, g, phi);
@@ -654,6 +709,38 @@ __global__ void __launch_bounds__(256) near_few_kernel(NearArgs a) {
             a.out[3 * a.out_stride + i] = v[3];
         }
         if (a.npairs) atomicAdd((unsigned long long*)a.npairs, cnt);
+    }
+}
+
+// Deferred boundary pairs: the reference's KD-tree test, then the general
+// kernel; contributions added atomically (a handful of pairs per solve).
+__global__ void near_boundary_kernel(NearArgs a) {
+    __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1)];
+    for (int e = threadIdx.x; e < SE_ERFCX_NP * (SE_ERFCX_DEG + 1); e += blockDim.x)
+        tab[e] = (&se_erfcx_tab[0][0])[e];
+    __syncthreads();
+    const int n = min(*a.bnd_cnt, a.bnd_cap);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        const int2 pr = a.bnd[e];
+        const int64_t i = pr.x;
+        const double px = a.eval[3 * i], py = a.eval[3 * i + 1], pz = a.eval[3 * i + 2];
+        const double4 sv = a.src[pr.y];
+        const double dx = min_image(__dsub_rn(px, sv.x), a.g.Lx);
+        const double dy = min_image(__dsub_rn(py, sv.y), a.g.Ly);
+        const double dz = __dsub_rn(pz, sv.z);
+        const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                    __dmul_rn(dz, dz));
+        if (!tree_keep(a, px, py, pz, sv.x, sv.y, sv.z)) continue;
+        double g, coef;
+        pair_terms<false>(a, tab, r2, g, coef);
+        atomicAdd(a.out + i, sv.w * g);
+        if (a.need_field) {
+            const double cq = coef * sv.w;
+            atomicAdd(a.out + a.out_stride + i, cq * dx);
+            atomicAdd(a.out + 2 * a.out_stride + i, cq * dy);
+            atomicAdd(a.out + 3 * a.out_stride + i, cq * dz);
+        }
+        if (a.npairs) atomicAdd((unsigned long long*)a.npairs, 1ull);
     }
 }
 
@@ -797,6 +884,12 @@ void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, boo
     SrcBuild sb{d_pos, d_q, n, p->P.H, fb, ft, nb, nt, p->d_near_src, ns};
     make_near_sources<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(sb);
     SE_LAUNCHED(p);
+    // device copy of the reference's KD-tree z origin (boundary pair tests)
+    if (!p->d_mm) p->d_mm = dalloc<double>(p, 256);
+    zrange_kernel<<<64, 256, 0, p->stream>>>(p->d_near_src, ns, p->d_mm);
+    SE_LAUNCHED(p);
+    zmin_kernel<<<1, 1, 0, p->stream>>>(p->d_mm, 64, p->P.r_cut, p->d_mm + 200);
+    SE_LAUNCHED(p);
     double zmin = 1e300, zmax = -1e300;
     if (in_domain) {
         // charges lie in the extended domain [z0, z1] (checked by the spread),
@@ -807,9 +900,6 @@ void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, boo
     } else {
         // z extent of the sources (one small device->host read)
         int nblk = 64;
-        if (!p->d_mm) p->d_mm = dalloc<double>(p, 256);
-        zrange_kernel<<<nblk, 256, 0, p->stream>>>(p->d_near_src, ns, p->d_mm);
-        SE_LAUNCHED(p);
         std::vector<double> mm(2 * nblk);
         SE_CUDA(cudaMemcpyAsync(mm.data(), p->d_mm, sizeof(double) * 2 * nblk,
                                 cudaMemcpyDeviceToHost, p->stream));
@@ -986,6 +1076,23 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     a.g = cell_geo(p);
     a.start = p->cl.start; a.src = p->cl.src; a.srcf = p->cl.srcf;
     a.r2max = r2_threshold(k.radius);
+    a.rr = k.radius * k.radius;
+    a.win_lo = std::min(a.rr, a.r2max) * (1.0 - 1e-12);
+    a.lzbox = 1e300;                 // pairs near the cutoff never wrap in z
+    a.zmin = p->d_mm + 200;
+    {
+        const int64_t cap = std::max<int64_t>(4096, 8 * ne);
+        if (cap > p->bnd_cap) {
+            dfree(p, p->d_bnd); dfree(p, p->d_bnd_cnt);
+            p->d_bnd = dalloc<int2>(p, cap);
+            p->d_bnd_cnt = dalloc<int>(p, 1);
+            p->bnd_cap = cap;
+        }
+        SE_CUDA(cudaMemsetAsync(p->d_bnd_cnt, 0, sizeof(int), p->stream));
+        a.bnd = p->d_bnd; a.bnd_cnt = p->d_bnd_cnt;
+        a.bnd_cap = (int)std::min<int64_t>(p->bnd_cap, INT32_MAX);
+        a.flags = p->d_flags;
+    }
     a.c1 = k.c1; a.c2 = k.c2; a.ic1 = 1.0 / k.c1; a.ic2 = 1.0 / k.c2;
     a.inv4pie = k.inv4pie;
     a.self_value = k.self_value; a.point0 = k.point0;
@@ -1030,6 +1137,8 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     }
     if (ne <= FEW_POINTS) {
         near_few_kernel<<<(unsigned)ne, 256, 0, p->stream>>>(a);
+        SE_LAUNCHED(p);
+        near_boundary_kernel<<<4, 256, 0, p->stream>>>(a);
         SE_LAUNCHED(p);
         return;
     }
@@ -1138,6 +1247,8 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     NearArgs ac = a;
     ac.use_ctab = close_ok ? 1 : 0;
     near_eval_kernel<false, 6><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
+    SE_LAUNCHED(p);
+    near_boundary_kernel<<<4, 256, 0, p->stream>>>(a);
     if (d_npairs) { p->ktoc(5); p->ktoc(3); }
     SE_LAUNCHED(p);
 }
