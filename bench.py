@@ -13,8 +13,10 @@ phi and E inside the timed region.  L2 (126 MB) is flushed between timed steps
 by writing a 256 MB buffer outside the event pair.
 
 Multi-GPU (torchrun, one process per GPU): ONE system solved across the
-ranks (``ShardedSlabSolver``): charges split by index, each rank spreads its
-shard into full grids, NCCL all-reduce of the grids, replicated grid solve,
+ranks (``ShardedSlabSolver(decompose=True)``): charges split by index, each
+rank spreads its shard into full grids, NCCL reduce-scatter into z slabs,
+slab xy FFTs, all-to-all to (kx, ky) pencils, pencil z transforms + mode
+BVPs, all-to-all back, slab inverse FFTs, all-gather of the field grid,
 interpolation + near field for the rank's own charges, energy all-reduce
 (strong scaling).  Timing is the max over ranks of the
 summed per-step CUDA-event times.
@@ -52,6 +54,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded solver even on one rank")
+    ap.add_argument("--replicate-grid", action="store_true",
+                    help="N>1: replicate the grid pipeline on every rank "
+                         "instead of the slab / pencil decomposition")
     return ap.parse_args()
 
 
@@ -223,7 +228,8 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     if sharded:
         from paper_2101_07088_b200.sharded import ShardedSlabSolver
-        solver = ShardedSlabSolver(system, params, device=local)
+        solver = ShardedSlabSolver(system, params, device=local,
+                                   decompose=not args.replicate_grid)
 
         def step(timings=False):
             _, _, U, diag = solver.solve_shard(pos_d, timings=timings)
@@ -348,10 +354,15 @@ def run_ours(args):
                        "grid": [params.Nx, params.Ny, params.Nz],
                        "eps_b": system.geometry.eps_b,
                        "eps_t": system.geometry.eps_t, "delta": params.delta,
-                       "parallelism": ("shard%d: charges split by index, NCCL "
-                                       "all-reduce of the spread grids, "
-                                       "replicated grid solve, per-rank "
-                                       "interp + near field" % world)
+                       "parallelism": (("shard%d: charges split by index; grid "
+                                        "pipeline replicated after an NCCL "
+                                        "all-reduce" % world)
+                                       if args.replicate_grid else
+                                       ("shard%d: charges split by index; NCCL "
+                                        "reduce-scatter to z slabs, slab xy "
+                                        "FFTs, all-to-all to (kx,ky) pencils, "
+                                        "pencil DCT + BVPs, all-to-all back, "
+                                        "all-gather of the fields" % world))
                        if sharded else "single",
                        "l2": "flushed (256 MB write) between timed steps"},
             "e2e": {"value": n / (e2e_ms * 1e-3), "unit": "charges/s",
@@ -371,6 +382,9 @@ def main():
         run_reference(args)
     else:
         run_ours(args)
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -128,6 +128,25 @@ int se_shard_fields(se_plan* plan);
 int se_shard_charges(se_plan* plan, const double* d_pos_all, double* d_phi,
                      double* d_E, double* U_part, se_diag* diag);
 
+/* Distributed grid pipeline for a sharded solve: after
+ * se_dist_setup(plan, rank, nranks, sizes) a rank's solve is
+ *   se_shard_spread          -> caller: reduce-scatter  rho_full -> rho_slab
+ *   se_dist_forward          -> caller: all-to-all      a2a_send -> a2a_recv
+ *   se_dist_modes            -> caller: all-to-all      a2a_send -> a2a_recv
+ *                               caller: all-reduce(sum) dsc
+ *   se_dist_fields           -> caller: all-gather      fields_slab -> fields
+ *   se_shard_charges
+ * Rank r owns the z planes [r zc, (r+1) zc) for the xy FFTs and the
+ * half-spectrum modes [r mc, (r+1) mc) for the z transforms and BVPs.
+ * sizes[0..6] = doubles in rho_full, rho_slab, a2a forward block (all
+ * ranks), a2a back block (all ranks), fields_slab, fields, dsc;
+ * se_dist_buffers returns the seven device pointers in the same order. */
+int se_dist_setup(se_plan* plan, int rank, int nranks, int64_t* sizes);
+int se_dist_buffers(se_plan* plan, void** ptrs);
+int se_dist_forward(se_plan* plan);
+int se_dist_modes(se_plan* plan);
+int se_dist_fields(se_plan* plan);
+
 /* near_field_sum (slab.py:184-191): sources = pos[n] with charges q[n]
  * (plus the mirrored layers of the geometry in params), evaluated at
  * eval_pos[ne].  kind 0 = "avg" (r_cut), 1 = "point" (r_nf).  Host buffers.

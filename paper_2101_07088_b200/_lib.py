@@ -31,7 +31,9 @@ EXPORTS = ("se_plan_create", "se_plan_destroy", "se_plan_set_stream",
            "se_set_charges", "se_solve",
            "se_solve_device", "se_near_field", "se_build_partition",
            "se_debug_fetch", "se_fp64_peak", "se_last_error", "se_version",
-           "se_shard_spread", "se_shard_fields", "se_shard_charges")
+           "se_shard_spread", "se_shard_fields", "se_shard_charges",
+           "se_dist_setup", "se_dist_buffers", "se_dist_forward",
+           "se_dist_modes", "se_dist_fields")
 
 
 class SeParams(ctypes.Structure):
@@ -107,6 +109,13 @@ def load():
     lib.se_shard_charges.argtypes = [_P, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.c_void_p, _D, ctypes.POINTER(SeDiag)]
     lib.se_shard_charges.restype = ctypes.c_int
+    lib.se_dist_setup.argtypes = [_P, ctypes.c_int, ctypes.c_int, _I64P]
+    lib.se_dist_setup.restype = ctypes.c_int
+    lib.se_dist_buffers.argtypes = [_P, ctypes.POINTER(ctypes.c_void_p)]
+    lib.se_dist_buffers.restype = ctypes.c_int
+    for name in ("se_dist_forward", "se_dist_modes", "se_dist_fields"):
+        getattr(lib, name).argtypes = [_P]
+        getattr(lib, name).restype = ctypes.c_int
     lib.se_fp64_peak.argtypes = [ctypes.c_int, _D]
     lib.se_fp64_peak.restype = ctypes.c_int
     lib.se_last_error.argtypes = []

@@ -256,6 +256,184 @@ void phase_results(Plan* p, double* U, se_diag* diag) {
     S.timed = false;
 }
 
+// ---------------------------------------------------------------------------
+// distributed grid pipeline: spread grids summed by a
+// reduce-scatter into z slabs -> xy FFT of the slab -> all-to-all to (kx,ky)
+// pencils -> z DCT, mode BVPs, correction, inverse z DCT, assembly ->
+// all-to-all back to slabs -> inverse xy FFT -> all-gather of the fields.
+// The collectives are the caller's (NCCL through torch.distributed); the
+// library packs and unpacks contiguous per-rank blocks.
+// ---------------------------------------------------------------------------
+namespace {
+
+// hat slab [zc][2][M] -> send [P][zc][2][mc] (dest q: modes q mc ..)
+__global__ void pack_modes_kernel(const double2* hat, int64_t M, int64_t zc, int64_t mc, int P,
+                                  double2* send) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t per = zc * 2 * mc;
+    if (e >= (int64_t)P * per) return;
+    const int64_t q = e / per, r = e - q * per;
+    const int64_t row = r / mc, l = r - row * mc;       // row = plane * 2 + grid
+    const int64_t gm = q * mc + l;
+    send[e] = gm < M ? hat[row * M + gm] : make_double2(0, 0);
+}
+
+// recv [P][zc][F][mc] (from s: planes s zc ..) -> pencil [Nz][F][mc]
+__global__ void unpack_planes_kernel(const double2* recv, int64_t zc, int64_t mc, int F, int P,
+                                     int Nz, double2* pen) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t per = zc * F * mc;
+    if (e >= (int64_t)P * per) return;
+    const int64_t s = e / per, r = e - s * per;
+    const int64_t j = r / (F * mc), rest = r - j * F * mc;
+    const int64_t z = s * zc + j;
+    if (z < Nz) pen[z * F * mc + rest] = recv[e];
+}
+
+// pencil [Nz][4][mc] -> send [P][zc][4][mc] (dest q: planes q zc ..)
+__global__ void pack_planes_kernel(const double2* pen, int64_t zc, int64_t mc, int P, int Nz,
+                                   double2* send) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t per = zc * 4 * mc;
+    if (e >= (int64_t)P * per) return;
+    const int64_t q = e / per, r = e - q * per;
+    const int64_t j = r / (4 * mc), rest = r - j * 4 * mc;
+    const int64_t z = q * zc + j;
+    send[e] = z < Nz ? pen[z * 4 * mc + rest] : make_double2(0, 0);
+}
+
+// recv [P][zc][4][mc] (from s: modes s mc ..) -> spec slab [zc][4][M]
+__global__ void unpack_modes_kernel(const double2* recv, int64_t M, int64_t zc, int64_t mc, int P,
+                                    double2* spec) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t per = zc * 4 * mc;
+    if (e >= (int64_t)P * per) return;
+    const int64_t s = e / per, r = e - s * per;
+    const int64_t row = r / mc, l = r - row * mc;       // row = plane * 4 + field
+    const int64_t gm = s * mc + l;
+    if (gm < M) spec[row * M + gm] = recv[e];
+}
+
+// scalars of the mode stage to be summed over ranks: A_i, the k = 0
+// diagnostics (owner of mode 0 only) and the flag bits as counts
+__global__ void dsc_pack_kernel(const double* scal, const double* k0, const int* flags,
+                                int owner, double* dsc) {
+    for (int i = 0; i < 16; ++i) dsc[i] = 0.0;
+    if (owner) {
+        dsc[0] = scal[0];
+        for (int i = 0; i < 10; ++i) dsc[1 + i] = k0[i];
+        dsc[12] = (*flags & FLAG_K0_FAIL) ? 1.0 : 0.0;
+        dsc[13] = (*flags & FLAG_K0_WARN) ? 1.0 : 0.0;
+    }
+    dsc[11] = (*flags & FLAG_NONFINITE) ? 1.0 : 0.0;
+}
+
+__global__ void dsc_apply_kernel(const double* dsc, double* scal, double* k0, int* flags) {
+    scal[0] = dsc[0];
+    for (int i = 0; i < 10; ++i) k0[i] = dsc[1 + i];
+    int f = *flags;
+    if (dsc[11] > 0) f |= FLAG_NONFINITE;
+    if (dsc[12] > 0) f |= FLAG_K0_FAIL;
+    if (dsc[13] > 0) f |= FLAG_K0_WARN;
+    *flags = f;
+}
+
+}  // namespace
+
+static ModeView my_modes(const Plan* p) {
+    const int64_t m0 = (int64_t)p->rank * p->mc;
+    const int64_t mv = std::max<int64_t>(0, std::min<int64_t>(p->mc, p->M - m0));
+    return ModeView{p->mc, mv, m0};
+}
+
+void dist_setup(Plan* p, int rank, int nranks) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(SE_ERR_VALUE, "bad rank / nranks");
+    if (p->dist) throw Error(SE_ERR_VALUE, "plan already distributed");
+    const int64_t P = nranks;
+    p->rank = rank; p->nranks = nranks;
+    p->zc = (p->Nz + P - 1) / P;
+    p->mc = (p->M + P - 1) / P;
+    p->Nz_pad = p->zc * P;
+    // full grids padded to whole slabs (pad planes stay zero)
+    dfree(p, p->d_rho); dfree(p, p->d_fields);
+    p->d_rho = dalloc<double>(p, 2 * (size_t)p->Nz_pad * p->NXY);
+    p->d_fields = dalloc<double>(p, 4 * (size_t)p->Nz_pad * p->NXY);
+    SE_CUDA(cudaMemsetAsync(p->d_rho, 0, sizeof(double) * 2 * (size_t)p->Nz_pad * p->NXY, p->stream));
+    SE_CUDA(cudaMemsetAsync(p->d_fields, 0, sizeof(double) * 4 * (size_t)p->Nz_pad * p->NXY, p->stream));
+    p->d_rho_slab = dalloc<double>(p, 2 * (size_t)p->zc * p->NXY);
+    p->d_fields_slab = dalloc<double>(p, 4 * (size_t)p->zc * p->NXY);
+    const size_t a2a = (size_t)P * p->zc * 4 * p->mc;
+    p->d_a2a_send = dalloc<cufftDoubleComplex>(p, a2a);
+    p->d_a2a_recv = dalloc<cufftDoubleComplex>(p, a2a);
+    p->d_dsc = dalloc<double>(p, 16);
+    const int zc = (int)p->zc;
+    make_plan2d(&p->fft_fwd_slab, p->Nx, p->Ny, p->Nyh, CUFFT_D2Z, p->NXY, p->M, 2 * zc, p->stream);
+    make_plan2d(&p->fft_inv4_slab, p->Nx, p->Ny, p->Nyh, CUFFT_Z2D, p->M, p->NXY, 4 * zc, p->stream);
+    make_plan2d(&p->fft_inv1_slab, p->Nx, p->Ny, p->Nyh, CUFFT_Z2D, 4 * p->M, 4 * p->NXY, zc,
+                p->stream);
+    p->dist = true;
+}
+
+// phase 2a: xy FFT of the summed slab, packed for the all-to-all to pencils
+void dist_forward(Plan* p) {
+    Solve& S = current(p);
+    if (!p->dist) throw Error(SE_ERR_CUDA, "plan not distributed (se_dist_setup)");
+    if (S.phase != 1) throw Error(SE_ERR_CUDA, "se_dist_forward before se_shard_spread");
+    SE_CUFFT(cufftExecD2Z(p->fft_fwd_slab, p->d_rho_slab, p->d_hat));
+    const int64_t total = (int64_t)p->nranks * p->zc * 2 * p->mc;
+    pack_modes_kernel<<<(unsigned)((total + 255) / 256), 256, 0, p->stream>>>(
+        reinterpret_cast<const double2*>(p->d_hat), p->M, p->zc, p->mc, p->nranks,
+        reinterpret_cast<double2*>(p->d_a2a_send));
+    SE_LAUNCHED(p);
+    S.phase = 11;
+}
+
+// phase 2b: this rank's mode pencils: z DCT, BVPs, correction, inverse z DCT,
+// assembly; packed for the all-to-all back; mode-stage scalars in d_dsc
+void dist_modes(Plan* p) {
+    Solve& S = current(p);
+    if (S.phase != 11) throw Error(SE_ERR_CUDA, "se_dist_modes before se_dist_forward");
+    const ModeView v = my_modes(p);
+    const int64_t tot2 = (int64_t)p->nranks * p->zc * 2 * p->mc;
+    unpack_planes_kernel<<<(unsigned)((tot2 + 255) / 256), 256, 0, p->stream>>>(
+        reinterpret_cast<const double2*>(p->d_a2a_recv), p->zc, p->mc, 2, p->nranks, p->Nz,
+        reinterpret_cast<double2*>(p->d_hat));
+    SE_LAUNCHED(p);
+    z_forward(p, v);
+    mark(p, S);
+    bvp_solve_view(p, S.two, S.mode, S.corr, v);
+    mark(p, S);
+    z_inverse_assemble(p, S.forces, S.corr, v);
+    const int64_t tot4 = (int64_t)p->nranks * p->zc * 4 * p->mc;
+    pack_planes_kernel<<<(unsigned)((tot4 + 255) / 256), 256, 0, p->stream>>>(
+        reinterpret_cast<const double2*>(p->d_spec), p->zc, p->mc, p->nranks, p->Nz,
+        reinterpret_cast<double2*>(p->d_a2a_send));
+    SE_LAUNCHED(p);
+    dsc_pack_kernel<<<1, 1, 0, p->stream>>>(p->d_scal, p->d_k0, p->d_flags, v.m0 == 0 ? 1 : 0,
+                                            p->d_dsc);
+    SE_LAUNCHED(p);
+    S.phase = 12;
+}
+
+// phase 2c: summed scalars applied, spectra of this rank's planes unpacked,
+// inverse xy FFT into the field slab (the caller all-gathers the slabs into
+// the full field grid before se_shard_charges)
+void dist_fields(Plan* p) {
+    Solve& S = current(p);
+    if (S.phase != 12) throw Error(SE_ERR_CUDA, "se_dist_fields before se_dist_modes");
+    dsc_apply_kernel<<<1, 1, 0, p->stream>>>(p->d_dsc, p->d_scal, p->d_k0, p->d_flags);
+    SE_LAUNCHED(p);
+    const int64_t tot4 = (int64_t)p->nranks * p->zc * 4 * p->mc;
+    unpack_modes_kernel<<<(unsigned)((tot4 + 255) / 256), 256, 0, p->stream>>>(
+        reinterpret_cast<const double2*>(p->d_a2a_recv), p->M, p->zc, p->mc, p->nranks,
+        reinterpret_cast<double2*>(p->d_spec));
+    SE_LAUNCHED(p);
+    if (S.forces) SE_CUFFT(cufftExecZ2D(p->fft_inv4_slab, p->d_spec, p->d_fields_slab));
+    else SE_CUFFT(cufftExecZ2D(p->fft_inv1_slab, p->d_spec, p->d_fields_slab));
+    mark(p, S);
+    S.phase = 2;
+}
+
 void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
                 double* d_phi_out, double* d_E_out, double* U, se_diag* diag) {
     phase_spread(p, d_pos, n, 0, n, flags);
@@ -476,7 +654,8 @@ void se_plan_destroy(se_plan* plan) {
     if (!p) return;
     cudaSetDevice(p->dev);
     if (p->stream) cudaStreamSynchronize(p->stream);
-    cufftHandle hs[] = {p->fft_fwd2, p->fft_fwd1, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig};
+    cufftHandle hs[] = {p->fft_fwd2, p->fft_fwd1, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig,
+                        p->fft_fwd_slab, p->fft_inv4_slab, p->fft_inv1_slab};
     for (auto h : hs) if (h) cufftDestroy(h);
     if (p->blas) cublasDestroy(p->blas);
     for (auto& b : p->owned) if (b.p) cudaFree(b.p);
@@ -493,7 +672,8 @@ int se_plan_set_stream(se_plan* plan, void* stream) {
         SE_CUDA(cudaStreamSynchronize(p->stream));
         if (p->own_stream && p->stream) { cudaStreamDestroy(p->stream); p->own_stream = false; }
         p->stream = reinterpret_cast<cudaStream_t>(stream);
-        cufftHandle hs[] = {p->fft_fwd2, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig};
+        cufftHandle hs[] = {p->fft_fwd2, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig,
+                            p->fft_fwd_slab, p->fft_inv4_slab, p->fft_inv1_slab};
         for (auto h : hs) if (h) SE_CUFFT(cufftSetStream(h, p->stream));
         if (p->blas) SE_CUBLAS(cublasSetStream(p->blas, p->stream));
         return SE_OK;
@@ -615,6 +795,76 @@ int se_shard_charges(se_plan* plan, const double* d_pos_all, double* d_phi, doub
         SE_CUDA(cudaSetDevice(p->dev));
         phase_charges(p, d_pos_all, d_phi, d_E);
         phase_results(p, U_part, diag);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_dist_setup(se_plan* plan, int rank, int nranks, int64_t* sizes) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        SE_CUDA(cudaSetDevice(p->dev));
+        dist_setup(p, rank, nranks);
+        if (sizes) {
+            sizes[0] = 2 * p->Nz_pad * p->NXY;        // full grids (doubles)
+            sizes[1] = 2 * p->zc * p->NXY;            // grid slab
+            sizes[2] = 2 * (int64_t)p->nranks * p->zc * 2 * p->mc;   // all-to-all forward
+            sizes[3] = 2 * (int64_t)p->nranks * p->zc * 4 * p->mc;   // all-to-all back
+            sizes[4] = 4 * p->zc * p->NXY;            // field slab
+            sizes[5] = 4 * p->Nz_pad * p->NXY;        // full fields
+            sizes[6] = 16;                            // summed scalars
+        }
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_dist_buffers(se_plan* plan, void** ptrs) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p || !p->dist) throw Error(SE_ERR_VALUE, "plan not distributed");
+        ptrs[0] = p->d_rho; ptrs[1] = p->d_rho_slab; ptrs[2] = p->d_a2a_send;
+        ptrs[3] = p->d_a2a_recv; ptrs[4] = p->d_fields_slab; ptrs[5] = p->d_fields;
+        ptrs[6] = p->d_dsc;
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_dist_forward(se_plan* plan) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        SE_CUDA(cudaSetDevice(p->dev));
+        dist_forward(p);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_dist_modes(se_plan* plan) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        SE_CUDA(cudaSetDevice(p->dev));
+        dist_modes(p);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_dist_fields(se_plan* plan) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        SE_CUDA(cudaSetDevice(p->dev));
+        dist_fields(p);
         return SE_OK;
     } catch (const Error& e) {
         return fail(e);

@@ -315,6 +315,19 @@ struct Plan {
 
     cufftHandle fft_fwd2 = 0, fft_fwd1 = 0, fft_z = 0, fft_inv4 = 0,
                 fft_inv1 = 0, fft_sig = 0;
+
+    // distributed grid pipeline (se_dist_*): rank `rank` of `nranks` owns the
+    // z planes [rank zc, (rank+1) zc) for the xy FFTs and the half-spectrum
+    // modes [rank mc, (rank+1) mc) for the z transforms and mode BVPs
+    bool dist = false;
+    int rank = 0, nranks = 1;
+    int64_t zc = 0, mc = 0, Nz_pad = 0;
+    double* d_rho_slab = nullptr;         // [zc][2][Nx][Ny]
+    double* d_fields_slab = nullptr;      // [zc][4][Nx][Ny]
+    cufftDoubleComplex* d_a2a_send = nullptr;   // [P][zc][4][mc]
+    cufftDoubleComplex* d_a2a_recv = nullptr;
+    double* d_dsc = nullptr;              // k = 0 / flag scalars summed over ranks
+    cufftHandle fft_fwd_slab = 0, fft_inv4_slab = 0, fft_inv1_slab = 0;
     void* fft_work = nullptr;
 
     std::vector<Buf> owned;
@@ -354,7 +367,16 @@ void interp_points(Plan* p, const double* d_pts, int64_t npts, double width,
 void ensure_sources(Plan* p, int64_t cap);
 
 // --- se_spectral.cu ---
+// a contiguous range of (kx, ky) half-spectrum modes held with column stride M
+struct ModeView {
+    int64_t M;     // stride (columns per row)
+    int64_t Mv;    // valid modes
+    int64_t m0;    // global index of the first
+};
 void factor_bvp(Plan* p);
+void z_forward(Plan* p, const ModeView& v);
+void bvp_solve_view(Plan* p, bool two_grids, int mode, bool correction, const ModeView& v);
+void z_inverse_assemble(Plan* p, bool forces, bool correction, const ModeView& v);
 void forward_transforms(Plan* p, bool two_grids);
 void bvp_solve(Plan* p, bool two_grids, int mode, bool correction);
 void inverse_transforms(Plan* p, bool forces, bool correction);

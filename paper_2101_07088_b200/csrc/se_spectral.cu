@@ -124,7 +124,8 @@ __global__ void mirror_kernel(double2* ext, int N, int64_t row) {
 // ---------------------------------------------------------------------------
 struct BvpArgs {
     Maps mp;
-    int Nz, Nx, Nyh; int64_t M;
+    int Nz, Nx, Nyh; int64_t M;  // M: mode stride of the scratch / ext columns
+    int64_t Mv;                  // modes to solve (< M on the last pencil rank)
     double half, eps, eps_b, eps_t, cb, ct, z0, z1, k_max, k0_scale;
     int refine, two, mode;       // mode 0 jump, 1 plain+sigma, 2 plain
     int correction;              // compute correction moments
@@ -401,8 +402,8 @@ __global__ void __launch_bounds__(64) bvp_kernel(BvpArgs a) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int g = (int)(tid & 1);
     const int64_t mm = tid >> 1;
-    const bool valid = mm < a.M;
-    const int64_t m = valid ? mm : a.M - 1;
+    const bool valid = mm < a.Mv;
+    const int64_t m = valid ? mm : (a.Mv > 0 ? a.Mv - 1 : 0);
     double2 w[4], e[2];
     for (int q = 0; q < 4; ++q) w[q] = make_double2(0, 0);
     e[0] = e[1] = make_double2(0, 0);
@@ -490,6 +491,7 @@ struct AsmArgs {
     const double2* ext; double2* spec; const double2* mom;
     const double* kx; const double* ky; const double* kmag; const unsigned char* sel;
     const double* z; int Nz, Nx, Ny, Nyh; int64_t M;
+    int64_t Mv, m0;              // valid modes, global index of local mode 0
     int w0, w1;                  // correction window [w0, w1)
     int corr, forces;
     double rb, rt, H;
@@ -500,6 +502,7 @@ __global__ void assemble_kernel(AsmArgs a) {
     if (e >= (int64_t)a.Nz * a.M) return;
     int j = (int)(e / a.M);
     int64_t m = e % a.M;
+    if (m >= a.Mv) return;
     const int64_t RS = 2 * a.M;
     // iDCT halves: value at node j = E_j + O_j, at node N - j = E_j - O_j
     const int Pe = (a.Nz + 1) / 2, Po = a.Nz / 2;
@@ -527,7 +530,8 @@ __global__ void assemble_kernel(AsmArgs a) {
     double2* out = a.spec + (int64_t)j * 4 * a.M + m;
     out[0] = v;
     if (a.forces) {
-        int ix = (int)(m / a.Nyh), iy = (int)(m % a.Nyh);
+        const int64_t gm = a.m0 + m;
+        int ix = (int)(gm / a.Nyh), iy = (int)(gm % a.Nyh);
         double ikx = (a.Nx % 2 == 0 && ix == a.Nx / 2) ? 0.0 : a.kx[ix];
         double iky = (a.Ny % 2 == 0 && iy == a.Ny / 2) ? 0.0 : a.ky[iy];
         out[a.M] = make_double2(-ikx * v.y, ikx * v.x);        // i kx v
@@ -636,9 +640,8 @@ void factor_bvp(Plan* p) {
 // cuFFT); as a 258 x 258 matrix it runs on the FP64 tensor pipe.
 // out (W x cols, ldo) = in (W x k, ldi) * D^T with D (cols x k) column-major;
 // W x k column-major == row-major [k][W] (z-slowest rows)
-static void z_gemm(Plan* p, const double* D, int cols, int k, const double* in, int64_t ldi,
-                   double* out, int64_t ldo) {
-    const int64_t W = 4 * p->M;
+static void z_gemm(Plan* p, int64_t W, const double* D, int cols, int k, const double* in,
+                   int64_t ldi, double* out, int64_t ldo) {
     const double one = 1.0, zero = 0.0;
     SE_CUBLAS(cublasDgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_T, (int)W, cols, k, &one, in, (int)ldi,
                           D, cols, &zero, out, (int)ldo));
@@ -662,26 +665,37 @@ __global__ void fold_kernel(const double* v, int n, int64_t W, double* s, double
     }
 }
 
-void forward_transforms(Plan* p, bool two_grids) {
-    (void)two_grids;
-    SE_CUFFT(cufftExecD2Z(p->fft_fwd2, p->d_rho, p->d_hat));
+// z DCT-I of the xy spectra in d_hat ([Nz][2][M] for the mode view) into
+// the Chebyshev coefficients d_ext (same layout)
+void z_forward(Plan* p, const ModeView& v) {
     const int n = p->Nz, Pe = (n + 1) / 2, Po = n / 2;
-    const int64_t W = 4 * p->M;
+    const int64_t W = 4 * v.M;
     double* S = reinterpret_cast<double*>(p->d_scr);   // BVP scratch, free here
     double* D = S + (int64_t)Pe * W;
     fold_kernel<<<(unsigned)(((int64_t)Pe * W + 255) / 256), 256, 0, p->stream>>>(
         reinterpret_cast<const double*>(p->d_hat), n, W, S, D);
     SE_LAUNCHED(p);
     double* ext = reinterpret_cast<double*>(p->d_ext);
-    z_gemm(p, p->d_dct_fwd, Pe, Pe, S, W, ext, 2 * W);                     // even rows
+    z_gemm(p, W, p->d_dct_fwd, Pe, Pe, S, W, ext, 2 * W);                     // even rows
     if (Po > 0)
-        z_gemm(p, p->d_dct_fwd + (size_t)Pe * Pe, Po, Po, D, W, ext + W, 2 * W);   // odd rows
+        z_gemm(p, W, p->d_dct_fwd + (size_t)Pe * Pe, Po, Po, D, W, ext + W, 2 * W);   // odd rows
+}
+
+void forward_transforms(Plan* p, bool two_grids) {
+    (void)two_grids;
+    SE_CUFFT(cufftExecD2Z(p->fft_fwd2, p->d_rho, p->d_hat));
+    z_forward(p, ModeView{p->M, p->M, 0});
 }
 
 void bvp_solve(Plan* p, bool two_grids, int mode, bool correction) {
+    bvp_solve_view(p, two_grids, mode, correction, ModeView{p->M, p->M, 0});
+}
+
+void bvp_solve_view(Plan* p, bool two_grids, int mode, bool correction, const ModeView& v) {
     BvpArgs a{};
+    const bool whole = v.m0 == 0 && v.M == p->M;
     a.mp = maps_of(p, p->d_maps);
-    a.Nz = p->Nz; a.Nx = p->Nx; a.Nyh = p->Nyh; a.M = p->M;
+    a.Nz = p->Nz; a.Nx = p->Nx; a.Nyh = p->Nyh; a.M = v.M; a.Mv = v.Mv;
     a.half = 0.5 * (p->P.z1 - p->P.z0);
     a.eps = p->P.eps; a.eps_b = p->P.eps_b; a.eps_t = p->P.eps_t;
     a.cb = 2.0 * p->P.eps / (p->P.eps_b + p->P.eps);
@@ -689,47 +703,56 @@ void bvp_solve(Plan* p, bool two_grids, int mode, bool correction) {
     a.z0 = p->P.z0; a.z1 = p->P.z1; a.k_max = p->P.k_max; a.k0_scale = p->k0_scale;
     a.refine = p->P.refine; a.two = two_grids ? 1 : 0; a.mode = mode;
     a.correction = correction ? 1 : 0;
-    a.kidx = p->d_kidx; a.kmag = p->d_kmag; a.sel = p->d_sel;
+    // per-mode tables seen from the view's first mode
+    a.kidx = p->d_kidx + v.m0; a.kmag = p->d_kmag + v.m0; a.sel = p->d_sel + v.m0;
     a.fac = p->d_fac; a.sinv = p->d_sinv; a.kappa = p->d_kappa;
     a.tw0 = p->d_tw0; a.twH = p->d_twH;
-    a.sbh = reinterpret_cast<const double2*>(p->d_sbh);
-    a.sth = reinterpret_cast<const double2*>(p->d_sth);
+    a.sbh = reinterpret_cast<const double2*>(p->d_sbh) + v.m0;
+    a.sth = reinterpret_cast<const double2*>(p->d_sth) + v.m0;
     a.ext = reinterpret_cast<double2*>(p->d_ext);
     a.scrF = reinterpret_cast<double2*>(p->d_scr);
-    a.scrA = a.scrF + (int64_t)p->Nz * 2 * p->M;
-    a.scrB = a.scrA + (int64_t)p->Nz * 2 * p->M;
+    a.scrA = a.scrF + (int64_t)p->Nz * 2 * v.M;
+    a.scrB = a.scrA + (int64_t)p->Nz * 2 * v.M;
     a.inv_nxy = 1.0 / (double)p->NXY;
     a.mom = reinterpret_cast<double2*>(p->d_mom);
-    a.mism = reinterpret_cast<double2*>(p->d_mism);
-    a.keep = p->keep_stages ? reinterpret_cast<double2*>(p->d_keep) : nullptr;
+    a.mism = whole ? reinterpret_cast<double2*>(p->d_mism) : nullptr;
+    a.keep = (whole && p->keep_stages) ? reinterpret_cast<double2*>(p->d_keep) : nullptr;
     a.k0out = p->d_k0; a.scal = p->d_scal; a.flags = p->d_flags;
     a.rb = p->P.eps_b / p->P.eps; a.rt = p->P.eps_t / p->P.eps; a.H = p->P.H;
     p->ktic(1);
-    bvp_kernel<<<(unsigned)((2 * p->M + 63) / 64), 64, 0, p->stream>>>(a);
+    bvp_kernel<<<(unsigned)((2 * v.M + 63) / 64), 64, 0, p->stream>>>(a);
     p->ktoc(1);
     SE_LAUNCHED(p);
 }
 
-void inverse_transforms(Plan* p, bool forces, bool correction) {
+// inverse z DCT-I of the mode view and the assembly of the four spectral
+// fields into d_spec ([Nz][4][M] of the view)
+void z_inverse_assemble(Plan* p, bool forces, bool correction, const ModeView& v) {
     // E (rows 0..Pe-1) from the even coefficients, O (rows Pe..) from the odd
     const int n = p->Nz, Pe = (n + 1) / 2, Po = n / 2;
-    const int64_t W = 4 * p->M;
+    const int64_t W = 4 * v.M;
     const double* ext = reinterpret_cast<const double*>(p->d_ext);
     double* hat = reinterpret_cast<double*>(p->d_hat);
-    z_gemm(p, p->d_dct_inv, Pe, Pe, ext, 2 * W, hat, W);
+    z_gemm(p, W, p->d_dct_inv, Pe, Pe, ext, 2 * W, hat, W);
     if (Po > 0)
-        z_gemm(p, p->d_dct_inv + (size_t)Pe * Pe, Po, Po, ext + W, 2 * W, hat + (int64_t)Pe * W, W);
+        z_gemm(p, W, p->d_dct_inv + (size_t)Pe * Pe, Po, Po, ext + W, 2 * W,
+               hat + (int64_t)Pe * W, W);
     AsmArgs a{};
     a.ext = reinterpret_cast<const double2*>(p->d_hat);
     a.spec = reinterpret_cast<double2*>(p->d_spec);
     a.mom = reinterpret_cast<const double2*>(p->d_mom);
-    a.kx = p->d_kx; a.ky = p->d_ky; a.kmag = p->d_kmag; a.sel = p->d_sel;
-    a.z = p->d_z; a.Nz = p->Nz; a.Nx = p->Nx; a.Ny = p->Ny; a.Nyh = p->Nyh; a.M = p->M;
+    a.kx = p->d_kx; a.ky = p->d_ky; a.kmag = p->d_kmag + v.m0; a.sel = p->d_sel + v.m0;
+    a.z = p->d_z; a.Nz = p->Nz; a.Nx = p->Nx; a.Ny = p->Ny; a.Nyh = p->Nyh; a.M = v.M;
+    a.Mv = v.Mv; a.m0 = v.m0;
     a.w0 = p->win0; a.w1 = p->win1; a.corr = correction ? 1 : 0; a.forces = forces ? 1 : 0;
     a.rb = p->P.eps_b / p->P.eps; a.rt = p->P.eps_t / p->P.eps; a.H = p->P.H;
-    int64_t total = (int64_t)p->Nz * p->M;
+    int64_t total = (int64_t)p->Nz * v.M;
     assemble_kernel<<<(unsigned)((total + 255) / 256), 256, 0, p->stream>>>(a);
     SE_LAUNCHED(p);
+}
+
+void inverse_transforms(Plan* p, bool forces, bool correction) {
+    z_inverse_assemble(p, forces, correction, ModeView{p->M, p->M, 0});
     if (forces) SE_CUFFT(cufftExecZ2D(p->fft_inv4, p->d_spec, p->d_fields));
     else SE_CUFFT(cufftExecZ2D(p->fft_inv1, p->d_spec, p->d_fields));
 }

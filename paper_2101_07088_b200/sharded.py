@@ -5,11 +5,14 @@ The charges are split by index into contiguous shards, one per rank
 
 1. spreads its own charges (and their first images) into a full copy of the
    grids (``se_shard_spread``),
-2. sums the grids over ranks in place (``torch.distributed.all_reduce``, NCCL
-   over NVLink on the solver's stream),
+2. sums the grids over ranks (``torch.distributed`` collectives, NCCL over
+   NVLink on the solver's stream),
 3. runs the grid pipeline -- xy FFTs, z DCT-I, mode BVPs, correction, inverse
-   transforms -- on the summed grids (``se_shard_fields``; replicated, it is
-   a small share of the solve),
+   transforms -- on the summed grids: replicated on every rank
+   (``se_shard_fields``), or with ``decompose=True`` distributed as the
+   prescribed scheme: reduce-scatter into z slabs, slab xy FFTs, all-to-all
+   to (kx, ky) pencils, pencil z transforms + BVPs, all-to-all back, slab
+   inverse FFTs, all-gather of the field grid (``se_dist_*``),
 4. interpolates the fields and evaluates the near field at its own charges,
    with every charge as a near-field source (``se_shard_charges``),
 
@@ -81,6 +84,40 @@ class CudaShardEngine:
     def fields(self):
         _lib.check(self._lib.se_shard_fields(self.solver._plan))
 
+    # -- distributed grid pipeline (se_dist_*) ---------------------------
+    def dist_setup(self, rank, world):
+        """Decompose the grid pipeline over ``world`` ranks; returns the
+        library buffers the collectives act on (torch views)."""
+        sizes = (ctypes.c_int64 * 7)()
+        _lib.check(self._lib.se_dist_setup(self.solver._plan, rank, world, sizes))
+        ptrs = (ctypes.c_void_p * 7)()
+        _lib.check(self._lib.se_dist_buffers(self.solver._plan, ptrs))
+        names = ("rho", "rho_slab", "a2a_fwd_send", "a2a_back_send",
+                 "fields_slab", "fields", "dsc")
+        view = lambda ptr, n: torch.as_tensor(_DeviceArray(ptr, n), device=self.device)
+        buf = {
+            "rho": view(ptrs[0], sizes[0]),
+            "rho_slab": view(ptrs[1], sizes[1]),
+            "send_fwd": view(ptrs[2], sizes[2]),
+            "recv_fwd": view(ptrs[3], sizes[2]),
+            "send_back": view(ptrs[2], sizes[3]),
+            "recv_back": view(ptrs[3], sizes[3]),
+            "fields_slab": view(ptrs[4], sizes[4]),
+            "fields": view(ptrs[5], sizes[5]),
+            "dsc": view(ptrs[6], sizes[6]),
+        }
+        del names
+        return buf
+
+    def dist_forward(self):
+        _lib.check(self._lib.se_dist_forward(self.solver._plan))
+
+    def dist_modes(self):
+        _lib.check(self._lib.se_dist_modes(self.solver._plan))
+
+    def dist_fields(self):
+        _lib.check(self._lib.se_dist_fields(self.solver._plan))
+
     def charges(self, pos_all, count, need_forces):
         phi = torch.empty(count, dtype=torch.float64, device=self.device)
         E = torch.zeros((count, 3), dtype=torch.float64, device=self.device)
@@ -105,7 +142,7 @@ class ShardedSlabSolver:
     the same system; ``solve`` returns the full result on every rank."""
 
     def __init__(self, system, params, threads=1, refine=1, group=None,
-                 device=None, engine=None, precision="fp64"):
+                 device=None, engine=None, precision="fp64", decompose=False):
         if not dist.is_initialized():
             raise RuntimeError("ShardedSlabSolver needs torch.distributed "
                                "initialised (one process per GPU)")
@@ -124,6 +161,8 @@ class ShardedSlabSolver:
             engine = CudaShardEngine(system, params, refine, device, precision)
         self.engine = engine
         self.precision = precision
+        self.decompose = decompose
+        self.buf = engine.dist_setup(self.rank, self.world) if self.decompose else None
         self.last_timings = None
 
     def close(self):
@@ -140,9 +179,12 @@ class ShardedSlabSolver:
                        subtract_self, include_correction, force_general,
                        timings, self.precision == "fp32")
         rho = self.engine.spread(pos_all, self.first, self.count, flags)
-        if self.world > 1:
-            dist.all_reduce(rho, group=self.group)
-        self.engine.fields()
+        if self.decompose:
+            self._grid_pipeline_distributed()
+        else:
+            if self.world > 1:
+                dist.all_reduce(rho, group=self.group)
+            self.engine.fields()
         phi, E, u_part, diag = self.engine.charges(pos_all, self.count,
                                                    need_forces)
         U = u_part
@@ -153,6 +195,20 @@ class ShardedSlabSolver:
         if timings and hasattr(diag, "t_ms"):
             self.last_timings = dict(zip(STAGES, list(diag.t_ms)[:len(STAGES)]))
         return phi, E, U, diag
+
+    def _grid_pipeline_distributed(self):
+        """Reduce-scatter of the spread grids into z slabs, xy FFT, all-to-all
+        to (kx, ky) pencils, mode stage, all-to-all back, inverse xy FFT,
+        all-gather of the fields."""
+        b, g = self.buf, self.group
+        dist.reduce_scatter_tensor(b["rho_slab"], b["rho"], group=g)
+        self.engine.dist_forward()
+        dist.all_to_all_single(b["recv_fwd"], b["send_fwd"], group=g)
+        self.engine.dist_modes()
+        dist.all_to_all_single(b["recv_back"], b["send_back"], group=g)
+        dist.all_reduce(b["dsc"], group=g)
+        self.engine.dist_fields()
+        dist.all_gather_into_tensor(b["fields"], b["fields_slab"], group=g)
 
     def _gather(self, local, width):
         if self.world == 1:

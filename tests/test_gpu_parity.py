@@ -328,7 +328,8 @@ def test_sharded_phases_one_gpu(case, world):
         e.close()
 
 
-def test_sharded_solver_one_rank():
+@pytest.mark.parametrize("decompose", [False, True])
+def test_sharded_solver_one_rank(decompose):
     import socket
     import torch.distributed as dist
     from paper_2101_07088_b200.sharded import ShardedSlabSolver
@@ -340,7 +341,7 @@ def test_sharded_solver_one_rank():
                             rank=0, world_size=1)
     try:
         system, params, kw = variant_problem("c2n256")
-        solver = ShardedSlabSolver(system, params, device=0)
+        solver = ShardedSlabSolver(system, params, device=0, decompose=decompose)
         res = solver.solve(**kw)
         g = solves()["c2n256"]
         assert rel_l2(res.phi_bar, g["phi"]) < TOL
@@ -395,3 +396,70 @@ def test_fp32_mode_rejects_unknown_precision():
     system, params = W.build("c2", N=64)
     with pytest.raises(ValueError):
         SlabSolver(system, params, precision="bf16")
+
+
+# ---------------------------------------------------------------------------
+# distributed grid pipeline (se_dist_*): P ranks emulated sequentially on one
+# GPU, the collectives (reduce-scatter, two all-to-alls, all-reduce,
+# all-gather) done with torch between the library phases
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("case,world", [("c2n256", 2), ("c2n256", 3),
+                                        ("c3n256_gauss_sigma", 4),
+                                        ("c2n256_noforce", 2),
+                                        ("c2n256_nocorr", 3)])
+def test_distributed_grid_pipeline_one_gpu(case, world):
+    import torch
+    from paper_2101_07088_b200.sharded import CudaShardEngine, shard_range
+    from paper_2101_07088_b200.slab import _flags
+    from test_oracle_golden import variant_problem
+    system, params, kw = variant_problem(case)
+    refine = kw.pop("refine", 1)
+    forces = kw.get("need_forces", True)
+    flags = _flags(kw.get("need_energy", True), forces,
+                   kw.get("need_potential", True),
+                   kw.get("subtract_self", False),
+                   kw.get("include_correction", True),
+                   kw.get("force_general", False))
+    n = system.charges.size
+    eng = [CudaShardEngine(system, params, refine=refine, device=0)
+           for _ in range(world)]
+    buf = [e.dist_setup(r, world) for r, e in enumerate(eng)]
+    pos = [e.positions(system.positions) for e in eng]
+    ranges = [shard_range(n, r, world) for r in range(world)]
+    for e, p_, (f, c) in zip(eng, pos, ranges):
+        e.spread(p_, f, c, flags)
+    total = torch.stack([b["rho"] for b in buf]).sum(0)
+    for r, b in enumerate(buf):                              # reduce-scatter
+        k = b["rho_slab"].numel()
+        b["rho_slab"].copy_(total[r * k:(r + 1) * k])
+
+    def all_to_all(send, recv):
+        for r in range(world):
+            for s in range(world):
+                k = buf[r][recv].numel() // world
+                buf[r][recv][s * k:(s + 1) * k].copy_(buf[s][send][r * k:(r + 1) * k])
+    for e in eng:
+        e.dist_forward()
+    all_to_all("send_fwd", "recv_fwd")
+    for e in eng:
+        e.dist_modes()
+    all_to_all("send_back", "recv_back")
+    dsc = torch.stack([b["dsc"] for b in buf]).sum(0)        # all-reduce
+    for b in buf:
+        b["dsc"].copy_(dsc)
+    for e in eng:
+        e.dist_fields()
+    slabs = torch.cat([b["fields_slab"] for b in buf])       # all-gather
+    for b in buf:
+        b["fields"].copy_(slabs)
+    outs = [e.charges(p_, c, forces) for e, p_, (_, c) in zip(eng, pos, ranges)]
+    phi = torch.cat([o[0] for o in outs]).cpu().numpy()
+    E = torch.cat([o[1] for o in outs]).cpu().numpy()
+    U = sum(o[2] for o in outs)
+    g = solves()[case]
+    assert rel_l2(phi, g["phi"]) < TOL
+    if forces:
+        assert rel_l2(E, g["E"]) < TOL
+    assert abs(U - g["U"]) <= TOL * max(1.0, abs(g["U"]))
+    for e in eng:
+        e.close()
