@@ -32,7 +32,6 @@ namespace {
 
 constexpr double TWO_OVER_SQRTPI = 1.1283791670955126;   // 2/sqrt(pi)
 
-__device__ __forceinline__ int pmod_i(int a, int n) { int r = a % n; return r < 0 ? r + n : r; }
 
 // ---------------------------------------------------------------------------
 // cell list
@@ -173,8 +172,6 @@ constexpr int NB_THREADS = 128;
 constexpr int FAR_DEG = 18;
 constexpr int CL_P = 32, CL_D = 12;             // close-pair table: pieces, degree
 constexpr int CL_TAB = 2 * CL_P * (CL_D + 1);
-constexpr int NQ = 48;            // per-lane far-pair queue (shared memory)
-constexpr int NQC = 12;           // per-lane close-pair queue
 
 // 1/sqrt(x) for normal positive x: hardware approximation + 2 Newton steps
 __device__ __forceinline__ double rsqrt_pos(double x) {
@@ -312,9 +309,6 @@ __device__ __forceinline__ void pair_terms(const NearArgs& a, const double* tab,
     coef = -((d1 - d2) * a.inv4pie) * rinv;
 }
 
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-    asm volatile("prefetch.global.L1 [%0];" :: "l"(p));
-}
 
 // exact displacement and squared distance, reference operation order
 //   d = p - s; d_xy -= L * round(d_xy / L); r2 = (dx^2 + dy^2) + dz^2
@@ -353,20 +347,6 @@ __device__ __noinline__ bool tree_keep_s(double Lx, double Ly, double lz, double
 #define tree_keep(a, px, py, pz, sx, sy, sz) \
     tree_keep_s((a).g.Lx, (a).g.Ly, (a).lzbox, *(a).zmin, (a).rr, px, py, pz, sx, sy, sz)
 
-// Butterfly transpose-reduction across the warp: lane l starts with 32
-// partial values v[0..31] and ends with the warp total of value index l.
-__device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) {
-#pragma unroll
-    for (int w = 16; w >= 1; w >>= 1) {
-        const bool up = lane & w;
-#pragma unroll
-        for (int j = 0; j < w; ++j) {
-            const double send = up ? v[j] : v[j + w], keep = up ? v[j + w] : v[j];
-            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, w);
-        }
-    }
-    return v[0];
-}
 
 // ---------------------------------------------------------------------------
 // two-phase near field
@@ -378,7 +358,6 @@ __device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) 
 //        membership test and the erf kernels.  Lists have nearly equal
 //        lengths across a warp (same cell), so the evaluation is dense.
 // ---------------------------------------------------------------------------
-constexpr int MAXNB = 27;
 constexpr int SCAN_Q = 16;                  // per-lane staging before a flush
 constexpr int SCAN_STAGE = 128;             // staged candidates per warp
 

@@ -9,12 +9,13 @@
 //
 // B200 design.  The xy transforms are batched cuFFT D2Z / C2R over the
 // Chebyshev planes of the z-slowest layout.  The DCT-I along z (Nz = 258 at
-// the north-star size, 2(Nz-1) = 2*257: Bluestein-hostile for a hand radix
-// kernel) is one batched length-2(Nz-1) Z2Z FFT over the even extension,
-// strided across modes so every transform reads coalesced rows.  The BVP is
-// one thread per (kx, ky) mode of the half spectrum: sweeps along z touch
-// row n of all modes together, so every global access is coalesced across
-// the warp; factors are precomputed per distinct |k| at plan time.  The
+// the north-star size, 2(Nz-1) = 2*257: Bluestein for an FFT) is a matrix
+// product over all modes at once: folded by the node reflection into two
+// half-order DGEMMs (even / odd coefficient rows) on the FP64 tensor pipe.
+// The BVP is a lane pair per (kx, ky) mode of the half spectrum (over /
+// in-slab grid): sweeps along z touch row n of all modes together, so every
+// global access is coalesced across the warp; factors are precomputed per
+// distinct |k| at plan time.  The
 // mismatch, harmonic-correction moments and the k = 0 combination are fused
 // into the same kernel (a mode needs only its own wall values), and the
 // correction values themselves are evaluated on the fly while assembling
@@ -109,17 +110,6 @@ __global__ void factor_kernel(FactorArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// even extension in z: ext[2N - j] = ext[j], j = 1..N-1
-// ---------------------------------------------------------------------------
-__global__ void mirror_kernel(double2* ext, int N, int64_t row) {
-    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    int64_t total = (int64_t)(N - 1) * row;
-    if (e >= total) return;
-    int64_t j = 1 + e / row, c = e % row;
-    ext[(2 * N - j) * row + c] = ext[j * row + c];
-}
-
-// ---------------------------------------------------------------------------
 // the per-mode solve
 // ---------------------------------------------------------------------------
 struct BvpArgs {
@@ -147,8 +137,8 @@ struct BvpArgs {
 
 // Solve one grid of one mode (column m, grid slot g of ext).  Returns the
 // wall values wv = {y(0), y(H), y'(0), y'(H)} and ends = {y'(z0), y'(z1)}.
-// With emit, writes the iDCT inputs of y (slot 0) and y' (slot 1), i.e. the
-// coefficients with the interior halved, mirrored to rows 2N - k.
+// With emit, writes the Chebyshev coefficients of y (slot 0) and y' (slot 1)
+// for the inverse DCT GEMMs.
 // Scratch columns (stride M): F = f_sc, A = y'' (ypp), B = Thomas d / x.
 __device__ __forceinline__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
                                            double2 ends[2], bool emit) {
