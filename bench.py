@@ -299,7 +299,8 @@ def run_ours(args):
     pin.copy_(torch.from_numpy(system.positions))
     pos_h = pin.numpy()
     e2e_steps = args.e2e_steps or args.steps
-    solver.solve(positions=pos_h)
+    for _ in range(2):                    # warms the pinned output pool
+        solver.solve(positions=pos_h)
     e2e = []
     barrier()
     for _ in range(e2e_steps):
@@ -311,6 +312,10 @@ def run_ours(args):
         e1.record(stream)
         e1.synchronize()
         e2e.append(e0.elapsed_time(e1))
+        _ = float(res.U)                  # the caller consumes the result
+        del res
+    if os.environ.get("SE_BENCH_DEBUG"):
+        print("e2e steps", ["%.1f" % x for x in e2e], file=sys.stderr)
     te = torch.tensor([float(np.sum(e2e))], dtype=torch.float64, device="cuda")
     if world > 1:
         import torch.distributed as dist

@@ -45,3 +45,20 @@ print("se_solve pinned  %.2f ms" % timeit(pinned))
 def fresh_alloc():
     a = np.empty(n); b = np.zeros((n, 3)); a[:] = 1; b[:] = 1
 print("numpy alloc+touch %.2f ms" % timeit(fresh_alloc))
+
+# the bench's e2e loop: events around solve(), previous result kept alive
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+stream = torch.cuda.current_stream()
+res = solver.solve(positions=pos_h)
+for use_flush in (False, True):
+    ts = []
+    for _ in range(6):
+        if use_flush:
+            flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        t = time.perf_counter()
+        res = solver.solve(positions=pos_h)
+        e1.record(stream); e1.synchronize()
+        ts.append((e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t)))
+    print("bench-style flush=%s events/wall" % use_flush, [("%.1f/%.1f" % x) for x in ts])
