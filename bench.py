@@ -321,7 +321,6 @@ def run_ours(args):
         import torch.distributed as dist
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms = float(te.item()) / e2e_steps
-    _ = res
 
     if rank != 0:
         return
