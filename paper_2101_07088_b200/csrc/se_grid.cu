@@ -258,13 +258,6 @@ __device__ __forceinline__ int map_candidate(int idx, const int* s_lo,
     return -1;
 }
 
-// D = A B + C on the FP64 tensor pipe, m8n8k4: lane l holds A[l/4][l%4],
-// B[l%4][l/4] and C[l/4][2(l%4) .. 2(l%4)+1]
-__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
-    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-        : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
-}
-
 __device__ __forceinline__ int imod(int a, int n) { int r = a % n; return r < 0 ? r + n : r; }
 
 // 8-byte asynchronous global -> shared copy (LDGSTS) and its completion wait
@@ -629,181 +622,6 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgs a)
     }
 }
 
-// DMMA variant: groups of 8 charges (the 8 rows of an m8n8k4 fragment).
-// For a window column octet (8 consecutive y of one x), the z contraction
-// G[m][col] = sum_z wz_m(z) F(z, col) is a chain of mma.sync over 4-node
-// k-steps with A[m][k] = wz_m(z_k) (shared by the 4 fields) and
-// B[k][n] = F(z_k, col_n); the x / y weights are applied to the
-// accumulator fragment afterwards (two FMAs per lane and field).
-constexpr int IZC8 = 64;         // z nodes per weight-table chunk
-
-template <int NF, int MINB>
-__global__ void __launch_bounds__(IWARPS * 32, MINB) interp_mma_kernel(InterpArgs a) {
-    constexpr int IG8 = 8;
-    extern __shared__ __align__(16) double ism[];
-    __shared__ GroupInfo ginfo[IWARPS];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = blockIdx.x * IWARPS + warp;
-    if (g >= *a.ngroups) return;
-    const int SX = 2 * a.mx + 1, SY = 2 * a.my + 1;
-    double* swx = ism + (size_t)warp * IG8 * (SX + SY + IZC8);
-    double* swy = swx + IG8 * SX;
-    double* swz = swy + IG8 * SY;
-    GroupInfo& gi = ginfo[warp];
-    const int2 gr = a.groups[g];
-    const int cnt = gr.y;
-    if (lane < IG8) {
-        int i = -1, lo = 0, hi = 0, jxw = 0, jyw = 0;
-        long long jx = 0, jy = 0;
-        double x = 0, y = 0, z = 0;
-        if (lane < cnt) {
-            i = a.perm[gr.x + lane];
-            x = a.pos[3 * i]; y = a.pos[3 * i + 1]; z = a.pos[3 * i + 2];
-            jx = (long long)floor(x / a.hx);
-            jy = (long long)floor(y / a.hy);
-            jxw = pmod(jx, a.Nx); jyw = pmod(jy, a.Ny);
-            lo = lower_bound_d(a.znodes, a.Nz, __dsub_rn(z, a.rad));
-            hi = upper_bound_d(a.znodes, a.Nz, __dadd_rn(z, a.rad));
-        }
-        gi.x[lane] = x; gi.y[lane] = y; gi.z[lane] = z;
-        gi.jx[lane] = jx; gi.jy[lane] = jy; gi.jxw[lane] = jxw; gi.jyw[lane] = jyw;
-        gi.lo[lane] = lo; gi.hi[lane] = hi; gi.idx[lane] = i;
-    }
-    __syncwarp();
-    int xmin = 1 << 30, xmax = -1, ymin = 1 << 30, ymax = -1, zlo = 1 << 30, zhi = 0;
-#pragma unroll
-    for (int m = 0; m < IG8; ++m) {
-        if (m < cnt) {
-            xmin = min(xmin, gi.jxw[m]); xmax = max(xmax, gi.jxw[m]);
-            ymin = min(ymin, gi.jyw[m]); ymax = max(ymax, gi.jyw[m]);
-            zlo = min(zlo, gi.lo[m]); zhi = max(zhi, gi.hi[m]);
-        }
-    }
-    // x / y weights: offsets o = 0 .. 2m of each charge (gridops.py:20-25)
-    for (int e = lane; e < IG8 * SX; e += 32) {
-        const int m = e / SX, o = e - m * SX;
-        double wt = 0.0;
-        if (m < cnt) {
-            const double xj = __dmul_rn((double)(gi.jx[m] + o - a.mx), a.hx);
-            const double d = __dsub_rn(gi.x[m], xj);
-            if (fabs(d) <= a.rad_keep) wt = gauss_w(d, a.inv_width, a.inv_norm);
-        }
-        swx[e] = wt;
-    }
-    for (int e = lane; e < IG8 * SY; e += 32) {
-        const int m = e / SY, o = e - m * SY;
-        double wt = 0.0;
-        if (m < cnt) {
-            const double yj = __dmul_rn((double)(gi.jy[m] + o - a.my), a.hy);
-            const double d = __dsub_rn(gi.y[m], yj);
-            if (fabs(d) <= a.rad_keep) wt = gauss_w(d, a.inv_width, a.inv_norm);
-        }
-        swy[e] = wt;
-    }
-    __syncwarp();
-    // separable sums for the k = 0 linear terms (lane m: charge m)
-    double sx = 0.0, sy = 0.0, sz0 = 0.0, sz1 = 0.0;
-    if (lane < IG8) {
-        for (int o = 0; o < SX; ++o) sx += swx[lane * SX + o];
-        for (int o = 0; o < SY; ++o) sy += swy[lane * SY + o];
-    }
-    const int fm = lane >> 2, fk = lane & 3;   // fragment row (charge) / k index
-    const int jxm = gi.jxw[fm], jym = gi.jyw[fm];
-    const int Wx = xmax - xmin + SX, Wy = ymax - ymin + SY;
-    const int noct = (Wy + 7) >> 3;
-    const int64_t zstride = 4 * a.NXY;
-    double acc[NF];
-#pragma unroll
-    for (int c = 0; c < NF; ++c) acc[c] = 0.0;
-    for (int zc = zlo; zc < zhi; zc += IZC8) {
-        const int nz = min(IZC8, zhi - zc);
-        __syncwarp();
-        // z weights x Clenshaw-Curtis weights (gridops.py:29-39, 128-129)
-        for (int e = lane; e < IG8 * IZC8; e += 32) {
-            const int m = e / IZC8, r = e - m * IZC8, k = zc + r;
-            double wt = 0.0;
-            if (m < cnt && r < nz && k >= gi.lo[m] && k < gi.hi[m] && k < a.Nz) {
-                const double d = __dsub_rn(gi.z[m], a.znodes[k]);
-                if (fabs(d) <= a.rad) wt = gauss_w(d, a.inv_width, a.inv_norm);
-                wt = wt * a.wcc[k];
-            }
-            swz[e] = wt;
-        }
-        __syncwarp();
-        if (lane < IG8) {
-            for (int r = 0; r < nz; ++r) {
-                const double w = swz[lane * IZC8 + r];
-                sz1 += w;
-                sz0 += w * a.znodes[zc + r];
-            }
-        }
-        const int nks = (nz + 3) >> 2;
-        for (int oc = 0; oc < Wx * noct; ++oc) {
-            const int ux = oc / noct, uy0 = (oc - ux * noct) * 8;
-            // B column n = fm: window column (ux, uy0 + fm)
-            int gx = xmin - a.mx + ux, gy = ymin - a.my + uy0 + fm;
-            gx %= a.Nx; if (gx < 0) gx += a.Nx;
-            gy %= a.Ny; if (gy < 0) gy += a.Ny;
-            const double* F = a.fields + (int64_t)zc * zstride + (int64_t)gx * a.Ny + gy;
-            double cf[NF][2];
-#pragma unroll
-            for (int c = 0; c < NF; ++c) { cf[c][0] = 0.0; cf[c][1] = 0.0; }
-            // two k-steps per iteration: their 2 NF loads are issued before
-            // the tensor-core ops that consume them
-            for (int ks = 0; ks < nks; ks += 2) {
-                double aw[2], bv[2][NF];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int r = 4 * (ks + h) + fk;            // z offset of this lane's k
-                    aw[h] = (ks + h < nks) ? swz[fm * IZC8 + r] : 0.0;   // A[m = fm][k = fk]
-                    const bool zin = ks + h < nks && r < nz && zc + r < a.Nz;
-                    const double* Fr = F + (int64_t)r * zstride;
-#pragma unroll
-                    for (int c = 0; c < NF; ++c)                // B[k = fk][n = fm]
-                        bv[h][c] = zin ? __ldg(Fr + (int64_t)c * a.NXY) : 0.0;
-                }
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                    for (int c = 0; c < NF; ++c) dmma_8x8x4(cf[c], aw[h], bv[h][c]);
-            }
-            // cf[c][i] = G[m = fm][col n = 2 fk + i]: apply the x / y weights
-            const int ox = xmin + ux - jxm;
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const int n = 2 * fk + i;
-                const int oy = ymin + uy0 + n - jym;
-                double wxy = 0.0;
-                if (fm < cnt && uy0 + n < Wy && ox >= 0 && ox < SX && oy >= 0 && oy < SY)
-                    wxy = swx[fm * SX + ox] * swy[fm * SY + oy];
-#pragma unroll
-                for (int c = 0; c < NF; ++c) acc[c] = fma(wxy, cf[c][i], acc[c]);
-            }
-        }
-    }
-    // sum over the 4 lanes of each charge (lanes 4 fm .. 4 fm + 3)
-#pragma unroll
-    for (int c = 0; c < NF; ++c) {
-        acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 1);
-        acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 2);
-    }
-    const double A_i = a.scal[0];
-    const double Sx = __shfl_sync(0xffffffffu, sx, fm);
-    const double Sy = __shfl_sync(0xffffffffu, sy, fm);
-    const double Sz0 = __shfl_sync(0xffffffffu, sz0, fm);
-    const double Sz1 = __shfl_sync(0xffffffffu, sz1, fm);
-    if (fk == 0 && fm < cnt) {
-        const int64_t idx = gi.idx[fm];
-#pragma unroll
-        for (int c = 0; c < NF; ++c) {
-            double v = acc[c];
-            if (c == 0) v += A_i * ((Sx * Sy) * Sz0);
-            if (c == 3) v += A_i * ((Sx * Sy) * Sz1);
-            a.out[(int64_t)c * a.N + idx] = v;
-        }
-    }
-}
-
 // ---------------------------------------------------------------------------
 // pointwise interpolation of field 0 (psi + A_i z) at arbitrary points with
 // an arbitrary width: the gauge (slab.py:253-256,377-384) and the wall nodes
@@ -995,6 +813,10 @@ static TileArgs tile_args(Plan* p) {
 // k-step with A[y][s] = q_s wx_s(x) wy_s(y) and B[s][z] = wz_s(z), so one
 // mma.sync does the 256 FMAs that would cost eight DFMAs per lane.  A warp
 // skips k-steps whose sources all miss its z group.
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
 
 template <int TZ, int CAP, int MINB>
 __global__ void __launch_bounds__(4 * TZ, MINB) spread_mma_kernel(SpreadArgs a) {
@@ -1089,8 +911,7 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
     if (((uint64_t)nbins << zb) >> 32)
         throw Error(SE_ERR_VALUE, "grid too large for the interpolation sort keys");
     ensure_sources(p, n);               // key / permutation / sort scratch (>= 3n)
-    static const int iv = [] { const char* e = getenv("SE_INTERP_V"); return e ? atoi(e) : 0; }();
-    const int ig = iv >= 1 ? 8 : 4;
+    const int ig = 4;                   // charges per group (measured best of 2, 3, 4, 8)
     const int64_t gcap = count / ig + nbins + 1;
     if (nbins + 1 > p->iseg_cap || gcap > p->igroup_cap) {
         dfree(p, p->d_iseg); dfree(p, p->d_igroups); dfree(p, p->d_ingroups);
@@ -1134,23 +955,15 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
     InterpArgs a{p->d_fields, p->d_pos_cur, p->d_z, p->d_wcc, p->d_scal, p->d_perm2,
                  p->d_igroups, p->d_ingroups, p->Nx, p->Ny, p->Nz, p->NXY, p->hx, p->hy,
                  p->rad, p->rad_keep, 1.0 / p->width, 1.0 / p->norm, p->mx, p->my, p->d_far, n};
-    const int smem = IWARPS * ig * (2 * p->mx + 1 + 2 * p->my + 1 + (iv >= 1 ? IZC8 : IZC)) *
-                     (int)sizeof(double);
+    const int smem = IWARPS * ig * (2 * p->mx + 1 + 2 * p->my + 1 + IZC) * (int)sizeof(double);
     if (smem > 200 * 1024) throw Error(SE_ERR_VALUE, "stencil too wide for the interpolation");
     const unsigned blocks = (unsigned)((gcap + IWARPS - 1) / IWARPS);
     auto go = [&](auto kern) {
         SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         kern<<<blocks, IWARPS * 32, smem, p->stream>>>(a);
     };
-    if (iv == 1) {
-        if (forces) go(interp_mma_kernel<4, 1>); else go(interp_mma_kernel<1, 1>);
-    } else if (iv == 2) {
-        if (forces) go(interp_mma_kernel<4, 3>); else go(interp_mma_kernel<1, 3>);
-    } else if (iv == 3) {
-        if (forces) go(interp_mma_kernel<4, 4>); else go(interp_mma_kernel<1, 4>);
-    } else {
-        if (forces) go(interp_kernel<4, 4, 1, 2>); else go(interp_kernel<1, 4, 1, 2>);
-    }
+    if (forces) go(interp_kernel<4, 4, 1, 2>);
+    else go(interp_kernel<1, 4, 1, 2>);
     p->ktoc(2);
     SE_LAUNCHED(p);
 }
