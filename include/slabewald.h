@@ -147,6 +147,13 @@ int se_dist_forward(se_plan* plan);
 int se_dist_modes(se_plan* plan);
 int se_dist_fields(se_plan* plan);
 
+/* Brownian-dynamics steric pair forces (bd.py:246-270): truncated LJ
+ * repulsion 4 U0 ((2a/r)^2p - (2a/r)^p) + U0 cut at 2^(1/p) 2a, core capped
+ * below r_m, minimum image in x, y (periodic Lx, Ly), open z.  pos[n][3],
+ * out[n][3] host buffers. */
+int se_steric_forces(int device, const double* pos, int64_t n, double Lx, double Ly,
+                     double a, double U0, double r_m, int p, double* out);
+
 /* near_field_sum (slab.py:184-191): sources = pos[n] with charges q[n]
  * (plus the mirrored layers of the geometry in params), evaluated at
  * eval_pos[ne].  kind 0 = "avg" (r_cut), 1 = "point" (r_nf).  Host buffers.

@@ -33,7 +33,7 @@ EXPORTS = ("se_plan_create", "se_plan_destroy", "se_plan_set_stream",
            "se_debug_fetch", "se_fp64_peak", "se_last_error", "se_version",
            "se_shard_spread", "se_shard_fields", "se_shard_charges",
            "se_dist_setup", "se_dist_buffers", "se_dist_forward",
-           "se_dist_modes", "se_dist_fields")
+           "se_dist_modes", "se_dist_fields", "se_steric_forces")
 
 
 class SeParams(ctypes.Structure):
@@ -116,6 +116,10 @@ def load():
     for name in ("se_dist_forward", "se_dist_modes", "se_dist_fields"):
         getattr(lib, name).argtypes = [_P]
         getattr(lib, name).restype = ctypes.c_int
+    lib.se_steric_forces.argtypes = [ctypes.c_int, _D, _I64, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_int, _D]
+    lib.se_steric_forces.restype = ctypes.c_int
     lib.se_fp64_peak.argtypes = [ctypes.c_int, _D]
     lib.se_fp64_peak.restype = ctypes.c_int
     lib.se_last_error.argtypes = []

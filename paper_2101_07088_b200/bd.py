@@ -1,0 +1,155 @@
+"""Brownian dynamics on top of the B200 solver.
+
+Mirrors the reference module ``slabewald.bd`` (bd.py) for the parts the BD
+driver needs (``cmd_bd``, cli.py:174-230): the steric model (bd.py:27-74),
+the two-step-noise Euler-Maruyama step with z-bound rejection and xy wrap
+(bd.py:77-133), the pairwise steric forces (bd.py:246-270, on the GPU through
+``se_steric_forces``) and the mirror-wall forces (bd.py:273-279).  The noise
+stream is numpy's Philox generator seeded like the reference, so trajectories
+match the reference draw for draw.  The triply periodic validation solver and
+the observables / theory curves are out of scope.
+"""
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+
+@dataclass(frozen=True)
+class StericParams:
+    """Truncated, mollified repulsion 4 U0 ((2a/r)^2p - (2a/r)^p) + U0, zero
+    beyond its minimum at r = 2^(1/p) 2a, force capped below r_m."""
+
+    a: float
+    U0: float = 1.0
+    r_m: float = 0.0
+    p: int = 6
+
+    @property
+    def cutoff(self):
+        return 2.0 ** (1.0 / self.p) * 2.0 * self.a
+
+
+def lj_force(r, s):
+    """-dU/dr of the uncut 2p-p potential."""
+    x = (2.0 * s.a / r) ** s.p
+    return 4.0 * s.U0 * s.p * x * (2.0 * x - 1.0) / r
+
+
+def _core(r, s):
+    floor = s.r_m if s.r_m > 0 else 1e-12 * s.a
+    return np.maximum(r, floor)
+
+
+def steric_force(r, s):
+    """Capped core, repulsive flank, zero past the cutoff (bd.py:52-57)."""
+    r = np.asarray(r, dtype=float)
+    return np.where(r > s.cutoff, 0.0, lj_force(_core(r, s), s))
+
+
+def steric_energy(r, s):
+    """Potential matching :func:`steric_force`, zero at the cutoff and
+    continued linearly inside r_m (bd.py:60-68)."""
+    r = np.asarray(r, dtype=float)
+    rc = _core(r, s)
+    x = (2.0 * s.a / rc) ** s.p
+    u = 4.0 * s.U0 * (x * x - x) + s.U0
+    if s.r_m > 0:
+        u = u + lj_force(s.r_m, s) * np.maximum(s.r_m - r, 0.0)
+    return np.where(r > s.cutoff, 0.0, u)
+
+
+@dataclass
+class BdConfig:
+    dt: float
+    steps: int
+    equil_steps: int = 0
+    mu: float = 1.0
+    kT: float = 1.0
+    seed: int = 0
+    max_disp: float = np.inf
+    max_retries: int = 100
+    sample_every: int = 50
+
+
+@dataclass
+class BdState:
+    positions: np.ndarray
+    prev_noise: np.ndarray
+    rng: np.random.Generator
+    rejections: int = 0
+    steps_done: int = 0
+
+
+def make_state(positions, config):
+    """Initial state: Philox stream of the seed, first noise drawn."""
+    rng = np.random.Generator(np.random.Philox(config.seed))
+    prev = rng.standard_normal(np.shape(positions))
+    return BdState(np.array(positions, dtype=float), prev, rng)
+
+
+def bd_step(state, forces, config, z_bounds=None, wrap=None):
+    """One step  x += mu F dt + sqrt(kT mu dt / 2) (W_n + W_{n+1}), each
+    displacement capped at max_disp; a step leaving (lo, hi) in z is redrawn
+    with a fresh W_{n+1} (bd.py:101-133); periodic axes wrapped with mod."""
+    drift = config.mu * config.dt * np.asarray(forces)
+    amp = math.sqrt(0.5 * config.kT * config.mu * config.dt)
+    shape = state.positions.shape
+    for _ in range(config.max_retries + 1):
+        fresh = state.rng.standard_normal(shape) if config.kT > 0 else np.zeros(shape)
+        step = drift + amp * (state.prev_noise + fresh)
+        if np.isfinite(config.max_disp):
+            length = np.linalg.norm(step, axis=1, keepdims=True)
+            too_long = length > config.max_disp
+            if np.any(too_long):
+                step = np.where(too_long, step * (config.max_disp / length), step)
+        trial = state.positions + step
+        inside = z_bounds is None or (np.all(trial[:, 2] > z_bounds[0])
+                                      and np.all(trial[:, 2] < z_bounds[1]))
+        if inside:
+            if wrap is not None:
+                for axis, box in enumerate(wrap):
+                    if box is not None:
+                        trial[:, axis] = np.mod(trial[:, axis], box)
+            state.positions = trial
+            state.prev_noise = fresh
+            state.steps_done += 1
+            return state
+        state.rejections += 1
+    raise RuntimeError("unrecoverable configuration: %d retries exhausted"
+                       % config.max_retries)
+
+
+def steric_pair_forces(positions, steric, boxes, tree=None, device=0):
+    """Pairwise steric forces on the GPU (``se_steric_forces``), periodic in
+    x and y, open in z (the slab case of bd.py:246-270)."""
+    del tree                                   # the GPU builds its own cells
+    if len(boxes) != 3 or boxes[0] is None or boxes[1] is None or boxes[2] is not None:
+        raise NotImplementedError("steric forces: periodic x, y and open z only")
+    lib = _lib.load()
+    pos = _lib.as_f64(np.atleast_2d(positions)).reshape(-1, 3)
+    out = np.zeros_like(pos)
+    _lib.check(lib.se_steric_forces(int(device), _lib.dptr(pos), pos.shape[0],
+                                    float(boxes[0]), float(boxes[1]),
+                                    float(steric.a), float(steric.U0),
+                                    float(steric.r_m), int(steric.p),
+                                    _lib.dptr(out)))
+    return out
+
+
+def wall_steric_forces(positions, steric, H):
+    """Repulsion from mirror particles behind both walls, z only
+    (bd.py:273-279)."""
+    z = np.asarray(positions)[:, 2]
+    out = np.zeros(np.shape(positions))
+    out[:, 2] = steric_force(2.0 * z, steric) - steric_force(2.0 * (H - z), steric)
+    return out
+
+
+__all__ = ["StericParams", "BdConfig", "BdState", "lj_force", "steric_force",
+           "steric_energy", "make_state", "bd_step", "steric_pair_forces",
+           "wall_steric_forces"]

@@ -871,6 +871,16 @@ int se_dist_fields(se_plan* plan) {
     }
 }
 
+int se_steric_forces(int device, const double* pos, int64_t n, double Lx, double Ly,
+                     double a, double U0, double r_m, int p, double* out) {
+    try {
+        steric_forces(device, pos, n, Lx, Ly, a, U0, r_m, p, out);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
 int se_near_field(const se_params* params, int device, const double* pos, const double* q,
                   int64_t n, const double* eval_pos, int64_t ne, int kind, int need_field,
                   int subtract_unsplit, double* phi, double* E) {

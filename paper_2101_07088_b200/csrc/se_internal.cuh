@@ -396,4 +396,8 @@ void finalize(Plan* p, int64_t first, int64_t count, uint32_t flags, double self
               double* d_phi, double* d_E);
 void wall_energy(Plan* p, const NearKernel& kpoint);
 
+// --- se_bd.cu ---
+void steric_forces(int device, const double* pos, int64_t n, double Lx, double Ly, double a,
+                   double U0, double r_m, int p, double* out);
+
 }  // namespace se

@@ -1,0 +1,65 @@
+"""Brownian dynamics against reference goldens
+(tests/golden/make_bd.py): steric force / energy curves, mirror-wall forces
+and three integrator steps with the reference's Philox noise on CPU; the
+GPU steric pair forces (periodic xy, open z) on the GPU."""
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_2101_07088_b200 import bd as B
+from _golden import rel_l2
+
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "bd.npz"))
+L, H = 1.0, 0.6
+
+
+def _steric(name):
+    a, U0, r_m, p = G["steric_%s" % name]
+    return B.StericParams(a=float(a), U0=float(U0), r_m=float(r_m), p=int(p))
+
+
+@pytest.mark.parametrize("name", ["a", "b", "c"])
+def test_steric_curves(name):
+    s = _steric(name)
+    assert np.array_equal(B.steric_force(G["r"], s), G["force_%s" % name])
+    assert np.array_equal(B.steric_energy(G["r"], s), G["energy_%s" % name])
+
+
+@pytest.mark.parametrize("name", ["a", "b", "c"])
+def test_wall_forces(name):
+    got = B.wall_steric_forces(G["pos"], _steric(name), H)
+    assert np.array_equal(got, G["wall_%s" % name])
+
+
+def test_bd_steps_match_reference_stream():
+    cfg = B.BdConfig(dt=2e-5, steps=3, seed=5, max_disp=0.01)
+    state = B.make_state(G["bd_pos0"], cfg)
+    for k in range(3):
+        B.bd_step(state, G["bd_forces"], cfg, z_bounds=(0.05, H - 0.05), wrap=(L, L, None))
+        assert np.array_equal(state.positions, G["bd_traj"][k])
+    assert state.rejections == int(G["bd_rejections"])
+
+
+def test_bd_step_rejects_and_exhausts():
+    cfg = B.BdConfig(dt=1e-3, steps=1, seed=1, max_retries=3)
+    state = B.make_state(np.array([[0.5, 0.5, 0.3]]), cfg)
+    with pytest.raises(RuntimeError):
+        B.bd_step(state, np.zeros((1, 3)), cfg, z_bounds=(0.4, 0.5))
+    assert state.rejections == 4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["a", "b", "c"])
+def test_gpu_steric_pair_forces(name):
+    got = B.steric_pair_forces(G["pos"], _steric(name), (L, L, None))
+    ref = G["pair_%s" % name]
+    assert rel_l2(got, ref) < 1e-12
+    # the per-particle zero pattern (who has neighbours) is exact
+    assert np.array_equal(np.abs(got).sum(1) > 0, np.abs(ref).sum(1) > 0)
+
+
+def test_steric_pair_forces_rejects_periodic_z():
+    with pytest.raises(NotImplementedError):
+        B.steric_pair_forces(G["pos"], _steric("a"), (L, L, 1.0))
