@@ -150,6 +150,28 @@ def wall_steric_forces(positions, steric, H):
     return out
 
 
+def bd_run(solver, steric, config, steps=None, state=None):
+    """The BD loop of ``cmd_bd`` (cli.py:199-215) without its file output:
+    forces = q E from the solver (need_energy=False) + steric pair forces +
+    mirror-wall forces, then one :func:`bd_step` with the z margin
+    n_sigma g_w and xy wrap.  Returns the state after ``steps`` steps."""
+    system, params = solver.system, solver.params
+    geo = system.geometry
+    margin = params.n_sigma * system.g_w
+    if state is None:
+        state = make_state(system.positions, config)
+    total = config.equil_steps + config.steps if steps is None else steps
+    for _ in range(total):
+        res = solver.solve(positions=state.positions, need_energy=False)
+        f = res.forces \
+            + steric_pair_forces(state.positions, steric, (geo.Lx, geo.Ly, None),
+                                 device=getattr(solver, "device", 0)) \
+            + wall_steric_forces(state.positions, steric, geo.H)
+        bd_step(state, f, config, z_bounds=(margin, geo.H - margin),
+                wrap=(geo.Lx, geo.Ly, None))
+    return state
+
+
 __all__ = ["StericParams", "BdConfig", "BdState", "lj_force", "steric_force",
            "steric_energy", "make_state", "bd_step", "steric_pair_forces",
-           "wall_steric_forces"]
+           "wall_steric_forces", "bd_run"]

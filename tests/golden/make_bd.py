@@ -68,3 +68,35 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def bd_loop_golden():
+    """Two steps of the cmd_bd loop (cli.py:203-215) on a small C2-box
+    electrolyte: forces = q E (solver, need_energy=False) + steric + wall."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    import slabewald as sw
+    from paper_2101_07088_b200 import workloads as W
+    desc = dict(W.WORKLOADS["c2"])
+    geo = sw.SlabGeometry(desc["L"], desc["L"], desc["H"], 1.0, desc["eps_b"], desc["eps_t"])
+    pos, q = W.make_inputs(desc, 256)
+    system = sw.ChargeSystem(geo, pos, q, desc["g_w"])
+    params = sw.plan_grid(geo, desc["g_w"], desc["delta"], Nxy=desc["Nxy"])
+    solver = sw.SlabSolver(system, params)
+    st = sb.StericParams(a=0.01)
+    cfg = sb.BdConfig(dt=1e-6, steps=2, seed=3, max_disp=st.a)
+    margin = params.n_sigma * system.g_w
+    state = sb.make_state(system.positions, cfg)
+    traj = []
+    for _ in range(2):
+        res = solver.solve(positions=state.positions, need_energy=False)
+        f = res.forces + sb.steric_pair_forces(state.positions, st, (geo.Lx, geo.Ly, None)) \
+            + sb.wall_steric_forces(state.positions, st, geo.H)
+        sb.bd_step(state, f, cfg, z_bounds=(margin, geo.H - margin), wrap=(geo.Lx, geo.Ly, None))
+        traj.append(state.positions.copy())
+    np.savez_compressed(os.path.join(HERE, "bd_loop.npz"), traj=np.stack(traj),
+                        rejections=np.int64(state.rejections))
+    print("bd_loop.npz", state.rejections, "rejections")
+
+
+if __name__ == "__main__" and "--loop" in sys.argv:
+    bd_loop_golden()

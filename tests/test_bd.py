@@ -63,3 +63,21 @@ def test_gpu_steric_pair_forces(name):
 def test_steric_pair_forces_rejects_periodic_z():
     with pytest.raises(NotImplementedError):
         B.steric_pair_forces(G["pos"], _steric("a"), (L, L, 1.0))
+
+
+@pytest.mark.gpu
+def test_gpu_bd_loop_matches_reference():
+    """Two steps of the cmd_bd loop with the GPU solver and steric forces
+    against the reference's own loop (tests/golden/make_bd.py --loop)."""
+    from paper_2101_07088_b200 import workloads as W
+    from paper_2101_07088_b200.slab import SlabSolver
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "bd_loop.npz"))
+    system, params = W.build("c2", N=256)
+    solver = SlabSolver(system, params)
+    st = B.StericParams(a=0.01)
+    cfg = B.BdConfig(dt=1e-6, steps=2, seed=3, max_disp=st.a)
+    state = B.make_state(system.positions, cfg)
+    for k in range(2):
+        B.bd_run(solver, st, cfg, steps=1, state=state)
+        assert np.max(np.abs(state.positions - g["traj"][k])) < 1e-12
+    assert state.rejections == int(g["rejections"])
