@@ -149,10 +149,32 @@ int se_dist_fields(se_plan* plan);
 
 /* Brownian-dynamics steric pair forces (bd.py:246-270): truncated LJ
  * repulsion 4 U0 ((2a/r)^2p - (2a/r)^p) + U0 cut at 2^(1/p) 2a, core capped
- * below r_m, minimum image in x, y (periodic Lx, Ly), open z.  pos[n][3],
- * out[n][3] host buffers. */
+ * below r_m, minimum image on the periodic axes (box length > 0; Lz <= 0
+ * means open z, the slab case; Lz > 0 the triply periodic box of the g2
+ * experiment, validate.py:245).  pos[n][3], out[n][3] host buffers. */
 int se_steric_forces(int device, const double* pos, int64_t n, double Lx, double Ly,
-                     double a, double U0, double r_m, int p, double* out);
+                     double Lz, double a, double U0, double r_m, int p, double* out);
+
+/* Triply periodic twin.  A plan holds the uniform
+ * periodic grid nx x ny x nz of the box Lx x Ly x Lz and the permittivity.
+ *   se_tp_poisson: solve_triply_periodic (dpsolver.py:221-249); rho, phi
+ *     [nx][ny][nz], E [3][nx][ny][nz] (NULL or with_field 0: no field).
+ *   se_tp_forces: TriplyPeriodicSolver.forces (bd.py:323-331): spread with
+ *     Gaussian width g_t inside radius, FFT Poisson solve, field
+ *     interpolation, near_gradient_avg pair forces within r_cut (split g_w,
+ *     xi); forces[n][3] = q (far + near).  Host buffers.
+ *   se_tp_forces_device: the same on device buffers, on the plan's stream. */
+typedef struct se_tp se_tp;
+int se_tp_create(int device, double Lx, double Ly, double Lz, int nx, int ny, int nz,
+                 double eps, se_tp** plan);
+int se_tp_destroy(se_tp* plan);
+int se_tp_set_stream(se_tp* plan, void* stream);
+int se_tp_poisson(se_tp* plan, const double* rho, int with_field, double* phi, double* E);
+int se_tp_forces(se_tp* plan, const double* pos, const double* q, int64_t n, double g_t,
+                 double radius, double g_w, double xi, double r_cut, double* forces);
+int se_tp_forces_device(se_tp* plan, const double* d_pos, const double* d_q, int64_t n,
+                        double g_t, double radius, double g_w, double xi, double r_cut,
+                        double* d_forces);
 
 /* near_field_sum (slab.py:184-191): sources = pos[n] with charges q[n]
  * (plus the mirrored layers of the geometry in params), evaluated at

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libslabewald_cuda.so")
-SOURCES = ["se_api.cu", "se_grid.cu", "se_spectral.cu", "se_near.cu", "se_bd.cu"]
+SOURCES = ["se_api.cu", "se_grid.cu", "se_spectral.cu", "se_near.cu", "se_bd.cu", "se_tp.cu"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

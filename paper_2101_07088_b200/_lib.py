@@ -33,7 +33,9 @@ EXPORTS = ("se_plan_create", "se_plan_destroy", "se_plan_set_stream",
            "se_debug_fetch", "se_fp64_peak", "se_last_error", "se_version",
            "se_shard_spread", "se_shard_fields", "se_shard_charges",
            "se_dist_setup", "se_dist_buffers", "se_dist_forward",
-           "se_dist_modes", "se_dist_fields", "se_steric_forces")
+           "se_dist_modes", "se_dist_fields", "se_steric_forces",
+           "se_tp_create", "se_tp_destroy", "se_tp_set_stream", "se_tp_poisson",
+           "se_tp_forces", "se_tp_forces_device")
 
 
 class SeParams(ctypes.Structure):
@@ -116,10 +118,21 @@ def load():
     for name in ("se_dist_forward", "se_dist_modes", "se_dist_fields"):
         getattr(lib, name).argtypes = [_P]
         getattr(lib, name).restype = ctypes.c_int
-    lib.se_steric_forces.argtypes = [ctypes.c_int, _D, _I64, ctypes.c_double, ctypes.c_double,
-                                     ctypes.c_double, ctypes.c_double, ctypes.c_double,
+    _f = ctypes.c_double
+    lib.se_steric_forces.argtypes = [ctypes.c_int, _D, _I64, _f, _f, _f, _f, _f, _f,
                                      ctypes.c_int, _D]
     lib.se_steric_forces.restype = ctypes.c_int
+    lib.se_tp_create.argtypes = [ctypes.c_int, _f, _f, _f, ctypes.c_int, ctypes.c_int,
+                                 ctypes.c_int, _f, ctypes.POINTER(ctypes.c_void_p)]
+    lib.se_tp_destroy.argtypes = [ctypes.c_void_p]
+    lib.se_tp_set_stream.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+    lib.se_tp_poisson.argtypes = [ctypes.c_void_p, _D, ctypes.c_int, _D, _D]
+    lib.se_tp_forces.argtypes = [ctypes.c_void_p, _D, _D, _I64, _f, _f, _f, _f, _f, _D]
+    lib.se_tp_forces_device.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        _I64, _f, _f, _f, _f, _f, ctypes.c_void_p]
+    for name in ("se_tp_create", "se_tp_destroy", "se_tp_set_stream", "se_tp_poisson",
+                 "se_tp_forces", "se_tp_forces_device"):
+        getattr(lib, name).restype = ctypes.c_int
     lib.se_fp64_peak.argtypes = [ctypes.c_int, _D]
     lib.se_fp64_peak.restype = ctypes.c_int
     lib.se_last_error.argtypes = []

@@ -6,8 +6,8 @@ the two-step-noise Euler-Maruyama step with z-bound rejection and xy wrap
 (bd.py:77-133), the pairwise steric forces (bd.py:246-270, on the GPU through
 ``se_steric_forces``) and the mirror-wall forces (bd.py:273-279).  The noise
 stream is numpy's Philox generator seeded like the reference, so trajectories
-match the reference draw for draw.  The triply periodic validation solver and
-the observables / theory curves are out of scope.
+match the reference draw for draw.  ``TriplyPeriodicSolver`` (bd.py:297)
+lives in :mod:`.periodic`; the observables / theory curves are out of scope.
 """
 
 import ctypes
@@ -125,16 +125,18 @@ def bd_step(state, forces, config, z_bounds=None, wrap=None):
 
 
 def steric_pair_forces(positions, steric, boxes, tree=None, device=0):
-    """Pairwise steric forces on the GPU (``se_steric_forces``), periodic in
-    x and y, open in z (the slab case of bd.py:246-270)."""
+    """Pairwise steric forces on the GPU (``se_steric_forces``), bd.py:246-270:
+    periodic x and y, and z open (``boxes[2] is None``, the slab) or periodic
+    (the triply periodic box of the g2 experiment)."""
     del tree                                   # the GPU builds its own cells
-    if len(boxes) != 3 or boxes[0] is None or boxes[1] is None or boxes[2] is not None:
-        raise NotImplementedError("steric forces: periodic x, y and open z only")
+    if len(boxes) != 3 or boxes[0] is None or boxes[1] is None:
+        raise NotImplementedError("steric forces: periodic x and y")
     lib = _lib.load()
     pos = _lib.as_f64(np.atleast_2d(positions)).reshape(-1, 3)
     out = np.zeros_like(pos)
+    lz = 0.0 if boxes[2] is None else float(boxes[2])
     _lib.check(lib.se_steric_forces(int(device), _lib.dptr(pos), pos.shape[0],
-                                    float(boxes[0]), float(boxes[1]),
+                                    float(boxes[0]), float(boxes[1]), lz,
                                     float(steric.a), float(steric.U0),
                                     float(steric.r_m), int(steric.p),
                                     _lib.dptr(out)))
@@ -172,6 +174,14 @@ def bd_run(solver, steric, config, steps=None, state=None):
     return state
 
 
+def __getattr__(name):
+    # bd.py:297 hosts the triply periodic solver in the reference
+    if name == "TriplyPeriodicSolver":
+        from .periodic import TriplyPeriodicSolver
+        return TriplyPeriodicSolver
+    raise AttributeError(name)
+
+
 __all__ = ["StericParams", "BdConfig", "BdState", "lj_force", "steric_force",
            "steric_energy", "make_state", "bd_step", "steric_pair_forces",
-           "wall_steric_forces", "bd_run"]
+           "wall_steric_forces", "bd_run", "TriplyPeriodicSolver"]

@@ -872,9 +872,67 @@ int se_dist_fields(se_plan* plan) {
 }
 
 int se_steric_forces(int device, const double* pos, int64_t n, double Lx, double Ly,
-                     double a, double U0, double r_m, int p, double* out) {
+                     double Lz, double a, double U0, double r_m, int p, double* out) {
     try {
-        steric_forces(device, pos, n, Lx, Ly, a, U0, r_m, p, out);
+        steric_forces(device, pos, n, Lx, Ly, Lz, a, U0, r_m, p, out);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_tp_create(int device, double Lx, double Ly, double Lz, int nx, int ny, int nz,
+                 double eps, se_tp** plan) {
+    try {
+        const double L[3] = {Lx, Ly, Lz};
+        const int n[3] = {nx, ny, nz};
+        *plan = reinterpret_cast<se_tp*>(tp_create(device, L, n, eps));
+        return SE_OK;
+    } catch (const Error& e) {
+        *plan = nullptr;
+        return fail(e);
+    }
+}
+
+int se_tp_destroy(se_tp* plan) {
+    tp_destroy(reinterpret_cast<TpPlan*>(plan));
+    return SE_OK;
+}
+
+int se_tp_set_stream(se_tp* plan, void* stream) {
+    try {
+        tp_set_stream(reinterpret_cast<TpPlan*>(plan), static_cast<cudaStream_t>(stream));
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_tp_poisson(se_tp* plan, const double* rho, int with_field, double* phi, double* E) {
+    try {
+        tp_poisson(reinterpret_cast<TpPlan*>(plan), rho, with_field, phi, E);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_tp_forces(se_tp* plan, const double* pos, const double* q, int64_t n, double g_t,
+                 double radius, double g_w, double xi, double r_cut, double* forces) {
+    try {
+        tp_forces(reinterpret_cast<TpPlan*>(plan), pos, q, n, g_t, radius, g_w, xi, r_cut, forces);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_tp_forces_device(se_tp* plan, const double* d_pos, const double* d_q, int64_t n,
+                        double g_t, double radius, double g_w, double xi, double r_cut,
+                        double* d_forces) {
+    try {
+        tp_forces_device(reinterpret_cast<TpPlan*>(plan), d_pos, d_q, n, g_t, radius, g_w, xi,
+                         r_cut, d_forces);
         return SE_OK;
     } catch (const Error& e) {
         return fail(e);

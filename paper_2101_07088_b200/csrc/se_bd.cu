@@ -1,15 +1,19 @@
-// Brownian-dynamics steric forces.
+// Pair forces on a cell list: the Brownian-dynamics steric forces
+// and the near field of the triply periodic
+// twin (section 8f, next #3).
 //
-// Reference: steric_pair_forces / steric_force / lj_force (bd.py:46-63,
+// References: steric_pair_forces / steric_force / lj_force (bd.py:46-63,
 // 246-270): truncated, mollified Lennard-Jones repulsion between all pairs
-// within the cutoff 2^(1/p) 2a, minimum image in x and y (periodic), open z;
-// the reference sums the pair forces with np.bincount over a KD-tree pair
-// list, here every particle gathers its own sum (same terms, its own order).
+// within the cutoff 2^(1/p) 2a, minimum image on the periodic axes;
+// TriplyPeriodicSolver._near_field (bd.py:335-355): near_gradient_avg pair
+// forces within r_cut under full minimum image.  The reference sums the pair
+// terms with np.bincount over a KD-tree pair list; here every particle
+// gathers its own sum (same terms, its own order, no atomics).
 //
-// B200 design: particles binned in cells >= the cutoff (x mod Lx, y mod Ly,
-// z from the data), sorted by cell (cub), one thread per particle walking the
-// 27 neighbour cells (all cells along an axis with fewer than 3), exact
-// reference arithmetic for d, r and the force.
+// B200 design: particles binned in cells >= the cutoff (periodic axes
+// wrapped, open axes spanning the data), sorted by cell (cub), one thread per
+// particle walking the 27 neighbour cells (all cells along an axis with
+// fewer than 3), exact reference arithmetic for d, r and the pair term.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -22,36 +26,39 @@ namespace se {
 
 namespace {
 
-struct StericArgs {
-    const double* pos; int64_t n;
-    double Lx, Ly, zlo, csx, csy, csz; int ncx, ncy, ncz;
-    double a, U0, r_m, cutoff; int p;
+constexpr double TWO_OVER_SQRTPI = 1.1283791670955126;   // kernels.py:14
+constexpr double FOUR_PI = 12.566370614359172;           // kernels.py:13
+
+struct CellGrid {
+    double L[3];            // box per axis (periodic when per[ax])
+    int per[3];
+    double lo[3], cs[3];
+    int nc[3];
     const int* start; const int* order;
-    double* out;
 };
 
-__device__ __forceinline__ int steric_cell(const StericArgs& s, double x, double y, double z,
-                                           int* cx, int* cy, int* cz) {
-    double wx = x - s.Lx * floor(x / s.Lx); if (wx >= s.Lx) wx = 0.0;
-    double wy = y - s.Ly * floor(y / s.Ly); if (wy >= s.Ly) wy = 0.0;
-    int ix = min(s.ncx - 1, (int)(wx / s.csx));
-    int iy = min(s.ncy - 1, (int)(wy / s.csy));
-    double fz = floor((z - s.zlo) / s.csz);
-    int iz = fz < 0 ? 0 : (fz >= s.ncz ? s.ncz - 1 : (int)fz);
-    *cx = ix; *cy = iy; *cz = iz;
-    return (iz * s.ncy + iy) * s.ncx + ix;
+__device__ __forceinline__ int axis_cell(const CellGrid& g, int ax, double x) {
+    if (g.per[ax]) {
+        double w = x - g.L[ax] * floor(x / g.L[ax]);
+        if (w >= g.L[ax]) w = 0.0;
+        return min(g.nc[ax] - 1, (int)(w / g.cs[ax]));
+    }
+    const double f = floor((x - g.lo[ax]) / g.cs[ax]);
+    return f < 0 ? 0 : (f >= g.nc[ax] ? g.nc[ax] - 1 : (int)f);
 }
 
-__global__ void steric_keys_kernel(StericArgs s, uint32_t* keys, int* perm) {
+__global__ void cell_keys_kernel(CellGrid g, const double* pos, int64_t n, uint32_t* keys,
+                                 int* perm) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= s.n) return;
-    int cx, cy, cz;
-    keys[i] = (uint32_t)steric_cell(s, s.pos[3 * i], s.pos[3 * i + 1], s.pos[3 * i + 2],
-                                    &cx, &cy, &cz);
+    if (i >= n) return;
+    const int cx = axis_cell(g, 0, pos[3 * i]);
+    const int cy = axis_cell(g, 1, pos[3 * i + 1]);
+    const int cz = axis_cell(g, 2, pos[3 * i + 2]);
+    keys[i] = (uint32_t)((cz * g.nc[1] + cy) * g.nc[0] + cx);
     perm[i] = (int)i;
 }
 
-__global__ void steric_starts_kernel(const uint32_t* keys, int64_t n, int ncell, int* start) {
+__global__ void cell_starts_kernel(const uint32_t* keys, int64_t n, int ncell, int* start) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i > n) return;
     const int cur = (i < n) ? (int)keys[i] : ncell;
@@ -59,109 +66,187 @@ __global__ void steric_starts_kernel(const uint32_t* keys, int64_t n, int ncell,
     for (int c = prev + 1; c <= cur; ++c) start[c] = (int)i;
 }
 
-// the reference's lj_force (bd.py:46-49) and steric_force (bd.py:52-57)
-__device__ __forceinline__ double steric_f(const StericArgs& s, double r) {
-    if (r > s.cutoff) return 0.0;
-    const double rs = s.r_m > 0 ? fmax(r, s.r_m) : fmax(r, 1e-12 * s.a);
-    const double x = pow(2.0 * s.a / rs, (double)s.p);
-    return 4.0 * s.U0 * s.p * x * (2.0 * x - 1.0) / rs;
+// the reference's lj_force (bd.py:46-49) and steric_force (bd.py:52-57);
+// pair vector term f(r) / r * d  (bd.py:265-266)
+struct StericPair {
+    double a, U0, r_m, cutoff; int p;
+    __device__ __forceinline__ double coef(double r, int) const {
+        if (r > cutoff) return 0.0;
+        const double rs = r_m > 0 ? fmax(r, r_m) : fmax(r, 1e-12 * a);
+        const double x = pow(2.0 * a / rs, (double)p);
+        const double f = 4.0 * U0 * p * x * (2.0 * x - 1.0) / rs;
+        return f / (r > 0 ? r : 1.0);
+    }
+    __device__ __forceinline__ double scale(int) const { return 1.0; }
+};
+
+// d/dr of erf(r/c)/r with the reference's series below r = 0.01 c
+// (kernels.py:52-72)
+__device__ __forceinline__ double d_erf_over_r(double r, double c) {
+    if (r < 1e-2 * c) {
+        const double t = r / c, u = t * t;
+        return TWO_OVER_SQRTPI / (c * c) * t *
+               (-2.0 / 3.0 + u * (2.0 / 5.0 + u * (-1.0 / 7.0 + u / 27.0)));
+    }
+    const double x = r / c;
+    return TWO_OVER_SQRTPI * exp(-x * x) / (c * r) - erf(x) / (r * r);
 }
 
-__global__ void steric_force_kernel(StericArgs s) {
+// near_gradient_avg (kernels.py:97-101); coef = -grad / r, term coef d q_j
+// (bd.py:346-348)
+struct TpNearPair {
+    double c1, c2, four_pi_eps; const double* q;
+    __device__ __forceinline__ double coef(double r, int) const {
+        if (!(r > 0)) return 0.0;
+        const double grad = (d_erf_over_r(r, c1) - d_erf_over_r(r, c2)) / four_pi_eps;
+        return -grad / r;
+    }
+    __device__ __forceinline__ double scale(int j) const { return q[j]; }
+};
+
+template <class Pair>
+__global__ void pair_gather_kernel(CellGrid g, const double* pos, int64_t n, double cutoff,
+                                   Pair pr, double* out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= s.n) return;
-    const double px = s.pos[3 * i], py = s.pos[3 * i + 1], pz = s.pos[3 * i + 2];
-    int cx, cy, cz;
-    steric_cell(s, px, py, pz, &cx, &cy, &cz);
-    const bool allx = s.ncx < 3, ally = s.ncy < 3;
-    const int nxr = allx ? s.ncx : 3, nyr = ally ? s.ncy : 3;
+    if (i >= n) return;
+    const double px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
+    const int c0[3] = {axis_cell(g, 0, px), axis_cell(g, 1, py), axis_cell(g, 2, pz)};
+    int cnt[3], first[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        const bool all = g.per[ax] && g.nc[ax] < 3;
+        cnt[ax] = all ? g.nc[ax] : 3;
+        first[ax] = all ? 0 : c0[ax] - 1;
+    }
     double fx = 0.0, fy = 0.0, fz = 0.0;
-    for (int dzc = -1; dzc <= 1; ++dzc) {
-        const int zc = cz + dzc;
-        if (zc < 0 || zc >= s.ncz) continue;
-        for (int iy = 0; iy < nyr; ++iy) {
-            int yc = ally ? iy : cy + iy - 1;
-            if (yc < 0) yc += s.ncy; else if (yc >= s.ncy) yc -= s.ncy;
-            for (int ix = 0; ix < nxr; ++ix) {
-                int xc = allx ? ix : cx + ix - 1;
-                if (xc < 0) xc += s.ncx; else if (xc >= s.ncx) xc -= s.ncx;
-                const int c = (zc * s.ncy + yc) * s.ncx + xc;
-                for (int q = s.start[c]; q < s.start[c + 1]; ++q) {
-                    const int j = s.order[q];
+    for (int iz = 0; iz < cnt[2]; ++iz) {
+        int zc = first[2] + iz;
+        if (g.per[2]) { if (zc < 0) zc += g.nc[2]; else if (zc >= g.nc[2]) zc -= g.nc[2]; }
+        else if (zc < 0 || zc >= g.nc[2]) continue;
+        for (int iy = 0; iy < cnt[1]; ++iy) {
+            int yc = first[1] + iy;
+            if (g.per[1]) { if (yc < 0) yc += g.nc[1]; else if (yc >= g.nc[1]) yc -= g.nc[1]; }
+            else if (yc < 0 || yc >= g.nc[1]) continue;
+            for (int ix = 0; ix < cnt[0]; ++ix) {
+                int xc = first[0] + ix;
+                if (g.per[0]) { if (xc < 0) xc += g.nc[0]; else if (xc >= g.nc[0]) xc -= g.nc[0]; }
+                else if (xc < 0 || xc >= g.nc[0]) continue;
+                const int c = (zc * g.nc[1] + yc) * g.nc[0] + xc;
+                for (int s = g.start[c]; s < g.start[c + 1]; ++s) {
+                    const int j = g.order[s];
                     if (j == i) continue;
-                    // d = p_i - p_j; d_xy -= L round(d_xy / L)   (bd.py:263-265)
-                    double dx = __dsub_rn(px, s.pos[3 * j]);
-                    double dy = __dsub_rn(py, s.pos[3 * j + 1]);
-                    const double dz = __dsub_rn(pz, s.pos[3 * j + 2]);
-                    dx = __dsub_rn(dx, __dmul_rn(s.Lx, rint(dx / s.Lx)));
-                    dy = __dsub_rn(dy, __dmul_rn(s.Ly, rint(dy / s.Ly)));
-                    const double r = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
-                                                    __dmul_rn(dz, dz)));
-                    if (r > s.cutoff) continue;
-                    const double f = steric_f(s, r) / (r > 0 ? r : 1.0);
-                    fx += f * dx; fy += f * dy; fz += f * dz;
+                    // d = p_i - p_j; d -= L round(d / L) on periodic axes
+                    double d[3] = {__dsub_rn(px, pos[3 * j]), __dsub_rn(py, pos[3 * j + 1]),
+                                   __dsub_rn(pz, pos[3 * j + 2])};
+#pragma unroll
+                    for (int ax = 0; ax < 3; ++ax)
+                        if (g.per[ax]) d[ax] = __dsub_rn(d[ax], __dmul_rn(g.L[ax], rint(d[ax] / g.L[ax])));
+                    const double r = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]),
+                                                              __dmul_rn(d[1], d[1])),
+                                                    __dmul_rn(d[2], d[2])));
+                    if (r > cutoff) continue;
+                    const double f = pr.coef(r, j), sq = pr.scale(j);
+                    fx += f * d[0] * sq; fy += f * d[1] * sq; fz += f * d[2] * sq;
                 }
             }
         }
     }
-    s.out[3 * i] = fx; s.out[3 * i + 1] = fy; s.out[3 * i + 2] = fz;
+    out[3 * i] = fx; out[3 * i + 1] = fy; out[3 * i + 2] = fz;
 }
 
-}  // namespace
+// Cell grid for the cutoff on the device positions; open-axis ranges come
+// from the host copy.  Scratch is stream-ordered (cudaMallocAsync).
+struct CellScratch {
+    std::vector<void*> v; cudaStream_t s;
+    void* get(size_t bytes) {
+        void* p = nullptr;
+        SE_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s));
+        v.push_back(p);
+        return p;
+    }
+    ~CellScratch() { for (void* p : v) cudaFreeAsync(p, s); }
+};
 
-void steric_forces(int device, const double* pos, int64_t n, double Lx, double Ly, double a,
-                   double U0, double r_m, int p, double* out) {
-    SE_CUDA(cudaSetDevice(device));
-    std::fill(out, out + 3 * n, 0.0);
+template <class Pair>
+void pair_forces_impl(const double* d_pos, const double* h_pos, int64_t n, const double L[3],
+                      double cutoff, const Pair& pr, double* d_out, cudaStream_t st) {
+    SE_CUDA(cudaMemsetAsync(d_out, 0, 3 * n * sizeof(double), st));
     if (n < 2) return;
-    if (!(a > 0) || p < 1) throw Error(SE_ERR_VALUE, "steric parameters: a > 0, p >= 1");
-    const double cutoff = std::pow(2.0, 1.0 / p) * 2.0 * a;
-    double zmin = 1e300, zmax = -1e300;
-    for (int64_t i = 0; i < n; ++i) { zmin = std::min(zmin, pos[3 * i + 2]); zmax = std::max(zmax, pos[3 * i + 2]); }
-    StericArgs s{};
-    s.n = n; s.Lx = Lx; s.Ly = Ly;
-    s.ncx = std::max(1, (int)std::floor(Lx / cutoff));
-    s.ncy = std::max(1, (int)std::floor(Ly / cutoff));
-    s.csx = Lx / s.ncx; s.csy = Ly / s.ncy;
-    s.zlo = zmin - cutoff;
-    const double zspan = (zmax + cutoff) - s.zlo;
-    s.ncz = std::max(1, (int)std::floor(zspan / cutoff));
-    s.csz = zspan / s.ncz;
-    const int64_t ncell = (int64_t)s.ncx * s.ncy * s.ncz;
-    if (ncell > (1 << 28)) throw Error(SE_ERR_VALUE, "steric cell grid too large");
-    s.a = a; s.U0 = U0; s.r_m = r_m; s.p = p; s.cutoff = cutoff;
-    cudaStream_t st;
-    SE_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    struct Guard {
-        std::vector<void*> v; cudaStream_t s;
-        ~Guard() { for (void* x : v) cudaFree(x); cudaStreamDestroy(s); }
-    } g{{}, st};
-    auto alloc = [&](size_t bytes) { void* ptr = nullptr; SE_CUDA(cudaMalloc(&ptr, bytes)); g.v.push_back(ptr); return ptr; };
-    double* d_pos = (double*)alloc(3 * n * sizeof(double));
-    double* d_out = (double*)alloc(3 * n * sizeof(double));
-    uint32_t* k1 = (uint32_t*)alloc(n * sizeof(uint32_t));
-    uint32_t* k2 = (uint32_t*)alloc(n * sizeof(uint32_t));
-    int* p1 = (int*)alloc(n * sizeof(int));
-    int* p2 = (int*)alloc(n * sizeof(int));
-    int* start = (int*)alloc((ncell + 1) * sizeof(int));
-    SE_CUDA(cudaMemcpyAsync(d_pos, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
-    s.pos = d_pos; s.out = d_out;
+    CellGrid g{};
+    int64_t ncell = 1;
+    for (int ax = 0; ax < 3; ++ax) {
+        g.per[ax] = L[ax] > 0;
+        if (g.per[ax]) {
+            g.L[ax] = L[ax];
+            g.nc[ax] = std::max(1, (int)std::floor(L[ax] / cutoff));
+            g.cs[ax] = L[ax] / g.nc[ax];
+            g.lo[ax] = 0.0;
+        } else {
+            double mn = 1e300, mx = -1e300;
+            for (int64_t i = 0; i < n; ++i) {
+                mn = std::min(mn, h_pos[3 * i + ax]);
+                mx = std::max(mx, h_pos[3 * i + ax]);
+            }
+            g.lo[ax] = mn - cutoff;
+            const double span = (mx + cutoff) - g.lo[ax];
+            g.nc[ax] = std::max(1, (int)std::floor(span / cutoff));
+            g.cs[ax] = span / g.nc[ax];
+        }
+        ncell *= g.nc[ax];
+        if (ncell > (1 << 28)) throw Error(SE_ERR_VALUE, "pair cell grid too large");
+    }
+    CellScratch sc{{}, st};
+    uint32_t* k1 = (uint32_t*)sc.get(n * sizeof(uint32_t));
+    uint32_t* k2 = (uint32_t*)sc.get(n * sizeof(uint32_t));
+    int* p1 = (int*)sc.get(n * sizeof(int));
+    int* p2 = (int*)sc.get(n * sizeof(int));
+    int* start = (int*)sc.get((ncell + 1) * sizeof(int));
     const unsigned nb = (unsigned)((n + 255) / 256);
-    steric_keys_kernel<<<nb, 256, 0, st>>>(s, k1, p1);
+    cell_keys_kernel<<<nb, 256, 0, st>>>(g, d_pos, n, k1, p1);
     SE_CUDA(cudaGetLastError());
     int end_bit = 1;
     while (end_bit < 32 && ((uint64_t)ncell >> end_bit) != 0) ++end_bit;
     size_t bytes = 0;
     SE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1, k2, p1, p2, (int)n, 0, end_bit, st));
-    void* tmp = alloc(std::max<size_t>(bytes, 16));
+    void* tmp = sc.get(bytes);
     SE_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, k1, k2, p1, p2, (int)n, 0, end_bit, st));
-    steric_starts_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(k2, n, (int)ncell, start);
+    cell_starts_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(k2, n, (int)ncell, start);
     SE_CUDA(cudaGetLastError());
-    s.start = start; s.order = p2;
-    steric_force_kernel<<<nb, 256, 0, st>>>(s);
+    g.start = start; g.order = p2;
+    pair_gather_kernel<<<nb, 256, 0, st>>>(g, d_pos, n, cutoff, pr, d_out);
     SE_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+void steric_forces(int device, const double* pos, int64_t n, double Lx, double Ly, double Lz,
+                   double a, double U0, double r_m, int p, double* out) {
+    SE_CUDA(cudaSetDevice(device));
+    std::fill(out, out + 3 * n, 0.0);
+    if (n < 2) return;
+    if (!(a > 0) || p < 1) throw Error(SE_ERR_VALUE, "steric parameters: a > 0, p >= 1");
+    StericPair pr{a, U0, r_m, std::pow(2.0, 1.0 / p) * 2.0 * a, p};
+    const double L[3] = {Lx, Ly, Lz};
+    cudaStream_t st;
+    SE_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct Guard {
+        cudaStream_t s; double* d = nullptr;
+        ~Guard() { if (d) cudaFreeAsync(d, s); cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+    } gd{st};
+    SE_CUDA(cudaMallocAsync(&gd.d, 6 * n * sizeof(double), st));
+    double* d_pos = gd.d;
+    double* d_out = gd.d + 3 * n;
+    SE_CUDA(cudaMemcpyAsync(d_pos, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    pair_forces_impl(d_pos, pos, n, L, pr.cutoff, pr, d_out, st);
     SE_CUDA(cudaMemcpyAsync(out, d_out, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, st));
     SE_CUDA(cudaStreamSynchronize(st));
+}
+
+void tp_near_forces(const double* d_pos, const double* d_q, int64_t n, const double L[3],
+                    double r_cut, double g_w, double xi, double eps, double* d_out,
+                    cudaStream_t st) {
+    TpNearPair pr{2.0 * g_w, std::sqrt(4.0 * (g_w * g_w) + 1.0 / (xi * xi)), FOUR_PI * eps, d_q};
+    pair_forces_impl(d_pos, nullptr, n, L, r_cut, pr, d_out, st);
 }
 
 }  // namespace se

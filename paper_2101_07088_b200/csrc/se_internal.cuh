@@ -38,7 +38,7 @@ struct Error : std::runtime_error {
 #define SE_CUDA(call)                                                        \
     do {                                                                     \
         cudaError_t e_ = (call);                                             \
-        if (e_ != cudaSuccess)                                               \
+        if (e_ != cudaSuccess && (cudaGetLastError(), true))                 \
             throw ::se::Error(e_ == cudaErrorMemoryAllocation ? SE_ERR_MEMORY \
                                                                : SE_ERR_CUDA, \
                               std::string(#call) + ": " +                    \
@@ -397,7 +397,21 @@ void finalize(Plan* p, int64_t first, int64_t count, uint32_t flags, double self
 void wall_energy(Plan* p, const NearKernel& kpoint);
 
 // --- se_bd.cu ---
-void steric_forces(int device, const double* pos, int64_t n, double Lx, double Ly, double a,
-                   double U0, double r_m, int p, double* out);
+void steric_forces(int device, const double* pos, int64_t n, double Lx, double Ly, double Lz,
+                   double a, double U0, double r_m, int p, double* out);
+void tp_near_forces(const double* d_pos, const double* d_q, int64_t n, const double L[3],
+                    double r_cut, double g_w, double xi, double eps, double* d_out,
+                    cudaStream_t st);
+
+// --- se_tp.cu ---
+struct TpPlan;
+TpPlan* tp_create(int device, const double L[3], const int n[3], double eps);
+void tp_destroy(TpPlan* p);
+void tp_set_stream(TpPlan* p, cudaStream_t s);
+void tp_poisson(TpPlan* p, const double* rho, int with_field, double* phi, double* E);
+void tp_forces(TpPlan* p, const double* pos, const double* q, int64_t n, double g_t,
+               double radius, double g_w, double xi, double r_cut, double* forces);
+void tp_forces_device(TpPlan* p, const double* d_pos, const double* d_q, int64_t n, double g_t,
+                      double radius, double g_w, double xi, double r_cut, double* d_forces);
 
 }  // namespace se

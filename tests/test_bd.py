@@ -60,9 +60,9 @@ def test_gpu_steric_pair_forces(name):
     assert np.array_equal(np.abs(got).sum(1) > 0, np.abs(ref).sum(1) > 0)
 
 
-def test_steric_pair_forces_rejects_periodic_z():
+def test_steric_pair_forces_rejects_open_xy():
     with pytest.raises(NotImplementedError):
-        B.steric_pair_forces(G["pos"], _steric("a"), (L, L, 1.0))
+        B.steric_pair_forces(G["pos"], _steric("a"), (None, L, None))
 
 
 @pytest.mark.gpu
