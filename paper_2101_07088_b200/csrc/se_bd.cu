@@ -11,14 +11,16 @@
 // gathers its own sum (same terms, its own order, no atomics).
 //
 // B200 design: particles binned in cells >= the cutoff (periodic axes
-// wrapped, open axes spanning the data), sorted by cell (cub), one thread per
+// wrapped, open axes spanning the data), sorted by cell (cub), one warp per
 // particle walking the 27 neighbour cells (all cells along an axis with
-// fewer than 3), exact reference arithmetic for d, r and the pair term.
+// fewer than 3) with in-warp compaction of the hits, exact reference
+// arithmetic for d, r and the pair term.
 #include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cmath>
-#include <vector>
+#include <map>
+#include <mutex>
 
 #include "se_internal.cuh"
 
@@ -31,6 +33,8 @@ constexpr double FOUR_PI = 12.566370614359172;           // kernels.py:13
 
 struct CellGrid {
     double L[3];            // box per axis (periodic when per[ax])
+    double iL[3];           // 1 / L
+    double cut2_hi;         // cutoff^2 (1 + 1e-9): r2 pretest before sqrt
     int per[3];
     double lo[3], cs[3];
     int nc[3];
@@ -104,10 +108,18 @@ struct TpNearPair {
     __device__ __forceinline__ double scale(int j) const { return q[j]; }
 };
 
+// One warp per particle: the lanes test consecutive candidates of each
+// neighbour cell, the hits are compacted into a per-warp queue (ballot) and
+// evaluated 32 at a time, so the expensive pair term runs on full warps.
+constexpr int PAIR_WARPS = 4;
+
 template <class Pair>
-__global__ void pair_gather_kernel(CellGrid g, const double* pos, int64_t n, double cutoff,
-                                   Pair pr, double* out) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(PAIR_WARPS * 32) pair_gather_kernel(
+        CellGrid g, const double* pos, int64_t n, double cutoff, Pair pr, double* out) {
+    __shared__ double qd[PAIR_WARPS][4][64];        // dx, dy, dz, r of queued hits
+    __shared__ int qj[PAIR_WARPS][64];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * (int64_t)PAIR_WARPS + wib;
     if (i >= n) return;
     const double px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
     const int c0[3] = {axis_cell(g, 0, px), axis_cell(g, 1, py), axis_cell(g, 2, pz)};
@@ -119,6 +131,15 @@ __global__ void pair_gather_kernel(CellGrid g, const double* pos, int64_t n, dou
         first[ax] = all ? 0 : c0[ax] - 1;
     }
     double fx = 0.0, fy = 0.0, fz = 0.0;
+    int qn = 0;
+    auto eval = [&](int e) {
+        const double r = qd[wib][3][e];
+        const int j = qj[wib][e];
+        const double f = pr.coef(r, j), sq = pr.scale(j);
+        fx += f * qd[wib][0][e] * sq;
+        fy += f * qd[wib][1][e] * sq;
+        fz += f * qd[wib][2][e] * sq;
+    };
     for (int iz = 0; iz < cnt[2]; ++iz) {
         int zc = first[2] + iz;
         if (g.per[2]) { if (zc < 0) zc += g.nc[2]; else if (zc >= g.nc[2]) zc -= g.nc[2]; }
@@ -132,52 +153,81 @@ __global__ void pair_gather_kernel(CellGrid g, const double* pos, int64_t n, dou
                 if (g.per[0]) { if (xc < 0) xc += g.nc[0]; else if (xc >= g.nc[0]) xc -= g.nc[0]; }
                 else if (xc < 0 || xc >= g.nc[0]) continue;
                 const int c = (zc * g.nc[1] + yc) * g.nc[0] + xc;
-                for (int s = g.start[c]; s < g.start[c + 1]; ++s) {
-                    const int j = g.order[s];
-                    if (j == i) continue;
-                    // d = p_i - p_j; d -= L round(d / L) on periodic axes
-                    double d[3] = {__dsub_rn(px, pos[3 * j]), __dsub_rn(py, pos[3 * j + 1]),
-                                   __dsub_rn(pz, pos[3 * j + 2])};
+                const int e0 = g.start[c], e1 = g.start[c + 1];
+                for (int b = e0; b < e1; b += 32) {
+                    const int s = b + lane;
+                    bool hit = false;
+                    double d[3], r = 0.0;
+                    int j = -1;
+                    if (s < e1) {
+                        j = g.order[s];
+                        // d = p_i - p_j; d -= L round(d / L) on periodic axes.
+                        // round(d * (1/L)) differs from round(d / L) only
+                        // for |d| within ulps of L/2 > cutoff: never a pair
+                        d[0] = __dsub_rn(px, pos[3 * j]);
+                        d[1] = __dsub_rn(py, pos[3 * j + 1]);
+                        d[2] = __dsub_rn(pz, pos[3 * j + 2]);
 #pragma unroll
-                    for (int ax = 0; ax < 3; ++ax)
-                        if (g.per[ax]) d[ax] = __dsub_rn(d[ax], __dmul_rn(g.L[ax], rint(d[ax] / g.L[ax])));
-                    const double r = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]),
-                                                              __dmul_rn(d[1], d[1])),
-                                                    __dmul_rn(d[2], d[2])));
-                    if (r > cutoff) continue;
-                    const double f = pr.coef(r, j), sq = pr.scale(j);
-                    fx += f * d[0] * sq; fy += f * d[1] * sq; fz += f * d[2] * sq;
+                        for (int ax = 0; ax < 3; ++ax)
+                            if (g.per[ax]) d[ax] = __dsub_rn(d[ax], __dmul_rn(g.L[ax], rint(d[ax] * g.iL[ax])));
+                        const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])),
+                                                    __dmul_rn(d[2], d[2]));
+                        // sqrt (correctly rounded) only near or inside the cutoff
+                        if (r2 <= g.cut2_hi) {
+                            r = sqrt(r2);
+                            hit = j != i && r <= cutoff;
+                        }
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                    if (hit) {
+                        const int slot = qn + __popc(bal & ((1u << lane) - 1u));
+                        qd[wib][0][slot] = d[0]; qd[wib][1][slot] = d[1];
+                        qd[wib][2][slot] = d[2]; qd[wib][3][slot] = r;
+                        qj[wib][slot] = j;
+                    }
+                    qn += __popc(bal);
+                    __syncwarp();
+                    if (qn >= 32) {
+                        eval(lane);
+                        __syncwarp();
+                        if (lane < qn - 32) {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) qd[wib][k][lane] = qd[wib][k][32 + lane];
+                            qj[wib][lane] = qj[wib][32 + lane];
+                        }
+                        qn -= 32;
+                        __syncwarp();
+                    }
                 }
             }
         }
     }
-    out[3 * i] = fx; out[3 * i + 1] = fy; out[3 * i + 2] = fz;
+    if (lane < qn) eval(lane);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        fx += __shfl_xor_sync(0xffffffffu, fx, o);
+        fy += __shfl_xor_sync(0xffffffffu, fy, o);
+        fz += __shfl_xor_sync(0xffffffffu, fz, o);
+    }
+    if (lane == 0) { out[3 * i] = fx; out[3 * i + 1] = fy; out[3 * i + 2] = fz; }
 }
 
 // Cell grid for the cutoff on the device positions; open-axis ranges come
-// from the host copy.  Scratch is stream-ordered (cudaMallocAsync).
-struct CellScratch {
-    std::vector<void*> v; cudaStream_t s;
-    void* get(size_t bytes) {
-        void* p = nullptr;
-        SE_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s));
-        v.push_back(p);
-        return p;
-    }
-    ~CellScratch() { for (void* p : v) cudaFreeAsync(p, s); }
-};
-
+// from the host copy.  Scratch persists in a PairScratch.
 template <class Pair>
 void pair_forces_impl(const double* d_pos, const double* h_pos, int64_t n, const double L[3],
-                      double cutoff, const Pair& pr, double* d_out, cudaStream_t st) {
+                      double cutoff, const Pair& pr, double* d_out, cudaStream_t st,
+                      PairScratch& sc) {
     SE_CUDA(cudaMemsetAsync(d_out, 0, 3 * n * sizeof(double), st));
     if (n < 2) return;
     CellGrid g{};
+    g.cut2_hi = cutoff * cutoff * (1.0 + 1e-9);
     int64_t ncell = 1;
     for (int ax = 0; ax < 3; ++ax) {
         g.per[ax] = L[ax] > 0;
         if (g.per[ax]) {
             g.L[ax] = L[ax];
+            g.iL[ax] = 1.0 / L[ax];
             g.nc[ax] = std::max(1, (int)std::floor(L[ax] / cutoff));
             g.cs[ax] = L[ax] / g.nc[ax];
             g.lo[ax] = 0.0;
@@ -195,58 +245,91 @@ void pair_forces_impl(const double* d_pos, const double* h_pos, int64_t n, const
         ncell *= g.nc[ax];
         if (ncell > (1 << 28)) throw Error(SE_ERR_VALUE, "pair cell grid too large");
     }
-    CellScratch sc{{}, st};
-    uint32_t* k1 = (uint32_t*)sc.get(n * sizeof(uint32_t));
-    uint32_t* k2 = (uint32_t*)sc.get(n * sizeof(uint32_t));
-    int* p1 = (int*)sc.get(n * sizeof(int));
-    int* p2 = (int*)sc.get(n * sizeof(int));
-    int* start = (int*)sc.get((ncell + 1) * sizeof(int));
+    sc.reserve(n, ncell);
+    uint32_t *k1 = sc.k1, *k2 = sc.k2;
+    int *p1 = sc.p1, *p2 = sc.p2, *start = sc.start;
     const unsigned nb = (unsigned)((n + 255) / 256);
     cell_keys_kernel<<<nb, 256, 0, st>>>(g, d_pos, n, k1, p1);
     SE_CUDA(cudaGetLastError());
     int end_bit = 1;
     while (end_bit < 32 && ((uint64_t)ncell >> end_bit) != 0) ++end_bit;
-    size_t bytes = 0;
-    SE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1, k2, p1, p2, (int)n, 0, end_bit, st));
-    void* tmp = sc.get(bytes);
-    SE_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, k1, k2, p1, p2, (int)n, 0, end_bit, st));
+    size_t bytes = sc.tbytes;
+    SE_CUDA(cub::DeviceRadixSort::SortPairs(sc.tmp, bytes, k1, k2, p1, p2, (int)n, 0, end_bit, st));
     cell_starts_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(k2, n, (int)ncell, start);
     SE_CUDA(cudaGetLastError());
     g.start = start; g.order = p2;
-    pair_gather_kernel<<<nb, 256, 0, st>>>(g, d_pos, n, cutoff, pr, d_out);
+    pair_gather_kernel<<<(unsigned)((n + PAIR_WARPS - 1) / PAIR_WARPS), PAIR_WARPS * 32, 0, st>>>(
+        g, d_pos, n, cutoff, pr, d_out);
     SE_CUDA(cudaGetLastError());
 }
 
 }  // namespace
 
+void PairScratch::reserve(int64_t n, int64_t ncell) {
+    if (n > ncap) {
+        cudaFree(k1); cudaFree(k2); cudaFree(p1); cudaFree(p2); cudaFree(tmp);
+        k1 = k2 = nullptr; p1 = p2 = nullptr; tmp = nullptr; ncap = 0;
+        SE_CUDA(cudaMalloc(&k1, n * sizeof(uint32_t)));
+        SE_CUDA(cudaMalloc(&k2, n * sizeof(uint32_t)));
+        SE_CUDA(cudaMalloc(&p1, n * sizeof(int)));
+        SE_CUDA(cudaMalloc(&p2, n * sizeof(int)));
+        size_t b = 0;
+        SE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, k1, k2, p1, p2, (int)n, 0, 32));
+        tbytes = std::max<size_t>(b, 16);
+        SE_CUDA(cudaMalloc(&tmp, tbytes));
+        ncap = n;
+    }
+    if (ncell + 1 > ccap) {
+        cudaFree(start);
+        start = nullptr; ccap = 0;
+        SE_CUDA(cudaMalloc(&start, (ncell + 1) * sizeof(int)));
+        ccap = ncell + 1;
+    }
+}
+
+void PairScratch::release() {
+    cudaFree(k1); cudaFree(k2); cudaFree(p1); cudaFree(p2); cudaFree(start); cudaFree(tmp);
+    cudaFree(buf);
+    if (stream) cudaStreamDestroy(stream);
+    k1 = k2 = nullptr; p1 = p2 = start = nullptr; tmp = nullptr; buf = nullptr; stream = nullptr;
+    ncap = ccap = bcap = 0;
+}
+
+// se_steric_forces keeps one scratch (and stream) per device between calls
+static std::mutex g_steric_mu;
+static std::map<int, PairScratch> g_steric;
+
 void steric_forces(int device, const double* pos, int64_t n, double Lx, double Ly, double Lz,
                    double a, double U0, double r_m, int p, double* out) {
-    SE_CUDA(cudaSetDevice(device));
     std::fill(out, out + 3 * n, 0.0);
     if (n < 2) return;
     if (!(a > 0) || p < 1) throw Error(SE_ERR_VALUE, "steric parameters: a > 0, p >= 1");
+    std::lock_guard<std::mutex> lock(g_steric_mu);
+    SE_CUDA(cudaSetDevice(device));
+    PairScratch& sc = g_steric[device];
+    if (!sc.stream) SE_CUDA(cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking));
+    if (n > sc.bcap) {
+        cudaFree(sc.buf);
+        sc.buf = nullptr; sc.bcap = 0;
+        SE_CUDA(cudaMalloc(&sc.buf, 6 * n * sizeof(double)));
+        sc.bcap = n;
+    }
     StericPair pr{a, U0, r_m, std::pow(2.0, 1.0 / p) * 2.0 * a, p};
     const double L[3] = {Lx, Ly, Lz};
-    cudaStream_t st;
-    SE_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    struct Guard {
-        cudaStream_t s; double* d = nullptr;
-        ~Guard() { if (d) cudaFreeAsync(d, s); cudaStreamSynchronize(s); cudaStreamDestroy(s); }
-    } gd{st};
-    SE_CUDA(cudaMallocAsync(&gd.d, 6 * n * sizeof(double), st));
-    double* d_pos = gd.d;
-    double* d_out = gd.d + 3 * n;
+    cudaStream_t st = sc.stream;
+    double* d_pos = sc.buf;
+    double* d_out = sc.buf + 3 * sc.bcap;
     SE_CUDA(cudaMemcpyAsync(d_pos, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
-    pair_forces_impl(d_pos, pos, n, L, pr.cutoff, pr, d_out, st);
+    pair_forces_impl(d_pos, pos, n, L, pr.cutoff, pr, d_out, st, sc);
     SE_CUDA(cudaMemcpyAsync(out, d_out, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, st));
     SE_CUDA(cudaStreamSynchronize(st));
 }
 
 void tp_near_forces(const double* d_pos, const double* d_q, int64_t n, const double L[3],
                     double r_cut, double g_w, double xi, double eps, double* d_out,
-                    cudaStream_t st) {
+                    cudaStream_t st, PairScratch& sc) {
     TpNearPair pr{2.0 * g_w, std::sqrt(4.0 * (g_w * g_w) + 1.0 / (xi * xi)), FOUR_PI * eps, d_q};
-    pair_forces_impl(d_pos, nullptr, n, L, r_cut, pr, d_out, st);
+    pair_forces_impl(d_pos, nullptr, n, L, r_cut, pr, d_out, st, sc);
 }
 
 }  // namespace se

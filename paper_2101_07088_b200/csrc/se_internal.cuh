@@ -397,11 +397,24 @@ void finalize(Plan* p, int64_t first, int64_t count, uint32_t flags, double self
 void wall_energy(Plan* p, const NearKernel& kpoint);
 
 // --- se_bd.cu ---
+// persistent device scratch of the cell-list pair kernels (grown on demand)
+struct PairScratch {
+    int64_t ncap = 0, ccap = 0, bcap = 0;
+    size_t tbytes = 0;
+    uint32_t *k1 = nullptr, *k2 = nullptr;
+    int *p1 = nullptr, *p2 = nullptr, *start = nullptr;
+    void* tmp = nullptr;
+    double* buf = nullptr;            // host-API staging: pos[3n] + out[3n]
+    cudaStream_t stream = nullptr;    // host-API stream
+    void reserve(int64_t n, int64_t ncell);
+    void release();
+    ~PairScratch() { release(); }
+};
 void steric_forces(int device, const double* pos, int64_t n, double Lx, double Ly, double Lz,
                    double a, double U0, double r_m, int p, double* out);
 void tp_near_forces(const double* d_pos, const double* d_q, int64_t n, const double L[3],
                     double r_cut, double g_w, double xi, double eps, double* d_out,
-                    cudaStream_t st);
+                    cudaStream_t st, PairScratch& sc);
 
 // --- se_tp.cu ---
 struct TpPlan;

@@ -185,8 +185,10 @@ struct TpPlan {
     cufftDoubleComplex* d_hat = nullptr;       // [5][half]: rho_hat, phi_hat, E_hat x3
     int64_t cap = 0;
     double* d_pts = nullptr;                   // pos[3cap] q[cap] far[3cap] near[3cap] F[3cap]
+    PairScratch pairs;                         // near-field cell list
     ~TpPlan() {
         if (dev >= 0) cudaSetDevice(dev);
+        pairs.release();
         if (fwd) cufftDestroy(fwd);
         if (inv) cufftDestroy(inv);
         cudaFree(d_grid); cudaFree(d_hat); cudaFree(d_pts);
@@ -308,7 +310,7 @@ void tp_forces_device(TpPlan* p, const double* d_pos, const double* d_q, int64_t
     tp_interp_kernel<<<nb, TP_WARPS * 32, 0, p->stream>>>(g, d_pos, n, p->d_grid + p->G,
                                                           p->h[0] * p->h[1] * p->h[2], d_far);
     SE_CUDA(cudaGetLastError());
-    tp_near_forces(d_pos, d_q, n, p->L, r_cut, g_w, xi, p->eps, d_near, p->stream);
+    tp_near_forces(d_pos, d_q, n, p->L, r_cut, g_w, xi, p->eps, d_near, p->stream, p->pairs);
     tp_combine_kernel<<<(unsigned)((3 * n + 255) / 256), 256, 0, p->stream>>>(d_q, d_far, d_near,
                                                                             n, d_forces);
     SE_CUDA(cudaGetLastError());

@@ -33,6 +33,10 @@ WORKLOADS = {
     "c5": dict(L=8.0, H=1.0, eps_b=0.05, eps_t=0.05,
                g_w=0.25 * 1.4 * 2.0 / 256, delta=1e-4, Nxy=1024,
                N=1 << 24, seed=0),
+    # the paper's performance study:
+    # 2e4 charges, H = 50, L = 185, g_w = a/4 (a = 1), optimum N_xy = 88
+    "paper": dict(L=185.0, H=50.0, eps_b=0.05, eps_t=0.05, g_w=0.25,
+                  delta=1e-4, Nxy=88, N=20000, seed=0),
 }
 
 

@@ -1,0 +1,151 @@
+"""The paper's own performance configuration on this GPU (BASELINE.md 1,
+PAPER.md:1043-1060): 2e4 random charges, H = 50, L = 185, g_w = a/4.
+
+* DP solve (energy + forces + potential) at N_xy = 88 (paper: 4.3 ms on an
+  RTX 2080Ti in fp32 with the correction in fp64), fp64 and fp32 modes;
+* triply periodic forces, Lz = 2H, N_xy = 70 (paper: 0.84 ms);
+* one BD step of the slab run (solve with need_energy=False + steric + wall
+  forces + the host Euler-Maruyama update; paper: ~5 ms).
+
+Device times are CUDA events around device-resident calls, median of
+``steps`` after ``warmup``; the BD step is wall clock (it includes the host
+RNG and the host<->device copies of the public API).
+
+    python tools/paper_perf.py [steps]
+"""
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2101_07088_b200 import bd as B                       # noqa: E402
+from paper_2101_07088_b200 import workloads as W                # noqa: E402
+from paper_2101_07088_b200.periodic import TriplyPeriodicSolver  # noqa: E402
+from paper_2101_07088_b200.slab import SlabSolver               # noqa: E402
+
+
+def _median_ms(fn, steps, warmup, stream):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    return float(np.median(times))
+
+
+DP_SWEEP = (88, 104, 120, 136, 152, 168, 184, 200)
+TP_SWEEP = (70, 90, 110, 130, 150, 170, 190)
+
+
+def measure(steps=20, warmup=5, sweep=True):
+    """Times at the paper's grids and, with ``sweep``, at the optimum split
+    on this GPU (the paper quotes each method at its own optimum N_xy)."""
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev)
+    system, params = W.build("paper")
+    n = system.charges.size
+    pos = torch.as_tensor(system.positions, device=dev).contiguous()
+    q = torch.as_tensor(system.charges, device=dev).contiguous()
+    phi = torch.empty(n, dtype=torch.float64, device=dev)
+    E = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    out = {"workload": "paper: N=2e4, H=50, L=185, g_w=0.25, eps_b=eps_t=0.05, delta=1e-4",
+           "grid_dp": [params.Nx, params.Ny, params.Nz]}
+    for prec in ("fp64", "fp32"):
+        s = SlabSolver(system, params, precision=prec)
+        s.set_stream(stream.cuda_stream)
+        out["dp_ms_" + prec] = _median_ms(
+            lambda: s.solve_device(pos.data_ptr(), phi.data_ptr(), E.data_ptr(), n),
+            steps, warmup, stream)
+        s.close()
+    out["dp_ms_published"] = 4.3
+    if sweep:
+        best = None
+        for nxy in DP_SWEEP:
+            try:
+                sy, pr = W.build("paper", Nxy=nxy)
+            except Exception:
+                continue
+            s = SlabSolver(sy, pr)
+            s.set_stream(stream.cuda_stream)
+            t = _median_ms(lambda: s.solve_device(pos.data_ptr(), phi.data_ptr(), E.data_ptr(), n),
+                           steps, warmup, stream)
+            s.close()
+            out.setdefault("dp_sweep_ms", {})[nxy] = t
+            if best is None or t < best[1]:
+                best = (nxy, t)
+        out["dp_opt"] = {"Nxy": best[0], "ms_fp64": best[1]}
+    geo = system.geometry
+    box = (geo.Lx, geo.Ly, 2.0 * geo.H)
+    tp = TriplyPeriodicSolver(box, 70, system.g_w, geo.eps, delta=1e-4)
+    tp.set_stream(stream.cuda_stream)
+    F = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    out["tp_grid"] = list(tp.n)
+    out["tp_ms"] = _median_ms(
+        lambda: tp.forces_device(pos.data_ptr(), q.data_ptr(), n, F.data_ptr()),
+        steps, warmup, stream)
+    out["tp_ms_published"] = 0.84
+    tp.close()
+    if sweep:
+        best = None
+        for ng in TP_SWEEP:
+            try:
+                t2 = TriplyPeriodicSolver(box, ng, system.g_w, geo.eps, delta=1e-4)
+            except ValueError:
+                continue
+            t2.set_stream(stream.cuda_stream)
+            t = _median_ms(lambda: t2.forces_device(pos.data_ptr(), q.data_ptr(), n, F.data_ptr()),
+                           steps, warmup, stream)
+            t2.close()
+            out.setdefault("tp_sweep_ms", {})[ng] = t
+            if best is None or t < best[1]:
+                best = (ng, t)
+        out["tp_opt"] = {"n_grid": best[0], "ms": best[1]}
+    # one BD step of the slab run through the public host API
+    solver = SlabSolver(system, params)
+    steric = B.StericParams(a=1.0)
+    cfg = B.BdConfig(dt=1e-4, steps=1, seed=1, max_disp=1.0)
+    # random placement puts charges arbitrarily close to the z bounds, where
+    # a capped step (max_disp) can be rejected forever: start them max_disp
+    # inside the bounds (same x, y and ordering)
+    lo = params.n_sigma * system.g_w
+    z = system.positions[:, 2]
+    start = system.positions.copy()
+    start[:, 2] = (lo + 1.5) + (z - lo) * (geo.H - 2 * lo - 3.0) / (geo.H - 2 * lo)
+    state = B.make_state(start, cfg)
+    for _ in range(3):
+        B.bd_run(solver, steric, cfg, steps=1, state=state)
+    t = []
+    for _ in range(max(3, steps // 4)):
+        t0 = time.perf_counter()
+        B.bd_run(solver, steric, cfg, steps=1, state=state)
+        t.append((time.perf_counter() - t0) * 1e3)
+    out["bd_step_ms_wall"] = float(np.median(t))
+    parts = {"solve": lambda: solver.solve(positions=state.positions, need_energy=False),
+             "steric": lambda: B.steric_pair_forces(state.positions, steric, (geo.Lx, geo.Ly, None)),
+             "wall": lambda: B.wall_steric_forces(state.positions, steric, geo.H)}
+    for k, fn in parts.items():
+        fn()
+        t0 = time.perf_counter()
+        for _ in range(5):
+            fn()
+        out["bd_part_ms_" + k] = (time.perf_counter() - t0) * 200.0
+    out["bd_step_ms_published"] = 5.0
+    solver.close()
+    return out
+
+
+if __name__ == "__main__":
+    print(json.dumps(measure(int(sys.argv[1]) if len(sys.argv) > 1 else 20)))
