@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-paper-config", action="store_true",
+                    help="skip the paper's own performance configuration")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded solver even on one rank")
@@ -382,6 +384,12 @@ def run_ours(args):
             "gpu_launches": launches,
             "kernel_ms": stage, "near_pairs": pairs,
             "roofline": roof, "clocks": clk}
+    if world == 1 and not args.no_paper_config:
+        # the paper's published timings (DP 4.3 ms, TP 0.84 ms,
+        # BD step ~5 ms, RTX 2080Ti fp32) on their configuration, N = 2e4
+        sys.path.insert(0, os.path.join(REPO, "tools"))
+        import paper_perf
+        line["paper_config"] = paper_perf.measure(steps=10, warmup=3)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(system, params)
     print(json.dumps(line), flush=True)
