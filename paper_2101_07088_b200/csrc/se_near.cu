@@ -603,6 +603,141 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_eval_kernel(NearArgs a)
     if (lane == 0 && a.npairs && cnt) atomicAdd((unsigned long long*)a.npairs, cnt);
 }
 
+// One pair of an evaluation point (eval_list's body for one source).
+template <bool FAR, bool F32>
+__device__ __forceinline__ void eval_pair(const NearArgs& a, const double* tab, int j,
+                                          double px, double py, double pz, int64_t self_i,
+                                          double& phi, double& ex, double& ey, double& ez,
+                                          int& count) {
+    const double4 sv = a.src[j];
+    const double dx = min_image(__dsub_rn(px, sv.x), a.g.Lx);
+    const double dy = min_image(__dsub_rn(py, sv.y), a.g.Ly);
+    const double dz = __dsub_rn(pz, sv.z);
+    const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    if (r2 >= a.win_lo && r2 <= a.r2max) {
+        defer_pair(a, self_i, j);                 // decided by near_boundary_kernel
+    } else if (r2 <= a.r2max) {
+        double g, coef;
+        pair_terms<FAR, F32>(a, tab, r2, g, coef);
+        phi = fma(sv.w, g, phi);
+        if (a.need_field) {
+            const double cq = coef * sv.w;
+            ex = fma(cq, dx, ex); ey = fma(cq, dy, ey); ez = fma(cq, dz, ez);
+        }
+        ++count;
+    }
+}
+
+// Fused near field: one warp per evaluation point (cell-sorted order, so
+// neighbouring warps share their source windows in L1).  The lanes walk the
+// point's chord windows 32 sources at a time with the fp32 pre-test; the
+// hits are compacted (ballot) into a far and a close queue in shared memory
+// and evaluated 32 at a time, so the pair kernels run on full warps and no
+// pair list goes through HBM.
+constexpr int FQ = 64;
+constexpr int64_t NEAR_FUSED_MAX = 40000;       // evaluation points (measured crossover)
+
+template <bool F32, int MINB>
+__global__ void __launch_bounds__(NB_THREADS, MINB) near_fused_kernel(NearArgs a) {
+    constexpr int W = NB_THREADS / 32;
+    __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + CL_TAB];
+    __shared__ int qf[W][FQ], qc[W][FQ];
+    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+    for (int e = tid; e < SE_ERFCX_NP * (SE_ERFCX_DEG + 1); e += blockDim.x)
+        tab[e] = (&se_erfcx_tab[0][0])[e];
+    if (a.use_ctab)
+        for (int e = tid; e < CL_TAB; e += blockDim.x)
+            tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + e] = a.ctab[e];
+    __syncthreads();
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
+    if (w >= a.ne) return;
+    const int64_t i = a.order[w];
+    const double px = a.eval[3 * i], py = a.eval[3 * i + 1], pz = a.eval[3 * i + 2];
+    int cx, cy, cz;
+    cell_of(a.g, px, py, pz, &cx, &cy, &cz);
+    const float pxf = (float)wrap(px, a.g.Lx), pyf = (float)wrap(py, a.g.Ly);
+    const float pzf = (float)(pz - a.g.zlo);
+    const ColumnWalk cw = column_walk(a.g);
+    const float r2f = a.r2f, r2c = a.r2close;
+    const float csxf = (float)a.g.csx, csyf = (float)a.g.csy, icsz = (float)(1.0 / a.g.csz);
+    const int nzb = a.g.ncz;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int count = 0, nf = 0, nc = 0;
+    const unsigned below = (1u << lane) - 1u;
+    for (int iy = 0; iy < cw.nyr; ++iy) {
+        int yc; float sy, dyd;
+        column_axis(cy, iy, cw.ally, a.g.ncy, csyf, a.Lyf, pyf, &yc, &sy, &dyd);
+        for (int ix = 0; ix < cw.nxr; ++ix) {
+            int xc; float sx, dxd;
+            column_axis(cx, ix, cw.allx, a.g.ncx, csxf, a.Lxf, pxf, &xc, &sx, &dxd);
+            const float d2 = fmaf(dxd, dxd, dyd * dyd);
+            if (d2 > r2f) continue;
+            const float hz = sqrtf(r2f - d2) * 1.0001f + a.zmarg;
+            const int z0 = max(0, min(nzb - 1, (int)floorf((pzf - hz) * icsz)));
+            const int z1 = max(0, min(nzb - 1, (int)floorf((pzf + hz) * icsz)));
+            const int base = (yc * a.g.ncx + xc) * nzb;
+            const int j0 = a.start[base + z0], j1 = a.start[base + z1 + 1];
+            const float qx = pxf - sx, qy = pyf - sy;
+            for (int b = j0; b < j1; b += 32) {
+                const int s = b + lane;
+                bool far = false, close = false;
+                if (s < j1) {
+                    const float4 f = a.srcf[s];
+                    float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
+                    if (cw.allx) dx -= a.Lxf * rintf(dx * a.iLxf);
+                    if (cw.ally) dy -= a.Lyf * rintf(dy * a.iLyf);
+                    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                    if (r2 <= r2f) { far = r2 > r2c; close = !far; }
+                }
+                const unsigned bf = __ballot_sync(0xffffffffu, far);
+                const unsigned bc = __ballot_sync(0xffffffffu, close);
+                if (far) qf[wib][nf + __popc(bf & below)] = s;
+                if (close) qc[wib][nc + __popc(bc & below)] = s;
+                nf += __popc(bf);
+                nc += __popc(bc);
+                __syncwarp();
+                if (nf >= 32) {
+                    eval_pair<true, F32>(a, tab, qf[wib][lane], px, py, pz, i, acc[0], acc[1],
+                                         acc[2], acc[3], count);
+                    __syncwarp();
+                    if (lane < nf - 32) qf[wib][lane] = qf[wib][32 + lane];
+                    nf -= 32;
+                    __syncwarp();
+                }
+                if (nc >= 32) {
+                    eval_pair<false, false>(a, tab, qc[wib][lane], px, py, pz, i, acc[0], acc[1],
+                                            acc[2], acc[3], count);
+                    __syncwarp();
+                    if (lane < nc - 32) qc[wib][lane] = qc[wib][32 + lane];
+                    nc -= 32;
+                    __syncwarp();
+                }
+            }
+        }
+    }
+    if (lane < nf)
+        eval_pair<true, F32>(a, tab, qf[wib][lane], px, py, pz, i, acc[0], acc[1], acc[2], acc[3],
+                             count);
+    if (lane < nc)
+        eval_pair<false, false>(a, tab, qc[wib][lane], px, py, pz, i, acc[0], acc[1], acc[2],
+                                acc[3], count);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+        count += __shfl_xor_sync(0xffffffffu, count, o);
+    }
+    if (lane == 0) {
+        a.out[i] = acc[0];
+        if (a.need_field) {
+            a.out[a.out_stride + i] = acc[1];
+            a.out[2 * a.out_stride + i] = acc[2];
+            a.out[3 * a.out_stride + i] = acc[3];
+        }
+        if (a.npairs && count) atomicAdd((unsigned long long*)a.npairs, (unsigned long long)count);
+    }
+}
+
 // A few evaluation points (the gauge origin): one CTA per point, the threads
 // stride over the 27 neighbour cells' sources with the exact test and the
 // general kernel, then a block reduction.  Avoids the sort / task / list
@@ -1163,6 +1298,25 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     point_starts_kernel<<<(unsigned)((ne + 1 + 255) / 256), 256, 0, p->stream>>>(ns.keys2, ne,
                                                                                   ncell, ns.pstart);
     SE_LAUNCHED(p);
+    // Small problems (latency-bound: too few 32-point tasks to fill the GPU)
+    // take the fused one-warp-per-point kernel, no pair lists and no host
+    // sync; large ones the scan -> lists -> eval pipeline, which amortises
+    // the chord-window set-up over the 32 points of a task.
+    static const char* fenv = getenv("SE_NEAR_FUSED");
+    const bool fused = fenv ? atoi(fenv) != 0 : ne <= NEAR_FUSED_MAX;
+    if (fused) {
+        a.order = ns.order;
+        const unsigned nblk = (unsigned)((ne * 32 + NB_THREADS - 1) / NB_THREADS);
+        a.use_ctab = close_ok ? 1 : 0;
+        if (d_npairs) { p->ktic(3); p->ktic(4); p->ktoc(4); p->ktic(5); }
+        if (k.fp32) near_fused_kernel<true, 6><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        else near_fused_kernel<false, 6><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        SE_LAUNCHED(p);
+        near_boundary_kernel<<<4, 256, 0, p->stream>>>(a);
+        if (d_npairs) { p->ktoc(5); p->ktoc(3); }
+        SE_LAUNCHED(p);
+        return;
+    }
     const int nzb = p->cl.ncz;
     task_count_kernel<<<(ncol + 255) / 256, 256, 0, p->stream>>>(ns.pstart, ncol, nzb, ns.tcount);
     SE_LAUNCHED(p);

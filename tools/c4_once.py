@@ -8,7 +8,7 @@ from paper_2101_07088_b200.slab import SlabSolver
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c4"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-s, p = W.build(name)
+s, p = W.build(name, N=int(sys.argv[3]) if len(sys.argv) > 3 else None)
 solver = SlabSolver(s, p)
 for _ in range(reps):
     res = solver.solve(timings=True)
