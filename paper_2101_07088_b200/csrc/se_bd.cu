@@ -39,6 +39,7 @@ struct CellGrid {
     double lo[3], cs[3];
     int nc[3];
     const int* start; const int* order;
+    const double4* spos;    // cell-sorted (x, y, z, q)
 };
 
 __device__ __forceinline__ int axis_cell(const CellGrid& g, int ax, double x) {
@@ -62,6 +63,14 @@ __global__ void cell_keys_kernel(CellGrid g, const double* pos, int64_t n, uint3
     perm[i] = (int)i;
 }
 
+__global__ void cell_gather_kernel(const double* pos, const double* q, const int* order,
+                                   int64_t n, double4* spos) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const int j = order[s];
+    spos[s] = make_double4(pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], q ? q[j] : 1.0);
+}
+
 __global__ void cell_starts_kernel(const uint32_t* keys, int64_t n, int ncell, int* start) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i > n) return;
@@ -81,7 +90,7 @@ struct StericPair {
         const double f = 4.0 * U0 * p * x * (2.0 * x - 1.0) / rs;
         return f / (r > 0 ? r : 1.0);
     }
-    __device__ __forceinline__ double scale(int) const { return 1.0; }
+    static constexpr bool kUsesQ = false;
 };
 
 // d/dr of erf(r/c)/r with the reference's series below r = 0.01 c
@@ -102,10 +111,13 @@ struct TpNearPair {
     double c1, c2, four_pi_eps; const double* q;
     __device__ __forceinline__ double coef(double r, int) const {
         if (!(r > 0)) return 0.0;
-        const double grad = (d_erf_over_r(r, c1) - d_erf_over_r(r, c2)) / four_pi_eps;
+        // beyond r = 6.5 c1 the exp term is < 1e-17 of erf(x)/r^2 and erf(x)
+        // rounds to 1: the closed form is -1/r^2 to the last bit
+        const double d1 = r > 6.5 * c1 ? -1.0 / (r * r) : d_erf_over_r(r, c1);
+        const double grad = (d1 - d_erf_over_r(r, c2)) / four_pi_eps;
         return -grad / r;
     }
-    __device__ __forceinline__ double scale(int j) const { return q[j]; }
+    static constexpr bool kUsesQ = true;
 };
 
 // One warp per particle: the lanes test consecutive candidates of each
@@ -116,7 +128,7 @@ constexpr int PAIR_WARPS = 4;
 template <class Pair>
 __global__ void __launch_bounds__(PAIR_WARPS * 32) pair_gather_kernel(
         CellGrid g, const double* pos, int64_t n, double cutoff, Pair pr, double* out) {
-    __shared__ double qd[PAIR_WARPS][4][64];        // dx, dy, dz, r of queued hits
+    __shared__ double qd[PAIR_WARPS][5][64];        // dx, dy, dz, r, q_j of queued hits
     __shared__ int qj[PAIR_WARPS][64];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t i = blockIdx.x * (int64_t)PAIR_WARPS + wib;
@@ -135,7 +147,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32) pair_gather_kernel(
     auto eval = [&](int e) {
         const double r = qd[wib][3][e];
         const int j = qj[wib][e];
-        const double f = pr.coef(r, j), sq = pr.scale(j);
+        const double f = pr.coef(r, j), sq = Pair::kUsesQ ? qd[wib][4][e] : 1.0;
         fx += f * qd[wib][0][e] * sq;
         fy += f * qd[wib][1][e] * sq;
         fz += f * qd[wib][2][e] * sq;
@@ -157,16 +169,18 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32) pair_gather_kernel(
                 for (int b = e0; b < e1; b += 32) {
                     const int s = b + lane;
                     bool hit = false;
-                    double d[3], r = 0.0;
+                    double d[3], r = 0.0, qv = 1.0;
                     int j = -1;
                     if (s < e1) {
                         j = g.order[s];
+                        const double4 v = g.spos[s];
+                        qv = v.w;
                         // d = p_i - p_j; d -= L round(d / L) on periodic axes.
                         // round(d * (1/L)) differs from round(d / L) only
                         // for |d| within ulps of L/2 > cutoff: never a pair
-                        d[0] = __dsub_rn(px, pos[3 * j]);
-                        d[1] = __dsub_rn(py, pos[3 * j + 1]);
-                        d[2] = __dsub_rn(pz, pos[3 * j + 2]);
+                        d[0] = __dsub_rn(px, v.x);
+                        d[1] = __dsub_rn(py, v.y);
+                        d[2] = __dsub_rn(pz, v.z);
 #pragma unroll
                         for (int ax = 0; ax < 3; ++ax)
                             if (g.per[ax]) d[ax] = __dsub_rn(d[ax], __dmul_rn(g.L[ax], rint(d[ax] * g.iL[ax])));
@@ -183,6 +197,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32) pair_gather_kernel(
                         const int slot = qn + __popc(bal & ((1u << lane) - 1u));
                         qd[wib][0][slot] = d[0]; qd[wib][1][slot] = d[1];
                         qd[wib][2][slot] = d[2]; qd[wib][3][slot] = r;
+                        if (Pair::kUsesQ) qd[wib][4][slot] = qv;
                         qj[wib][slot] = j;
                     }
                     qn += __popc(bal);
@@ -192,7 +207,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32) pair_gather_kernel(
                         __syncwarp();
                         if (lane < qn - 32) {
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) qd[wib][k][lane] = qd[wib][k][32 + lane];
+                            for (int k = 0; k < 5; ++k) qd[wib][k][lane] = qd[wib][k][32 + lane];
                             qj[wib][lane] = qj[wib][32 + lane];
                         }
                         qn -= 32;
@@ -215,9 +230,9 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32) pair_gather_kernel(
 // Cell grid for the cutoff on the device positions; open-axis ranges come
 // from the host copy.  Scratch persists in a PairScratch.
 template <class Pair>
-void pair_forces_impl(const double* d_pos, const double* h_pos, int64_t n, const double L[3],
-                      double cutoff, const Pair& pr, double* d_out, cudaStream_t st,
-                      PairScratch& sc) {
+void pair_forces_impl(const double* d_pos, const double* d_q, const double* h_pos, int64_t n,
+                      const double L[3], double cutoff, const Pair& pr, double* d_out,
+                      cudaStream_t st, PairScratch& sc) {
     SE_CUDA(cudaMemsetAsync(d_out, 0, 3 * n * sizeof(double), st));
     if (n < 2) return;
     CellGrid g{};
@@ -257,7 +272,9 @@ void pair_forces_impl(const double* d_pos, const double* h_pos, int64_t n, const
     SE_CUDA(cub::DeviceRadixSort::SortPairs(sc.tmp, bytes, k1, k2, p1, p2, (int)n, 0, end_bit, st));
     cell_starts_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(k2, n, (int)ncell, start);
     SE_CUDA(cudaGetLastError());
-    g.start = start; g.order = p2;
+    cell_gather_kernel<<<nb, 256, 0, st>>>(d_pos, d_q, p2, n, sc.spos);
+    SE_CUDA(cudaGetLastError());
+    g.start = start; g.order = p2; g.spos = sc.spos;
     pair_gather_kernel<<<(unsigned)((n + PAIR_WARPS - 1) / PAIR_WARPS), PAIR_WARPS * 32, 0, st>>>(
         g, d_pos, n, cutoff, pr, d_out);
     SE_CUDA(cudaGetLastError());
@@ -273,6 +290,9 @@ void PairScratch::reserve(int64_t n, int64_t ncell) {
         SE_CUDA(cudaMalloc(&k2, n * sizeof(uint32_t)));
         SE_CUDA(cudaMalloc(&p1, n * sizeof(int)));
         SE_CUDA(cudaMalloc(&p2, n * sizeof(int)));
+        cudaFree(spos);
+        spos = nullptr;
+        SE_CUDA(cudaMalloc(&spos, n * sizeof(double4)));
         size_t b = 0;
         SE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, k1, k2, p1, p2, (int)n, 0, 32));
         tbytes = std::max<size_t>(b, 16);
@@ -289,7 +309,8 @@ void PairScratch::reserve(int64_t n, int64_t ncell) {
 
 void PairScratch::release() {
     cudaFree(k1); cudaFree(k2); cudaFree(p1); cudaFree(p2); cudaFree(start); cudaFree(tmp);
-    cudaFree(buf);
+    cudaFree(buf); cudaFree(spos);
+    spos = nullptr;
     if (stream) cudaStreamDestroy(stream);
     k1 = k2 = nullptr; p1 = p2 = start = nullptr; tmp = nullptr; buf = nullptr; stream = nullptr;
     ncap = ccap = bcap = 0;
@@ -320,7 +341,7 @@ void steric_forces(int device, const double* pos, int64_t n, double Lx, double L
     double* d_pos = sc.buf;
     double* d_out = sc.buf + 3 * sc.bcap;
     SE_CUDA(cudaMemcpyAsync(d_pos, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
-    pair_forces_impl(d_pos, pos, n, L, pr.cutoff, pr, d_out, st, sc);
+    pair_forces_impl(d_pos, nullptr, pos, n, L, pr.cutoff, pr, d_out, st, sc);
     SE_CUDA(cudaMemcpyAsync(out, d_out, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, st));
     SE_CUDA(cudaStreamSynchronize(st));
 }
@@ -329,7 +350,7 @@ void tp_near_forces(const double* d_pos, const double* d_q, int64_t n, const dou
                     double r_cut, double g_w, double xi, double eps, double* d_out,
                     cudaStream_t st, PairScratch& sc) {
     TpNearPair pr{2.0 * g_w, std::sqrt(4.0 * (g_w * g_w) + 1.0 / (xi * xi)), FOUR_PI * eps, d_q};
-    pair_forces_impl(d_pos, nullptr, n, L, r_cut, pr, d_out, st, sc);
+    pair_forces_impl(d_pos, d_q, nullptr, n, L, r_cut, pr, d_out, st, sc);
 }
 
 }  // namespace se

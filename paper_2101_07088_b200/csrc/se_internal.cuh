@@ -403,6 +403,7 @@ struct PairScratch {
     size_t tbytes = 0;
     uint32_t *k1 = nullptr, *k2 = nullptr;
     int *p1 = nullptr, *p2 = nullptr, *start = nullptr;
+    double4* spos = nullptr;          // cell-sorted (x, y, z, q)
     void* tmp = nullptr;
     double* buf = nullptr;            // host-API staging: pos[3n] + out[3n]
     cudaStream_t stream = nullptr;    // host-API stream
