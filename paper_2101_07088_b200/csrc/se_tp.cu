@@ -33,6 +33,7 @@ struct TpGrid {
     int n[3]; double h[3];
     int m[3];                         // stencil half widths (gridops.py:20)
     double radius, keep, inv_width, inv_norm;
+    int64_t stride;                   // field plane stride (even: cuFFT alignment)
 };
 
 // per-warp stencil tables: weights and wrapped indices per axis
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(TP_WARPS * 32) tp_interp_kernel(TpGrid g, cons
     tp_stencil(g, p, s, lane);
     __syncwarp();
     const int Sx = 2 * g.m[0] + 1, Sy = 2 * g.m[1] + 1, Sz = 2 * g.m[2] + 1;
-    const int64_t G = (int64_t)g.n[0] * g.n[1] * g.n[2];
+    const int64_t G = g.stride;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     for (int e = lane; e < Sx * Sy * Sz; e += 32) {
         const int oz = e % Sz, c = e / Sz, oy = c % Sy, ox = c / Sy;
@@ -179,7 +180,7 @@ struct TpPlan {
     cudaStream_t stream = nullptr;
     bool own_stream = true;
     int n[3]{}; double L[3]{}, h[3]{}, eps = 1.0;
-    int64_t G = 0, half = 0;
+    int64_t G = 0, Gs = 0, half = 0;   // grid size, plane stride (even), half spectrum
     cufftHandle fwd = 0, inv = 0;
     double* d_grid = nullptr;                  // [4][G]: rho / phi, Ex, Ey, Ez
     cufftDoubleComplex* d_hat = nullptr;       // [5][half]: rho_hat, phi_hat, E_hat x3
@@ -208,9 +209,10 @@ TpPlan* tp_create(int device, const double L[3], const int n[3], double eps) {
         p->eps = eps;
         for (int ax = 0; ax < 3; ++ax) { p->n[ax] = n[ax]; p->L[ax] = L[ax]; p->h[ax] = L[ax] / n[ax]; }
         p->G = (int64_t)n[0] * n[1] * n[2];
+        p->Gs = (p->G + 1) & ~(int64_t)1;   // cuFFT wants 16-byte aligned real planes
         p->half = (int64_t)n[0] * n[1] * (n[2] / 2 + 1);
         SE_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
-        SE_CUDA(cudaMalloc(&p->d_grid, 4 * p->G * sizeof(double)));
+        SE_CUDA(cudaMalloc(&p->d_grid, 4 * p->Gs * sizeof(double)));
         SE_CUDA(cudaMalloc(&p->d_hat, 5 * p->half * sizeof(cufftDoubleComplex)));
         SE_CUFFT(cufftPlan3d(&p->fwd, n[0], n[1], n[2], CUFFT_D2Z));
         SE_CUFFT(cufftPlan3d(&p->inv, n[0], n[1], n[2], CUFFT_Z2D));
@@ -253,7 +255,7 @@ static void tp_solve_grid(TpPlan* p, bool want_phi, bool want_field) {
     if (want_phi) SE_CUFFT(cufftExecZ2D(p->inv, phi_hat, p->d_grid));
     if (want_field)
         for (int c = 0; c < 3; ++c)
-            SE_CUFFT(cufftExecZ2D(p->inv, e_hat + c * p->half, p->d_grid + (1 + c) * p->G));
+            SE_CUFFT(cufftExecZ2D(p->inv, e_hat + c * p->half, p->d_grid + (1 + c) * p->Gs));
 }
 
 void tp_poisson(TpPlan* p, const double* rho, int with_field, double* phi, double* E) {
@@ -262,8 +264,9 @@ void tp_poisson(TpPlan* p, const double* rho, int with_field, double* phi, doubl
     tp_solve_grid(p, true, with_field != 0);
     SE_CUDA(cudaMemcpyAsync(phi, p->d_grid, p->G * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
     if (with_field && E)
-        SE_CUDA(cudaMemcpyAsync(E, p->d_grid + p->G, 3 * p->G * sizeof(double),
-                                cudaMemcpyDeviceToHost, p->stream));
+        for (int c = 0; c < 3; ++c)
+            SE_CUDA(cudaMemcpyAsync(E + c * p->G, p->d_grid + (1 + c) * p->Gs,
+                                    p->G * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
     SE_CUDA(cudaStreamSynchronize(p->stream));
 }
 
@@ -275,6 +278,7 @@ static TpGrid tp_grid(const TpPlan* p, double width, double radius) {
         g.m[ax] = (int)std::floor(radius / p->h[ax] + 1e-12);
         if (2 * g.m[ax] + 1 > TP_MAXS) throw Error(SE_ERR_VALUE, "stencil too wide for the periodic grid");
     }
+    g.stride = p->Gs;
     g.radius = radius;
     g.keep = radius + 1e-12 * radius;
     g.inv_width = 1.0 / width;
@@ -307,7 +311,7 @@ void tp_forces_device(TpPlan* p, const double* d_pos, const double* d_q, int64_t
     }
     tp_solve_grid(p, false, true);
     if (n == 0) return;
-    tp_interp_kernel<<<nb, TP_WARPS * 32, 0, p->stream>>>(g, d_pos, n, p->d_grid + p->G,
+    tp_interp_kernel<<<nb, TP_WARPS * 32, 0, p->stream>>>(g, d_pos, n, p->d_grid + p->Gs,
                                                           p->h[0] * p->h[1] * p->h[2], d_far);
     SE_CUDA(cudaGetLastError());
     tp_near_forces(d_pos, d_q, n, p->L, r_cut, g_w, xi, p->eps, d_near, p->stream, p->pairs);

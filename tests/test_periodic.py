@@ -90,3 +90,26 @@ def test_gpu_g2_bd_loop_matches_reference():
         f = s.forces(state.positions, G["g2_q"]) + B.steric_pair_forces(state.positions, st, boxes)
         B.bd_step(state, f, cfg, wrap=boxes)
         assert np.max(np.abs(state.positions - G["g2_traj"][k])) < 1e-9
+
+
+@pytest.mark.gpu
+def test_gpu_tp_edges():
+    """Empty and single-charge systems, positions outside the primary box
+    (wrapped by the stencils and the minimum image), odd grid sizes."""
+    from paper_2101_07088_b200.periodic import TriplyPeriodicSolver
+    box, boxes, eps = _g2()
+    s = TriplyPeriodicSolver(boxes, 32, 0.25, eps, delta=5e-4)
+    assert s.forces(np.zeros((0, 3)), np.zeros(0)).shape == (0, 3)
+    one = s.forces(G["g2_pos"][:1], np.array([1.0]))
+    assert one.shape == (1, 3) and np.all(np.isfinite(one))
+    assert np.max(np.abs(one)) < 1e-8          # a lone charge feels no net force
+    pos = G["g2_pos"].copy()
+    shifted = pos + np.array([box, -box, 2 * box])
+    f0 = s.forces(pos, G["g2_q"])
+    f1 = s.forces(shifted, G["g2_q"])
+    assert rel_l2(f1, f0) < 1e-10
+    o = T.TpSolver(boxes, 31, 0.25, eps)
+    g = TriplyPeriodicSolver(boxes, 31, 0.25, eps, delta=5e-4)
+    assert g.n == o.n
+    sub = slice(0, 120)
+    assert rel_l2(g.forces(pos[sub], G["g2_q"][sub]), o.forces(pos[sub], G["g2_q"][sub])) < 1e-10
