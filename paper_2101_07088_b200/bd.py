@@ -85,6 +85,52 @@ class BdState:
     steps_done: int = 0
 
 
+@dataclass
+class Observables:
+    """Density (and pair-correlation) histograms with the reference's
+    normalisation (bd.py:139-181); host numpy, sampled rarely."""
+
+    H: float
+    area: float
+    z_bin: float
+    r_max: float = 0.0
+    r_bin: float = 0.0
+    samples: int = 0
+    z_counts: np.ndarray = None
+    pair_counts: np.ndarray = None
+    _pair_norm: float = 0.0
+
+    def __post_init__(self):
+        self.z_edges = np.arange(0.0, self.H + self.z_bin, self.z_bin)
+        self.z_counts = np.zeros(self.z_edges.size - 1)
+        if self.r_max > 0:
+            self.r_edges = np.arange(0.0, self.r_max + self.r_bin, self.r_bin)
+            self.pair_counts = np.zeros(self.r_edges.size - 1)
+
+    def record_density(self, z):
+        self.z_counts += np.histogram(z, bins=self.z_edges)[0]
+        self.samples += 1
+
+    def record_pairs(self, distances, n_pairs_ideal_per_volume):
+        self.pair_counts += np.histogram(distances, bins=self.r_edges)[0]
+        self._pair_norm += n_pairs_ideal_per_volume
+
+    def density(self):
+        """(z centers, n(z)) normalised so the profile integrates to N/area."""
+        centers = 0.5 * (self.z_edges[1:] + self.z_edges[:-1])
+        vol = self.area * self.z_bin * max(self.samples, 1)
+        return centers, self.z_counts / vol
+
+    def pair_correlation(self):
+        """(r centers, g2) with ideal-gas shell normalisation."""
+        centers = 0.5 * (self.r_edges[1:] + self.r_edges[:-1])
+        shells = (4.0 / 3.0) * np.pi * (self.r_edges[1:] ** 3 - self.r_edges[:-1] ** 3)
+        ideal = shells * self._pair_norm
+        with np.errstate(invalid="ignore", divide="ignore"):
+            g2 = np.where(ideal > 0, self.pair_counts / ideal, 0.0)
+        return centers, g2
+
+
 def make_state(positions, config):
     """Initial state: Philox stream of the seed, first noise drawn."""
     rng = np.random.Generator(np.random.Philox(config.seed))
@@ -182,6 +228,6 @@ def __getattr__(name):
     raise AttributeError(name)
 
 
-__all__ = ["StericParams", "BdConfig", "BdState", "lj_force", "steric_force",
+__all__ = ["StericParams", "BdConfig", "BdState", "Observables", "lj_force", "steric_force",
            "steric_energy", "make_state", "bd_step", "steric_pair_forces",
            "wall_steric_forces", "bd_run", "TriplyPeriodicSolver"]
