@@ -155,6 +155,32 @@ int se_dist_fields(se_plan* plan);
 int se_steric_forces(int device, const double* pos, int64_t n, double Lx, double Ly,
                      double Lz, double a, double U0, double r_m, int p, double* out);
 
+/* Device-resident Brownian dynamics (SURVEY 8f next #1 at scale).
+ *   se_steric_forces_device: se_steric_forces on device buffers on a
+ *     caller's stream; open z (Lz <= 0) uses the cell range [zlo, zhi].
+ *   se_bd_first_noise_device: the initial noise W_0 (Philox, subsequence i).
+ *   se_bd_step_device: bd_step (bd.py:101-133) on device buffers: forces
+ *     q E + f_ext (+ the mirror-wall steric force when wall != 0,
+ *     bd.py:273-279), W_{n+1} from Philox4x32-10 (seed, subsequence i,
+ *     offset 8 per draw; *draws counts the draws), max_disp cap, z-bound
+ *     rejection with a full redraw (*rejections incremented), x/y wrap with
+ *     numpy's mod when Lx / Ly > 0.  pos, prev [n][3] updated in place; E
+ *     [n][3] (or NULL), q [n] (or NULL), f_ext [n][3] (or NULL).  The noise
+ *     stream is NOT numpy's: the host path (bd.py) reproduces the
+ *     reference draw for draw, this one is for device-resident runs. */
+typedef struct {
+    double dt, mu, kT, max_disp, z_lo, z_hi, Lx, Ly, H, a, U0, r_m;
+    int32_t p, wall, has_zb, max_retries;
+    uint64_t seed;
+} se_bd_params;
+int se_steric_forces_device(int device, void* stream, const double* d_pos, int64_t n, double Lx,
+                            double Ly, double Lz, double zlo, double zhi, double a, double U0,
+                            double r_m, int p, double* d_out);
+int se_bd_first_noise_device(int device, void* stream, int64_t n, uint64_t seed, double* d_prev);
+int se_bd_step_device(int device, void* stream, double* d_pos, double* d_prev, const double* d_E,
+                      const double* d_q, const double* d_fext, int64_t n,
+                      const se_bd_params* params, uint64_t* draws, int64_t* rejections);
+
 /* Triply periodic twin.  A plan holds the uniform
  * periodic grid nx x ny x nz of the box Lx x Ly x Lz and the permittivity.
  *   se_tp_poisson: solve_triply_periodic (dpsolver.py:221-249); rho, phi

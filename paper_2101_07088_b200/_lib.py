@@ -35,7 +35,16 @@ EXPORTS = ("se_plan_create", "se_plan_destroy", "se_plan_set_stream",
            "se_dist_setup", "se_dist_buffers", "se_dist_forward",
            "se_dist_modes", "se_dist_fields", "se_steric_forces",
            "se_tp_create", "se_tp_destroy", "se_tp_set_stream", "se_tp_poisson",
-           "se_tp_forces", "se_tp_forces_device")
+           "se_tp_forces", "se_tp_forces_device", "se_steric_forces_device",
+           "se_bd_first_noise_device", "se_bd_step_device")
+
+
+class SeBdParams(ctypes.Structure):
+    """se_bd_params (include/slabewald.h)."""
+    _fields_ = [(n, ctypes.c_double) for n in (
+        "dt", "mu", "kT", "max_disp", "z_lo", "z_hi", "Lx", "Ly", "H", "a", "U0", "r_m")] + \
+        [(n, ctypes.c_int32) for n in ("p", "wall", "has_zb", "max_retries")] + \
+        [("seed", ctypes.c_uint64)]
 
 
 class SeParams(ctypes.Structure):
@@ -130,8 +139,19 @@ def load():
     lib.se_tp_forces.argtypes = [ctypes.c_void_p, _D, _D, _I64, _f, _f, _f, _f, _f, _D]
     lib.se_tp_forces_device.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                         _I64, _f, _f, _f, _f, _f, ctypes.c_void_p]
+    _v = ctypes.c_void_p
+    lib.se_steric_forces_device.argtypes = [ctypes.c_int, _v, _v, _I64, _f, _f, _f, _f, _f, _f,
+                                            _f, _f, ctypes.c_int, _v]
+    lib.se_bd_first_noise_device.argtypes = [ctypes.c_int, _v, _I64, ctypes.c_uint64, _v]
+    lib.se_bd_step_device.argtypes = [ctypes.c_int, _v, _v, _v, _v, _v, _v, _I64,
+                                      ctypes.POINTER(SeBdParams),
+                                      ctypes.POINTER(ctypes.c_uint64),
+                                      ctypes.POINTER(ctypes.c_int64)]
+    for name in ("se_steric_forces_device", "se_bd_first_noise_device", "se_bd_step_device"):
+        getattr(lib, name).restype = ctypes.c_int
     for name in ("se_tp_create", "se_tp_destroy", "se_tp_set_stream", "se_tp_poisson",
-                 "se_tp_forces", "se_tp_forces_device"):
+                 "se_tp_forces", "se_tp_forces_device", "se_steric_forces_device",
+           "se_bd_first_noise_device", "se_bd_step_device"):
         getattr(lib, name).restype = ctypes.c_int
     lib.se_fp64_peak.argtypes = [ctypes.c_int, _D]
     lib.se_fp64_peak.restype = ctypes.c_int

@@ -220,6 +220,74 @@ def bd_run(solver, steric, config, steps=None, state=None):
     return state
 
 
+class DeviceBd:
+    """Device-resident BD run of the slab (the cmd_bd loop, cli.py:203-215,
+    at scale): positions, noise and forces stay in HBM; per step one
+    ``solve_device`` (need_energy=False), the steric pair forces
+    (``se_steric_forces_device``) and one ``se_bd_step_device`` (forces
+    q E + steric + mirror walls, Philox noise, max_disp cap, z-bound
+    rejection with margin n_sigma g_w, xy wrap).  Same dynamics as
+    :func:`bd_run`, but the noise is Philox4x32-10 on the device, not numpy's
+    stream, so trajectories agree with the reference statistically, not
+    draw for draw."""
+
+    def __init__(self, solver, steric, config, positions=None):
+        import torch
+        self._torch = torch
+        self.solver, self.steric, self.config = solver, steric, config
+        system, params = solver.system, solver.params
+        geo = system.geometry
+        self.geo = geo
+        self.dev = torch.device("cuda", solver.device)
+        self.stream = torch.cuda.current_stream(self.dev)
+        solver.set_stream(self.stream.cuda_stream)
+        self.n = n = int(system.charges.size)
+        pos = system.positions if positions is None else positions
+        f64 = torch.float64
+        self.pos = torch.as_tensor(np.ascontiguousarray(pos, dtype=np.float64)).to(self.dev).contiguous()
+        self.q = torch.as_tensor(np.ascontiguousarray(system.charges, dtype=np.float64)).to(self.dev)
+        self.prev = torch.empty((n, 3), dtype=f64, device=self.dev)
+        self.E = torch.empty((n, 3), dtype=f64, device=self.dev)
+        self.phi = torch.empty(n, dtype=f64, device=self.dev)
+        self.fst = torch.empty((n, 3), dtype=f64, device=self.dev)
+        self.draws = ctypes.c_uint64(0)
+        self.rejections = ctypes.c_int64(0)
+        margin = params.n_sigma * system.g_w
+        self.k = _lib.SeBdParams(
+            dt=config.dt, mu=config.mu, kT=config.kT,
+            max_disp=config.max_disp if np.isfinite(config.max_disp) else 1e300,
+            z_lo=margin, z_hi=geo.H - margin, Lx=geo.Lx, Ly=geo.Ly, H=geo.H,
+            a=steric.a, U0=steric.U0, r_m=steric.r_m, p=steric.p, wall=1, has_zb=1,
+            max_retries=config.max_retries, seed=config.seed)
+        self._lib = _lib.load()
+        _lib.check(self._lib.se_bd_first_noise_device(
+            self.dev.index, ctypes.c_void_p(self.stream.cuda_stream), n, config.seed,
+            ctypes.c_void_p(self.prev.data_ptr())))
+        self.steps_done = 0
+
+    def step(self, steps=1):
+        lib, st = self._lib, ctypes.c_void_p(self.stream.cuda_stream)
+        s, g = self.steric, self.geo
+        for _ in range(steps):
+            self.solver.solve_device(self.pos.data_ptr(), self.phi.data_ptr(),
+                                     self.E.data_ptr(), self.n, need_energy=False)
+            _lib.check(lib.se_steric_forces_device(
+                self.dev.index, st, ctypes.c_void_p(self.pos.data_ptr()), self.n, g.Lx, g.Ly,
+                0.0, 0.0, g.H, s.a, s.U0, s.r_m, s.p, ctypes.c_void_p(self.fst.data_ptr())))
+            _lib.check(lib.se_bd_step_device(
+                self.dev.index, st, ctypes.c_void_p(self.pos.data_ptr()),
+                ctypes.c_void_p(self.prev.data_ptr()), ctypes.c_void_p(self.E.data_ptr()),
+                ctypes.c_void_p(self.q.data_ptr()), ctypes.c_void_p(self.fst.data_ptr()),
+                self.n, ctypes.byref(self.k), ctypes.byref(self.draws),
+                ctypes.byref(self.rejections)))
+            self.steps_done += 1
+        return self
+
+    def positions(self):
+        self._torch.cuda.synchronize(self.dev)
+        return self.pos.cpu().numpy()
+
+
 def __getattr__(name):
     # bd.py:297 hosts the triply periodic solver in the reference
     if name == "TriplyPeriodicSolver":
@@ -228,6 +296,6 @@ def __getattr__(name):
     raise AttributeError(name)
 
 
-__all__ = ["StericParams", "BdConfig", "BdState", "Observables", "lj_force", "steric_force",
+__all__ = ["StericParams", "BdConfig", "BdState", "Observables", "DeviceBd", "lj_force", "steric_force",
            "steric_energy", "make_state", "bd_step", "steric_pair_forces",
            "wall_steric_forces", "bd_run", "TriplyPeriodicSolver"]

@@ -881,6 +881,39 @@ int se_steric_forces(int device, const double* pos, int64_t n, double Lx, double
     }
 }
 
+int se_steric_forces_device(int device, void* stream, const double* d_pos, int64_t n, double Lx,
+                            double Ly, double Lz, double zlo, double zhi, double a, double U0,
+                            double r_m, int p, double* d_out) {
+    try {
+        steric_forces_device(device, static_cast<cudaStream_t>(stream), d_pos, n, Lx, Ly, Lz, zlo,
+                             zhi, a, U0, r_m, p, d_out);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_bd_first_noise_device(int device, void* stream, int64_t n, uint64_t seed, double* d_prev) {
+    try {
+        bd_first_noise_device(device, static_cast<cudaStream_t>(stream), n, seed, d_prev);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_bd_step_device(int device, void* stream, double* d_pos, double* d_prev, const double* d_E,
+                      const double* d_q, const double* d_fext, int64_t n,
+                      const se_bd_params* params, uint64_t* draws, int64_t* rejections) {
+    try {
+        bd_step_device(device, static_cast<cudaStream_t>(stream), d_pos, d_prev, d_E, d_q, d_fext,
+                       n, *params, draws, rejections);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
 int se_tp_create(int device, double Lx, double Ly, double Lz, int nx, int ny, int nz,
                  double eps, se_tp** plan) {
     try {

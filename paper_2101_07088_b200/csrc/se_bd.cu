@@ -16,6 +16,7 @@
 // fewer than 3) with in-warp compaction of the hits, exact reference
 // arithmetic for d, r and the pair term.
 #include <cub/cub.cuh>
+#include <curand_kernel.h>
 
 #include <algorithm>
 #include <cmath>
@@ -83,12 +84,14 @@ __global__ void cell_starts_kernel(const uint32_t* keys, int64_t n, int ncell, i
 // pair vector term f(r) / r * d  (bd.py:265-266)
 struct StericPair {
     double a, U0, r_m, cutoff; int p;
-    __device__ __forceinline__ double coef(double r, int) const {
+    __device__ __forceinline__ double force(double r) const {
         if (r > cutoff) return 0.0;
         const double rs = r_m > 0 ? fmax(r, r_m) : fmax(r, 1e-12 * a);
         const double x = pow(2.0 * a / rs, (double)p);
-        const double f = 4.0 * U0 * p * x * (2.0 * x - 1.0) / rs;
-        return f / (r > 0 ? r : 1.0);
+        return 4.0 * U0 * p * x * (2.0 * x - 1.0) / rs;
+    }
+    __device__ __forceinline__ double coef(double r, int) const {
+        return force(r) / (r > 0 ? r : 1.0);
     }
     static constexpr bool kUsesQ = false;
 };
@@ -232,34 +235,48 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32) pair_gather_kernel(
 template <class Pair>
 void pair_forces_impl(const double* d_pos, const double* d_q, const double* h_pos, int64_t n,
                       const double L[3], double cutoff, const Pair& pr, double* d_out,
-                      cudaStream_t st, PairScratch& sc) {
+                      cudaStream_t st, PairScratch& sc, const double* zr = nullptr) {
     SE_CUDA(cudaMemsetAsync(d_out, 0, 3 * n * sizeof(double), st));
     if (n < 2) return;
     CellGrid g{};
     g.cut2_hi = cutoff * cutoff * (1.0 + 1e-9);
-    int64_t ncell = 1;
+    double span[3];
     for (int ax = 0; ax < 3; ++ax) {
         g.per[ax] = L[ax] > 0;
         if (g.per[ax]) {
             g.L[ax] = L[ax];
             g.iL[ax] = 1.0 / L[ax];
-            g.nc[ax] = std::max(1, (int)std::floor(L[ax] / cutoff));
-            g.cs[ax] = L[ax] / g.nc[ax];
             g.lo[ax] = 0.0;
+            span[ax] = L[ax];
         } else {
+            // open axis: the data's range from the host copy, or the caller's
+            // (points outside are clamped into the edge cells, which keeps
+            // every pair within the cutoff in the same or adjacent cells)
             double mn = 1e300, mx = -1e300;
-            for (int64_t i = 0; i < n; ++i) {
-                mn = std::min(mn, h_pos[3 * i + ax]);
-                mx = std::max(mx, h_pos[3 * i + ax]);
+            if (h_pos) {
+                for (int64_t i = 0; i < n; ++i) {
+                    mn = std::min(mn, h_pos[3 * i + ax]);
+                    mx = std::max(mx, h_pos[3 * i + ax]);
+                }
+            } else {
+                if (!zr) throw Error(SE_ERR_VALUE, "open axis without a coordinate range");
+                mn = zr[0]; mx = zr[1];
             }
             g.lo[ax] = mn - cutoff;
-            const double span = (mx + cutoff) - g.lo[ax];
-            g.nc[ax] = std::max(1, (int)std::floor(span / cutoff));
-            g.cs[ax] = span / g.nc[ax];
+            span[ax] = (mx + cutoff) - g.lo[ax];
         }
-        ncell *= g.nc[ax];
-        if (ncell > (1 << 28)) throw Error(SE_ERR_VALUE, "pair cell grid too large");
+        g.nc[ax] = (int)std::max(1.0, std::min(1048576.0, std::floor(span[ax] / cutoff)));
     }
+    // a cutoff tiny against the box: coarser cells (still >= the cutoff) so
+    // the cell table stays O(n)
+    const int64_t cmax = std::max<int64_t>(1 << 20, 4 * n);
+    while ((int64_t)g.nc[0] * g.nc[1] * g.nc[2] > cmax) {
+        int ax = 0;
+        for (int b = 1; b < 3; ++b) if (g.nc[b] > g.nc[ax]) ax = b;
+        g.nc[ax] = std::max(1, g.nc[ax] / 2);
+    }
+    for (int ax = 0; ax < 3; ++ax) g.cs[ax] = span[ax] / g.nc[ax];
+    const int64_t ncell = (int64_t)g.nc[0] * g.nc[1] * g.nc[2];
     sc.reserve(n, ncell);
     uint32_t *k1 = sc.k1, *k2 = sc.k2;
     int *p1 = sc.p1, *p2 = sc.p2, *start = sc.start;
@@ -344,6 +361,162 @@ void steric_forces(int device, const double* pos, int64_t n, double Lx, double L
     pair_forces_impl(d_pos, nullptr, pos, n, L, pr.cutoff, pr, d_out, st, sc);
     SE_CUDA(cudaMemcpyAsync(out, d_out, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, st));
     SE_CUDA(cudaStreamSynchronize(st));
+}
+
+static std::map<int, PairScratch> g_steric_dev;
+
+void steric_forces_device(int device, cudaStream_t st, const double* d_pos, int64_t n, double Lx,
+                          double Ly, double Lz, double zlo, double zhi, double a, double U0,
+                          double r_m, int p, double* d_out) {
+    if (!(a > 0) || p < 1) throw Error(SE_ERR_VALUE, "steric parameters: a > 0, p >= 1");
+    std::lock_guard<std::mutex> lock(g_steric_mu);
+    SE_CUDA(cudaSetDevice(device));
+    PairScratch& sc = g_steric_dev[device];
+    StericPair pr{a, U0, r_m, std::pow(2.0, 1.0 / p) * 2.0 * a, p};
+    const double L[3] = {Lx, Ly, Lz};
+    const double zr[2] = {zlo, zhi};
+    pair_forces_impl(d_pos, nullptr, nullptr, n, L, pr.cutoff, pr, d_out, st, sc, zr);
+}
+
+namespace {
+
+// numpy's float remainder (npy_divmod): fmod moved into [0, L)
+__device__ __forceinline__ double bd_np_mod(double x, double L) {
+    double m = fmod(x, L);
+    if (m != 0.0) { if (m < 0.0) m = __dadd_rn(m, L); }
+    else m = 0.0;
+    return m;
+}
+
+struct BdStepArgs {
+    const double* pos; const double* prev; const double* E; const double* q; const double* fext;
+    int64_t n;
+    se_bd_params k;
+    double drift_scale, amp;
+    StericPair wall;
+    double* trial; double* fresh; int* outside;
+};
+
+// One trial step (bd.py:101-133): F = q E + f_ext + wall, W_{n+1} from
+// Philox (subsequence i, 8 draws per trial), displacement capped at max_disp,
+// z bounds checked
+__global__ void bd_trial_kernel(BdStepArgs a, unsigned long long draw) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    double f[3];
+    const double qi = a.q ? a.q[i] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        f[c] = a.E ? qi * a.E[3 * i + c] : 0.0;
+        if (a.fext) f[c] = f[c] + a.fext[3 * i + c];
+    }
+    const double z = a.pos[3 * i + 2];
+    if (a.k.wall) {                                   // bd.py:273-279
+        f[2] = f[2] + (a.wall.force(2.0 * z) - a.wall.force(2.0 * (a.k.H - z)));
+    }
+    double w[3] = {0.0, 0.0, 0.0};
+    if (a.k.kT > 0) {
+        curandStatePhilox4_32_10_t rs;
+        curand_init(a.k.seed, (unsigned long long)i, draw * 8ull, &rs);
+        const double2 u0 = curand_normal2_double(&rs), u1 = curand_normal2_double(&rs);
+        w[0] = u0.x; w[1] = u0.y; w[2] = u1.x;
+    }
+    double st[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) st[c] = a.drift_scale * f[c] + a.amp * (a.prev[3 * i + c] + w[c]);
+    const double len = sqrt((st[0] * st[0] + st[1] * st[1]) + st[2] * st[2]);
+    if (len > a.k.max_disp) {
+        const double sc = a.k.max_disp / len;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) st[c] = st[c] * sc;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        a.trial[3 * i + c] = a.pos[3 * i + c] + st[c];
+        a.fresh[3 * i + c] = w[c];
+    }
+    const double tz = a.trial[3 * i + 2];
+    if (a.k.has_zb && !(tz > a.k.z_lo && tz < a.k.z_hi)) atomicOr(a.outside, 1);
+}
+
+__global__ void bd_commit_kernel(BdStepArgs a, double* pos, double* prev) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    double t[3] = {a.trial[3 * i], a.trial[3 * i + 1], a.trial[3 * i + 2]};
+    if (a.k.Lx > 0) t[0] = bd_np_mod(t[0], a.k.Lx);
+    if (a.k.Ly > 0) t[1] = bd_np_mod(t[1], a.k.Ly);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        pos[3 * i + c] = t[c];
+        prev[3 * i + c] = a.fresh[3 * i + c];
+    }
+}
+
+__global__ void bd_first_noise_kernel(int64_t n, unsigned long long seed, double* prev) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    curandStatePhilox4_32_10_t rs;
+    curand_init(seed, (unsigned long long)i, 0ull, &rs);
+    const double2 u0 = curand_normal2_double(&rs), u1 = curand_normal2_double(&rs);
+    prev[3 * i] = u0.x; prev[3 * i + 1] = u0.y; prev[3 * i + 2] = u1.x;
+}
+
+}  // namespace
+
+struct BdScratch {
+    int64_t cap = 0;
+    double* buf = nullptr;      // trial[3n] fresh[3n]
+    int* flag = nullptr;
+    int* h_flag = nullptr;      // pinned
+};
+static std::map<int, BdScratch> g_bd;
+
+void bd_first_noise_device(int device, cudaStream_t st, int64_t n, uint64_t seed, double* d_prev) {
+    SE_CUDA(cudaSetDevice(device));
+    if (n > 0) {
+        bd_first_noise_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, seed, d_prev);
+        SE_CUDA(cudaGetLastError());
+    }
+}
+
+void bd_step_device(int device, cudaStream_t st, double* d_pos, double* d_prev, const double* d_E,
+                    const double* d_q, const double* d_fext, int64_t n, const se_bd_params& k,
+                    uint64_t* draws, int64_t* rejections) {
+    std::lock_guard<std::mutex> lock(g_steric_mu);
+    SE_CUDA(cudaSetDevice(device));
+    if (n == 0) return;
+    BdScratch& sc = g_bd[device];
+    if (n > sc.cap) {
+        cudaFree(sc.buf);
+        sc.buf = nullptr; sc.cap = 0;
+        SE_CUDA(cudaMalloc(&sc.buf, 6 * n * sizeof(double)));
+        sc.cap = n;
+        if (!sc.flag) SE_CUDA(cudaMalloc(&sc.flag, sizeof(int)));
+        if (!sc.h_flag) SE_CUDA(cudaMallocHost(&sc.h_flag, sizeof(int)));
+    }
+    BdStepArgs a{};
+    a.pos = d_pos; a.prev = d_prev; a.E = d_E; a.q = d_q; a.fext = d_fext; a.n = n; a.k = k;
+    a.drift_scale = k.mu * k.dt;
+    a.amp = std::sqrt(0.5 * k.kT * k.mu * k.dt);
+    a.wall = StericPair{k.a, k.U0, k.r_m, k.p >= 1 ? std::pow(2.0, 1.0 / k.p) * 2.0 * k.a : 0.0,
+                        k.p};
+    a.trial = sc.buf; a.fresh = sc.buf + 3 * sc.cap; a.outside = sc.flag;
+    const unsigned nb = (unsigned)((n + 255) / 256);
+    for (int attempt = 0; attempt <= k.max_retries; ++attempt) {
+        SE_CUDA(cudaMemsetAsync(sc.flag, 0, sizeof(int), st));
+        bd_trial_kernel<<<nb, 256, 0, st>>>(a, (unsigned long long)(++*draws));
+        SE_CUDA(cudaGetLastError());
+        SE_CUDA(cudaMemcpyAsync(sc.h_flag, sc.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+        SE_CUDA(cudaStreamSynchronize(st));
+        if (!*sc.h_flag) {
+            bd_commit_kernel<<<nb, 256, 0, st>>>(a, d_pos, d_prev);
+            SE_CUDA(cudaGetLastError());
+            return;
+        }
+        ++*rejections;
+    }
+    throw Error(SE_ERR_CUDA, "unrecoverable configuration: " + std::to_string(k.max_retries) +
+                                 " retries exhausted");
 }
 
 void tp_near_forces(const double* d_pos, const double* d_q, int64_t n, const double L[3],

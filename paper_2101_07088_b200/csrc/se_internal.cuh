@@ -413,6 +413,13 @@ struct PairScratch {
 };
 void steric_forces(int device, const double* pos, int64_t n, double Lx, double Ly, double Lz,
                    double a, double U0, double r_m, int p, double* out);
+void steric_forces_device(int device, cudaStream_t st, const double* d_pos, int64_t n, double Lx,
+                          double Ly, double Lz, double zlo, double zhi, double a, double U0,
+                          double r_m, int p, double* d_out);
+void bd_first_noise_device(int device, cudaStream_t st, int64_t n, uint64_t seed, double* d_prev);
+void bd_step_device(int device, cudaStream_t st, double* d_pos, double* d_prev, const double* d_E,
+                    const double* d_q, const double* d_fext, int64_t n, const se_bd_params& k,
+                    uint64_t* draws, int64_t* rejections);
 void tp_near_forces(const double* d_pos, const double* d_q, int64_t n, const double L[3],
                     double r_cut, double g_w, double xi, double eps, double* d_out,
                     cudaStream_t st, PairScratch& sc);

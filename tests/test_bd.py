@@ -81,3 +81,45 @@ def test_gpu_bd_loop_matches_reference():
         B.bd_run(solver, st, cfg, steps=1, state=state)
         assert np.max(np.abs(state.positions - g["traj"][k])) < 1e-12
     assert state.rejections == int(g["rejections"])
+
+
+@pytest.mark.gpu
+def test_gpu_device_bd_deterministic_matches_host_loop():
+    """kT = 0: the device-resident loop is the deterministic drift of the
+    host loop (same forces, cap, walls, wrap) step for step."""
+    from paper_2101_07088_b200 import workloads as W
+    from paper_2101_07088_b200.slab import SlabSolver
+    system, params = W.build("c2", N=256)
+    st = B.StericParams(a=0.01)
+    cfg = B.BdConfig(dt=1e-6, steps=3, seed=3, max_disp=st.a, kT=0.0)
+    host = B.bd_run(SlabSolver(system, params), st, cfg, steps=3)
+    dev = B.DeviceBd(SlabSolver(system, params), st, cfg).step(3)
+    assert np.max(np.abs(dev.positions() - host.positions)) < 1e-12
+
+
+@pytest.mark.gpu
+def test_gpu_device_bd_noise_statistics():
+    """Free diffusion (no charges' forces: q = 0 would be rejected by the
+    solver, so a dilute system with a huge dt-scale noise): the step is
+    N(0, kT mu dt) per component in the bulk; no particle leaves (0, H)."""
+    from paper_2101_07088_b200 import workloads as W
+    from paper_2101_07088_b200.slab import SlabSolver
+    system, params = W.build("c3")
+    st = B.StericParams(a=1e-4)
+    dt = 1e-7
+    cfg = B.BdConfig(dt=dt, steps=1, seed=11, max_disp=1.0, kT=1.0)
+    # keep the start > 30 noise widths inside the z bounds (a random start on
+    # the bound is rejected forever, as in the reference)
+    zb = params.n_sigma * system.g_w
+    H = system.geometry.H
+    start = system.positions.copy()
+    start[:, 2] = (zb + 0.01) + (start[:, 2] - zb) * (H - 2 * zb - 0.02) / (H - 2 * zb)
+    bd = B.DeviceBd(SlabSolver(system, params), st, cfg, positions=start)
+    p0 = bd.positions()
+    p1 = bd.step(1).positions()
+    d = p1 - p0
+    d[:, :2] -= system.geometry.Lx * np.round(d[:, :2] / system.geometry.Lx)
+    var = d.var(axis=0) / (cfg.kT * cfg.mu * dt)
+    assert np.all(np.abs(var - 1.0) < 0.05), var      # 32768 samples per axis
+    assert np.all(np.abs(d.mean(axis=0)) < 0.05 * np.sqrt(dt))
+    assert np.all((p1[:, 2] > zb) & (p1[:, 2] < H - zb))

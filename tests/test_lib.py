@@ -38,6 +38,7 @@ def test_struct_layouts_match_header():
     # 2 int64, 16 doubles
     assert ctypes.sizeof(_lib.SeParams) == 16 * 8 + 4 * 4
     assert ctypes.sizeof(_lib.SeDiag) == 12 * 8 + 2 * 4 + 2 * 8 + 16 * 8
+    assert ctypes.sizeof(_lib.SeBdParams) == 12 * 8 + 4 * 4 + 8
 
 
 def test_solver_fails_loudly_without_library(monkeypatch, tmp_path):
