@@ -463,3 +463,32 @@ def test_distributed_grid_pipeline_one_gpu(case, world):
     assert abs(U - g["U"]) <= TOL * max(1.0, abs(g["U"]))
     for e in eng:
         e.close()
+
+
+@pytest.mark.gpu
+def test_freespace_slab_agreement():
+    """The reference's `validate --suite freespace` (validate.py:110-132,
+    PAPER Table 2): L = 28 and 32 solves extrapolated to L = infinity against
+    the 400-image open-slab field; the GPU fields match the reference's
+    solver to 1e-10 and the extrapolated error is its 9.755e-6 (<= 5e-5)."""
+    import warnings
+    from paper_2101_07088_b200 import ChargeSystem, SlabGeometry, plan_grid
+    from paper_2101_07088_b200.slab import SlabSolver
+    G = np.load(os.path.join(os.path.dirname(__file__), "golden", "freespace.npz"))
+    fields = {}
+    for L in (28.0, 32.0):
+        geo = SlabGeometry(L, L, 2.0, eps=1.0, eps_b=0.5, eps_t=0.2)
+        pos = G["charges"].copy()
+        pos[:, :2] += 0.5 * L
+        system = ChargeSystem(geo, pos, G["q"], 1e-2)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            params = plan_grid(geo, 1e-2, 1e-4, xi=3.0177, h_min=0.01, strict=False)
+        fields[L] = SlabSolver(system, params).solve().E_bar
+        ref = G["E_L%d" % int(L)]
+        assert np.linalg.norm(fields[L] - ref) <= 1e-10 * np.linalg.norm(ref)
+    e_inf = (32.0 * fields[32.0] - 28.0 * fields[28.0]) / 4.0   # reference.py:78-80
+    e_f = G["e_f"]
+    err = np.max(np.abs(e_inf - e_f)) / np.mean(np.linalg.norm(e_f, axis=1))
+    assert err <= 5e-5
+    assert abs(err - float(G["err"])) <= 1e-3 * float(G["err"])
