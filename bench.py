@@ -384,6 +384,29 @@ def run_ours(args):
             "gpu_launches": launches,
             "kernel_ms": stage, "near_pairs": pairs,
             "roofline": roof, "clocks": clk}
+    if world == 1 and not sharded:
+        # the optional fp32 mode (SE_FP32: far pair kernels in single
+        # precision, same pair set) on the same workload and timing rules
+        s32 = SlabSolver(system, params, device=local, precision="fp32")
+        s32.set_stream(stream.cuda_stream)
+        for _ in range(args.warmup):
+            s32.solve_device(pos_d.data_ptr(), phi_d.data_ptr(), E_d.data_ptr(), n)
+        t32 = []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            s32.solve_device(pos_d.data_ptr(), phi_d.data_ptr(), E_d.data_ptr(), n)
+            e1.record(stream)
+            e1.synchronize()
+            t32.append(e0.elapsed_time(e1))
+        s32.close()
+        ms32 = float(np.mean(t32))
+        line["fp32_mode"] = {"ms_per_step": ms32, "value": n / (ms32 * 1e-3),
+                             "unit": "charges/s",
+                             "scope": "near-field pair kernels in fp32; grids, FFTs, "
+                                      "BVPs, spread and interpolation in fp64"}
     if world == 1 and not args.no_paper_config:
         # the paper's published timings (DP 4.3 ms, TP 0.84 ms,
         # BD step ~5 ms, RTX 2080Ti fp32) on their configuration, N = 2e4
