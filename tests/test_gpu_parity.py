@@ -492,3 +492,22 @@ def test_freespace_slab_agreement():
     err = np.max(np.abs(e_inf - e_f)) / np.mean(np.linalg.norm(e_f, axis=1))
     assert err <= 5e-5
     assert abs(err - float(G["err"])) <= 1e-3 * float(G["err"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_both_near_field_paths_against_goldens(fused):
+    """The near field has two kernels chosen by size (fused one-warp-per-
+    point below 40000 points, scan -> lists -> eval above): force each on
+    the golden workloads and the exact pair count (SE_NEAR_FUSED is read
+    once per process, hence the subprocess)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, SE_NEAR_FUSED=fused)
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x",
+                        os.path.join(here, "test_gpu_parity.py"), "-k",
+                        "workloads_against_golden or pair_count or near_field_sum "
+                        "or variants_against_golden"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
