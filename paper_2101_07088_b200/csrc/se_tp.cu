@@ -28,6 +28,7 @@ namespace {
 
 constexpr int TP_MAXS = 64;           // stencil nodes per axis
 constexpr int TP_WARPS = 4;
+constexpr int TP_K = 8;               // (oy, oz) pairs per lane (Sy Sz <= 256)
 
 struct TpGrid {
     int n[3]; double h[3];
@@ -73,7 +74,32 @@ __global__ void __launch_bounds__(TP_WARPS * 32) tp_spread_kernel(TpGrid g, cons
     __syncwarp();
     const double qi = q[i];
     const int Sx = 2 * g.m[0] + 1, Sy = 2 * g.m[1] + 1, Sz = 2 * g.m[2] + 1;
-    // lanes over (oy, oz) with z fastest: consecutive addresses per column
+    if (Sy * Sz <= 32 * TP_K) {
+        // each lane owns up to TP_K (oy, oz) pairs (z fastest: consecutive
+        // addresses per column), reused for every x offset
+        int off[TP_K]; double wy[TP_K], wz[TP_K];
+#pragma unroll
+        for (int k = 0; k < TP_K; ++k) {
+            const int e = lane + 32 * k;
+            off[k] = 0; wy[k] = 0.0; wz[k] = 0.0;
+            if (e < Sy * Sz) {
+                const int oy = e / Sz, oz = e - oy * Sz;
+                off[k] = s.idx[1][oy] * g.n[2] + s.idx[2][oz];
+                wy[k] = s.w[1][oy]; wz[k] = s.w[2][oz];
+            }
+        }
+        for (int ox = 0; ox < Sx; ++ox) {
+            const double qwx = qi * s.w[0][ox];
+            if (qwx == 0.0) continue;
+            double* plane = rho + (int64_t)s.idx[0][ox] * g.n[1] * g.n[2];
+#pragma unroll
+            for (int k = 0; k < TP_K; ++k) {
+                const double w = (qwx * wy[k]) * wz[k];                   // q wx wy wz
+                if (w != 0.0) atomicAdd(plane + off[k], w);
+            }
+        }
+        return;
+    }
     for (int e = lane; e < Sx * Sy * Sz; e += 32) {
         const int oz = e % Sz, c = e / Sz, oy = c % Sy, ox = c / Sy;
         const double w = ((qi * s.w[0][ox]) * s.w[1][oy]) * s.w[2][oz];   // q wx wy wz
@@ -141,6 +167,33 @@ __global__ void __launch_bounds__(TP_WARPS * 32) tp_interp_kernel(TpGrid g, cons
     const int Sx = 2 * g.m[0] + 1, Sy = 2 * g.m[1] + 1, Sz = 2 * g.m[2] + 1;
     const int64_t G = g.stride;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    if (Sy * Sz <= 32 * TP_K) {
+        int off[TP_K]; double wy[TP_K], wz[TP_K];
+#pragma unroll
+        for (int k = 0; k < TP_K; ++k) {
+            const int e = lane + 32 * k;
+            off[k] = 0; wy[k] = 0.0; wz[k] = 0.0;
+            if (e < Sy * Sz) {
+                const int oy = e / Sz, oz = e - oy * Sz;
+                off[k] = s.idx[1][oy] * g.n[2] + s.idx[2][oz];
+                wy[k] = s.w[1][oy]; wz[k] = s.w[2][oz];
+            }
+        }
+        for (int ox = 0; ox < Sx; ++ox) {
+            const double wx = s.w[0][ox];
+            if (wx == 0.0) continue;
+            const double* plane = f + (int64_t)s.idx[0][ox] * g.n[1] * g.n[2];
+#pragma unroll
+            for (int k = 0; k < TP_K; ++k) {
+                const double w = (wx * wy[k]) * wz[k];                    // wx wy wz
+                if (w != 0.0) {
+                    a0 = fma(w, __ldg(plane + off[k]), a0);
+                    a1 = fma(w, __ldg(plane + G + off[k]), a1);
+                    a2 = fma(w, __ldg(plane + 2 * G + off[k]), a2);
+                }
+            }
+        }
+    } else
     for (int e = lane; e < Sx * Sy * Sz; e += 32) {
         const int oz = e % Sz, c = e / Sz, oy = c % Sy, ox = c / Sy;
         const double w = (s.w[0][ox] * s.w[1][oy]) * s.w[2][oz];         // wx wy wz
