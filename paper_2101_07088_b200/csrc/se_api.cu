@@ -659,6 +659,7 @@ void se_plan_destroy(se_plan* plan) {
     for (auto h : hs) if (h) cufftDestroy(h);
     if (p->blas) cublasDestroy(p->blas);
     for (auto& b : p->owned) if (b.p) cudaFree(b.p);
+    if (p->nl.h_ovf) cudaFreeHost(p->nl.h_ovf);
     for (auto& pr : p->kev) { if (pr[0]) cudaEventDestroy(pr[0]); if (pr[1]) cudaEventDestroy(pr[1]); }
     if (p->stream && p->own_stream) cudaStreamDestroy(p->stream);
     delete p;

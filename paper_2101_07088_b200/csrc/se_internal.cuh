@@ -137,6 +137,9 @@ struct Buf {
 struct NearLists {
     int64_t cap_far_total = 0, cap_close_total = 0, ncap = 0;
     int *far = nullptr, *close = nullptr, *cfar = nullptr, *cclose = nullptr, *ovf = nullptr;
+    int* ovl = nullptr;        // slots whose lists overflowed (fallback list)
+    int* h_ovf = nullptr;      // pinned: overflow count of the previous solve
+    int64_t grow = 1;          // capacity multiplier learned from overflows
 };
 
 // scratch of near_eval: evaluation points sorted by cell, one-cell warp tasks

@@ -165,7 +165,8 @@ struct NearArgs {
     int64_t* npairs;
     void* stats;
     int* list_far; int* list_close; int64_t cap_far, cap_close;
-    int* cnt_far; int* cnt_close; int* overflow;
+    int* cnt_far; int* cnt_close; int* overflow;   // overflow: count of ovl
+    int* ovl;                                      // slots whose lists overflowed
 };
 
 constexpr int NB_THREADS = 128;
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(NB_THREADS, 10) near_scan_kernel(NearArgs a) {
     // warp-wide flush of whole groups of 4 (16-byte stores, lists stay aligned)
     auto flush = [&](int (*q)[32], int& cnt, int& n, int* list, int cap, bool all) {
         const int m = all ? cnt : (cnt & ~3);
-        if (n + m + 4 > cap) { overflow = true; cnt = 0; return; }
+        if (n + m + 4 > cap) { overflow = true; cnt = 0; return; }   // point re-done by the fallback
         for (int e = 0; e < m; e += 4) {
             int4 v;
             v.x = q[e][lane];
@@ -500,10 +501,10 @@ __global__ void __launch_bounds__(NB_THREADS, 10) near_scan_kernel(NearArgs a) {
     flush(qf[wib], qn, nf, lfar, a.cap_far, true);
     flush(qcl[wib], qc, nc, lcls, a.cap_close, true);
     if (live) {
-        a.cnt_far[slot] = nf;
-        a.cnt_close[slot] = nc;
+        a.cnt_far[slot] = overflow ? 0 : nf;
+        a.cnt_close[slot] = overflow ? 0 : nc;
+        if (overflow) a.ovl[atomicAdd(a.overflow, 1)] = (int)slot;
     }
-    if (overflow) atomicOr(a.overflow, 1);
 }
 
 // pairs within ulps of the cutoff need the reference's KD-tree test too:
@@ -637,7 +638,7 @@ __device__ __forceinline__ void eval_pair(const NearArgs& a, const double* tab, 
 constexpr int FQ = 64;
 constexpr int64_t NEAR_FUSED_MAX = 40000;       // evaluation points (measured crossover)
 
-template <bool F32, int MINB>
+template <bool F32, int MINB, bool FROM_LIST = false>
 __global__ void __launch_bounds__(NB_THREADS, MINB) near_fused_kernel(NearArgs a) {
     constexpr int W = NB_THREADS / 32;
     __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + CL_TAB];
@@ -649,9 +650,13 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_fused_kernel(NearArgs a
         for (int e = tid; e < CL_TAB; e += blockDim.x)
             tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + e] = a.ctab[e];
     __syncthreads();
-    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
-    if (w >= a.ne) return;
-    const int64_t i = a.order[w];
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
+    // FROM_LIST: the points whose pair lists overflowed in the scan (device
+    // count, grid-stride), evaluated here instead of rescanning
+    const int64_t nw = FROM_LIST ? (int64_t)(*a.overflow) : a.ne;
+    const int64_t wstep = FROM_LIST ? ((int64_t)gridDim.x * blockDim.x) >> 5 : nw;
+    for (int64_t w = w0; w < nw; w += wstep) {
+    const int64_t i = a.order[FROM_LIST ? a.ovl[w] : w];
     const double px = a.eval[3 * i], py = a.eval[3 * i + 1], pz = a.eval[3 * i + 2];
     int cx, cy, cz;
     cell_of(a.g, px, py, pz, &cx, &cy, &cz);
@@ -735,6 +740,7 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_fused_kernel(NearArgs a
             a.out[3 * a.out_stride + i] = acc[3];
         }
         if (a.npairs && count) atomicAdd((unsigned long long*)a.npairs, (unsigned long long)count);
+    }
     }
 }
 
@@ -1342,37 +1348,45 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     const double ballc = 4.0 / 3.0 * M_PI * std::pow(std::min(rclose, k.radius), 3.0);
     NearLists& L = p->nl;
     int64_t want_far = (int64_t)(1.6 * dens * ball + 64), want_close = (int64_t)(2.0 * dens * ballc + 64);
+    static const char* lsenv = getenv("SE_NEAR_LIST_SCALE");   // test hook: force overflows
+    if (lsenv) {
+        const double f = atof(lsenv);
+        want_far = std::max<int64_t>(16, (int64_t)(want_far * f));
+        want_close = std::max<int64_t>(16, (int64_t)(want_close * f));
+    }
     want_far = (want_far + 15) & ~15LL;
     want_close = (want_close + 15) & ~15LL;
-    for (int attempt = 0; attempt < 4; ++attempt) {
-        if (ne * want_far > L.cap_far_total || ne * want_close > L.cap_close_total || ne > L.ncap) {
-            void* olds[] = {L.far, L.close, L.cfar, L.cclose, L.ovf};
-            for (void* o : olds) dfree(p, o);
-            L.cap_far_total = std::max<int64_t>(ne * want_far, L.cap_far_total);
-            L.cap_close_total = std::max<int64_t>(ne * want_close, L.cap_close_total);
-            L.ncap = std::max<int64_t>(ne, L.ncap);
-            L.far = dalloc<int>(p, L.cap_far_total);
-            L.close = dalloc<int>(p, L.cap_close_total);
-            L.cfar = dalloc<int>(p, L.ncap);
-            L.cclose = dalloc<int>(p, L.ncap);
-            L.ovf = dalloc<int>(p, 1);
-        }
-        a.list_far = L.far; a.list_close = L.close;
-        a.cap_far = want_far; a.cap_close = want_close;
-        a.cnt_far = L.cfar; a.cnt_close = L.cclose; a.overflow = L.ovf;
-        SE_CUDA(cudaMemsetAsync(L.ovf, 0, sizeof(int), p->stream));
-        if (d_npairs) { p->ktic(3); p->ktic(4); }
-        near_scan_kernel<<<nblk, NB_THREADS, 0, p->stream>>>(a);
-        if (d_npairs) p->ktoc(4);
-        SE_LAUNCHED(p);
-        int ovf = 0;
-        SE_CUDA(cudaMemcpyAsync(&ovf, L.ovf, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
-        SE_CUDA(cudaStreamSynchronize(p->stream));
-        if (!ovf) break;
-        if (attempt == 3) throw Error(SE_ERR_CUDA, "near-field pair list overflow");
-        want_far *= 2;
-        want_close *= 2;
+    // no host sync: points whose lists overflow are evaluated by the fused
+    // kernel from a device list; the overflow count of the previous solve
+    // (read back asynchronously into pinned memory) grows the capacities
+    if (L.h_ovf && *L.h_ovf > 0) { L.grow *= 2; *L.h_ovf = 0; }
+    want_far *= L.grow;
+    want_close *= L.grow;
+    if (ne * want_far > L.cap_far_total || ne * want_close > L.cap_close_total || ne > L.ncap) {
+        void* olds[] = {L.far, L.close, L.cfar, L.cclose, L.ovf, L.ovl};
+        for (void* o : olds) dfree(p, o);
+        L.cap_far_total = std::max<int64_t>(ne * want_far, L.cap_far_total);
+        L.cap_close_total = std::max<int64_t>(ne * want_close, L.cap_close_total);
+        L.ncap = std::max<int64_t>(ne, L.ncap);
+        L.far = dalloc<int>(p, L.cap_far_total);
+        L.close = dalloc<int>(p, L.cap_close_total);
+        L.cfar = dalloc<int>(p, L.ncap);
+        L.cclose = dalloc<int>(p, L.ncap);
+        L.ovf = dalloc<int>(p, 1);
+        L.ovl = dalloc<int>(p, L.ncap);
     }
+    if (!L.h_ovf) {
+        SE_CUDA(cudaMallocHost(&L.h_ovf, sizeof(int)));
+        *L.h_ovf = 0;
+    }
+    a.list_far = L.far; a.list_close = L.close;
+    a.cap_far = want_far; a.cap_close = want_close;
+    a.cnt_far = L.cfar; a.cnt_close = L.cclose; a.overflow = L.ovf; a.ovl = L.ovl;
+    SE_CUDA(cudaMemsetAsync(L.ovf, 0, sizeof(int), p->stream));
+    if (d_npairs) { p->ktic(3); p->ktic(4); }
+    near_scan_kernel<<<nblk, NB_THREADS, 0, p->stream>>>(a);
+    if (d_npairs) p->ktoc(4);
+    SE_LAUNCHED(p);
     if (d_npairs) p->ktic(5);
     if (k.fp32) near_eval_kernel<true, 8, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
     else near_eval_kernel<true, 8><<<nblk, NB_THREADS, 0, p->stream>>>(a);
@@ -1381,6 +1395,10 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     ac.use_ctab = close_ok ? 1 : 0;
     near_eval_kernel<false, 6><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
     SE_LAUNCHED(p);
+    if (k.fp32) near_fused_kernel<true, 6, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
+    else near_fused_kernel<false, 6, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
+    SE_LAUNCHED(p);
+    SE_CUDA(cudaMemcpyAsync(L.h_ovf, L.ovf, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
     near_boundary_kernel<<<4, 256, 0, p->stream>>>(a);
     if (d_npairs) { p->ktoc(5); p->ktoc(3); }
     SE_LAUNCHED(p);
