@@ -359,7 +359,6 @@ __device__ __noinline__ bool tree_keep_s(double Lx, double Ly, double lz, double
 //        membership test and the erf kernels.  Lists have nearly equal
 //        lengths across a warp (same cell), so the evaluation is dense.
 // ---------------------------------------------------------------------------
-constexpr int SCAN_Q = 16;                  // per-lane staging before a flush
 constexpr int SCAN_STAGE = 128;             // staged candidates per warp
 
 // Neighbour columns of a target column and the candidate range of one lane
@@ -399,10 +398,11 @@ __device__ __forceinline__ void column_axis(int c, int i, bool all, int n, float
     *dist = fmaxf(0.f, fmaxf(lo - p, p - hi));
 }
 
-__global__ void __launch_bounds__(NB_THREADS, 10) near_scan_kernel(NearArgs a) {
+template <int SCAN_Q, int SU, int MINB>
+__global__ void __launch_bounds__(NB_THREADS, MINB) near_scan_kernel(NearArgs a) {
     constexpr int W = NB_THREADS / 32;
-    __shared__ int qf[W][SCAN_Q + 4][32];
-    __shared__ int qcl[W][SCAN_Q + 4][32];
+    __shared__ int qf[W][SCAN_Q + SU][32];
+    __shared__ int qcl[W][SCAN_Q + SU][32];
     __shared__ float4 stage[W][SCAN_STAGE];
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
     const int64_t task = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(NB_THREADS, 10) near_scan_kernel(NearArgs a) {
                 const int ee = min(e, c1);
                 while (__any_sync(0xffffffffu, jj < ee)) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < SU; ++u) {
                         if (jj + u < ee) {
                             const float4 f = stage[wib][jj + u - c0];
                             float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(NB_THREADS, 10) near_scan_kernel(NearArgs a) {
                             }
                         }
                     }
-                    jj += 4;
+                    jj += SU;
                     if (__any_sync(0xffffffffu, qn >= SCAN_Q)) flush(qf[wib], qn, nf, lfar, a.cap_far, false);
                     if (__any_sync(0xffffffffu, qc >= SCAN_Q)) flush(qcl[wib], qc, nc, lcls, a.cap_close, false);
                 }
@@ -1384,7 +1384,9 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     a.cnt_far = L.cfar; a.cnt_close = L.cclose; a.overflow = L.ovf; a.ovl = L.ovl;
     SE_CUDA(cudaMemsetAsync(L.ovf, 0, sizeof(int), p->stream));
     if (d_npairs) { p->ktic(3); p->ktic(4); }
-    near_scan_kernel<<<nblk, NB_THREADS, 0, p->stream>>>(a);
+    // 16-deep queues, 4 candidates per step, 7 CTAs / SM (73 registers):
+    // measured best of queue 8..24, step 4 / 8, 6..12 CTAs (3.17 vs 3.29 ms at 10)
+    near_scan_kernel<16, 4, 7><<<nblk, NB_THREADS, 0, p->stream>>>(a);
     if (d_npairs) p->ktoc(4);
     SE_LAUNCHED(p);
     if (d_npairs) p->ktic(5);
