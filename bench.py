@@ -127,25 +127,31 @@ class ClockSampler:
 
 
 def ncu_traffic(kernel):
-    """dram read + write bytes per launch of ``kernel`` from the newest
-    committed ncu --set full summary (profiles/*_ncu_*.json), or None."""
+    """dram read + write bytes per launch of ``kernel`` (summed over its
+    template instances, e.g. the far and close near-field evaluations that
+    make up the timed stage) from the newest committed ncu --set full summary
+    (profiles/*_ncu_*.json), or (None, None)."""
     import glob
     files = sorted(glob.glob(os.path.join(REPO, "profiles", "*_ncu_*.json")),
                    key=os.path.getmtime)
+
+    def gb(r, key):
+        v = r.get(key, "0").split()
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+        return float(v[0]) * scale.get(v[1] if len(v) > 1 else "byte", 1.0)
+
     for path in reversed(files):
         try:
             rows = json.load(open(path))
         except (OSError, ValueError):
             continue
-        for r in rows:
-            if r.get("kernel", "").split("<")[0].endswith(kernel):
-                def gb(key):
-                    v = r.get(key, "0").split()
-                    scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
-                    return float(v[0]) * scale.get(v[1] if len(v) > 1 else "byte", 1.0)
-                return {"bytes": gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum"),
-                        "source": os.path.relpath(path, REPO)}
-    return None
+        hit = [r for r in rows if r.get("kernel", "").split("<")[0].endswith(kernel)]
+        if hit:
+            total = sum(gb(r, "dram__bytes_read.sum") + gb(r, "dram__bytes_write.sum")
+                        for r in hit)
+            return total, "%s (%s)" % (os.path.relpath(path, REPO),
+                                       ", ".join(r["kernel"] for r in hit))
+    return None, None
 
 
 def cpu_baseline(system, params, sample=4096):
@@ -354,9 +360,11 @@ def run_ours(args):
         flops = 0.0
     t_dom = kern[dominant]
     achieved = flops / (t_dom * 1e-3) / 1e12 if t_dom > 0 else 0.0
+    traffic, traffic_src = ncu_traffic(names[dominant])
     roof.update({"achieved": achieved, "peak": fp64_peak,
                  "frac": achieved / fp64_peak if fp64_peak else None,
-                 "kernel_ms": t_dom, "traffic": ncu_traffic(names[dominant])})
+                 "kernel_ms": t_dom, "traffic": traffic,
+                 "traffic_source": traffic_src})
 
     line = {"metric": METRIC, "value": value, "unit": "charges/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
