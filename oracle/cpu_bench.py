@@ -15,7 +15,9 @@ count (the per-charge stages are independent per charge):
   density, the KD-tree over all 3N sources is built) — per target cost.
 
 The result is seconds per full solve = grid + N_src * t_spread + N * (t_interp
-+ t_near).  Single-threaded (numpy / scipy with workers=1).
++ t_near).  ``workers`` mirrors the reference's ``SlabSolver(threads=T)``
+(sw/slab.py:197, scipy.fft workers of the xy transforms, slab.py:242,250);
+every other stage is single-threaded numpy in the reference too.
 """
 
 import time
@@ -31,9 +33,9 @@ def _time(fn, *a, **kw):
     return time.perf_counter() - t, out
 
 
-def grid_stage_seconds(system, params):
+def grid_stage_seconds(system, params, workers=1):
     """Wall time of the oracle's grid pipeline on the full grid (jump path)."""
-    solver = O.OracleSlabSolver(system, params)
+    solver = O.OracleSlabSolver(system, params, workers=workers)
     geo, par = system.geometry, params
     rng = np.random.default_rng(1)
     shape = solver.grid.shape
@@ -81,10 +83,11 @@ def per_charge_seconds(system, params, sample=4096, seed=3):
     return t_sp / n_s, t_in / n_s, t_nf / max(1, len(pick) // 4)
 
 
-def estimate_solve_seconds(system, params, sample=4096, grid_seconds=None):
+def estimate_solve_seconds(system, params, sample=4096, grid_seconds=None,
+                           workers=1):
     """Extrapolated seconds of one full oracle solve and the stage parts."""
     if grid_seconds is None:
-        grid_seconds = grid_stage_seconds(system, params)
+        grid_seconds = grid_stage_seconds(system, params, workers=workers)
     t_sp, t_in, t_nf = per_charge_seconds(system, params, sample)
     n = system.n
     z = system.positions[:, 2]
