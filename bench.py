@@ -224,7 +224,7 @@ def run_reference(args):
                              "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "charges/s",
                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_ours(args):
@@ -438,11 +438,27 @@ def run_ours(args):
         line["paper_config"] = paper_perf.measure(steps=10, warmup=3)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(system, params)
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_JSON_OUT = None
+
+
+def emit(line):
+    """Print the one JSON line on the process's real stdout."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
+    global _JSON_OUT
     args = parse()
+    # libraries (NCCL's version banner, cuFFT / cuBLAS notices) write to fd 1
+    # from C; keep stdout for the JSON line alone by sending fd 1 to stderr
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if args.impl == "reference":
         run_reference(args)
     else:
