@@ -17,7 +17,9 @@ def test_reference_arm_json_line():
          "--config", "c2", "--steps", "1", "--warmup", "0"],
         capture_output=True, text=True, timeout=600, env=env, cwd=REPO)
     assert out.returncode == 0, out.stderr[-2000:]
-    line = json.loads(out.stdout.strip().splitlines()[-1])
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, lines            # stdout carries the JSON line only
+    line = json.loads(lines[0])
     assert line["impl"] == "reference"
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup",
                 "ms_per_step", "higher_is_better", "config", "e2e",
