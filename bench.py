@@ -126,32 +126,70 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def ncu_traffic(kernel):
-    """dram read + write bytes per launch of ``kernel`` (summed over its
-    template instances, e.g. the far and close near-field evaluations that
-    make up the timed stage) from the newest committed ncu --set full summary
-    (profiles/*_ncu_*.json), or (None, None)."""
-    import glob
-    files = sorted(glob.glob(os.path.join(REPO, "profiles", "*_ncu_*.json")),
-                   key=os.path.getmtime)
+# The one ncu --set full capture the roofline traffic is read from (a
+# committed summary of one warm C4 solve, tools/ncu_summary.py); each stage's
+# traffic is the sum over ALL of its kernels' launches in that capture.
+NCU_FILE = os.path.join("profiles", "ncu_c4_kernels.json")
+STAGE_KERNELS = {                      # stage -> kernel-name prefixes in the capture
+    "spread": ("spread_mma_kernel",),
+    "interp": ("interp_kernel",),
+    "bvp": ("bvp_kernel",),
+    "near": ("near_scan_kernel", "near_eval_kernel", "near_fq_kernel",
+             "near_fused_kernel", "near_boundary_kernel"),
+}
 
-    def gb(r, key):
+
+def ncu_stage(stage):
+    """(dram read+write bytes, duration ms, source) of ``stage`` in the
+    committed capture NCU_FILE, summed over its kernels, or Nones."""
+    path = os.path.join(REPO, NCU_FILE)
+    try:
+        rows = json.load(open(path))
+    except (OSError, ValueError):
+        return None, None, None
+
+    def val(r, key):
         v = r.get(key, "0").split()
-        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
-        return float(v[0]) * scale.get(v[1] if len(v) > 1 else "byte", 1.0)
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0,
+                 "ms": 1.0, "us": 1e-3, "ns": 1e-6}
+        return float(v[0].replace(",", "")) * scale.get(v[1] if len(v) > 1 else "byte", 1.0)
 
-    for path in reversed(files):
-        try:
-            rows = json.load(open(path))
-        except (OSError, ValueError):
-            continue
-        hit = [r for r in rows if r.get("kernel", "").split("<")[0].endswith(kernel)]
-        if hit:
-            total = sum(gb(r, "dram__bytes_read.sum") + gb(r, "dram__bytes_write.sum")
-                        for r in hit)
-            return total, "%s (%s)" % (os.path.relpath(path, REPO),
-                                       ", ".join(r["kernel"] for r in hit))
-    return None, None
+    pre = STAGE_KERNELS[stage]
+    hit = [r for r in rows
+           if r.get("kernel", "").replace("void ", "").split("<")[0].split("::")[-1]
+           .startswith(pre)]
+    if not hit:
+        return None, None, None
+    traffic = sum(val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum") for r in hit)
+    dur = sum(val(r, "gpu__time_duration.sum") for r in hit)
+    return traffic, dur, "%s (%s)" % (NCU_FILE, ", ".join(sorted({r["kernel"] for r in hit})))
+
+
+def stage_work(stage, n, n_src, params, pairs):
+    """Algorithmic bytes and fp64 flops of one launch of a stage at this
+    workload: b = 8, G = Nx Ny Nz,
+    S = 13 x 13 x 17 stencil nodes per charge at C4."""
+    G = params.Nx * params.Ny * params.Nz
+    Gh = params.Nx * (params.Ny // 2 + 1) * params.Nz
+    S = 13 * 13 * 17
+    if stage == "spread":           # 4b per source in, two real grids out
+        return 32.0 * n_src + 16.0 * G, 2.0 * n_src * S
+    if stage == "interp":           # 4 field grids + positions in, 4 values out
+        return 32.0 * G + 24.0 * n + 32.0 * n, 2.0 * 4 * n * S
+    if stage == "bvp":              # two complex coefficient stacks in and out
+        return 2 * 2 * 16.0 * Gh, 0.0
+    if stage == "near":             # positions + charges of 3N sources, 4 outputs
+        return 32.0 * 3 * n + 32.0 * n, FP64_PAIR_FLOPS * pairs
+    raise KeyError(stage)
+
+
+def measured_hbm_gbs():
+    """HBM copy bandwidth of this pool's B200s (MEASURED_PEAKS.json, driver
+    written), else the profiling recipe's fallback."""
+    try:
+        return float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6500.0
 
 
 def host_threads():
@@ -187,7 +225,33 @@ def cpu_baseline(system, params, sample=4096):
             "ms_per_solve": est["total_s"] * 1e3, "stages": est}
 
 
+def bench_config(args, system, params, world=1, sharded=False):
+    """The ``config`` dict of both arms (identical keys and values)."""
+    if not sharded:
+        par = "single"
+    elif args.replicate_grid:
+        par = ("shard%d: charges split by index; grid pipeline replicated after "
+               "an NCCL all-reduce" % world)
+    else:
+        par = ("shard%d: charges split by index; NCCL reduce-scatter to z slabs, "
+               "slab xy FFTs, all-to-all to (kx,ky) pencils, pencil DCT + BVPs, "
+               "all-to-all back, all-gather of the fields" % world)
+    return {"workload": args.config, "N": system.n,
+            "grid": [params.Nx, params.Ny, params.Nz],
+            "eps_b": system.geometry.eps_b, "eps_t": system.geometry.eps_t,
+            "delta": params.delta, "parallelism": par,
+            "l2": "flushed (256 MB write) between timed steps"}
+
+
 def run_reference(args):
+    """The reference's CPU path (the oracle port, oracle/), rank 0 only.
+    A full C4 solve on the CPU takes ~20 min and ~90 GB for the near-field
+    pair arrays, so every step times a bounded sample of the
+    workload -- the grid pipeline on the full grid once, then per step the
+    spread (in the reference's 256-charge chunks), interpolation and near
+    field of 2048 sampled charges at full density -- and reports the
+    solve time extrapolated linearly in the charge count.  ``sample_wall_s``
+    is what the steps actually took."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -195,31 +259,34 @@ def run_reference(args):
     from paper_2101_07088_b200 import workloads as W
     system, params = W.build(args.config)
     cores = host_threads()
-    t_grid = None
-    totals = []
+    t0 = time.perf_counter()
+    t_grid = cpu_bench.grid_stage_seconds(system, params, workers=cores)
+    totals, walls = [], []
     for step in range(args.warmup + args.steps):
-        if t_grid is None:
-            t_grid = cpu_bench.grid_stage_seconds(system, params, workers=cores)
+        ts = time.perf_counter()
         est = cpu_bench.estimate_solve_seconds(system, params, sample=2048,
                                                grid_seconds=t_grid)
         if step >= args.warmup:
             totals.append(est["total_s"])
+            walls.append(time.perf_counter() - ts)
     mean_s = float(np.mean(totals))
     value = system.n / mean_s
-    sample = ("oracle (numpy/scipy restatement of the reference solve; %d "
-              "threads for the xy FFTs as the reference's threads knob, other "
-              "stages single-threaded as in the reference): grid stages timed "
-              "once on the full grid (%.1f s), per-charge stages timed each "
-              "step on 2048 charges and extrapolated to N=%d"
-              % (cores, t_grid, system.n))
+    sample = ("oracle port of the reference solve (numpy/scipy; %d threads for "
+              "the xy FFTs as the reference's threads knob, other stages "
+              "single-threaded as in the reference; spread in the reference's "
+              "256-charge chunks): grid stages timed once on the full grid "
+              "(%.1f s), per-charge stages timed each step on 2048 charges "
+              "(%.2f s per step) and extrapolated to N=%d"
+              % (cores, t_grid, float(np.mean(walls)), system.n))
     line = {"impl": "reference", "metric": METRIC, "value": value,
             "unit": "charges/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": mean_s * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded random charges, electroneutral)",
-            "config": {"workload": args.config, "N": system.n,
-                       "grid": [params.Nx, params.Ny, params.Nz],
-                       "parallelism": "cpu"},
+            "config": bench_config(args, system, params),
+            "extrapolated": True,
+            "sample_wall_s": {"grid_once": t_grid, "per_step": float(np.mean(walls)),
+                              "total": time.perf_counter() - t0},
             "cpu_baseline": {"value": value, "unit": "charges/s", "cores": cores,
                              "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "charges/s",
@@ -347,66 +414,51 @@ def run_ours(args):
 
     if rank != 0:
         return
-    # ---- roofline of the dominant kernel (FP64-pipe bound)
+    # ---- rooflines: every timed stage against HBM and the FP64 pipe; the
+    # dominant one is the headline roofline (FP64-pipe bound)
     lib = _lib.load()
     import ctypes
     pk = ctypes.c_double(0.0)
     _lib.check(lib.se_fp64_peak(local, ctypes.byref(pk)))
     fp64_peak = pk.value
-    kern = {k: v for k, v in stage.items() if k in ("k_spread", "k_bvp", "k_interp",
-                                                     "k_near_scan", "k_near_eval")}
-    dominant = max(kern, key=kern.get)
-    names = {"k_near_eval": "near_eval_kernel", "k_near_scan": "near_scan_kernel",
-             "k_interp": "interp_kernel", "k_spread": "spread_kernel",
-             "k_bvp": "bvp_kernel"}
-    roof = {"kernel": names[dominant], "bound": "fp64", "unit": "TFLOP/s",
+    hbm_peak = measured_hbm_gbs()
+    n_src = int(diag.n_sources)
+    stages = {}
+    for st, key in (("spread", "k_spread"), ("interp", "k_interp"), ("bvp", "k_bvp"),
+                    ("near", "k_near")):
+        ms = stage[key]
+        nbytes, flops = stage_work(st, n, n_src, params, pairs)
+        traffic, ncu_ms, src = ncu_stage(st)
+        gbs = nbytes / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+        tfl = flops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+        stages[st] = {"ms": ms, "alg_bytes": nbytes, "hbm_gbs": gbs,
+                      "hbm_frac": gbs / hbm_peak, "alg_flop": flops,
+                      "fp64_tflops": tfl, "fp64_frac": tfl / fp64_peak if fp64_peak else None,
+                      "traffic": traffic, "traffic_ms_ncu": ncu_ms, "traffic_source": src}
+    dom = max(("spread", "interp", "near"), key=lambda k: stages[k]["ms"])
+    d = stages[dom]
+    roof = {"kernel": dom, "bound": "fp64", "unit": "TFLOP/s",
+            "achieved": d["fp64_tflops"], "peak": fp64_peak, "frac": d["fp64_frac"],
+            "traffic": d["traffic"], "traffic_source": d["traffic_source"],
+            "kernel_ms": d["ms"],
             "peak_source": "measured DFMA throughput on this GPU (se_fp64_peak); "
-                           "no tensor-core or HBM bound applies to this kernel"}
-    if dominant == "k_near_eval":
-        flops = pairs * FP64_PAIR_FLOPS
-        roof["work"] = "%d pairs x %g fp64 flop (SURVEY 8d)" % (pairs, FP64_PAIR_FLOPS)
-    elif dominant == "k_interp":
-        flops = 2.0 * 4 * n * 13 * 13 * 17
-        roof["work"] = "2 x 4 fields x N x 13x13x17 stencil nodes"
-    elif dominant == "k_spread":
-        flops = 2.0 * 1.17 * n * 13 * 13 * 17
-        roof["work"] = "2 x N' (1.17 N sources) x 13x13x17 stencil nodes"
-    else:
-        flops = 0.0
-    t_dom = kern[dominant]
-    achieved = flops / (t_dom * 1e-3) / 1e12 if t_dom > 0 else 0.0
-    traffic, traffic_src = ncu_traffic(names[dominant])
-    roof.update({"achieved": achieved, "peak": fp64_peak,
-                 "frac": achieved / fp64_peak if fp64_peak else None,
-                 "kernel_ms": t_dom, "traffic": traffic,
-                 "traffic_source": traffic_src})
+                           "no tensor-core op on this path, HBM fraction reported "
+                           "per stage in stage_roofline",
+            "work": ("%d pairs x %g fp64 flop (SURVEY 8d)" % (pairs, FP64_PAIR_FLOPS)
+                     if dom == "near" else "2 x 13x13x17 stencil nodes per charge/source")}
 
     line = {"metric": METRIC, "value": value, "unit": "charges/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded random charges, electroneutral)",
-            "config": {"workload": args.config, "N": n,
-                       "grid": [params.Nx, params.Ny, params.Nz],
-                       "eps_b": system.geometry.eps_b,
-                       "eps_t": system.geometry.eps_t, "delta": params.delta,
-                       "parallelism": (("shard%d: charges split by index; grid "
-                                        "pipeline replicated after an NCCL "
-                                        "all-reduce" % world)
-                                       if args.replicate_grid else
-                                       ("shard%d: charges split by index; NCCL "
-                                        "reduce-scatter to z slabs, slab xy "
-                                        "FFTs, all-to-all to (kx,ky) pencils, "
-                                        "pencil DCT + BVPs, all-to-all back, "
-                                        "all-gather of the fields" % world))
-                       if sharded else "single",
-                       "l2": "flushed (256 MB write) between timed steps"},
+            "config": bench_config(args, system, params, world, sharded),
             "e2e": {"value": n / (e2e_ms * 1e-3), "unit": "charges/s",
                     "ms_per_step": e2e_ms, "h2d_bytes_per_step": 24 * n,
                     "d2h_bytes_per_step": 32 * n + 8},
             "gpu_launches": launches,
             "kernel_ms": stage, "near_pairs": pairs,
-            "roofline": roof, "clocks": clk}
+            "roofline": roof, "stage_roofline": stages, "clocks": clk}
     if world == 1 and not sharded:
         # the optional fp32 mode (SE_FP32: far pair kernels in single
         # precision, same pair set) on the same workload and timing rules;

@@ -50,6 +50,10 @@ extern "C" {
                                           the exact fp64 test); results within
                                           the run's Ewald tolerance */
 
+#define SE_PAIR_HASH       (1u << 8)   /* record the near-field pair SET of the
+                                          charges (se_debug_fetch 6) for
+                                          parity tests */
+
 /* Solver parameters: the geometry plus the EwaldParams fields the device
  * path needs (params.py:28-50). */
 typedef struct {

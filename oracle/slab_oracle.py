@@ -26,6 +26,7 @@ from scipy.special import erf
 
 FOUR_PI = 4.0 * np.pi
 TWO_OVER_SQRTPI = 2.0 / np.sqrt(np.pi)
+CHUNK = 256                 # charges per vectorised chunk (gridops.py:15)
 
 
 # ---------------------------------------------------------------------------
@@ -163,8 +164,9 @@ class ChebGrid:
             return total.reshape(self.shape)
         self._check_z(p)
         (ix, wx), (iy, wy), (iz, wz) = self.stencils(p, width, rxy, rz)
-        per_point = wx.shape[1] * wy.shape[1] * wz.shape[1]
-        step = max(1, (1 << 22) // per_point)
+        # the reference's chunking (_CHUNK = 256, gridops.py:15,91): one
+        # full-grid bincount per 256 sources, which is also its cost profile
+        step = CHUNK
         for a in range(0, p.shape[0], step):
             s = slice(a, a + step)
             val = (q[s, None, None, None] * wx[s, :, None, None]
@@ -187,8 +189,7 @@ class ChebGrid:
         self._check_z(p)
         (ix, wx), (iy, wy), (iz, wz) = self.stencils(p, width, rxy, rz)
         wzq = wz * self.wz[iz]
-        per_point = wx.shape[1] * wy.shape[1] * wz.shape[1] * fs.shape[0]
-        step = max(1, (1 << 21) // per_point)
+        step = CHUNK                                      # gridops.py:15,125
         cell = self.hx * self.hy
         for a in range(0, p.shape[0], step):
             s = slice(a, a + step)

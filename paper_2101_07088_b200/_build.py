@@ -28,21 +28,35 @@ def _stale():
 
 
 def build(force=False, verbose=False):
-    """Compile the CUDA library if a source is newer than the .so."""
+    """Compile the CUDA library if a source is newer than the .so (one nvcc
+    per translation unit in parallel, then one link)."""
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, "-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
-           "-shared", "-Xptxas", "-v" if verbose else "-O3",
-           "-o", LIB + ".tmp"]
-    cmd += [os.path.join(CSRC, f) for f in SOURCES]
-    cmd += ["-L" + os.path.join(CUDA_HOME, "lib64"), "-lcufft", "-lcublas",
-            "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64")]
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    flags = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
+             "-Xptxas", "-v" if verbose else "-O3"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *flags, "-c", "-o", obj, os.path.join(CSRC, src)]
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for obj, res in results:
+        if res.returncode != 0 or verbose:
+            sys.stderr.write(res.stdout + res.stderr)
+        if res.returncode != 0:
+            raise RuntimeError("nvcc failed compiling %s" % obj)
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *[o for o, _ in results],
+           "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcufft", "-lcublas",
+           "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libslabewald_cuda.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc failed linking libslabewald_cuda.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -171,6 +171,16 @@ void phase_charges(Plan* p, const double* d_pos, double* d_phi_out, double* d_E_
         kavg.fp32 = (S.flags & SE_FP32) ? 1 : 0;
         kpt = kernel_of(P, 1, false, false);
     }
+    p->pair_hash = (S.flags & SE_PAIR_HASH) != 0;
+    if (p->pair_hash) {
+        if (p->phash_cap < count) {
+            dfree(p, p->d_phash);
+            p->d_phash = dalloc<unsigned long long>(p, 2 * (size_t)std::max<int64_t>(count, 1));
+            p->phash_cap = count;
+        }
+        SE_CUDA(cudaMemsetAsync(p->d_phash, 0, 16 * (size_t)std::max<int64_t>(count, 1), s));
+        p->phash_n = count;
+    }
     if (!S.near_empty) {
         build_cells(p, d_pos, p->d_q, n, true);           // sources: every charge
         near_eval(p, d_pos + 3 * first, nullptr, count, kavg, p->d_near, p->d_count);
@@ -1087,6 +1097,7 @@ int64_t se_debug_fetch(se_plan* plan, int which, void* host, int64_t nbytes) {
         case 3: src = p->d_mism; size = 4 * p->M * 16; break;
         case 4: src = p->d_far; size = 4 * p->N * sizeof(double); break;
         case 5: src = p->d_near; size = 4 * p->N * sizeof(double); break;
+        case 6: src = p->d_phash; size = p->d_phash ? 2 * p->phash_n * 8 : 0; break;
         default: return -1;
     }
     if (!host) return size;

@@ -298,6 +298,9 @@ struct Plan {
     int64_t cell_cap = 0;
     double* d_mm = nullptr;               // z-range partials
     int64_t* d_count = nullptr;
+    bool pair_hash = false;               // SE_PAIR_HASH on the solve in flight
+    unsigned long long* d_phash = nullptr;   // [2][N] pair-set hash, count
+    int64_t phash_cap = 0, phash_n = 0;
     double* d_partial = nullptr;          // reduction partials
     double* d_origin = nullptr;           // (0, 0, 0)
     double *d_wall_pts = nullptr, *d_wall_far = nullptr, *d_wall_near = nullptr;

@@ -167,6 +167,9 @@ struct NearArgs {
     int* list_far; int* list_close; int64_t cap_far, cap_close;
     int* cnt_far; int* cnt_close; int* overflow;   // overflow: count of ovl
     int* ovl;                                      // slots whose lists overflowed
+    // SE_PAIR_HASH: per evaluation point, the wrap-around sum of mix64(source
+    // index) over its accepted pairs ([0, ne)) and their count ([ne, 2 ne))
+    const int* orig; unsigned long long* phash;
 };
 
 constexpr int NB_THREADS = 128;
@@ -515,11 +518,13 @@ __device__ __forceinline__ void defer_pair(const NearArgs& a, int64_t i, int j) 
     else atomicOr(a.flags, FLAG_NEAR_BND);
 }
 
-template <bool FAR, bool F32 = false>
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z);
+
+template <bool FAR, bool F32 = false, bool HASH = false>
 __device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, const int* list,
                                           int n, double px, double py, double pz, int64_t self_i,
                                           double& phi, double& ex, double& ey, double& ez,
-                                          int& count) {
+                                          int& count, unsigned long long& hs) {
     const double Lx = a.g.Lx, Ly = a.g.Ly;
     const bool nd = a.need_field;
     for (int k = 0; k < n; k += 4) {
@@ -545,6 +550,7 @@ __device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, 
                         ex = fma(cq, dx, ex); ey = fma(cq, dy, ey); ez = fma(cq, dz, ez);
                     }
                     ++count;
+                    if (HASH) hs += mix64((unsigned long long)a.orig[jj[u]]);
                 }
             }
         }
@@ -554,7 +560,7 @@ __device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, 
 // Evaluation of one list kind per launch: the far lists (the bulk; erfc-only
 // kernel, small register footprint, high occupancy) write the sums, the close
 // lists (general kernel) add to them.
-template <bool FAR, int MINB, bool F32 = false>
+template <bool FAR, int MINB, bool F32 = false, bool HASH = false>
 __global__ void __launch_bounds__(NB_THREADS, MINB) near_eval_kernel(NearArgs a) {
     __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + (FAR ? 0 : CL_TAB)];
     const int tid = threadIdx.x, lane = tid & 31;
@@ -573,16 +579,22 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_eval_kernel(NearArgs a)
     const bool live = slot < a.pt_end[tk.x];
     double phi = 0, ex = 0, ey = 0, ez = 0;
     int count = 0;
+    unsigned long long hs = 0;
     int64_t i = 0;
     if (live) {
         i = a.order[slot];
         const double px = a.eval[3 * i], py = a.eval[3 * i + 1], pz = a.eval[3 * i + 2];
         if (FAR)
-            eval_list<true, F32>(a, tab, a.list_far + slot * a.cap_far, a.cnt_far[slot], px, py, pz,
-                                 i, phi, ex, ey, ez, count);
+            eval_list<true, F32, HASH>(a, tab, a.list_far + slot * a.cap_far, a.cnt_far[slot], px,
+                                       py, pz, i, phi, ex, ey, ez, count, hs);
         else
-            eval_list<false>(a, tab, a.list_close + slot * a.cap_close, a.cnt_close[slot], px,
-                             py, pz, i, phi, ex, ey, ez, count);
+            eval_list<false, false, HASH>(a, tab, a.list_close + slot * a.cap_close,
+                                          a.cnt_close[slot], px, py, pz, i, phi, ex, ey, ez,
+                                          count, hs);
+        if (HASH) {                                 // overflowed points are re-done below
+            if (FAR) { a.phash[i] = hs; a.phash[a.ne + i] = (unsigned long long)count; }
+            else { a.phash[i] += hs; a.phash[a.ne + i] += (unsigned long long)count; }
+        }
         if (FAR) {
             a.out[i] = phi;
             if (a.need_field) {
@@ -604,12 +616,21 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_eval_kernel(NearArgs a)
     if (lane == 0 && a.npairs && cnt) atomicAdd((unsigned long long*)a.npairs, cnt);
 }
 
+// splitmix64 finaliser: the per-pair term of the pair-set hash (SE_PAIR_HASH;
+// the test side is tests/_golden.py pair_hash)
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
 // One pair of an evaluation point (eval_list's body for one source).
-template <bool FAR, bool F32>
+template <bool FAR, bool F32, bool HASH = false>
 __device__ __forceinline__ void eval_pair(const NearArgs& a, const double* tab, int j,
                                           double px, double py, double pz, int64_t self_i,
                                           double& phi, double& ex, double& ey, double& ez,
-                                          int& count) {
+                                          int& count, unsigned long long* hsum = nullptr) {
     const double4 sv = a.src[j];
     const double dx = min_image(__dsub_rn(px, sv.x), a.g.Lx);
     const double dy = min_image(__dsub_rn(py, sv.y), a.g.Ly);
@@ -626,6 +647,7 @@ __device__ __forceinline__ void eval_pair(const NearArgs& a, const double* tab, 
             ex = fma(cq, dx, ex); ey = fma(cq, dy, ey); ez = fma(cq, dz, ez);
         }
         ++count;
+        if (HASH) *hsum += mix64((unsigned long long)a.orig[j]);
     }
 }
 
@@ -638,7 +660,7 @@ __device__ __forceinline__ void eval_pair(const NearArgs& a, const double* tab, 
 constexpr int FQ = 64;
 constexpr int64_t NEAR_FUSED_MAX = 40000;       // evaluation points (measured crossover)
 
-template <bool F32, int MINB, bool FROM_LIST = false>
+template <bool F32, int MINB, bool FROM_LIST = false, bool HASH = false>
 __global__ void __launch_bounds__(NB_THREADS, MINB) near_fused_kernel(NearArgs a) {
     constexpr int W = NB_THREADS / 32;
     __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + CL_TAB];
@@ -668,6 +690,7 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_fused_kernel(NearArgs a
     const int nzb = a.g.ncz;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     int count = 0, nf = 0, nc = 0;
+    unsigned long long hs = 0;
     const unsigned below = (1u << lane) - 1u;
     for (int iy = 0; iy < cw.nyr; ++iy) {
         int yc; float sy, dyd;
@@ -702,16 +725,16 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_fused_kernel(NearArgs a
                 nc += __popc(bc);
                 __syncwarp();
                 if (nf >= 32) {
-                    eval_pair<true, F32>(a, tab, qf[wib][lane], px, py, pz, i, acc[0], acc[1],
-                                         acc[2], acc[3], count);
+                    eval_pair<true, F32, HASH>(a, tab, qf[wib][lane], px, py, pz, i, acc[0],
+                                               acc[1], acc[2], acc[3], count, &hs);
                     __syncwarp();
                     if (lane < nf - 32) qf[wib][lane] = qf[wib][32 + lane];
                     nf -= 32;
                     __syncwarp();
                 }
                 if (nc >= 32) {
-                    eval_pair<false, false>(a, tab, qc[wib][lane], px, py, pz, i, acc[0], acc[1],
-                                            acc[2], acc[3], count);
+                    eval_pair<false, false, HASH>(a, tab, qc[wib][lane], px, py, pz, i, acc[0],
+                                                  acc[1], acc[2], acc[3], count, &hs);
                     __syncwarp();
                     if (lane < nc - 32) qc[wib][lane] = qc[wib][32 + lane];
                     nc -= 32;
@@ -721,18 +744,20 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_fused_kernel(NearArgs a
         }
     }
     if (lane < nf)
-        eval_pair<true, F32>(a, tab, qf[wib][lane], px, py, pz, i, acc[0], acc[1], acc[2], acc[3],
-                             count);
+        eval_pair<true, F32, HASH>(a, tab, qf[wib][lane], px, py, pz, i, acc[0], acc[1], acc[2],
+                                   acc[3], count, &hs);
     if (lane < nc)
-        eval_pair<false, false>(a, tab, qc[wib][lane], px, py, pz, i, acc[0], acc[1], acc[2],
-                                acc[3], count);
+        eval_pair<false, false, HASH>(a, tab, qc[wib][lane], px, py, pz, i, acc[0], acc[1],
+                                      acc[2], acc[3], count, &hs);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
         count += __shfl_xor_sync(0xffffffffu, count, o);
+        if (HASH) hs += __shfl_xor_sync(0xffffffffu, hs, o);
     }
     if (lane == 0) {
+        if (HASH) { a.phash[i] = hs; a.phash[a.ne + i] = (unsigned long long)count; }
         a.out[i] = acc[0];
         if (a.need_field) {
             a.out[a.out_stride + i] = acc[1];
@@ -742,6 +767,155 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_fused_kernel(NearArgs a
         if (a.npairs && count) atomicAdd((unsigned long long*)a.npairs, (unsigned long long)count);
     }
     }
+}
+
+// Fused scan + evaluation for many points (no pair lists in HBM).
+// One warp per task (<= 32 evaluation points of one xy column, sorted by z;
+// lane = point), as in the two-phase scan: the 25 neighbour columns are
+// pruned by xy distance, each lane's z window is the chord of its query
+// sphere, the warp's union window is staged through shared memory in
+// coalesced chunks and every lane tests its own part with the fp32
+// pre-test.  Survivors go to per-lane ring queues in shared memory (far /
+// close, lane-major so a lane's slots sit in its own bank); when a queue
+// nears full the warp drains it: every lane evaluates the entries of its own
+// queue (the exact fp64 test, then the erf kernels), as many as the
+// shortest live queue holds so all lanes stay busy (at least half a queue),
+// accumulating in registers.  Each point's sum is a fixed sequence of its
+// own pairs: deterministic, one store per point and component.
+constexpr int FQF = 32, FQC = 16;              // far / close ring depth per lane
+
+template <bool F32, bool HASH, int SU, int MINB>
+__global__ void __launch_bounds__(NB_THREADS, MINB) near_fq_kernel(NearArgs a) {
+    constexpr int W = NB_THREADS / 32;
+    constexpr unsigned F = 0xffffffffu;
+    __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + CL_TAB];
+    __shared__ int qf[W][FQF][32];
+    __shared__ int qc[W][FQC][32];
+    __shared__ float4 stage[W][SCAN_STAGE];
+    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+    if (!a.use_ctab || !a.use_poly)
+        for (int e = tid; e < SE_ERFCX_NP * (SE_ERFCX_DEG + 1); e += blockDim.x)
+            tab[e] = (&se_erfcx_tab[0][0])[e];
+    if (a.use_ctab)
+        for (int e = tid; e < CL_TAB; e += blockDim.x)
+            tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + e] = a.ctab[e];
+    __syncthreads();
+    const int64_t task = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
+    if (task >= a.ntask || task >= *a.ntask_dev) return;
+    const int2 tk = a.tasks[task];
+    const int col = tk.x;
+    const int64_t slot = (int64_t)tk.y + lane;
+    const bool live = slot < a.pt_end[col];
+    const int64_t i = live ? a.order[slot] : 0;
+    double px = 0, py = 0, pz = 0;
+    float pxf = 0.f, pyf = 0.f, pzf = 0.f;
+    if (live) {
+        px = a.eval[3 * i]; py = a.eval[3 * i + 1]; pz = a.eval[3 * i + 2];
+        pxf = (float)wrap(px, a.g.Lx);
+        pyf = (float)wrap(py, a.g.Ly);
+        pzf = (float)(pz - a.g.zlo);
+    }
+    const int cx = col % a.g.ncx, cy = col / a.g.ncx;
+    const ColumnWalk cw = column_walk(a.g);
+    const float r2f = a.r2f, r2c = a.r2close;
+    const float csxf = (float)a.g.csx, csyf = (float)a.g.csy, icsz = (float)(1.0 / a.g.csz);
+    const int nzb = a.g.ncz;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int count = 0;
+    unsigned long long hs = 0;
+    int nf = 0, hf = 0, nc = 0, hc = 0;           // queue fill and head per lane
+    // evaluate k entries of each lane's far (close) queue; lanes holding
+    // fewer evaluate all of theirs
+    auto drain_far = [&](int k) {
+        for (int t = 0; t < k; ++t) {
+            if (t < nf)
+                eval_pair<true, F32, HASH>(a, tab, qf[wib][(hf + t) & (FQF - 1)][lane], px, py,
+                                           pz, i, acc[0], acc[1], acc[2], acc[3], count, &hs);
+        }
+        const int d = min(k, nf);
+        hf = (hf + d) & (FQF - 1);
+        nf -= d;
+    };
+    auto drain_close = [&](int k) {
+        for (int t = 0; t < k; ++t) {
+            if (t < nc)
+                eval_pair<false, false, HASH>(a, tab, qc[wib][(hc + t) & (FQC - 1)][lane], px,
+                                              py, pz, i, acc[0], acc[1], acc[2], acc[3], count,
+                                              &hs);
+        }
+        const int d = min(k, nc);
+        hc = (hc + d) & (FQC - 1);
+        nc -= d;
+    };
+    for (int iy = 0; iy < cw.nyr; ++iy) {
+        int yc; float sy, dyd;
+        column_axis(cy, iy, cw.ally, a.g.ncy, csyf, a.Lyf, pyf, &yc, &sy, &dyd);
+        for (int ix = 0; ix < cw.nxr; ++ix) {
+            int xc; float sx, dxd;
+            column_axis(cx, ix, cw.allx, a.g.ncx, csxf, a.Lxf, pxf, &xc, &sx, &dxd);
+            const float d2 = fmaf(dxd, dxd, dyd * dyd);
+            int j = 0, e = 0;
+            if (live && d2 <= r2f) {
+                const float hz = sqrtf(r2f - d2) * 1.0001f + a.zmarg;
+                const int z0 = max(0, min(nzb - 1, (int)floorf((pzf - hz) * icsz)));
+                const int z1 = max(0, min(nzb - 1, (int)floorf((pzf + hz) * icsz)));
+                const int base = (yc * a.g.ncx + xc) * nzb;
+                j = a.start[base + z0];
+                e = a.start[base + z1 + 1];
+            }
+            if (!__any_sync(F, j < e)) continue;
+            const float qx = pxf - sx, qy = pyf - sy;
+            int umin = (j < e) ? j : 0x7fffffff, umax = (j < e) ? e : 0;
+            umin = __reduce_min_sync(F, umin);
+            umax = __reduce_max_sync(F, umax);
+            for (int c0 = umin; c0 < umax; c0 += SCAN_STAGE) {
+                const int c1 = min(umax, c0 + SCAN_STAGE);
+                __syncwarp();
+                for (int q = c0 + lane; q < c1; q += 32) stage[wib][q - c0] = a.srcf[q];
+                __syncwarp();
+                int jj = max(j, c0);
+                const int ee = min(e, c1);
+                while (__any_sync(F, jj < ee)) {
+#pragma unroll
+                    for (int u = 0; u < SU; ++u) {
+                        if (jj + u < ee) {
+                            const float4 f = stage[wib][jj + u - c0];
+                            float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
+                            if (cw.allx) dx -= a.Lxf * rintf(dx * a.iLxf);
+                            if (cw.ally) dy -= a.Lyf * rintf(dy * a.iLyf);
+                            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                            if (r2 <= r2f) {
+                                if (r2 > r2c) qf[wib][(hf + nf++) & (FQF - 1)][lane] = jj + u;
+                                else qc[wib][(hc + nc++) & (FQC - 1)][lane] = jj + u;
+                            }
+                        }
+                    }
+                    jj += SU;
+                    if (__any_sync(F, nf > FQF - SU)) {
+                        const int m = __reduce_min_sync(F, (unsigned)(live ? nf : FQF));
+                        drain_far(max(m, FQF / 2));
+                    }
+                    if (__any_sync(F, nc > FQC - SU)) {
+                        const int m = __reduce_min_sync(F, (unsigned)(live ? nc : FQC));
+                        drain_close(max(m, FQC / 2));
+                    }
+                }
+            }
+        }
+    }
+    drain_far(__reduce_max_sync(F, (unsigned)nf));
+    drain_close(__reduce_max_sync(F, (unsigned)nc));
+    if (live) {
+        a.out[i] = acc[0];
+        if (a.need_field) {
+            a.out[a.out_stride + i] = acc[1];
+            a.out[2 * a.out_stride + i] = acc[2];
+            a.out[3 * a.out_stride + i] = acc[3];
+        }
+        if (HASH) { a.phash[i] = hs; a.phash[a.ne + i] = (unsigned long long)count; }
+    }
+    const unsigned cnt = __reduce_add_sync(F, (unsigned)count);
+    if (lane == 0 && a.npairs && cnt) atomicAdd((unsigned long long*)a.npairs, (unsigned long long)cnt);
 }
 
 // A few evaluation points (the gauge origin): one CTA per point, the threads
@@ -767,7 +941,7 @@ __global__ void __launch_bounds__(256) near_few_kernel(NearArgs a) {
     const float pzf = (float)(pz - a.g.zlo);
     const float csxf = (float)a.g.csx, csyf = (float)a.g.csy, icsz = (float)(1.0 / a.g.csz);
     double phi = 0, ex = 0, ey = 0, ez = 0;
-    unsigned long long count = 0;
+    unsigned long long count = 0, hs = 0;
     const double Lx = a.g.Lx, Ly = a.g.Ly;
     for (int iy = 0; iy < cw.nyr; ++iy) {
         int yc; float sy, dyd;
@@ -799,6 +973,7 @@ __global__ void __launch_bounds__(256) near_few_kernel(NearArgs a) {
                         ex = fma(cq, dx, ex); ey = fma(cq, dy, ey); ez = fma(cq, dz, ez);
                     }
                     ++count;
+                    if (a.phash) hs += mix64((unsigned long long)a.orig[j]);
                 }
             }
         }
@@ -809,10 +984,15 @@ __global__ void __launch_bounds__(256) near_few_kernel(NearArgs a) {
         ey += __shfl_xor_sync(0xffffffffu, ey, o);
         ez += __shfl_xor_sync(0xffffffffu, ez, o);
         count += __shfl_xor_sync(0xffffffffu, count, o);
+        hs += __shfl_xor_sync(0xffffffffu, hs, o);
     }
     if (lane == 0) {
         red[0][warp] = phi; red[1][warp] = ex; red[2][warp] = ey; red[3][warp] = ez;
         redc[warp] = count;
+        if (a.phash) {                            // zeroed by the host
+            atomicAdd(a.phash + i, hs);
+            atomicAdd(a.phash + a.ne + i, count);
+        }
     }
     __syncthreads();
     if (tid == 0) {
@@ -861,6 +1041,10 @@ __global__ void near_boundary_kernel(NearArgs a) {
             atomicAdd(a.out + 3 * a.out_stride + i, cq * dz);
         }
         if (a.npairs) atomicAdd((unsigned long long*)a.npairs, 1ull);
+        if (a.phash) {
+            atomicAdd(a.phash + i, mix64((unsigned long long)a.orig[pr.y]));
+            atomicAdd(a.phash + a.ne + i, 1ull);
+        }
     }
 }
 
@@ -1250,6 +1434,10 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     a.zmarg = (float)(1e-6 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(p->cl.zlo)));
     a.out = d_out4; a.out_stride = ne;
     a.npairs = d_npairs;
+    a.orig = p->cl.orig;
+    // the pair-set record belongs to the charges' evaluation (d_npairs set)
+    a.phash = (d_npairs && p->pair_hash) ? p->d_phash : nullptr;
+    const bool hash = a.phash != nullptr;
     if (p->cl.n == 0) {
         SE_CUDA(cudaMemsetAsync(d_out4, 0, sizeof(double) * (k.need_field ? 4 : 1) * ne,
                                 p->stream));
@@ -1315,7 +1503,10 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         const unsigned nblk = (unsigned)((ne * 32 + NB_THREADS - 1) / NB_THREADS);
         a.use_ctab = close_ok ? 1 : 0;
         if (d_npairs) { p->ktic(3); p->ktic(4); p->ktoc(4); p->ktic(5); }
-        if (k.fp32) near_fused_kernel<true, 6><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        if (hash) {
+            if (k.fp32) near_fused_kernel<true, 6, false, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+            else near_fused_kernel<false, 6, false, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        } else if (k.fp32) near_fused_kernel<true, 6><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         else near_fused_kernel<false, 6><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         SE_LAUNCHED(p);
         near_boundary_kernel<<<4, 256, 0, p->stream>>>(a);
@@ -1339,6 +1530,24 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     a.ntask_dev = ns.toff + ncol;
     a.ntask = tcap;
     const unsigned nblk = (unsigned)((tcap * 32 + NB_THREADS - 1) / NB_THREADS);
+    static const char* fqenv = getenv("SE_NEAR_FQ");         // A/B: fused queue kernel
+    if (fqenv && atoi(fqenv)) {
+        a.use_ctab = close_ok ? 1 : 0;
+        if (d_npairs) { p->ktic(3); p->ktic(4); p->ktoc(4); p->ktic(5); }
+        if (hash) {
+            if (k.fp32) near_fq_kernel<true, true, 4, 4><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+            else near_fq_kernel<false, true, 4, 4><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        } else if (k.fp32) {
+            near_fq_kernel<true, false, 4, 4><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        } else {
+            near_fq_kernel<false, false, 4, 4><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        }
+        SE_LAUNCHED(p);
+        near_boundary_kernel<<<4, 256, 0, p->stream>>>(a);
+        if (d_npairs) { p->ktoc(5); p->ktoc(3); }
+        SE_LAUNCHED(p);
+        return;
+    }
     // pair-list capacities from the expected neighbour count (+ margin);
     // an overflow doubles them and reruns the scan
     const double vol_cell = p->cl.csx * p->cl.csy * p->cl.csz;
@@ -1390,15 +1599,25 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     if (d_npairs) p->ktoc(4);
     SE_LAUNCHED(p);
     if (d_npairs) p->ktic(5);
-    if (k.fp32) near_eval_kernel<true, 8, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
-    else near_eval_kernel<true, 8><<<nblk, NB_THREADS, 0, p->stream>>>(a);
-    SE_LAUNCHED(p);
     NearArgs ac = a;
     ac.use_ctab = close_ok ? 1 : 0;
-    near_eval_kernel<false, 6><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
-    SE_LAUNCHED(p);
-    if (k.fp32) near_fused_kernel<true, 6, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
-    else near_fused_kernel<false, 6, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
+    if (hash) {
+        if (k.fp32) near_eval_kernel<true, 8, true, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        else near_eval_kernel<true, 8, false, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        SE_LAUNCHED(p);
+        near_eval_kernel<false, 6, false, true><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
+        SE_LAUNCHED(p);
+        if (k.fp32) near_fused_kernel<true, 6, true, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
+        else near_fused_kernel<false, 6, true, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
+    } else {
+        if (k.fp32) near_eval_kernel<true, 8, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        else near_eval_kernel<true, 8><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        SE_LAUNCHED(p);
+        near_eval_kernel<false, 6><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
+        SE_LAUNCHED(p);
+        if (k.fp32) near_fused_kernel<true, 6, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
+        else near_fused_kernel<false, 6, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
+    }
     SE_LAUNCHED(p);
     SE_CUDA(cudaMemcpyAsync(L.h_ovf, L.ovf, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
     near_boundary_kernel<<<4, 256, 0, p->stream>>>(a);

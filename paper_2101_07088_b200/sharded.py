@@ -37,6 +37,27 @@ from . import _lib
 from .slab import STAGES, SlabSolver, SolveResult, _flags
 
 
+# exception type <-> the library's error codes (include/slabewald.h), so a
+# failure seen by one rank is raised with the same type on every rank
+_ERR_TYPES = ((ValueError, _lib.SE_ERR_VALUE), (FloatingPointError, _lib.SE_ERR_FLOAT),
+              (np.linalg.LinAlgError, _lib.SE_ERR_LINALG), (MemoryError, _lib.SE_ERR_MEMORY),
+              (RuntimeError, _lib.SE_ERR_CUDA))
+
+
+def _error_code(exc):
+    for typ, code in _ERR_TYPES:
+        if isinstance(exc, typ):
+            return code
+    return _lib.SE_ERR_CUDA
+
+
+def _error_type(code):
+    for typ, c in _ERR_TYPES:
+        if c == code:
+            return typ
+    return RuntimeError
+
+
 def shard_range(n, rank, world):
     """Contiguous index range [first, first + count) of ``rank``."""
     first = (n * rank) // world
@@ -185,8 +206,18 @@ class ShardedSlabSolver:
             if self.world > 1:
                 dist.all_reduce(rho, group=self.group)
             self.engine.fields()
-        phi, E, u_part, diag = self.engine.charges(pos_all, self.count,
-                                                   need_forces)
+        # Some input errors are detected by one rank only (a charge of its own
+        # shard outside the z domain, its own near-field buffers): agree on
+        # the outcome before the next collective, so every rank raises the
+        # same exception instead of the others blocking in the all-reduce.
+        try:
+            phi, E, u_part, diag = self.engine.charges(pos_all, self.count,
+                                                       need_forces)
+            err = None
+        except (ValueError, FloatingPointError, ArithmeticError, MemoryError,
+                RuntimeError) as exc:
+            err = exc
+        self._agree(err)
         U = u_part
         if self.world > 1:
             u = torch.tensor([u_part], dtype=torch.float64, device=phi.device)
@@ -195,6 +226,22 @@ class ShardedSlabSolver:
         if timings and hasattr(diag, "t_ms"):
             self.last_timings = dict(zip(STAGES, list(diag.t_ms)[:len(STAGES)]))
         return phi, E, U, diag
+
+    def _agree(self, err):
+        """All-reduce (MAX) the error code of this rank's phase; raise the
+        local exception, or one of the same type naming the failing rank."""
+        code = _error_code(err) if err is not None else 0
+        if self.world > 1:
+            dev = self.engine.device if dist.get_backend(self.group) == "nccl" \
+                else torch.device("cpu")
+            t = torch.tensor([code, self.rank if code else -1], dtype=torch.int64,
+                             device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+            if err is None and int(t[0]) != 0:
+                raise _error_type(int(t[0]))(
+                    "sharded solve failed on rank %d (see that rank's error)" % int(t[1]))
+        if err is not None:
+            raise err
 
     def _grid_pipeline_distributed(self):
         """Reduce-scatter of the spread grids into z slabs, xy FFT, all-to-all

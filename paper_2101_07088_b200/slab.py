@@ -68,8 +68,11 @@ class SolveResult:
 
 
 def _flags(need_energy, need_forces, need_potential, subtract_self,
-           include_correction, force_general, timings=False, fp32=False):
+           include_correction, force_general, timings=False, fp32=False,
+           record_pairs=False):
     f = 0
+    if record_pairs:
+        f |= _lib.PAIR_HASH
     if fp32:
         f |= _lib.FP32
     if need_energy:
@@ -199,14 +202,16 @@ class SlabSolver:
 
     def solve(self, positions=None, need_energy=True, need_forces=True,
               need_potential=True, subtract_self=False,
-              include_correction=True, force_general=False, timings=False):
+              include_correction=True, force_general=False, timings=False,
+              record_pairs=False):
         """Averaged potential and field at every charge, and the energy
-        (reference slab.py:259-394)."""
+        (reference slab.py:259-394).  ``record_pairs`` (not in the reference)
+        keeps the near-field pair set for :meth:`pair_set`."""
         pos = self._positions(positions)
         n = pos.shape[0]
         flags = _flags(need_energy, need_forces, need_potential,
                        subtract_self, include_correction, force_general,
-                       timings, self.precision == "fp32")
+                       timings, self.precision == "fp32", record_pairs)
         phi, E = _host_outputs(n, need_forces)
         U = ctypes.c_double(0.0)
         diag = _lib.SeDiag()
@@ -245,6 +250,23 @@ class SlabSolver:
         ``torch.cuda.current_stream().cuda_stream``)."""
         _lib.check(self._lib.se_plan_set_stream(self._plan,
                                                 ctypes.c_void_p(stream_handle)))
+
+    def pair_set(self):
+        """(count[N], hash[N]) of the near-field pairs of the last solve run
+        with ``record_pairs=True``: per charge the number of its sources
+        within r_cut and the wrap-around sum of splitmix64(source index),
+        sources numbered as the reference's NearField (charges, bottom
+        mirror layer, top mirror layer; slab.py:104-119)."""
+        size = self._lib.se_debug_fetch(self._plan, 6, None, 0)
+        if size <= 0:
+            raise RuntimeError("no pair set recorded (solve with record_pairs=True)")
+        buf = np.empty(size // 8, dtype=np.uint64)
+        got = self._lib.se_debug_fetch(self._plan, 6,
+                                       buf.ctypes.data_as(ctypes.c_void_p), size)
+        if got != size:
+            raise RuntimeError("pair set copy failed")
+        n = buf.size // 2
+        return buf[n:].astype(np.int64), buf[:n].copy()
 
     def debug_fetch(self, which):
         """Copy a stage buffer of the last solve (see se_debug_fetch)."""
@@ -289,8 +311,18 @@ def build_partition(positions, charges, geometry, params):
 
 
 def near_field_sum(positions, charges, geometry, params, eval_positions=None,
-                   kind="avg", need_field=True, subtract_unsplit_self=False):
-    """Near-field pair sums on the device (reference slab.py:184-191)."""
+                   kernel="avg", need_field=True, subtract_unsplit_self=False,
+                   **deprecated):
+    """Near-field pair sums on the device (reference slab.py:184-191, same
+    signature: ``kernel`` is "avg" (r_cut) or "point" (r_nf)).  The earlier
+    keyword ``kind`` is accepted as an alias."""
+    if deprecated:
+        if set(deprecated) != {"kind"}:
+            raise TypeError("near_field_sum() got unexpected keyword(s) %s"
+                            % sorted(set(deprecated) - {"kind"}))
+        kernel = deprecated["kind"]
+    if kernel not in ("avg", "point"):
+        raise ValueError("kernel must be 'avg' or 'point'")
     lib = _lib.load()
     pos = _lib.as_f64(np.atleast_2d(positions)).reshape(-1, 3)
     q = _lib.as_f64(charges).reshape(-1)
@@ -302,7 +334,7 @@ def near_field_sum(positions, charges, geometry, params, eval_positions=None,
     ps = _lib.params_struct(geometry, params)
     _lib.check(lib.se_near_field(
         ctypes.byref(ps), 0, _lib.dptr(pos), _lib.dptr(q), pos.shape[0],
-        _lib.dptr(ev), ne, 0 if kind == "avg" else 1, 1 if need_field else 0,
+        _lib.dptr(ev), ne, 0 if kernel == "avg" else 1, 1 if need_field else 0,
         1 if subtract_unsplit_self else 0, _lib.dptr(phi),
         _lib.dptr(E) if need_field else None))
     return (phi, E) if need_field else phi

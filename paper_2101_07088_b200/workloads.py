@@ -30,6 +30,11 @@ WORKLOADS = {
     "c4": dict(L=2.0, H=1.0, eps_b=0.05, eps_t=0.05,
                g_w=0.25 * 1.4 * 2.0 / 256, delta=1e-4, Nxy=256, N=1 << 20,
                seed=0),
+    # C4 density and grid spacing in a 0.5 x 0.5 box: the same h, Nz = 258,
+    # ~575 near pairs per charge, at a size the CPU reference finishes
+    "c4d": dict(L=0.5, H=1.0, eps_b=0.05, eps_t=0.05,
+                g_w=0.25 * 1.4 * 2.0 / 256, delta=1e-4, Nxy=64, N=1 << 16,
+                seed=0),
     "c5": dict(L=8.0, H=1.0, eps_b=0.05, eps_t=0.05,
                g_w=0.25 * 1.4 * 2.0 / 256, delta=1e-4, Nxy=1024,
                N=1 << 24, seed=0),

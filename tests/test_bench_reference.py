@@ -30,6 +30,17 @@ def test_reference_arm_json_line():
     cb = line["cpu_baseline"]
     assert cb["kind"] == "port" and cb["value"] == line["value"]
     assert cb["cores"] == len(os.sched_getaffinity(0))
+    # the same config dict as the GPU arm (bench.bench_config), so the
+    # driver can match the two lines
+    sys.path.insert(0, REPO)
+    import bench
+    from paper_2101_07088_b200 import workloads as W
+    system, params = W.build("c2")
+
+    class A:
+        config, replicate_grid = "c2", False
+    assert line["config"] == json.loads(json.dumps(bench.bench_config(A, system, params)))
+    assert line["extrapolated"] is True and line["sample_wall_s"]["total"] > 0
 
 
 def test_cpu_bench_workers_match_single_thread_grid():

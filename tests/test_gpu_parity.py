@@ -184,12 +184,16 @@ def test_near_field_sum_against_oracle():
     geo = system.geometry
     ev = np.random.default_rng(4).uniform([0, 0, 0.05], [2, 2, 0.95], (300, 3))
     nf = O.NearSources(system.positions, system.charges, geo, params)
-    for kind in ("avg", "point"):
+    for kernel in ("avg", "point"):
+        # the reference's keyword (slab.py:184-186), positional order too
         phi, E = near_field_sum(system.positions, system.charges, geo, params,
-                                eval_positions=ev, kind=kind)
-        rphi, rE = nf.evaluate(ev, kind)
+                                ev, kernel)
+        phi2, E2 = near_field_sum(system.positions, system.charges, geo,
+                                  params, eval_positions=ev, kernel=kernel)
+        rphi, rE = nf.evaluate(ev, kernel)
         assert rel_l2(phi, rphi) < 1e-13
         assert rel_l2(E, rE) < 1e-13
+        assert np.array_equal(phi, phi2) and np.array_equal(E, E2)
     phi = near_field_sum(system.positions, system.charges, geo, params,
                          need_field=False, subtract_unsplit_self=True)
     rphi = nf.evaluate(system.positions, "avg", need_field=False,

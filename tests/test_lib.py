@@ -46,3 +46,19 @@ def test_solver_fails_loudly_without_library(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(RuntimeError, match="not built"):
         _lib.load()
+
+
+def test_near_field_sum_signature_matches_reference():
+    """near_field_sum(positions, charges, geometry, params, eval_positions,
+    kernel, need_field, subtract_unsplit_self) as reference slab.py:184-186;
+    argument checks happen before any device work."""
+    import inspect
+    import pytest
+    from paper_2101_07088_b200.slab import near_field_sum
+    names = list(inspect.signature(near_field_sum).parameters)
+    assert names[:8] == ["positions", "charges", "geometry", "params", "eval_positions",
+                         "kernel", "need_field", "subtract_unsplit_self"]
+    with pytest.raises(ValueError):
+        near_field_sum(None, None, None, None, kernel="gauss")
+    with pytest.raises(TypeError):
+        near_field_sum(None, None, None, None, kern="avg")

@@ -3,7 +3,7 @@ the host logic of ``ShardedSlabSolver`` on CPU over ``gloo`` with
 world_size 2 and 3, each rank's phases computed by the oracle engine.  The
 result must equal the unsharded solve (and the reference's golden output)
 up to the summation order of the grids.  The GPU engine is covered by
-``test_gpu_parity.py::test_sharded_single_rank``."""
+``test_gpu_parity.py::test_sharded_solver_one_rank``."""
 
 import os
 import pickle
@@ -129,3 +129,50 @@ def test_distributed_grid_pipeline_plumbing(tmp_path, world):
              nprocs=world, join=True)
     for r in range(world):
         assert (tmp_path / ("dist%d.txt" % r)).read_text() == "ok"
+
+
+def _fault_worker(rank, world, port, outdir):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    for p in (here, os.path.dirname(here)):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    from _oracle_engine import OracleShardEngine
+    from test_oracle_golden import variant_problem
+
+    class FaultyEngine(OracleShardEngine):
+        """Rank 1 finds a charge of its own shard outside the z domain in
+        its charge phase (the library reports FLAG_Z_OUTSIDE there)."""
+        def charges(self, pos_all, count, need_forces):
+            if dist.get_rank() == 1:
+                raise ValueError("point outside the extended z domain")
+            return super().charges(pos_all, count, need_forces)
+
+    dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % port,
+                            rank=rank, world_size=world)
+    try:
+        system, params, kw = variant_problem("c2n256")
+        solver = ShardedSlabSolver(system, params,
+                                   engine=FaultyEngine(system, params))
+        try:
+            solver.solve()
+            res = "no error"
+        except ValueError as exc:
+            res = "ValueError: %s" % exc
+        with open(os.path.join(outdir, "fault%d.txt" % rank), "w") as f:
+            f.write(res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_error_on_one_rank_raises_everywhere(tmp_path):
+    """An error seen by one rank only is raised, with the same exception
+    type, on every rank instead of leaving the others in a collective."""
+    world = 3
+    mp.spawn(_fault_worker, args=(world, _free_port(), str(tmp_path)),
+             nprocs=world, join=True, daemon=False)
+    for r in range(world):
+        txt = (tmp_path / ("fault%d.txt" % r)).read_text()
+        assert txt.startswith("ValueError"), (r, txt)
+    assert "outside the extended z domain" in (tmp_path / "fault1.txt").read_text()
+    assert "rank 1" in (tmp_path / "fault0.txt").read_text()
