@@ -51,7 +51,7 @@ def build(force=False, verbose=False):
         if res.returncode != 0:
             raise RuntimeError("nvcc failed compiling %s" % obj)
     cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *[o for o, _ in results],
-           "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcufft", "-lcublas",
+           "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcufft",
            "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

@@ -644,9 +644,6 @@ int se_plan_create(const se_params* params, const double* z_nodes, const double*
         make_plan2d(&p->fft_fwd2, p->Nx, p->Ny, p->Nyh, CUFFT_D2Z, p->NXY, p->M, 2 * nz, p->stream);
         make_plan2d(&p->fft_inv4, p->Nx, p->Ny, p->Nyh, CUFFT_Z2D, p->M, p->NXY, 4 * nz, p->stream);
         make_plan2d(&p->fft_inv1, p->Nx, p->Ny, p->Nyh, CUFFT_Z2D, 4 * p->M, 4 * p->NXY, nz, p->stream);
-        SE_CUBLAS(cublasCreate(&p->blas));
-        SE_CUBLAS(cublasSetStream(p->blas, p->stream));
-        SE_CUBLAS(cublasSetMathMode(p->blas, CUBLAS_DEFAULT_MATH));
         SE_CUDA(cudaStreamSynchronize(p->stream));
         *out = reinterpret_cast<se_plan*>(p);
         return SE_OK;
@@ -667,7 +664,6 @@ void se_plan_destroy(se_plan* plan) {
     cufftHandle hs[] = {p->fft_fwd2, p->fft_fwd1, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig,
                         p->fft_fwd_slab, p->fft_inv4_slab, p->fft_inv1_slab};
     for (auto h : hs) if (h) cufftDestroy(h);
-    if (p->blas) cublasDestroy(p->blas);
     for (auto& b : p->owned) if (b.p) cudaFree(b.p);
     if (p->nl.h_ovf) cudaFreeHost(p->nl.h_ovf);
     for (auto& pr : p->kev) { if (pr[0]) cudaEventDestroy(pr[0]); if (pr[1]) cudaEventDestroy(pr[1]); }
@@ -686,7 +682,6 @@ int se_plan_set_stream(se_plan* plan, void* stream) {
         cufftHandle hs[] = {p->fft_fwd2, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig,
                             p->fft_fwd_slab, p->fft_inv4_slab, p->fft_inv1_slab};
         for (auto h : hs) if (h) SE_CUFFT(cufftSetStream(h, p->stream));
-        if (p->blas) SE_CUBLAS(cublasSetStream(p->blas, p->stream));
         return SE_OK;
     } catch (const Error& e) {
         return fail(e);

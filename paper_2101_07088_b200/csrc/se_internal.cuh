@@ -3,11 +3,9 @@
 // Data layout in HBM (z slowest, SURVEY.md section 7 "design decisions"):
 //   rho    [Nz][2][Nx][Ny]        real spread grids, slot 0 = rho_over,
 //                                 slot 1 = rho_in            (slab.py:282-289)
-//   ext    [2N][2][Nx][Ny/2+1]    complex, N = Nz-1: even extension in z of
-//                                 the xy half spectra; a batched length-2N
-//                                 FFT along z turns it into the DCT-I
-//                                 (cheb_transform / cheb_inverse,
-//                                 chebyshev.py:46-65)
+//   ext    [Nz][2][Nx][Ny/2+1]    complex: Chebyshev coefficients of the
+//                                 xy half spectra (DCT-I along z, hand-written
+//                                 FP64 tensor-core kernels, chebyshev.py:46-65)
 //   spec4  [Nz][4][Nx][Ny/2+1]    psi, ikx psi, iky psi, dpsi/dz mode values
 //   fields [Nz][4][Nx][Ny]        real field grids after the inverse xy FFT
 // Sources for spreading are sorted by (xy bin, class, first z node) so one
@@ -16,7 +14,6 @@
 
 #include <cuda_runtime.h>
 #include <cufft.h>
-#include <cublas_v2.h>
 
 #include <cstdint>
 #include <stdexcept>
@@ -52,15 +49,6 @@ struct Error : std::runtime_error {
             throw ::se::Error(SE_ERR_CUDA, std::string(#call) +              \
                                                ": cufft error " +            \
                                                std::to_string((int)r_));     \
-    } while (0)
-
-#define SE_CUBLAS(call)                                                      \
-    do {                                                                     \
-        cublasStatus_t s_ = (call);                                          \
-        if (s_ != CUBLAS_STATUS_SUCCESS)                                     \
-            throw ::se::Error(SE_ERR_CUDA, std::string(#call) +              \
-                                               ": cublas error " +           \
-                                               std::to_string((int)s_));     \
     } while (0)
 
 #define SE_LAUNCHED(plan)                                                    \
@@ -309,8 +297,8 @@ struct Plan {
     double* d_rho = nullptr;              // [Nz][2][Nx][Ny]
     cufftDoubleComplex* d_ext = nullptr;  // [Nz][2][M] Chebyshev coefficients
     cufftDoubleComplex* d_hat = nullptr;  // [Nz][2][M] xy spectra / iDCT values
-    double *d_dct_fwd = nullptr, *d_dct_inv = nullptr;   // [Nz][Nz] column-major
-    cublasHandle_t blas = nullptr;
+    double *d_dct_fwd = nullptr, *d_dct_inv = nullptr;   // [2][P8][P4] row-major
+    int dct_p8 = 0, dct_p4 = 0;           // padded parity block (8-row tiles, k by 4)
     cufftDoubleComplex* d_spec = nullptr; // [Nz][4][M]
     double* d_fields = nullptr;           // [Nz][4][Nx][Ny]
     cufftDoubleComplex* d_scr = nullptr;  // BVP scratch [3][Nz][M]

@@ -10,8 +10,11 @@
 // B200 design.  The xy transforms are batched cuFFT D2Z / C2R over the
 // Chebyshev planes of the z-slowest layout.  The DCT-I along z (Nz = 258 at
 // the north-star size, 2(Nz-1) = 2*257: Bluestein for an FFT) is a matrix
-// product over all modes at once: folded by the node reflection into two
-// half-order DGEMMs (even / odd coefficient rows) on the FP64 tensor pipe.
+// product over all modes at once, folded by the node reflection into two
+// half-order products (even / odd coefficient rows) that hand-written
+// kernels run on the FP64 tensor pipe (mma.sync m8n8k4): the fold is fused
+// into the forward kernel's staging, the node recombination, harmonic
+// correction and i k multipliers into the inverse kernel's epilogue.
 // The BVP is a lane pair per (kx, ky) mode of the half spectrum (over /
 // in-slab grid): sweeps along z touch row n of all modes together, so every
 // global access is coalesced across the warp; factors are precomputed per
@@ -20,6 +23,7 @@
 // into the same kernel (a mode needs only its own wall values), and the
 // correction values themselves are evaluated on the fly while assembling
 // the four spectral fields, so no (mode x node) correction table is stored.
+#include <algorithm>
 #include <cmath>
 
 #include "se_internal.cuh"
@@ -474,59 +478,240 @@ __global__ void __launch_bounds__(64) bvp_kernel(BvpArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// assemble the spectral fields at the nodes: values + correction, and the
-// ik multipliers (Nyquist zeroed)                       slab.py:223-230,335-353
+// z DCT-I (chebyshev.py:46-65) as hand-written FP64 tensor-core products.
+// With the node reflection j -> N - j the (Nz x Nz) transform splits into
+// an even-coefficient half acting on s_c = v_c + v_{N-c} and an odd half
+// acting on d_c = v_c - v_{N-c}, each of order ~Nz/2 (half the flops).
+// A CTA owns DCT_COLS real columns (of the [Nz][W] row layout, W = 4 M:
+// two grids x M modes x re/im) for all Nz rows: the folded / coefficient
+// columns are staged in shared memory column-major (k contiguous, so the
+// B fragments of mma.sync.m8n8k4 are bank-conflict free), the transform
+// matrices (zero-padded to multiples of 8 x 4, row-major, L2 resident) feed
+// the A fragments.  8 warps: warp w computes parity w / 4 and a quarter of
+// its 8-row tiles against all DCT_COLS columns.
 // ---------------------------------------------------------------------------
-struct AsmArgs {
-    const double2* ext; double2* spec; const double2* mom;
-    const double* kx; const double* ky; const double* kmag; const unsigned char* sel;
-    const double* z; int Nz, Nx, Ny, Nyh; int64_t M;
-    int64_t Mv, m0;              // valid modes, global index of local mode 0
-    int w0, w1;                  // correction window [w0, w1)
-    int corr, forces;
+constexpr int DCT_COLS = 32;
+constexpr int DCT_MT = 20;                 // max m-tiles per parity (Nz <= 320)
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
+
+struct DctArgs {
+    int n, Pe, Po, P8, P4;       // Nz, parity sizes, padded rows / k
+    int64_t W;                   // real columns per row
+    const double* De; const double* Do;    // [P8][P4] row-major, zero padded
+};
+
+// C[mt0*8 + 0:MW*8][0:DCT_COLS] = D[rows][k] * S[k][cols] for this warp's
+// parity and half of the row tiles: per k step MW A fragments (global, L2
+// resident matrix; prefetched one step ahead) and 4 B fragments (shared)
+// feed 4 MW DMMAs.
+template <int MW>
+__device__ __forceinline__ void dct_mma(const double* __restrict__ D, int P4, int mrows,
+                                        const double* __restrict__ Sc, int lane, int mt0,
+                                        double (&acc)[MW][4][2]) {
+#pragma unroll
+    for (int mt = 0; mt < MW; ++mt)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[mt][t][0] = acc[mt][t][1] = 0.0;
+    const int ar = lane >> 2, ak = lane & 3;
+    const double* bp = Sc + ar * P4 + ak;                    // column-major [col][k]
+    const double* ap = D + (mt0 * 8 + ar) * P4 + ak;
+    double an[MW];
+#pragma unroll
+    for (int mt = 0; mt < MW; ++mt)
+        an[mt] = (mt0 + mt) * 8 < mrows ? __ldg(ap + (mt * 8) * P4) : 0.0;
+    for (int k0 = 0; k0 < P4; k0 += 4) {
+        double av[MW];
+#pragma unroll
+        for (int mt = 0; mt < MW; ++mt) av[mt] = an[mt];
+        if (k0 + 4 < P4) {
+#pragma unroll
+            for (int mt = 0; mt < MW; ++mt)
+                an[mt] = (mt0 + mt) * 8 < mrows ? __ldg(ap + (mt * 8) * P4 + k0 + 4) : 0.0;
+        }
+        double bv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) bv[t] = bp[t * 8 * P4 + k0];
+#pragma unroll
+        for (int mt = 0; mt < MW; ++mt)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) dmma884(acc[mt][t], av[mt], bv[t]);
+    }
+}
+
+// forward: hat rows [n][W] (xy spectra per plane) -> ext rows [n][W]
+// (Chebyshev coefficient n in row n, unnormalised as the GEMM form was)
+template <int MT>
+__global__ void __launch_bounds__(256, 2) zdct_fwd_kernel(DctArgs a, const double* __restrict__ in,
+                                                         double* __restrict__ out) {
+    extern __shared__ double sm[];
+    double* Se = sm;                                   // [DCT_COLS][P4]
+    double* So = sm + DCT_COLS * a.P4;
+    const int64_t w0 = (int64_t)blockIdx.x * DCT_COLS;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int N = a.n - 1;
+    // fold (s_c, d_c) while staging: lanes run along the columns (coalesced);
+    // STG_U items per thread are loaded before any is stored, so 2 STG_U
+    // loads are in flight per thread
+    constexpr int STG_U = 6;
+    const int total = a.P4 * DCT_COLS;
+    for (int base = 0; base < total; base += 256 * STG_U) {
+        double xv[STG_U], yv[STG_U];
+#pragma unroll
+        for (int u = 0; u < STG_U; ++u) {
+            const int e = base + u * 256 + tid;
+            const int c = e / DCT_COLS, col = e - c * DCT_COLS;
+            const int64_t w = w0 + col;
+            const bool ok = e < total && w < a.W && c < a.Pe;
+            xv[u] = ok ? in[(int64_t)c * a.W + w] : 0.0;
+            yv[u] = (ok && c < a.Po) ? in[(int64_t)(N - c) * a.W + w] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < STG_U; ++u) {
+            const int e = base + u * 256 + tid;
+            if (e < total) {
+                const int c = e / DCT_COLS, col = e - c * DCT_COLS;
+                Se[col * a.P4 + c] = xv[u] + yv[u];
+                So[col * a.P4 + c] = xv[u] - yv[u];
+            }
+        }
+    }
+    __syncthreads();
+    constexpr int MW = (MT + 3) / 4;
+    const int par = warp >> 2, mt0 = (warp & 3) * MW;
+    const int rows = par ? a.Po : a.Pe;
+    double acc[MW][4][2];
+    dct_mma<MW>(par ? a.Do : a.De, a.P4, a.P8, par ? So : Se, lane, mt0, acc);
+#pragma unroll
+    for (int mt = 0; mt < MW; ++mt) {
+        const int i = (mt0 + mt) * 8 + (lane >> 2);
+        if (i >= rows) continue;
+        const int64_t row = 2 * (int64_t)i + par;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int64_t w = w0 + t * 8 + 2 * (lane & 3);
+            if (w + 1 < a.W)
+                *reinterpret_cast<double2*>(out + row * a.W + w) =
+                    make_double2(acc[mt][t][0], acc[mt][t][1]);
+            else if (w < a.W)
+                out[row * a.W + w] = acc[mt][t][0];
+        }
+    }
+}
+
+// inverse + assembly: the iDCT of the psi and dpsi/dz coefficient columns of
+// DCT_COLS / 4 modes (ext rows [n][W]: slot 0 = psi, slot 1 = dpsi at column
+// offset 2 M), the node values v_j = E_j + O_j, v_{N-j} = E_j - O_j, the
+// harmonic correction on the fly and the i k multipliers -> spec [n][4][M]
+// (slab.py:335-353)
+struct AsmArgs2 {
+    const double2* mom; const double* kx; const double* ky; const double* kmag;
+    const unsigned char* sel; const double* z;
+    int Nx, Ny, Nyh; int64_t M, Mv, m0;
+    int w0, w1, corr, forces;
     double rb, rt, H;
 };
 
-__global__ void assemble_kernel(AsmArgs a) {
-    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= (int64_t)a.Nz * a.M) return;
-    int j = (int)(e / a.M);
-    int64_t m = e % a.M;
-    if (m >= a.Mv) return;
-    const int64_t RS = 2 * a.M;
-    // iDCT halves: value at node j = E_j + O_j, at node N - j = E_j - O_j
-    const int Pe = (a.Nz + 1) / 2, Po = a.Nz / 2;
-    const int r = (j < Pe) ? j : a.Nz - 1 - j;
-    const double2* E = a.ext + (int64_t)r * RS + m;
-    double2 v = E[0], d = E[a.M];
-    if (r < Po) {
-        const double2* O = a.ext + (int64_t)(Pe + r) * RS + m;
-        const double2 ov = O[0], od = O[a.M];
-        v = (j < Pe) ? cadd(v, ov) : csub(v, ov);
-        d = (j < Pe) ? cadd(d, od) : csub(d, od);
+template <int MT>
+__global__ void __launch_bounds__(256, 2) zdct_inv_kernel(DctArgs a, AsmArgs2 q,
+                                                         const double* __restrict__ ext,
+                                                         double2* __restrict__ spec) {
+    extern __shared__ double sm[];
+    constexpr int MPB = DCT_COLS / 4;                  // modes per CTA
+    double* Ce = sm;                                   // [DCT_COLS][P4] even coefficients
+    double* Co = sm + DCT_COLS * a.P4;                 // odd
+    const int64_t mb = (int64_t)blockIdx.x * MPB;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // column col: slot = col / 16 (psi, dpsi), mode mb + (col % 16) / 2, re/im
+    constexpr int STG_U = 6;
+    const int total = a.P4 * DCT_COLS;
+    for (int base = 0; base < total; base += 256 * STG_U) {
+        double cev[STG_U], cov[STG_U];
+#pragma unroll
+        for (int u = 0; u < STG_U; ++u) {
+            const int e = base + u * 256 + tid;
+            const int i = e / DCT_COLS, col = e - i * DCT_COLS;
+            const int slot = col >> 4, r = col & 15;
+            const int64_t m = mb + (r >> 1);
+            const int64_t w = slot * 2 * q.M + 2 * m + (r & 1);
+            const bool ok = e < total && m < q.Mv;
+            cev[u] = (ok && i < a.Pe) ? ext[(2 * (int64_t)i) * a.W + w] : 0.0;
+            cov[u] = (ok && i < a.Po) ? ext[(2 * (int64_t)i + 1) * a.W + w] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < STG_U; ++u) {
+            const int e = base + u * 256 + tid;
+            if (e < total) {
+                const int i = e / DCT_COLS, col = e - i * DCT_COLS;
+                Ce[col * a.P4 + i] = cev[u];
+                Co[col * a.P4 + i] = cov[u];
+            }
+        }
     }
-    if (a.corr && a.sel[m] && j >= a.w0 && j < a.w1) {
-        double k = a.kmag[m], z = a.z[j];
-        double e1 = exp(-k * z), e2 = exp(k * (z - a.H));
-        double e3 = exp(-k * (a.H + z)), e4 = exp(k * (z - 2.0 * a.H));
-        double pb = (a.rt + 1.0) * e1 - (a.rt - 1.0) * e4;
-        double pt = -(a.rb + 1.0) * e2 + (a.rb - 1.0) * e3;
-        double db = -k * ((a.rt + 1.0) * e1 + (a.rt - 1.0) * e4);
-        double dt = -k * ((a.rb + 1.0) * e2 + (a.rb - 1.0) * e3);
-        double2 mb = a.mom[2 * m], mt = a.mom[2 * m + 1];
-        v = cadd(v, cadd(cscale(mb, pb), cscale(mt, pt)));
-        d = cadd(d, cadd(cscale(mb, db), cscale(mt, dt)));
+    __syncthreads();
+    constexpr int MW = (MT + 3) / 4;
+    const int par = warp >> 2, mt0 = (warp & 3) * MW;
+    double acc[MW][4][2];
+    dct_mma<MW>(par ? a.Do : a.De, a.P4, a.P8, par ? Co : Ce, lane, mt0, acc);
+    __syncthreads();                                   // coefficients consumed
+    // E (par 0) / O (par 1) node halves back to shared memory, row-major
+    double* EO = sm;                                   // [2][P8][DCT_COLS]
+#pragma unroll
+    for (int mt = 0; mt < MW; ++mt) {
+        const int j = (mt0 + mt) * 8 + (lane >> 2);
+        if (j >= a.P8) continue;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int col = t * 8 + 2 * (lane & 3);
+            double* dst = EO + ((int64_t)par * a.P8 + j) * DCT_COLS + col;
+            dst[0] = acc[mt][t][0];
+            dst[1] = acc[mt][t][1];
+        }
     }
-    double2* out = a.spec + (int64_t)j * 4 * a.M + m;
-    out[0] = v;
-    if (a.forces) {
-        const int64_t gm = a.m0 + m;
-        int ix = (int)(gm / a.Nyh), iy = (int)(gm % a.Nyh);
-        double ikx = (a.Nx % 2 == 0 && ix == a.Nx / 2) ? 0.0 : a.kx[ix];
-        double iky = (a.Ny % 2 == 0 && iy == a.Ny / 2) ? 0.0 : a.ky[iy];
-        out[a.M] = make_double2(-ikx * v.y, ikx * v.x);        // i kx v
-        out[2 * a.M] = make_double2(-iky * v.y, iky * v.x);    // i ky v
-        out[3 * a.M] = d;
+    __syncthreads();
+    const int N = a.n - 1;
+    for (int e = tid; e < a.n * MPB; e += blockDim.x) {
+        const int j = e / MPB, mi = e - j * MPB;
+        const int64_t m = mb + mi;
+        if (m >= q.Mv) continue;
+        const bool lo = j < a.Pe;
+        const int r = lo ? j : N - j;
+        const double* Er = EO + (int64_t)r * DCT_COLS;
+        const double* Or = EO + ((int64_t)a.P8 + r) * DCT_COLS;
+        double2 v = make_double2(Er[2 * mi], Er[2 * mi + 1]);
+        double2 d = make_double2(Er[16 + 2 * mi], Er[16 + 2 * mi + 1]);
+        if (r < a.Po) {
+            const double2 ov = make_double2(Or[2 * mi], Or[2 * mi + 1]);
+            const double2 od = make_double2(Or[16 + 2 * mi], Or[16 + 2 * mi + 1]);
+            v = lo ? cadd(v, ov) : csub(v, ov);
+            d = lo ? cadd(d, od) : csub(d, od);
+        }
+        if (q.corr && q.sel[m] && j >= q.w0 && j < q.w1) {
+            const double k = q.kmag[m], z = q.z[j];
+            const double e1 = exp(-k * z), e2 = exp(k * (z - q.H));
+            const double e3 = exp(-k * (q.H + z)), e4 = exp(k * (z - 2.0 * q.H));
+            const double pb = (q.rt + 1.0) * e1 - (q.rt - 1.0) * e4;
+            const double pt = -(q.rb + 1.0) * e2 + (q.rb - 1.0) * e3;
+            const double db = -k * ((q.rt + 1.0) * e1 + (q.rt - 1.0) * e4);
+            const double dt = -k * ((q.rb + 1.0) * e2 + (q.rb - 1.0) * e3);
+            const double2 mbv = q.mom[2 * m], mtv = q.mom[2 * m + 1];
+            v = cadd(v, cadd(cscale(mbv, pb), cscale(mtv, pt)));
+            d = cadd(d, cadd(cscale(mbv, db), cscale(mtv, dt)));
+        }
+        double2* out = spec + (int64_t)j * 4 * q.M + m;
+        out[0] = v;
+        if (q.forces) {
+            const int64_t gm = q.m0 + m;
+            const int ix = (int)(gm / q.Nyh), iy = (int)(gm % q.Nyh);
+            const double ikx = (q.Nx % 2 == 0 && ix == q.Nx / 2) ? 0.0 : q.kx[ix];
+            const double iky = (q.Ny % 2 == 0 && iy == q.Ny / 2) ? 0.0 : q.ky[iy];
+            out[q.M] = make_double2(-ikx * v.y, ikx * v.x);        // i kx v
+            out[2 * q.M] = make_double2(-iky * v.y, iky * v.x);    // i ky v
+            out[3 * q.M] = d;
+        }
     }
 }
 
@@ -592,16 +777,22 @@ void factor_bvp(Plan* p) {
             const long long nm = (long long)c * (N - r) % (2 * N);
             return std::cos(M_PI * (double)nm / N);
         };
-        // column-major: FEE (Pe x Pe), FOO (Po x Po), IEE (Pe x Pe), IOO (Po x Po)
-        std::vector<double> F((size_t)Pe * Pe + (size_t)Po * Po), I(F.size());
+        // row-major, zero padded to P8 rows x P4 columns (the DMMA tiles):
+        // forward even / odd (coefficient rows, folded-node columns) and
+        // inverse even / odd (node rows, coefficient columns)
+        const int P8 = ((Pe + 7) / 8) * 8, P4 = ((Pe + 3) / 4) * 4;
+        if (P8 / 8 > DCT_MT) throw Error(SE_ERR_VALUE, "Nz too large for the z transform kernels");
+        p->dct_p8 = P8; p->dct_p4 = P4;
+        const size_t blk = (size_t)P8 * P4;
+        std::vector<double> F(2 * blk, 0.0), I(2 * blk, 0.0);
         for (int i = 0; i < Pe; ++i)
-            for (int c = 0; c < Pe; ++c) F[(size_t)i + (size_t)c * Pe] = Fv(2 * i, c);
+            for (int c = 0; c < Pe; ++c) F[(size_t)i * P4 + c] = Fv(2 * i, c);
         for (int i = 0; i < Po; ++i)
-            for (int c = 0; c < Po; ++c) F[(size_t)Pe * Pe + i + (size_t)c * Po] = Fv(2 * i + 1, c);
+            for (int c = 0; c < Po; ++c) F[blk + (size_t)i * P4 + c] = Fv(2 * i + 1, c);
         for (int r = 0; r < Pe; ++r)
-            for (int i = 0; i < Pe; ++i) I[(size_t)r + (size_t)i * Pe] = Iv(r, 2 * i);
+            for (int i = 0; i < Pe; ++i) I[(size_t)r * P4 + i] = Iv(r, 2 * i);
         for (int r = 0; r < Po; ++r)
-            for (int i = 0; i < Po; ++i) I[(size_t)Pe * Pe + r + (size_t)i * Po] = Iv(r, 2 * i + 1);
+            for (int i = 0; i < Po; ++i) I[blk + (size_t)r * P4 + i] = Iv(r, 2 * i + 1);
         p->d_dct_fwd = dalloc<double>(p, F.size());
         p->d_dct_inv = dalloc<double>(p, I.size());
         SE_CUDA(cudaMemcpy(p->d_dct_fwd, F.data(), F.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -625,50 +816,59 @@ void factor_bvp(Plan* p) {
     if (bad) throw Error(SE_ERR_LINALG, "ill-conditioned Schur block in the mode BVP factorisation");
 }
 
-// z transforms as one DGEMM over all modes of both grids (W = 4M doubles per
-// row): the DCT-I of length Nz = 258 is 2*257 in FFT terms (Bluestein in
-// cuFFT); as a 258 x 258 matrix it runs on the FP64 tensor pipe.
-// out (W x cols, ldo) = in (W x k, ldi) * D^T with D (cols x k) column-major;
-// W x k column-major == row-major [k][W] (z-slowest rows)
-static void z_gemm(Plan* p, int64_t W, const double* D, int cols, int k, const double* in,
-                   int64_t ldi, double* out, int64_t ldo) {
-    const double one = 1.0, zero = 0.0;
-    SE_CUBLAS(cublasDgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_T, (int)W, cols, k, &one, in, (int)ldi,
-                          D, cols, &zero, out, (int)ldo));
+static DctArgs dct_args(Plan* p, const double* mats, int64_t W) {
+    DctArgs a{};
+    a.n = p->Nz; a.Pe = (p->Nz + 1) / 2; a.Po = p->Nz / 2;
+    a.P8 = p->dct_p8; a.P4 = p->dct_p4; a.W = W;
+    a.De = mats; a.Do = mats + (size_t)a.P8 * a.P4;
+    return a;
 }
 
-// symmetric / antisymmetric node combinations for the forward DCT:
-// s_c = v_c + v_{N-c}, d_c = v_c - v_{N-c} (c < n/2); s_h = v_h (odd n)
-__global__ void fold_kernel(const double* v, int n, int64_t W, double* s, double* d) {
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int Pe = (n + 1) / 2, Po = n / 2;
-    if (e >= (int64_t)Pe * W) return;
-    const int c = (int)(e / W);
-    const int64_t w = e - (int64_t)c * W;
-    const double a = v[(int64_t)c * W + w];
-    if (c < Po) {
-        const double b = v[(int64_t)(n - 1 - c) * W + w];
-        s[e] = a + b;
-        d[e] = a - b;
-    } else {
-        s[e] = a;
+// dispatch on the number of 8-row tiles per parity (accumulators in registers)
+#define SE_DCT_LAUNCH(KERNEL, MT, GRID, SMEM, ST, ...)                                   \
+    do {                                                                                  \
+        auto kfn = KERNEL<MT>;                                                            \
+        SE_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                     (int)(SMEM)));                                       \
+        kfn<<<GRID, 256, SMEM, ST>>>(__VA_ARGS__);                                        \
+    } while (0)
+
+#define SE_DCT_DISPATCH(KERNEL, MTV, GRID, SMEM, ST, ...)                                 \
+    switch (MTV) {                                                                        \
+        case 1: SE_DCT_LAUNCH(KERNEL, 1, GRID, SMEM, ST, __VA_ARGS__); break;             \
+        case 2: SE_DCT_LAUNCH(KERNEL, 2, GRID, SMEM, ST, __VA_ARGS__); break;             \
+        case 3: SE_DCT_LAUNCH(KERNEL, 3, GRID, SMEM, ST, __VA_ARGS__); break;             \
+        case 4: SE_DCT_LAUNCH(KERNEL, 4, GRID, SMEM, ST, __VA_ARGS__); break;             \
+        case 5: SE_DCT_LAUNCH(KERNEL, 5, GRID, SMEM, ST, __VA_ARGS__); break;             \
+        case 6: SE_DCT_LAUNCH(KERNEL, 6, GRID, SMEM, ST, __VA_ARGS__); break;             \
+        case 7: SE_DCT_LAUNCH(KERNEL, 7, GRID, SMEM, ST, __VA_ARGS__); break;             \
+        case 8: SE_DCT_LAUNCH(KERNEL, 8, GRID, SMEM, ST, __VA_ARGS__); break;             \
+        case 9: SE_DCT_LAUNCH(KERNEL, 9, GRID, SMEM, ST, __VA_ARGS__); break;             \
+        case 10: SE_DCT_LAUNCH(KERNEL, 10, GRID, SMEM, ST, __VA_ARGS__); break;           \
+        case 11: SE_DCT_LAUNCH(KERNEL, 11, GRID, SMEM, ST, __VA_ARGS__); break;           \
+        case 12: SE_DCT_LAUNCH(KERNEL, 12, GRID, SMEM, ST, __VA_ARGS__); break;           \
+        case 13: SE_DCT_LAUNCH(KERNEL, 13, GRID, SMEM, ST, __VA_ARGS__); break;           \
+        case 14: SE_DCT_LAUNCH(KERNEL, 14, GRID, SMEM, ST, __VA_ARGS__); break;           \
+        case 15: SE_DCT_LAUNCH(KERNEL, 15, GRID, SMEM, ST, __VA_ARGS__); break;           \
+        case 16: SE_DCT_LAUNCH(KERNEL, 16, GRID, SMEM, ST, __VA_ARGS__); break;           \
+        case 17: SE_DCT_LAUNCH(KERNEL, 17, GRID, SMEM, ST, __VA_ARGS__); break;           \
+        case 18: SE_DCT_LAUNCH(KERNEL, 18, GRID, SMEM, ST, __VA_ARGS__); break;           \
+        case 19: SE_DCT_LAUNCH(KERNEL, 19, GRID, SMEM, ST, __VA_ARGS__); break;           \
+        case 20: SE_DCT_LAUNCH(KERNEL, 20, GRID, SMEM, ST, __VA_ARGS__); break;           \
+        default: throw Error(SE_ERR_VALUE, "Nz outside the z transform kernels' range"); \
     }
-}
 
 // z DCT-I of the xy spectra in d_hat ([Nz][2][M] for the mode view) into
 // the Chebyshev coefficients d_ext (same layout)
 void z_forward(Plan* p, const ModeView& v) {
-    const int n = p->Nz, Pe = (n + 1) / 2, Po = n / 2;
     const int64_t W = 4 * v.M;
-    double* S = reinterpret_cast<double*>(p->d_scr);   // BVP scratch, free here
-    double* D = S + (int64_t)Pe * W;
-    fold_kernel<<<(unsigned)(((int64_t)Pe * W + 255) / 256), 256, 0, p->stream>>>(
-        reinterpret_cast<const double*>(p->d_hat), n, W, S, D);
+    const DctArgs a = dct_args(p, p->d_dct_fwd, W);
+    const size_t smem = 2 * (size_t)DCT_COLS * a.P4 * sizeof(double);
+    const unsigned grid = (unsigned)((W + DCT_COLS - 1) / DCT_COLS);
+    const double* in = reinterpret_cast<const double*>(p->d_hat);
+    double* out = reinterpret_cast<double*>(p->d_ext);
+    SE_DCT_DISPATCH(zdct_fwd_kernel, a.P8 / 8, grid, smem, p->stream, a, in, out);
     SE_LAUNCHED(p);
-    double* ext = reinterpret_cast<double*>(p->d_ext);
-    z_gemm(p, W, p->d_dct_fwd, Pe, Pe, S, W, ext, 2 * W);                     // even rows
-    if (Po > 0)
-        z_gemm(p, W, p->d_dct_fwd + (size_t)Pe * Pe, Po, Po, D, W, ext + W, 2 * W);   // odd rows
 }
 
 void forward_transforms(Plan* p, bool two_grids) {
@@ -718,27 +918,24 @@ void bvp_solve_view(Plan* p, bool two_grids, int mode, bool correction, const Mo
 // inverse z DCT-I of the mode view and the assembly of the four spectral
 // fields into d_spec ([Nz][4][M] of the view)
 void z_inverse_assemble(Plan* p, bool forces, bool correction, const ModeView& v) {
-    // E (rows 0..Pe-1) from the even coefficients, O (rows Pe..) from the odd
-    const int n = p->Nz, Pe = (n + 1) / 2, Po = n / 2;
     const int64_t W = 4 * v.M;
+    const DctArgs a = dct_args(p, p->d_dct_inv, W);
+    AsmArgs2 q{};
+    q.mom = reinterpret_cast<const double2*>(p->d_mom);
+    q.kx = p->d_kx; q.ky = p->d_ky; q.kmag = p->d_kmag + v.m0; q.sel = p->d_sel + v.m0;
+    q.z = p->d_z; q.Nx = p->Nx; q.Ny = p->Ny; q.Nyh = p->Nyh; q.M = v.M;
+    q.Mv = v.Mv; q.m0 = v.m0;
+    q.w0 = p->win0; q.w1 = p->win1; q.corr = correction ? 1 : 0; q.forces = forces ? 1 : 0;
+    q.rb = p->P.eps_b / p->P.eps; q.rt = p->P.eps_t / p->P.eps; q.H = p->P.H;
+    const size_t smem = std::max(2 * (size_t)DCT_COLS * a.P4, 2 * (size_t)a.P8 * DCT_COLS) *
+                        sizeof(double);
+    const unsigned grid = (unsigned)((v.Mv + DCT_COLS / 4 - 1) / (DCT_COLS / 4));
     const double* ext = reinterpret_cast<const double*>(p->d_ext);
-    double* hat = reinterpret_cast<double*>(p->d_hat);
-    z_gemm(p, W, p->d_dct_inv, Pe, Pe, ext, 2 * W, hat, W);
-    if (Po > 0)
-        z_gemm(p, W, p->d_dct_inv + (size_t)Pe * Pe, Po, Po, ext + W, 2 * W,
-               hat + (int64_t)Pe * W, W);
-    AsmArgs a{};
-    a.ext = reinterpret_cast<const double2*>(p->d_hat);
-    a.spec = reinterpret_cast<double2*>(p->d_spec);
-    a.mom = reinterpret_cast<const double2*>(p->d_mom);
-    a.kx = p->d_kx; a.ky = p->d_ky; a.kmag = p->d_kmag + v.m0; a.sel = p->d_sel + v.m0;
-    a.z = p->d_z; a.Nz = p->Nz; a.Nx = p->Nx; a.Ny = p->Ny; a.Nyh = p->Nyh; a.M = v.M;
-    a.Mv = v.Mv; a.m0 = v.m0;
-    a.w0 = p->win0; a.w1 = p->win1; a.corr = correction ? 1 : 0; a.forces = forces ? 1 : 0;
-    a.rb = p->P.eps_b / p->P.eps; a.rt = p->P.eps_t / p->P.eps; a.H = p->P.H;
-    int64_t total = (int64_t)p->Nz * v.M;
-    assemble_kernel<<<(unsigned)((total + 255) / 256), 256, 0, p->stream>>>(a);
-    SE_LAUNCHED(p);
+    double2* spec = reinterpret_cast<double2*>(p->d_spec);
+    if (grid > 0) {
+        SE_DCT_DISPATCH(zdct_inv_kernel, a.P8 / 8, grid, smem, p->stream, a, q, ext, spec);
+        SE_LAUNCHED(p);
+    }
 }
 
 void inverse_transforms(Plan* p, bool forces, bool correction) {
