@@ -127,7 +127,7 @@ __global__ void cell_fill_kernel(const uint32_t* keys, const int* perm, int64_t 
     double4 v = src_in[s];
     src[i] = v;
     srcf[i] = make_float4((float)wrap(v.x, g.Lx), (float)wrap(v.y, g.Ly),
-                          (float)(v.z - g.zlo), 0.f);
+                          (float)(v.z - g.zlo), (float)v.w);
     orig[i] = s;
 }
 
@@ -151,12 +151,20 @@ struct NearArgs {
                                   // general (close) path
     float Lxf, Lyf, iLxf, iLyf;
     float zmarg;                  // fp32 z-window margin
+    // SE_FP32 evaluation: single-precision displacements from the wrapped
+    // fp32 coordinates; |r2_f32 - r2| is bounded, so pairs with r2_f32 <=
+    // r2in_f are certainly inside the cutoff, > r2out_f certainly outside,
+    // and only the thin band between takes the exact fp64 test
+    float r2in_f, r2out_f, hLxf, hLyf;
     // far pairs: erfcx(x) on the far x range as one degree-FAR_DEG
     // polynomial in t = (x - pmid) * pinvh (coefficients in the kernel
     // parameter bank, so no table loads); use_poly = 0 falls back to the table
     int use_poly;
     double pmid, pinvh;
     double pc[19];
+    // fp32 mode: erfcx on the same x range as one degree-FAR_DEG32 polynomial
+    int use_poly32;
+    float pmid32, pinvh32, pc32[11];
     // close pairs: g(r) and coef(r) as CL_P piecewise degree-CL_D polynomials
     // in r on [0, CL_P cl_w) (table staged in shared memory by the close
     // launch); use_ctab = 0 evaluates the erf formulas
@@ -174,6 +182,7 @@ struct NearArgs {
 
 constexpr int NB_THREADS = 128;
 constexpr int FAR_DEG = 18;
+constexpr int FAR_DEG32 = 10;
 constexpr int CL_P = 32, CL_D = 12;             // close-pair table: pieces, degree
 constexpr int CL_TAB = 2 * CL_P * (CL_D + 1);
 
@@ -241,8 +250,17 @@ __device__ __forceinline__ void pair_terms(const NearArgs& a, const double* tab,
         const float sr = (float)r2;
         const float ri = rsqrtf(sr);
         const float x = sr * ri * (float)a.ic2;
-        const float C = erfcf(x);
         const float e = __expf(-x * x);
+        float C;
+        if (a.use_poly32) {                      // erfc = exp(-x^2) erfcx(x)
+            const float t = (x - a.pmid32) * a.pinvh32;
+            float acc = a.pc32[FAR_DEG32];
+#pragma unroll
+            for (int j = FAR_DEG32 - 1; j >= 0; --j) acc = fmaf(acc, t, a.pc32[j]);
+            C = e * acc;
+        } else {
+            C = erfcf(x);
+        }
         const float i4 = (float)a.inv4pie;
         g = (double)(C * ri * i4);
         coef = nd ? (double)((C * ri + 1.1283792f * e * (float)a.ic2) * (ri * ri) * i4) : 0.0;
@@ -557,6 +575,60 @@ __device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, 
     }
 }
 
+// fp32 mode: the same list walk in single precision (float4 sources with
+// the charge in w, fp32 minimum image), fp64 accumulation; membership is
+// decided in fp32 away from the cutoff and by the exact fp64 test (with the
+// boundary deferral) inside the thin band where fp32 cannot decide, so the
+// pair set is still the reference's.
+template <bool FAR, bool HASH>
+__device__ __forceinline__ void eval_list_f32(const NearArgs& a, const double* tab, const int* list,
+                                              int n, double px, double py, double pz,
+                                              int64_t self_i, double& phi, double& ex,
+                                              double& ey, double& ez, int& count,
+                                              unsigned long long& hs) {
+    const float pxf = (float)wrap(px, a.g.Lx), pyf = (float)wrap(py, a.g.Ly);
+    const float pzf = (float)(pz - a.g.zlo);
+    const bool nd = a.need_field;
+    for (int k = 0; k < n; k += 4) {
+        const int4 j4 = *reinterpret_cast<const int4*>(list + k);
+        const int jj[4] = {j4.x, j4.y, j4.z, j4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = jj[u];
+            if (j < 0) continue;
+            const float4 f = a.srcf[j];
+            float dx = pxf - f.x, dy = pyf - f.y;
+            const float dz = pzf - f.z;
+            dx = dx > a.hLxf ? dx - a.Lxf : (dx < -a.hLxf ? dx + a.Lxf : dx);
+            dy = dy > a.hLyf ? dy - a.Lyf : (dy < -a.hLyf ? dy + a.Lyf : dy);
+            const float r2f = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            if (r2f > a.r2out_f) continue;
+            double r2 = (double)r2f;
+            if (r2f > a.r2in_f) {                    // the band: exact fp64 decision
+                const double4 sv = a.src[j];
+                const double ddx = min_image(__dsub_rn(px, sv.x), a.g.Lx);
+                const double ddy = min_image(__dsub_rn(py, sv.y), a.g.Ly);
+                const double ddz = __dsub_rn(pz, sv.z);
+                r2 = __dadd_rn(__dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)),
+                               __dmul_rn(ddz, ddz));
+                if (r2 > a.r2max) continue;
+                if (r2 >= a.win_lo) { defer_pair(a, self_i, j); continue; }
+            }
+            double g, coef;
+            pair_terms<FAR, FAR>(a, tab, r2, g, coef);
+            const double q = (double)f.w;
+            phi = fma(q, g, phi);
+            if (nd) {
+                const double cq = coef * q;
+                ex = fma(cq, (double)dx, ex); ey = fma(cq, (double)dy, ey);
+                ez = fma(cq, (double)dz, ez);
+            }
+            ++count;
+            if (HASH) hs += mix64((unsigned long long)a.orig[j]);
+        }
+    }
+}
+
 // Evaluation of one list kind per launch: the far lists (the bulk; erfc-only
 // kernel, small register footprint, high occupancy) write the sums, the close
 // lists (general kernel) add to them.
@@ -584,9 +656,15 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_eval_kernel(NearArgs a)
     if (live) {
         i = a.order[slot];
         const double px = a.eval[3 * i], py = a.eval[3 * i + 1], pz = a.eval[3 * i + 2];
-        if (FAR)
-            eval_list<true, F32, HASH>(a, tab, a.list_far + slot * a.cap_far, a.cnt_far[slot], px,
-                                       py, pz, i, phi, ex, ey, ez, count, hs);
+        if (F32)
+            eval_list_f32<FAR, HASH>(a, tab,
+                                     FAR ? a.list_far + slot * a.cap_far
+                                         : a.list_close + slot * a.cap_close,
+                                     FAR ? a.cnt_far[slot] : a.cnt_close[slot], px, py, pz, i,
+                                     phi, ex, ey, ez, count, hs);
+        else if (FAR)
+            eval_list<true, false, HASH>(a, tab, a.list_far + slot * a.cap_far, a.cnt_far[slot],
+                                         px, py, pz, i, phi, ex, ey, ez, count, hs);
         else
             eval_list<false, false, HASH>(a, tab, a.list_close + slot * a.cap_close,
                                           a.cnt_close[slot], px, py, pz, i, phi, ex, ey, ez,
@@ -1245,8 +1323,9 @@ void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, boo
 // erfcx on [xa, xb] as a degree-FAR_DEG polynomial in t = (x - mid) / half:
 // Chebyshev interpolation, converted to the monomial basis; accepted when
 // the relative error at 400 test points is below 1e-14.
-static bool fit_far_poly(double xa, double xb, double* mid, double* inv_half, double* pc) {
-    const int n = FAR_DEG + 1;
+static bool fit_far_poly(double xa, double xb, double* mid, double* inv_half, double* pc,
+                         int deg = FAR_DEG, double tol = 1e-14) {
+    const int n = deg + 1;
     const double m = 0.5 * (xa + xb), h = 0.5 * (xb - xa);
     if (!(h > 0) || xa < 0.25 || xb > 26.0) return false;
     auto erfcx = [](double x) { return std::erfc(x) * std::exp(x * x); };
@@ -1276,7 +1355,7 @@ static bool fit_far_poly(double xa, double xb, double* mid, double* inv_half, do
         const double ref = erfcx(x);
         worst = std::max(worst, std::fabs(acc - ref) / ref);
     }
-    if (!(worst < 1e-14)) return false;
+    if (!(worst < tol)) return false;
     *mid = m; *inv_half = 1.0 / h;
     for (int i = 0; i < n; ++i) pc[i] = mono[i];
     return true;
@@ -1428,6 +1507,17 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         const double r_far = std::max(6.5 * k.c1, 1e-2 * k.c2);
         const double xa = r_far / k.c2 * (1.0 - 1e-6), xb = k.radius / k.c2 * (1.0 + 1e-6);
         a.use_poly = fit_far_poly(xa, xb, &a.pmid, &a.pinvh, a.pc) ? 1 : 0;
+        double m32 = 0, ih32 = 0, c32[FAR_DEG32 + 1];
+        a.use_poly32 = (k.fp32 && fit_far_poly(xa, xb, &m32, &ih32, c32, FAR_DEG32, 3e-7)) ? 1 : 0;
+        a.pmid32 = (float)m32; a.pinvh32 = (float)ih32;
+        for (int j = 0; j <= FAR_DEG32; ++j) a.pc32[j] = a.use_poly32 ? (float)c32[j] : 0.f;
+    }
+    {
+        const double err = 2.0 * 4e-7 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(p->cl.zlo));
+        const double rin = std::max(0.0, k.radius - err), rout = k.radius + err;
+        a.r2in_f = std::nextafter((float)(rin * rin), 0.0f);
+        a.r2out_f = std::nextafter((float)(rout * rout), INFINITY);
+        a.hLxf = (float)(0.5 * p->P.Lx); a.hLyf = (float)(0.5 * p->P.Ly);
     }
     a.Lxf = (float)p->P.Lx; a.Lyf = (float)p->P.Ly;
     a.iLxf = (float)(1.0 / p->P.Lx); a.iLyf = (float)(1.0 / p->P.Ly);
@@ -1605,7 +1695,8 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         if (k.fp32) near_eval_kernel<true, 8, true, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         else near_eval_kernel<true, 8, false, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         SE_LAUNCHED(p);
-        near_eval_kernel<false, 6, false, true><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
+        if (k.fp32) near_eval_kernel<false, 6, true, true><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
+        else near_eval_kernel<false, 6, false, true><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
         SE_LAUNCHED(p);
         if (k.fp32) near_fused_kernel<true, 6, true, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
         else near_fused_kernel<false, 6, true, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
@@ -1613,7 +1704,8 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         if (k.fp32) near_eval_kernel<true, 8, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         else near_eval_kernel<true, 8><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         SE_LAUNCHED(p);
-        near_eval_kernel<false, 6><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
+        if (k.fp32) near_eval_kernel<false, 6, true><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
+        else near_eval_kernel<false, 6><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
         SE_LAUNCHED(p);
         if (k.fp32) near_fused_kernel<true, 6, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
         else near_fused_kernel<false, 6, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
