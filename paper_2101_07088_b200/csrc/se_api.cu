@@ -59,14 +59,35 @@ void make_plan2d(cufftHandle* h, int nx, int ny, int nyh, cufftType type,
                  int64_t idist, int64_t odist, int batch, cudaStream_t s) {
     int real_embed[2] = {nx, ny};
     int cplx_embed[2] = {nx, nyh};
-    int* in_e = (type == CUFFT_D2Z) ? real_embed : cplx_embed;
-    int* out_e = (type == CUFFT_D2Z) ? cplx_embed : real_embed;
+    const bool r2c = type == CUFFT_D2Z || type == CUFFT_R2C;
+    int* in_e = r2c ? real_embed : cplx_embed;
+    int* out_e = r2c ? cplx_embed : real_embed;
     SE_CUFFT(cufftCreate(h));
     size_t ws = 0;
     long long nn[2] = {nx, ny}, ie[2] = {in_e[0], in_e[1]}, oe[2] = {out_e[0], out_e[1]};
     SE_CUFFT(cufftMakePlanMany64(*h, 2, nn, ie, 1, idist, oe, 1, odist, type, batch, &ws));
     SE_CUFFT(cufftSetStream(*h, s));
 }
+
+}  // namespace
+
+// buffers and cuFFT plans of the fp32 grid path, created on first use
+void ensure_grid32(Plan* p) {
+    if (p->d_rho32) return;
+    const size_t nz = (size_t)p->Nz;
+    p->d_rho32 = dalloc<float>(p, 2 * (size_t)p->G);
+    p->d_hat32 = dalloc<cufftComplex>(p, nz * 2 * p->M);
+    p->d_spec32 = dalloc<cufftComplex>(p, nz * 4 * p->M);
+    p->d_fields32 = dalloc<float>(p, 4 * (size_t)p->G);
+    make_plan2d(&p->fft_fwd2_f, p->Nx, p->Ny, p->Nyh, CUFFT_R2C, p->NXY, p->M, 2 * (int)nz,
+                p->stream);
+    make_plan2d(&p->fft_inv4_f, p->Nx, p->Ny, p->Nyh, CUFFT_C2R, p->M, p->NXY, 4 * (int)nz,
+                p->stream);
+    make_plan2d(&p->fft_inv1_f, p->Nx, p->Ny, p->Nyh, CUFFT_C2R, 4 * p->M, 4 * p->NXY, (int)nz,
+                p->stream);
+}
+
+namespace {
 
 // ---------------------------------------------------------------------------
 // the solve in three phases; the single-GPU solve runs them back to back and a
@@ -446,6 +467,9 @@ void dist_fields(Plan* p) {
 
 void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
                 double* d_phi_out, double* d_E_out, double* U, se_diag* diag) {
+    // fp32 mode of a whole (single-GPU) solve: the grid path in fp32 too
+    p->g32 = (flags & SE_FP32) != 0;
+    if (p->g32) ensure_grid32(p);
     phase_spread(p, d_pos, n, 0, n, flags);
     phase_fields(p);
     phase_charges(p, d_pos, d_phi_out, d_E_out);
@@ -662,7 +686,8 @@ void se_plan_destroy(se_plan* plan) {
     cudaSetDevice(p->dev);
     if (p->stream) cudaStreamSynchronize(p->stream);
     cufftHandle hs[] = {p->fft_fwd2, p->fft_fwd1, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig,
-                        p->fft_fwd_slab, p->fft_inv4_slab, p->fft_inv1_slab};
+                        p->fft_fwd_slab, p->fft_inv4_slab, p->fft_inv1_slab, p->fft_fwd2_f,
+                        p->fft_inv4_f, p->fft_inv1_f};
     for (auto h : hs) if (h) cufftDestroy(h);
     for (auto& b : p->owned) if (b.p) cudaFree(b.p);
     if (p->nl.h_ovf) cudaFreeHost(p->nl.h_ovf);
@@ -680,7 +705,8 @@ int se_plan_set_stream(se_plan* plan, void* stream) {
         if (p->own_stream && p->stream) { cudaStreamDestroy(p->stream); p->own_stream = false; }
         p->stream = reinterpret_cast<cudaStream_t>(stream);
         cufftHandle hs[] = {p->fft_fwd2, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig,
-                            p->fft_fwd_slab, p->fft_inv4_slab, p->fft_inv1_slab};
+                            p->fft_fwd_slab, p->fft_inv4_slab, p->fft_inv1_slab,
+                            p->fft_fwd2_f, p->fft_inv4_f, p->fft_inv1_f};
         for (auto h : hs) if (h) SE_CUFFT(cufftSetStream(h, p->stream));
         return SE_OK;
     } catch (const Error& e) {
@@ -772,6 +798,7 @@ int se_shard_spread(se_plan* plan, const double* d_pos_all, int64_t n_all, int64
     try {
         if (!p) throw Error(SE_ERR_VALUE, "null plan");
         SE_CUDA(cudaSetDevice(p->dev));
+        p->g32 = false;                 // the ranks sum fp64 grids
         phase_spread(p, d_pos_all, n_all, first, count, flags);
         if (d_rho) *d_rho = p->d_rho;
         if (rho_len) *rho_len = 2 * p->G;

@@ -388,6 +388,7 @@ struct SpreadArgs {
     TileArgs t;
     double* rho;                 // [Nz][2][Nx][Ny]
     int two;                     // slot 0 (over) as well as slot 1 (in)
+    float* rho32;                // fp32 mode: the same grids in single precision
 };
 
 // ---------------------------------------------------------------------------
@@ -447,8 +448,9 @@ __global__ void group_fill_kernel(const int64_t* seg, const int* off, int nbins,
         groups[o++] = make_int2((int)(s0 + j), (int)(n - j < IG ? n - j : IG));
 }
 
-struct InterpArgs {
-    const double* fields;        // [Nz][4][Nx][Ny]
+template <typename T>
+struct InterpArgsT {
+    const T* fields;             // [Nz][4][Nx][Ny]
     const double* pos; const double* znodes; const double* wcc;
     const double* scal;          // scal[0] = A_i
     const int* perm; const int2* groups; const int* ngroups;
@@ -456,6 +458,7 @@ struct InterpArgs {
     double hx, hy, rad, rad_keep, inv_width, inv_norm; int mx, my;
     double* out; int64_t N;      // [NF][N] raw sums (global charge index)
 };
+using InterpArgs = InterpArgsT<double>;
 
 struct GroupInfo {
     double x[IG_MAX], y[IG_MAX], z[IG_MAX];
@@ -463,8 +466,10 @@ struct GroupInfo {
     int jxw[IG_MAX], jyw[IG_MAX], lo[IG_MAX], hi[IG_MAX], idx[IG_MAX];
 };
 
-template <int NF, int IG, int MINB, int UNR>
-__global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgs a) {
+// T = float (fp32 mode): single-precision field loads and FMAs (weights
+// rounded to fp32), the k = 0 terms and the final sums in fp64
+template <int NF, int IG, int MINB, int UNR, typename T = double>
+__global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgsT<T> a) {
     extern __shared__ __align__(16) double ism[];
     __shared__ GroupInfo ginfo[IWARPS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -534,11 +539,11 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgs a)
         for (int o = 0; o < SX; ++o) sx += swx[lane * SX + o];
         for (int o = 0; o < SY; ++o) sy += swy[lane * SY + o];
     }
-    double acc[IG][NF];
+    T acc[IG][NF];
 #pragma unroll
     for (int m = 0; m < IG; ++m)
 #pragma unroll
-        for (int c = 0; c < NF; ++c) acc[m][c] = 0.0;
+        for (int c = 0; c < NF; ++c) acc[m][c] = T(0);
     const int Wx = xmax - xmin + SX, Wy = ymax - ymin + SY;
     const int64_t zstride = 4 * a.NXY;
     for (int zc = zlo; zc < zhi; zc += IZC) {
@@ -580,15 +585,15 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgs a)
             int gx = xmin - a.mx + ux, gy = ymin - a.my + uy;
             gx %= a.Nx; if (gx < 0) gx += a.Nx;
             gy %= a.Ny; if (gy < 0) gy += a.Ny;
-            const double* F = a.fields + (int64_t)zc * zstride + (int64_t)gx * a.Ny + gy;
+            const T* F = a.fields + (int64_t)zc * zstride + (int64_t)gx * a.Ny + gy;
 #pragma unroll UNR
             for (int r = 0; r < nz; ++r) {
-                double f[NF];
+                T f[NF];
 #pragma unroll
                 for (int c = 0; c < NF; ++c) f[c] = __ldg(F + (int64_t)r * zstride + c * a.NXY);
 #pragma unroll
                 for (int m = 0; m < IG; ++m) {
-                    const double W = wxy[m] * swz[m * IZC + r];
+                    const T W = (T)(wxy[m] * swz[m * IZC + r]);
 #pragma unroll
                     for (int c = 0; c < NF; ++c) acc[m][c] = fma(W, f[c], acc[m][c]);
                 }
@@ -601,7 +606,7 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgs a)
     for (int m = 0; m < IG; ++m)
 #pragma unroll
         for (int c = 0; c < NF; ++c) {
-            double v = acc[m][c];
+            double v = (double)acc[m][c];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             if (lane == m * NF + c) mine = v;
@@ -629,7 +634,8 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgs a)
 // ---------------------------------------------------------------------------
 struct PointArgs {
     const double* pts; int64_t n;
-    const double* fields; const double* znodes; const double* wcc;
+    const double* fields; const float* fields32;      // one of them (fp32 mode: fields32)
+    const double* znodes; const double* wcc;
     const double* scal; int Nx, Ny, Nz; int64_t NXY;
     double hx, hy, width, rad, rad_keep, norm; int mx, my;
     double* out; int* flags; double z0, z1;
@@ -661,8 +667,8 @@ __global__ void point_interp_kernel(PointArgs a) {
             if (fabs(dz) > a.rad) continue;
             double tz = dz / a.width;
             double wz = exp(-0.5 * (tz * tz)) / a.norm * a.wcc[k];
-            double f = a.fields[((int64_t)k * 4) * a.NXY + (int64_t)gx * a.Ny + gy]
-                       + A_i * a.znodes[k];
+            const int64_t at = ((int64_t)k * 4) * a.NXY + (int64_t)gx * a.Ny + gy;
+            double f = (a.fields32 ? (double)a.fields32[at] : a.fields[at]) + A_i * a.znodes[k];
             col += wz * f;
         }
         sum += wxy * col;
@@ -866,11 +872,14 @@ __global__ void __launch_bounds__(4 * TZ, MINB) spread_mma_kernel(SpreadArgs a) 
         for (int mb = 0; mb < TILE; ++mb) {
             const int gx = gx0 + mb;
             if (gx < A.Nx && gy < A.Ny) {
-                double* base_ptr = a.rho + (int64_t)(cls) * A.NXY + (int64_t)gx * A.Ny + gy;
+                const int64_t off = (int64_t)(cls) * A.NXY + (int64_t)gx * A.Ny + gy;
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
                     const int k = k0 + 8 * zg + 2 * kk + i;
-                    if (k < A.Nz) base_ptr[(int64_t)k * 2 * A.NXY] = c[mb][i];
+                    if (k < A.Nz) {
+                        if (a.rho32) a.rho32[off + (int64_t)k * 2 * A.NXY] = (float)c[mb][i];
+                        else a.rho[off + (int64_t)k * 2 * A.NXY] = c[mb][i];
+                    }
                 }
             }
         }
@@ -889,7 +898,7 @@ static void launch_spread_mma(Plan* p, const SpreadArgs& a) {
 
 
 void spread(Plan* p, bool two_grids) {
-    SpreadArgs a{tile_args(p), p->d_rho, two_grids ? 1 : 0};
+    SpreadArgs a{tile_args(p), p->d_rho, two_grids ? 1 : 0, p->g32 ? p->d_rho32 : nullptr};
     // 8x8-column x 16-node tiles, 2 warps (one per 8-node z group), DMMA
     // accumulation, 64 staged sources per round, 10 CTAs per SM: measured
     // best among tile heights {16, 32}, rounds {32..256}, scalar lane shapes
@@ -955,15 +964,25 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
     InterpArgs a{p->d_fields, p->d_pos_cur, p->d_z, p->d_wcc, p->d_scal, p->d_perm2,
                  p->d_igroups, p->d_ingroups, p->Nx, p->Ny, p->Nz, p->NXY, p->hx, p->hy,
                  p->rad, p->rad_keep, 1.0 / p->width, 1.0 / p->norm, p->mx, p->my, p->d_far, n};
+    InterpArgsT<float> a32{p->d_fields32, p->d_pos_cur, p->d_z, p->d_wcc, p->d_scal, p->d_perm2,
+                           p->d_igroups, p->d_ingroups, p->Nx, p->Ny, p->Nz, p->NXY, p->hx,
+                           p->hy, p->rad, p->rad_keep, 1.0 / p->width, 1.0 / p->norm, p->mx,
+                           p->my, p->d_far, n};
     const int smem = IWARPS * ig * (2 * p->mx + 1 + 2 * p->my + 1 + IZC) * (int)sizeof(double);
     if (smem > 200 * 1024) throw Error(SE_ERR_VALUE, "stencil too wide for the interpolation");
     const unsigned blocks = (unsigned)((gcap + IWARPS - 1) / IWARPS);
-    auto go = [&](auto kern) {
+    auto go = [&](auto kern, const auto& args) {
         SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        kern<<<blocks, IWARPS * 32, smem, p->stream>>>(a);
+        kern<<<blocks, IWARPS * 32, smem, p->stream>>>(args);
     };
-    if (forces) go(interp_kernel<4, 4, 1, 2>);
-    else go(interp_kernel<1, 4, 1, 2>);
+    if (p->g32) {
+        if (forces) go(interp_kernel<4, 4, 1, 2, float>, a32);
+        else go(interp_kernel<1, 4, 1, 2, float>, a32);
+    } else if (forces) {
+        go(interp_kernel<4, 4, 1, 2>, a);
+    } else {
+        go(interp_kernel<1, 4, 1, 2>, a);
+    }
     p->ktoc(2);
     SE_LAUNCHED(p);
 }
@@ -973,6 +992,7 @@ void interp_points(Plan* p, const double* d_pts, int64_t npts, double width,
     if (npts == 0) return;
     PointArgs a{};
     a.pts = d_pts; a.n = npts; a.fields = p->d_fields; a.znodes = p->d_z;
+    a.fields32 = p->g32 ? p->d_fields32 : nullptr;
     a.wcc = p->d_wcc; a.scal = p->d_scal; a.Nx = p->Nx; a.Ny = p->Ny;
     a.Nz = p->Nz; a.NXY = p->NXY; a.hx = p->hx; a.hy = p->hy;
     a.width = width; a.rad = radius; a.rad_keep = radius + 1e-12 * radius;

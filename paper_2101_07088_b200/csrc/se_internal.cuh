@@ -310,6 +310,16 @@ struct Plan {
     cufftHandle fft_fwd2 = 0, fft_fwd1 = 0, fft_z = 0, fft_inv4 = 0,
                 fft_inv1 = 0, fft_sig = 0;
 
+    // fp32 grid path (SE_FP32 on a single-GPU solve): spread grids, xy
+    // spectra, spectral fields and field grids in single precision; the z
+    // transforms, mode BVPs and correction stay fp64
+    bool g32 = false;
+    float* d_rho32 = nullptr;             // [Nz][2][Nx][Ny]
+    cufftComplex* d_hat32 = nullptr;      // [Nz][2][M]
+    cufftComplex* d_spec32 = nullptr;     // [Nz][4][M]
+    float* d_fields32 = nullptr;          // [Nz][4][Nx][Ny]
+    cufftHandle fft_fwd2_f = 0, fft_inv4_f = 0, fft_inv1_f = 0;
+
     // distributed grid pipeline (se_dist_*): rank `rank` of `nranks` owns the
     // z planes [rank zc, (rank+1) zc) for the xy FFTs and the half-spectrum
     // modes [rank mc, (rank+1) mc) for the z transforms and mode BVPs
@@ -372,6 +382,7 @@ void z_forward(Plan* p, const ModeView& v);
 void bvp_solve_view(Plan* p, bool two_grids, int mode, bool correction, const ModeView& v);
 void z_inverse_assemble(Plan* p, bool forces, bool correction, const ModeView& v);
 void forward_transforms(Plan* p, bool two_grids);
+void ensure_grid32(Plan* p);
 void bvp_solve(Plan* p, bool two_grids, int mode, bool correction);
 void inverse_transforms(Plan* p, bool forces, bool correction);
 

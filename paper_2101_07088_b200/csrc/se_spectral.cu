@@ -544,8 +544,8 @@ __device__ __forceinline__ void dct_mma(const double* __restrict__ D, int P4, in
 
 // forward: hat rows [n][W] (xy spectra per plane) -> ext rows [n][W]
 // (Chebyshev coefficient n in row n, unnormalised as the GEMM form was)
-template <int MT>
-__global__ void __launch_bounds__(256, 2) zdct_fwd_kernel(DctArgs a, const double* __restrict__ in,
+template <int MT, typename TIn = double>
+__global__ void __launch_bounds__(256, 2) zdct_fwd_kernel(DctArgs a, const TIn* __restrict__ in,
                                                          double* __restrict__ out) {
     extern __shared__ double sm[];
     double* Se = sm;                                   // [DCT_COLS][P4]
@@ -566,8 +566,8 @@ __global__ void __launch_bounds__(256, 2) zdct_fwd_kernel(DctArgs a, const doubl
             const int c = e / DCT_COLS, col = e - c * DCT_COLS;
             const int64_t w = w0 + col;
             const bool ok = e < total && w < a.W && c < a.Pe;
-            xv[u] = ok ? in[(int64_t)c * a.W + w] : 0.0;
-            yv[u] = (ok && c < a.Po) ? in[(int64_t)(N - c) * a.W + w] : 0.0;
+            xv[u] = ok ? (double)in[(int64_t)c * a.W + w] : 0.0;
+            yv[u] = (ok && c < a.Po) ? (double)in[(int64_t)(N - c) * a.W + w] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < STG_U; ++u) {
@@ -615,10 +615,10 @@ struct AsmArgs2 {
     double rb, rt, H;
 };
 
-template <int MT>
+template <int MT, typename TOut = double2>
 __global__ void __launch_bounds__(256, 2) zdct_inv_kernel(DctArgs a, AsmArgs2 q,
                                                          const double* __restrict__ ext,
-                                                         double2* __restrict__ spec) {
+                                                         TOut* __restrict__ spec) {
     extern __shared__ double sm[];
     constexpr int MPB = DCT_COLS / 4;                  // modes per CTA
     double* Ce = sm;                                   // [DCT_COLS][P4] even coefficients
@@ -701,16 +701,21 @@ __global__ void __launch_bounds__(256, 2) zdct_inv_kernel(DctArgs a, AsmArgs2 q,
             v = cadd(v, cadd(cscale(mbv, pb), cscale(mtv, pt)));
             d = cadd(d, cadd(cscale(mbv, db), cscale(mtv, dt)));
         }
-        double2* out = spec + (int64_t)j * 4 * q.M + m;
-        out[0] = v;
+        TOut* out = spec + (int64_t)j * 4 * q.M + m;
+        auto mk = [](double re, double im) {
+            TOut o;
+            o.x = re; o.y = im;
+            return o;
+        };
+        out[0] = mk(v.x, v.y);
         if (q.forces) {
             const int64_t gm = q.m0 + m;
             const int ix = (int)(gm / q.Nyh), iy = (int)(gm % q.Nyh);
             const double ikx = (q.Nx % 2 == 0 && ix == q.Nx / 2) ? 0.0 : q.kx[ix];
             const double iky = (q.Ny % 2 == 0 && iy == q.Ny / 2) ? 0.0 : q.ky[iy];
-            out[q.M] = make_double2(-ikx * v.y, ikx * v.x);        // i kx v
-            out[2 * q.M] = make_double2(-iky * v.y, iky * v.x);    // i ky v
-            out[3 * q.M] = d;
+            out[q.M] = mk(-ikx * v.y, ikx * v.x);            // i kx v
+            out[2 * q.M] = mk(-iky * v.y, iky * v.x);        // i ky v
+            out[3 * q.M] = mk(d.x, d.y);
         }
     }
 }
@@ -827,7 +832,7 @@ static DctArgs dct_args(Plan* p, const double* mats, int64_t W) {
 // dispatch on the number of 8-row tiles per parity (accumulators in registers)
 #define SE_DCT_LAUNCH(KERNEL, MT, GRID, SMEM, ST, ...)                                   \
     do {                                                                                  \
-        auto kfn = KERNEL<MT>;                                                            \
+        auto kfn = KERNEL<MT, DCT_T>;                                                     \
         SE_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                                      (int)(SMEM)));                                       \
         kfn<<<GRID, 256, SMEM, ST>>>(__VA_ARGS__);                                        \
@@ -865,15 +870,23 @@ void z_forward(Plan* p, const ModeView& v) {
     const DctArgs a = dct_args(p, p->d_dct_fwd, W);
     const size_t smem = 2 * (size_t)DCT_COLS * a.P4 * sizeof(double);
     const unsigned grid = (unsigned)((W + DCT_COLS - 1) / DCT_COLS);
-    const double* in = reinterpret_cast<const double*>(p->d_hat);
     double* out = reinterpret_cast<double*>(p->d_ext);
-    SE_DCT_DISPATCH(zdct_fwd_kernel, a.P8 / 8, grid, smem, p->stream, a, in, out);
+    if (p->g32) {
+        using DCT_T = float;
+        const float* in = reinterpret_cast<const float*>(p->d_hat32);
+        SE_DCT_DISPATCH(zdct_fwd_kernel, a.P8 / 8, grid, smem, p->stream, a, in, out);
+    } else {
+        using DCT_T = double;
+        const double* in = reinterpret_cast<const double*>(p->d_hat);
+        SE_DCT_DISPATCH(zdct_fwd_kernel, a.P8 / 8, grid, smem, p->stream, a, in, out);
+    }
     SE_LAUNCHED(p);
 }
 
 void forward_transforms(Plan* p, bool two_grids) {
     (void)two_grids;
-    SE_CUFFT(cufftExecD2Z(p->fft_fwd2, p->d_rho, p->d_hat));
+    if (p->g32) SE_CUFFT(cufftExecR2C(p->fft_fwd2_f, p->d_rho32, p->d_hat32));
+    else SE_CUFFT(cufftExecD2Z(p->fft_fwd2, p->d_rho, p->d_hat));
     z_forward(p, ModeView{p->M, p->M, 0});
 }
 
@@ -931,17 +944,30 @@ void z_inverse_assemble(Plan* p, bool forces, bool correction, const ModeView& v
                         sizeof(double);
     const unsigned grid = (unsigned)((v.Mv + DCT_COLS / 4 - 1) / (DCT_COLS / 4));
     const double* ext = reinterpret_cast<const double*>(p->d_ext);
-    double2* spec = reinterpret_cast<double2*>(p->d_spec);
     if (grid > 0) {
-        SE_DCT_DISPATCH(zdct_inv_kernel, a.P8 / 8, grid, smem, p->stream, a, q, ext, spec);
+        if (p->g32) {
+            using DCT_T = float2;
+            float2* spec = reinterpret_cast<float2*>(p->d_spec32);
+            SE_DCT_DISPATCH(zdct_inv_kernel, a.P8 / 8, grid, smem, p->stream, a, q, ext, spec);
+        } else {
+            using DCT_T = double2;
+            double2* spec = reinterpret_cast<double2*>(p->d_spec);
+            SE_DCT_DISPATCH(zdct_inv_kernel, a.P8 / 8, grid, smem, p->stream, a, q, ext, spec);
+        }
         SE_LAUNCHED(p);
     }
 }
 
 void inverse_transforms(Plan* p, bool forces, bool correction) {
     z_inverse_assemble(p, forces, correction, ModeView{p->M, p->M, 0});
-    if (forces) SE_CUFFT(cufftExecZ2D(p->fft_inv4, p->d_spec, p->d_fields));
-    else SE_CUFFT(cufftExecZ2D(p->fft_inv1, p->d_spec, p->d_fields));
+    if (p->g32) {
+        if (forces) SE_CUFFT(cufftExecC2R(p->fft_inv4_f, p->d_spec32, p->d_fields32));
+        else SE_CUFFT(cufftExecC2R(p->fft_inv1_f, p->d_spec32, p->d_fields32));
+    } else if (forces) {
+        SE_CUFFT(cufftExecZ2D(p->fft_inv4, p->d_spec, p->d_fields));
+    } else {
+        SE_CUFFT(cufftExecZ2D(p->fft_inv1, p->d_spec, p->d_fields));
+    }
 }
 
 }  // namespace se
