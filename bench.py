@@ -235,7 +235,8 @@ def bench_config(args, system, params, world=1, sharded=False):
     else:
         par = ("shard%d: charges split by index; NCCL reduce-scatter to z slabs, "
                "slab xy FFTs, all-to-all to (kx,ky) pencils, pencil DCT + BVPs, "
-               "all-to-all back, all-gather of the fields" % world)
+               "all-to-all back, all-gather of the fields; near field routed by x "
+               "slab (+r_cut halo) on a side stream" % world)
     return {"workload": args.config, "N": system.n,
             "grid": [params.Nx, params.Ny, params.Nz],
             "eps_b": system.geometry.eps_b, "eps_t": system.geometry.eps_t,
@@ -318,11 +319,20 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     if sharded:
         from paper_2101_07088_b200.sharded import ShardedSlabSolver
+        # near field routed by x slab when the slabs are at least r_cut wide
+        # (each rank holds only its index shard's positions), else every
+        # charge is a near-field source on every rank
+        cell = system.geometry.Lx / world >= params.r_cut and system.surface.is_zero
         solver = ShardedSlabSolver(system, params, device=local,
-                                   decompose=not args.replicate_grid)
+                                   decompose=not args.replicate_grid,
+                                   near="cell" if cell else "index")
+        pos_own_d = pos_d[solver.first:solver.first + solver.count].contiguous()
 
         def step(timings=False):
-            _, _, U, diag = solver.solve_shard(pos_d, timings=timings)
+            if cell:
+                _, _, U, diag = solver.solve_shard_own(pos_own_d, timings=timings)
+            else:
+                _, _, U, diag = solver.solve_shard(pos_d, timings=timings)
             return U, diag
     else:
         solver = SlabSolver(system, params, device=local)

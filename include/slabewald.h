@@ -132,6 +132,40 @@ int se_shard_fields(se_plan* plan);
 int se_shard_charges(se_plan* plan, const double* d_pos_all, double* d_phi,
                      double* d_E, double* U_part, se_diag* diag);
 
+/* Sharded solve with only the own shard's positions and the near field
+ * routed by cell (replaces the every-source near field
+ * of NearField, slab.py:94-181, on each rank):
+ *   se_shard_spread_own   as se_shard_spread, d_pos_own = [count][3] rows of
+ *                         charges first..first+count-1 only
+ *   se_shard_near         on `stream` (may run concurrently with the grid
+ *                         pipeline on the plan's stream): near-field sums of
+ *                         the first nt of ns sources (the charges this rank
+ *                         owns by cell; the rest are its halo) with all ns
+ *                         charges and their mirror images as sources;
+ *                         d_out [4][nt] (phi, E); gauge != 0: also the point
+ *                         kernel sum at the origin (device scalar d_near0,
+ *                         the gauge's near part, to be summed over ranks);
+ *                         device int64 d_npairs: the pairs.  d_zsrc_min
+ *                         (device scalar, optional): the minimum z over ALL
+ *                         ranks' sources incl. mirror layers, so pairs at
+ *                         the exact cutoff are decided as the reference's
+ *                         single KD tree does (slab.py:120-131).  No host sync.
+ *   se_shard_charges_own  interpolation + finalisation of the own shard with
+ *                         the caller's near sums in shard order d_near_own
+ *                         [4][count] and the summed near0 (device scalar;
+ *                         zero surface charge only). */
+int se_shard_spread_own(se_plan* plan, const double* d_pos_own, int64_t n_all,
+                        int64_t first, int64_t count, uint32_t flags,
+                        double** d_rho, int64_t* rho_len);
+int se_shard_near(se_plan* plan, void* stream, const double* d_src_pos,
+                  const double* d_src_q, int64_t ns, int64_t nt, int gauge,
+                  const double* d_zsrc_min, double* d_out, double* d_near0,
+                  int64_t* d_npairs);
+int se_shard_charges_own(se_plan* plan, const double* d_pos_own,
+                         const double* d_near_own, const double* d_near0,
+                         double* d_phi, double* d_E, double* U_part,
+                         se_diag* diag);
+
 /* Distributed grid pipeline for a sharded solve: after
  * se_dist_setup(plan, rank, nranks, sizes) a rank's solve is
  *   se_shard_spread          -> caller: reduce-scatter  rho_full -> rho_slab

@@ -804,7 +804,7 @@ class OracleSlabSolver:
 
     def charge_phase(self, state, pos, q, first=0, count=None,
                      need_energy=True, need_forces=True, need_potential=True,
-                     subtract_self=False, cap=None):
+                     subtract_self=False, cap=None, near_ext=None, near0_ext=None):
         """Interpolation, near field, gauge and energy at the charges
         ``first .. first+count-1`` with every charge as a near-field source
         (slab.py:354-391).  Returns (phi, E, U_part, diag); the parts of U
@@ -818,8 +818,14 @@ class OracleSlabSolver:
         k0, psi_vals, stack = state["k0"], state["psi_vals"], state["fields"]
         pe, qe = pos[own], q[own]
         far = self.grid.interpolate(stack, pe, par.g_t, par.H_E, par.H_E)
-        nf = NearSources(pos, q, geo, par)
-        if need_forces:
+        nf = NearSources(pos, q, geo, par) if near_ext is None else None
+        if near_ext is not None:
+            # near-field sums supplied by the caller (the cell-routed sharded
+            # solve computes them on the rank owning each charge's cell)
+            phi_near = near_ext[0]
+            e_near = np.stack(near_ext[1:4], axis=1) if need_forces else None
+            e_bar = far[1:4].T + e_near if need_forces else np.zeros((pe.shape[0], 3))
+        elif need_forces:
             phi_near, e_near = nf.evaluate(pe, "avg",
                                            subtract_unsplit=subtract_self)
             e_bar = far[1:4].T + e_near
@@ -837,7 +843,8 @@ class OracleSlabSolver:
         if need_potential and not np.isinf(par.xi):
             origin = np.zeros((1, 3))
             far0 = self.interp_gamma(psi_vals, origin)[0]
-            near0 = nf.evaluate(origin, "point", need_field=False)[0]
+            near0 = near0_ext if near_ext is not None else \
+                nf.evaluate(origin, "point", need_field=False)[0]
             b_i = -(far0 + near0)
             phi_bar = phi_bar + b_i
 

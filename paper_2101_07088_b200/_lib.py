@@ -37,7 +37,8 @@ EXPORTS = ("se_plan_create", "se_plan_destroy", "se_plan_set_stream",
            "se_dist_modes", "se_dist_fields", "se_steric_forces",
            "se_tp_create", "se_tp_destroy", "se_tp_set_stream", "se_tp_poisson",
            "se_tp_forces", "se_tp_forces_device", "se_steric_forces_device",
-           "se_bd_first_noise_device", "se_bd_step_device")
+           "se_bd_first_noise_device", "se_bd_step_device", "se_shard_spread_own",
+           "se_shard_near", "se_shard_charges_own")
 
 
 class SeBdParams(ctypes.Structure):
@@ -121,6 +122,14 @@ def load():
     lib.se_shard_charges.argtypes = [_P, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.c_void_p, _D, ctypes.POINTER(SeDiag)]
     lib.se_shard_charges.restype = ctypes.c_int
+    _v = ctypes.c_void_p
+    lib.se_shard_spread_own.argtypes = [_P, _v, _I64, _I64, _I64, ctypes.c_uint32,
+                                        ctypes.POINTER(ctypes.c_void_p), _I64P]
+    lib.se_shard_spread_own.restype = ctypes.c_int
+    lib.se_shard_near.argtypes = [_P, _v, _v, _v, _I64, _I64, ctypes.c_int, _v, _v, _v, _v]
+    lib.se_shard_near.restype = ctypes.c_int
+    lib.se_shard_charges_own.argtypes = [_P, _v, _v, _v, _v, _v, _D, ctypes.POINTER(SeDiag)]
+    lib.se_shard_charges_own.restype = ctypes.c_int
     lib.se_dist_setup.argtypes = [_P, ctypes.c_int, ctypes.c_int, _I64P]
     lib.se_dist_setup.restype = ctypes.c_int
     lib.se_dist_buffers.argtypes = [_P, ctypes.POINTER(ctypes.c_void_p)]
@@ -152,7 +161,8 @@ def load():
         getattr(lib, name).restype = ctypes.c_int
     for name in ("se_tp_create", "se_tp_destroy", "se_tp_set_stream", "se_tp_poisson",
                  "se_tp_forces", "se_tp_forces_device", "se_steric_forces_device",
-           "se_bd_first_noise_device", "se_bd_step_device"):
+           "se_bd_first_noise_device", "se_bd_step_device", "se_shard_spread_own",
+           "se_shard_near", "se_shard_charges_own"):
         getattr(lib, name).restype = ctypes.c_int
     lib.se_fp64_peak.argtypes = [ctypes.c_int, _D]
     lib.se_fp64_peak.restype = ctypes.c_int

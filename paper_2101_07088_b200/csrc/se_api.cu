@@ -111,6 +111,7 @@ void phase_spread(Plan* p, const double* d_pos, int64_t n_all, int64_t first, in
     Solve& S = current(p);
     S.phase = 0;
     S.flags = flags;
+    S.near_external = false;
     S.n_all = n_all; S.first = first; S.count = count;
     S.xi_inf = P.xi_is_inf != 0.0;
     S.forces = flags & SE_NEED_FORCES;
@@ -202,7 +203,12 @@ void phase_charges(Plan* p, const double* d_pos, double* d_phi_out, double* d_E_
         SE_CUDA(cudaMemsetAsync(p->d_phash, 0, 16 * (size_t)std::max<int64_t>(count, 1), s));
         p->phash_n = count;
     }
-    if (!S.near_empty) {
+    if (S.near_external) {
+        // routed by cell: the caller's sums for this shard (se_shard_near)
+        if (count > 0)
+            SE_CUDA(cudaMemcpyAsync(p->d_near, S.ext_near, sizeof(double) * 4 * (size_t)count,
+                                    cudaMemcpyDeviceToDevice, s));
+    } else if (!S.near_empty) {
         build_cells(p, d_pos, p->d_q, n, true);           // sources: every charge
         near_eval(p, d_pos + 3 * first, nullptr, count, kavg, p->d_near, p->d_count);
     } else {
@@ -214,7 +220,15 @@ void phase_charges(Plan* p, const double* d_pos, double* d_phi_out, double* d_E_
         const double w = 0.5 / P.xi;
         const double rad = (P.H_E / P.g_t) * w;
         interp_points(p, p->d_origin, 1, w, rad, p->d_scal + 4);
-        if (!S.near_empty) near_eval(p, p->d_origin, nullptr, 1, kpt, p->d_scal + 5, nullptr);
+        if (S.near_external) {
+            if (S.ext_near0)
+                SE_CUDA(cudaMemcpyAsync(p->d_scal + 5, S.ext_near0, sizeof(double),
+                                        cudaMemcpyDeviceToDevice, s));
+            else
+                SE_CUDA(cudaMemsetAsync(p->d_scal + 5, 0, sizeof(double), s));
+        }
+        else if (!S.near_empty)
+            near_eval(p, p->d_origin, nullptr, 1, kpt, p->d_scal + 5, nullptr);
         gauge_kernel<<<1, 1, 0, s>>>(p->d_scal);
         SE_LAUNCHED(p);
     }
@@ -224,6 +238,8 @@ void phase_charges(Plan* p, const double* d_pos, double* d_phi_out, double* d_E_
     if (count > 0) finalize(p, first, count, S.flags, self_inf, d_phi_out, d_E_out);
     // the wall-charge energy is global: the shard holding charge 0 adds it
     if (S.energy && !p->sigma_zero && first == 0) {
+        if (S.near_external)
+            throw Error(SE_ERR_VALUE, "the cell-routed near field needs a zero surface charge");
         if (S.xi_inf) throw Error(SE_ERR_VALUE, "wall-charge energy needs a finite xi");
         if (S.near_empty) p->cl.n = 0;
         wall_energy(p, kpt);
@@ -830,6 +846,86 @@ int se_shard_charges(se_plan* plan, const double* d_pos_all, double* d_phi, doub
         phase_results(p, U_part, diag);
         return SE_OK;
     } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+// ---- sharded solve with positions of the own shard only and the near field
+// routed by cell.  The library indexes charges
+// globally; the own-shard positions are addressed through a base pointer
+// offset by -first rows, of which only rows [first, first + count) are read.
+int se_shard_spread_own(se_plan* plan, const double* d_pos_own, int64_t n_all, int64_t first,
+                        int64_t count, uint32_t flags, double** d_rho, int64_t* rho_len) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        SE_CUDA(cudaSetDevice(p->dev));
+        p->g32 = false;
+        const double* base = d_pos_own - 3 * first;
+        phase_spread(p, base, n_all, first, count, flags);
+        if (d_rho) *d_rho = p->d_rho;
+        if (rho_len) *rho_len = 2 * p->G;
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
+int se_shard_near(se_plan* plan, void* stream, const double* d_src_pos, const double* d_src_q,
+                  int64_t ns, int64_t nt, int gauge, const double* d_zsrc_min, double* d_out,
+                  double* d_near0, int64_t* d_npairs) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    cudaStream_t saved = p ? p->stream : nullptr;
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        if (nt < 0 || nt > ns) throw Error(SE_ERR_VALUE, "targets must be the first sources");
+        SE_CUDA(cudaSetDevice(p->dev));
+        const se_params& P = p->P;
+        const Solve& S = p->solve;
+        if (S.phase == 0) throw Error(SE_ERR_CUDA, "se_shard_near outside a sharded solve");
+        if (S.xi_inf) throw Error(SE_ERR_VALUE, "no near field at xi = inf");
+        p->stream = reinterpret_cast<cudaStream_t>(stream);
+        const bool timing = p->timing;
+        p->timing = false;
+        p->pair_hash = false;
+        if (d_npairs) SE_CUDA(cudaMemsetAsync(d_npairs, 0, sizeof(int64_t), p->stream));
+        if (d_near0) SE_CUDA(cudaMemsetAsync(d_near0, 0, sizeof(double), p->stream));
+        NearKernel kavg = kernel_of(P, 0, S.forces, S.flags & SE_SUBTRACT_SELF);
+        kavg.fp32 = (S.flags & SE_FP32) ? 1 : 0;
+        if (ns > 0) {
+            build_cells(p, d_src_pos, d_src_q, ns, true, d_zsrc_min);
+            near_eval(p, d_src_pos, nullptr, nt, kavg, d_out, d_npairs);
+            if (gauge && d_near0)
+                near_eval(p, p->d_origin, nullptr, 1, kernel_of(P, 1, false, false), d_near0,
+                          nullptr);
+        }
+        p->timing = timing;
+        p->stream = saved;
+        return SE_OK;
+    } catch (const Error& e) {
+        if (p) p->stream = saved;
+        return fail(e);
+    }
+}
+
+int se_shard_charges_own(se_plan* plan, const double* d_pos_own, const double* d_near_own,
+                         const double* d_near0, double* d_phi, double* d_E, double* U_part,
+                         se_diag* diag) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    try {
+        if (!p) throw Error(SE_ERR_VALUE, "null plan");
+        SE_CUDA(cudaSetDevice(p->dev));
+        Solve& S = p->solve;
+        S.near_external = true;
+        S.ext_near = d_near_own;
+        S.ext_near0 = d_near0;
+        const double* base = d_pos_own - 3 * S.first;
+        phase_charges(p, base, d_phi, d_E);
+        phase_results(p, U_part, diag);
+        S.near_external = false;
+        return SE_OK;
+    } catch (const Error& e) {
+        p->solve.near_external = false;
         return fail(e);
     }
 }

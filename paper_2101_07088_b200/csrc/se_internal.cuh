@@ -151,6 +151,12 @@ struct NearScratch {
 // state of one solve between its phases (se_api.cu)
 struct Solve {
     uint32_t flags = 0;
+    // sharded solve with the near field routed by cell: the caller supplies
+    // the near-field sums of this shard's charges (se_shard_near) and the
+    // near part of the gauge (summed over ranks)
+    bool near_external = false;
+    const double* ext_near = nullptr;     // [4][count]
+    const double* ext_near0 = nullptr;    // device scalar
     bool xi_inf = false, forces = false, potential = false, energy = false, corr = false,
          two = false, near_empty = true;
     int mode = 0;
@@ -393,7 +399,8 @@ struct NearKernel {
     int need_field;
     int fp32;            // far pairs in single precision (SE_FP32)
 };
-void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, bool in_domain);
+void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, bool in_domain,
+                 const double* d_zsrc_min = nullptr);
 void near_eval(Plan* p, const double* d_eval, const int* d_eval_order,
                int64_t ne, const NearKernel& k, double* d_out4,
                int64_t* d_npairs);

@@ -97,10 +97,14 @@ __global__ void zrange_kernel(const double4* s, int64_t ns, double* mm) {
     }
 }
 
-// the reference's tree z origin: min(source z) - r_cut - 1 (slab.py:120)
-__global__ void zmin_kernel(const double* mm, int nblk, double r_cut, double* zmin) {
+// the reference's tree z origin: min(source z) - r_cut - 1 (slab.py:120);
+// zsrc (optional): the minimum over ALL sources when this cell list holds a
+// rank's share of them (the cell-routed sharded near field)
+__global__ void zmin_kernel(const double* mm, int nblk, double r_cut, const double* zsrc,
+                            double* zmin) {
     double lo = 1e300;
-    for (int b = 0; b < nblk; ++b) lo = fmin(lo, mm[2 * b]);
+    if (zsrc) lo = *zsrc;
+    else for (int b = 0; b < nblk; ++b) lo = fmin(lo, mm[2 * b]);
     *zmin = __dsub_rn(__dsub_rn(lo, r_cut), 1.0);
 }
 
@@ -1227,7 +1231,8 @@ static CellGeo cell_geo(const Plan* p) {
     return g;
 }
 
-void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, bool in_domain) {
+void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, bool in_domain,
+                 const double* d_zsrc_min) {
     const double eps = p->P.eps;
     const double fb = -(p->P.eps_b - eps) / (p->P.eps_b + eps);
     const double ft = -(p->P.eps_t - eps) / (p->P.eps_t + eps);
@@ -1270,7 +1275,7 @@ void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, boo
     if (!p->d_mm) p->d_mm = dalloc<double>(p, 256);
     zrange_kernel<<<64, 256, 0, p->stream>>>(p->d_near_src, ns, p->d_mm);
     SE_LAUNCHED(p);
-    zmin_kernel<<<1, 1, 0, p->stream>>>(p->d_mm, 64, p->P.r_cut, p->d_mm + 200);
+    zmin_kernel<<<1, 1, 0, p->stream>>>(p->d_mm, 64, p->P.r_cut, d_zsrc_min, p->d_mm + 200);
     SE_LAUNCHED(p);
     double zmin = 1e300, zmax = -1e300;
     if (in_domain) {

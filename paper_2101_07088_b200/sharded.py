@@ -65,6 +65,49 @@ def shard_range(n, rank, world):
     return first, last - first
 
 
+def cell_destinations(x, Lx, world, halo):
+    """Ranks that need each charge for the cell-routed near field: the owner
+    of its x slab ([r Lx/P, (r+1) Lx/P), as a target) and the slabs within
+    ``halo`` of it across a slab face (as a source; periodic in x).
+    Returns (charge index, destination rank, is_target) rows, each charge
+    sent at most once to a rank.  Needs a slab width >= halo."""
+    w = Lx / world
+    xw = torch.remainder(x, Lx)
+    owner = torch.clamp((xw / w).floor().to(torch.int64), 0, world - 1)
+    idx = torch.arange(x.shape[0], device=x.device)
+    rows = [(idx, owner, torch.ones_like(owner, dtype=torch.bool))]
+    if world > 1:
+        lo = owner.to(x.dtype) * w
+        left = (owner - 1) % world
+        right = (owner + 1) % world
+        near_lo = (xw - lo) < halo
+        near_hi = (lo + w - xw) <= halo
+        rows.append((idx[near_lo], left[near_lo], torch.zeros_like(left[near_lo], dtype=torch.bool)))
+        # with two ranks the right neighbour is the left one: send once
+        keep = near_hi & ~(near_lo & (right == left))
+        rows.append((idx[keep], right[keep], torch.zeros_like(right[keep], dtype=torch.bool)))
+    ci = torch.cat([r[0] for r in rows])
+    dest = torch.cat([r[1] for r in rows])
+    tgt = torch.cat([r[2] for r in rows])
+    return ci, dest, tgt
+
+
+def _exchange(rows, dest, world, group):
+    """all-to-all of float64 record rows by destination rank (sorted send,
+    counts exchanged first).  Returns the received rows."""
+    order = torch.argsort(dest, stable=True)
+    rows = rows[order].contiguous()
+    counts = torch.bincount(dest, minlength=world)
+    if world == 1:
+        return rows
+    recv_counts = torch.empty_like(counts)
+    dist.all_to_all_single(recv_counts, counts, group=group)
+    sc, rc = counts.tolist(), recv_counts.tolist()
+    out = torch.empty((sum(rc), rows.shape[1]), dtype=rows.dtype, device=rows.device)
+    dist.all_to_all_single(out, rows, output_split_sizes=rc, input_split_sizes=sc, group=group)
+    return out
+
+
 class _DeviceArray:
     """Zero-copy view of a library-owned device buffer for torch."""
 
@@ -151,6 +194,44 @@ class CudaShardEngine:
             ctypes.byref(U), ctypes.byref(diag)))
         return phi, E, float(U.value), diag
 
+    # -- cell-routed near field (near="cell") ---------------------------
+    def spread_own(self, pos_own, first, count, flags):
+        ptr = ctypes.c_void_p()
+        size = ctypes.c_int64()
+        _lib.check(self._lib.se_shard_spread_own(
+            self.solver._plan, ctypes.c_void_p(pos_own.data_ptr()), self.solver._q.size,
+            first, count, flags, ctypes.byref(ptr), ctypes.byref(size)))
+        return torch.as_tensor(_DeviceArray(ptr.value, size.value), device=self.device)
+
+    def near(self, src_pos, src_q, nt, gauge, zsrc_min, stream=None):
+        """Near-field sums at the first ``nt`` of the routed sources, on
+        ``stream`` (concurrent with the grid pipeline)."""
+        out = torch.empty((4, max(nt, 1)), dtype=torch.float64, device=self.device)
+        near0 = torch.zeros(1, dtype=torch.float64, device=self.device)
+        npairs = torch.zeros(1, dtype=torch.int64, device=self.device)
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        _lib.check(self._lib.se_shard_near(
+            self.solver._plan, ctypes.c_void_p(st), ctypes.c_void_p(src_pos.data_ptr()),
+            ctypes.c_void_p(src_q.data_ptr()), src_pos.shape[0], nt, 1 if gauge else 0,
+            ctypes.c_void_p(zsrc_min.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+            ctypes.c_void_p(near0.data_ptr()), ctypes.c_void_p(npairs.data_ptr())))
+        return out[:, :nt], near0, npairs
+
+    def charges_own(self, pos_own, near_own, near0, need_forces):
+        count = pos_own.shape[0]
+        phi = torch.empty(count, dtype=torch.float64, device=self.device)
+        E = torch.zeros((count, 3), dtype=torch.float64, device=self.device)
+        near_own = near_own.contiguous()
+        U = ctypes.c_double(0.0)
+        diag = _lib.SeDiag()
+        _lib.check(self._lib.se_shard_charges_own(
+            self.solver._plan, ctypes.c_void_p(pos_own.data_ptr()),
+            ctypes.c_void_p(near_own.data_ptr()), ctypes.c_void_p(near0.data_ptr()),
+            ctypes.c_void_p(phi.data_ptr()),
+            ctypes.c_void_p(E.data_ptr() if need_forces else 0),
+            ctypes.byref(U), ctypes.byref(diag)))
+        return phi, E, float(U.value), diag
+
     def diagnostics(self, diag):
         return self.solver._diagnostics(diag)
 
@@ -163,7 +244,8 @@ class ShardedSlabSolver:
     the same system; ``solve`` returns the full result on every rank."""
 
     def __init__(self, system, params, threads=1, refine=1, group=None,
-                 device=None, engine=None, precision="fp64", decompose=False):
+                 device=None, engine=None, precision="fp64", decompose=False,
+                 near="index"):
         if not dist.is_initialized():
             raise RuntimeError("ShardedSlabSolver needs torch.distributed "
                                "initialised (one process per GPU)")
@@ -183,8 +265,20 @@ class ShardedSlabSolver:
         self.engine = engine
         self.precision = precision
         self.decompose = decompose
+        if near not in ("index", "cell"):
+            raise ValueError("near must be 'index' or 'cell'")
+        geo = system.geometry
+        # the cell-routed near field: x slabs of width Lx / P, halo r_cut
+        # (the query radius of the charges; the gauge's r_nf is smaller)
+        self.halo = float(params.r_cut)
+        if near == "cell" and (geo.Lx / self.world < self.halo or
+                               not system.surface.is_zero or np.isinf(params.xi)):
+            raise ValueError("near='cell' needs Lx / ranks >= r_cut, zero surface "
+                             "charge and a finite xi")
+        self.near_mode = near
         self.buf = engine.dist_setup(self.rank, self.world) if self.decompose else None
         self.last_timings = None
+        self._side = None
 
     def close(self):
         self.engine.close()
@@ -223,6 +317,118 @@ class ShardedSlabSolver:
             u = torch.tensor([u_part], dtype=torch.float64, device=phi.device)
             dist.all_reduce(u, group=self.group)
             U = float(u.item())
+        if timings and hasattr(diag, "t_ms"):
+            self.last_timings = dict(zip(STAGES, list(diag.t_ms)[:len(STAGES)]))
+        return phi, E, U, diag
+
+    # -- cell-routed near field --------------------------------------------
+    def _route_sources(self, pos_own):
+        """Send each own charge to the rank owning its x slab (target) and to
+        the neighbouring slabs within r_cut (halo source).  Returns the
+        received (positions [ns][3], charges [ns], global indices of the
+        nt targets), targets first."""
+        dev = pos_own.device
+        q = torch.as_tensor(self.system.charges[self.first:self.first + self.count],
+                            dtype=torch.float64, device=dev)
+        gidx = torch.arange(self.first, self.first + self.count, dtype=torch.float64,
+                            device=dev)
+        ci, dest, tgt = cell_destinations(pos_own[:, 0], self.system.geometry.Lx,
+                                          self.world, self.halo)
+        rows = torch.cat([pos_own[ci], q[ci, None], gidx[ci, None],
+                          tgt[:, None].to(torch.float64)], dim=1)
+        got = _exchange(rows, dest, self.world, self.group)
+        order = torch.argsort(-got[:, 5], stable=True)          # targets first
+        got = got[order]
+        nt = int((got[:, 5] > 0.5).sum().item())
+        return (got[:, 0:3].contiguous(), got[:, 3].contiguous(),
+                got[:nt, 4].to(torch.int64))
+
+    def _route_back(self, near_t, tgt_gidx):
+        """Near sums of this rank's targets -> the ranks holding those
+        charges' index shards, in shard order ([4][count])."""
+        dev = near_t.device
+        firsts = torch.tensor([shard_range(self.system.charges.size, r, self.world)[0]
+                               for r in range(self.world)], dtype=torch.int64, device=dev)
+        dest = torch.searchsorted(firsts, tgt_gidx, right=True) - 1
+        rows = torch.cat([tgt_gidx[:, None].to(torch.float64), near_t.T], dim=1)
+        got = _exchange(rows, dest, self.world, self.group)
+        out = torch.zeros((4, self.count), dtype=torch.float64, device=dev)
+        out[:, got[:, 0].to(torch.int64) - self.first] = got[:, 1:5].T
+        return out
+
+    def _zsrc_min(self, pos_own):
+        """Minimum z over all near-field sources of all ranks (charges and
+        mirror layers), the reference KD tree's z origin (slab.py:120)."""
+        geo = self.system.geometry
+        z = pos_own[:, 2]
+        dev = pos_own.device
+        big = torch.tensor(1e300, dtype=torch.float64, device=dev)
+        zmin = z.min() if z.numel() else big
+        zmax = z.max() if z.numel() else -big
+        t = torch.stack([zmin, -zmax])
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        zmin, zmax = t[0], -t[1]
+        cands = [zmin]
+        if geo.eps_b != geo.eps:
+            cands.append(-zmax)
+        if geo.eps_t != geo.eps:
+            cands.append(2.0 * geo.H - zmax)
+        return torch.stack(cands).min().reshape(1)
+
+    def solve_shard_own(self, pos_own, need_energy=True, need_forces=True,
+                        need_potential=True, subtract_self=False,
+                        include_correction=True, force_general=False, timings=False):
+        """The sharded solve with only this rank's index-shard positions
+        (``pos_own`` [count][3] on the engine's device) and the near field
+        routed by cell: the routed near field runs on a side stream while
+        the grid pipeline's collectives and kernels run on the main one.
+        Returns (phi, E, U, diag) of the own shard; diag["n_pairs"] summed."""
+        flags = _flags(need_energy, need_forces, need_potential,
+                       subtract_self, include_correction, force_general,
+                       timings, self.precision == "fp32")
+        rho = self.engine.spread_own(pos_own, self.first, self.count, flags)
+        src_pos, src_q, tgt_gidx = self._route_sources(pos_own)
+        zsrc = self._zsrc_min(pos_own)
+        nt = int(tgt_gidx.numel())
+        gauge = need_potential and self.rank == 0     # rank 0's slab holds x = 0
+        cuda = pos_own.is_cuda
+        if cuda:
+            main = torch.cuda.current_stream(pos_own.device)
+            if self._side is None:
+                self._side = torch.cuda.Stream(pos_own.device)
+            self._side.wait_stream(main)
+            with torch.cuda.stream(self._side):
+                near_t, near0, npairs = self.engine.near(src_pos, src_q, nt, gauge, zsrc,
+                                                         self._side)
+        else:
+            near_t, near0, npairs = self.engine.near(src_pos, src_q, nt, gauge, zsrc)
+        if self.decompose:
+            self._grid_pipeline_distributed()
+        else:
+            if self.world > 1:
+                dist.all_reduce(rho, group=self.group)
+            self.engine.fields()
+        if cuda:
+            main.wait_stream(self._side)
+        near_own = self._route_back(near_t, tgt_gidx)
+        stat = torch.cat([near0.reshape(1), npairs.to(torch.float64).reshape(1)])
+        if self.world > 1:
+            dist.all_reduce(stat, group=self.group)
+        try:
+            phi, E, u_part, diag = self.engine.charges_own(pos_own, near_own, stat[0:1],
+                                                           need_forces)
+            err = None
+        except (ValueError, FloatingPointError, ArithmeticError, MemoryError,
+                RuntimeError) as exc:
+            err = exc
+        self._agree(err)
+        U = u_part
+        if self.world > 1:
+            u = torch.tensor([u_part], dtype=torch.float64, device=phi.device)
+            dist.all_reduce(u, group=self.group)
+            U = float(u.item())
+        self.last_pairs = int(stat[1].item())
         if timings and hasattr(diag, "t_ms"):
             self.last_timings = dict(zip(STAGES, list(diag.t_ms)[:len(STAGES)]))
         return phi, E, U, diag
@@ -278,14 +484,23 @@ class ShardedSlabSolver:
             raise ValueError("positions must be (N, 3)")
         if pos.shape[0] != self.system.charges.size:
             raise ValueError("positions and charges disagree on N")
-        pos_all = self.engine.positions(pos)
-        phi, E, U, diag = self.solve_shard(
-            pos_all, need_energy, need_forces, need_potential, subtract_self,
-            include_correction, force_general, timings)
+        if self.near_mode == "cell":
+            # only this rank's index shard goes to the device
+            pos_own = self.engine.positions(pos[self.first:self.first + self.count])
+            phi, E, U, diag = self.solve_shard_own(
+                pos_own, need_energy, need_forces, need_potential, subtract_self,
+                include_correction, force_general, timings)
+        else:
+            pos_all = self.engine.positions(pos)
+            phi, E, U, diag = self.solve_shard(
+                pos_all, need_energy, need_forces, need_potential, subtract_self,
+                include_correction, force_general, timings)
         phi_all = self._gather(phi.reshape(-1, 1), 1).reshape(-1)
         E_all = self._gather(E, 3) if need_forces else \
             torch.zeros((pos.shape[0], 3), dtype=torch.float64)
         out = self.engine.diagnostics(diag)
+        if self.near_mode == "cell" and isinstance(out, dict):
+            out["n_pairs"] = self.last_pairs
         if timings and self.last_timings is not None:
             out["timings_ms"] = self.last_timings
         return SolveResult(phi_bar=phi_all.cpu().numpy(),

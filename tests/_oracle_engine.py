@@ -44,6 +44,46 @@ class OracleShardEngine:
             bool(f & _lib.NEED_POTENTIAL), bool(f & _lib.SUBTRACT_SELF))
         return torch.from_numpy(phi), torch.from_numpy(np.asarray(E)), U, diag
 
+    # -- cell-routed near field (ShardedSlabSolver(near="cell")) ----------
+    device = torch.device("cpu")
+
+    def spread_own(self, pos_own, first, count, flags):
+        self.flags, self.first, self.count = flags, first, count
+        self.pos_own = pos_own.numpy()
+        own = slice(first, first + count)
+        rho = self.oracle.spread_phase(
+            self.pos_own, self.q[own],
+            bool(flags & _lib.CORRECTION), bool(flags & _lib.FORCE_GENERAL))
+        self.shape = rho.shape
+        self.rho = torch.from_numpy(np.ascontiguousarray(rho)).reshape(-1)
+        return self.rho
+
+    def near(self, src_pos, src_q, nt, gauge, zsrc_min, stream=None):
+        sp, sq = src_pos.numpy(), src_q.numpy()
+        nf = O.NearSources(sp, sq, self.oracle.system.geometry, self.oracle.params)
+        out = np.zeros((4, nt))
+        if nt:
+            phi, E = nf.evaluate(sp[:nt], "avg",
+                                 subtract_unsplit=bool(self.flags & _lib.SUBTRACT_SELF))
+            out[0], out[1:4] = phi, np.asarray(E).T
+        near0 = 0.0
+        if gauge:
+            near0 = nf.evaluate(np.zeros((1, 3)), "point", need_field=False)[0]
+        return (torch.from_numpy(out), torch.tensor([near0], dtype=torch.float64),
+                torch.tensor([0], dtype=torch.int64))
+
+    def charges_own(self, pos_own, near_own, near0, need_forces):
+        f = self.flags
+        n = self.q.size
+        pos = np.zeros((n, 3))
+        pos[self.first:self.first + self.count] = pos_own.numpy()
+        phi, E, U, diag = self.oracle.charge_phase(
+            self.state, pos, self.q, self.first, self.count,
+            bool(f & _lib.NEED_ENERGY), need_forces, bool(f & _lib.NEED_POTENTIAL),
+            bool(f & _lib.SUBTRACT_SELF), near_ext=near_own.numpy(),
+            near0_ext=float(near0.reshape(-1)[0]))
+        return torch.from_numpy(phi), torch.from_numpy(np.asarray(E)), U, diag
+
     def diagnostics(self, diag):
         return diag
 

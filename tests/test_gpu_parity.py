@@ -332,8 +332,9 @@ def test_sharded_phases_one_gpu(case, world):
         e.close()
 
 
-@pytest.mark.parametrize("decompose", [False, True])
-def test_sharded_solver_one_rank(decompose):
+@pytest.mark.parametrize("decompose,near", [(False, "index"), (True, "index"),
+                                            (True, "cell")])
+def test_sharded_solver_one_rank(decompose, near):
     import socket
     import torch.distributed as dist
     from paper_2101_07088_b200.sharded import ShardedSlabSolver
@@ -345,7 +346,8 @@ def test_sharded_solver_one_rank(decompose):
                             rank=0, world_size=1)
     try:
         system, params, kw = variant_problem("c2n256")
-        solver = ShardedSlabSolver(system, params, device=0, decompose=decompose)
+        solver = ShardedSlabSolver(system, params, device=0, decompose=decompose,
+                                   near=near)
         res = solver.solve(**kw)
         g = solves()["c2n256"]
         assert rel_l2(res.phi_bar, g["phi"]) < TOL
@@ -354,6 +356,53 @@ def test_sharded_solver_one_rank(decompose):
         solver.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_cell_routed_near_field_one_gpu(ranks):
+    """The cell-routed near field of P virtual ranks on one GPU: each rank's
+    sources are the charges routed to it (its x slab + r_cut halo), its
+    targets those it owns; the assembled near sums, with the index-sharded
+    grid pipeline of one plan, reproduce the reference solve (C3, jumps at
+    both walls) and the single-GPU pair count."""
+    import torch
+    from paper_2101_07088_b200 import _lib
+    from paper_2101_07088_b200.sharded import CudaShardEngine, cell_destinations
+    from paper_2101_07088_b200.slab import _flags
+    g = solves()["c3"]
+    system, params = W.build("c3")
+    n = system.n
+    ref_pairs = _solver(system, params).solve().diagnostics["n_pairs"]
+    eng = CudaShardEngine(system, params, device=0)
+    dev = eng.device
+    pos = torch.as_tensor(system.positions, device=dev)
+    q = torch.as_tensor(system.charges, device=dev)
+    flags = _flags(True, True, True, False, True, False)
+    eng.spread_own(pos, 0, n, flags)
+    ci, dest, tgt = cell_destinations(pos[:, 0], system.geometry.Lx, ranks,
+                                      float(params.r_cut))
+    geo = system.geometry
+    zmin = torch.stack([pos[:, 2].min(), -pos[:, 2].max(),
+                        2 * geo.H - pos[:, 2].max()]).min().reshape(1)
+    near = torch.zeros((4, n), dtype=torch.float64, device=dev)
+    near0 = torch.zeros(1, dtype=torch.float64, device=dev)
+    pairs = 0
+    for r in range(ranks):
+        mine = dest == r
+        idx = torch.cat([ci[mine & tgt], ci[mine & ~tgt]])
+        nt = int((mine & tgt).sum())
+        out, n0, npairs = eng.near(pos[idx].contiguous(), q[idx].contiguous(), nt,
+                                   r == 0, zmin)
+        near[:, idx[:nt]] = out
+        near0 += n0
+        pairs += int(npairs.item())
+    eng.fields()
+    phi, E, U, diag = eng.charges_own(pos, near, near0, True)
+    assert pairs == ref_pairs
+    assert rel_l2(phi.cpu().numpy(), g["phi"]) < TOL
+    assert rel_l2(E.cpu().numpy(), g["E"]) < TOL
+    assert abs(U - float(g["U"])) <= TOL * max(1.0, abs(float(g["U"])))
+    eng.close()
 
 
 def test_shard_phase_order():

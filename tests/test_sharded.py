@@ -27,7 +27,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, cases, outdir):
+def _worker(rank, world, port, cases, outdir, near="index"):
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     for p in (here, os.path.dirname(here)):
@@ -43,7 +43,7 @@ def _worker(rank, world, port, cases, outdir):
             system, params, kw = variant_problem(case)
             refine = kw.pop("refine", 1)
             eng = OracleShardEngine(system, params, refine=refine)
-            solver = ShardedSlabSolver(system, params, engine=eng)
+            solver = ShardedSlabSolver(system, params, engine=eng, near=near)
             res = solver.solve(**kw)
             out[case] = (res.phi_bar, res.E_bar, res.U,
                          res.diagnostics["B_i"], solver.first, solver.count)
@@ -64,10 +64,14 @@ def test_shard_ranges_cover():
             assert max(c for _, c in got) - min(c for _, c in got) <= 1
 
 
-@pytest.mark.parametrize("world,cases", [(2, CASES),
-                                         (3, ["c3n256_gauss_sigma"])])
-def test_sharded_matches_golden(tmp_path, world, cases):
-    mp.spawn(_worker, args=(world, _free_port(), cases, str(tmp_path)),
+@pytest.mark.parametrize("world,cases,near", [(2, CASES, "index"),
+                                              (3, ["c3n256_gauss_sigma"], "index"),
+                                              (2, ["c2n256", "c2n256_noforce"], "cell"),
+                                              (3, ["c2n256_nocorr"], "cell")])
+def test_sharded_matches_golden(tmp_path, world, cases, near):
+    """Index-sharded spread; near field either with every charge as a source
+    on every rank (index) or routed by x slab with an r_cut halo (cell)."""
+    mp.spawn(_worker, args=(world, _free_port(), cases, str(tmp_path), near),
              nprocs=world, join=True)
     gold = solves()
     ranks = []
@@ -176,3 +180,27 @@ def test_sharded_error_on_one_rank_raises_everywhere(tmp_path):
         assert txt.startswith("ValueError"), (r, txt)
     assert "outside the extended z domain" in (tmp_path / "fault1.txt").read_text()
     assert "rank 1" in (tmp_path / "fault0.txt").read_text()
+
+
+def test_cell_destinations_cover_every_neighbour():
+    """Every charge is a target on exactly one rank, and every charge within
+    r_cut (periodic in x) of a target is among that rank's sources."""
+    import torch
+    from paper_2101_07088_b200.sharded import cell_destinations
+    rng = np.random.default_rng(5)
+    L, halo = 2.0, 0.3
+    x = rng.uniform(0, L, 4000)
+    x[:4] = [0.0, L - 1e-12, 0.5 * L, 0.3]        # faces and exact boundaries
+    for world in (1, 2, 3, 6):
+        ci, dest, tgt = cell_destinations(torch.from_numpy(x), L, world, halo)
+        ci, dest, tgt = ci.numpy(), dest.numpy(), tgt.numpy()
+        assert np.array_equal(np.sort(ci[tgt]), np.arange(x.size))
+        pairs = set(zip(ci.tolist(), dest.tolist()))
+        assert len(pairs) == ci.size                  # never twice to a rank
+        owner = dict(zip(ci[tgt].tolist(), dest[tgt].tolist()))
+        sample = rng.choice(x.size, 300, replace=False)
+        for i in sample:
+            d = np.abs(x - x[i])
+            d = np.minimum(d, L - d)
+            for j in np.nonzero(d <= halo)[0]:
+                assert (int(j), owner[int(i)]) in pairs
