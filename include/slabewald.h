@@ -50,6 +50,11 @@ extern "C" {
                                           the exact fp64 test); results within
                                           the run's Ewald tolerance */
 
+#define SE_GRAPH           (1u << 9)   /* capture the solve as a CUDA graph
+                                          (after one warm solve with the same
+                                          buffers, size and flags) and replay
+                                          it while those repeat: no per-kernel
+                                          launch cost (BD loops, small N) */
 #define SE_PAIR_HASH       (1u << 8)   /* record the near-field pair SET of the
                                           charges (se_debug_fetch 6) for
                                           parity tests */

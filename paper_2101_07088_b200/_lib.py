@@ -26,6 +26,7 @@ FORCE_GENERAL = 1 << 5
 TIMINGS = 1 << 6
 FP32 = 1 << 7
 PAIR_HASH = 1 << 8
+GRAPH = 1 << 9
 
 #: every entry point declared in include/slabewald.h
 EXPORTS = ("se_plan_create", "se_plan_destroy", "se_plan_set_stream",

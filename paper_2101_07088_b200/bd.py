@@ -270,7 +270,8 @@ class DeviceBd:
         s, g = self.steric, self.geo
         for _ in range(steps):
             self.solver.solve_device(self.pos.data_ptr(), self.phi.data_ptr(),
-                                     self.E.data_ptr(), self.n, need_energy=False)
+                                     self.E.data_ptr(), self.n, need_energy=False,
+                                     graph=True)
             _lib.check(lib.se_steric_forces_device(
                 self.dev.index, st, ctypes.c_void_p(self.pos.data_ptr()), self.n, g.Lx, g.Ly,
                 0.0, 0.0, g.H, s.a, s.U0, s.r_m, s.p, ctypes.c_void_p(self.fst.data_ptr())))

@@ -128,6 +128,7 @@ void phase_spread(Plan* p, const double* d_pos, int64_t n_all, int64_t first, in
     SE_CUDA(cudaMemsetAsync(p->d_flags, 0, sizeof(int), s));
     SE_CUDA(cudaMemsetAsync(p->d_scal, 0, 8 * sizeof(double), s));
     SE_CUDA(cudaMemsetAsync(p->d_count, 0, sizeof(int64_t), s));
+    SE_CUDA(cudaMemsetAsync(p->d_ovf_acc, 0, sizeof(int), s));
     S.timed = flags & SE_TIMINGS;
     S.ne = 0;
     if (S.timed) for (auto& e : S.ev) SE_CUDA(cudaEventCreate(&e));
@@ -257,7 +258,13 @@ void phase_results(Plan* p, double* U, se_diag* diag) {
     SE_CUDA(cudaMemcpyAsync(k0, p->d_k0, sizeof(k0), cudaMemcpyDeviceToHost, s));
     SE_CUDA(cudaMemcpyAsync(&hflags, p->d_flags, sizeof(int), cudaMemcpyDeviceToHost, s));
     SE_CUDA(cudaMemcpyAsync(&npairs, p->d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    int ovf = 0;
+    SE_CUDA(cudaMemcpyAsync(&ovf, p->d_ovf_acc, sizeof(int), cudaMemcpyDeviceToHost, s));
     SE_CUDA(cudaStreamSynchronize(s));
+    if (ovf > 0) {                  // lists overflowed: larger capacities next solve
+        p->nl.grow *= 2;
+        if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; p->gkey = {}; }
+    }
     p->timing = false;
     if (hflags & FLAG_Z_OUTSIDE) throw Error(SE_ERR_VALUE, "point outside the extended z domain");
     if (hflags & FLAG_NONFINITE) throw Error(SE_ERR_FLOAT, "non-finite mismatch field");
@@ -486,10 +493,60 @@ void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
     // fp32 mode of a whole (single-GPU) solve: the grid path in fp32 too
     p->g32 = (flags & SE_FP32) != 0;
     if (p->g32) ensure_grid32(p);
+    const bool graph = (flags & SE_GRAPH) && !(flags & (SE_TIMINGS | SE_PAIR_HASH));
+    const Plan::GraphKey key{d_pos, d_phi_out, d_E_out, n, flags};
+    if (graph && p->gexec && p->gkey == key) {
+        // the host-side solve state is as the capture left it
+        SE_CUDA(cudaGraphLaunch(p->gexec, p->stream));
+        phase_results(p, U, diag);
+        return;
+    }
+    if (graph && p->gwarm == key) {
+        // capture (the warm solve sized every buffer and table) on a private
+        // stream -- the caller's may be the legacy stream, which cannot be
+        // captured -- then launch on the caller's
+        if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+        if (!p->cap_stream) SE_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+        const cudaStream_t run = p->stream;
+        auto bind = [&](cudaStream_t st) {
+            p->stream = st;
+            cufftHandle hs[] = {p->fft_fwd2, p->fft_inv4, p->fft_inv1, p->fft_sig, p->fft_fwd2_f,
+                                p->fft_inv4_f, p->fft_inv1_f};
+            for (auto h : hs) if (h) cufftSetStream(h, st);
+        };
+        SE_CUDA(cudaStreamSynchronize(run));
+        bind(p->cap_stream);
+        cudaGraph_t g = nullptr;
+        cudaError_t ce = cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal);
+        if (ce != cudaSuccess) { bind(run); SE_CUDA(ce); }
+        try {
+            phase_spread(p, d_pos, n, 0, n, flags);
+            phase_fields(p);
+            phase_charges(p, d_pos, d_phi_out, d_E_out);
+        } catch (...) {
+            cudaStreamEndCapture(p->cap_stream, &g);
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            bind(run);
+            p->gwarm = {};
+            throw;
+        }
+        ce = cudaStreamEndCapture(p->cap_stream, &g);
+        bind(run);
+        SE_CUDA(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&p->gexec, g, 0);
+        cudaGraphDestroy(g);
+        SE_CUDA(ie);
+        p->gkey = key;
+        SE_CUDA(cudaGraphLaunch(p->gexec, p->stream));
+        phase_results(p, U, diag);
+        return;
+    }
     phase_spread(p, d_pos, n, 0, n, flags);
     phase_fields(p);
     phase_charges(p, d_pos, d_phi_out, d_E_out);
     phase_results(p, U, diag);
+    if (graph) p->gwarm = key;
 }
 
 void ensure_charges(Plan* p, int64_t n) {
@@ -647,6 +704,7 @@ int se_plan_create(const se_params* params, const double* z_nodes, const double*
         p->d_scal = dalloc<double>(p, 8);
         p->d_flags = dalloc<int>(p, 1);
         p->d_count = dalloc<int64_t>(p, 1);
+        p->d_ovf_acc = dalloc<int>(p, 1);
         p->d_partial = dalloc<double>(p, 1024);
         p->d_mm = dalloc<double>(p, 256);
         p->d_origin = dalloc<double>(p, 3);
@@ -706,7 +764,8 @@ void se_plan_destroy(se_plan* plan) {
                         p->fft_inv4_f, p->fft_inv1_f};
     for (auto h : hs) if (h) cufftDestroy(h);
     for (auto& b : p->owned) if (b.p) cudaFree(b.p);
-    if (p->nl.h_ovf) cudaFreeHost(p->nl.h_ovf);
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     for (auto& pr : p->kev) { if (pr[0]) cudaEventDestroy(pr[0]); if (pr[1]) cudaEventDestroy(pr[1]); }
     if (p->stream && p->own_stream) cudaStreamDestroy(p->stream);
     delete p;
@@ -739,6 +798,8 @@ int se_set_charges(se_plan* plan, const double* q, int64_t n) {
         ensure_charges(p, n);
         if (n > 0)
             SE_CUDA(cudaMemcpy(p->d_q, q, n * sizeof(double), cudaMemcpyHostToDevice));
+        if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+        p->gkey = {}; p->gwarm = {};
         p->N = n;
         double aq = 0;
         for (int64_t i = 0; i < n; ++i) aq += std::fabs(q[i]);

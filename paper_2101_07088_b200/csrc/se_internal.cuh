@@ -126,7 +126,6 @@ struct NearLists {
     int64_t cap_far_total = 0, cap_close_total = 0, ncap = 0;
     int *far = nullptr, *close = nullptr, *cfar = nullptr, *cclose = nullptr, *ovf = nullptr;
     int* ovl = nullptr;        // slots whose lists overflowed (fallback list)
-    int* h_ovf = nullptr;      // pinned: overflow count of the previous solve
     int64_t grow = 1;          // capacity multiplier learned from overflows
 };
 
@@ -292,6 +291,18 @@ struct Plan {
     int64_t cell_cap = 0;
     double* d_mm = nullptr;               // z-range partials
     int64_t* d_count = nullptr;
+    int* d_ovf_acc = nullptr;             // near-list overflows of the charges this solve
+    // CUDA graph of a whole solve (SE_GRAPH): replayed while the device
+    // buffers, size and flags repeat; invalidated when list capacities grow
+    cudaGraphExec_t gexec = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    struct GraphKey {
+        const void *pos = nullptr, *phi = nullptr, *E = nullptr;
+        int64_t n = -1; uint32_t flags = 0;
+        bool operator==(const GraphKey& o) const {
+            return pos == o.pos && phi == o.phi && E == o.E && n == o.n && flags == o.flags;
+        }
+    } gkey, gwarm;
     bool pair_hash = false;               // SE_PAIR_HASH on the solve in flight
     unsigned long long* d_phash = nullptr;   // [2][N] pair-set hash, count
     int64_t phash_cap = 0, phash_n = 0;

@@ -1130,6 +1130,8 @@ __global__ void near_boundary_kernel(NearArgs a) {
     }
 }
 
+__global__ void add_count_kernel(const int* src, int* acc) { *acc += *src; }
+
 // point tasks: per xy column, ceil(count/32) warps (points sorted by z
 // within the column, so a warp's z windows overlap)
 __global__ void task_count_kernel(const int* pt_start, int ncol, int nzb, int* ntask) {
@@ -1661,9 +1663,9 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     want_far = (want_far + 15) & ~15LL;
     want_close = (want_close + 15) & ~15LL;
     // no host sync: points whose lists overflow are evaluated by the fused
-    // kernel from a device list; the overflow count of the previous solve
-    // (read back asynchronously into pinned memory) grows the capacities
-    if (L.h_ovf && *L.h_ovf > 0) { L.grow *= 2; *L.h_ovf = 0; }
+    // kernel from a device list; the charges' overflow count accumulates in
+    // a per-plan device counter that phase_results reads after its stream
+    // sync and turns into a larger L.grow for the next solve
     want_far *= L.grow;
     want_close *= L.grow;
     if (ne * want_far > L.cap_far_total || ne * want_close > L.cap_close_total || ne > L.ncap) {
@@ -1678,10 +1680,6 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         L.cclose = dalloc<int>(p, L.ncap);
         L.ovf = dalloc<int>(p, 1);
         L.ovl = dalloc<int>(p, L.ncap);
-    }
-    if (!L.h_ovf) {
-        SE_CUDA(cudaMallocHost(&L.h_ovf, sizeof(int)));
-        *L.h_ovf = 0;
     }
     a.list_far = L.far; a.list_close = L.close;
     a.cap_far = want_far; a.cap_close = want_close;
@@ -1716,7 +1714,10 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         else near_fused_kernel<false, 6, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
     }
     SE_LAUNCHED(p);
-    SE_CUDA(cudaMemcpyAsync(L.h_ovf, L.ovf, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    if (d_npairs) {                                  // the charges' evaluation
+        add_count_kernel<<<1, 1, 0, p->stream>>>(L.ovf, p->d_ovf_acc);
+        SE_LAUNCHED(p);
+    }
     near_boundary_kernel<<<4, 256, 0, p->stream>>>(a);
     if (d_npairs) { p->ktoc(5); p->ktoc(3); }
     SE_LAUNCHED(p);

@@ -69,8 +69,10 @@ class SolveResult:
 
 def _flags(need_energy, need_forces, need_potential, subtract_self,
            include_correction, force_general, timings=False, fp32=False,
-           record_pairs=False):
+           record_pairs=False, graph=False):
     f = 0
+    if graph:
+        f |= _lib.GRAPH
     if record_pairs:
         f |= _lib.PAIR_HASH
     if fp32:
@@ -229,12 +231,14 @@ class SlabSolver:
     def solve_device(self, d_pos, d_phi, d_E, n, need_energy=True,
                      need_forces=True, need_potential=True,
                      subtract_self=False, include_correction=True,
-                     force_general=False, timings=False):
+                     force_general=False, timings=False, graph=False):
         """Device-resident variant: ``d_pos``, ``d_phi``, ``d_E`` are raw
-        device pointers (ints) on the plan's device.  Returns (U, diag)."""
+        device pointers (ints) on the plan's device.  Returns (U, diag).
+        ``graph``: capture the solve as a CUDA graph on the second call with
+        the same buffers and flags and replay it from then on."""
         flags = _flags(need_energy, need_forces, need_potential,
                        subtract_self, include_correction, force_general,
-                       timings, self.precision == "fp32")
+                       timings, self.precision == "fp32", graph=graph)
         U = ctypes.c_double(0.0)
         diag = _lib.SeDiag()
         _lib.check(self._lib.se_solve_device(

@@ -568,3 +568,31 @@ def test_both_near_field_paths_against_goldens(fused):
                         "or variants_against_golden"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_graph_replay_matches_direct_solve():
+    """SE_GRAPH: the warm solve, the capture and the replays give the same
+    results as direct solves, also after the positions change in place."""
+    import torch
+    system, params = W.build("c3", N=4096)
+    n = system.n
+    s = _solver(system, params)
+    s.set_stream(torch.cuda.current_stream().cuda_stream)
+    pos = torch.as_tensor(system.positions, device="cuda").contiguous()
+    phi = torch.empty(n, dtype=torch.float64, device="cuda")
+    E = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    direct = s.solve()
+    for _ in range(4):                       # warm, capture, replay, replay
+        U, diag = s.solve_device(pos.data_ptr(), phi.data_ptr(), E.data_ptr(), n, graph=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(phi.cpu().numpy(), direct.phi_bar)
+        assert np.array_equal(E.cpu().numpy(), direct.E_bar)
+        assert U == direct.U
+    moved = system.positions.copy()
+    moved[:, :2] = (moved[:, :2] + 0.013) % 2.0
+    pos.copy_(torch.as_tensor(moved))
+    U, diag = s.solve_device(pos.data_ptr(), phi.data_ptr(), E.data_ptr(), n, graph=True)
+    torch.cuda.synchronize()
+    ref = s.solve(positions=moved)
+    assert np.array_equal(phi.cpu().numpy(), ref.phi_bar)
+    assert U == ref.U

@@ -69,6 +69,11 @@ def measure(steps=20, warmup=5, sweep=True):
         out["dp_ms_" + prec] = _median_ms(
             lambda: s.solve_device(pos.data_ptr(), phi.data_ptr(), E.data_ptr(), n),
             steps, warmup, stream)
+        # the same solve replayed as a captured CUDA graph (SE_GRAPH)
+        out["dp_ms_%s_graph" % prec] = _median_ms(
+            lambda: s.solve_device(pos.data_ptr(), phi.data_ptr(), E.data_ptr(), n,
+                                   graph=True),
+            steps, warmup, stream)
         s.close()
     out["dp_ms_published"] = 4.3
     if sweep:
