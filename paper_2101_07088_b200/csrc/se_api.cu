@@ -102,6 +102,7 @@ static Solve& current(Plan* p) { return p->solve; }
 
 void phase_spread(Plan* p, const double* d_pos, int64_t n_all, int64_t first, int64_t count,
                   uint32_t flags) {
+    NvtxRange nv("se.spread_phase");
     p->launches = 0;
     if (n_all != p->N)
         throw Error(SE_ERR_VALUE, "positions and charges disagree on N");
@@ -145,6 +146,7 @@ void phase_spread(Plan* p, const double* d_pos, int64_t n_all, int64_t first, in
 }
 
 void phase_fields(Plan* p) {
+    NvtxRange nv("se.field_phase");
     Solve& S = current(p);
     if (S.phase != 1) throw Error(SE_ERR_CUDA, "se_shard_fields before se_shard_spread");
     forward_transforms(p, S.two);
@@ -179,6 +181,7 @@ static NearKernel kernel_of(const se_params& P, int kind, bool field, bool sub_u
 }
 
 void phase_charges(Plan* p, const double* d_pos, double* d_phi_out, double* d_E_out) {
+    NvtxRange nv("se.charge_phase");
     Solve& S = current(p);
     if (S.phase != 2) throw Error(SE_ERR_CUDA, "se_shard_charges before se_shard_fields");
     if (d_pos != p->d_pos_cur) throw Error(SE_ERR_VALUE, "positions changed between phases");
@@ -249,6 +252,7 @@ void phase_charges(Plan* p, const double* d_pos, double* d_phi_out, double* d_E_
 }
 
 void phase_results(Plan* p, double* U, se_diag* diag) {
+    NvtxRange nv("se.results");
     Solve& S = current(p);
     cudaStream_t s = p->stream;
     double scal[8], k0[16];

@@ -755,6 +755,7 @@ void partition_sources(Plan* p, const double* d_pos, int64_t n) {
 }
 
 void build_sources(Plan* p, const double* d_pos, int64_t first, int64_t n, bool two_grids) {
+    NvtxRange nv("se.sources");
     ensure_sources(p, n);
     const int64_t total = 3 * n;
     const int TB = 256;
@@ -898,6 +899,7 @@ static void launch_spread_mma(Plan* p, const SpreadArgs& a) {
 
 
 void spread(Plan* p, bool two_grids) {
+    NvtxRange nv("se.spread");
     SpreadArgs a{tile_args(p), p->d_rho, two_grids ? 1 : 0, p->g32 ? p->d_rho32 : nullptr};
     // 8x8-column x 16-node tiles, 2 warps (one per 8-node z group), DMMA
     // accumulation, 64 staged sources per round, 10 CTAs per SM: measured
@@ -911,6 +913,7 @@ void spread(Plan* p, bool two_grids) {
 
 void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool forces) {
     if (count == 0) return;
+    NvtxRange nv("se.interpolate");
     const int TB = 256;
     const int nbx = (p->Nx + IBIN - 1) / IBIN, nby = (p->Ny + IBIN - 1) / IBIN;
     const int nbins = nbx * nby;

@@ -1235,6 +1235,7 @@ static CellGeo cell_geo(const Plan* p) {
 
 void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, bool in_domain,
                  const double* d_zsrc_min) {
+    NvtxRange nv("se.cell_list");
     const double eps = p->P.eps;
     const double fb = -(p->P.eps_b - eps) / (p->P.eps_b + eps);
     const double ft = -(p->P.eps_t - eps) / (p->P.eps_t + eps);
@@ -1460,6 +1461,7 @@ static double r2_threshold(double radius) {
 void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
                const NearKernel& k, double* d_out4, int64_t* d_npairs) {
     if (ne == 0) return;
+    NvtxRange nv("se.near_field");
     bool close_ok = false;
     NearArgs a{};
     a.eval = d_eval; a.order = d_order; a.ne = ne;

@@ -884,6 +884,7 @@ void z_forward(Plan* p, const ModeView& v) {
 }
 
 void forward_transforms(Plan* p, bool two_grids) {
+    NvtxRange nv("se.forward_transforms");
     (void)two_grids;
     if (p->g32) SE_CUFFT(cufftExecR2C(p->fft_fwd2_f, p->d_rho32, p->d_hat32));
     else SE_CUFFT(cufftExecD2Z(p->fft_fwd2, p->d_rho, p->d_hat));
@@ -895,6 +896,7 @@ void bvp_solve(Plan* p, bool two_grids, int mode, bool correction) {
 }
 
 void bvp_solve_view(Plan* p, bool two_grids, int mode, bool correction, const ModeView& v) {
+    NvtxRange nv("se.mode_bvp");
     BvpArgs a{};
     const bool whole = v.m0 == 0 && v.M == p->M;
     a.mp = maps_of(p, p->d_maps);
@@ -959,6 +961,7 @@ void z_inverse_assemble(Plan* p, bool forces, bool correction, const ModeView& v
 }
 
 void inverse_transforms(Plan* p, bool forces, bool correction) {
+    NvtxRange nv("se.inverse_transforms");
     z_inverse_assemble(p, forces, correction, ModeView{p->M, p->M, 0});
     if (p->g32) {
         if (forces) SE_CUFFT(cufftExecC2R(p->fft_inv4_f, p->d_spec32, p->d_fields32));
