@@ -851,155 +851,6 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_fused_kernel(NearArgs a
     }
 }
 
-// Fused scan + evaluation for many points (no pair lists in HBM).
-// One warp per task (<= 32 evaluation points of one xy column, sorted by z;
-// lane = point), as in the two-phase scan: the 25 neighbour columns are
-// pruned by xy distance, each lane's z window is the chord of its query
-// sphere, the warp's union window is staged through shared memory in
-// coalesced chunks and every lane tests its own part with the fp32
-// pre-test.  Survivors go to per-lane ring queues in shared memory (far /
-// close, lane-major so a lane's slots sit in its own bank); when a queue
-// nears full the warp drains it: every lane evaluates the entries of its own
-// queue (the exact fp64 test, then the erf kernels), as many as the
-// shortest live queue holds so all lanes stay busy (at least half a queue),
-// accumulating in registers.  Each point's sum is a fixed sequence of its
-// own pairs: deterministic, one store per point and component.
-constexpr int FQF = 32, FQC = 16;              // far / close ring depth per lane
-
-template <bool F32, bool HASH, int SU, int MINB>
-__global__ void __launch_bounds__(NB_THREADS, MINB) near_fq_kernel(NearArgs a) {
-    constexpr int W = NB_THREADS / 32;
-    constexpr unsigned F = 0xffffffffu;
-    __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + CL_TAB];
-    __shared__ int qf[W][FQF][32];
-    __shared__ int qc[W][FQC][32];
-    __shared__ float4 stage[W][SCAN_STAGE];
-    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
-    if (!a.use_ctab || !a.use_poly)
-        for (int e = tid; e < SE_ERFCX_NP * (SE_ERFCX_DEG + 1); e += blockDim.x)
-            tab[e] = (&se_erfcx_tab[0][0])[e];
-    if (a.use_ctab)
-        for (int e = tid; e < CL_TAB; e += blockDim.x)
-            tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + e] = a.ctab[e];
-    __syncthreads();
-    const int64_t task = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
-    if (task >= a.ntask || task >= *a.ntask_dev) return;
-    const int2 tk = a.tasks[task];
-    const int col = tk.x;
-    const int64_t slot = (int64_t)tk.y + lane;
-    const bool live = slot < a.pt_end[col];
-    const int64_t i = live ? a.order[slot] : 0;
-    double px = 0, py = 0, pz = 0;
-    float pxf = 0.f, pyf = 0.f, pzf = 0.f;
-    if (live) {
-        px = a.eval[3 * i]; py = a.eval[3 * i + 1]; pz = a.eval[3 * i + 2];
-        pxf = (float)wrap(px, a.g.Lx);
-        pyf = (float)wrap(py, a.g.Ly);
-        pzf = (float)(pz - a.g.zlo);
-    }
-    const int cx = col % a.g.ncx, cy = col / a.g.ncx;
-    const ColumnWalk cw = column_walk(a.g);
-    const float r2f = a.r2f, r2c = a.r2close;
-    const float csxf = (float)a.g.csx, csyf = (float)a.g.csy, icsz = (float)(1.0 / a.g.csz);
-    const int nzb = a.g.ncz;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    int count = 0;
-    unsigned long long hs = 0;
-    int nf = 0, hf = 0, nc = 0, hc = 0;           // queue fill and head per lane
-    // evaluate k entries of each lane's far (close) queue; lanes holding
-    // fewer evaluate all of theirs
-    auto drain_far = [&](int k) {
-        for (int t = 0; t < k; ++t) {
-            if (t < nf)
-                eval_pair<true, F32, HASH>(a, tab, qf[wib][(hf + t) & (FQF - 1)][lane], px, py,
-                                           pz, i, acc[0], acc[1], acc[2], acc[3], count, &hs);
-        }
-        const int d = min(k, nf);
-        hf = (hf + d) & (FQF - 1);
-        nf -= d;
-    };
-    auto drain_close = [&](int k) {
-        for (int t = 0; t < k; ++t) {
-            if (t < nc)
-                eval_pair<false, false, HASH>(a, tab, qc[wib][(hc + t) & (FQC - 1)][lane], px,
-                                              py, pz, i, acc[0], acc[1], acc[2], acc[3], count,
-                                              &hs);
-        }
-        const int d = min(k, nc);
-        hc = (hc + d) & (FQC - 1);
-        nc -= d;
-    };
-    for (int iy = 0; iy < cw.nyr; ++iy) {
-        int yc; float sy, dyd;
-        column_axis(cy, iy, cw.ally, a.g.ncy, csyf, a.Lyf, pyf, &yc, &sy, &dyd);
-        for (int ix = 0; ix < cw.nxr; ++ix) {
-            int xc; float sx, dxd;
-            column_axis(cx, ix, cw.allx, a.g.ncx, csxf, a.Lxf, pxf, &xc, &sx, &dxd);
-            const float d2 = fmaf(dxd, dxd, dyd * dyd);
-            int j = 0, e = 0;
-            if (live && d2 <= r2f) {
-                const float hz = sqrtf(r2f - d2) * 1.0001f + a.zmarg;
-                const int z0 = max(0, min(nzb - 1, (int)floorf((pzf - hz) * icsz)));
-                const int z1 = max(0, min(nzb - 1, (int)floorf((pzf + hz) * icsz)));
-                const int base = (yc * a.g.ncx + xc) * nzb;
-                j = a.start[base + z0];
-                e = a.start[base + z1 + 1];
-            }
-            if (!__any_sync(F, j < e)) continue;
-            const float qx = pxf - sx, qy = pyf - sy;
-            int umin = (j < e) ? j : 0x7fffffff, umax = (j < e) ? e : 0;
-            umin = __reduce_min_sync(F, umin);
-            umax = __reduce_max_sync(F, umax);
-            for (int c0 = umin; c0 < umax; c0 += SCAN_STAGE) {
-                const int c1 = min(umax, c0 + SCAN_STAGE);
-                __syncwarp();
-                for (int q = c0 + lane; q < c1; q += 32) stage[wib][q - c0] = a.srcf[q];
-                __syncwarp();
-                int jj = max(j, c0);
-                const int ee = min(e, c1);
-                while (__any_sync(F, jj < ee)) {
-#pragma unroll
-                    for (int u = 0; u < SU; ++u) {
-                        if (jj + u < ee) {
-                            const float4 f = stage[wib][jj + u - c0];
-                            float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
-                            if (cw.allx) dx -= a.Lxf * rintf(dx * a.iLxf);
-                            if (cw.ally) dy -= a.Lyf * rintf(dy * a.iLyf);
-                            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                            if (r2 <= r2f) {
-                                if (r2 > r2c) qf[wib][(hf + nf++) & (FQF - 1)][lane] = jj + u;
-                                else qc[wib][(hc + nc++) & (FQC - 1)][lane] = jj + u;
-                            }
-                        }
-                    }
-                    jj += SU;
-                    if (__any_sync(F, nf > FQF - SU)) {
-                        const int m = __reduce_min_sync(F, (unsigned)(live ? nf : FQF));
-                        drain_far(max(m, FQF / 2));
-                    }
-                    if (__any_sync(F, nc > FQC - SU)) {
-                        const int m = __reduce_min_sync(F, (unsigned)(live ? nc : FQC));
-                        drain_close(max(m, FQC / 2));
-                    }
-                }
-            }
-        }
-    }
-    drain_far(__reduce_max_sync(F, (unsigned)nf));
-    drain_close(__reduce_max_sync(F, (unsigned)nc));
-    if (live) {
-        a.out[i] = acc[0];
-        if (a.need_field) {
-            a.out[a.out_stride + i] = acc[1];
-            a.out[2 * a.out_stride + i] = acc[2];
-            a.out[3 * a.out_stride + i] = acc[3];
-        }
-        if (HASH) { a.phash[i] = hs; a.phash[a.ne + i] = (unsigned long long)count; }
-    }
-    const unsigned cnt = __reduce_add_sync(F, (unsigned)count);
-    if (lane == 0 && a.npairs && cnt) atomicAdd((unsigned long long*)a.npairs, (unsigned long long)cnt);
-}
-
 // A few evaluation points (the gauge origin): one CTA per point, the threads
 // stride over the 27 neighbour cells' sources with the exact test and the
 // general kernel, then a block reduction.  Avoids the sort / task / list
@@ -1629,24 +1480,6 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     a.ntask_dev = ns.toff + ncol;
     a.ntask = tcap;
     const unsigned nblk = (unsigned)((tcap * 32 + NB_THREADS - 1) / NB_THREADS);
-    static const char* fqenv = getenv("SE_NEAR_FQ");         // A/B: fused queue kernel
-    if (fqenv && atoi(fqenv)) {
-        a.use_ctab = close_ok ? 1 : 0;
-        if (d_npairs) { p->ktic(3); p->ktic(4); p->ktoc(4); p->ktic(5); }
-        if (hash) {
-            if (k.fp32) near_fq_kernel<true, true, 4, 4><<<nblk, NB_THREADS, 0, p->stream>>>(a);
-            else near_fq_kernel<false, true, 4, 4><<<nblk, NB_THREADS, 0, p->stream>>>(a);
-        } else if (k.fp32) {
-            near_fq_kernel<true, false, 4, 4><<<nblk, NB_THREADS, 0, p->stream>>>(a);
-        } else {
-            near_fq_kernel<false, false, 4, 4><<<nblk, NB_THREADS, 0, p->stream>>>(a);
-        }
-        SE_LAUNCHED(p);
-        near_boundary_kernel<<<4, 256, 0, p->stream>>>(a);
-        if (d_npairs) { p->ktoc(5); p->ktoc(3); }
-        SE_LAUNCHED(p);
-        return;
-    }
     // pair-list capacities from the expected neighbour count (+ margin);
     // an overflow doubles them and reruns the scan
     const double vol_cell = p->cl.csx * p->cl.csy * p->cl.csz;

@@ -74,12 +74,11 @@ def test_pair_set_small_case_exact():
 
 
 @pytest.mark.parametrize("env", [{"SE_NEAR_FUSED": "0"}, {"SE_NEAR_FUSED": "1"},
-                                 {"SE_NEAR_FUSED": "0", "SE_NEAR_FQ": "1"},
                                  {"SE_NEAR_FUSED": "0", "SE_NEAR_LIST_SCALE": "0.3"}])
 def test_pair_set_all_paths_c4d(env):
     """Every near-field path gives the reference's pair set: scan -> lists
     -> eval (default at this size), one warp per point (SE_NEAR_FUSED=1),
-    the fused queue kernel (SE_NEAR_FQ=1), and the list path with capacities
+    and the list path with capacities
     cut so that points overflow into the fallback kernel."""
     import subprocess
     import sys
