@@ -25,6 +25,7 @@
 // the four spectral fields, so no (mode x node) correction table is stored.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "se_internal.cuh"
 
@@ -391,31 +392,13 @@ __device__ __forceinline__ void solve_mode(const BvpArgs& a, int64_t m, int g, d
 
 __device__ __forceinline__ bool finite2(double2 v) { return isfinite(v.x) && isfinite(v.y); }
 
-__global__ void __launch_bounds__(64) bvp_kernel(BvpArgs a) {
-    // lane pair (2m, 2m+1) = (over grid, in-slab grid) of mode m
-    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int g = (int)(tid & 1);
-    const int64_t mm = tid >> 1;
-    const bool valid = mm < a.Mv;
-    const int64_t m = valid ? mm : (a.Mv > 0 ? a.Mv - 1 : 0);
-    double2 w[4], e[2];
-    for (int q = 0; q < 4; ++q) w[q] = make_double2(0, 0);
-    e[0] = e[1] = make_double2(0, 0);
-    if (valid && (a.two || g == 1)) solve_mode(a, m, g, w, e, g == 1);
-    double2 wo[4], eo[2], wi[4], ei[2];
-    for (int q = 0; q < 4; ++q) {
-        double2 o;
-        o.x = __shfl_xor_sync(0xffffffffu, w[q].x, 1);
-        o.y = __shfl_xor_sync(0xffffffffu, w[q].y, 1);
-        wo[q] = o; wi[q] = w[q];
-    }
-    for (int q = 0; q < 2; ++q) {
-        double2 o;
-        o.x = __shfl_xor_sync(0xffffffffu, e[q].x, 1);
-        o.y = __shfl_xor_sync(0xffffffffu, e[q].y, 1);
-        eo[q] = o; ei[q] = e[q];
-    }
-    if (!valid || g == 0) return;
+// The mode's wall data -> mismatch, correction moments and (mode k = 0) the
+// linear k = 0 coefficients (slab.py:302-318,397-445; dpsolver.py:131-138,
+// 189-218).  wi / ei: in-slab grid's wall values / ends, wo / eo: the
+// over grid's (zero when only the in-slab grid is solved).
+__device__ __forceinline__ void finish_mode(const BvpArgs& a, int64_t m, const double2 (&wi)[4],
+                                            const double2 (&ei)[2], const double2 (&wo)[4],
+                                            const double2 (&eo)[2]) {
     double2 sb = a.sbh[m], st = a.sth[m];
     double2 phib, eb, phit, et;
     if (a.mode == 0) {                                   // slab.py:306-316
@@ -475,6 +458,34 @@ __global__ void __launch_bounds__(64) bvp_kernel(BvpArgs a) {
     o[0] = ai1; o[1] = ai2; o[2] = disc; o[3] = A_i; o[4] = A_b; o[5] = A_t;
     o[6] = pib; o[7] = pit; o[8] = pbb; o[9] = ptt;
     a.scal[0] = A_i;
+}
+
+__global__ void __launch_bounds__(64) bvp_kernel(BvpArgs a) {
+    // lane pair (2m, 2m+1) = (over grid, in-slab grid) of mode m
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int g = (int)(tid & 1);
+    const int64_t mm = tid >> 1;
+    const bool valid = mm < a.Mv;
+    const int64_t m = valid ? mm : (a.Mv > 0 ? a.Mv - 1 : 0);
+    double2 w[4], e[2];
+    for (int q = 0; q < 4; ++q) w[q] = make_double2(0, 0);
+    e[0] = e[1] = make_double2(0, 0);
+    if (valid && (a.two || g == 1)) solve_mode(a, m, g, w, e, g == 1);
+    double2 wo[4], eo[2], wi[4], ei[2];
+    for (int q = 0; q < 4; ++q) {
+        double2 o;
+        o.x = __shfl_xor_sync(0xffffffffu, w[q].x, 1);
+        o.y = __shfl_xor_sync(0xffffffffu, w[q].y, 1);
+        wo[q] = o; wi[q] = w[q];
+    }
+    for (int q = 0; q < 2; ++q) {
+        double2 o;
+        o.x = __shfl_xor_sync(0xffffffffu, e[q].x, 1);
+        o.y = __shfl_xor_sync(0xffffffffu, e[q].y, 1);
+        eo[q] = o; ei[q] = e[q];
+    }
+    if (!valid || g == 0) return;
+    finish_mode(a, m, wi, ei, wo, eo);
 }
 
 // ---------------------------------------------------------------------------
