@@ -493,8 +493,11 @@ def run_ours(args):
         ms32 = float(np.mean(t32))
         line["fp32_mode"] = {"ms_per_step": ms32, "value": n / (ms32 * 1e-3),
                              "unit": "charges/s",
-                             "scope": "near-field pair kernels in fp32; grids, FFTs, "
-                                      "BVPs, spread and interpolation in fp64"}
+                             "scope": "near-field pairs (fp32 membership outside a "
+                                      "bounded band, exact fp64 test inside it), spread "
+                                      "grids, xy FFTs, spectral and field grids and the "
+                                      "interpolation in fp32; z DCT-I, mode BVPs and "
+                                      "harmonic correction in fp64"}
     if world == 1 and not args.no_paper_config:
         # the paper's published timings (DP 4.3 ms, TP 0.84 ms,
         # BD step ~5 ms, RTX 2080Ti fp32) on their configuration, N = 2e4
