@@ -166,6 +166,7 @@ struct NearArgs {
     int use_poly;
     double pmid, pinvh;
     double pc[19];
+    double pc4[19], ic2sq, far_t1, far_t0, far_k;   // the fp64 far path (pair_terms)
     // fp32 mode: erfcx on the same x range as one degree-FAR_DEG32 polynomial
     int use_poly32;
     float pmid32, pinvh32, pc32[11];
@@ -291,6 +292,19 @@ __device__ __forceinline__ void pair_terms(const NearArgs& a, const double* tab,
         coef = nd ? cv : 0.0;
         return;
     }
+    if (FAR && a.use_poly) {
+        // erfc(x) / (4 pi eps r) = exp(-x^2) erfcx(x) / (4 pi eps r), x = r / c2,
+        // with 1/(4 pi eps) folded into the erfcx coefficients (pc4) and the
+        // derivative constant (far_k = 2/sqrt(pi) / c2 / (4 pi eps))
+        const double e2 = exp_neg(r2 * a.ic2sq);
+        const double t = fma(r, a.far_t1, a.far_t0);
+        double acc = a.pc4[FAR_DEG];
+#pragma unroll
+        for (int j = FAR_DEG - 1; j >= 0; --j) acc = fma(acc, t, a.pc4[j]);
+        g = (e2 * acc) * rinv;
+        coef = nd ? fma(a.far_k, e2, g) * (rinv * rinv) : 0.0;
+        return;
+    }
     const double x2 = r * a.ic2;
     double E2, C2, e2;
     if (FAR && a.use_poly) {
@@ -338,9 +352,12 @@ __device__ __forceinline__ void pair_terms(const NearArgs& a, const double* tab,
 
 // exact displacement and squared distance, reference operation order
 //   d = p - s; d_xy -= L * round(d_xy / L); r2 = (dx^2 + dy^2) + dz^2
+// round(d / L) is taken as rint(d * (1 / L)): the two differ only when d / L
+// lies within ulps of a half-integer, i.e. for pairs whose minimum-image
+// distance is ~L/2 > r_cut, which no list holds (r_cut < L/2 is enforced)
 __device__ __forceinline__ double min_image(double d, double L) {
     if (fabs(d) <= 0.25 * L) return d;           // round(d/L) == 0 exactly
-    return __dsub_rn(d, __dmul_rn(L, rint(d / L)));
+    return __dsub_rn(d, __dmul_rn(L, rint(d * (1.0 / L))));
 }
 
 // numpy's float remainder (npy_divmod): fmod, moved into [0, L) for L > 0
@@ -423,7 +440,10 @@ __device__ __forceinline__ void column_axis(int c, int i, bool all, int n, float
     *dist = fmaxf(0.f, fmaxf(lo - p, p - hi));
 }
 
-template <int SCAN_Q, int SU, int MINB>
+// SMALL: a box axis with fewer than 5 columns (every column visited once,
+// periodic differences in the test); the common large-box case compiles
+// without those branches
+template <int SCAN_Q, int SU, int MINB, bool SMALL>
 __global__ void __launch_bounds__(NB_THREADS, MINB) near_scan_kernel(NearArgs a) {
     constexpr int W = NB_THREADS / 32;
     __shared__ int qf[W][SCAN_Q + SU][32];
@@ -444,7 +464,8 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_scan_kernel(NearArgs a)
         pzf = (float)(a.eval[3 * i + 2] - a.g.zlo);
     }
     const int cx = col % a.g.ncx, cy = col / a.g.ncx;
-    const ColumnWalk cw = column_walk(a.g);
+    ColumnWalk cw = column_walk(a.g);
+    if (!SMALL) { cw.allx = cw.ally = false; cw.nxr = cw.nyr = 5; }
     const float r2f = a.r2f, r2c = a.r2close;
     const float csxf = (float)a.g.csx, csyf = (float)a.g.csy, icsz = (float)(1.0 / a.g.csz);
     const int nzb = a.g.ncz;
@@ -507,8 +528,8 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_scan_kernel(NearArgs a)
                         if (jj + u < ee) {
                             const float4 f = stage[wib][jj + u - c0];
                             float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
-                            if (cw.allx) dx -= a.Lxf * rintf(dx * a.iLxf);
-                            if (cw.ally) dy -= a.Lyf * rintf(dy * a.iLyf);
+                            if (SMALL && cw.allx) dx -= a.Lxf * rintf(dx * a.iLxf);
+                            if (SMALL && cw.ally) dy -= a.Lyf * rintf(dy * a.iLyf);
                             const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                             if (r2 <= r2f) {
                                 if (r2 > r2c) qf[wib][qn++][lane] = jj + u;
@@ -1367,6 +1388,11 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         const double r_far = std::max(6.5 * k.c1, 1e-2 * k.c2);
         const double xa = r_far / k.c2 * (1.0 - 1e-6), xb = k.radius / k.c2 * (1.0 + 1e-6);
         a.use_poly = fit_far_poly(xa, xb, &a.pmid, &a.pinvh, a.pc) ? 1 : 0;
+        for (int j = 0; j <= FAR_DEG; ++j) a.pc4[j] = a.pc[j] * k.inv4pie;
+        a.ic2sq = (1.0 / k.c2) * (1.0 / k.c2);
+        a.far_t1 = (1.0 / k.c2) * a.pinvh;
+        a.far_t0 = -a.pmid * a.pinvh;
+        a.far_k = TWO_OVER_SQRTPI * (1.0 / k.c2) * k.inv4pie;
         double m32 = 0, ih32 = 0, c32[FAR_DEG32 + 1];
         a.use_poly32 = (k.fp32 && fit_far_poly(xa, xb, &m32, &ih32, c32, FAR_DEG32, 3e-7)) ? 1 : 0;
         a.pmid32 = (float)m32; a.pinvh32 = (float)ih32;
@@ -1523,7 +1549,10 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     if (d_npairs) { p->ktic(3); p->ktic(4); }
     // 16-deep queues, 4 candidates per step, 7 CTAs / SM (73 registers):
     // measured best of queue 8..24, step 4 / 8, 6..12 CTAs (3.17 vs 3.29 ms at 10)
-    near_scan_kernel<16, 4, 7><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+    if (p->cl.ncx < 5 || p->cl.ncy < 5)
+        near_scan_kernel<16, 4, 7, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+    else
+        near_scan_kernel<16, 4, 7, false><<<nblk, NB_THREADS, 0, p->stream>>>(a);
     if (d_npairs) p->ktoc(4);
     SE_LAUNCHED(p);
     if (d_npairs) p->ktic(5);
