@@ -120,7 +120,11 @@ struct CellList {
     double4* src = nullptr;      // sorted sources (x, y, z, q) original coords
     float4* srcf = nullptr;      // wrapped fp32 copy for the pre-test
     int* orig = nullptr;         // sorted -> original source index
+    int64_t cap = 0, cell_cap = 0;   // allocated sources / cell starts
 };
+
+// which sources a cell list holds: the charges, their mirror layers, or both
+enum : int { CL_CHARGES = 1, CL_IMAGES = 2, CL_ALL = 3 };
 
 // ----------------------------------------------------------------------------
 // the plan
@@ -278,7 +282,8 @@ struct Plan {
     SourceSet ss;
 
     // near field
-    CellList cl;
+    CellList cl;                          // charges + their mirror layers
+
     NearScratch ns;
     NearLists nl;
     CloseFit close_fit[2];
@@ -420,10 +425,12 @@ struct NearKernel {
     int fp32;            // far pairs in single precision (SE_FP32)
 };
 void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, bool in_domain,
-                 const double* d_zsrc_min = nullptr);
+                 const double* d_zsrc_min = nullptr, CellList* cl = nullptr,
+                 int parts = CL_ALL);
 void near_eval(Plan* p, const double* d_eval, const int* d_eval_order,
                int64_t ne, const NearKernel& k, double* d_out4,
-               int64_t* d_npairs);
+               int64_t* d_npairs, const CellList* cl = nullptr);
+
 void finalize(Plan* p, int64_t first, int64_t count, uint32_t flags, double self_inf_value,
               double* d_phi, double* d_E);
 void wall_energy(Plan* p, const NearKernel& kpoint);

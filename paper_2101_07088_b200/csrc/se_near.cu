@@ -120,7 +120,8 @@ __global__ void cell_keys_kernel(const double4* s, int64_t ns, CellGeo g,
 
 __global__ void cell_fill_kernel(const uint32_t* keys, const int* perm, int64_t ns,
                                  int ncell, const double4* src_in, CellGeo g,
-                                 int* start, double4* src, float4* srcf, int* orig) {
+                                 int* start, double4* src, float4* srcf, int* orig,
+                                 int orig_off) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i > ns) return;
     int cur = (i < ns) ? (int)keys[i] : ncell;
@@ -132,7 +133,7 @@ __global__ void cell_fill_kernel(const uint32_t* keys, const int* perm, int64_t 
     src[i] = v;
     srcf[i] = make_float4((float)wrap(v.x, g.Lx), (float)wrap(v.y, g.Ly),
                           (float)(v.z - g.zlo), (float)v.w);
-    orig[i] = s;
+    orig[i] = s + orig_off;
 }
 
 // ---------------------------------------------------------------------------
@@ -1097,32 +1098,41 @@ __global__ void sum_partials_kernel(const double* partial, int nb, double scale,
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-static CellGeo cell_geo(const Plan* p) {
+static CellGeo cell_geo(const Plan* p, const CellList& cl) {
     CellGeo g;
-    g.ncx = p->cl.ncx; g.ncy = p->cl.ncy; g.ncz = p->cl.ncz;
-    g.csx = p->cl.csx; g.csy = p->cl.csy; g.csz = p->cl.csz; g.zlo = p->cl.zlo;
+    g.ncx = cl.ncx; g.ncy = cl.ncy; g.ncz = cl.ncz;
+    g.csx = cl.csx; g.csy = cl.csy; g.csz = cl.csz; g.zlo = cl.zlo;
     g.Lx = p->P.Lx; g.Ly = p->P.Ly;
     return g;
 }
 
 void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, bool in_domain,
-                 const double* d_zsrc_min) {
+                 const double* d_zsrc_min, CellList* clp, int parts) {
     NvtxRange nv("se.cell_list");
     const double eps = p->P.eps;
     const double fb = -(p->P.eps_b - eps) / (p->P.eps_b + eps);
     const double ft = -(p->P.eps_t - eps) / (p->P.eps_t + eps);
     const int nb = fb != 0.0, nt = ft != 0.0;
-    const int64_t ns = n * (1 + nb + nt);
-    CellList& cl = p->cl;
-    if (ns > p->cl_cap) {
-        void* olds[] = {cl.src, cl.srcf, cl.orig, p->d_ckeys, p->d_ckeys2,
-                        p->d_cperm, p->d_cperm2, p->d_near_src, p->d_near_cub,
-                        p->d_tgt, p->d_tkeys, p->d_tkeys2, p->d_tperm};
+    const int64_t ns_all = n * (1 + nb + nt);
+    // the list holds [off, off + ns) of the sources [charges; bottom; top]
+    const int64_t off = (parts == CL_IMAGES) ? n : 0;
+    const int64_t ns = (parts == CL_CHARGES) ? n : (parts == CL_IMAGES ? ns_all - n : ns_all);
+    CellList& cl = clp ? *clp : p->cl;
+    if (ns > cl.cap) {
+        void* olds[] = {cl.src, cl.srcf, cl.orig};
         for (void* o : olds) dfree(p, o);
-        int64_t cap = ns < 64 ? 64 : ns;
+        const int64_t cap = ns < 64 ? 64 : ns;
         cl.src = dalloc<double4>(p, cap);
         cl.srcf = dalloc<float4>(p, cap);
         cl.orig = dalloc<int>(p, cap);
+        cl.cap = cap;
+    }
+    if (ns_all > p->cl_cap) {
+        void* olds[] = {p->d_ckeys, p->d_ckeys2,
+                        p->d_cperm, p->d_cperm2, p->d_near_src, p->d_near_cub,
+                        p->d_tgt, p->d_tkeys, p->d_tkeys2, p->d_tperm};
+        for (void* o : olds) dfree(p, o);
+        int64_t cap = ns_all < 64 ? 64 : ns_all;
         p->d_ckeys = dalloc<uint32_t>(p, cap);
         p->d_ckeys2 = dalloc<uint32_t>(p, cap);
         p->d_cperm = dalloc<int>(p, cap);
@@ -1139,16 +1149,17 @@ void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, boo
                                                 p->stream));
         p->near_cub_bytes = bytes;
         p->d_near_cub = dalloc<char>(p, bytes);
-        p->cl_cap = ns;
+        p->cl_cap = ns_all;
     }
     cl.n = ns;
-    if (ns == 0) return;
-    SrcBuild sb{d_pos, d_q, n, p->P.H, fb, ft, nb, nt, p->d_near_src, ns};
+    if (ns_all == 0) { cl.n = 0; return; }
+    SrcBuild sb{d_pos, d_q, n, p->P.H, fb, ft, nb, nt, p->d_near_src, ns_all};
     make_near_sources<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(sb);
     SE_LAUNCHED(p);
-    // device copy of the reference's KD-tree z origin (boundary pair tests)
+    // device copy of the reference's KD-tree z origin (boundary pair tests),
+    // over ALL sources whichever part this list holds
     if (!p->d_mm) p->d_mm = dalloc<double>(p, 256);
-    zrange_kernel<<<64, 256, 0, p->stream>>>(p->d_near_src, ns, p->d_mm);
+    zrange_kernel<<<64, 256, 0, p->stream>>>(p->d_near_src, ns_all, p->d_mm);
     SE_LAUNCHED(p);
     zmin_kernel<<<1, 1, 0, p->stream>>>(p->d_mm, 64, p->P.r_cut, d_zsrc_min, p->d_mm + 200);
     SE_LAUNCHED(p);
@@ -1179,14 +1190,18 @@ void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, boo
     cl.csz = zspan / cl.ncz;
     int64_t ncell = (int64_t)cl.ncx * cl.ncy * cl.ncz;
     if (ncell > (1 << 26)) throw Error(SE_ERR_VALUE, "near-field cell grid too large");
-    if (ncell + 1 > p->cell_cap) {
+    if (ncell + 1 > cl.cell_cap) {
         dfree(p, cl.start);
         cl.start = dalloc<int>(p, ncell + 1);
-        p->cell_cap = ncell + 1;
+        cl.cell_cap = ncell + 1;
     }
-    CellGeo g = cell_geo(p);
+    CellGeo g = cell_geo(p, cl);
+    if (ns == 0) {
+        SE_CUDA(cudaMemsetAsync(cl.start, 0, sizeof(int) * (ncell + 1), p->stream));
+        return;
+    }
     cell_keys_kernel<<<(unsigned)((ns + 255) / 256), 256, 0, p->stream>>>(
-        p->d_near_src, ns, g, p->d_ckeys, p->d_cperm);
+        p->d_near_src + off, ns, g, p->d_ckeys, p->d_cperm);
     SE_LAUNCHED(p);
     int end_bit = 1;
     while (end_bit < 32 && ((uint64_t)ncell >> end_bit) != 0) ++end_bit;
@@ -1195,8 +1210,8 @@ void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, boo
                                             p->d_cperm, p->d_cperm2, (int)ns, 0, end_bit,
                                             p->stream));
     cell_fill_kernel<<<(unsigned)((ns + 1 + 255) / 256), 256, 0, p->stream>>>(
-        p->d_ckeys2, p->d_cperm2, ns, (int)ncell, p->d_near_src, g, cl.start, cl.src,
-        cl.srcf, cl.orig);
+        p->d_ckeys2, p->d_cperm2, ns, (int)ncell, p->d_near_src + off, g, cl.start, cl.src,
+        cl.srcf, cl.orig, (int)off);
     SE_LAUNCHED(p);
 }
 
@@ -1330,15 +1345,16 @@ static double r2_threshold(double radius) {
     return t;
 }
 
-void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
-               const NearKernel& k, double* d_out4, int64_t* d_npairs) {
-    if (ne == 0) return;
-    NvtxRange nv("se.near_field");
+// kernel constants, cutoff tests, tables and buffers of one near-field
+// evaluation over cell list `cl` (the boundary-pair buffer is bnd / bnd_cnt)
+static NearArgs near_args(Plan* p, const CellList& cl, const double* d_eval, const int* d_order,
+                          int64_t ne, const NearKernel& k, double* d_out4, int64_t* d_npairs,
+                          int2*& bnd, int*& bnd_cnt, int64_t& bnd_cap, bool* close_ok_out) {
     bool close_ok = false;
     NearArgs a{};
     a.eval = d_eval; a.order = d_order; a.ne = ne;
-    a.g = cell_geo(p);
-    a.start = p->cl.start; a.src = p->cl.src; a.srcf = p->cl.srcf;
+    a.g = cell_geo(p, cl);
+    a.start = cl.start; a.src = cl.src; a.srcf = cl.srcf;
     a.r2max = r2_threshold(k.radius);
     a.rr = k.radius * k.radius;
     a.win_lo = std::min(a.rr, a.r2max) * (1.0 - 1e-12);
@@ -1346,25 +1362,25 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     a.zmin = p->d_mm + 200;
     {
         const int64_t cap = std::max<int64_t>(4096, 8 * ne);
-        if (cap > p->bnd_cap) {
-            dfree(p, p->d_bnd); dfree(p, p->d_bnd_cnt);
-            p->d_bnd = dalloc<int2>(p, cap);
-            p->d_bnd_cnt = dalloc<int>(p, 1);
-            p->bnd_cap = cap;
+        if (cap > bnd_cap) {
+            dfree(p, bnd); dfree(p, bnd_cnt);
+            bnd = dalloc<int2>(p, cap);
+            bnd_cnt = dalloc<int>(p, 1);
+            bnd_cap = cap;
         }
-        SE_CUDA(cudaMemsetAsync(p->d_bnd_cnt, 0, sizeof(int), p->stream));
-        a.bnd = p->d_bnd; a.bnd_cnt = p->d_bnd_cnt;
-        a.bnd_cap = (int)std::min<int64_t>(p->bnd_cap, INT32_MAX);
+        SE_CUDA(cudaMemsetAsync(bnd_cnt, 0, sizeof(int), p->stream));
+        a.bnd = bnd; a.bnd_cnt = bnd_cnt;
+        a.bnd_cap = (int)std::min<int64_t>(bnd_cap, INT32_MAX);
         a.flags = p->d_flags;
     }
     a.c1 = k.c1; a.c2 = k.c2; a.ic1 = 1.0 / k.c1; a.ic2 = 1.0 / k.c2;
     a.inv4pie = k.inv4pie;
     a.self_value = k.self_value; a.point0 = k.point0;
     a.kind = k.kind; a.need_field = k.need_field;
-    double rr = k.radius * (1.0 + 1e-5) + 4e-7 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(p->cl.zlo));
+    double rr = k.radius * (1.0 + 1e-5) + 4e-7 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(cl.zlo));
     a.r2f = (float)(rr * rr);
     // close path needed below max(6.5 c1, 0.01 c2) (+margin for fp32 error)
-    double rcl = std::max(6.5 * k.c1, 1e-2 * k.c2) * (1.0 + 1e-4) + 1e-6 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(p->cl.zlo));
+    double rcl = std::max(6.5 * k.c1, 1e-2 * k.c2) * (1.0 + 1e-4) + 1e-6 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(cl.zlo));
     a.r2close = (float)(rcl * rcl);
     {
         // close-pair table, cached per kernel (rebuilt when the kernel changes)
@@ -1399,7 +1415,7 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         for (int j = 0; j <= FAR_DEG32; ++j) a.pc32[j] = a.use_poly32 ? (float)c32[j] : 0.f;
     }
     {
-        const double err = 2.0 * 4e-7 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(p->cl.zlo));
+        const double err = 2.0 * 4e-7 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(cl.zlo));
         const double rin = std::max(0.0, k.radius - err), rout = k.radius + err;
         a.r2in_f = std::nextafter((float)(rin * rin), 0.0f);
         a.r2out_f = std::nextafter((float)(rout * rout), INFINITY);
@@ -1407,14 +1423,27 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     }
     a.Lxf = (float)p->P.Lx; a.Lyf = (float)p->P.Ly;
     a.iLxf = (float)(1.0 / p->P.Lx); a.iLyf = (float)(1.0 / p->P.Ly);
-    a.zmarg = (float)(1e-6 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(p->cl.zlo)));
+    a.zmarg = (float)(1e-6 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(cl.zlo)));
     a.out = d_out4; a.out_stride = ne;
     a.npairs = d_npairs;
-    a.orig = p->cl.orig;
+    a.orig = cl.orig;
     // the pair-set record belongs to the charges' evaluation (d_npairs set)
     a.phash = (d_npairs && p->pair_hash) ? p->d_phash : nullptr;
     const bool hash = a.phash != nullptr;
-    if (p->cl.n == 0) {
+    if (close_ok_out) *close_ok_out = close_ok;
+    return a;
+}
+
+void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
+               const NearKernel& k, double* d_out4, int64_t* d_npairs, const CellList* clp) {
+    if (ne == 0) return;
+    NvtxRange nv("se.near_field");
+    const CellList& cl = clp ? *clp : p->cl;
+    bool close_ok = false;
+    NearArgs a = near_args(p, cl, d_eval, d_order, ne, k, d_out4, d_npairs, p->d_bnd,
+                           p->d_bnd_cnt, p->bnd_cap, &close_ok);
+    const bool hash = a.phash != nullptr;
+    if (cl.n == 0) {
         SE_CUDA(cudaMemsetAsync(d_out4, 0, sizeof(double) * (k.need_field ? 4 : 1) * ne,
                                 p->stream));
         return;
@@ -1427,8 +1456,8 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         return;
     }
     // sort the evaluation points by cell and cut them into one-cell warp tasks
-    const int ncell = p->cl.ncx * p->cl.ncy * p->cl.ncz;
-    const int ncol = p->cl.ncx * p->cl.ncy;
+    const int ncell = cl.ncx * cl.ncy * cl.ncz;
+    const int ncol = cl.ncx * cl.ncy;
     NearScratch& ns = p->ns;
     const int64_t tcap = ne / 32 + ncol + 1;
     if (ne > ns.pcap || ncell + 1 > ns.ccap || tcap > ns.tcap) {
@@ -1456,7 +1485,7 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         ns.cub_bytes = std::max(b1, b2);
         ns.cub = dalloc<char>(p, ns.cub_bytes);
     }
-    CellGeo g = cell_geo(p);
+    CellGeo g = cell_geo(p, cl);
     point_keys_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, p->stream>>>(d_eval, ne, g, ns.keys,
                                                                              ns.perm);
     SE_LAUNCHED(p);
@@ -1490,7 +1519,7 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         SE_LAUNCHED(p);
         return;
     }
-    const int nzb = p->cl.ncz;
+    const int nzb = cl.ncz;
     task_count_kernel<<<(ncol + 255) / 256, 256, 0, p->stream>>>(ns.pstart, ncol, nzb, ns.tcount);
     SE_LAUNCHED(p);
     SE_CUDA(cudaMemsetAsync(ns.tcount + ncol, 0, sizeof(int), p->stream));
@@ -1508,8 +1537,8 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     const unsigned nblk = (unsigned)((tcap * 32 + NB_THREADS - 1) / NB_THREADS);
     // pair-list capacities from the expected neighbour count (+ margin);
     // an overflow doubles them and reruns the scan
-    const double vol_cell = p->cl.csx * p->cl.csy * p->cl.csz;
-    const double dens = (double)p->cl.n / ((double)ncell * vol_cell);
+    const double vol_cell = cl.csx * cl.csy * cl.csz;
+    const double dens = (double)cl.n / ((double)ncell * vol_cell);
     const double ball = 4.0 / 3.0 * M_PI * std::pow(k.radius, 3.0);
     const double rclose = std::sqrt((double)a.r2close);
     const double ballc = 4.0 / 3.0 * M_PI * std::pow(std::min(rclose, k.radius), 3.0);
@@ -1549,7 +1578,7 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     if (d_npairs) { p->ktic(3); p->ktic(4); }
     // 16-deep queues, 4 candidates per step, 7 CTAs / SM (73 registers):
     // measured best of queue 8..24, step 4 / 8, 6..12 CTAs (3.17 vs 3.29 ms at 10)
-    if (p->cl.ncx < 5 || p->cl.ncy < 5)
+    if (cl.ncx < 5 || cl.ncy < 5)
         near_scan_kernel<16, 4, 7, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
     else
         near_scan_kernel<16, 4, 7, false><<<nblk, NB_THREADS, 0, p->stream>>>(a);
