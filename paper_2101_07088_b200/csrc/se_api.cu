@@ -71,6 +71,28 @@ void make_plan2d(cufftHandle* h, int nx, int ny, int nyh, cufftType type,
 
 }  // namespace
 
+// buffers and cuFFT plans of the fp64 grid path, created on first use (a
+// plan that only runs fp32 solves never holds them: C5 needs ~37 GB less)
+void ensure_grid64(Plan* p) {
+    const size_t nz = (size_t)p->Nz;
+    if (!p->d_rho) {
+        p->d_rho = dalloc<double>(p, 2 * (size_t)p->G);
+        SE_CUDA(cudaMemsetAsync(p->d_rho, 0, 2 * (size_t)p->G * sizeof(double), p->stream));
+    }
+    if (!p->d_hat) p->d_hat = dalloc<cufftDoubleComplex>(p, nz * 2 * p->M);
+    if (!p->d_spec) p->d_spec = dalloc<cufftDoubleComplex>(p, nz * 4 * p->M);
+    if (!p->d_fields) p->d_fields = dalloc<double>(p, 4 * (size_t)p->G);
+    if (!p->fft_fwd2)
+        make_plan2d(&p->fft_fwd2, p->Nx, p->Ny, p->Nyh, CUFFT_D2Z, p->NXY, p->M, 2 * (int)nz,
+                    p->stream);
+    if (!p->fft_inv4)
+        make_plan2d(&p->fft_inv4, p->Nx, p->Ny, p->Nyh, CUFFT_Z2D, p->M, p->NXY, 4 * (int)nz,
+                    p->stream);
+    if (!p->fft_inv1)
+        make_plan2d(&p->fft_inv1, p->Nx, p->Ny, p->Nyh, CUFFT_Z2D, 4 * p->M, 4 * p->NXY,
+                    (int)nz, p->stream);
+}
+
 // buffers and cuFFT plans of the fp32 grid path, created on first use
 void ensure_grid32(Plan* p) {
     if (p->d_rho32) return;
@@ -413,6 +435,7 @@ void dist_setup(Plan* p, int rank, int nranks) {
     p->mc = (p->M + P - 1) / P;
     p->Nz_pad = p->zc * P;
     // full grids padded to whole slabs (pad planes stay zero)
+    ensure_grid64(p);
     dfree(p, p->d_rho); dfree(p, p->d_fields);
     p->d_rho = dalloc<double>(p, 2 * (size_t)p->Nz_pad * p->NXY);
     p->d_fields = dalloc<double>(p, 4 * (size_t)p->Nz_pad * p->NXY);
@@ -497,6 +520,7 @@ void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
     // fp32 mode of a whole (single-GPU) solve: the grid path in fp32 too
     p->g32 = (flags & SE_FP32) != 0;
     if (p->g32) ensure_grid32(p);
+    else ensure_grid64(p);
     const bool graph = (flags & SE_GRAPH) && !(flags & (SE_TIMINGS | SE_PAIR_HASH));
     const Plan::GraphKey key{d_pos, d_phi_out, d_E_out, n, flags};
     if (graph && p->gexec && p->gkey == key) {
@@ -692,12 +716,9 @@ int se_plan_create(const se_params* params, const double* z_nodes, const double*
         factor_bvp(p);
 
         // buffers
-        p->d_rho = dalloc<double>(p, 2 * (size_t)p->G);
-        SE_CUDA(cudaMemset(p->d_rho, 0, 2 * (size_t)p->G * sizeof(double)));
+        // the fp64 grids and their cuFFT plans come with the first fp64
+        // solve (ensure_grid64), the fp32 ones with the first fp32 solve
         p->d_ext = dalloc<cufftDoubleComplex>(p, (size_t)nz * 2 * p->M);
-        p->d_hat = dalloc<cufftDoubleComplex>(p, (size_t)nz * 2 * p->M);
-        p->d_spec = dalloc<cufftDoubleComplex>(p, (size_t)nz * 4 * p->M);
-        p->d_fields = dalloc<double>(p, 4 * (size_t)p->G);
         p->d_scr = dalloc<cufftDoubleComplex>(p, 6 * (size_t)nz * p->M);
         p->d_mom = dalloc<cufftDoubleComplex>(p, 2 * (size_t)p->M);
         p->d_mism = dalloc<cufftDoubleComplex>(p, 4 * (size_t)p->M);
@@ -742,10 +763,6 @@ int se_plan_create(const se_params* params, const double* z_nodes, const double*
         }
         p->sigma_scale = sscale;
 
-        // cuFFT plans
-        make_plan2d(&p->fft_fwd2, p->Nx, p->Ny, p->Nyh, CUFFT_D2Z, p->NXY, p->M, 2 * nz, p->stream);
-        make_plan2d(&p->fft_inv4, p->Nx, p->Ny, p->Nyh, CUFFT_Z2D, p->M, p->NXY, 4 * nz, p->stream);
-        make_plan2d(&p->fft_inv1, p->Nx, p->Ny, p->Nyh, CUFFT_Z2D, 4 * p->M, 4 * p->NXY, nz, p->stream);
         SE_CUDA(cudaStreamSynchronize(p->stream));
         *out = reinterpret_cast<se_plan*>(p);
         return SE_OK;
@@ -880,6 +897,7 @@ int se_shard_spread(se_plan* plan, const double* d_pos_all, int64_t n_all, int64
         if (!p) throw Error(SE_ERR_VALUE, "null plan");
         SE_CUDA(cudaSetDevice(p->dev));
         p->g32 = false;                 // the ranks sum fp64 grids
+        ensure_grid64(p);
         phase_spread(p, d_pos_all, n_all, first, count, flags);
         if (d_rho) *d_rho = p->d_rho;
         if (rho_len) *rho_len = 2 * p->G;
@@ -926,6 +944,7 @@ int se_shard_spread_own(se_plan* plan, const double* d_pos_own, int64_t n_all, i
         if (!p) throw Error(SE_ERR_VALUE, "null plan");
         SE_CUDA(cudaSetDevice(p->dev));
         p->g32 = false;
+        ensure_grid64(p);
         const double* base = d_pos_own - 3 * first;
         phase_spread(p, base, n_all, first, count, flags);
         if (d_rho) *d_rho = p->d_rho;
@@ -1274,9 +1293,9 @@ int64_t se_debug_fetch(se_plan* plan, int which, void* host, int64_t nbytes) {
     const void* src = nullptr;
     int64_t size = 0;
     switch (which) {
-        case 0: src = p->d_rho; size = 2 * p->G * sizeof(double); break;
+        case 0: src = p->d_rho; size = p->d_rho ? 2 * p->G * sizeof(double) : 0; break;
         case 1: src = p->d_keep; size = p->keep_stages ? p->Nz * 2 * p->M * 16 : 0; break;
-        case 2: src = p->d_fields; size = 4 * p->G * sizeof(double); break;
+        case 2: src = p->d_fields; size = p->d_fields ? 4 * p->G * sizeof(double) : 0; break;
         case 3: src = p->d_mism; size = 4 * p->M * 16; break;
         case 4: src = p->d_far; size = 4 * p->N * sizeof(double); break;
         case 5: src = p->d_near; size = 4 * p->N * sizeof(double); break;

@@ -414,6 +414,7 @@ void bvp_solve_view(Plan* p, bool two_grids, int mode, bool correction, const Mo
 void z_inverse_assemble(Plan* p, bool forces, bool correction, const ModeView& v);
 void forward_transforms(Plan* p, bool two_grids);
 void ensure_grid32(Plan* p);
+void ensure_grid64(Plan* p);
 void bvp_solve(Plan* p, bool two_grids, int mode, bool correction);
 void inverse_transforms(Plan* p, bool forces, bool correction);
 
