@@ -128,6 +128,7 @@ struct TpNearPair {
 // neighbour cell, the hits are compacted into a per-warp queue (ballot) and
 // evaluated 32 at a time, so the expensive pair term runs on full warps.
 constexpr int PAIR_WARPS = 4;
+constexpr int PAIR_MAXC = 125;                 // neighbour cells per particle (reach <= 2)
 
 template <class Pair>
 __global__ void __launch_bounds__(PAIR_WARPS * 32) pair_gather_kernel(
@@ -140,12 +141,33 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32) pair_gather_kernel(
     const double px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
     const int c0[3] = {axis_cell(g, 0, px), axis_cell(g, 1, py), axis_cell(g, 2, pz)};
     int cnt[3], first[3];
+    bool all[3];
+    double pw[3];                              // position in the cell frame
+    const double pp[3] = {px, py, pz};
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-        const bool all = g.per[ax] && g.nc[ax] < 2 * g.reach + 1;
-        cnt[ax] = all ? g.nc[ax] : 2 * g.reach + 1;
-        first[ax] = all ? 0 : c0[ax] - g.reach;
+        all[ax] = g.per[ax] && g.nc[ax] < 2 * g.reach + 1;
+        cnt[ax] = all[ax] ? g.nc[ax] : 2 * g.reach + 1;
+        first[ax] = all[ax] ? 0 : c0[ax] - g.reach;
+        if (g.per[ax]) {
+            double w = pp[ax] - g.L[ax] * floor(pp[ax] / g.L[ax]);
+            pw[ax] = w >= g.L[ax] ? 0.0 : w;
+        } else {
+            pw[ax] = pp[ax] - g.lo[ax];
+        }
     }
+    // distance from the particle to the slab of neighbour cell i along an
+    // axis: cells farther than the cutoff are skipped (with reach > 1 the
+    // corner cells of the (2 reach + 1)^3 block mostly are)
+    auto gap = [&](int ax, int i) -> double {
+        if (all[ax]) return 0.0;
+        const int u = first[ax] + i;
+        // open-axis edge cells also hold the clamped points outside the range
+        if (!g.per[ax] && (u <= 0 || u >= g.nc[ax] - 1)) return 0.0;
+        const double lo = u * g.cs[ax], hi = lo + g.cs[ax];
+        return fmax(0.0, fmax(lo - pw[ax], pw[ax] - hi));
+    };
+    const double cut2 = g.cut2_hi;
     double fx = 0.0, fy = 0.0, fz = 0.0;
     int qn = 0;
     auto eval = [&](int e) {
@@ -156,69 +178,101 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32) pair_gather_kernel(
         fy += f * qd[wib][1][e] * sq;
         fz += f * qd[wib][2][e] * sq;
     };
-    for (int iz = 0; iz < cnt[2]; ++iz) {
-        int zc = first[2] + iz;
-        if (g.per[2]) { if (zc < 0) zc += g.nc[2]; else if (zc >= g.nc[2]) zc -= g.nc[2]; }
-        else if (zc < 0 || zc >= g.nc[2]) continue;
-        for (int iy = 0; iy < cnt[1]; ++iy) {
-            int yc = first[1] + iy;
+    // the neighbour cells' candidate ranges (pruned by distance) are listed
+    // per warp first, then the lanes walk their concatenation 32 candidates
+    // at a time: at low density (a few particles per cell) a batch spans
+    // several cells instead of one mostly idle batch per cell
+    __shared__ int rs[PAIR_WARPS][PAIR_MAXC + 1], rb[PAIR_WARPS][PAIR_MAXC];
+    const int ncand_cells = cnt[0] * cnt[1] * cnt[2];
+    int total = 0;
+    for (int c0i = 0; c0i < ncand_cells; c0i += 32) {
+        const int ci = c0i + lane;
+        int b0 = 0, len = 0;
+        if (ci < ncand_cells) {
+            const int ix = ci % cnt[0], iy = (ci / cnt[0]) % cnt[1], iz = ci / (cnt[0] * cnt[1]);
+            int xc = first[0] + ix, yc = first[1] + iy, zc = first[2] + iz;
+            bool ok = true;
+            if (g.per[0]) { if (xc < 0) xc += g.nc[0]; else if (xc >= g.nc[0]) xc -= g.nc[0]; }
+            else ok &= xc >= 0 && xc < g.nc[0];
             if (g.per[1]) { if (yc < 0) yc += g.nc[1]; else if (yc >= g.nc[1]) yc -= g.nc[1]; }
-            else if (yc < 0 || yc >= g.nc[1]) continue;
-            for (int ix = 0; ix < cnt[0]; ++ix) {
-                int xc = first[0] + ix;
-                if (g.per[0]) { if (xc < 0) xc += g.nc[0]; else if (xc >= g.nc[0]) xc -= g.nc[0]; }
-                else if (xc < 0 || xc >= g.nc[0]) continue;
-                const int c = (zc * g.nc[1] + yc) * g.nc[0] + xc;
-                const int e0 = g.start[c], e1 = g.start[c + 1];
-                for (int b = e0; b < e1; b += 32) {
-                    const int s = b + lane;
-                    bool hit = false;
-                    double d[3], r = 0.0, qv = 1.0;
-                    int j = -1;
-                    if (s < e1) {
-                        j = g.order[s];
-                        const double4 v = g.spos[s];
-                        qv = v.w;
-                        // d = p_i - p_j; d -= L round(d / L) on periodic axes.
-                        // round(d * (1/L)) differs from round(d / L) only
-                        // for |d| within ulps of L/2 > cutoff: never a pair
-                        d[0] = __dsub_rn(px, v.x);
-                        d[1] = __dsub_rn(py, v.y);
-                        d[2] = __dsub_rn(pz, v.z);
-#pragma unroll
-                        for (int ax = 0; ax < 3; ++ax)
-                            if (g.per[ax]) d[ax] = __dsub_rn(d[ax], __dmul_rn(g.L[ax], rint(d[ax] * g.iL[ax])));
-                        const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])),
-                                                    __dmul_rn(d[2], d[2]));
-                        // sqrt (correctly rounded) only near or inside the cutoff
-                        if (r2 <= g.cut2_hi) {
-                            r = sqrt(r2);
-                            hit = j != i && r <= cutoff;
-                        }
-                    }
-                    const unsigned bal = __ballot_sync(0xffffffffu, hit);
-                    if (hit) {
-                        const int slot = qn + __popc(bal & ((1u << lane) - 1u));
-                        qd[wib][0][slot] = d[0]; qd[wib][1][slot] = d[1];
-                        qd[wib][2][slot] = d[2]; qd[wib][3][slot] = r;
-                        if (Pair::kUsesQ) qd[wib][4][slot] = qv;
-                        qj[wib][slot] = j;
-                    }
-                    qn += __popc(bal);
-                    __syncwarp();
-                    if (qn >= 32) {
-                        eval(lane);
-                        __syncwarp();
-                        if (lane < qn - 32) {
-#pragma unroll
-                            for (int k = 0; k < 5; ++k) qd[wib][k][lane] = qd[wib][k][32 + lane];
-                            qj[wib][lane] = qj[wib][32 + lane];
-                        }
-                        qn -= 32;
-                        __syncwarp();
-                    }
-                }
+            else ok &= yc >= 0 && yc < g.nc[1];
+            if (g.per[2]) { if (zc < 0) zc += g.nc[2]; else if (zc >= g.nc[2]) zc -= g.nc[2]; }
+            else ok &= zc >= 0 && zc < g.nc[2];
+            if (ok) {
+                const double gx = gap(0, ix), gy = gap(1, iy), gz = gap(2, iz);
+                ok = gx * gx + gy * gy + gz * gz <= cut2;
             }
+            if (ok) {
+                const int c = (zc * g.nc[1] + yc) * g.nc[0] + xc;
+                b0 = g.start[c];
+                len = g.start[c + 1] - b0;
+            }
+        }
+        // warp prefix sum of the lengths
+        int pre = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += u;
+        }
+        const int tot = __shfl_sync(0xffffffffu, pre, 31);
+        if (ci < ncand_cells) {
+            rs[wib][ci] = total + pre - len;
+            rb[wib][ci] = b0;
+        }
+        total += tot;
+    }
+    if (lane == 0) rs[wib][ncand_cells] = total;
+    __syncwarp();
+    int cell = 0;
+    for (int b = 0; b < total; b += 32) {
+        const int qi = b + lane;
+        bool hit = false;
+        double d[3], r = 0.0, qv = 1.0;
+        int j = -1;
+        if (qi < total) {
+            while (rs[wib][cell + 1] <= qi) ++cell;          // ascending per lane
+            const int sidx = rb[wib][cell] + (qi - rs[wib][cell]);
+            j = g.order[sidx];
+            const double4 v = g.spos[sidx];
+            qv = v.w;
+            // d = p_i - p_j; d -= L round(d / L) on periodic axes.
+            // round(d * (1/L)) differs from round(d / L) only
+            // for |d| within ulps of L/2 > cutoff: never a pair
+            d[0] = __dsub_rn(px, v.x);
+            d[1] = __dsub_rn(py, v.y);
+            d[2] = __dsub_rn(pz, v.z);
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax)
+                if (g.per[ax]) d[ax] = __dsub_rn(d[ax], __dmul_rn(g.L[ax], rint(d[ax] * g.iL[ax])));
+            const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])),
+                                        __dmul_rn(d[2], d[2]));
+            // sqrt (correctly rounded) only near or inside the cutoff
+            if (r2 <= g.cut2_hi) {
+                r = sqrt(r2);
+                hit = j != i && r <= cutoff;
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+            const int slot = qn + __popc(bal & ((1u << lane) - 1u));
+            qd[wib][0][slot] = d[0]; qd[wib][1][slot] = d[1];
+            qd[wib][2][slot] = d[2]; qd[wib][3][slot] = r;
+            if (Pair::kUsesQ) qd[wib][4][slot] = qv;
+            qj[wib][slot] = j;
+        }
+        qn += __popc(bal);
+        __syncwarp();
+        if (qn >= 32) {
+            eval(lane);
+            __syncwarp();
+            if (lane < qn - 32) {
+#pragma unroll
+                for (int k = 0; k < 5; ++k) qd[wib][k][lane] = qd[wib][k][32 + lane];
+                qj[wib][lane] = qj[wib][32 + lane];
+            }
+            qn -= 32;
+            __syncwarp();
         }
     }
     if (lane < qn) eval(lane);
