@@ -678,6 +678,52 @@ __global__ void point_interp_kernel(PointArgs a) {
     if (lane == 0) a.out[wid] = a.hx * a.hy * sum;
 }
 
+// the same for a few points (the gauge origin): one CTA per point, a thread
+// per stencil column, block reduction -- a single warp walking 169 columns x
+// ~17 nodes of exp() is latency-bound (~55 us at the paper configuration)
+__global__ void __launch_bounds__(256) point_interp_cta_kernel(PointArgs a) {
+    __shared__ double red[8];
+    const int64_t pt = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double px = a.pts[3 * pt], py = a.pts[3 * pt + 1], pz = a.pts[3 * pt + 2];
+    if (tid == 0 && (pz < a.z0 || pz > a.z1)) atomicOr(a.flags, FLAG_Z_OUTSIDE);
+    const double A_i = a.scal[0];
+    const long long jx = (long long)floor(px / a.hx), jy = (long long)floor(py / a.hy);
+    const int lo = lower_bound_d(a.znodes, a.Nz, __dsub_rn(pz, a.rad));
+    const int hi = upper_bound_d(a.znodes, a.Nz, __dadd_rn(pz, a.rad));
+    const int wx = 2 * a.mx + 1, wy = 2 * a.my + 1;
+    double sum = 0.0;
+    for (int e = tid; e < wx * wy; e += blockDim.x) {
+        const int ox = e / wy, oy = e % wy;
+        const double dx = __dsub_rn(px, __dmul_rn((double)(jx + ox - a.mx), a.hx));
+        const double dy = __dsub_rn(py, __dmul_rn((double)(jy + oy - a.my), a.hy));
+        if (fabs(dx) > a.rad_keep || fabs(dy) > a.rad_keep) continue;
+        const double tx = dx / a.width, ty = dy / a.width;
+        const double wxy = (exp(-0.5 * (tx * tx)) / a.norm) * (exp(-0.5 * (ty * ty)) / a.norm);
+        const int gx = pmod(jx + ox - a.mx, a.Nx), gy = pmod(jy + oy - a.my, a.Ny);
+        double col = 0.0;
+        for (int k = lo; k < hi; ++k) {
+            const double dz = __dsub_rn(pz, a.znodes[k]);
+            if (fabs(dz) > a.rad) continue;
+            const double tz = dz / a.width;
+            const double wz = exp(-0.5 * (tz * tz)) / a.norm * a.wcc[k];
+            const int64_t at = ((int64_t)k * 4) * a.NXY + (int64_t)gx * a.Ny + gy;
+            const double f = (a.fields32 ? (double)a.fields32[at] : a.fields[at]) + A_i * a.znodes[k];
+            col += wz * f;
+        }
+        sum += wxy * col;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    if (lane == 0) red[warp] = sum;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        a.out[pt] = a.hx * a.hy * t;
+    }
+}
+
 int zbits_for(int Nz) {
     int b = 1;
     while ((1 << b) <= Nz) ++b;
@@ -1003,8 +1049,12 @@ void interp_points(Plan* p, const double* d_pts, int64_t npts, double width,
     a.mx = (int)std::floor(radius / p->hx + 1e-12);
     a.my = (int)std::floor(radius / p->hy + 1e-12);
     a.out = d_out; a.flags = p->d_flags; a.z0 = p->P.z0; a.z1 = p->P.z1;
-    int64_t threads = npts * 32;
-    point_interp_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, p->stream>>>(a);
+    if (npts <= 64) {
+        point_interp_cta_kernel<<<(unsigned)npts, 256, 0, p->stream>>>(a);
+    } else {
+        const int64_t threads = npts * 32;
+        point_interp_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, p->stream>>>(a);
+    }
     SE_LAUNCHED(p);
 }
 

@@ -489,6 +489,378 @@ __global__ void __launch_bounds__(64) bvp_kernel(BvpArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Small problems: the mode BVP with a WARP per (mode, grid) column.  With a
+// few thousand modes (the paper's N_xy = 88: 3960) the lane-pair kernel runs
+// ~8000 threads, one or two warps per SM, each walking ~14 dependent sweeps
+// of Nz rows -- latency, not bandwidth.  Here the parity-split Thomas sweeps
+// (bvp.py:76-90, 216-227), the derivative recurrence (chebyshev.py:68-79)
+// and the Schur / wall sums are chunked warp scans: lane l owns rows
+// [l C, (l+1) C), C = ceil(Nz / 32), composes its chunk's affine maps, one
+// 5-step shuffle scan carries each chain into every chunk, and the chunk is
+// swept again.  The column, its y'' and Thomas scratch, the k-only maps and
+// the mode's per-|k| factor rows are staged in shared memory (coalesced), so
+// a sweep costs ~C + 5 dependent steps instead of Nz.  At the north-star
+// size (33 K modes) the lane-pair kernel is faster (1.27 vs 1.61 ms): the
+// dispatch takes this kernel below BVPW_MAX_MODES.
+// ---------------------------------------------------------------------------
+constexpr int BVPW_MODES = 2;                   // modes per CTA (x 2 grids = warps)
+constexpr int64_t BVPW_MAX_MODES = 12000;
+constexpr int BVPW_MAPS = 7;                    // q_lo q_dg q_hi e_lo e_hi tw0 twH
+constexpr int BVPW_FACS = 5;                    // cp inv aib c0 c1 (FAC_* order)
+constexpr unsigned BFULL = 0xffffffffu;
+
+__host__ __device__ inline int bvpw_dbl(int n) {         // maps + factors, 16 B aligned
+    return ((BVPW_MAPS + BVPW_MODES * BVPW_FACS) * n + 1) & ~1;
+}
+__host__ __device__ inline size_t bvpw_smem(int n) {
+    return (size_t)bvpw_dbl(n) * 8 + (size_t)2 * BVPW_MODES * 3 * n * 16;
+}
+
+__device__ __forceinline__ double2 shfl_up2(double2 v, int o) {
+    return make_double2(__shfl_up_sync(BFULL, v.x, o), __shfl_up_sync(BFULL, v.y, o));
+}
+__device__ __forceinline__ double2 shfl_down2(double2 v, int o) {
+    return make_double2(__shfl_down_sync(BFULL, v.x, o), __shfl_down_sync(BFULL, v.y, o));
+}
+__device__ __forceinline__ double2 warp_sum2(double2 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(BFULL, v.x, o);
+        v.y += __shfl_xor_sync(BFULL, v.y, o);
+    }
+    return v;
+}
+
+// Carry of an affine chain x_next = a x_prev + b across the warp's chunks:
+// (a, b) is the composition of this lane's chunk for each parity; returns
+// the value entering this lane's chunk (the chain starts from 0).  up: the
+// chain runs with the lane index (forward sweep), else against it.
+__device__ __forceinline__ void chain_carry(double (&a)[2], double2 (&b)[2], bool up, int lane,
+                                            double2 (&in)[2]) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const double ap = up ? __shfl_up_sync(BFULL, a[q], o) : __shfl_down_sync(BFULL, a[q], o);
+            const double2 bp = up ? shfl_up2(b[q], o) : shfl_down2(b[q], o);
+            if (up ? lane >= o : lane + o < 32) {
+                b[q] = make_double2(fma(a[q], bp.x, b[q].x), fma(a[q], bp.y, b[q].y));
+                a[q] *= ap;
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const double2 v = up ? shfl_up2(b[q], 1) : shfl_down2(b[q], 1);
+        const bool first = up ? lane == 0 : lane == 31;
+        in[q] = first ? make_double2(0, 0) : v;
+    }
+}
+
+// exclusive suffix sums of the lane totals, per parity (against the lane index)
+__device__ __forceinline__ void suffix_carry(double2 (&t)[2], int lane, double2 (&in)[2]) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const double2 v = shfl_down2(t[q], o);
+            if (lane + o < 32) t[q] = cadd(t[q], v);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const double2 v = shfl_down2(t[q], 1);
+        in[q] = lane == 31 ? make_double2(0, 0) : v;
+    }
+}
+
+__global__ void __launch_bounds__(64 * BVPW_MODES) bvp_warp_kernel(BvpArgs a) {
+    extern __shared__ double2 bsm[];
+    __shared__ double2 wall[2 * BVPW_MODES][6];
+    const int n = a.Nz;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = warp & 1, mi = warp >> 1;
+    const int64_t mb = (int64_t)blockIdx.x * BVPW_MODES;
+    const int64_t m = mb + mi;
+    const bool valid = m < a.Mv;
+    double* maps = reinterpret_cast<double*>(bsm);
+    double* facs = maps + BVPW_MAPS * n;
+    double2* cols = reinterpret_cast<double2*>(maps + bvpw_dbl(n));
+    const double* srcmap[BVPW_MAPS] = {a.mp.q_lo, a.mp.q_dg, a.mp.q_hi, a.mp.e_lo, a.mp.e_hi,
+                                       a.tw0, a.twH};
+    constexpr int U = 8;                         // loads in flight per thread
+    {
+        const int tot = BVPW_MAPS * n;
+        for (int b0 = 0; b0 < tot; b0 += U * blockDim.x) {
+            double v[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int e = b0 + j * blockDim.x + tid;
+                v[j] = e < tot ? __ldg(srcmap[e / n] + e % n) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int e = b0 + j * blockDim.x + tid;
+                if (e < tot) maps[e] = v[j];
+            }
+        }
+    }
+    {
+        const int tot = BVPW_MODES * BVPW_FACS * n;
+        for (int b0 = 0; b0 < tot; b0 += U * blockDim.x) {
+            double v[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int e = b0 + j * blockDim.x + tid;
+                const int md = e / (BVPW_FACS * n), r = e - md * BVPW_FACS * n;
+                const int64_t mm = mb + md;
+                const int u = (e < tot && mm < a.Mv) ? a.kidx[mm] : -1;
+                v[j] = u >= 0 ? __ldg(a.fac + (int64_t)u * FAC_ROWS * n + r) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int e = b0 + j * blockDim.x + tid;
+                if (e < tot) facs[e] = v[j];
+            }
+        }
+    }
+    // the columns' Chebyshev coefficients: row k holds 2 grids x the CTA's
+    // modes (two contiguous runs)
+    const int64_t RS = 2 * a.M;
+    const double base = -(a.half * a.half) / a.eps * a.inv_nxy;
+    {
+        const int tot = n * 2 * BVPW_MODES;
+        for (int b0 = 0; b0 < tot; b0 += U * blockDim.x) {
+            double2 v[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int e = b0 + j * blockDim.x + tid;
+                const int k = e / (2 * BVPW_MODES), r = e - k * 2 * BVPW_MODES;
+                const int gg = r / BVPW_MODES, md = r - gg * BVPW_MODES;
+                const int64_t mm = mb + md;
+                v[j] = (e < tot && mm < a.Mv) ? a.ext[(int64_t)k * RS + gg * a.M + mm]
+                                              : make_double2(0, 0);
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int e = b0 + j * blockDim.x + tid;
+                if (e < tot) {
+                    const int k = e / (2 * BVPW_MODES), r = e - k * 2 * BVPW_MODES;
+                    const int gg = r / BVPW_MODES, md = r - gg * BVPW_MODES;
+                    cols[(size_t)(2 * md + gg) * 3 * n + k] = cscale(v[j], base);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const double* q_lo = maps;
+    const double* q_dg = maps + n;
+    const double* q_hi = maps + 2 * n;
+    const double* e_lo = maps + 3 * n;
+    const double* e_hi = maps + 4 * n;
+    const double* tw0 = maps + 5 * n;
+    const double* twH = maps + 6 * n;
+    double2* F = cols + (size_t)warp * 3 * n;    // right-hand side f_sc
+    double2* A = F + n;                          // y''
+    double2* B = A + n;                          // Thomas d / x
+    const int C = (n + 31) / 32, k0 = lane * C, k1 = min(n, k0 + C);
+    double2 w_out[4], e_out[2];
+    for (int q = 0; q < 4; ++q) w_out[q] = make_double2(0, 0);
+    e_out[0] = e_out[1] = make_double2(0, 0);
+    const bool solve = valid && (a.two || g == 1);
+    if (solve) {                                  // warp-uniform
+        const int u = a.kidx[m];
+        double2 c0v = make_double2(0, 0), c1v = make_double2(0, 0);
+        auto yq_at = [&](int k) -> double2 {      // (Q y'')_k, k > 0
+            double2 y = cscale(A[k], q_dg[k]);
+            if (k >= 2) y = cadd(y, cscale(A[k - 2], q_lo[k]));
+            if (k + 2 < n) y = cadd(y, cscale(A[k + 2], q_hi[k]));
+            return y;
+        };
+        if (u < 0) {
+            // ---- k = 0: y'' = f, y(z0) = y(z1) = 0           bvp.py:281-296
+            for (int k = k0; k < k1; ++k) A[k] = F[k];
+            __syncwarp();
+            double2 P = make_double2(0, 0), Qs = make_double2(0, 0);
+            for (int k = max(k0, 1); k < k1; ++k) {
+                const double2 y = yq_at(k);
+                P = cadd(P, y);
+                Qs = (k & 1) ? csub(Qs, y) : cadd(Qs, y);
+            }
+            P = warp_sum2(P); Qs = warp_sum2(Qs);
+            c0v = cscale(cadd(P, Qs), -0.5);
+            c1v = cscale(csub(Qs, P), 0.5);
+        } else {
+            const double* fm = facs + (size_t)mi * BVPW_FACS * n;
+            const double* cp = fm + FAC_CP * n;
+            const double* iv = fm + FAC_INV * n;
+            const double* aib = fm + FAC_AINVB * n;
+            const double* cr0 = fm + FAC_C0 * n;
+            const double* cr1 = fm + FAC_C1 * n;
+            const double kap = a.kappa[u], k2 = kap * kap;
+            const double S00 = a.sinv[4 * u], S01 = a.sinv[4 * u + 1];
+            const double S10 = a.sinv[4 * u + 2], S11 = a.sinv[4 * u + 3];
+            // forward sweep d_k = alpha_k d_{k-2} + beta_k, alpha_k = k^2 q_lo
+            // iv, beta_k = r_k iv; r = F (first) or the residual in B
+            auto forward = [&](bool from_f) {
+                double ca[2] = {1.0, 1.0};
+                double2 cb[2] = {make_double2(0, 0), make_double2(0, 0)};
+                for (int k = k0; k < k1; ++k) {
+                    const int q = k & 1;
+                    const double al = k >= 2 ? k2 * q_lo[k] * iv[k] : 0.0;
+                    const double2 be = cscale(from_f ? F[k] : B[k], iv[k]);
+                    cb[q] = make_double2(fma(al, cb[q].x, be.x), fma(al, cb[q].y, be.y));
+                    ca[q] *= al;
+                }
+                double2 in[2];
+                chain_carry(ca, cb, true, lane, in);
+                for (int k = k0; k < k1; ++k) {
+                    const int q = k & 1;
+                    const double al = k >= 2 ? k2 * q_lo[k] * iv[k] : 0.0;
+                    const double2 be = cscale(from_f ? F[k] : B[k], iv[k]);
+                    const double2 d = make_double2(fma(al, in[q].x, be.x), fma(al, in[q].y, be.y));
+                    B[k] = d;
+                    in[q] = d;
+                }
+                __syncwarp();
+            };
+            // backward sweep x_k = -cp_k x_{k+2} + d_k; Schur rhs C.x
+            auto backward = [&](double2& s0, double2& s1) {
+                double ca[2] = {1.0, 1.0};
+                double2 cb[2] = {make_double2(0, 0), make_double2(0, 0)};
+                for (int k = k1 - 1; k >= k0; --k) {
+                    const int q = k & 1;
+                    const double ga = k + 2 < n ? -cp[k] : 0.0;
+                    const double2 d = B[k];
+                    cb[q] = make_double2(fma(ga, cb[q].x, d.x), fma(ga, cb[q].y, d.y));
+                    ca[q] *= ga;
+                }
+                double2 in[2];
+                chain_carry(ca, cb, false, lane, in);
+                s0 = make_double2(0, 0); s1 = make_double2(0, 0);
+                for (int k = k1 - 1; k >= k0; --k) {
+                    const int q = k & 1;
+                    const double ga = k + 2 < n ? -cp[k] : 0.0;
+                    const double2 d = B[k];
+                    const double2 x = make_double2(fma(ga, in[q].x, d.x), fma(ga, in[q].y, d.y));
+                    B[k] = x;
+                    in[q] = x;
+                    s0 = cfma(cr0[k], x, s0);
+                    s1 = cfma(cr1[k], x, s1);
+                }
+                s0 = warp_sum2(s0); s1 = warp_sum2(s1);
+                __syncwarp();
+            };
+            auto update = [&](double2 v0, double2 v1, bool accumulate) {
+                for (int k = k0; k < k1; ++k) {
+                    double2 y = cfma(-aib[k], (k & 1) ? v1 : v0, B[k]);
+                    if (accumulate) y = cadd(A[k], y);
+                    A[k] = y;
+                }
+                __syncwarp();
+            };
+            double2 s0, s1;
+            forward(true);
+            backward(s0, s1);
+            c0v = make_double2(S00 * s0.x + S01 * s1.x, S00 * s0.y + S01 * s1.y);
+            c1v = make_double2(S10 * s0.x + S11 * s1.x, S10 * s0.y + S11 * s1.y);
+            update(c0v, c1v, false);
+            for (int it = 0; it < a.refine; ++it) {     // bvp.py:229-246,268-273
+                double2 yq_sum = make_double2(0, 0), yq_sgn = make_double2(0, 0);
+                double2 ye_sum = make_double2(0, 0), ye_sgn = make_double2(0, 0);
+                for (int k = k0; k < k1; ++k) {
+                    double2 yq = make_double2(0, 0), ye = make_double2(0, 0);
+                    if (k > 0) {
+                        yq = yq_at(k);
+                        ye = cscale(A[k - 1], e_lo[k]);
+                        if (k + 1 < n) ye = cadd(ye, cscale(A[k + 1], e_hi[k]));
+                    }
+                    double2 r = csub(F[k], csub(A[k], cscale(yq, k2)));
+                    if (k == 0) r = cadd(r, cscale(c0v, k2));
+                    if (k == 1) r = cadd(r, cscale(c1v, k2));
+                    yq_sum = cadd(yq_sum, yq); ye_sum = cadd(ye_sum, ye);
+                    if (k & 1) { yq_sgn = csub(yq_sgn, yq); ye_sgn = csub(ye_sgn, ye); }
+                    else { yq_sgn = cadd(yq_sgn, yq); ye_sgn = cadd(ye_sgn, ye); }
+                    B[k] = r;
+                }
+                yq_sum = warp_sum2(yq_sum); ye_sum = warp_sum2(ye_sum);
+                yq_sgn = warp_sum2(yq_sgn); ye_sgn = warp_sum2(ye_sgn);
+                __syncwarp();
+                const double2 r20 = cscale(cadd(cadd(ye_sum, cscale(yq_sum, kap)),
+                                                cadd(cscale(c0v, kap), cscale(c1v, 1.0 + kap))), -1.0);
+                const double2 r21 = cscale(cadd(csub(ye_sgn, cscale(yq_sgn, kap)),
+                                                cadd(cscale(c0v, -kap), cscale(c1v, 1.0 + kap))), -1.0);
+                forward(false);
+                double2 t0, t1;
+                backward(t0, t1);
+                t0 = csub(t0, r20); t1 = csub(t1, r21);
+                const double2 dc0 = make_double2(S00 * t0.x + S01 * t1.x, S00 * t0.y + S01 * t1.y);
+                const double2 dc1 = make_double2(S10 * t0.x + S11 * t1.x, S10 * t0.y + S11 * t1.y);
+                update(dc0, dc1, true);
+                c0v = cadd(c0v, dc0);
+                c1v = cadd(c1v, dc1);
+            }
+        }
+        // ---- y = Q y'' + c0 T0 + c1 T1 (into F), the derivative b by suffix
+        // sums of w_j = 2 j y_j over each parity chain (into B), wall values
+        for (int k = k0; k < k1; ++k) {
+            double2 y = k > 0 ? yq_at(k) : make_double2(0, 0);
+            if (k == 0) y = cadd(y, c0v);
+            if (k == 1) y = cadd(y, c1v);
+            F[k] = y;
+        }
+        __syncwarp();
+        double2 tot[2] = {make_double2(0, 0), make_double2(0, 0)};
+        for (int k = k0; k < k1; ++k) tot[k & 1] = cfma(2.0 * k, F[k], tot[k & 1]);
+        double2 run[2];
+        suffix_carry(tot, lane, run);
+        const double dscale = 2.0 / (a.z1 - a.z0);
+        double2 w_y0 = make_double2(0, 0), w_yH = make_double2(0, 0);
+        double2 w_d0 = make_double2(0, 0), w_dH = make_double2(0, 0);
+        double2 d_sum = make_double2(0, 0), d_sgn = make_double2(0, 0);
+        for (int k = k1 - 1; k >= k0; --k) {
+            const double2 y = F[k];
+            const double2 b = run[(k + 1) & 1];       // sum of w_j, j > k, j = k+1 mod 2
+            run[k & 1] = cfma(2.0 * k, y, run[k & 1]);
+            const double2 bs = cscale(k == 0 ? cscale(b, 0.5) : b, dscale);
+            B[k] = bs;
+            w_y0 = cfma(tw0[k], y, w_y0);
+            w_yH = cfma(twH[k], y, w_yH);
+            w_d0 = cfma(tw0[k], bs, w_d0);
+            w_dH = cfma(twH[k], bs, w_dH);
+            d_sum = cadd(d_sum, bs);
+            d_sgn = (k & 1) ? csub(d_sgn, bs) : cadd(d_sgn, bs);
+        }
+        w_out[0] = warp_sum2(w_y0); w_out[1] = warp_sum2(w_yH);
+        w_out[2] = warp_sum2(w_d0); w_out[3] = warp_sum2(w_dH);
+        e_out[0] = warp_sum2(d_sgn); e_out[1] = warp_sum2(d_sum);
+    }
+    if (lane == 0) {
+        for (int q = 0; q < 4; ++q) wall[warp][q] = w_out[q];
+        wall[warp][4] = e_out[0]; wall[warp][5] = e_out[1];
+    }
+    __syncthreads();
+    // coalesced stores: psi (F) and dpsi (B) coefficients of the in-slab
+    // columns for the iDCT (slot 0 / 1 of ext), the debug copy of both grids
+    for (int e = tid; e < n * 2 * BVPW_MODES; e += blockDim.x) {
+        const int k = e / (2 * BVPW_MODES), r = e - k * 2 * BVPW_MODES;
+        const int slot = r / BVPW_MODES, md = r - slot * BVPW_MODES;
+        const int64_t mm = mb + md;
+        if (mm >= a.Mv) continue;
+        const double2* col = cols + (size_t)(2 * md + 1) * 3 * n;
+        a.ext[(int64_t)k * RS + slot * a.M + mm] = slot ? col[2 * n + k] : col[k];
+        if (a.keep && (slot == 1 || a.two))
+            a.keep[((int64_t)k * 2 + slot) * a.M + mm] = cols[(size_t)(2 * md + slot) * 3 * n + k];
+    }
+    if (!valid || g == 0 || lane != 0) return;
+    double2 wi[4], ei[2], wo[4], eo[2];
+    for (int q = 0; q < 4; ++q) { wi[q] = wall[warp][q]; wo[q] = wall[warp - 1][q]; }
+    ei[0] = wall[warp][4]; ei[1] = wall[warp][5];
+    eo[0] = wall[warp - 1][4]; eo[1] = wall[warp - 1][5];
+    finish_mode(a, m, wi, ei, wo, eo);
+}
+
+// ---------------------------------------------------------------------------
 // z DCT-I (chebyshev.py:46-65) as hand-written FP64 tensor-core products.
 // With the node reflection j -> N - j the (Nz x Nz) transform splits into
 // an even-coefficient half acting on s_c = v_c + v_{N-c} and an odd half
@@ -936,7 +1308,15 @@ void bvp_solve_view(Plan* p, bool two_grids, int mode, bool correction, const Mo
     a.k0out = p->d_k0; a.scal = p->d_scal; a.flags = p->d_flags;
     a.rb = p->P.eps_b / p->P.eps; a.rt = p->P.eps_t / p->P.eps; a.H = p->P.H;
     p->ktic(1);
-    bvp_kernel<<<(unsigned)((2 * v.M + 63) / 64), 64, 0, p->stream>>>(a);
+    const size_t wsmem = bvpw_smem(p->Nz);
+    if (v.Mv <= BVPW_MAX_MODES && wsmem <= 200 * 1024) {
+        SE_CUDA(cudaFuncSetAttribute(bvp_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)wsmem));
+        bvp_warp_kernel<<<(unsigned)((v.Mv + BVPW_MODES - 1) / BVPW_MODES), 64 * BVPW_MODES,
+                          wsmem, p->stream>>>(a);
+    } else {
+        bvp_kernel<<<(unsigned)((2 * v.M + 63) / 64), 64, 0, p->stream>>>(a);
+    }
     p->ktoc(1);
     SE_LAUNCHED(p);
 }
