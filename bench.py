@@ -340,9 +340,13 @@ def run_ours(args):
         phi_d = torch.empty(n, dtype=torch.float64, device="cuda")
         E_d = torch.empty((n, 3), dtype=torch.float64, device="cuda")
 
+        # repeated solves on the same device buffers replay the solve as one
+        # CUDA graph (SE_GRAPH; captured on the second call); the per-kernel
+        # breakdown steps run eagerly with the event timers
         def step(timings=False):
             return solver.solve_device(pos_d.data_ptr(), phi_d.data_ptr(),
-                                       E_d.data_ptr(), n, timings=timings)
+                                       E_d.data_ptr(), n, timings=timings,
+                                       graph=not timings)
 
     for _ in range(args.warmup):
         step()
@@ -467,6 +471,9 @@ def run_ours(args):
                     "ms_per_step": e2e_ms, "h2d_bytes_per_step": 24 * n,
                     "d2h_bytes_per_step": 32 * n + 8},
             "gpu_launches": launches,
+            "execution": ("repeated solves on the same device buffers replayed as one "
+                          "CUDA graph; near-field cell list + pair scan forked onto a "
+                          "high-priority side stream" if not sharded else "eager"),
             "kernel_ms": stage, "near_pairs": pairs,
             "roofline": roof, "stage_roofline": stages, "clocks": clk}
     if world == 1 and not sharded:
@@ -478,14 +485,16 @@ def run_ours(args):
         s32 = SlabSolver(system, params, device=local, precision="fp32")
         s32.set_stream(stream.cuda_stream)
         for _ in range(args.warmup):
-            s32.solve_device(pos_d.data_ptr(), phi_d.data_ptr(), E_d.data_ptr(), n)
+            s32.solve_device(pos_d.data_ptr(), phi_d.data_ptr(), E_d.data_ptr(), n,
+                             graph=True)
         t32 = []
         for _ in range(args.steps):
             flush.zero_()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            s32.solve_device(pos_d.data_ptr(), phi_d.data_ptr(), E_d.data_ptr(), n)
+            s32.solve_device(pos_d.data_ptr(), phi_d.data_ptr(), E_d.data_ptr(), n,
+                             graph=True)
             e1.record(stream)
             e1.synchronize()
             t32.append(e0.elapsed_time(e1))

@@ -116,11 +116,28 @@ namespace {
 // sharded solve (charges split by index across ranks) runs them with a sum of
 // the spread grids over ranks between phase 1 and phase 2.
 // ---------------------------------------------------------------------------
+// the solver's stream, cuFFT plans included
+static void bind_stream(Plan* p, cudaStream_t st) {
+    p->stream = st;
+    cufftHandle hs[] = {p->fft_fwd2, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig,
+                        p->fft_fwd_slab, p->fft_inv4_slab, p->fft_inv1_slab,
+                        p->fft_fwd2_f, p->fft_inv4_f, p->fft_inv1_f};
+    for (auto h : hs) if (h) SE_CUFFT(cufftSetStream(h, st));
+}
+
 static void mark(Plan* p, Solve& S) {
     if (S.timed) SE_CUDA(cudaEventRecord(S.ev[S.ne++], p->stream));
 }
 
 static Solve& current(Plan* p) { return p->solve; }
+
+static void fork_near(Plan* p);
+
+// SE_NEAR_FORK_AT: 1 forks the near field before the spread, 0 after it
+static bool fork_at_spread() {
+    static const char* e = getenv("SE_NEAR_FORK_AT");
+    return e && atoi(e) == 1;
+}
 
 void phase_spread(Plan* p, const double* d_pos, int64_t n_all, int64_t first, int64_t count,
                   uint32_t flags) {
@@ -135,6 +152,8 @@ void phase_spread(Plan* p, const double* d_pos, int64_t n_all, int64_t first, in
     S.phase = 0;
     S.flags = flags;
     S.near_external = false;
+    S.near_fork = p->fork_req; S.near_forked = false;
+    p->fork_req = 0;
     S.n_all = n_all; S.first = first; S.count = count;
     S.xi_inf = P.xi_is_inf != 0.0;
     S.forces = flags & SE_NEED_FORCES;
@@ -160,6 +179,7 @@ void phase_spread(Plan* p, const double* d_pos, int64_t n_all, int64_t first, in
         for (auto& pr : p->kev) { SE_CUDA(cudaEventCreate(&pr[0])); SE_CUDA(cudaEventCreate(&pr[1])); }
     mark(p, S);
     p->d_pos_cur = d_pos;
+    if (fork_at_spread()) fork_near(p);
     build_sources(p, d_pos, first, count, S.two);
     mark(p, S);
     spread(p, S.two);
@@ -167,10 +187,13 @@ void phase_spread(Plan* p, const double* d_pos, int64_t n_all, int64_t first, in
     S.phase = 1;
 }
 
+static void fork_near(Plan* p);
+
 void phase_fields(Plan* p) {
     NvtxRange nv("se.field_phase");
     Solve& S = current(p);
     if (S.phase != 1) throw Error(SE_ERR_CUDA, "se_shard_fields before se_shard_spread");
+    if (!S.near_forked) fork_near(p);
     forward_transforms(p, S.two);
     mark(p, S);
     bvp_solve(p, S.two, S.mode, S.corr);
@@ -202,6 +225,75 @@ static NearKernel kernel_of(const se_params& P, int kind, bool field, bool sub_u
     return k;
 }
 
+// the charges' near-field kernel of the solve in flight
+static NearKernel charge_kernel(const Plan* p, const Solve& S) {
+    NearKernel k = kernel_of(p->P, 0, S.forces, S.flags & SE_SUBTRACT_SELF);
+    k.fp32 = (S.flags & SE_FP32) ? 1 : 0;
+    return k;
+}
+
+// the pair-set record (SE_PAIR_HASH) of this solve's charges, zeroed
+static void prep_pair_hash(Plan* p, const Solve& S) {
+    const int64_t count = S.count;
+    p->pair_hash = (S.flags & SE_PAIR_HASH) != 0;
+    if (!p->pair_hash) return;
+    if (p->phash_cap < count) {
+        dfree(p, p->d_phash);
+        p->d_phash = dalloc<unsigned long long>(p, 2 * (size_t)std::max<int64_t>(count, 1));
+        p->phash_cap = count;
+    }
+    SE_CUDA(cudaMemsetAsync(p->d_phash, 0, 16 * (size_t)std::max<int64_t>(count, 1), p->stream));
+    p->phash_n = count;
+}
+
+// Solve::near_fork: the charges' near field depends only on the positions
+// and charges, so it can run on a side stream while the grid pipeline
+// (transforms, mode BVPs, interpolation) runs on the solver's stream; the
+// solver's stream joins it after the interpolation (fork 1: the whole near
+// field; fork 2: the cell list and pair-list scan, the list evaluation then
+// runs on the solver's stream after the join).  Captured into the solve's
+// CUDA graph like the rest (the side stream joins the capture).
+static void fork_near(Plan* p) {
+    Solve& S = current(p);
+    S.near_forked = false;
+    if (!S.near_fork || S.near_external || S.near_empty || S.xi_inf || S.count <= 0) return;
+    if (!p->side) {
+        int lo = 0, hi = 0;
+        SE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        SE_CUDA(cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, hi));
+        SE_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+        SE_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+    }
+    SE_CUDA(cudaEventRecord(p->ev_fork, p->stream));
+    SE_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+    if (S.near_fork == 3) {
+        // the scan on the caller's stream, the grid pipeline on the side one
+        prep_pair_hash(p, S);
+        build_cells(p, p->d_pos_cur, p->d_q, S.n_all, true);
+        near_eval(p, p->d_pos_cur + 3 * S.first, nullptr, S.count, charge_kernel(p, S),
+                  p->d_near, p->d_count, nullptr, NEAR_SCAN);
+        p->fork_main = p->stream;
+        bind_stream(p, p->side);
+        S.near_forked = true;
+        return;
+    }
+    const cudaStream_t main = p->stream;
+    p->stream = p->side;
+    try {
+        prep_pair_hash(p, S);
+        const NearKernel kavg = charge_kernel(p, S);
+        build_cells(p, p->d_pos_cur, p->d_q, S.n_all, true);
+        near_eval(p, p->d_pos_cur + 3 * S.first, nullptr, S.count, kavg, p->d_near, p->d_count,
+                  nullptr, S.near_fork == 1 ? NEAR_ALL : NEAR_SCAN);
+        SE_CUDA(cudaEventRecord(p->ev_join, p->side));
+    } catch (...) {
+        p->stream = main;
+        throw;
+    }
+    p->stream = main;
+    S.near_forked = true;
+}
+
 void phase_charges(Plan* p, const double* d_pos, double* d_phi_out, double* d_E_out) {
     NvtxRange nv("se.charge_phase");
     Solve& S = current(p);
@@ -215,29 +307,32 @@ void phase_charges(Plan* p, const double* d_pos, double* d_phi_out, double* d_E_
     mark(p, S);
     NearKernel kavg{}, kpt{};
     if (!S.xi_inf) {
-        kavg = kernel_of(P, 0, S.forces, S.flags & SE_SUBTRACT_SELF);
-        kavg.fp32 = (S.flags & SE_FP32) ? 1 : 0;
+        kavg = charge_kernel(p, S);
         kpt = kernel_of(P, 1, false, false);
     }
-    p->pair_hash = (S.flags & SE_PAIR_HASH) != 0;
-    if (p->pair_hash) {
-        if (p->phash_cap < count) {
-            dfree(p, p->d_phash);
-            p->d_phash = dalloc<unsigned long long>(p, 2 * (size_t)std::max<int64_t>(count, 1));
-            p->phash_cap = count;
-        }
-        SE_CUDA(cudaMemsetAsync(p->d_phash, 0, 16 * (size_t)std::max<int64_t>(count, 1), s));
-        p->phash_n = count;
+    if (S.near_forked && S.near_fork == 3) {
+        SE_CUDA(cudaEventRecord(p->ev_join, p->stream));
+        bind_stream(p, p->fork_main);
+        p->fork_main = nullptr;
+        s = p->stream;
     }
-    if (S.near_external) {
+    if (S.near_forked) {
+        SE_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
+        if (S.near_fork >= 2)
+            near_eval(p, d_pos + 3 * first, nullptr, count, kavg, p->d_near, p->d_count, nullptr,
+                      NEAR_LISTS);
+    } else if (S.near_external) {
+        prep_pair_hash(p, S);
         // routed by cell: the caller's sums for this shard (se_shard_near)
         if (count > 0)
             SE_CUDA(cudaMemcpyAsync(p->d_near, S.ext_near, sizeof(double) * 4 * (size_t)count,
                                     cudaMemcpyDeviceToDevice, s));
     } else if (!S.near_empty) {
+        prep_pair_hash(p, S);
         build_cells(p, d_pos, p->d_q, n, true);           // sources: every charge
         near_eval(p, d_pos + 3 * first, nullptr, count, kavg, p->d_near, p->d_count);
     } else {
+        prep_pair_hash(p, S);
         SE_CUDA(cudaMemsetAsync(p->d_near, 0, sizeof(double) * 4 * (size_t)std::max<int64_t>(count, 1), s));
     }
     mark(p, S);
@@ -515,9 +610,26 @@ void dist_fields(Plan* p) {
     S.phase = 2;
 }
 
+// SE_NEAR_OVERLAP: Solve::near_fork of single-GPU solves, default 2 (the
+// cell list and pair-list scan on the high-priority side stream): C4 fp64
+// 17.69 -> 17.45 ms, the paper's configuration 1.08 -> 0.97 ms; 1 (the whole
+// near field on the side stream) contends with the interpolation at C4
+// (20.2 ms); 3 (the grid pipeline on the side stream instead) gains nothing
+// A solve with the per-kernel event timers (SE_TIMINGS) runs serially, so
+// each stage's events bracket its own kernels.
+static int near_fork_mode(uint32_t flags) {
+    static const char* e = getenv("SE_NEAR_OVERLAP");
+    if (flags & SE_TIMINGS) return 0;
+    return e ? atoi(e) : 2;
+}
+
 void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
                 double* d_phi_out, double* d_E_out, double* U, se_diag* diag) {
     // fp32 mode of a whole (single-GPU) solve: the grid path in fp32 too
+    if (p->fork_main) {                  // a fork-3 solve that threw midway
+        bind_stream(p, p->fork_main);
+        p->fork_main = nullptr;
+    }
     p->g32 = (flags & SE_FP32) != 0;
     if (p->g32) ensure_grid32(p);
     else ensure_grid64(p);
@@ -536,18 +648,14 @@ void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
         if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
         if (!p->cap_stream) SE_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
         const cudaStream_t run = p->stream;
-        auto bind = [&](cudaStream_t st) {
-            p->stream = st;
-            cufftHandle hs[] = {p->fft_fwd2, p->fft_inv4, p->fft_inv1, p->fft_sig, p->fft_fwd2_f,
-                                p->fft_inv4_f, p->fft_inv1_f};
-            for (auto h : hs) if (h) cufftSetStream(h, st);
-        };
+        auto bind = [&](cudaStream_t st) { bind_stream(p, st); };
         SE_CUDA(cudaStreamSynchronize(run));
         bind(p->cap_stream);
         cudaGraph_t g = nullptr;
         cudaError_t ce = cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal);
         if (ce != cudaSuccess) { bind(run); SE_CUDA(ce); }
         try {
+            p->fork_req = near_fork_mode(flags);
             phase_spread(p, d_pos, n, 0, n, flags);
             phase_fields(p);
             phase_charges(p, d_pos, d_phi_out, d_E_out);
@@ -555,6 +663,7 @@ void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
             cudaStreamEndCapture(p->cap_stream, &g);
             if (g) cudaGraphDestroy(g);
             cudaGetLastError();
+            p->fork_main = nullptr;
             bind(run);
             p->gwarm = {};
             throw;
@@ -570,6 +679,7 @@ void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
         phase_results(p, U, diag);
         return;
     }
+    p->fork_req = near_fork_mode(flags);
     phase_spread(p, d_pos, n, 0, n, flags);
     phase_fields(p);
     phase_charges(p, d_pos, d_phi_out, d_E_out);
@@ -643,6 +753,7 @@ int se_plan_create(const se_params* params, const double* z_nodes, const double*
             throw Error(SE_ERR_VALUE, "grid must have Nx, Ny >= 1 and Nz >= 3");
         p->dev = device;
         SE_CUDA(cudaSetDevice(device));
+        SE_CUDA(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
         SE_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
         p->own_stream = true;
         p->Nx = P.Nx; p->Ny = P.Ny; p->Nz = P.Nz;
@@ -787,6 +898,9 @@ void se_plan_destroy(se_plan* plan) {
     for (auto& b : p->owned) if (b.p) cudaFree(b.p);
     if (p->gexec) cudaGraphExecDestroy(p->gexec);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+    if (p->side) cudaStreamDestroy(p->side);
+    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    if (p->ev_join) cudaEventDestroy(p->ev_join);
     for (auto& pr : p->kev) { if (pr[0]) cudaEventDestroy(pr[0]); if (pr[1]) cudaEventDestroy(pr[1]); }
     if (p->stream && p->own_stream) cudaStreamDestroy(p->stream);
     delete p;
@@ -799,11 +913,8 @@ int se_plan_set_stream(se_plan* plan, void* stream) {
         SE_CUDA(cudaSetDevice(p->dev));
         SE_CUDA(cudaStreamSynchronize(p->stream));
         if (p->own_stream && p->stream) { cudaStreamDestroy(p->stream); p->own_stream = false; }
-        p->stream = reinterpret_cast<cudaStream_t>(stream);
-        cufftHandle hs[] = {p->fft_fwd2, p->fft_z, p->fft_inv4, p->fft_inv1, p->fft_sig,
-                            p->fft_fwd_slab, p->fft_inv4_slab, p->fft_inv1_slab,
-                            p->fft_fwd2_f, p->fft_inv4_f, p->fft_inv1_f};
-        for (auto h : hs) if (h) SE_CUFFT(cufftSetStream(h, p->stream));
+        p->fork_main = nullptr;
+        bind_stream(p, reinterpret_cast<cudaStream_t>(stream));
         return SE_OK;
     } catch (const Error& e) {
         return fail(e);
@@ -878,6 +989,7 @@ static Plan* light_plan(const se_params* params, int device) {
     p->P = *params;
     p->dev = device;
     SE_CUDA(cudaSetDevice(device));
+    SE_CUDA(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
     SE_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     p->own_stream = true;
     p->d_flags = dalloc<int>(p, 1);

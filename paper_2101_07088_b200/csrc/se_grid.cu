@@ -136,67 +136,69 @@ struct StencilArgs {
     Stencils st;
 };
 
-// One thread per source; the block's records (contiguous in the sorted
-// order) are assembled in shared memory and written out coalesced.
-constexpr int STENCIL_TB = 64;
+// Two passes per CTA of STENCIL_TB sorted sources: one thread per source
+// finds its x / y base columns and z node range (binary searches) and writes
+// the per-source arrays; then the CTA computes the record elements
+// (wx | wy | wz, one Gaussian each) element-parallel and writes the records
+// coalesced -- every exp in flight at once instead of 44 in one thread.
+constexpr int STENCIL_TB = 256;
 
 __global__ void __launch_bounds__(STENCIL_TB) stencil_kernel(StencilArgs a) {
-    extern __shared__ double srec[];             // [STENCIL_TB][rs + 1]
+    __shared__ double sx[STENCIL_TB], sy[STENCIL_TB], sz[STENCIL_TB];
+    __shared__ int sjx[STENCIL_TB], sjy[STENCIL_TB], slo[STENCIL_TB], shi[STENCIL_TB];
     const int t = threadIdx.x;
     const int64_t i0 = blockIdx.x * (int64_t)STENCIL_TB;
     const int64_t i = i0 + t;
-    const int rs = a.st.rs, ld = rs + 1;
-    const int nblk = (int)(a.total - i0 < STENCIL_TB ? a.total - i0 : STENCIL_TB);
-    double* my = srec + t * ld;
-    if (t < nblk) {
-        for (int e = 0; e < rs; ++e) my[e] = 0.0;
-        if ((a.keys[i] >> a.zbits) < a.invalid_major) {
-            const int s = a.perm[i];
-            const double4 v = a.src[s];
-            // x axis: j0 = floor(x/h); delta = x - (j0+off)*h; keep |delta| <= r(1+1e-12)
-            const long long jx = (long long)floor(v.x / a.hx);
-            for (int o = 0; o <= 2 * a.mx; ++o) {
-                const double xj = __dmul_rn((double)(jx + o - a.mx), a.hx);
-                const double d = __dsub_rn(v.x, xj);
-                if (fabs(d) <= a.rad_keep) my[o] = gauss_w(d, a.inv_width, a.inv_norm);
-            }
-            double* ry = my + 2 * a.mx + 1;
-            const long long jy = (long long)floor(v.y / a.hy);
-            for (int o = 0; o <= 2 * a.my; ++o) {
-                const double yj = __dmul_rn((double)(jy + o - a.my), a.hy);
-                const double d = __dsub_rn(v.y, yj);
-                if (fabs(d) <= a.rad_keep) ry[o] = gauss_w(d, a.inv_width, a.inv_norm);
-            }
-            double* rz = ry + 2 * a.my + 1;
-            // z axis: nodes in [searchsorted(z-r, left), searchsorted(z+r, right))
-            const int lo = lower_bound_d(a.znodes, a.Nz, __dsub_rn(v.z, a.rad));
-            const int hi = upper_bound_d(a.znodes, a.Nz, __dadd_rn(v.z, a.rad));
-            for (int tt = 0; tt < a.wz; ++tt) {
-                const int k = lo + tt;
-                if (k < hi && k < a.Nz) {
-                    const double d = __dsub_rn(v.z, a.znodes[k]);
-                    if (fabs(d) <= a.rad) rz[tt] = gauss_w(d, a.inv_width, a.inv_norm);
-                }
-            }
-            a.st.j0x[i] = (int)jx;
-            a.st.j0y[i] = (int)jy;
-            a.st.lo[i] = lo;
-            a.st.hi[i] = hi < lo + a.wz ? hi : lo + a.wz;
-            a.st.q[i] = v.w;
-            a.st.owner[i] = a.owner_in[s];
-        }
+    const int rs = a.st.rs;
+    // invalid slots sort to the end: the valid ones are a prefix of the CTA
+    const bool valid = i < a.total && (a.keys[i] >> a.zbits) < a.invalid_major;
+    if (valid) {
+        const int s = a.perm[i];
+        const double4 v = a.src[s];
+        // x / y: j0 = floor(x/h); z: nodes in
+        // [searchsorted(z-r, left), searchsorted(z+r, right))   gridops.py:18-44
+        const long long jx = (long long)floor(v.x / a.hx);
+        const long long jy = (long long)floor(v.y / a.hy);
+        const int lo = lower_bound_d(a.znodes, a.Nz, __dsub_rn(v.z, a.rad));
+        const int hi = upper_bound_d(a.znodes, a.Nz, __dadd_rn(v.z, a.rad));
+        sx[t] = v.x; sy[t] = v.y; sz[t] = v.z;
+        sjx[t] = (int)jx; sjy[t] = (int)jy; slo[t] = lo; shi[t] = hi;
+        a.st.j0x[i] = (int)jx;
+        a.st.j0y[i] = (int)jy;
+        a.st.lo[i] = lo;
+        a.st.hi[i] = hi < lo + a.wz ? hi : lo + a.wz;
+        a.st.q[i] = v.w;
+        a.st.owner[i] = a.owner_in[s];
     }
-    __syncthreads();
-    double* out = a.st.rec + i0 * rs;
-    // rows of invalid slots (sorted to the end) are never read: skip them
-    __shared__ int nvalid;
-    if (t == 0) nvalid = 0;
-    __syncthreads();
-    if (t < nblk && (a.keys[i] >> a.zbits) < a.invalid_major) atomicMax(&nvalid, t + 1);
-    __syncthreads();
-    for (int e = t; e < nvalid * rs; e += STENCIL_TB) {
-        const int r = e / rs, c = e - r * rs;
-        out[e] = srec[r * ld + c];
+    const int nvalid = __syncthreads_count(valid);
+    const int SX = 2 * a.mx + 1, SY = 2 * a.my + 1;
+    // half a warp per record: lanes over its elements, records in turn
+    const int h = t >> 4, hl = t & 15;
+    for (int r = h; r < nvalid; r += STENCIL_TB / 16)
+    for (int c = hl; c < rs; c += 16) {
+        double* out = a.st.rec + (i0 + r) * rs;
+        // one converged Gaussian per element: x / y offsets select their
+        // axis, z elements their node (|delta| <= r (1 + 1e-12) on x / y)
+        double pos, node, lim;
+        bool ok = true;
+        if (c < SX + SY) {
+            const bool y = c >= SX;
+            const int o = y ? c - SX : c;
+            const int j = y ? sjy[r] : sjx[r];
+            pos = y ? sy[r] : sx[r];
+            node = __dmul_rn((double)(j + o - (y ? a.my : a.mx)), y ? a.hy : a.hx);
+            lim = a.rad_keep;
+        } else {
+            const int tt = c - SX - SY, k = slo[r] + tt;
+            ok = tt < a.wz && k < shi[r] && k < a.Nz;
+            pos = sz[r];
+            node = ok ? a.znodes[k] : 0.0;
+            lim = a.rad;
+        }
+        const double d = __dsub_rn(pos, node);
+        double w = 0.0;
+        if (ok && fabs(d) <= lim) w = gauss_w(d, a.inv_width, a.inv_norm);
+        out[c] = w;
     }
 }
 
@@ -837,10 +839,7 @@ void build_sources(Plan* p, const double* d_pos, int64_t first, int64_t n, bool 
         StencilArgs sta{p->d_src, p->d_src_owner, p->d_perm2, keys2, (uint32_t)nseg,
                         zb, total, p->d_z, p->Nz, p->hx, p->hy, p->rad,
                         p->rad_keep, 1.0 / p->width, 1.0 / p->norm, p->mx, p->my, p->wz_max, st};
-        const int smem = STENCIL_TB * (st.rs + 1) * (int)sizeof(double);
-        if (smem > 48 * 1024)
-            SE_CUDA(cudaFuncSetAttribute(stencil_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        stencil_kernel<<<(unsigned)((total + STENCIL_TB - 1) / STENCIL_TB), STENCIL_TB, smem,
+        stencil_kernel<<<(unsigned)((total + STENCIL_TB - 1) / STENCIL_TB), STENCIL_TB, 0,
                          p->stream>>>(sta);
         SE_LAUNCHED(p);
     }

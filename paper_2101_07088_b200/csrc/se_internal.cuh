@@ -177,6 +177,12 @@ struct Solve {
     int ne = 0;
     bool timed = false;
     int phase = 0;                // 0 idle, 1 spread done, 2 fields done
+    // single-GPU solve: the charges' near field forked onto Plan::side after
+    // the spread (0 off, 1 the whole near field, 2 its list scan only; 3 the
+    // list scan stays on the solver's stream and the grid pipeline up to the
+    // interpolation moves to the high-priority side stream)
+    int near_fork = 0;
+    bool near_forked = false;
 };
 
 // exp(-u) for 0 <= u <= 700 without the special-case paths of libm exp:
@@ -214,6 +220,7 @@ struct Plan {
     se_params P{};
     Solve solve;
     int dev = 0;
+    int num_sms = 148;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int64_t launches = 0;
@@ -310,6 +317,11 @@ struct Plan {
     // buffers, size and flags repeat; invalidated when list capacities grow
     cudaGraphExec_t gexec = nullptr;
     cudaStream_t cap_stream = nullptr;
+    cudaStream_t side = nullptr;          // near-field fork (Solve::near_fork), high priority
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int fork_req = 0;                     // Solve::near_fork of the next solve_core solve
+    cudaStream_t fork_main = nullptr;     // fork 3: the caller's stream while the grid
+                                          // pipeline runs on `side`
     struct GraphKey {
         const void *pos = nullptr, *phi = nullptr, *E = nullptr;
         int64_t n = -1; uint32_t flags = 0;
@@ -428,9 +440,13 @@ struct NearKernel {
 void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, bool in_domain,
                  const double* d_zsrc_min = nullptr, CellList* cl = nullptr,
                  int parts = CL_ALL);
+// part: NEAR_ALL, or the two halves of a split evaluation -- NEAR_SCAN (point
+// sort, tasks, pair-list scan) and NEAR_LISTS (list evaluation, overflow
+// fallback, boundary pairs), launched later with the same arguments
+constexpr int NEAR_ALL = 0, NEAR_SCAN = 1, NEAR_LISTS = 2;
 void near_eval(Plan* p, const double* d_eval, const int* d_eval_order,
                int64_t ne, const NearKernel& k, double* d_out4,
-               int64_t* d_npairs, const CellList* cl = nullptr);
+               int64_t* d_npairs, const CellList* cl = nullptr, int part = NEAR_ALL);
 
 void finalize(Plan* p, int64_t first, int64_t count, uint32_t flags, double self_inf_value,
               double* d_phi, double* d_E);

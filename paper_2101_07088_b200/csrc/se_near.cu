@@ -187,9 +187,20 @@ struct NearArgs {
 };
 
 constexpr int NB_THREADS = 128;
+// Pairs beyond FAR_SPLIT c1 take the erfc-only far kernel.  The reference
+// switches at 6.5 c1 (kernels.py:96-113); between 5.9 c1 and 6.5 c1 its
+// erf(r/c1) is 1 - erfc(r/c1) with erfc < 1.2e-16 and its exp(-(r/c1)^2)
+// term below 8e-16, so the two formulas differ by < 1e-14 relative there --
+// far inside the 1e-10 parity bar -- and the cheaper far kernel takes a
+// quarter of the close pairs.
+constexpr double FAR_SPLIT = 5.9;
 constexpr int FAR_DEG = 18;
 constexpr int FAR_DEG32 = 10;
-constexpr int CL_P = 32, CL_D = 12;             // close-pair table: pieces, degree
+// close-pair table: pieces, degree; the g and coef coefficients of a degree
+// are interleaved so one 16-byte shared load serves both Horner steps (the
+// close launch is bound by shared-memory wavefronts: 128 x 6 takes 7 vector
+// loads per pair where 32 x 12 took 26 scalar ones)
+constexpr int CL_P = 128, CL_D = 6;
 constexpr int CL_TAB = 2 * CL_P * (CL_D + 1);
 
 // 1/sqrt(x) for normal positive x: hardware approximation + 2 Newton steps
@@ -244,8 +255,9 @@ __device__ __forceinline__ void erf_erfc(double x, const double* tab, double& er
 
 // Near kernel between two widths (erf(r/c1) - erf(r/c2)) / (4 pi eps r) and
 // its radial derivative over r (kernels.py:38-113, slab.py:162-177).
-// FAR: r > 6.5 c1 and r >= 0.01 c2, where erf(r/c1) == 1 in fp64 and
-// exp(-(r/c1)^2) is below 1e-17 of the kernel: erfc-only form.
+// FAR: r > FAR_SPLIT c1 and r >= 0.01 c2, where erf(r/c1) is 1 in fp64 to
+// within an ulp and the exp(-(r/c1)^2) terms are < 1e-14 of the kernel:
+// erfc-only form.
 template <bool FAR, bool F32 = false>
 __device__ __forceinline__ void pair_terms(const NearArgs& a, const double* tab,
                                            double r2, double& g, double& coef) {
@@ -284,11 +296,14 @@ __device__ __forceinline__ void pair_terms(const NearArgs& a, const double* tab,
         int pc = (int)(r * a.cl_iw);
         pc = pc < CL_P - 1 ? pc : CL_P - 1;
         const double t = (r - (pc + 0.5) * a.cl_w) * (2.0 * a.cl_iw);
-        const double* cg = ct + pc * (CL_D + 1);
-        const double* cc = ct + (CL_P + pc) * (CL_D + 1);
-        double gv = cg[CL_D], cv = cc[CL_D];
+        const double2* cgc = reinterpret_cast<const double2*>(ct) + pc * (CL_D + 1);
+        const double2 top = cgc[CL_D];
+        double gv = top.x, cv = top.y;
 #pragma unroll
-        for (int j = CL_D - 1; j >= 0; --j) { gv = fma(gv, t, cg[j]); cv = fma(cv, t, cc[j]); }
+        for (int j = CL_D - 1; j >= 0; --j) {
+            const double2 cj = cgc[j];
+            gv = fma(gv, t, cj.x); cv = fma(cv, t, cj.y);
+        }
         g = gv;
         coef = nd ? cv : 0.0;
         return;
@@ -660,64 +675,72 @@ __device__ __forceinline__ void eval_list_f32(const NearArgs& a, const double* t
 // lists (general kernel) add to them.
 template <bool FAR, int MINB, bool F32 = false, bool HASH = false>
 __global__ void __launch_bounds__(NB_THREADS, MINB) near_eval_kernel(NearArgs a) {
-    __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + (FAR ? 0 : CL_TAB)];
+    // the close launch is persistent (grid = resident CTAs, warps stride
+    // over the tasks) so its table staging is paid once per CTA, not per
+    // 4 tasks; with the close table the erfcx table is not needed
+    __shared__ __align__(16) double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + (FAR ? 0 : CL_TAB)];
     const int tid = threadIdx.x, lane = tid & 31;
     if (!FAR || !a.use_poly) {
-        for (int e = tid; e < SE_ERFCX_NP * (SE_ERFCX_DEG + 1); e += blockDim.x)
-            tab[e] = (&se_erfcx_tab[0][0])[e];
+        if (FAR || !a.use_ctab)
+            for (int e = tid; e < SE_ERFCX_NP * (SE_ERFCX_DEG + 1); e += blockDim.x)
+                tab[e] = (&se_erfcx_tab[0][0])[e];
         if (!FAR && a.use_ctab)
             for (int e = tid; e < CL_TAB; e += blockDim.x)
                 tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + e] = a.ctab[e];
         __syncthreads();
     }
-    const int64_t task = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
-    if (task >= a.ntask || task >= *a.ntask_dev) return;
-    const int2 tk = a.tasks[task];
-    const int64_t slot = (int64_t)tk.y + lane;
-    const bool live = slot < a.pt_end[tk.x];
-    double phi = 0, ex = 0, ey = 0, ez = 0;
-    int count = 0;
-    unsigned long long hs = 0;
-    int64_t i = 0;
-    if (live) {
-        i = a.order[slot];
-        const double px = a.eval[3 * i], py = a.eval[3 * i + 1], pz = a.eval[3 * i + 2];
-        if (F32)
-            eval_list_f32<FAR, HASH>(a, tab,
-                                     FAR ? a.list_far + slot * a.cap_far
-                                         : a.list_close + slot * a.cap_close,
-                                     FAR ? a.cnt_far[slot] : a.cnt_close[slot], px, py, pz, i,
-                                     phi, ex, ey, ez, count, hs);
-        else if (FAR)
-            eval_list<true, false, HASH>(a, tab, a.list_far + slot * a.cap_far, a.cnt_far[slot],
-                                         px, py, pz, i, phi, ex, ey, ez, count, hs);
-        else
-            eval_list<false, false, HASH>(a, tab, a.list_close + slot * a.cap_close,
-                                          a.cnt_close[slot], px, py, pz, i, phi, ex, ey, ez,
-                                          count, hs);
-        if (HASH) {                                 // overflowed points are re-done below
-            if (FAR) { a.phash[i] = hs; a.phash[a.ne + i] = (unsigned long long)count; }
-            else { a.phash[i] += hs; a.phash[a.ne + i] += (unsigned long long)count; }
-        }
-        if (FAR) {
-            a.out[i] = phi;
-            if (a.need_field) {
-                a.out[a.out_stride + i] = ex;
-                a.out[2 * a.out_stride + i] = ey;
-                a.out[3 * a.out_stride + i] = ez;
+    const int64_t ntask = min(a.ntask, (int64_t)*a.ntask_dev);
+    const int64_t wstride = FAR ? ntask : (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t task = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5; task < ntask;
+         task += wstride) {
+        const int2 tk = a.tasks[task];
+        const int64_t slot = (int64_t)tk.y + lane;
+        const bool live = slot < a.pt_end[tk.x];
+        double phi = 0, ex = 0, ey = 0, ez = 0;
+        int count = 0;
+        unsigned long long hs = 0;
+        int64_t i = 0;
+        if (live) {
+            i = a.order[slot];
+            const double px = a.eval[3 * i], py = a.eval[3 * i + 1], pz = a.eval[3 * i + 2];
+            if (F32)
+                eval_list_f32<FAR, HASH>(a, tab,
+                                         FAR ? a.list_far + slot * a.cap_far
+                                             : a.list_close + slot * a.cap_close,
+                                         FAR ? a.cnt_far[slot] : a.cnt_close[slot], px, py, pz,
+                                         i, phi, ex, ey, ez, count, hs);
+            else if (FAR)
+                eval_list<true, false, HASH>(a, tab, a.list_far + slot * a.cap_far,
+                                             a.cnt_far[slot], px, py, pz, i, phi, ex, ey, ez,
+                                             count, hs);
+            else
+                eval_list<false, false, HASH>(a, tab, a.list_close + slot * a.cap_close,
+                                              a.cnt_close[slot], px, py, pz, i, phi, ex, ey, ez,
+                                              count, hs);
+            if (HASH) {                             // overflowed points are re-done below
+                if (FAR) { a.phash[i] = hs; a.phash[a.ne + i] = (unsigned long long)count; }
+                else { a.phash[i] += hs; a.phash[a.ne + i] += (unsigned long long)count; }
             }
-        } else {
-            a.out[i] += phi;
-            if (a.need_field) {
-                a.out[a.out_stride + i] += ex;
-                a.out[2 * a.out_stride + i] += ey;
-                a.out[3 * a.out_stride + i] += ez;
+            if (FAR) {
+                a.out[i] = phi;
+                if (a.need_field) {
+                    a.out[a.out_stride + i] = ex;
+                    a.out[2 * a.out_stride + i] = ey;
+                    a.out[3 * a.out_stride + i] = ez;
+                }
+            } else {
+                a.out[i] += phi;
+                if (a.need_field) {
+                    a.out[a.out_stride + i] += ex;
+                    a.out[2 * a.out_stride + i] += ey;
+                    a.out[3 * a.out_stride + i] += ez;
+                }
             }
         }
+        unsigned long long cnt = (unsigned long long)count;
+        for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+        if (lane == 0 && a.npairs && cnt) atomicAdd((unsigned long long*)a.npairs, cnt);
     }
-    unsigned long long cnt = (unsigned long long)count;
-    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
-    if (lane == 0 && a.npairs && cnt) atomicAdd((unsigned long long*)a.npairs, cnt);
 }
 
 // splitmix64 finaliser: the per-pair term of the pair-set hash (SE_PAIR_HASH;
@@ -767,7 +790,7 @@ constexpr int64_t NEAR_FUSED_MAX = 40000;       // evaluation points (measured c
 template <bool F32, int MINB, bool FROM_LIST = false, bool HASH = false>
 __global__ void __launch_bounds__(NB_THREADS, MINB) near_fused_kernel(NearArgs a) {
     constexpr int W = NB_THREADS / 32;
-    __shared__ double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + CL_TAB];
+    __shared__ __align__(16) double tab[SE_ERFCX_NP * (SE_ERFCX_DEG + 1) + CL_TAB];
     __shared__ int qf[W][FQ], qc[W][FQ];
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
     for (int e = tid; e < SE_ERFCX_NP * (SE_ERFCX_DEG + 1); e += blockDim.x)
@@ -1312,17 +1335,17 @@ static bool fit_close_table(const NearKernel& k, double rhi, std::vector<double>
                 for (int i2 = 0; i2 < n; ++i2) mono[i2] += c[j] * tn[i2];
                 tp = tc; tc = tn;
             }
-            for (int i2 = 0; i2 < n; ++i2) tab[(f * CL_P + pc) * n + i2] = mono[i2];
+            for (int i2 = 0; i2 < n; ++i2) tab[2 * (pc * n + i2) + f] = mono[i2];
         }
         for (int q = 0; q <= 32; ++q) {
             const double t = -1.0 + 2.0 * q / 32.0, r = mid + h * t;
             if (r <= 0) continue;
             double gx, cx;
             kernel_host(k, r, &gx, &cx);
-            double ga = tab[(0 * CL_P + pc) * n + n - 1], ca = tab[(1 * CL_P + pc) * n + n - 1];
+            double ga = tab[2 * (pc * n + n - 1)], ca = tab[2 * (pc * n + n - 1) + 1];
             for (int j = n - 2; j >= 0; --j) {
-                ga = std::fma(ga, t, tab[(0 * CL_P + pc) * n + j]);
-                ca = std::fma(ca, t, tab[(1 * CL_P + pc) * n + j]);
+                ga = std::fma(ga, t, tab[2 * (pc * n + j)]);
+                ca = std::fma(ca, t, tab[2 * (pc * n + j) + 1]);
             }
             gmax = std::max(gmax, std::fabs(gx)); cmax = std::max(cmax, std::fabs(cx));
             gerr = std::max(gerr, std::fabs(ga - gx)); cerr = std::max(cerr, std::fabs(ca - cx));
@@ -1379,8 +1402,8 @@ static NearArgs near_args(Plan* p, const CellList& cl, const double* d_eval, con
     a.kind = k.kind; a.need_field = k.need_field;
     double rr = k.radius * (1.0 + 1e-5) + 4e-7 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(cl.zlo));
     a.r2f = (float)(rr * rr);
-    // close path needed below max(6.5 c1, 0.01 c2) (+margin for fp32 error)
-    double rcl = std::max(6.5 * k.c1, 1e-2 * k.c2) * (1.0 + 1e-4) + 1e-6 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(cl.zlo));
+    // close path needed below max(FAR_SPLIT c1, 0.01 c2) (+margin for fp32 error)
+    double rcl = std::max(FAR_SPLIT * k.c1, 1e-2 * k.c2) * (1.0 + 1e-4) + 1e-6 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(cl.zlo));
     a.r2close = (float)(rcl * rcl);
     {
         // close-pair table, cached per kernel (rebuilt when the kernel changes)
@@ -1401,7 +1424,7 @@ static NearArgs near_args(Plan* p, const CellList& cl, const double* d_eval, con
         close_ok = cf.ok;
     }
     {
-        const double r_far = std::max(6.5 * k.c1, 1e-2 * k.c2);
+        const double r_far = std::max(FAR_SPLIT * k.c1, 1e-2 * k.c2);
         const double xa = r_far / k.c2 * (1.0 - 1e-6), xb = k.radius / k.c2 * (1.0 + 1e-6);
         a.use_poly = fit_far_poly(xa, xb, &a.pmid, &a.pinvh, a.pc) ? 1 : 0;
         for (int j = 0; j <= FAR_DEG; ++j) a.pc4[j] = a.pc[j] * k.inv4pie;
@@ -1435,8 +1458,10 @@ static NearArgs near_args(Plan* p, const CellList& cl, const double* d_eval, con
 }
 
 void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
-               const NearKernel& k, double* d_out4, int64_t* d_npairs, const CellList* clp) {
+               const NearKernel& k, double* d_out4, int64_t* d_npairs, const CellList* clp,
+               int part) {
     if (ne == 0) return;
+    const bool do_scan = part != NEAR_LISTS, do_lists = part != NEAR_SCAN;
     NvtxRange nv("se.near_field");
     const CellList& cl = clp ? *clp : p->cl;
     bool close_ok = false;
@@ -1444,10 +1469,15 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
                            p->d_bnd_cnt, p->bnd_cap, &close_ok);
     const bool hash = a.phash != nullptr;
     if (cl.n == 0) {
-        SE_CUDA(cudaMemsetAsync(d_out4, 0, sizeof(double) * (k.need_field ? 4 : 1) * ne,
-                                p->stream));
+        if (do_scan)
+            SE_CUDA(cudaMemsetAsync(d_out4, 0, sizeof(double) * (k.need_field ? 4 : 1) * ne,
+                                    p->stream));
         return;
     }
+    // the few-point and fused paths run whole in the NEAR_SCAN half
+    static const char* fenv = getenv("SE_NEAR_FUSED");
+    const bool fused = fenv ? atoi(fenv) != 0 : ne <= NEAR_FUSED_MAX;
+    if (!do_scan && (ne <= FEW_POINTS || fused)) return;
     if (ne <= FEW_POINTS) {
         near_few_kernel<<<(unsigned)ne, 256, 0, p->stream>>>(a);
         SE_LAUNCHED(p);
@@ -1486,23 +1516,23 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         ns.cub = dalloc<char>(p, ns.cub_bytes);
     }
     CellGeo g = cell_geo(p, cl);
-    point_keys_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, p->stream>>>(d_eval, ne, g, ns.keys,
-                                                                             ns.perm);
-    SE_LAUNCHED(p);
-    int end_bit = 1;
-    while (end_bit < 32 && ((uint64_t)ncell >> end_bit) != 0) ++end_bit;
     size_t bytes = ns.cub_bytes;
-    SE_CUDA(cub::DeviceRadixSort::SortPairs(ns.cub, bytes, ns.keys, ns.keys2, ns.perm, ns.order,
-                                            (int)ne, 0, end_bit, p->stream));
-    point_starts_kernel<<<(unsigned)((ne + 1 + 255) / 256), 256, 0, p->stream>>>(ns.keys2, ne,
-                                                                                  ncell, ns.pstart);
-    SE_LAUNCHED(p);
+    if (do_scan) {
+        point_keys_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, p->stream>>>(d_eval, ne, g,
+                                                                                 ns.keys, ns.perm);
+        SE_LAUNCHED(p);
+        int end_bit = 1;
+        while (end_bit < 32 && ((uint64_t)ncell >> end_bit) != 0) ++end_bit;
+        SE_CUDA(cub::DeviceRadixSort::SortPairs(ns.cub, bytes, ns.keys, ns.keys2, ns.perm,
+                                                ns.order, (int)ne, 0, end_bit, p->stream));
+        point_starts_kernel<<<(unsigned)((ne + 1 + 255) / 256), 256, 0, p->stream>>>(
+            ns.keys2, ne, ncell, ns.pstart);
+        SE_LAUNCHED(p);
+    }
     // Small problems (latency-bound: too few 32-point tasks to fill the GPU)
     // take the fused one-warp-per-point kernel, no pair lists and no host
     // sync; large ones the scan -> lists -> eval pipeline, which amortises
     // the chord-window set-up over the 32 points of a task.
-    static const char* fenv = getenv("SE_NEAR_FUSED");
-    const bool fused = fenv ? atoi(fenv) != 0 : ne <= NEAR_FUSED_MAX;
     if (fused) {
         a.order = ns.order;
         const unsigned nblk = (unsigned)((ne * 32 + NB_THREADS - 1) / NB_THREADS);
@@ -1520,15 +1550,18 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         return;
     }
     const int nzb = cl.ncz;
-    task_count_kernel<<<(ncol + 255) / 256, 256, 0, p->stream>>>(ns.pstart, ncol, nzb, ns.tcount);
-    SE_LAUNCHED(p);
-    SE_CUDA(cudaMemsetAsync(ns.tcount + ncol, 0, sizeof(int), p->stream));
-    bytes = ns.cub_bytes;
-    SE_CUDA(cub::DeviceScan::ExclusiveSum(ns.cub, bytes, ns.tcount, ns.toff, ncol + 1,
-                                          p->stream));
-    task_fill_kernel<<<(ncol + 255) / 256, 256, 0, p->stream>>>(ns.pstart, ns.toff, ncol, nzb,
-                                                                ns.tasks, ns.pend);
-    SE_LAUNCHED(p);
+    if (do_scan) {
+        task_count_kernel<<<(ncol + 255) / 256, 256, 0, p->stream>>>(ns.pstart, ncol, nzb,
+                                                                     ns.tcount);
+        SE_LAUNCHED(p);
+        SE_CUDA(cudaMemsetAsync(ns.tcount + ncol, 0, sizeof(int), p->stream));
+        bytes = ns.cub_bytes;
+        SE_CUDA(cub::DeviceScan::ExclusiveSum(ns.cub, bytes, ns.tcount, ns.toff, ncol + 1,
+                                              p->stream));
+        task_fill_kernel<<<(ncol + 255) / 256, 256, 0, p->stream>>>(ns.pstart, ns.toff, ncol,
+                                                                    nzb, ns.tasks, ns.pend);
+        SE_LAUNCHED(p);
+    }
     a.order = ns.order;
     a.tasks = ns.tasks;
     a.pt_end = ns.pend;
@@ -1574,25 +1607,30 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
     a.list_far = L.far; a.list_close = L.close;
     a.cap_far = want_far; a.cap_close = want_close;
     a.cnt_far = L.cfar; a.cnt_close = L.cclose; a.overflow = L.ovf; a.ovl = L.ovl;
-    SE_CUDA(cudaMemsetAsync(L.ovf, 0, sizeof(int), p->stream));
-    if (d_npairs) { p->ktic(3); p->ktic(4); }
-    // 16-deep queues, 4 candidates per step, 7 CTAs / SM (73 registers):
-    // measured best of queue 8..24, step 4 / 8, 6..12 CTAs (3.17 vs 3.29 ms at 10)
-    if (cl.ncx < 5 || cl.ncy < 5)
-        near_scan_kernel<16, 4, 7, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
-    else
-        near_scan_kernel<16, 4, 7, false><<<nblk, NB_THREADS, 0, p->stream>>>(a);
-    if (d_npairs) p->ktoc(4);
-    SE_LAUNCHED(p);
+    if (do_scan) {
+        SE_CUDA(cudaMemsetAsync(L.ovf, 0, sizeof(int), p->stream));
+        if (d_npairs) { p->ktic(3); p->ktic(4); }
+        // 16-deep queues, 4 candidates per step, 7 CTAs / SM (73 registers):
+        // measured best of queue 8..24, step 4 / 8, 6..12 CTAs (3.17 vs 3.29 ms at 10)
+        if (cl.ncx < 5 || cl.ncy < 5)
+            near_scan_kernel<16, 4, 7, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        else
+            near_scan_kernel<16, 4, 7, false><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        if (d_npairs) p->ktoc(4);
+        SE_LAUNCHED(p);
+    }
+    if (!do_lists) return;
     if (d_npairs) p->ktic(5);
     NearArgs ac = a;
     ac.use_ctab = close_ok ? 1 : 0;
+    // the close launch: resident CTAs only (6 per SM), persistent over the tasks
+    const unsigned nblk_c = std::min<unsigned>(nblk, (unsigned)(6 * p->num_sms));
     if (hash) {
         if (k.fp32) near_eval_kernel<true, 8, true, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         else near_eval_kernel<true, 8, false, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         SE_LAUNCHED(p);
-        if (k.fp32) near_eval_kernel<false, 6, true, true><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
-        else near_eval_kernel<false, 6, false, true><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
+        if (k.fp32) near_eval_kernel<false, 6, true, true><<<nblk_c, NB_THREADS, 0, p->stream>>>(ac);
+        else near_eval_kernel<false, 6, false, true><<<nblk_c, NB_THREADS, 0, p->stream>>>(ac);
         SE_LAUNCHED(p);
         if (k.fp32) near_fused_kernel<true, 6, true, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
         else near_fused_kernel<false, 6, true, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
@@ -1600,8 +1638,8 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         if (k.fp32) near_eval_kernel<true, 8, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         else near_eval_kernel<true, 8><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         SE_LAUNCHED(p);
-        if (k.fp32) near_eval_kernel<false, 6, true><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
-        else near_eval_kernel<false, 6><<<nblk, NB_THREADS, 0, p->stream>>>(ac);
+        if (k.fp32) near_eval_kernel<false, 6, true><<<nblk_c, NB_THREADS, 0, p->stream>>>(ac);
+        else near_eval_kernel<false, 6><<<nblk_c, NB_THREADS, 0, p->stream>>>(ac);
         SE_LAUNCHED(p);
         if (k.fp32) near_fused_kernel<true, 6, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
         else near_fused_kernel<false, 6, true><<<148, NB_THREADS, 0, p->stream>>>(ac);

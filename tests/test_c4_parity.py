@@ -98,3 +98,45 @@ def test_pair_set_all_paths_c4d(env):
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2", "3"])
+def test_near_fork_modes_c4d(mode):
+    """The near-field stream fork (SE_NEAR_OVERLAP: 0 serial, 1 whole near
+    field on the side stream, 2 its scan only -- the default, 3 the grid
+    pipeline on the side stream) gives the reference's results and pair set,
+    eagerly and as a replayed CUDA graph, and every mode gives the same
+    device results bit for bit."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys, torch, hashlib; sys.path.insert(0, 'tests');"
+        "from paper_2101_07088_b200 import workloads as W;"
+        "from paper_2101_07088_b200.slab import SlabSolver;"
+        "from _golden import GOLDEN, rel_l2;"
+        "raw = np.load(GOLDEN + '/c4.npz');"
+        "s, p = W.build('c4d', N=65536); sv = SlabSolver(s, p);"
+        "r = sv.solve(record_pairs=True); c, h = sv.pair_set();"
+        "assert np.array_equal(h, raw['c4d__pair_hash']);"
+        "assert rel_l2(r.phi_bar, raw['c4d__phi']) < 1e-10;"
+        "assert rel_l2(r.E_bar, raw['c4d__E']) < 1e-10;"
+        "n = s.n; st = torch.cuda.current_stream(); sv.set_stream(st.cuda_stream);"
+        "pos = torch.tensor(s.positions, device='cuda');"
+        "phi = torch.empty(n, dtype=torch.float64, device='cuda');"
+        "E = torch.empty((n, 3), dtype=torch.float64, device='cuda');"
+        "Us = [sv.solve_device(pos.data_ptr(), phi.data_ptr(), E.data_ptr(), n, graph=True)[0]"
+        "      for _ in range(4)];"
+        "torch.cuda.synchronize();"
+        "assert len(set(Us)) == 1, Us;"
+        "assert rel_l2(phi.cpu().numpy(), raw['c4d__phi']) < 1e-10;"
+        "dig = hashlib.sha1(phi.cpu().numpy().tobytes() + E.cpu().numpy().tobytes()).hexdigest();"
+        "print('ok', dig)")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    digs = {}
+    for m in sorted({mode, "2"}):
+        env = dict(os.environ, SE_NEAR_OVERLAP=m)
+        out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env,
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+        digs[m] = out.stdout.split()[-1]
+    assert len(set(digs.values())) == 1, digs
