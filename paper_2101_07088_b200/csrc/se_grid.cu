@@ -466,6 +466,7 @@ struct GroupInfo {
     double x[IG_MAX], y[IG_MAX], z[IG_MAX];
     long long jx[IG_MAX], jy[IG_MAX];
     int jxw[IG_MAX], jyw[IG_MAX], lo[IG_MAX], hi[IG_MAX], idx[IG_MAX];
+    double sx[IG_MAX], sy[IG_MAX], sz0[IG_MAX], sz1[IG_MAX];   // k = 0 separable sums
 };
 
 // T = float (fp32 mode): single-precision field loads and FMAs (weights
@@ -481,6 +482,9 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgsT<T
     double* swx = ism + (size_t)warp * IG * (SX + SY + IZC);
     double* swy = swx + IG * SX;
     double* swz = swy + IG * SY;
+    // the inner loop's z weights in the field precision (fp32 mode: fp32)
+    float* swzf = reinterpret_cast<float*>(ism + (size_t)IWARPS * IG * (SX + SY + IZC)) +
+                  (size_t)warp * IG * IZC;
     GroupInfo& gi = ginfo[warp];
     const int2 gr = a.groups[g];
     const int cnt = gr.y;
@@ -502,14 +506,14 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgsT<T
         gi.lo[lane] = lo; gi.hi[lane] = hi; gi.idx[lane] = i;
     }
     __syncwarp();
-    int jxw[IG], jyw[IG];
+    // the group's window; per-charge data stays in shared memory (GroupInfo)
+    // so the column loop holds only its accumulators in registers
     int xmin = 1 << 30, xmax = -1, ymin = 1 << 30, ymax = -1, zlo = 1 << 30, zhi = 0;
 #pragma unroll
     for (int m = 0; m < IG; ++m) {
-        jxw[m] = gi.jxw[m]; jyw[m] = gi.jyw[m];
         if (m < cnt) {
-            xmin = min(xmin, jxw[m]); xmax = max(xmax, jxw[m]);
-            ymin = min(ymin, jyw[m]); ymax = max(ymax, jyw[m]);
+            xmin = min(xmin, gi.jxw[m]); xmax = max(xmax, gi.jxw[m]);
+            ymin = min(ymin, gi.jyw[m]); ymax = max(ymax, gi.jyw[m]);
             zlo = min(zlo, gi.lo[m]); zhi = max(zhi, gi.hi[m]);
         }
     }
@@ -536,10 +540,11 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgsT<T
     }
     __syncwarp();
     // separable sums for the k = 0 linear terms (lane m: charge m)
-    double sx = 0.0, sy = 0.0, sz0 = 0.0, sz1 = 0.0;
     if (lane < IG) {
+        double sx = 0.0, sy = 0.0;
         for (int o = 0; o < SX; ++o) sx += swx[lane * SX + o];
         for (int o = 0; o < SY; ++o) sy += swy[lane * SY + o];
+        gi.sx[lane] = sx; gi.sy[lane] = sy; gi.sz0[lane] = 0.0; gi.sz1[lane] = 0.0;
     }
     T acc[IG][NF];
 #pragma unroll
@@ -561,26 +566,29 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgsT<T
                 wt = wt * a.wcc[k];
             }
             swz[e] = wt;
+            if (sizeof(T) == sizeof(float)) swzf[e] = (float)wt;
         }
         __syncwarp();
         if (lane < IG) {
+            double sz0 = gi.sz0[lane], sz1 = gi.sz1[lane];
             for (int r = 0; r < nz; ++r) {
                 const double w = swz[lane * IZC + r];
                 sz1 += w;
                 sz0 += w * a.znodes[zc + r];
             }
+            gi.sz0[lane] = sz0; gi.sz1[lane] = sz1;
         }
         for (int p = lane; p < Wx * Wy; p += 32) {
             const int ux = p / Wy, uy = p - ux * Wy;
-            double wxy[IG];
+            T wxy[IG];
             bool any = false;
 #pragma unroll
             for (int m = 0; m < IG; ++m) {
-                const int ox = xmin + ux - jxw[m], oy = ymin + uy - jyw[m];
+                const int ox = xmin + ux - gi.jxw[m], oy = ymin + uy - gi.jyw[m];
                 double w = 0.0;
                 if (m < cnt && ox >= 0 && ox < SX && oy >= 0 && oy < SY)
                     w = swx[m * SX + ox] * swy[m * SY + oy];
-                wxy[m] = w;
+                wxy[m] = (T)w;
                 any |= (w != 0.0);
             }
             if (!any) continue;
@@ -595,7 +603,8 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgsT<T
                 for (int c = 0; c < NF; ++c) f[c] = __ldg(F + (int64_t)r * zstride + c * a.NXY);
 #pragma unroll
                 for (int m = 0; m < IG; ++m) {
-                    const T W = (T)(wxy[m] * swz[m * IZC + r]);
+                    const T W = (sizeof(T) == sizeof(float)) ? (T)(wxy[m] * (T)swzf[m * IZC + r])
+                                                             : (T)(wxy[m] * (T)swz[m * IZC + r]);
 #pragma unroll
                     for (int c = 0; c < NF; ++c) acc[m][c] = fma(W, f[c], acc[m][c]);
                 }
@@ -616,10 +625,9 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgsT<T
     // analytic k = 0 terms: sum_nodes W * (A_i z) and W * A_i
     const double A_i = a.scal[0];
     const int src = lane / NF;
-    const double Sx = __shfl_sync(0xffffffffu, sx, src % IG);
-    const double Sy = __shfl_sync(0xffffffffu, sy, src % IG);
-    const double Sz0 = __shfl_sync(0xffffffffu, sz0, src % IG);
-    const double Sz1 = __shfl_sync(0xffffffffu, sz1, src % IG);
+    __syncwarp();
+    const double Sx = gi.sx[src % IG], Sy = gi.sy[src % IG];
+    const double Sz0 = gi.sz0[src % IG], Sz1 = gi.sz1[src % IG];
     if (lane < IG * NF && src < cnt) {
         const int c = lane - src * NF;
         double v = mine;
@@ -968,7 +976,8 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
     if (((uint64_t)nbins << zb) >> 32)
         throw Error(SE_ERR_VALUE, "grid too large for the interpolation sort keys");
     ensure_sources(p, n);               // key / permutation / sort scratch (>= 3n)
-    const int ig = 4;                   // charges per group (measured best of 2, 3, 4, 8)
+    const int ig = 4;                   // charges per group (measured best of 2, 3, 4, 8;
+                                        // fp32 mode 8: 4.39 vs 3.62 ms)
     const int64_t gcap = count / ig + nbins + 1;
     if (nbins + 1 > p->iseg_cap || gcap > p->igroup_cap) {
         dfree(p, p->d_iseg); dfree(p, p->d_igroups); dfree(p, p->d_ingroups);
@@ -1016,16 +1025,23 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
                            p->d_igroups, p->d_ingroups, p->Nx, p->Ny, p->Nz, p->NXY, p->hx,
                            p->hy, p->rad, p->rad_keep, 1.0 / p->width, 1.0 / p->norm, p->mx,
                            p->my, p->d_far, n};
-    const int smem = IWARPS * ig * (2 * p->mx + 1 + 2 * p->my + 1 + IZC) * (int)sizeof(double);
+    // per warp: x / y / z weight tables in fp64 and (fp32 mode) the z table
+    // again in fp32 for the inner loop
+    const int smem = IWARPS * ig * ((2 * p->mx + 1 + 2 * p->my + 1 + IZC) * (int)sizeof(double) +
+                                    IZC * (int)sizeof(float));
     if (smem > 200 * 1024) throw Error(SE_ERR_VALUE, "stencil too wide for the interpolation");
     const unsigned blocks = (unsigned)((gcap + IWARPS - 1) / IWARPS);
     auto go = [&](auto kern, const auto& args) {
         SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         kern<<<blocks, IWARPS * 32, smem, p->stream>>>(args);
     };
+    // fp32 mode: 3 CTAs / SM (80 registers, no spills; the per-charge data
+    // lives in shared memory): 2.99 vs 3.62 ms at 2 CTAs.  fp64 stays at 2
+    // CTAs / SM (120 registers): capped at 80 it spills (4.28-4.38 vs
+    // 4.02 ms), and 3-charge groups fit but load more (4.77 ms)
     if (p->g32) {
-        if (forces) go(interp_kernel<4, 4, 1, 2, float>, a32);
-        else go(interp_kernel<1, 4, 1, 2, float>, a32);
+        if (forces) go(interp_kernel<4, 4, 3, 2, float>, a32);
+        else go(interp_kernel<1, 4, 3, 2, float>, a32);
     } else if (forces) {
         go(interp_kernel<4, 4, 1, 2>, a);
     } else {
