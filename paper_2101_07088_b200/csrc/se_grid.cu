@@ -471,19 +471,20 @@ struct GroupInfo {
 
 // T = float (fp32 mode): single-precision field loads and FMAs (weights
 // rounded to fp32), the k = 0 terms and the final sums in fp64
-template <int NF, int IG, int MINB, int UNR, typename T = double>
-__global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgsT<T> a) {
+template <int NF, int IG, int MINB, int UNR, typename T = double, int IW = IWARPS,
+          bool ZC = false>
+__global__ void __launch_bounds__(IW * 32, MINB) interp_kernel(InterpArgsT<T> a) {
     extern __shared__ __align__(16) double ism[];
-    __shared__ GroupInfo ginfo[IWARPS];
+    __shared__ GroupInfo ginfo[IW];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = blockIdx.x * IWARPS + warp;
+    const int g = blockIdx.x * IW + warp;
     if (g >= *a.ngroups) return;
     const int SX = 2 * a.mx + 1, SY = 2 * a.my + 1;
     double* swx = ism + (size_t)warp * IG * (SX + SY + IZC);
     double* swy = swx + IG * SX;
     double* swz = swy + IG * SY;
     // the inner loop's z weights in the field precision (fp32 mode: fp32)
-    float* swzf = reinterpret_cast<float*>(ism + (size_t)IWARPS * IG * (SX + SY + IZC)) +
+    float* swzf = reinterpret_cast<float*>(ism + (size_t)IW * IG * (SX + SY + IZC)) +
                   (size_t)warp * IG * IZC;
     GroupInfo& gi = ginfo[warp];
     const int2 gr = a.groups[g];
@@ -596,6 +597,34 @@ __global__ void __launch_bounds__(IWARPS * 32, MINB) interp_kernel(InterpArgsT<T
             gx %= a.Nx; if (gx < 0) gx += a.Nx;
             gy %= a.Ny; if (gy < 0) gy += a.Ny;
             const T* F = a.fields + (int64_t)zc * zstride + (int64_t)gx * a.Ny + gy;
+            if (ZC) {
+                // z contracted first (column partial sums), the xy weight
+                // applied once per column: 16 FMAs per node instead of 4
+                // products + 16 FMAs
+                T t[IG][NF];
+#pragma unroll
+                for (int m = 0; m < IG; ++m)
+#pragma unroll
+                    for (int c = 0; c < NF; ++c) t[m][c] = T(0);
+#pragma unroll UNR
+                for (int r = 0; r < nz; ++r) {
+                    T f[NF];
+#pragma unroll
+                    for (int c = 0; c < NF; ++c) f[c] = __ldg(F + (int64_t)r * zstride + c * a.NXY);
+#pragma unroll
+                    for (int m = 0; m < IG; ++m) {
+                        const T W = (sizeof(T) == sizeof(float)) ? (T)swzf[m * IZC + r]
+                                                                 : (T)swz[m * IZC + r];
+#pragma unroll
+                        for (int c = 0; c < NF; ++c) t[m][c] = fma(W, f[c], t[m][c]);
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < IG; ++m)
+#pragma unroll
+                    for (int c = 0; c < NF; ++c) acc[m][c] = fma(wxy[m], t[m][c], acc[m][c]);
+                continue;
+            }
 #pragma unroll UNR
             for (int r = 0; r < nz; ++r) {
                 T f[NF];
@@ -1030,20 +1059,38 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
     const int smem = IWARPS * ig * ((2 * p->mx + 1 + 2 * p->my + 1 + IZC) * (int)sizeof(double) +
                                     IZC * (int)sizeof(float));
     if (smem > 200 * 1024) throw Error(SE_ERR_VALUE, "stencil too wide for the interpolation");
-    const unsigned blocks = (unsigned)((gcap + IWARPS - 1) / IWARPS);
-    auto go = [&](auto kern, const auto& args) {
-        SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        kern<<<blocks, IWARPS * 32, smem, p->stream>>>(args);
+    auto go = [&](auto kern, const auto& args, int iw = IWARPS) {
+        const unsigned blocks = (unsigned)((gcap + iw - 1) / iw);
+        const int sm = smem / IWARPS * iw;
+        SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        kern<<<blocks, iw * 32, sm, p->stream>>>(args);
     };
     // fp32 mode: 3 CTAs / SM (80 registers, no spills; the per-charge data
     // lives in shared memory): 2.99 vs 3.62 ms at 2 CTAs.  fp64 stays at 2
     // CTAs / SM (120 registers): capped at 80 it spills (4.28-4.38 vs
     // 4.02 ms), and 3-charge groups fit but load more (4.77 ms)
     if (p->g32) {
-        if (forces) go(interp_kernel<4, 4, 3, 2, float>, a32);
+        static const char* xe32 = getenv("SE_INTERP_X32");
+        const int xv32 = xe32 ? atoi(xe32) : 0;
+        if (xv32 == 1) go(interp_kernel<4, 4, 3, 2, float, 8, true>, a32);
+        else if (xv32 == 2) go(interp_kernel<4, 4, 6, 2, float, 4, true>, a32, 4);
+        else if (xv32 == 3) go(interp_kernel<4, 4, 6, 2, float, 4>, a32, 4);
+        else if (forces) go(interp_kernel<4, 4, 3, 2, float>, a32);
         else go(interp_kernel<1, 4, 3, 2, float>, a32);
     } else if (forces) {
-        go(interp_kernel<4, 4, 1, 2>, a);
+        static const char* xe = getenv("SE_INTERP_X");
+        const int xv = xe ? atoi(xe) : 0;
+        if (xv == 1) go(interp_kernel<4, 4, 1, 2, double, 8, true>, a);
+        else if (xv == 2) go(interp_kernel<4, 4, 3, 2, double, 4, true>, a, 4);
+        else if (xv == 3) go(interp_kernel<4, 4, 3, 1, double, 4, true>, a, 4);
+        else if (xv == 4) go(interp_kernel<4, 4, 4, 1, double, 4, true>, a, 4);
+        else if (xv == 51) go(interp_kernel<4, 4, 5, 1, double, 4>, a, 4);
+        else if (xv == 52) go(interp_kernel<4, 4, 5, 2, double, 4>, a, 4);
+        else if (xv == 61) go(interp_kernel<4, 4, 6, 1, double, 4>, a, 4);
+        else if (xv == 62) go(interp_kernel<4, 4, 6, 2, double, 4>, a, 4);
+        else if (xv == 41) go(interp_kernel<4, 4, 4, 1, double, 4>, a, 4);
+        else if (xv == 42) go(interp_kernel<4, 4, 4, 2, double, 4>, a, 4);
+        else go(interp_kernel<4, 4, 1, 2>, a);
     } else {
         go(interp_kernel<1, 4, 1, 2>, a);
     }

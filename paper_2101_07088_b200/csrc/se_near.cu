@@ -155,6 +155,7 @@ struct NearArgs {
     float r2close;                // fp32 bound below which a pair may need the
                                   // general (close) path
     float Lxf, Lyf, iLxf, iLyf;
+    double qLx, qLy;              // L / 4: |d| below it needs no minimum-image shift
     float zmarg;                  // fp32 z-window margin
     // SE_FP32 evaluation: single-precision displacements from the wrapped
     // fp32 coordinates; |r2_f32 - r2| is bounded, so pairs with r2_f32 <=
@@ -601,8 +602,15 @@ __device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, 
         for (int u = 0; u < 4; ++u) {
             if (jj[u] >= 0) {
                 const double4 sv = a.src[jj[u]];
-                const double dx = min_image(__dsub_rn(px, sv.x), Lx);
-                const double dy = min_image(__dsub_rn(py, sv.y), Ly);
+                double dx = __dsub_rn(px, sv.x), dy = __dsub_rn(py, sv.y);
+                // minimum image (min_image): |d| <= L/4 needs no shift, and
+                // pairs across the periodic boundary are rare -- a warp-
+                // uniform branch keeps the shift off the common path
+                const bool wx = fabs(dx) > a.qLx, wy = fabs(dy) > a.qLy;
+                if (__any_sync(__activemask(), wx || wy)) {
+                    if (wx) dx = __dsub_rn(dx, __dmul_rn(Lx, rint(dx * (1.0 / Lx))));
+                    if (wy) dy = __dsub_rn(dy, __dmul_rn(Ly, rint(dy * (1.0 / Ly))));
+                }
                 const double dz = __dsub_rn(pz, sv.z);
                 const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
                                             __dmul_rn(dz, dz));
@@ -1492,6 +1500,7 @@ static NearArgs near_args(Plan* p, const CellList& cl, const double* d_eval, con
         a.hLxf = (float)(0.5 * p->P.Lx); a.hLyf = (float)(0.5 * p->P.Ly);
     }
     a.Lxf = (float)p->P.Lx; a.Lyf = (float)p->P.Ly;
+    a.qLx = 0.25 * p->P.Lx; a.qLy = 0.25 * p->P.Ly;
     a.iLxf = (float)(1.0 / p->P.Lx); a.iLyf = (float)(1.0 / p->P.Ly);
     a.zmarg = (float)(1e-6 * (p->P.Lx + p->P.Ly + p->P.H + std::fabs(cl.zlo)));
     a.out = d_out4; a.out_stride = ne;
