@@ -205,15 +205,19 @@ class SlabSolver:
     def solve(self, positions=None, need_energy=True, need_forces=True,
               need_potential=True, subtract_self=False,
               include_correction=True, force_general=False, timings=False,
-              record_pairs=False):
+              record_pairs=False, graph=True):
         """Averaged potential and field at every charge, and the energy
         (reference slab.py:259-394).  ``record_pairs`` (not in the reference)
-        keeps the near-field pair set for :meth:`pair_set`."""
+        keeps the near-field pair set for :meth:`pair_set`; ``graph`` (not in
+        the reference) replays repeated solves with the same flags as one
+        CUDA graph (the positions are copied into the plan's own device
+        buffer, so every call reuses the captured solve)."""
         pos = self._positions(positions)
         n = pos.shape[0]
         flags = _flags(need_energy, need_forces, need_potential,
                        subtract_self, include_correction, force_general,
-                       timings, self.precision == "fp32", record_pairs)
+                       timings, self.precision == "fp32", record_pairs,
+                       graph=graph)
         phi, E = _host_outputs(n, need_forces)
         U = ctypes.c_double(0.0)
         diag = _lib.SeDiag()
