@@ -471,8 +471,7 @@ struct GroupInfo {
 
 // T = float (fp32 mode): single-precision field loads and FMAs (weights
 // rounded to fp32), the k = 0 terms and the final sums in fp64
-template <int NF, int IG, int MINB, int UNR, typename T = double, int IW = IWARPS,
-          bool ZC = false>
+template <int NF, int IG, int MINB, int UNR, typename T = double, int IW = IWARPS>
 __global__ void __launch_bounds__(IW * 32, MINB) interp_kernel(InterpArgsT<T> a) {
     extern __shared__ __align__(16) double ism[];
     __shared__ GroupInfo ginfo[IW];
@@ -597,34 +596,6 @@ __global__ void __launch_bounds__(IW * 32, MINB) interp_kernel(InterpArgsT<T> a)
             gx %= a.Nx; if (gx < 0) gx += a.Nx;
             gy %= a.Ny; if (gy < 0) gy += a.Ny;
             const T* F = a.fields + (int64_t)zc * zstride + (int64_t)gx * a.Ny + gy;
-            if (ZC) {
-                // z contracted first (column partial sums), the xy weight
-                // applied once per column: 16 FMAs per node instead of 4
-                // products + 16 FMAs
-                T t[IG][NF];
-#pragma unroll
-                for (int m = 0; m < IG; ++m)
-#pragma unroll
-                    for (int c = 0; c < NF; ++c) t[m][c] = T(0);
-#pragma unroll UNR
-                for (int r = 0; r < nz; ++r) {
-                    T f[NF];
-#pragma unroll
-                    for (int c = 0; c < NF; ++c) f[c] = __ldg(F + (int64_t)r * zstride + c * a.NXY);
-#pragma unroll
-                    for (int m = 0; m < IG; ++m) {
-                        const T W = (sizeof(T) == sizeof(float)) ? (T)swzf[m * IZC + r]
-                                                                 : (T)swz[m * IZC + r];
-#pragma unroll
-                        for (int c = 0; c < NF; ++c) t[m][c] = fma(W, f[c], t[m][c]);
-                    }
-                }
-#pragma unroll
-                for (int m = 0; m < IG; ++m)
-#pragma unroll
-                    for (int c = 0; c < NF; ++c) acc[m][c] = fma(wxy[m], t[m][c], acc[m][c]);
-                continue;
-            }
 #pragma unroll UNR
             for (int r = 0; r < nz; ++r) {
                 T f[NF];
@@ -1066,33 +1037,18 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
         kern<<<blocks, iw * 32, sm, p->stream>>>(args);
     };
     // fp32 mode: 3 CTAs / SM (80 registers, no spills; the per-charge data
-    // lives in shared memory): 2.99 vs 3.62 ms at 2 CTAs.  fp64 stays at 2
-    // CTAs / SM (120 registers): capped at 80 it spills (4.28-4.38 vs
-    // 4.02 ms), and 3-charge groups fit but load more (4.77 ms)
+    // lives in shared memory): 2.99 vs 3.62 ms at 2 CTAs.  fp64 keeps 16
+    // warps / SM (120 registers) in 4-warp CTAs (3.93 vs 4.01 ms with
+    // 8-warp CTAs): capped at 80 registers it spills (4.28-4.38 ms), at 96
+    // (20 warps) it runs 4.24 ms, and 3-charge groups fit but load more
+    // (4.77 ms)
     if (p->g32) {
-        static const char* xe32 = getenv("SE_INTERP_X32");
-        const int xv32 = xe32 ? atoi(xe32) : 0;
-        if (xv32 == 1) go(interp_kernel<4, 4, 3, 2, float, 8, true>, a32);
-        else if (xv32 == 2) go(interp_kernel<4, 4, 6, 2, float, 4, true>, a32, 4);
-        else if (xv32 == 3) go(interp_kernel<4, 4, 6, 2, float, 4>, a32, 4);
-        else if (forces) go(interp_kernel<4, 4, 3, 2, float>, a32);
+        if (forces) go(interp_kernel<4, 4, 3, 2, float>, a32);
         else go(interp_kernel<1, 4, 3, 2, float>, a32);
     } else if (forces) {
-        static const char* xe = getenv("SE_INTERP_X");
-        const int xv = xe ? atoi(xe) : 0;
-        if (xv == 1) go(interp_kernel<4, 4, 1, 2, double, 8, true>, a);
-        else if (xv == 2) go(interp_kernel<4, 4, 3, 2, double, 4, true>, a, 4);
-        else if (xv == 3) go(interp_kernel<4, 4, 3, 1, double, 4, true>, a, 4);
-        else if (xv == 4) go(interp_kernel<4, 4, 4, 1, double, 4, true>, a, 4);
-        else if (xv == 51) go(interp_kernel<4, 4, 5, 1, double, 4>, a, 4);
-        else if (xv == 52) go(interp_kernel<4, 4, 5, 2, double, 4>, a, 4);
-        else if (xv == 61) go(interp_kernel<4, 4, 6, 1, double, 4>, a, 4);
-        else if (xv == 62) go(interp_kernel<4, 4, 6, 2, double, 4>, a, 4);
-        else if (xv == 41) go(interp_kernel<4, 4, 4, 1, double, 4>, a, 4);
-        else if (xv == 42) go(interp_kernel<4, 4, 4, 2, double, 4>, a, 4);
-        else go(interp_kernel<4, 4, 1, 2>, a);
+        go(interp_kernel<4, 4, 4, 2, double, 4>, a, 4);
     } else {
-        go(interp_kernel<1, 4, 1, 2>, a);
+        go(interp_kernel<1, 4, 4, 2, double, 4>, a, 4);
     }
     p->ktoc(2);
     SE_LAUNCHED(p);

@@ -1692,6 +1692,8 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         else near_fused_kernel<false, 6, true, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
     } else {
         // fp32 far pairs at 10 CTAs / SM (48 registers): 3.33 vs 3.52 ms at 8
+        // fp64 at 8 CTAs / SM (64 registers): 7 / 9 / 10 measured 4.35 / 4.28 / 4.69
+        // vs 4.27 ms
         if (k.fp32) near_eval_kernel<true, 10, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         else near_eval_kernel<true, 8><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         SE_LAUNCHED(p);
