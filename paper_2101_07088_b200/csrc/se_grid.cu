@@ -275,11 +275,11 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // Rows are per source so the compute loop reads a source's weights with
 // broadcast (vector) loads; the fill maps consecutive threads to consecutive
 // addresses both in shared memory and in the AoS stencil records.
-template <int TZ, int CAP>
+template <int TZ, int CAP, bool ZW = true>
 struct Stage {
     double wx[CAP][TILE];
     double wy[CAP][TILE];
-    double wz[CAP][TZ];
+    double wz[ZW ? CAP : 1][TZ];       // ZW = false: the z weights are read from the records
     double q[CAP];
     int idx[CAP], lo[CAP], ox[CAP], oy[CAP];
     unsigned xm[CAP], zm[CAP];
@@ -289,7 +289,8 @@ struct Stage {
 // Mask of the TILE columns g0.. lying in the periodic stencil j0-m..j0+m;
 // *o0 returns the stencil offset of column g0.
 __device__ __forceinline__ unsigned axis_mask(int j0, int m, int n, int g0, int* o0) {
-    int o = imod(g0 - j0 + m, n);
+    int o = g0 - j0 + m;
+    if ((unsigned)o >= (unsigned)n) o = imod(o, n);
     *o0 = o;
     unsigned mask = 0;
 #pragma unroll
@@ -303,8 +304,8 @@ __device__ __forceinline__ unsigned axis_mask(int j0, int m, int n, int g0, int*
 // One staging round: candidates [cursor, cursor + CAP) are tested against
 // the tile, the touching ones are compacted (warp ballots + block prefix)
 // and their tile-restricted weights staged.  Returns the staged count.
-template <int TZ, int NG, int CAP, bool FOLD_Q>
-__device__ int stage_round(Stage<TZ, CAP>& sm, const TileArgs& A, int cursor,
+template <int TZ, int NG, int CAP, bool FOLD_Q, bool ZW = true>
+__device__ int stage_round(Stage<TZ, CAP, ZW>& sm, const TileArgs& A, int cursor,
                            int total, const int* s_lo, const int* s_len, int nr,
                            int gx0, int gy0, int k0) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -370,6 +371,7 @@ __device__ int stage_round(Stage<TZ, CAP>& sm, const TileArgs& A, int cursor,
             sm.wy[sl][c] = wyv;
         }
     }
+    if (ZW)
     for (int e = threadIdx.x; e < n * TZ; e += blockDim.x) {
         const int sl = e / TZ, r = e % TZ;
         const int k = k0 + r, tt = k - sm.lo[sl];
@@ -882,7 +884,7 @@ template <int TZ, int CAP, int MINB>
 __global__ void __launch_bounds__(4 * TZ, MINB) spread_mma_kernel(SpreadArgs a) {
     constexpr int NG = TZ / 8;
     extern __shared__ __align__(16) unsigned char dsm[];
-    Stage<TZ, CAP>& sm = *reinterpret_cast<Stage<TZ, CAP>*>(dsm);
+    Stage<TZ, CAP, false>& sm = *reinterpret_cast<Stage<TZ, CAP, false>*>(dsm);
     __shared__ int s_lo[MAX_BINS], s_len[MAX_BINS], s_nr, s_total;
 
     const TileArgs& A = a.t;
@@ -891,6 +893,8 @@ __global__ void __launch_bounds__(4 * TZ, MINB) spread_mma_kernel(SpreadArgs a) 
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int zg = warp, kk = lane & 3, rr = lane >> 2;
     const unsigned wzbit = 1u << zg;
+    const int kz = k0 + 8 * zg + rr;                       // this lane's B row (z node)
+    const int zoffr = (2 * A.st.mx + 1) + (2 * A.st.my + 1);   // wz offset in a record
 
     double c[TILE][2];
 #pragma unroll
@@ -900,13 +904,20 @@ __global__ void __launch_bounds__(4 * TZ, MINB) spread_mma_kernel(SpreadArgs a) 
         tile_ranges<TZ>(A, bx, by, k0, cls, s_lo, s_len, &s_nr, &s_total);
         const int total = s_total, nr = s_nr;
         for (int cursor = 0; cursor < total; cursor += CAP) {
-            const int n = stage_round<TZ, NG, CAP, true>(
+            const int n = stage_round<TZ, NG, CAP, true, false>(
                 sm, A, cursor, total, s_lo, s_len, nr, gx0, gy0, k0);
             for (int s0 = 0; s0 < n; s0 += 4) {
                 const int sidx = s0 + kk;
                 const bool ok = sidx < n && (sm.zm[sidx] & wzbit);
                 if (!__any_sync(0xffffffffu, ok)) continue;
-                const double b = ok ? sm.wz[sidx][8 * zg + rr] : 0.0;
+                // B = wz_s(z) straight from the source's record (zeros past
+                // its last node); lanes rr read 8 consecutive doubles
+                double b = 0.0;
+                if (ok) {
+                    const int tt = kz - sm.lo[sidx];
+                    if (tt >= 0 && tt < A.st.wz && kz < A.Nz)
+                        b = __ldg(A.st.rec + (int64_t)sm.idx[sidx] * A.st.rs + zoffr + tt);
+                }
                 const double qwy = ok ? sm.q[sidx] * sm.wy[sidx][rr] : 0.0;
                 const int sl = ok ? sidx : 0;
                 const double2* wx2 = reinterpret_cast<const double2*>(&sm.wx[sl][0]);
@@ -943,7 +954,7 @@ __global__ void __launch_bounds__(4 * TZ, MINB) spread_mma_kernel(SpreadArgs a) 
 template <int TZ, int CAP, int MINB>
 static void launch_spread_mma(Plan* p, const SpreadArgs& a) {
     dim3 grid(p->ss.nbx, p->ss.nby, (p->Nz + TZ - 1) / TZ);
-    const int smem = (int)sizeof(Stage<TZ, CAP>);
+    const int smem = (int)sizeof(Stage<TZ, CAP, false>);
     SE_CUDA(cudaFuncSetAttribute(spread_mma_kernel<TZ, CAP, MINB>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     spread_mma_kernel<TZ, CAP, MINB><<<grid, 4 * TZ, smem, p->stream>>>(a);
@@ -955,11 +966,15 @@ void spread(Plan* p, bool two_grids) {
     NvtxRange nv("se.spread");
     SpreadArgs a{tile_args(p), p->d_rho, two_grids ? 1 : 0, p->g32 ? p->d_rho32 : nullptr};
     // 8x8-column x 16-node tiles, 2 warps (one per 8-node z group), DMMA
-    // accumulation, 64 staged sources per round, 10 CTAs per SM: measured
-    // best among tile heights {16, 32}, rounds {32..256}, scalar lane shapes
-    // and 2..16 CTAs per SM (scalar 2.67 ms -> DMMA 2.08 ms at C4)
+    // accumulation, 64 staged sources per round: measured best among tile
+    // heights {16, 32}, rounds {32..256}, scalar lane shapes and 2..16 CTAs
+    // per SM (scalar 2.67 ms -> DMMA 2.08 ms at C4).  Round 2: the z weights
+    // are read from the records inside the k-steps instead of being staged
+    // (10 KB of shared memory per CTA instead of 18), which lets 18 CTAs
+    // share an SM (56 registers): 2.13 -> 1.94 ms (10 / 12 / 14 / 16 / 20
+    // CTAs: 2.27 / 2.10 / 1.98 / 2.02 / 2.19 ms)
     p->ktic(0);
-    launch_spread_mma<16, 64, 10>(p, a);
+    launch_spread_mma<16, 64, 18>(p, a);
     p->ktoc(0);
     SE_LAUNCHED(p);
 }
