@@ -292,6 +292,19 @@ __device__ __forceinline__ unsigned axis_mask(int j0, int m, int n, int g0, int*
     int o = g0 - j0 + m;
     if ((unsigned)o >= (unsigned)n) o = imod(o, n);
     *o0 = o;
+    const int w = 2 * m + 1;
+    if (w < 32 && n >= w + TILE) {
+        // the stencil covers each column at most once: bits c with
+        // o + c <= 2m, and after the periodic wrap those with o + c - n <= 2m
+        const unsigned full = (1u << w) - 1u;
+        unsigned mask = 0;
+        if (o < w) mask = full >> o;
+        if (o > n - TILE) mask |= full << (n - o);
+        mask &= (1u << TILE) - 1u;
+        const int rem = n - g0;
+        if (rem < TILE) mask &= (1u << rem) - 1u;
+        return mask;
+    }
     unsigned mask = 0;
 #pragma unroll
     for (int c = 0; c < TILE; ++c) {
