@@ -572,8 +572,10 @@ __global__ void __launch_bounds__(IW * 32, MINB) interp_kernel(InterpArgsT<T> a)
         const int nz = min(IZC, zhi - zc);
         __syncwarp();
         // z weights x Clenshaw-Curtis weights (gridops.py:29-39, 128-129)
+        // layout [r][m]: the inner loop reads a node's IG weights with
+        // vector loads
         for (int e = lane; e < IG * IZC; e += 32) {
-            const int m = e / IZC, r = e - m * IZC, k = zc + r;
+            const int r = e / IG, m = e - r * IG, k = zc + r;
             double wt = 0.0;
             if (m < cnt && k >= gi.lo[m] && k < gi.hi[m] && k < a.Nz) {
                 const double d = __dsub_rn(gi.z[m], a.znodes[k]);
@@ -587,7 +589,7 @@ __global__ void __launch_bounds__(IW * 32, MINB) interp_kernel(InterpArgsT<T> a)
         if (lane < IG) {
             double sz0 = gi.sz0[lane], sz1 = gi.sz1[lane];
             for (int r = 0; r < nz; ++r) {
-                const double w = swz[lane * IZC + r];
+                const double w = swz[r * IG + lane];
                 sz1 += w;
                 sz0 += w * a.znodes[zc + r];
             }
@@ -616,10 +618,22 @@ __global__ void __launch_bounds__(IW * 32, MINB) interp_kernel(InterpArgsT<T> a)
                 T f[NF];
 #pragma unroll
                 for (int c = 0; c < NF; ++c) f[c] = __ldg(F + (int64_t)r * zstride + c * a.NXY);
+                T wz[IG];
+                if constexpr (IG == 4 && sizeof(T) == sizeof(float)) {
+                    const float4 v = *reinterpret_cast<const float4*>(swzf + r * IG);
+                    wz[0] = v.x; wz[1] = v.y; wz[2] = v.z; wz[3] = v.w;
+                } else if constexpr (IG == 4) {
+                    const double2 v0 = *reinterpret_cast<const double2*>(swz + r * IG);
+                    const double2 v1 = *reinterpret_cast<const double2*>(swz + r * IG + 2);
+                    wz[0] = (T)v0.x; wz[1] = (T)v0.y; wz[2] = (T)v1.x; wz[3] = (T)v1.y;
+                } else {
+#pragma unroll
+                    for (int m = 0; m < IG; ++m)
+                        wz[m] = (sizeof(T) == sizeof(float)) ? (T)swzf[r * IG + m] : (T)swz[r * IG + m];
+                }
 #pragma unroll
                 for (int m = 0; m < IG; ++m) {
-                    const T W = (sizeof(T) == sizeof(float)) ? (T)(wxy[m] * (T)swzf[m * IZC + r])
-                                                             : (T)(wxy[m] * (T)swz[m * IZC + r]);
+                    const T W = wxy[m] * wz[m];
 #pragma unroll
                     for (int c = 0; c < NF; ++c) acc[m][c] = fma(W, f[c], acc[m][c]);
                 }
