@@ -907,11 +907,11 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
                  : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
 }
 
-template <int TZ, int CAP, int MINB>
+template <int TZ, int CAP, int MINB, bool ZW>
 __global__ void __launch_bounds__(4 * TZ, MINB) spread_mma_kernel(SpreadArgs a) {
     constexpr int NG = TZ / 8;
     extern __shared__ __align__(16) unsigned char dsm[];
-    Stage<TZ, CAP, false>& sm = *reinterpret_cast<Stage<TZ, CAP, false>*>(dsm);
+    Stage<TZ, CAP, ZW>& sm = *reinterpret_cast<Stage<TZ, CAP, ZW>*>(dsm);
     __shared__ int s_lo[MAX_BINS], s_len[MAX_BINS], s_nr, s_total;
 
     const TileArgs& A = a.t;
@@ -931,7 +931,7 @@ __global__ void __launch_bounds__(4 * TZ, MINB) spread_mma_kernel(SpreadArgs a) 
         tile_ranges<TZ>(A, bx, by, k0, cls, s_lo, s_len, &s_nr, &s_total);
         const int total = s_total, nr = s_nr;
         for (int cursor = 0; cursor < total; cursor += CAP) {
-            const int n = stage_round<TZ, NG, CAP, true, false>(
+            const int n = stage_round<TZ, NG, CAP, true, ZW>(
                 sm, A, cursor, total, s_lo, s_len, nr, gx0, gy0, k0);
             for (int s0 = 0; s0 < n; s0 += 4) {
                 const int sidx = s0 + kk;
@@ -940,7 +940,9 @@ __global__ void __launch_bounds__(4 * TZ, MINB) spread_mma_kernel(SpreadArgs a) 
                 // B = wz_s(z) straight from the source's record (zeros past
                 // its last node); lanes rr read 8 consecutive doubles
                 double b = 0.0;
-                if (ok) {
+                if (ZW) {
+                    if (ok) b = sm.wz[sidx][8 * zg + rr];
+                } else if (ok) {
                     const int tt = kz - sm.lo[sidx];
                     if (tt >= 0 && tt < A.st.wz && kz < A.Nz)
                         b = __ldg(A.st.rec + (int64_t)sm.idx[sidx] * A.st.rs + zoffr + tt);
@@ -978,13 +980,13 @@ __global__ void __launch_bounds__(4 * TZ, MINB) spread_mma_kernel(SpreadArgs a) 
     }
 }
 
-template <int TZ, int CAP, int MINB>
+template <int TZ, int CAP, int MINB, bool ZW>
 static void launch_spread_mma(Plan* p, const SpreadArgs& a) {
     dim3 grid(p->ss.nbx, p->ss.nby, (p->Nz + TZ - 1) / TZ);
-    const int smem = (int)sizeof(Stage<TZ, CAP, false>);
-    SE_CUDA(cudaFuncSetAttribute(spread_mma_kernel<TZ, CAP, MINB>,
+    const int smem = (int)sizeof(Stage<TZ, CAP, ZW>);
+    SE_CUDA(cudaFuncSetAttribute(spread_mma_kernel<TZ, CAP, MINB, ZW>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    spread_mma_kernel<TZ, CAP, MINB><<<grid, 4 * TZ, smem, p->stream>>>(a);
+    spread_mma_kernel<TZ, CAP, MINB, ZW><<<grid, 4 * TZ, smem, p->stream>>>(a);
 }
 
 
@@ -999,9 +1001,14 @@ void spread(Plan* p, bool two_grids) {
     // are read from the records inside the k-steps instead of being staged
     // (10 KB of shared memory per CTA instead of 18), which lets 18 CTAs
     // share an SM (56 registers): 2.13 -> 1.94 ms (10 / 12 / 14 / 16 / 20
-    // CTAs: 2.27 / 2.10 / 1.98 / 2.02 / 2.19 ms)
+    // CTAs: 2.27 / 2.10 / 1.98 / 2.02 / 2.19 ms).  Grids of less than ~16
+    // tiles per SM (the paper's configuration: 726 tiles) are latency-bound
+    // on those loads instead and keep the staged z weights (0.171 vs
+    // 0.242 ms there)
     p->ktic(0);
-    launch_spread_mma<16, 64, 18>(p, a);
+    const int64_t tiles = (int64_t)p->ss.nbx * p->ss.nby * ((p->Nz + 15) / 16);
+    if (tiles >= 16 * (int64_t)p->num_sms) launch_spread_mma<16, 64, 18, false>(p, a);
+    else launch_spread_mma<16, 64, 10, true>(p, a);
     p->ktoc(0);
     SE_LAUNCHED(p);
 }
