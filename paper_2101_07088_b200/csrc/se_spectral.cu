@@ -269,22 +269,31 @@ __device__ __forceinline__ void solve_mode(const BvpArgs& a, int64_t m, int g, d
         descend(s0, s1);                       // rhs2 = bc = 0
         c0v = make_double2(S00 * s0.x + S01 * s1.x, S00 * s0.y + S01 * s1.y);
         c1v = make_double2(S10 * s0.x + S11 * s1.x, S10 * s0.y + S11 * s1.y);
-        update_a(c0v, c1v, false);
+        // with refinement the first refinement pass materialises
+        // y'' = x - A^{-1}B c as it reads it (one column pass fewer)
+        if (a.refine <= 0) update_a(c0v, c1v, false);
 
         for (int it = 0; it < a.refine; ++it) {     // bvp.py:229-246,268-273
+            const bool mat = it == 0;
+            auto ypp0 = [&](int k) -> double2 {      // y''_k = x_k - aib_k c_(k mod 2)
+                return cfma(-aib[k], (k & 1) ? c1v : c0v, B[(int64_t)k * RS]);
+            };
             double2 yq_sum = make_double2(0, 0), yq_sgn = make_double2(0, 0);
             double2 ye_sum = make_double2(0, 0), ye_sgn = make_double2(0, 0);
             double2 ym2 = make_double2(0, 0), ym1 = make_double2(0, 0);
-            double2 y0 = A[0];
-            double2 yp1 = (n > 1) ? A[RS] : make_double2(0, 0);
+            double2 y0 = mat ? ypp0(0) : A[0];
+            double2 yp1 = (n > 1) ? (mat ? ypp0(1) : A[RS]) : make_double2(0, 0);
             double2 dm1 = make_double2(0, 0), dm2 = make_double2(0, 0);
             for (int k0 = 0; k0 < n; k0 += CH) {
-                double2 ap[CH], fv[CH]; double ivv[CH];
+                double2 ap[CH], fv[CH]; double ivv[CH], abv[CH];
 #pragma unroll
                 for (int j = 0; j < CH; ++j) {
                     const int k = k0 + j;
                     if (k < n) {
-                        ap[j] = (k + 2 < n) ? A[(int64_t)(k + 2) * RS] : make_double2(0, 0);
+                        // B[k+2] is read before this chunk overwrites B[k0 ..]
+                        ap[j] = (k + 2 < n) ? (mat ? B : A)[(int64_t)(k + 2) * RS]
+                                            : make_double2(0, 0);
+                        abv[j] = (mat && k + 2 < n) ? aib[k + 2] : 0.0;
                         fv[j] = F[(int64_t)k * RS];
                         ivv[j] = iv[k];
                     }
@@ -293,7 +302,9 @@ __device__ __forceinline__ void solve_mode(const BvpArgs& a, int64_t m, int g, d
                 for (int j = 0; j < CH; ++j) {
                     const int k = k0 + j;
                     if (k < n) {
-                        const double2 yp2 = ap[j];
+                        double2 yp2 = ap[j];
+                        if (mat && k + 2 < n) yp2 = cfma(-abv[j], (k & 1) ? c1v : c0v, yp2);
+                        if (mat) A[(int64_t)k * RS] = y0;
                         double2 yq = make_double2(0, 0), ye = make_double2(0, 0);
                         if (k > 0) {
                             yq = cscale(y0, q_dg[k]);
