@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_scan_kernel(NearArgs a)
     constexpr int W = NB_THREADS / 32;
     __shared__ int qf[W][SCAN_Q + SU][32];
     __shared__ int qcl[W][SCAN_Q + SU][32];
-    __shared__ float4 stage[W][SCAN_STAGE];
+    __shared__ float4 stage[W][SCAN_STAGE + SU];   // + SU: a step's reads never leave it
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
     const int64_t task = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
     if (task >= a.ntask || task >= *a.ntask_dev) return;
@@ -545,24 +545,32 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_scan_kernel(NearArgs a)
                 __syncwarp();
                 for (int q = c0 + lane; q < c1; q += 32) stage[wib][q - c0] = a.srcf[q];
                 __syncwarp();
-                int jj = max(j, c0);
                 const int ee = min(e, c1);
+                // jj stays within [c0, max(ee, c0)], so a step's reads
+                // (jj .. jj + SU - 1) stay inside the padded stage
+                const int eec = max(ee, c0);
+                int jj = min(max(j, c0), eec);
                 while (__any_sync(0xffffffffu, jj < ee)) {
+                    // branch-free candidate tests: out-of-window slots read a
+                    // stage entry past the window (padded) and are masked; a
+                    // hit is pushed with one predicated store into the far or
+                    // close queue
 #pragma unroll
                     for (int u = 0; u < SU; ++u) {
-                        if (jj + u < ee) {
-                            const float4 f = stage[wib][jj + u - c0];
-                            float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
-                            if (SMALL && cw.allx) dx -= a.Lxf * rintf(dx * a.iLxf);
-                            if (SMALL && cw.ally) dy -= a.Lyf * rintf(dy * a.iLyf);
-                            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                            if (r2 <= r2f) {
-                                if (r2 > r2c) qf[wib][qn++][lane] = jj + u;
-                                else qcl[wib][qc++][lane] = jj + u;
-                            }
-                        }
+                        const int q = jj + u;
+                        const float4 f = stage[wib][q - c0];
+                        float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
+                        if (SMALL && cw.allx) dx -= a.Lxf * rintf(dx * a.iLxf);
+                        if (SMALL && cw.ally) dy -= a.Lyf * rintf(dy * a.iLyf);
+                        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                        const bool hit = q < ee && r2 <= r2f;
+                        const bool far = r2 > r2c;
+                        int* slot = far ? &qf[wib][qn][lane] : &qcl[wib][qc][lane];
+                        if (hit) *slot = q;
+                        qn += (hit && far) ? 1 : 0;
+                        qc += (hit && !far) ? 1 : 0;
                     }
-                    jj += SU;
+                    jj = min(jj + SU, eec);
                     if (__any_sync(0xffffffffu, qn >= SCAN_Q)) flush(qf[wib], qn, nf, lfar, a.cap_far, false);
                     if (__any_sync(0xffffffffu, qc >= SCAN_Q)) flush(qcl[wib], qc, nc, lcls, a.cap_close, false);
                 }
@@ -1668,6 +1676,8 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         if (d_npairs) { p->ktic(3); p->ktic(4); }
         // 16-deep queues, 4 candidates per step, 7 CTAs / SM (73 registers):
         // measured best of queue 8..24, step 4 / 8, 6..12 CTAs (3.17 vs 3.29 ms at 10)
+        // (round 2, branch-free tests: queue 8 / 16 / 24, step 4 / 8, 6..8
+        // CTAs all within 2.68-2.78 ms)
         if (cl.ncx < 5 || cl.ncy < 5)
             near_scan_kernel<16, 4, 7, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         else
