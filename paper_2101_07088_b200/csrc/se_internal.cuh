@@ -186,24 +186,24 @@ struct Solve {
 };
 
 // exp(-u) for 0 <= u <= 700 without the special-case paths of libm exp:
-// Cody-Waite reduction by ln2, degree-11 Taylor polynomial on |r| <= ln2/2,
-// scaling by 2^n through the exponent bits.  ~1 ulp.
+// Cody-Waite reduction by ln2, a degree-10 polynomial on |r| <= ln2/2
+// (Chebyshev interpolant in monomial form, 4.5e-16 relative including the
+// Horner rounding), scaling by 2^n through the exponent bits.
 __device__ __forceinline__ double exp_neg(double u) {
     const double v = -u;
     const double n = rint(v * 1.4426950408889634);
     double r = fma(n, -6.93147180369123816490e-01, v);   // ln2 hi
     r = fma(n, -1.90821492927058770002e-10, r);          // ln2 lo
-    double p = 2.5052108385441720e-08;                   // 1/11!
-    p = fma(p, r, 2.7557319223985893e-07);
-    p = fma(p, r, 2.7557319223985888e-06);
-    p = fma(p, r, 2.4801587301587302e-05);
-    p = fma(p, r, 1.9841269841269841e-04);
-    p = fma(p, r, 1.3888888888888889e-03);
-    p = fma(p, r, 8.3333333333333332e-03);
-    p = fma(p, r, 4.1666666666666664e-02);
-    p = fma(p, r, 1.6666666666666666e-01);
-    p = fma(p, r, 0.5);
-    p = fma(p, r, 1.0);
+    double p = 2.7626357241447223e-07;
+    p = fma(p, r, 2.764018079620985e-06);
+    p = fma(p, r, 2.4801504346997686e-05);
+    p = fma(p, r, 1.9841170270440067e-04);
+    p = fma(p, r, 1.3888888932488599e-03);
+    p = fma(p, r, 8.333333385667782e-03);
+    p = fma(p, r, 4.166666666657314e-02);
+    p = fma(p, r, 1.6666666666554406e-01);
+    p = fma(p, r, 5.000000000000006e-01);
+    p = fma(p, r, 1.0000000000000067);
     p = fma(p, r, 1.0);
     const long long bits = (long long)(1023 + (int)n) << 52;
     return p * __longlong_as_double(bits);
