@@ -596,3 +596,41 @@ def test_graph_replay_matches_direct_solve():
     ref = s.solve(positions=moved)
     assert np.array_equal(phi.cpu().numpy(), ref.phi_bar)
     assert U == ref.U
+
+
+# ---------------------------------------------------------------------------
+# repeated host-API solves replay the captured CUDA graph (SlabSolver.solve
+# graph=True, the default): every flag / geometry variant -- surface charge
+# (wall energy), no jump, no correction, potential or forces only, self
+# subtraction -- gives the reference's result on the replays too, and a
+# replay on moved positions gives the moved-positions golden
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("case", ["c2n256", "c2n256_noforce", "c2n256_nopot",
+                                  "c2n256_selfsub", "c2n256_nocorr", "c2n256_nojump",
+                                  "c2n256_general", "c2n256_nojump_sigma",
+                                  "c3n256_gauss_sigma", "c3n512_vacuum_metal"])
+def test_graph_replay_variants(case):
+    from test_oracle_golden import variant_problem
+    gold = solves()
+    system, params, kw = variant_problem(case)
+    refine = kw.pop("refine", 1)
+    solver = _solver(system, params, refine=refine)
+    g = gold[case]
+    ref = (g["phi"], g["E"], float(g["U"]), {"B_i": float(g["B_i"])})
+    outs = [solver.solve(**kw) for _ in range(4)]      # warm, capture, 2 replays
+    for res in outs:
+        _compare(res, ref, forces=kw.get("need_forces", True))
+    assert outs[2].U == outs[3].U
+    solver.close()
+
+
+def test_graph_replay_moved_positions():
+    gold = solves()
+    g = gold["c2n256_moved"]
+    system, params = W.build("c2", N=256)
+    solver = _solver(system, params)
+    for _ in range(3):                                 # warm, capture, replay
+        solver.solve()
+    res = solver.solve(positions=g["positions"])       # replay, new positions
+    _compare(res, (g["phi"], g["E"], float(g["U"]), {"B_i": float(g["B_i"])}))
+    solver.close()
