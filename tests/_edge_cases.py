@@ -1,5 +1,5 @@
 """Edge-case inputs shared by the golden generator and the parity tests
-(tests/golden/make_edges.py): small systems on the C2 box (L = 2, H = 1,
+(tests/golden/make_edges.py, tests/test_edges.py): small systems on the C2 box (L = 2, H = 1,
 eps_b = 0.05, eps_t = 1, g_w = 0.02, delta = 1e-4, 64 x 64 xy modes)."""
 
 import numpy as np
@@ -33,8 +33,8 @@ def _on_nodes():
 
 
 def _at_cutoff():
-    from .params import plan_grid
-    from .geometry import SlabGeometry
+    from paper_2101_07088_b200.params import plan_grid
+    from paper_2101_07088_b200.geometry import SlabGeometry
     p = plan_grid(SlabGeometry(*GEO), G_W, DELTA, Nxy=NXY)
     pos, q = _random(64, 23)
     pos[0] = [0.5, 0.5, 0.5]

@@ -19,11 +19,12 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.dirname(HERE))               # tests/ (_edge_cases)
 sys.path.insert(0, "/root/reference/pkg/src")
 
 import slabewald as sw                                   # noqa: E402
 
-from paper_2101_07088_b200 import edge_cases as EC        # noqa: E402
+import _edge_cases as EC                                  # noqa: E402
 
 
 def main():

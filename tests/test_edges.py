@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from oracle import slab_oracle as O
-from paper_2101_07088_b200 import edge_cases as EC
+import _edge_cases as EC
 from paper_2101_07088_b200.geometry import ChargeSystem, SlabGeometry
 from paper_2101_07088_b200.params import plan_grid
 from _golden import rel_l2
