@@ -808,7 +808,11 @@ void ensure_sources(Plan* p, int64_t n) {
     st.hi = dalloc<int>(p, cap);
     st.rs = (2 * p->mx + 1) + (2 * p->my + 1) + p->wz_max;
     st.rs += st.rs & 1;
-    st.rec = dalloc<double>(p, (size_t)st.rs * cap);
+    // records exist for the valid sources only, which sort first: a charge
+    // has at most one mirror image unless it lies within 2 H_E of both walls
+    // (H < 4 H_E), so 2n records suffice then (C5: 12 GB instead of 18)
+    const int64_t rec_cap = (p->P.H >= 4.0 * p->P.H_E) ? std::max<int64_t>(64, 2 * n) : cap;
+    st.rec = dalloc<double>(p, (size_t)st.rs * rec_cap);
     st.owner = dalloc<int>(p, cap);
     p->src_cap = cap;
 }
