@@ -232,12 +232,16 @@ int se_bd_step_device(int device, void* stream, double* d_pos, double* d_prev, c
  *     Gaussian width g_t inside radius, FFT Poisson solve, field
  *     interpolation, near_gradient_avg pair forces within r_cut (split g_w,
  *     xi); forces[n][3] = q (far + near).  Host buffers.
- *   se_tp_forces_device: the same on device buffers, on the plan's stream. */
+ *   se_tp_forces_device: the same on device buffers, on the plan's stream.
+ *   se_tp_set_graph: (new) with enable != 0, se_tp_forces_device captures
+ *     its kernels as a CUDA graph on the second call with the same buffers
+ *     and parameters and replays the graph from then on. */
 typedef struct se_tp se_tp;
 int se_tp_create(int device, double Lx, double Ly, double Lz, int nx, int ny, int nz,
                  double eps, se_tp** plan);
 int se_tp_destroy(se_tp* plan);
 int se_tp_set_stream(se_tp* plan, void* stream);
+int se_tp_set_graph(se_tp* plan, int enable);
 int se_tp_poisson(se_tp* plan, const double* rho, int with_field, double* phi, double* E);
 int se_tp_forces(se_tp* plan, const double* pos, const double* q, int64_t n, double g_t,
                  double radius, double g_w, double xi, double r_cut, double* forces);

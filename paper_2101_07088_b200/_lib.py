@@ -36,7 +36,7 @@ EXPORTS = ("se_plan_create", "se_plan_destroy", "se_plan_set_stream",
            "se_shard_spread", "se_shard_fields", "se_shard_charges",
            "se_dist_setup", "se_dist_buffers", "se_dist_forward",
            "se_dist_modes", "se_dist_fields", "se_steric_forces",
-           "se_tp_create", "se_tp_destroy", "se_tp_set_stream", "se_tp_poisson",
+           "se_tp_create", "se_tp_destroy", "se_tp_set_stream", "se_tp_set_graph", "se_tp_poisson",
            "se_tp_forces", "se_tp_forces_device", "se_steric_forces_device",
            "se_bd_first_noise_device", "se_bd_step_device", "se_shard_spread_own",
            "se_shard_near", "se_shard_charges_own")
@@ -146,6 +146,7 @@ def load():
                                  ctypes.c_int, _f, ctypes.POINTER(ctypes.c_void_p)]
     lib.se_tp_destroy.argtypes = [ctypes.c_void_p]
     lib.se_tp_set_stream.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+    lib.se_tp_set_graph.argtypes = [ctypes.c_void_p, ctypes.c_int]
     lib.se_tp_poisson.argtypes = [ctypes.c_void_p, _D, ctypes.c_int, _D, _D]
     lib.se_tp_forces.argtypes = [ctypes.c_void_p, _D, _D, _I64, _f, _f, _f, _f, _f, _D]
     lib.se_tp_forces_device.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -160,8 +161,8 @@ def load():
                                       ctypes.POINTER(ctypes.c_int64)]
     for name in ("se_steric_forces_device", "se_bd_first_noise_device", "se_bd_step_device"):
         getattr(lib, name).restype = ctypes.c_int
-    for name in ("se_tp_create", "se_tp_destroy", "se_tp_set_stream", "se_tp_poisson",
-                 "se_tp_forces", "se_tp_forces_device", "se_steric_forces_device",
+    for name in ("se_tp_create", "se_tp_destroy", "se_tp_set_stream", "se_tp_set_graph",
+                 "se_tp_poisson", "se_tp_forces", "se_tp_forces_device", "se_steric_forces_device",
            "se_bd_first_noise_device", "se_bd_step_device", "se_shard_spread_own",
            "se_shard_near", "se_shard_charges_own"):
         getattr(lib, name).restype = ctypes.c_int

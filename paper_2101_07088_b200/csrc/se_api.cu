@@ -1267,6 +1267,16 @@ int se_tp_set_stream(se_tp* plan, void* stream) {
     }
 }
 
+int se_tp_set_graph(se_tp* plan, int enable) {
+    try {
+        if (!plan) throw Error(SE_ERR_VALUE, "null plan");
+        tp_set_graph(reinterpret_cast<TpPlan*>(plan), enable != 0);
+        return SE_OK;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+}
+
 int se_tp_poisson(se_tp* plan, const double* rho, int with_field, double* phi, double* E) {
     try {
         tp_poisson(reinterpret_cast<TpPlan*>(plan), rho, with_field, phi, E);

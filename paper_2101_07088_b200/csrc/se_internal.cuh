@@ -485,6 +485,7 @@ struct TpPlan;
 TpPlan* tp_create(int device, const double L[3], const int n[3], double eps);
 void tp_destroy(TpPlan* p);
 void tp_set_stream(TpPlan* p, cudaStream_t s);
+void tp_set_graph(TpPlan* p, bool enable);
 void tp_poisson(TpPlan* p, const double* rho, int with_field, double* phi, double* E);
 void tp_forces(TpPlan* p, const double* pos, const double* q, int64_t n, double g_t,
                double radius, double g_w, double xi, double r_cut, double* forces);

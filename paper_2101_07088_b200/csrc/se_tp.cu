@@ -240,8 +240,23 @@ struct TpPlan {
     int64_t cap = 0;
     double* d_pts = nullptr;                   // pos[3cap] q[cap] far[3cap] near[3cap] F[3cap]
     PairScratch pairs;                         // near-field cell list
+    // CUDA graph of tp_forces_device (se_tp_set_graph): captured on the
+    // second call with the same buffers and parameters, replayed after
+    bool graph = false;
+    cudaGraphExec_t gexec = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    struct Key {
+        const void *pos = nullptr, *q = nullptr, *out = nullptr;
+        int64_t n = -1; double g_t = 0, radius = 0, g_w = 0, xi = 0, r_cut = 0;
+        bool operator==(const Key& o) const {
+            return pos == o.pos && q == o.q && out == o.out && n == o.n && g_t == o.g_t &&
+                   radius == o.radius && g_w == o.g_w && xi == o.xi && r_cut == o.r_cut;
+        }
+    } gkey, gwarm;
     ~TpPlan() {
         if (dev >= 0) cudaSetDevice(dev);
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (cap_stream) cudaStreamDestroy(cap_stream);
         pairs.release();
         if (fwd) cufftDestroy(fwd);
         if (inv) cufftDestroy(inv);
@@ -349,9 +364,73 @@ static void tp_reserve(TpPlan* p, int64_t n) {
     p->cap = n;
 }
 
+static void tp_forces_eager(TpPlan* p, const double* d_pos, const double* d_q, int64_t n,
+                            double g_t, double radius, double g_w, double xi, double r_cut,
+                            double* d_forces);
+
+void tp_set_graph(TpPlan* p, bool enable) {
+    p->graph = enable;
+    if (!enable && p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+    p->gkey = TpPlan::Key{};
+    p->gwarm = TpPlan::Key{};
+}
+
 void tp_forces_device(TpPlan* p, const double* d_pos, const double* d_q, int64_t n, double g_t,
                       double radius, double g_w, double xi, double r_cut, double* d_forces) {
     SE_CUDA(cudaSetDevice(p->dev));
+    if (!p->graph) {
+        tp_forces_eager(p, d_pos, d_q, n, g_t, radius, g_w, xi, r_cut, d_forces);
+        return;
+    }
+    TpPlan::Key key;
+    key.pos = d_pos; key.q = d_q; key.out = d_forces; key.n = n;
+    key.g_t = g_t; key.radius = radius; key.g_w = g_w; key.xi = xi; key.r_cut = r_cut;
+    if (p->gexec && p->gkey == key) {
+        SE_CUDA(cudaGraphLaunch(p->gexec, p->stream));
+        return;
+    }
+    if (!(p->gwarm == key)) {                       // first call: eager, sizes every buffer
+        tp_forces_eager(p, d_pos, d_q, n, g_t, radius, g_w, xi, r_cut, d_forces);
+        p->gwarm = key;
+        return;
+    }
+    // capture on a private stream (the caller's may be the legacy stream)
+    if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+    if (!p->cap_stream) SE_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+    const cudaStream_t run = p->stream;
+    SE_CUDA(cudaStreamSynchronize(run));
+    auto bind = [&](cudaStream_t st) {
+        p->stream = st;
+        cufftSetStream(p->fwd, st);
+        cufftSetStream(p->inv, st);
+    };
+    bind(p->cap_stream);
+    cudaGraph_t gr = nullptr;
+    cudaError_t ce = cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (ce != cudaSuccess) { bind(run); SE_CUDA(ce); }
+    try {
+        tp_forces_eager(p, d_pos, d_q, n, g_t, radius, g_w, xi, r_cut, d_forces);
+    } catch (...) {
+        cudaStreamEndCapture(p->cap_stream, &gr);
+        if (gr) cudaGraphDestroy(gr);
+        cudaGetLastError();
+        bind(run);
+        p->gwarm = TpPlan::Key{};
+        throw;
+    }
+    ce = cudaStreamEndCapture(p->cap_stream, &gr);
+    bind(run);
+    SE_CUDA(ce);
+    const cudaError_t ie = cudaGraphInstantiate(&p->gexec, gr, 0);
+    cudaGraphDestroy(gr);
+    SE_CUDA(ie);
+    p->gkey = key;
+    SE_CUDA(cudaGraphLaunch(p->gexec, p->stream));
+}
+
+static void tp_forces_eager(TpPlan* p, const double* d_pos, const double* d_q, int64_t n,
+                            double g_t, double radius, double g_w, double xi, double r_cut,
+                            double* d_forces) {
     tp_reserve(p, n);
     double* d_far = p->d_pts + 4 * p->cap;
     double* d_near = d_far + 3 * p->cap;

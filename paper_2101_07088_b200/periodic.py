@@ -97,9 +97,14 @@ class TriplyPeriodicSolver:
             self.radius, self.g_w, self.xi, self.r_cut, _lib.dptr(out)))
         return out
 
-    def forces_device(self, d_pos, d_q, n, d_out):
+    def forces_device(self, d_pos, d_q, n, d_out, graph=False):
         """Same on device buffers (pointers, e.g. ``tensor.data_ptr()``), on
-        the plan's stream (``set_stream``)."""
+        the plan's stream (``set_stream``).  ``graph``: capture the kernels as
+        a CUDA graph on the second call with the same buffers and replay it
+        from then on."""
+        if graph != getattr(self, "_graph", False):
+            _lib.check(self._plan._lib.se_tp_set_graph(self._plan._h, 1 if graph else 0))
+            self._graph = graph
         _lib.check(self._plan._lib.se_tp_forces_device(
             self._plan._h, ctypes.c_void_p(d_pos), ctypes.c_void_p(d_q), int(n), self.g_t,
             self.radius, self.g_w, self.xi, self.r_cut, ctypes.c_void_p(d_out)))

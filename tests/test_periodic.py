@@ -113,3 +113,32 @@ def test_gpu_tp_edges():
     assert g.n == o.n
     sub = slice(0, 120)
     assert rel_l2(g.forces(pos[sub], G["g2_q"][sub]), o.forces(pos[sub], G["g2_q"][sub])) < 1e-10
+
+
+@pytest.mark.gpu
+def test_gpu_tp_forces_device_graph():
+    """forces_device replayed as a CUDA graph (se_tp_set_graph): warm call,
+    capture, replays -- all equal to the reference's forces, and a replay
+    on moved positions (same buffer) equals the eager result there."""
+    import torch
+    from paper_2101_07088_b200.periodic import TriplyPeriodicSolver
+    box, boxes, eps = _g2()
+    s = TriplyPeriodicSolver(boxes, 32, 0.25, eps, delta=5e-4)
+    st = torch.cuda.current_stream()
+    s.set_stream(st.cuda_stream)
+    n = G["g2_q"].size
+    pos = torch.tensor(G["g2_pos"], device="cuda")
+    q = torch.tensor(G["g2_q"], device="cuda")
+    out = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    for _ in range(4):
+        s.forces_device(pos.data_ptr(), q.data_ptr(), n, out.data_ptr(), graph=True)
+        torch.cuda.synchronize()
+        assert rel_l2(out.cpu().numpy(), G["g2_forces"]) < 1e-11
+    h = box / 32
+    moved = G["g2_pos"] + np.array([0.3 * h, -0.7 * h, 0.2 * h])
+    pos.copy_(torch.tensor(moved))
+    s.forces_device(pos.data_ptr(), q.data_ptr(), n, out.data_ptr(), graph=True)
+    torch.cuda.synchronize()
+    ref = s.forces(moved, G["g2_q"])
+    assert rel_l2(out.cpu().numpy(), ref) < 1e-12
+    s.close()

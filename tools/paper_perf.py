@@ -101,6 +101,9 @@ def measure(steps=20, warmup=5, sweep=True):
     out["tp_ms"] = _median_ms(
         lambda: tp.forces_device(pos.data_ptr(), q.data_ptr(), n, F.data_ptr()),
         steps, warmup, stream)
+    out["tp_ms_graph"] = _median_ms(
+        lambda: tp.forces_device(pos.data_ptr(), q.data_ptr(), n, F.data_ptr(), graph=True),
+        steps, warmup, stream)
     out["tp_ms_published"] = 0.84
     tp.close()
     if sweep:
