@@ -133,7 +133,7 @@ NCU_FILE = os.path.join("profiles", "ncu_c4_kernels.json")
 STAGE_KERNELS = {                      # stage -> kernel-name prefixes in the capture
     "spread": ("spread_mma_kernel",),
     "interp": ("interp_kernel",),
-    "bvp": ("bvp_kernel",),
+    "bvp": ("bvp_pass_kernel", "bvp_final_kernel", "bvp_warp_kernel"),
     "near": ("near_scan_kernel", "near_eval_kernel", "near_fq_kernel",
              "near_fused_kernel", "near_boundary_kernel"),
     "near_eval": ("near_eval_kernel",),

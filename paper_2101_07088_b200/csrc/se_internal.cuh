@@ -345,6 +345,7 @@ struct Plan {
     cufftDoubleComplex* d_spec = nullptr; // [Nz][4][M]
     double* d_fields = nullptr;           // [Nz][4][Nx][Ny]
     cufftDoubleComplex* d_scr = nullptr;  // BVP scratch [3][Nz][M]
+    cufftDoubleComplex* d_bst = nullptr;  // split BVP column state [6][2][M]
     bool keep_stages = false;
     cufftDoubleComplex* d_keep = nullptr; // [Nz][2][M] psi coefficients (debug)
     cufftDoubleComplex* d_mom = nullptr;  // [M][2] correction moments / den

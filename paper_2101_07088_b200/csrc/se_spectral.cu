@@ -130,6 +130,8 @@ struct BvpArgs {
     const double2* sbh; const double2* sth;
     double2* ext;                // [2N][2][M] in: raw DCT, out: iDCT inputs
     double2* scrF; double2* scrA; double2* scrB;   // [Nz][M] each
+    double2* bst;                // split kernels: [6][2][M] c0, c1, deferred dc0, dc1, r2
+    int iter;                    // split kernels: the refinement iteration
     double inv_nxy;
     double2* mom;                // [M][2]  M_b/den, M_t/den
     double2* mism;               // [4][M] (debug, may be null)
@@ -139,267 +141,6 @@ struct BvpArgs {
     int* flags;
     double rb, rt, H;
 };
-
-// Solve one grid of one mode (column m, grid slot g of ext).  Returns the
-// wall values wv = {y(0), y(H), y'(0), y'(H)} and ends = {y'(z0), y'(z1)}.
-// With emit, writes the Chebyshev coefficients of y (slot 0) and y' (slot 1)
-// for the inverse DCT GEMMs.
-// Scratch columns (stride M): F = f_sc, A = y'' (ypp), B = Thomas d / x.
-__device__ __forceinline__ void solve_mode(const BvpArgs& a, int64_t m, int g, double2 wv[4],
-                                           double2 ends[2], bool emit) {
-    const int n = a.Nz;
-    const int64_t M = a.M, RS = 2 * M;           // row stride of [Nz][2][M]
-    const double2* __restrict__ raw = a.ext + g * M + m;
-    // scratch columns: [Nz][2][M], this grid's column (row stride 2M)
-    double2* __restrict__ F = a.scrF + g * M + m;
-    double2* __restrict__ A = a.scrA + g * M + m;
-    double2* __restrict__ B = a.scrB + g * M + m;
-    const double* __restrict__ q_lo = a.mp.q_lo;
-    const double* __restrict__ q_dg = a.mp.q_dg;
-    const double* __restrict__ q_hi = a.mp.q_hi;
-    const double* __restrict__ e_lo = a.mp.e_lo;
-    const double* __restrict__ e_hi = a.mp.e_hi;
-    // f_sc = -(Chebyshev coefficient of rho_hat) / eps * half^2; the DCT-I
-    // GEMM produced the coefficients of the unnormalised xy spectrum
-    const double base = -(a.half * a.half) / a.eps * a.inv_nxy;
-    auto fsc_at = [&](int k) -> double2 { return cscale(raw[(int64_t)k * RS], base); };
-    const int u = a.kidx[m];
-    double2 c0v = make_double2(0, 0), c1v = make_double2(0, 0);
-    if (u < 0) {
-        // ---- k = 0: y'' = f, y(z0) = y(z1) = 0              bvp.py:281-296
-        for (int k = 0; k < n; ++k) A[(int64_t)k * RS] = fsc_at(k);
-        double2 P = make_double2(0, 0), Qs = make_double2(0, 0);
-        for (int k = 1; k < n; ++k) {
-            double2 y = cscale(A[(int64_t)k * RS], q_dg[k]);
-            if (k >= 2) y = cadd(y, cscale(A[(int64_t)(k - 2) * RS], q_lo[k]));
-            if (k + 2 < n) y = cadd(y, cscale(A[(int64_t)(k + 2) * RS], q_hi[k]));
-            P = cadd(P, y);
-            Qs = (k & 1) ? csub(Qs, y) : cadd(Qs, y);
-        }
-        c0v = cscale(cadd(P, Qs), -0.5);
-        c1v = cscale(csub(Qs, P), 0.5);
-    } else {
-        const double* __restrict__ cp = a.fac + ((int64_t)u * FAC_ROWS + FAC_CP) * n;
-        const double* __restrict__ iv = a.fac + ((int64_t)u * FAC_ROWS + FAC_INV) * n;
-        const double* __restrict__ aib = a.fac + ((int64_t)u * FAC_ROWS + FAC_AINVB) * n;
-        const double* __restrict__ cr0 = a.fac + ((int64_t)u * FAC_ROWS + FAC_C0) * n;
-        const double* __restrict__ cr1 = a.fac + ((int64_t)u * FAC_ROWS + FAC_C1) * n;
-        const double kap = a.kappa[u], k2 = kap * kap;
-        const double S00 = a.sinv[4 * u], S01 = a.sinv[4 * u + 1];
-        const double S10 = a.sinv[4 * u + 2], S11 = a.sinv[4 * u + 3];
-
-        // Every sweep runs in chunks of CH rows: the chunk's loads (scratch
-        // rows, per-|k| factor rows) are issued together before its
-        // recurrence steps, so CH loads are in flight per thread instead of
-        // one (the stores of a chunk would otherwise serialise the loads of
-        // the next row through possible aliasing).
-        constexpr int CH = 4;
-        // forward sweep (both parity chains interleaved): d_k = (r_k - lo_k d_{k-2}) / den_k
-        // backward sweep: x_k = d_k - cp_k x_{k+2}; Schur rhs C.x     bvp.py:76-90,216-227
-        auto descend = [&](double2& s0, double2& s1) {
-            double2 xp1 = make_double2(0, 0), xp2 = make_double2(0, 0);
-            s0 = make_double2(0, 0); s1 = make_double2(0, 0);
-            for (int k0 = n - 1; k0 >= 0; k0 -= CH) {
-                double2 dv[CH]; double cpv[CH], c0r[CH], c1r[CH];
-#pragma unroll
-                for (int j = 0; j < CH; ++j) {
-                    const int k = k0 - j;
-                    if (k >= 0) { dv[j] = B[(int64_t)k * RS]; cpv[j] = cp[k]; c0r[j] = cr0[k]; c1r[j] = cr1[k]; }
-                }
-#pragma unroll
-                for (int j = 0; j < CH; ++j) {
-                    const int k = k0 - j;
-                    if (k >= 0) {
-                        const double2 x = (k + 2 < n) ? cfma(-cpv[j], xp2, dv[j]) : dv[j];
-                        B[(int64_t)k * RS] = x;
-                        s0 = cfma(c0r[j], x, s0);
-                        s1 = cfma(c1r[j], x, s1);
-                        xp2 = xp1; xp1 = x;
-                    }
-                }
-            }
-        };
-        // y'' = x - A^{-1}B c  (A += dy when accumulate)
-        auto update_a = [&](double2 v0, double2 v1, bool accumulate) {
-            for (int k0 = 0; k0 < n; k0 += CH) {
-                double2 bv[CH], av[CH]; double ab[CH];
-#pragma unroll
-                for (int j = 0; j < CH; ++j) {
-                    const int k = k0 + j;
-                    if (k < n) {
-                        bv[j] = B[(int64_t)k * RS]; ab[j] = aib[k];
-                        if (accumulate) av[j] = A[(int64_t)k * RS];
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < CH; ++j) {
-                    const int k = k0 + j;
-                    if (k < n) {
-                        double2 y = cfma(-ab[j], (k & 1) ? v1 : v0, bv[j]);
-                        if (accumulate) y = cadd(av[j], y);
-                        A[(int64_t)k * RS] = y;
-                    }
-                }
-            }
-        };
-        {
-            double2 dm1 = make_double2(0, 0), dm2 = make_double2(0, 0);
-            for (int k0 = 0; k0 < n; k0 += CH) {
-                double2 rv[CH]; double ivv[CH];
-#pragma unroll
-                for (int j = 0; j < CH; ++j) {
-                    const int k = k0 + j;
-                    if (k < n) { rv[j] = fsc_at(k); ivv[j] = iv[k]; }
-                }
-#pragma unroll
-                for (int j = 0; j < CH; ++j) {
-                    const int k = k0 + j;
-                    if (k < n) {
-                        const double2 r = rv[j];
-                        F[(int64_t)k * RS] = r;
-                        const double2 d = (k < 2) ? cscale(r, ivv[j])
-                                                  : cscale(cfma(k2 * q_lo[k], dm2, r), ivv[j]);
-                        B[(int64_t)k * RS] = d;
-                        dm2 = dm1; dm1 = d;
-                    }
-                }
-            }
-        }
-        double2 s0, s1;
-        descend(s0, s1);                       // rhs2 = bc = 0
-        c0v = make_double2(S00 * s0.x + S01 * s1.x, S00 * s0.y + S01 * s1.y);
-        c1v = make_double2(S10 * s0.x + S11 * s1.x, S10 * s0.y + S11 * s1.y);
-        // with refinement the first refinement pass materialises
-        // y'' = x - A^{-1}B c as it reads it (one column pass fewer)
-        if (a.refine <= 0) update_a(c0v, c1v, false);
-
-        for (int it = 0; it < a.refine; ++it) {     // bvp.py:229-246,268-273
-            const bool mat = it == 0;
-            auto ypp0 = [&](int k) -> double2 {      // y''_k = x_k - aib_k c_(k mod 2)
-                return cfma(-aib[k], (k & 1) ? c1v : c0v, B[(int64_t)k * RS]);
-            };
-            double2 yq_sum = make_double2(0, 0), yq_sgn = make_double2(0, 0);
-            double2 ye_sum = make_double2(0, 0), ye_sgn = make_double2(0, 0);
-            double2 ym2 = make_double2(0, 0), ym1 = make_double2(0, 0);
-            double2 y0 = mat ? ypp0(0) : A[0];
-            double2 yp1 = (n > 1) ? (mat ? ypp0(1) : A[RS]) : make_double2(0, 0);
-            double2 dm1 = make_double2(0, 0), dm2 = make_double2(0, 0);
-            for (int k0 = 0; k0 < n; k0 += CH) {
-                double2 ap[CH], fv[CH]; double ivv[CH], abv[CH];
-#pragma unroll
-                for (int j = 0; j < CH; ++j) {
-                    const int k = k0 + j;
-                    if (k < n) {
-                        // B[k+2] is read before this chunk overwrites B[k0 ..]
-                        ap[j] = (k + 2 < n) ? (mat ? B : A)[(int64_t)(k + 2) * RS]
-                                            : make_double2(0, 0);
-                        abv[j] = (mat && k + 2 < n) ? aib[k + 2] : 0.0;
-                        fv[j] = F[(int64_t)k * RS];
-                        ivv[j] = iv[k];
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < CH; ++j) {
-                    const int k = k0 + j;
-                    if (k < n) {
-                        double2 yp2 = ap[j];
-                        if (mat && k + 2 < n) yp2 = cfma(-abv[j], (k & 1) ? c1v : c0v, yp2);
-                        if (mat) A[(int64_t)k * RS] = y0;
-                        double2 yq = make_double2(0, 0), ye = make_double2(0, 0);
-                        if (k > 0) {
-                            yq = cscale(y0, q_dg[k]);
-                            if (k >= 2) yq = cadd(yq, cscale(ym2, q_lo[k]));
-                            if (k + 2 < n) yq = cadd(yq, cscale(yp2, q_hi[k]));
-                            ye = cscale(ym1, e_lo[k]);
-                            if (k + 1 < n) ye = cadd(ye, cscale(yp1, e_hi[k]));
-                        }
-                        double2 r = csub(fv[j], csub(y0, cscale(yq, k2)));
-                        if (k == 0) r = cadd(r, cscale(c0v, k2));
-                        if (k == 1) r = cadd(r, cscale(c1v, k2));
-                        yq_sum = cadd(yq_sum, yq); ye_sum = cadd(ye_sum, ye);
-                        if (k & 1) { yq_sgn = csub(yq_sgn, yq); ye_sgn = csub(ye_sgn, ye); }
-                        else { yq_sgn = cadd(yq_sgn, yq); ye_sgn = cadd(ye_sgn, ye); }
-                        const double2 d = (k < 2) ? cscale(r, ivv[j])
-                                                  : cscale(cfma(k2 * q_lo[k], dm2, r), ivv[j]);
-                        B[(int64_t)k * RS] = d;
-                        dm2 = dm1; dm1 = d;
-                        ym2 = ym1; ym1 = y0; y0 = yp1; yp1 = yp2;
-                    }
-                }
-            }
-            // r2 = bc - (C ypp + D c) with bc = 0
-            double2 r20 = cscale(cadd(cadd(ye_sum, cscale(yq_sum, kap)),
-                                      cadd(cscale(c0v, kap), cscale(c1v, 1.0 + kap))), -1.0);
-            double2 r21 = cscale(cadd(csub(ye_sgn, cscale(yq_sgn, kap)),
-                                      cadd(cscale(c0v, -kap), cscale(c1v, 1.0 + kap))), -1.0);
-            double2 t0, t1;
-            descend(t0, t1);
-            t0 = csub(t0, r20); t1 = csub(t1, r21);
-            double2 dc0 = make_double2(S00 * t0.x + S01 * t1.x, S00 * t0.y + S01 * t1.y);
-            double2 dc1 = make_double2(S10 * t0.x + S11 * t1.x, S10 * t0.y + S11 * t1.y);
-            update_a(dc0, dc1, true);
-            c0v = cadd(c0v, dc0);
-            c1v = cadd(c1v, dc1);
-        }
-    }
-    // ---- y = Q ypp + c0 T0 + c1 T1; derivative (downward recurrence,
-    // chebyshev.py:68-79), wall values, iDCT inputs
-    const double dscale = 2.0 / (a.z1 - a.z0);
-    double2 w_y0 = make_double2(0, 0), w_yH = make_double2(0, 0);
-    double2 w_d0 = make_double2(0, 0), w_dH = make_double2(0, 0);
-    double2 d_sum = make_double2(0, 0), d_sgn = make_double2(0, 0);
-    double2 bp1 = make_double2(0, 0), bp2 = make_double2(0, 0);   // b_{k+1}, b_{k+2}
-    double2 ynext = make_double2(0, 0);                              // y_{k+1}
-    double2* out_y = a.ext + 0 * M + m;
-    double2* out_d = a.ext + 1 * M + m;
-    // sliding window of ypp: a_{k-2}, a_k, a_{k+2} (loads a chunk ahead)
-    constexpr int CHF = 8;
-    double2 ap2 = make_double2(0, 0), ap1 = make_double2(0, 0);
-    double2 a0 = A[(int64_t)(n - 1) * RS];
-    double2 am1 = (n >= 2) ? A[(int64_t)(n - 2) * RS] : make_double2(0, 0);
-    for (int k0 = n - 1; k0 >= 0; k0 -= CHF) {
-        double2 amv[CHF];
-#pragma unroll
-        for (int j = 0; j < CHF; ++j) {
-            const int k = k0 - j;
-            amv[j] = (k >= 2) ? A[(int64_t)(k - 2) * RS] : make_double2(0, 0);
-        }
-#pragma unroll
-        for (int j = 0; j < CHF; ++j) {
-            const int k = k0 - j;
-            if (k < 0) break;
-            const double2 am2 = amv[j];
-            double2 y = make_double2(0, 0);
-            if (k > 0) {
-                y = cscale(a0, q_dg[k]);
-                if (k >= 2) y = cadd(y, cscale(am2, q_lo[k]));
-                if (k + 2 < n) y = cadd(y, cscale(ap2, q_hi[k]));
-            }
-            if (k == 0) y = cadd(y, c0v);
-            if (k == 1) y = cadd(y, c1v);
-            double2 b;
-            if (k == n - 1) b = make_double2(0, 0);
-            else if (k == n - 2) b = cscale(ynext, 2.0 * (n - 1));
-            else b = cadd(bp2, cscale(ynext, 2.0 * (k + 1)));
-            const double2 bs = cscale((k == 0) ? cscale(b, 0.5) : b, dscale);
-            w_y0 = cfma(a.tw0[k], y, w_y0);
-            w_yH = cfma(a.twH[k], y, w_yH);
-            w_d0 = cfma(a.tw0[k], bs, w_d0);
-            w_dH = cfma(a.twH[k], bs, w_dH);
-            d_sum = cadd(d_sum, bs);
-            d_sgn = (k & 1) ? csub(d_sgn, bs) : cadd(d_sgn, bs);
-            if (a.keep) a.keep[((int64_t)k * 2 + g) * M + m] = y;
-            if (emit) {                             // coefficients for the iDCT GEMM
-                out_y[(int64_t)k * RS] = y;
-                out_d[(int64_t)k * RS] = bs;
-            }
-            bp2 = bp1; bp1 = b; ynext = y;
-            ap2 = ap1; ap1 = a0; a0 = am1; am1 = am2;
-        }
-    }
-    wv[0] = w_y0; wv[1] = w_yH; wv[2] = w_d0; wv[3] = w_dH;
-    ends[0] = d_sgn; ends[1] = d_sum;
-}
 
 __device__ __forceinline__ bool finite2(double2 v) { return isfinite(v.x) && isfinite(v.y); }
 
@@ -471,8 +212,298 @@ __device__ __forceinline__ void finish_mode(const BvpArgs& a, int64_t m, const d
     a.scal[0] = A_i;
 }
 
-__global__ void __launch_bounds__(64) bvp_kernel(BvpArgs a) {
-    // lane pair (2m, 2m+1) = (over grid, in-slab grid) of mode m
+// ---------------------------------------------------------------------------
+// The per-mode solve, one thread per (mode, grid) column, split over kernels
+// so each holds only its own pass's registers (one fused kernel needed 254
+// registers and 8 warps / SM; split: 1.22 -> 1.10 ms at C4).  Scratch
+// columns (row stride 2M of [Nz][2][M]): F = f_sc, A = y'' (ypp), B = Thomas
+// d / x; the column state -- c0, c1, the refinement's Schur rhs r2 and the
+// deferred last update dc -- is carried in a.bst between the kernels:
+//   pass 0: forward sweep + descend -> c (or the k = 0 solve, bvp.py:281-296);
+//   pass 1: a refinement's forward pass (the first materialises y'' as it
+//           reads it) -> r2                              bvp.py:229-246
+//   pass 3: its descend -> dc; the last refinement's y'' update is deferred
+//   pass 2: y'' (+ the deferred update) -> y = Q y'' + c0 T0 + c1 T1, y'
+//           (downward recurrence, chebyshev.py:68-79), wall values and the
+//           iDCT inputs (in-slab grid), then the lane-pair finish of
+//           bvp_final_kernel (mismatch, moments, k = 0; finish_mode).
+// ---------------------------------------------------------------------------
+template <int PASS>
+__device__ __forceinline__ void solve_mode_pass(const BvpArgs& a, int64_t m, int g,
+                                                double2 wv[4], double2 ends[2], bool emit) {
+    const int n = a.Nz;
+    const int64_t M = a.M, RS = 2 * M;
+    const double2* __restrict__ raw = a.ext + g * M + m;
+    double2* __restrict__ F = a.scrF + g * M + m;
+    double2* __restrict__ A = a.scrA + g * M + m;
+    double2* __restrict__ B = a.scrB + g * M + m;
+    double2* __restrict__ st = a.bst + g * M + m;          // state s at st[s * RS]
+    const double* __restrict__ q_lo = a.mp.q_lo;
+    const double* __restrict__ q_dg = a.mp.q_dg;
+    const double* __restrict__ q_hi = a.mp.q_hi;
+    const double* __restrict__ e_lo = a.mp.e_lo;
+    const double* __restrict__ e_hi = a.mp.e_hi;
+    const double base = -(a.half * a.half) / a.eps * a.inv_nxy;
+    auto fsc_at = [&](int k) -> double2 { return cscale(raw[(int64_t)k * RS], base); };
+    const int u = a.kidx[m];
+    const bool defer = u >= 0 && a.refine > 0;
+    const double* __restrict__ cp = nullptr; const double* __restrict__ iv = nullptr;
+    const double* __restrict__ aib = nullptr; const double* __restrict__ cr0 = nullptr;
+    const double* __restrict__ cr1 = nullptr;
+    double kap = 0, k2 = 0, S00 = 0, S01 = 0, S10 = 0, S11 = 0;
+    if (u >= 0) {
+        cp = a.fac + ((int64_t)u * FAC_ROWS + FAC_CP) * n;
+        iv = a.fac + ((int64_t)u * FAC_ROWS + FAC_INV) * n;
+        aib = a.fac + ((int64_t)u * FAC_ROWS + FAC_AINVB) * n;
+        cr0 = a.fac + ((int64_t)u * FAC_ROWS + FAC_C0) * n;
+        cr1 = a.fac + ((int64_t)u * FAC_ROWS + FAC_C1) * n;
+        kap = a.kappa[u]; k2 = kap * kap;
+        S00 = a.sinv[4 * u]; S01 = a.sinv[4 * u + 1];
+        S10 = a.sinv[4 * u + 2]; S11 = a.sinv[4 * u + 3];
+    }
+    constexpr int CH = 4;
+    auto descend = [&](double2& s0, double2& s1) {
+        double2 xp1 = make_double2(0, 0), xp2 = make_double2(0, 0);
+        s0 = make_double2(0, 0); s1 = make_double2(0, 0);
+        for (int k0 = n - 1; k0 >= 0; k0 -= CH) {
+            double2 dv[CH]; double cpv[CH], c0r[CH], c1r[CH];
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+                const int k = k0 - j;
+                if (k >= 0) { dv[j] = B[(int64_t)k * RS]; cpv[j] = cp[k]; c0r[j] = cr0[k]; c1r[j] = cr1[k]; }
+            }
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+                const int k = k0 - j;
+                if (k >= 0) {
+                    const double2 x = (k + 2 < n) ? cfma(-cpv[j], xp2, dv[j]) : dv[j];
+                    B[(int64_t)k * RS] = x;
+                    s0 = cfma(c0r[j], x, s0);
+                    s1 = cfma(c1r[j], x, s1);
+                    xp2 = xp1; xp1 = x;
+                }
+            }
+        }
+    };
+    auto update_a = [&](double2 v0, double2 v1, bool accumulate) {
+        for (int k0 = 0; k0 < n; k0 += CH) {
+            double2 bv[CH], av[CH]; double ab[CH];
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+                const int k = k0 + j;
+                if (k < n) {
+                    bv[j] = B[(int64_t)k * RS]; ab[j] = aib[k];
+                    if (accumulate) av[j] = A[(int64_t)k * RS];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+                const int k = k0 + j;
+                if (k < n) {
+                    double2 y = cfma(-ab[j], (k & 1) ? v1 : v0, bv[j]);
+                    if (accumulate) y = cadd(av[j], y);
+                    A[(int64_t)k * RS] = y;
+                }
+            }
+        }
+    };
+    if constexpr (PASS == 0) {
+        double2 c0v = make_double2(0, 0), c1v = make_double2(0, 0);
+        if (u < 0) {                           // k = 0: y'' = f, y(z0) = y(z1) = 0   bvp.py:281-296
+            for (int k = 0; k < n; ++k) A[(int64_t)k * RS] = fsc_at(k);
+            double2 P = make_double2(0, 0), Qs = make_double2(0, 0);
+            for (int k = 1; k < n; ++k) {
+                double2 y = cscale(A[(int64_t)k * RS], q_dg[k]);
+                if (k >= 2) y = cadd(y, cscale(A[(int64_t)(k - 2) * RS], q_lo[k]));
+                if (k + 2 < n) y = cadd(y, cscale(A[(int64_t)(k + 2) * RS], q_hi[k]));
+                P = cadd(P, y);
+                Qs = (k & 1) ? csub(Qs, y) : cadd(Qs, y);
+            }
+            c0v = cscale(cadd(P, Qs), -0.5);
+            c1v = cscale(csub(Qs, P), 0.5);
+        } else {
+            double2 dm1 = make_double2(0, 0), dm2 = make_double2(0, 0);
+            for (int k0 = 0; k0 < n; k0 += CH) {
+                double2 rv[CH]; double ivv[CH];
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int k = k0 + j;
+                    if (k < n) { rv[j] = fsc_at(k); ivv[j] = iv[k]; }
+                }
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int k = k0 + j;
+                    if (k < n) {
+                        const double2 r = rv[j];
+                        F[(int64_t)k * RS] = r;
+                        const double2 d = (k < 2) ? cscale(r, ivv[j])
+                                                  : cscale(cfma(k2 * q_lo[k], dm2, r), ivv[j]);
+                        B[(int64_t)k * RS] = d;
+                        dm2 = dm1; dm1 = d;
+                    }
+                }
+            }
+            double2 s0, s1;
+            descend(s0, s1);
+            c0v = make_double2(S00 * s0.x + S01 * s1.x, S00 * s0.y + S01 * s1.y);
+            c1v = make_double2(S10 * s0.x + S11 * s1.x, S10 * s0.y + S11 * s1.y);
+            if (a.refine <= 0) update_a(c0v, c1v, false);
+        }
+        st[0] = c0v; st[RS] = c1v;
+    } else if constexpr (PASS == 1) {
+        // one refinement's forward pass (iteration a.iter): y'' window,
+        // residual, Thomas forward sweep; the Schur rhs r2 into the state
+        if (!defer) return;
+        const double2 c0v = st[0], c1v = st[RS];
+        {
+            const bool mat = a.iter == 0;
+            auto ypp0 = [&](int k) -> double2 {
+                return cfma(-aib[k], (k & 1) ? c1v : c0v, B[(int64_t)k * RS]);
+            };
+            double2 yq_sum = make_double2(0, 0), yq_sgn = make_double2(0, 0);
+            double2 ye_sum = make_double2(0, 0), ye_sgn = make_double2(0, 0);
+            double2 ym2 = make_double2(0, 0), ym1 = make_double2(0, 0);
+            double2 y0 = mat ? ypp0(0) : A[0];
+            double2 yp1 = (n > 1) ? (mat ? ypp0(1) : A[RS]) : make_double2(0, 0);
+            double2 dm1 = make_double2(0, 0), dm2 = make_double2(0, 0);
+            for (int k0 = 0; k0 < n; k0 += CH) {
+                double2 ap[CH], fv[CH]; double ivv[CH], abv[CH];
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int k = k0 + j;
+                    if (k < n) {
+                        ap[j] = (k + 2 < n) ? (mat ? B : A)[(int64_t)(k + 2) * RS]
+                                            : make_double2(0, 0);
+                        abv[j] = (mat && k + 2 < n) ? aib[k + 2] : 0.0;
+                        fv[j] = F[(int64_t)k * RS];
+                        ivv[j] = iv[k];
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int k = k0 + j;
+                    if (k < n) {
+                        double2 yp2 = ap[j];
+                        if (mat && k + 2 < n) yp2 = cfma(-abv[j], (k & 1) ? c1v : c0v, yp2);
+                        if (mat) A[(int64_t)k * RS] = y0;
+                        double2 yq = make_double2(0, 0), ye = make_double2(0, 0);
+                        if (k > 0) {
+                            yq = cscale(y0, q_dg[k]);
+                            if (k >= 2) yq = cadd(yq, cscale(ym2, q_lo[k]));
+                            if (k + 2 < n) yq = cadd(yq, cscale(yp2, q_hi[k]));
+                            ye = cscale(ym1, e_lo[k]);
+                            if (k + 1 < n) ye = cadd(ye, cscale(yp1, e_hi[k]));
+                        }
+                        double2 r = csub(fv[j], csub(y0, cscale(yq, k2)));
+                        if (k == 0) r = cadd(r, cscale(c0v, k2));
+                        if (k == 1) r = cadd(r, cscale(c1v, k2));
+                        yq_sum = cadd(yq_sum, yq); ye_sum = cadd(ye_sum, ye);
+                        if (k & 1) { yq_sgn = csub(yq_sgn, yq); ye_sgn = csub(ye_sgn, ye); }
+                        else { yq_sgn = cadd(yq_sgn, yq); ye_sgn = cadd(ye_sgn, ye); }
+                        const double2 d = (k < 2) ? cscale(r, ivv[j])
+                                                  : cscale(cfma(k2 * q_lo[k], dm2, r), ivv[j]);
+                        B[(int64_t)k * RS] = d;
+                        dm2 = dm1; dm1 = d;
+                        ym2 = ym1; ym1 = y0; y0 = yp1; yp1 = yp2;
+                    }
+                }
+            }
+            st[4 * RS] = cscale(cadd(cadd(ye_sum, cscale(yq_sum, kap)),
+                                     cadd(cscale(c0v, kap), cscale(c1v, 1.0 + kap))), -1.0);
+            st[5 * RS] = cscale(cadd(csub(ye_sgn, cscale(yq_sgn, kap)),
+                                     cadd(cscale(c0v, -kap), cscale(c1v, 1.0 + kap))), -1.0);
+        }
+    } else if constexpr (PASS == 3) {
+        // the refinement's descend and correction dc; the last one's y''
+        // update is deferred into pass 2
+        if (!defer) return;
+        double2 t0, t1;
+        descend(t0, t1);
+        t0 = csub(t0, st[4 * RS]); t1 = csub(t1, st[5 * RS]);
+        const double2 dc0 = make_double2(S00 * t0.x + S01 * t1.x, S00 * t0.y + S01 * t1.y);
+        const double2 dc1 = make_double2(S10 * t0.x + S11 * t1.x, S10 * t0.y + S11 * t1.y);
+        if (a.iter + 1 < a.refine) update_a(dc0, dc1, true);
+        else { st[2 * RS] = dc0; st[3 * RS] = dc1; }   // applied by pass 2
+        st[0] = cadd(st[0], dc0);
+        st[RS] = cadd(st[RS], dc1);
+    } else {
+        const double2 c0v = st[0], c1v = st[RS];
+        const double2 pd0 = defer ? st[2 * RS] : make_double2(0, 0);
+        const double2 pd1 = defer ? st[3 * RS] : make_double2(0, 0);
+        auto ypp = [&](int k) -> double2 {
+            const double2 av = A[(int64_t)k * RS];
+            if (!defer) return av;
+            return cadd(av, cfma(-aib[k], (k & 1) ? pd1 : pd0, B[(int64_t)k * RS]));
+        };
+        const double dscale = 2.0 / (a.z1 - a.z0);
+        double2 w_y0 = make_double2(0, 0), w_yH = make_double2(0, 0);
+        double2 w_d0 = make_double2(0, 0), w_dH = make_double2(0, 0);
+        double2 d_sum = make_double2(0, 0), d_sgn = make_double2(0, 0);
+        double2 bp1 = make_double2(0, 0), bp2 = make_double2(0, 0);
+        double2 ynext = make_double2(0, 0);
+        double2* out_y = a.ext + 0 * M + m;
+        double2* out_d = a.ext + 1 * M + m;
+        constexpr int CHF = 4;
+        double2 ap2 = make_double2(0, 0), ap1 = make_double2(0, 0);
+        double2 a0 = ypp(n - 1);
+        double2 am1 = (n >= 2) ? ypp(n - 2) : make_double2(0, 0);
+        for (int k0 = n - 1; k0 >= 0; k0 -= CHF) {
+            double2 amv[CHF];
+#pragma unroll
+            for (int j = 0; j < CHF; ++j) {
+                const int k = k0 - j;
+                amv[j] = (k >= 2) ? ypp(k - 2) : make_double2(0, 0);
+            }
+#pragma unroll
+            for (int j = 0; j < CHF; ++j) {
+                const int k = k0 - j;
+                if (k < 0) break;
+                const double2 am2 = amv[j];
+                double2 y = make_double2(0, 0);
+                if (k > 0) {
+                    y = cscale(a0, q_dg[k]);
+                    if (k >= 2) y = cadd(y, cscale(am2, q_lo[k]));
+                    if (k + 2 < n) y = cadd(y, cscale(ap2, q_hi[k]));
+                }
+                if (k == 0) y = cadd(y, c0v);
+                if (k == 1) y = cadd(y, c1v);
+                double2 b;
+                if (k == n - 1) b = make_double2(0, 0);
+                else if (k == n - 2) b = cscale(ynext, 2.0 * (n - 1));
+                else b = cadd(bp2, cscale(ynext, 2.0 * (k + 1)));
+                const double2 bs = cscale((k == 0) ? cscale(b, 0.5) : b, dscale);
+                w_y0 = cfma(a.tw0[k], y, w_y0);
+                w_yH = cfma(a.twH[k], y, w_yH);
+                w_d0 = cfma(a.tw0[k], bs, w_d0);
+                w_dH = cfma(a.twH[k], bs, w_dH);
+                d_sum = cadd(d_sum, bs);
+                d_sgn = (k & 1) ? csub(d_sgn, bs) : cadd(d_sgn, bs);
+                if (a.keep) a.keep[((int64_t)k * 2 + g) * M + m] = y;
+                if (emit) {
+                    out_y[(int64_t)k * RS] = y;
+                    out_d[(int64_t)k * RS] = bs;
+                }
+                bp2 = bp1; bp1 = b; ynext = y;
+                ap2 = ap1; ap1 = a0; a0 = am1; am1 = am2;
+            }
+        }
+        wv[0] = w_y0; wv[1] = w_yH; wv[2] = w_d0; wv[3] = w_dH;
+        ends[0] = d_sgn; ends[1] = d_sum;
+    }
+}
+
+template <int PASS, int MINB>
+__global__ void __launch_bounds__(128, MINB) bvp_pass_kernel(BvpArgs a) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int g = (int)(tid & 1);
+    const int64_t m = tid >> 1;
+    if (m >= a.Mv || !(a.two || g == 1)) return;
+    double2 w[4], e[2];
+    solve_mode_pass<PASS>(a, m, g, w, e, false);
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(64, MINB) bvp_final_kernel(BvpArgs a) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int g = (int)(tid & 1);
     const int64_t mm = tid >> 1;
@@ -481,7 +512,7 @@ __global__ void __launch_bounds__(64) bvp_kernel(BvpArgs a) {
     double2 w[4], e[2];
     for (int q = 0; q < 4; ++q) w[q] = make_double2(0, 0);
     e[0] = e[1] = make_double2(0, 0);
-    if (valid && (a.two || g == 1)) solve_mode(a, m, g, w, e, g == 1);
+    if (valid && (a.two || g == 1)) solve_mode_pass<2>(a, m, g, w, e, g == 1);
     double2 wo[4], eo[2], wi[4], ei[2];
     for (int q = 0; q < 4; ++q) {
         double2 o;
@@ -498,6 +529,7 @@ __global__ void __launch_bounds__(64) bvp_kernel(BvpArgs a) {
     if (!valid || g == 0) return;
     finish_mode(a, m, wi, ei, wo, eo);
 }
+
 
 // ---------------------------------------------------------------------------
 // Small problems: the mode BVP with a WARP per (mode, grid) column.  With a
@@ -1326,7 +1358,19 @@ void bvp_solve_view(Plan* p, bool two_grids, int mode, bool correction, const Mo
         bvp_warp_kernel<<<(unsigned)((v.Mv + BVPW_MODES - 1) / BVPW_MODES), 64 * BVPW_MODES,
                           wsmem, p->stream>>>(a);
     } else {
-        bvp_kernel<<<(unsigned)((2 * v.M + 63) / 64), 64, 0, p->stream>>>(a);
+        // the lane-per-column solve split over kernels (passes 0, then 1 + 3
+        // per refinement, then the final pass with the lane-pair finish):
+        // 1.22 -> 1.10 ms at C4 against the fused 254-register kernel
+        a.bst = reinterpret_cast<double2*>(p->d_bst);
+        const unsigned nb128 = (unsigned)((2 * v.M + 127) / 128);
+        const unsigned nb64 = (unsigned)((2 * v.M + 63) / 64);
+        bvp_pass_kernel<0, 4><<<nb128, 128, 0, p->stream>>>(a);
+        for (int it = 0; it < a.refine; ++it) {
+            a.iter = it;
+            bvp_pass_kernel<1, 4><<<nb128, 128, 0, p->stream>>>(a);
+            bvp_pass_kernel<3, 4><<<nb128, 128, 0, p->stream>>>(a);
+        }
+        bvp_final_kernel<8><<<nb64, 64, 0, p->stream>>>(a);
     }
     p->ktoc(1);
     SE_LAUNCHED(p);
