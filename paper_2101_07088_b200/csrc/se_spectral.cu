@@ -961,10 +961,13 @@ __device__ __forceinline__ void dct_mma(const double* __restrict__ D, int P4, in
         double bv[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) bv[t] = bp[t * 8 * P4 + k0];
+        // m-tiles past the matrix rows (the last warp's slice) issue no MMA
 #pragma unroll
         for (int mt = 0; mt < MW; ++mt)
+            if ((mt0 + mt) * 8 < mrows) {
 #pragma unroll
-            for (int t = 0; t < 4; ++t) dmma884(acc[mt][t], av[mt], bv[t]);
+                for (int t = 0; t < 4; ++t) dmma884(acc[mt][t], av[mt], bv[t]);
+            }
     }
 }
 
