@@ -326,20 +326,42 @@ class ShardedSlabSolver:
         """Send each own charge to the rank owning its x slab (target) and to
         the neighbouring slabs within r_cut (halo source).  Returns the
         received (positions [ns][3], charges [ns], global indices of the
-        nt targets), targets first."""
+        nt targets), targets first.  One sort of the destination keys, one
+        row gather and one all-to-all: rows go out grouped by destination,
+        targets before halo copies, and the receiver concatenates the
+        senders' target blocks, then their halo blocks."""
         dev = pos_own.device
-        q = torch.as_tensor(self.system.charges[self.first:self.first + self.count],
-                            dtype=torch.float64, device=dev)
-        gidx = torch.arange(self.first, self.first + self.count, dtype=torch.float64,
-                            device=dev)
+        if getattr(self, "_qg", None) is None or self._qg.device != dev:
+            q = torch.as_tensor(self.system.charges[self.first:self.first + self.count],
+                                dtype=torch.float64, device=dev)
+            g = torch.arange(self.first, self.first + self.count, dtype=torch.float64,
+                             device=dev)
+            self._qg = torch.stack([q, g], dim=1)
+        if self.world == 1:                       # every charge is an own target
+            return (pos_own.contiguous(), self._qg[:, 0].contiguous(),
+                    self._qg[:, 1].to(torch.int64))
+        own = torch.cat([pos_own, self._qg], dim=1)                 # [count][5]
         ci, dest, tgt = cell_destinations(pos_own[:, 0], self.system.geometry.Lx,
                                           self.world, self.halo)
-        rows = torch.cat([pos_own[ci], q[ci, None], gidx[ci, None],
-                          tgt[:, None].to(torch.float64)], dim=1)
-        got = _exchange(rows, dest, self.world, self.group)
-        order = torch.argsort(-got[:, 5], stable=True)          # targets first
-        got = got[order]
-        nt = int((got[:, 5] > 0.5).sum().item())
+        key = dest * 2 + (~tgt).to(torch.int64)                     # (rank, halo?)
+        order = torch.argsort(key, stable=True)
+        rows = own.index_select(0, ci[order])
+        counts = torch.bincount(key, minlength=2 * self.world)
+        recv = torch.empty_like(counts)
+        dist.all_to_all_single(recv, counts, group=self.group)
+        sc = counts.view(self.world, 2).sum(1).tolist()
+        rc2 = recv.view(self.world, 2).tolist()
+        rc = [a + b for a, b in rc2]
+        got = torch.empty((sum(rc), 5), dtype=torch.float64, device=dev)
+        dist.all_to_all_single(got, rows, output_split_sizes=rc, input_split_sizes=sc,
+                               group=self.group)
+        blocks_t, blocks_h, off = [], [], 0
+        for nt_s, nh_s in rc2:
+            blocks_t.append(got[off:off + nt_s])
+            blocks_h.append(got[off + nt_s:off + nt_s + nh_s])
+            off += nt_s + nh_s
+        got = torch.cat(blocks_t + blocks_h)
+        nt = sum(b[0] for b in rc2)
         return (got[:, 0:3].contiguous(), got[:, 3].contiguous(),
                 got[:nt, 4].to(torch.int64))
 
@@ -347,6 +369,10 @@ class ShardedSlabSolver:
         """Near sums of this rank's targets -> the ranks holding those
         charges' index shards, in shard order ([4][count])."""
         dev = near_t.device
+        if self.world == 1:                       # targets are the shard, in order
+            out = torch.zeros((4, self.count), dtype=torch.float64, device=dev)
+            out[:, tgt_gidx - self.first] = near_t
+            return out
         firsts = torch.tensor([shard_range(self.system.charges.size, r, self.world)[0]
                                for r in range(self.world)], dtype=torch.int64, device=dev)
         dest = torch.searchsorted(firsts, tgt_gidx, right=True) - 1
