@@ -383,9 +383,13 @@ void phase_results(Plan* p, double* U, se_diag* diag) {
     int ovf = 0;
     SE_CUDA(cudaMemcpyAsync(&ovf, p->d_ovf_acc, sizeof(int), cudaMemcpyDeviceToHost, s));
     SE_CUDA(cudaStreamSynchronize(s));
+    p->last_overflow = ovf > 0;
     if (ovf > 0) {                  // lists overflowed: larger capacities next solve
         p->nl.grow *= 2;
+        // the graph is stale and the next solve allocates: it runs eagerly
+        // and a later one is captured
         if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; p->gkey = {}; }
+        p->gwarm = {};
     }
     p->timing = false;
     if (hflags & FLAG_Z_OUTSIDE) throw Error(SE_ERR_VALUE, "point outside the extended z domain");
@@ -685,7 +689,7 @@ void solve_core(Plan* p, const double* d_pos, int64_t n, uint32_t flags,
     phase_fields(p);
     phase_charges(p, d_pos, d_phi_out, d_E_out);
     phase_results(p, U, diag);
-    if (graph) p->gwarm = key;
+    if (graph && !p->last_overflow) p->gwarm = key;
 }
 
 void ensure_charges(Plan* p, int64_t n) {

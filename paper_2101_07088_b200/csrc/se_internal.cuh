@@ -330,6 +330,7 @@ struct Plan {
         }
     } gkey, gwarm;
     bool pair_hash = false;               // SE_PAIR_HASH on the solve in flight
+    bool last_overflow = false;           // the last solve's pair lists overflowed
     unsigned long long* d_phash = nullptr;   // [2][N] pair-set hash, count
     int64_t phash_cap = 0, phash_n = 0;
     double* d_partial = nullptr;          // reduction partials
