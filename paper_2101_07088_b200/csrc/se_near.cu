@@ -603,11 +603,16 @@ __device__ __forceinline__ void eval_list(const NearArgs& a, const double* tab, 
                                           int& count, unsigned long long& hs) {
     const double Lx = a.g.Lx, Ly = a.g.Ly;
     const bool nd = a.need_field;
-    for (int k = 0; k < n; k += 4) {
+    // far lists: two 16-byte groups per step (one 32-byte sector of the
+    // lane's list; 4.27 -> 4.22 ms); the close kernel keeps one (registers)
+    constexpr int STEP = FAR ? 8 : 4;
+    for (int k = 0; k < n; k += STEP) {
         const int4 j4 = *reinterpret_cast<const int4*>(list + k);
-        const int jj[4] = {j4.x, j4.y, j4.z, j4.w};
+        const int4 j5 = (STEP == 8 && k + 4 < n) ? *reinterpret_cast<const int4*>(list + k + 4)
+                                                 : make_int4(-1, -1, -1, -1);
+        const int jj[8] = {j4.x, j4.y, j4.z, j4.w, j5.x, j5.y, j5.z, j5.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < STEP; ++u) {
             if (jj[u] >= 0) {
                 const double4 sv = a.src[jj[u]];
                 double dx = __dsub_rn(px, sv.x), dy = __dsub_rn(py, sv.y);
