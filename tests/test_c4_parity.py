@@ -170,3 +170,15 @@ def test_graph_replay_through_list_overflow_c4d():
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_fp32_graph_replay_c4():
+    """fp32 mode through repeated host-API solves (warm, capture, replay)
+    at the C4 grid: every result within delta / 10 of the reference's."""
+    from paper_2101_07088_b200.slab import SlabSolver
+    g = _gold("c4n64k")
+    system, params = W.build("c4", N=65536)
+    solver = SlabSolver(system, params, precision="fp32")
+    for _ in range(3):
+        _check(solver.solve(), g, 0.1 * DELTA)
+    solver.close()
