@@ -659,15 +659,18 @@ __device__ __forceinline__ void eval_list_f32(const NearArgs& a, const double* t
     const float pxf = (float)wrap(px, a.g.Lx), pyf = (float)wrap(py, a.g.Ly);
     const float pzf = (float)(pz - a.g.zlo);
     const bool nd = a.need_field;
-    for (int k = 0; k < n; k += 4) {
+    constexpr int STEP = FAR ? 8 : 4;     // far lists: two int4 groups per step
+    for (int k = 0; k < n; k += STEP) {
         const int4 j4 = *reinterpret_cast<const int4*>(list + k);
-        const int jj[4] = {j4.x, j4.y, j4.z, j4.w};
+        const int4 j5 = (STEP == 8 && k + 4 < n) ? *reinterpret_cast<const int4*>(list + k + 4)
+                                                 : make_int4(-1, -1, -1, -1);
+        const int jj[8] = {j4.x, j4.y, j4.z, j4.w, j5.x, j5.y, j5.z, j5.w};
         if (FAR) {
-            // far pairs: the group's four terms summed in fp32 (each term is
-            // an fp32 evaluation already), one fp64 add per group and field
+            // far pairs: the step's terms summed in fp32 (each term is an
+            // fp32 evaluation already), one fp64 add per step and field
             float gphi = 0.f, gex = 0.f, gey = 0.f, gez = 0.f;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < STEP; ++u) {
                 const int j = jj[u];
                 if (j < 0) continue;
                 const float4 f = a.srcf[j];
