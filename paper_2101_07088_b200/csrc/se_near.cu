@@ -553,23 +553,29 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_scan_kernel(NearArgs a)
                 while (__any_sync(0xffffffffu, jj < ee)) {
                     // branch-free candidate tests: out-of-window slots read a
                     // stage entry past the window (padded) and are masked; a
-                    // hit is pushed with one predicated store into the far or
-                    // close queue
+                    // hit is pushed with one predicated shared store into the
+                    // far or close queue
+                    const float4* sp = &stage[wib][jj - c0];
+                    int* const pf = &qf[wib][qn][lane];
+                    int* const pc = &qcl[wib][qc][lane];
+                    int nfh = 0, nch = 0;
 #pragma unroll
                     for (int u = 0; u < SU; ++u) {
                         const int q = jj + u;
-                        const float4 f = stage[wib][q - c0];
+                        const float4 f = sp[u];
                         float dx = qx - f.x, dy = qy - f.y, dz = pzf - f.z;
                         if (SMALL && cw.allx) dx -= a.Lxf * rintf(dx * a.iLxf);
                         if (SMALL && cw.ally) dy -= a.Lyf * rintf(dy * a.iLyf);
                         const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                         const bool hit = q < ee && r2 <= r2f;
                         const bool far = r2 > r2c;
-                        int* slot = far ? &qf[wib][qn][lane] : &qcl[wib][qc][lane];
-                        if (hit) *slot = q;
-                        qn += (hit && far) ? 1 : 0;
-                        qc += (hit && !far) ? 1 : 0;
+                        int* const dst = far ? pf + 32 * nfh : pc + 32 * nch;
+                        if (hit) *dst = q;
+                        nfh += (hit && far) ? 1 : 0;
+                        nch += (hit && !far) ? 1 : 0;
                     }
+                    qn += nfh;
+                    qc += nch;
                     jj = min(jj + SU, eec);
                     if (__any_sync(0xffffffffu, qn >= SCAN_Q)) flush(qf[wib], qn, nf, lfar, a.cap_far, false);
                     if (__any_sync(0xffffffffu, qc >= SCAN_Q)) flush(qcl[wib], qc, nc, lcls, a.cap_close, false);
