@@ -1029,8 +1029,9 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
     if (((uint64_t)nbins << zb) >> 32)
         throw Error(SE_ERR_VALUE, "grid too large for the interpolation sort keys");
     ensure_sources(p, n);               // key / permutation / sort scratch (>= 3n)
-    const int ig = 4;                   // charges per group (measured best of 2, 3, 4, 8;
-                                        // fp32 mode 8: 4.39 vs 3.62 ms)
+    // charges per group: 5 (round 2: fp64 3.51 ms vs 3.90 with 4 and 4.01
+    // with 6; fp32 2.68 vs 2.82 / 3.08; round 1 measured 2, 3, 4, 8)
+    const int ig = 5;
     const int64_t gcap = count / ig + nbins + 1;
     if (nbins + 1 > p->iseg_cap || gcap > p->igroup_cap) {
         dfree(p, p->d_iseg); dfree(p, p->d_igroups); dfree(p, p->d_ingroups);
@@ -1090,18 +1091,18 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
         kern<<<blocks, iw * 32, sm, p->stream>>>(args);
     };
     // fp32 mode: 3 CTAs / SM (80 registers, no spills; the per-charge data
-    // lives in shared memory): 2.99 vs 3.62 ms at 2 CTAs.  fp64 keeps 16
-    // warps / SM (120 registers) in 4-warp CTAs (3.93 vs 4.01 ms with
-    // 8-warp CTAs): capped at 80 registers it spills (4.28-4.38 ms), at 96
-    // (20 warps) it runs 4.24 ms, and 3-charge groups fit but load more
-    // (4.77 ms)
+    // lives in shared memory): 2.99 vs 3.62 ms at 2 CTAs (4-charge groups).
+    // fp64: 4-warp CTAs at 125 registers, 16 warps / SM (4-charge groups:
+    // 3.93 vs 4.01 ms with 8-warp CTAs; capped at 80 registers they spilled,
+    // 4.28-4.38 ms).  z weight rows padded to 8 for 16-byte loads: 4.27 vs
+    // 3.51 ms (130 registers, 12 warps / SM)
     if (p->g32) {
-        if (forces) go(interp_kernel<4, 4, 3, 2, float>, a32);
-        else go(interp_kernel<1, 4, 3, 2, float>, a32);
+        if (forces) go(interp_kernel<4, 5, 3, 2, float>, a32);
+        else go(interp_kernel<1, 5, 3, 2, float>, a32);
     } else if (forces) {
-        go(interp_kernel<4, 4, 4, 2, double, 4>, a, 4);
+        go(interp_kernel<4, 5, 3, 2, double, 4>, a, 4);
     } else {
-        go(interp_kernel<1, 4, 4, 2, double, 4>, a, 4);
+        go(interp_kernel<1, 5, 3, 2, double, 4>, a, 4);
     }
     p->ktoc(2);
     SE_LAUNCHED(p);
