@@ -188,25 +188,26 @@ struct Solve {
 // exp(-u) for 0 <= u <= 700 without the special-case paths of libm exp:
 // Cody-Waite reduction by ln2, a degree-10 polynomial on |r| <= ln2/2
 // (Chebyshev interpolant in monomial form, 4.5e-16 relative including the
-// Horner rounding), scaling by 2^n through the exponent bits.
+// Horner rounding), scaling by 2^n through the exponent bits.  n is rounded
+// by the 1.5 x 2^52 shifter (its low word is n), so no FRND / F2I.F64, and
+// the coefficients sit in constant memory, so each DFMA takes its operand
+// from the constant bank (immediates cost two UMOVs per DFMA).
+static __constant__ double kExpNegC[13] = {
+    2.7626357241447223e-07, 2.764018079620985e-06, 2.4801504346997686e-05,
+    1.9841170270440067e-04, 1.3888888932488599e-03, 8.333333385667782e-03,
+    4.166666666657314e-02,  1.6666666666554406e-01, 5.000000000000006e-01,
+    1.0000000000000067,     1.0,
+    -6.93147180369123816490e-01, -1.90821492927058770002e-10};   // -ln2 hi, lo
 __device__ __forceinline__ double exp_neg(double u) {
     const double v = -u;
-    const double n = rint(v * 1.4426950408889634);
-    double r = fma(n, -6.93147180369123816490e-01, v);   // ln2 hi
-    r = fma(n, -1.90821492927058770002e-10, r);          // ln2 lo
-    double p = 2.7626357241447223e-07;
-    p = fma(p, r, 2.764018079620985e-06);
-    p = fma(p, r, 2.4801504346997686e-05);
-    p = fma(p, r, 1.9841170270440067e-04);
-    p = fma(p, r, 1.3888888932488599e-03);
-    p = fma(p, r, 8.333333385667782e-03);
-    p = fma(p, r, 4.166666666657314e-02);
-    p = fma(p, r, 1.6666666666554406e-01);
-    p = fma(p, r, 5.000000000000006e-01);
-    p = fma(p, r, 1.0000000000000067);
-    p = fma(p, r, 1.0);
-    const long long bits = (long long)(1023 + (int)n) << 52;
-    return p * __longlong_as_double(bits);
+    const double sh = fma(v, 1.4426950408889634, 6755399441055744.0);
+    const double n = sh - 6755399441055744.0;
+    double r = fma(n, kExpNegC[11], v);
+    r = fma(n, kExpNegC[12], r);
+    double p = kExpNegC[0];
+#pragma unroll
+    for (int j = 1; j < 11; ++j) p = fma(p, r, kExpNegC[j]);
+    return p * __hiloint2double((1023 + __double2loint(sh)) << 20, 0);
 }
 
 // Gaussian stencil weight exp(-(d/w)^2 / 2) / norm with the reciprocals
