@@ -926,17 +926,19 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 
 struct DctArgs {
     int n, Pe, Po, P8, P4;       // Nz, parity sizes, padded rows / k
+    int tmap;                    // warp -> (parity, tiles) map (zdct_fwd_kernel)
     int64_t W;                   // real columns per row
     const double* De; const double* Do;    // [P8][P4] row-major, zero padded
 };
 
-// C[mt0*8 + 0:MW*8][0:DCT_COLS] = D[rows][k] * S[k][cols] for this warp's
+// C[tile rows][0:DCT_COLS] = D[rows][k] * S[k][cols] for this warp's 8-row
+// tiles mt0 + ts * i (i < MW)
 // parity and half of the row tiles: per k step MW A fragments (global, L2
 // resident matrix; prefetched one step ahead) and 4 B fragments (shared)
 // feed 4 MW DMMAs.
 template <int MW>
 __device__ __forceinline__ void dct_mma(const double* __restrict__ D, int P4, int mrows,
-                                        const double* __restrict__ Sc, int lane, int mt0,
+                                        const double* __restrict__ Sc, int lane, int mt0, int ts,
                                         double (&acc)[MW][4][2]) {
 #pragma unroll
     for (int mt = 0; mt < MW; ++mt)
@@ -945,10 +947,11 @@ __device__ __forceinline__ void dct_mma(const double* __restrict__ D, int P4, in
     const int ar = lane >> 2, ak = lane & 3;
     const double* bp = Sc + ar * P4 + ak;                    // column-major [col][k]
     const double* ap = D + (mt0 * 8 + ar) * P4 + ak;
+    const int rs = ts * 8 * P4;                                // row stride between tiles
     double an[MW];
 #pragma unroll
     for (int mt = 0; mt < MW; ++mt)
-        an[mt] = (mt0 + mt) * 8 < mrows ? __ldg(ap + (mt * 8) * P4) : 0.0;
+        an[mt] = (mt0 + ts * mt) * 8 < mrows ? __ldg(ap + mt * rs) : 0.0;
     for (int k0 = 0; k0 < P4; k0 += 4) {
         double av[MW];
 #pragma unroll
@@ -956,7 +959,7 @@ __device__ __forceinline__ void dct_mma(const double* __restrict__ D, int P4, in
         if (k0 + 4 < P4) {
 #pragma unroll
             for (int mt = 0; mt < MW; ++mt)
-                an[mt] = (mt0 + mt) * 8 < mrows ? __ldg(ap + (mt * 8) * P4 + k0 + 4) : 0.0;
+                an[mt] = (mt0 + ts * mt) * 8 < mrows ? __ldg(ap + mt * rs + k0 + 4) : 0.0;
         }
         double bv[4];
 #pragma unroll
@@ -964,7 +967,7 @@ __device__ __forceinline__ void dct_mma(const double* __restrict__ D, int P4, in
         // m-tiles past the matrix rows (the last warp's slice) issue no MMA
 #pragma unroll
         for (int mt = 0; mt < MW; ++mt)
-            if ((mt0 + mt) * 8 < mrows) {
+            if ((mt0 + ts * mt) * 8 < mrows) {
 #pragma unroll
                 for (int t = 0; t < 4; ++t) dmma884(acc[mt][t], av[mt], bv[t]);
             }
@@ -1010,13 +1013,18 @@ __global__ void __launch_bounds__(256, 2) zdct_fwd_kernel(DctArgs a, const TIn* 
     }
     __syncthreads();
     constexpr int MW = (MT + 3) / 4;
-    const int par = warp >> 2, mt0 = (warp & 3) * MW;
+    // tmap 1: warp w takes parity w & 1 and the tiles w / 2 + 4 i, so the
+    // two warps on each SM sub-partition (w, w + 4) share its DMMA unit with
+    // balanced tile counts (9 / 9 / 8 / 8 of the 34 at Nz = 258, where the
+    // contiguous split (tmap 0) gives 10 / 10 / 10 / 4)
+    const int par = a.tmap ? (warp & 1) : (warp >> 2);
+    const int mt0 = a.tmap ? (warp >> 1) : (warp & 3) * MW, ts = a.tmap ? 4 : 1;
     const int rows = par ? a.Po : a.Pe;
     double acc[MW][4][2];
-    dct_mma<MW>(par ? a.Do : a.De, a.P4, a.P8, par ? So : Se, lane, mt0, acc);
+    dct_mma<MW>(par ? a.Do : a.De, a.P4, a.P8, par ? So : Se, lane, mt0, ts, acc);
 #pragma unroll
     for (int mt = 0; mt < MW; ++mt) {
-        const int i = (mt0 + mt) * 8 + (lane >> 2);
+        const int i = (mt0 + ts * mt) * 8 + (lane >> 2);
         if (i >= rows) continue;
         const int64_t row = 2 * (int64_t)i + par;
 #pragma unroll
@@ -1082,15 +1090,16 @@ __global__ void __launch_bounds__(256, 2) zdct_inv_kernel(DctArgs a, AsmArgs2 q,
     }
     __syncthreads();
     constexpr int MW = (MT + 3) / 4;
-    const int par = warp >> 2, mt0 = (warp & 3) * MW;
+    const int par = a.tmap ? (warp & 1) : (warp >> 2);
+    const int mt0 = a.tmap ? (warp >> 1) : (warp & 3) * MW, ts = a.tmap ? 4 : 1;
     double acc[MW][4][2];
-    dct_mma<MW>(par ? a.Do : a.De, a.P4, a.P8, par ? Co : Ce, lane, mt0, acc);
+    dct_mma<MW>(par ? a.Do : a.De, a.P4, a.P8, par ? Co : Ce, lane, mt0, ts, acc);
     __syncthreads();                                   // coefficients consumed
     // E (par 0) / O (par 1) node halves back to shared memory, row-major
     double* EO = sm;                                   // [2][P8][DCT_COLS]
 #pragma unroll
     for (int mt = 0; mt < MW; ++mt) {
-        const int j = (mt0 + mt) * 8 + (lane >> 2);
+        const int j = (mt0 + ts * mt) * 8 + (lane >> 2);
         if (j >= a.P8) continue;
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -1255,6 +1264,11 @@ static DctArgs dct_args(Plan* p, const double* mats, int64_t W) {
     a.n = p->Nz; a.Pe = (p->Nz + 1) / 2; a.Po = p->Nz / 2;
     a.P8 = p->dct_p8; a.P4 = p->dct_p4; a.W = W;
     a.De = mats; a.Do = mats + (size_t)a.P8 * a.P4;
+    static const int tmap = [] {
+        const char* e = std::getenv("SE_DCT_TMAP");
+        return e ? std::atoi(e) : 1;
+    }();
+    a.tmap = tmap;
     return a;
 }
 
