@@ -185,7 +185,7 @@ struct Solve {
     bool near_forked = false;
 };
 
-// exp(-u) for 0 <= u <= 700 without the special-case paths of libm exp:
+// exp(-u) for |u| <= 700 without the special-case paths of libm exp:
 // Cody-Waite reduction by ln2, a degree-10 polynomial on |r| <= ln2/2
 // (Chebyshev interpolant in monomial form, 4.5e-16 relative including the
 // Horner rounding), scaling by 2^n through the exponent bits.  n is rounded

@@ -1129,8 +1129,11 @@ __global__ void __launch_bounds__(256, 2) zdct_inv_kernel(DctArgs a, AsmArgs2 q,
         }
         if (q.corr && q.sel[m] && j >= q.w0 && j < q.w1) {
             const double k = q.kmag[m], z = q.z[j];
-            const double e1 = exp(-k * z), e2 = exp(k * (z - q.H));
-            const double e3 = exp(-k * (q.H + z)), e4 = exp(k * (z - 2.0 * q.H));
+            // exp(-u) by exp_neg (valid for |u| <= 700; clamped: beyond it the
+            // terms are < 1e-304 of the others) instead of libm exp
+            auto ex = [](double u) { return exp_neg(fmin(fmax(u, -700.0), 700.0)); };
+            const double e1 = ex(k * z), e2 = ex(k * (q.H - z));
+            const double e3 = ex(k * (q.H + z)), e4 = ex(k * (2.0 * q.H - z));
             const double pb = (q.rt + 1.0) * e1 - (q.rt - 1.0) * e4;
             const double pt = -(q.rb + 1.0) * e2 + (q.rb - 1.0) * e3;
             const double db = -k * ((q.rt + 1.0) * e1 + (q.rt - 1.0) * e4);
