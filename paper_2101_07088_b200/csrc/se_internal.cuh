@@ -113,7 +113,7 @@ struct SourceSet {
 // near field cell list
 // ----------------------------------------------------------------------------
 struct CellList {
-    int ncx = 0, ncy = 0, ncz = 0;
+    int ncx = 0, ncy = 0, ncz = 0, hw = 2;   // hw: neighbour columns each side
     double csx = 0, csy = 0, csz = 0, zlo = 0;
     int64_t n = 0;
     int* start = nullptr;        // [ncells + 1]

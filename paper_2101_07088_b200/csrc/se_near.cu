@@ -37,9 +37,10 @@ constexpr double TWO_OVER_SQRTPI = 1.1283791670955126;   // 2/sqrt(pi)
 // ---------------------------------------------------------------------------
 // cell list
 // ---------------------------------------------------------------------------
-// xy columns of width >= r/2 (r = max query radius), z bins of ~r/16
+// xy columns of width >= r/hw (r = max query radius; hw neighbour columns
+// each side), z bins of ~r/16
 struct CellGeo {
-    int ncx, ncy, ncz;
+    int ncx, ncy, ncz, hw;
     double csx, csy, csz, zlo, Lx, Ly;
 };
 
@@ -434,22 +435,24 @@ constexpr int SCAN_STAGE = 128;             // staged candidates per warp
 // in one of them: columns whose xy distance to the target exceeds the query
 // radius are skipped, and the z window is the chord sqrt(r^2 - d_xy^2).
 struct ColumnWalk {
-    int nxr, nyr;          // columns visited per axis (5, or all when fewer)
+    int nxr, nyr;          // columns visited per axis (2 hw + 1, or all when fewer)
     bool allx, ally;
 };
 
 __device__ __forceinline__ ColumnWalk column_walk(const CellGeo& g) {
     ColumnWalk w;
-    w.allx = g.ncx < 5; w.ally = g.ncy < 5;
-    w.nxr = w.allx ? g.ncx : 5; w.nyr = w.ally ? g.ncy : 5;
+    const int nw = 2 * g.hw + 1;
+    w.allx = g.ncx < nw; w.ally = g.ncy < nw;
+    w.nxr = w.allx ? g.ncx : nw; w.nyr = w.ally ? g.ncy : nw;
     return w;
 }
 
 // neighbour column (i) of target column c along one axis: wrapped index, the
 // shift that brings its sources next to the target, and the fp32 distance
 // from the target coordinate p to the column's interval
-__device__ __forceinline__ void column_axis(int c, int i, bool all, int n, float cs, float L,
-                                           float p, int* idx, float* shift, float* dist) {
+__device__ __forceinline__ void column_axis(int c, int i, bool all, int n, int hw, float cs,
+                                           float L, float p, int* idx, float* shift,
+                                           float* dist) {
     if (all) {                         // every column once, periodic distance
         *idx = i; *shift = 0.f;
         const float lo = i * cs, hi = lo + cs;
@@ -459,7 +462,7 @@ __device__ __forceinline__ void column_axis(int c, int i, bool all, int n, float
         *dist = d;
         return;
     }
-    const int u = c + i - 2;
+    const int u = c + i - hw;
     int w = u; float sh = 0.f;
     if (w < 0) { w += n; sh = -L; } else if (w >= n) { w -= n; sh = L; }
     *idx = w; *shift = sh;
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_scan_kernel(NearArgs a)
     }
     const int cx = col % a.g.ncx, cy = col / a.g.ncx;
     ColumnWalk cw = column_walk(a.g);
-    if (!SMALL) { cw.allx = cw.ally = false; cw.nxr = cw.nyr = 5; }
+    if (!SMALL) { cw.allx = cw.ally = false; cw.nxr = cw.nyr = 2 * a.g.hw + 1; }
     const float r2f = a.r2f, r2c = a.r2close;
     const float csxf = (float)a.g.csx, csyf = (float)a.g.csy, icsz = (float)(1.0 / a.g.csz);
     const int nzb = a.g.ncz;
@@ -518,10 +521,10 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_scan_kernel(NearArgs a)
     };
     for (int iy = 0; iy < cw.nyr; ++iy) {
         int yc; float sy, dyd;
-        column_axis(cy, iy, cw.ally, a.g.ncy, csyf, a.Lyf, pyf, &yc, &sy, &dyd);
+        column_axis(cy, iy, cw.ally, a.g.ncy, a.g.hw, csyf, a.Lyf, pyf, &yc, &sy, &dyd);
         for (int ix = 0; ix < cw.nxr; ++ix) {
             int xc; float sx, dxd;
-            column_axis(cx, ix, cw.allx, a.g.ncx, csxf, a.Lxf, pxf, &xc, &sx, &dxd);
+            column_axis(cx, ix, cw.allx, a.g.ncx, a.g.hw, csxf, a.Lxf, pxf, &xc, &sx, &dxd);
             const float d2 = fmaf(dxd, dxd, dyd * dyd);
             int j = 0, e = 0;
             if (live && d2 <= r2f) {
@@ -900,10 +903,10 @@ __global__ void __launch_bounds__(NB_THREADS, MINB) near_fused_kernel(NearArgs a
     const unsigned below = (1u << lane) - 1u;
     for (int iy = 0; iy < cw.nyr; ++iy) {
         int yc; float sy, dyd;
-        column_axis(cy, iy, cw.ally, a.g.ncy, csyf, a.Lyf, pyf, &yc, &sy, &dyd);
+        column_axis(cy, iy, cw.ally, a.g.ncy, a.g.hw, csyf, a.Lyf, pyf, &yc, &sy, &dyd);
         for (int ix = 0; ix < cw.nxr; ++ix) {
             int xc; float sx, dxd;
-            column_axis(cx, ix, cw.allx, a.g.ncx, csxf, a.Lxf, pxf, &xc, &sx, &dxd);
+            column_axis(cx, ix, cw.allx, a.g.ncx, a.g.hw, csxf, a.Lxf, pxf, &xc, &sx, &dxd);
             const float d2 = fmaf(dxd, dxd, dyd * dyd);
             if (d2 > r2f) continue;
             const float hz = sqrtf(r2f - d2) * 1.0001f + a.zmarg;
@@ -1002,10 +1005,10 @@ __global__ void __launch_bounds__(256) near_few_kernel(NearArgs a) {
     const double Lx = a.g.Lx, Ly = a.g.Ly;
     for (int iy = 0; iy < cw.nyr; ++iy) {
         int yc; float sy, dyd;
-        column_axis(cy, iy, cw.ally, a.g.ncy, csyf, a.Lyf, pyf, &yc, &sy, &dyd);
+        column_axis(cy, iy, cw.ally, a.g.ncy, a.g.hw, csyf, a.Lyf, pyf, &yc, &sy, &dyd);
         for (int ix = 0; ix < cw.nxr; ++ix) {
             int xc; float sx, dxd;
-            column_axis(cx, ix, cw.allx, a.g.ncx, csxf, a.Lxf, pxf, &xc, &sx, &dxd);
+            column_axis(cx, ix, cw.allx, a.g.ncx, a.g.hw, csxf, a.Lxf, pxf, &xc, &sx, &dxd);
             const float d2 = fmaf(dxd, dxd, dyd * dyd);
             if (d2 > a.r2f) continue;
             const float hz = sqrtf(a.r2f - d2) * 1.0001f + a.zmarg;
@@ -1202,7 +1205,7 @@ __global__ void sum_partials_kernel(const double* partial, int nb, double scale,
 // ---------------------------------------------------------------------------
 static CellGeo cell_geo(const Plan* p, const CellList& cl) {
     CellGeo g;
-    g.ncx = cl.ncx; g.ncy = cl.ncy; g.ncz = cl.ncz;
+    g.ncx = cl.ncx; g.ncy = cl.ncy; g.ncz = cl.ncz; g.hw = cl.hw;
     g.csx = cl.csx; g.csy = cl.csy; g.csz = cl.csz; g.zlo = cl.zlo;
     g.Lx = p->P.Lx; g.Ly = p->P.Ly;
     return g;
@@ -1282,8 +1285,16 @@ void build_cells(Plan* p, const double* d_pos, const double* d_q, int64_t n, boo
         for (int b = 0; b < nblk; ++b) { zmin = std::min(zmin, mm[2 * b]); zmax = std::max(zmax, mm[2 * b + 1]); }
     }
     const double rc = std::max(p->P.r_cut, p->P.r_nf);
-    cl.ncx = std::max(1, (int)std::floor(p->P.Lx / (0.5 * rc)));
-    cl.ncy = std::max(1, (int)std::floor(p->P.Ly / (0.5 * rc)));
+    // xy columns of r_c / 2 (5 x 5 walk).  r_c / 3 (7 x 7): scan 2.59 ->
+    // 2.44 ms but the evaluation 4.13 -> 4.25 ms (its lanes' list walks
+    // drift apart, fewer shared source lines in L1); r_c / 4: 7.2 ms in all
+    static const int cdiv = [] {
+        const char* e = std::getenv("SE_CELL_XYDIV");
+        return e ? std::max(2, std::atoi(e)) : 2;
+    }();
+    cl.hw = cdiv;
+    cl.ncx = std::max(1, (int)std::floor(p->P.Lx / (rc / cdiv)));
+    cl.ncy = std::max(1, (int)std::floor(p->P.Ly / (rc / cdiv)));
     cl.csx = p->P.Lx / cl.ncx;
     cl.csy = p->P.Ly / cl.ncy;
     cl.zlo = zmin - rc;
@@ -1702,7 +1713,7 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         // measured best of queue 8..24, step 4 / 8, 6..12 CTAs (3.17 vs 3.29 ms at 10)
         // (round 2, branch-free tests: queue 8 / 16 / 24, step 4 / 8, 6..8
         // CTAs all within 2.68-2.78 ms)
-        if (cl.ncx < 5 || cl.ncy < 5)
+        if (cl.ncx < 2 * cl.hw + 1 || cl.ncy < 2 * cl.hw + 1)
             near_scan_kernel<16, 4, 7, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         else
             near_scan_kernel<16, 4, 7, false><<<nblk, NB_THREADS, 0, p->stream>>>(a);
