@@ -171,34 +171,36 @@ __global__ void __launch_bounds__(STENCIL_TB) stencil_kernel(StencilArgs a) {
         a.st.owner[i] = a.owner_in[s];
     }
     const int nvalid = __syncthreads_count(valid);
-    const int SX = 2 * a.mx + 1, SY = 2 * a.my + 1;
-    // half a warp per record: lanes over its elements, records in turn
+    const int SX = 2 * a.mx + 1, SXY = SX + 2 * a.my + 1;
+    // half a warp per record: lanes over its elements, records in turn; the
+    // record's scalars are read once per record, not per element
     const int h = t >> 4, hl = t & 15;
-    for (int r = h; r < nvalid; r += STENCIL_TB / 16)
-    for (int c = hl; c < rs; c += 16) {
-        double* out = a.st.rec + (i0 + r) * rs;
-        // one converged Gaussian per element: x / y offsets select their
-        // axis, z elements their node (|delta| <= r (1 + 1e-12) on x / y)
-        double pos, node, lim;
-        bool ok = true;
-        if (c < SX + SY) {
-            const bool y = c >= SX;
-            const int o = y ? c - SX : c;
-            const int j = y ? sjy[r] : sjx[r];
-            pos = y ? sy[r] : sx[r];
-            node = __dmul_rn((double)(j + o - (y ? a.my : a.mx)), y ? a.hy : a.hx);
-            lim = a.rad_keep;
-        } else {
-            const int tt = c - SX - SY, k = slo[r] + tt;
-            ok = tt < a.wz && k < shi[r] && k < a.Nz;
-            pos = sz[r];
-            node = ok ? a.znodes[k] : 0.0;
-            lim = a.rad;
+    const double hx = a.hx, hy = a.hy, rk = a.rad_keep, rz = a.rad;
+    const double iw = a.inv_width, inrm = a.inv_norm;
+    const int wz = a.wz, Nz = a.Nz;
+    double* const rec0 = a.st.rec + i0 * rs;
+    for (int r = h; r < nvalid; r += STENCIL_TB / 16) {
+        const double px = sx[r], py = sy[r], pz = sz[r];
+        const int bx = sjx[r] - a.mx, by = sjy[r] - a.my - SX, lo = slo[r] - SXY;
+        const int zend = min(min(shi[r], Nz), slo[r] + wz) + SXY;   // element bound of z
+        double* const out = rec0 + (int64_t)r * rs;
+        for (int c = hl; c < rs; c += 16) {
+            // one converged Gaussian per element: x / y offsets select their
+            // axis, z elements their node (|delta| <= r (1 + 1e-12) on x / y)
+            double d, lim;
+            bool ok = true;
+            if (c < SXY) {
+                const bool y = c >= SX;
+                const double node = __dmul_rn((double)((y ? by : bx) + c), y ? hy : hx);
+                d = __dsub_rn(y ? py : px, node);
+                lim = rk;
+            } else {
+                ok = c < zend;
+                d = __dsub_rn(pz, ok ? a.znodes[lo + c] : 0.0);
+                lim = rz;
+            }
+            out[c] = (ok && fabs(d) <= lim) ? gauss_w(d, iw, inrm) : 0.0;
         }
-        const double d = __dsub_rn(pos, node);
-        double w = 0.0;
-        if (ok && fabs(d) <= lim) w = gauss_w(d, a.inv_width, a.inv_norm);
-        out[c] = w;
     }
 }
 
