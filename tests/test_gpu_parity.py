@@ -570,6 +570,28 @@ def test_both_near_field_paths_against_goldens(fused):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("layout", ["xy3", "xy4_z8", "tmap0"])
+def test_alternative_layouts_against_goldens(layout):
+    """The measured-and-kept-off layout switches stay correct: near-field
+    columns of r_c / 3 or r_c / 4 (7 x 7 / 9 x 9 column walks), z bins of
+    r_c / 8, and the contiguous DCT warp-tile map, on the list path, against
+    the goldens and the exact pair count (env switches are read once per
+    process, hence the subprocess)."""
+    import subprocess
+    import sys
+    extra = {"xy3": {"SE_CELL_XYDIV": "3"},
+             "xy4_z8": {"SE_CELL_XYDIV": "4", "SE_CELL_ZDIV": "8"},
+             "tmap0": {"SE_DCT_TMAP": "0"}}[layout]
+    env = dict(os.environ, SE_NEAR_FUSED="0", **extra)
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x",
+                        os.path.join(here, "test_gpu_parity.py"), "-k",
+                        "workloads_against_golden or pair_count or variants_against_golden"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_graph_replay_matches_direct_solve():
     """SE_GRAPH: the warm solve, the capture and the replays give the same
     results as direct solves, also after the positions change in place."""
