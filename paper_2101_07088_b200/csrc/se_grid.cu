@@ -1097,10 +1097,11 @@ void interp_charges(Plan* p, int64_t n, int64_t first, int64_t count, bool force
     // fp64: 4-warp CTAs at 125 registers, 16 warps / SM (4-charge groups:
     // 3.93 vs 4.01 ms with 8-warp CTAs; capped at 80 registers they spilled,
     // 4.28-4.38 ms).  z weight rows padded to 8 for 16-byte loads: 4.27 vs
-    // 3.51 ms (130 registers, 12 warps / SM)
+    // 3.51 ms (130 registers, 12 warps / SM); 2-warp CTAs: 3.61 ms
     if (p->g32) {
-        if (forces) go(interp_kernel<4, 5, 3, 2, float>, a32);
-        else go(interp_kernel<1, 5, 3, 2, float>, a32);
+        // 4-warp CTAs, 6 per SM: 2.66 vs 2.67 ms for 8-warp CTAs, 3 per SM
+        if (forces) go(interp_kernel<4, 5, 6, 2, float, 4>, a32, 4);
+        else go(interp_kernel<1, 5, 6, 2, float, 4>, a32, 4);
     } else if (forces) {
         go(interp_kernel<4, 5, 3, 2, double, 4>, a, 4);
     } else {
