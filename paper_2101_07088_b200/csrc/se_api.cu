@@ -835,7 +835,7 @@ int se_plan_create(const se_params* params, const double* z_nodes, const double*
         // the fp64 grids and their cuFFT plans come with the first fp64
         // solve (ensure_grid64), the fp32 ones with the first fp32 solve
         p->d_ext = dalloc<cufftDoubleComplex>(p, (size_t)nz * 2 * p->M);
-        p->d_scr = dalloc<cufftDoubleComplex>(p, 6 * (size_t)nz * p->M);
+        p->d_scr = dalloc<cufftDoubleComplex>(p, 4 * (size_t)nz * p->M);   // A, B columns
         p->d_bst = dalloc<cufftDoubleComplex>(p, 12 * (size_t)p->M);
         p->d_mom = dalloc<cufftDoubleComplex>(p, 2 * (size_t)p->M);
         p->d_mism = dalloc<cufftDoubleComplex>(p, 4 * (size_t)p->M);

@@ -346,7 +346,7 @@ struct Plan {
     int dct_p8 = 0, dct_p4 = 0;           // padded parity block (8-row tiles, k by 4)
     cufftDoubleComplex* d_spec = nullptr; // [Nz][4][M]
     double* d_fields = nullptr;           // [Nz][4][Nx][Ny]
-    cufftDoubleComplex* d_scr = nullptr;  // BVP scratch [3][Nz][M]
+    cufftDoubleComplex* d_scr = nullptr;  // BVP scratch [2][Nz][2][M] (y'', Thomas d / x)
     cufftDoubleComplex* d_bst = nullptr;  // split BVP column state [6][2][M]
     bool keep_stages = false;
     cufftDoubleComplex* d_keep = nullptr; // [Nz][2][M] psi coefficients (debug)

@@ -129,7 +129,7 @@ struct BvpArgs {
     const double* tw0; const double* twH;
     const double2* sbh; const double2* sth;
     double2* ext;                // [2N][2][M] in: raw DCT, out: iDCT inputs
-    double2* scrF; double2* scrA; double2* scrB;   // [Nz][M] each
+    double2* scrA; double2* scrB;   // [Nz][2][M] each
     double2* bst;                // split kernels: [6][2][M] c0, c1, deferred dc0, dc1, r2
     int iter;                    // split kernels: the refinement iteration
     double inv_nxy;
@@ -216,8 +216,9 @@ __device__ __forceinline__ void finish_mode(const BvpArgs& a, int64_t m, const d
 // The per-mode solve, one thread per (mode, grid) column, split over kernels
 // so each holds only its own pass's registers (one fused kernel needed 254
 // registers and 8 warps / SM; split: 1.22 -> 1.10 ms at C4).  Scratch
-// columns (row stride 2M of [Nz][2][M]): F = f_sc, A = y'' (ypp), B = Thomas
-// d / x; the column state -- c0, c1, the refinement's Schur rhs r2 and the
+// columns (row stride 2M of [Nz][2][M]): A = y'' (ypp), B = Thomas d / x
+// (the scaled rhs f_sc is re-derived from the raw DCT column where needed:
+// 1.10 -> 1.06 ms against keeping a third column); the column state -- c0, c1, the refinement's Schur rhs r2 and the
 // deferred last update dc -- is carried in a.bst between the kernels:
 //   pass 0: forward sweep + descend -> c (or the k = 0 solve, bvp.py:281-296);
 //   pass 1: a refinement's forward pass (the first materialises y'' as it
@@ -234,7 +235,6 @@ __device__ __forceinline__ void solve_mode_pass(const BvpArgs& a, int64_t m, int
     const int n = a.Nz;
     const int64_t M = a.M, RS = 2 * M;
     const double2* __restrict__ raw = a.ext + g * M + m;
-    double2* __restrict__ F = a.scrF + g * M + m;
     double2* __restrict__ A = a.scrA + g * M + m;
     double2* __restrict__ B = a.scrB + g * M + m;
     double2* __restrict__ st = a.bst + g * M + m;          // state s at st[s * RS]
@@ -335,7 +335,6 @@ __device__ __forceinline__ void solve_mode_pass(const BvpArgs& a, int64_t m, int
                     const int k = k0 + j;
                     if (k < n) {
                         const double2 r = rv[j];
-                        F[(int64_t)k * RS] = r;
                         const double2 d = (k < 2) ? cscale(r, ivv[j])
                                                   : cscale(cfma(k2 * q_lo[k], dm2, r), ivv[j]);
                         B[(int64_t)k * RS] = d;
@@ -375,7 +374,7 @@ __device__ __forceinline__ void solve_mode_pass(const BvpArgs& a, int64_t m, int
                         ap[j] = (k + 2 < n) ? (mat ? B : A)[(int64_t)(k + 2) * RS]
                                             : make_double2(0, 0);
                         abv[j] = (mat && k + 2 < n) ? aib[k + 2] : 0.0;
-                        fv[j] = F[(int64_t)k * RS];
+                        fv[j] = fsc_at(k);            // f_sc re-derived from the raw column
                         ivv[j] = iv[k];
                     }
                 }
@@ -1361,8 +1360,7 @@ void bvp_solve_view(Plan* p, bool two_grids, int mode, bool correction, const Mo
     a.sbh = reinterpret_cast<const double2*>(p->d_sbh) + v.m0;
     a.sth = reinterpret_cast<const double2*>(p->d_sth) + v.m0;
     a.ext = reinterpret_cast<double2*>(p->d_ext);
-    a.scrF = reinterpret_cast<double2*>(p->d_scr);
-    a.scrA = a.scrF + (int64_t)p->Nz * 2 * v.M;
+    a.scrA = reinterpret_cast<double2*>(p->d_scr);
     a.scrB = a.scrA + (int64_t)p->Nz * 2 * v.M;
     a.inv_nxy = 1.0 / (double)p->NXY;
     a.mom = reinterpret_cast<double2*>(p->d_mom);
