@@ -1736,10 +1736,11 @@ void near_eval(Plan* p, const double* d_eval, const int* d_order, int64_t ne,
         if (k.fp32) near_fused_kernel<true, 6, true, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
         else near_fused_kernel<false, 6, true, true><<<148, NB_THREADS, 0, p->stream>>>(ac);
     } else {
-        // fp32 far pairs at 10 CTAs / SM (48 registers): 3.33 vs 3.52 ms at 8
-        // fp64 at 8 CTAs / SM (64 registers): 7 / 9 / 10 measured 4.35 / 4.28 / 4.69
-        // vs 4.27 ms
-        if (k.fp32) near_eval_kernel<true, 10, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
+        // fp32 far pairs at 14 CTAs / SM (36 registers, small spills): 10 / 11 /
+        // 12 / 14 / 16 measured 3.20 / 3.15 / 3.14 / 3.10 / 3.10 ms (round 1:
+        // 10 vs 8, 3.33 vs 3.52 ms); fp64 at 8 CTAs / SM (64 registers): 7 / 9
+        // / 10 measured 4.35 / 4.28 / 4.69 vs 4.27 ms
+        if (k.fp32) near_eval_kernel<true, 14, true><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         else near_eval_kernel<true, 8><<<nblk, NB_THREADS, 0, p->stream>>>(a);
         SE_LAUNCHED(p);
         if (k.fp32) near_eval_kernel<false, 6, true><<<nblk_c, NB_THREADS, 0, p->stream>>>(ac);
