@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cstdlib>
+
 #include "se_internal.cuh"
 
 namespace se {
@@ -245,6 +247,9 @@ struct TpPlan {
     bool graph = false;
     cudaGraphExec_t gexec = nullptr;
     cudaStream_t cap_stream = nullptr;
+    // the near field forked onto `side` next to the grid part (SE_TP_FORK)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     struct Key {
         const void *pos = nullptr, *q = nullptr, *out = nullptr;
         int64_t n = -1; double g_t = 0, radius = 0, g_w = 0, xi = 0, r_cut = 0;
@@ -257,6 +262,9 @@ struct TpPlan {
         if (dev >= 0) cudaSetDevice(dev);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (cap_stream) cudaStreamDestroy(cap_stream);
+        if (side) cudaStreamDestroy(side);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
         pairs.release();
         if (fwd) cufftDestroy(fwd);
         if (inv) cufftDestroy(inv);
@@ -435,6 +443,27 @@ static void tp_forces_eager(TpPlan* p, const double* d_pos, const double* d_q, i
     double* d_far = p->d_pts + 4 * p->cap;
     double* d_near = d_far + 3 * p->cap;
     const TpGrid g = tp_grid(p, g_t, radius);
+    static const bool fork = [] {
+        const char* e = std::getenv("SE_TP_FORK");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    // the near field (pairs -> d_near) and the grid part (-> d_far) share
+    // only the inputs: the pair pass runs on a high-priority side stream
+    // next to the spread / FFTs / interpolation and joins before the sum
+    const bool forked = fork && n > 0;
+    if (forked) {
+        if (!p->side) {
+            int lo = 0, hi = 0;
+            SE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            SE_CUDA(cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, hi));
+            SE_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+            SE_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+        }
+        SE_CUDA(cudaEventRecord(p->ev_fork, p->stream));
+        SE_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+        tp_near_forces(d_pos, d_q, n, p->L, r_cut, g_w, xi, p->eps, d_near, p->side, p->pairs);
+        SE_CUDA(cudaEventRecord(p->ev_join, p->side));
+    }
     SE_CUDA(cudaMemsetAsync(p->d_grid, 0, p->G * sizeof(double), p->stream));
     const unsigned nb = (unsigned)((n + TP_WARPS - 1) / TP_WARPS);
     if (n > 0) {
@@ -446,7 +475,8 @@ static void tp_forces_eager(TpPlan* p, const double* d_pos, const double* d_q, i
     tp_interp_kernel<<<nb, TP_WARPS * 32, 0, p->stream>>>(g, d_pos, n, p->d_grid + p->Gs,
                                                           p->h[0] * p->h[1] * p->h[2], d_far);
     SE_CUDA(cudaGetLastError());
-    tp_near_forces(d_pos, d_q, n, p->L, r_cut, g_w, xi, p->eps, d_near, p->stream, p->pairs);
+    if (forked) SE_CUDA(cudaStreamWaitEvent(p->stream, p->ev_join, 0));
+    else tp_near_forces(d_pos, d_q, n, p->L, r_cut, g_w, xi, p->eps, d_near, p->stream, p->pairs);
     tp_combine_kernel<<<(unsigned)((3 * n + 255) / 256), 256, 0, p->stream>>>(d_q, d_far, d_near,
                                                                             n, d_forces);
     SE_CUDA(cudaGetLastError());
