@@ -1108,6 +1108,20 @@ __global__ void __launch_bounds__(256, 2) zdct_inv_kernel(DctArgs a, AsmArgs2 q,
             dst[1] = acc[mt][t][1];
         }
     }
+    // per-mode constants of the CTA's MPB modes, once per CTA (the i k
+    // multipliers need a 64-bit division of the mode index)
+    __shared__ double s_ik[MPB][2];
+    if (tid < MPB) {
+        const int64_t m = mb + tid;
+        double ikx = 0.0, iky = 0.0;
+        if (q.forces && m < q.Mv) {
+            const int64_t gm = q.m0 + m;
+            const int ix = (int)(gm / q.Nyh), iy = (int)(gm % q.Nyh);
+            ikx = (q.Nx % 2 == 0 && ix == q.Nx / 2) ? 0.0 : q.kx[ix];
+            iky = (q.Ny % 2 == 0 && iy == q.Ny / 2) ? 0.0 : q.ky[iy];
+        }
+        s_ik[tid][0] = ikx; s_ik[tid][1] = iky;
+    }
     __syncthreads();
     const int N = a.n - 1;
     for (int e = tid; e < a.n * MPB; e += blockDim.x) {
@@ -1149,10 +1163,7 @@ __global__ void __launch_bounds__(256, 2) zdct_inv_kernel(DctArgs a, AsmArgs2 q,
         };
         out[0] = mk(v.x, v.y);
         if (q.forces) {
-            const int64_t gm = q.m0 + m;
-            const int ix = (int)(gm / q.Nyh), iy = (int)(gm % q.Nyh);
-            const double ikx = (q.Nx % 2 == 0 && ix == q.Nx / 2) ? 0.0 : q.kx[ix];
-            const double iky = (q.Ny % 2 == 0 && iy == q.Ny / 2) ? 0.0 : q.ky[iy];
+            const double ikx = s_ik[mi][0], iky = s_ik[mi][1];
             out[q.M] = mk(-ikx * v.y, ikx * v.x);            // i kx v
             out[2 * q.M] = mk(-iky * v.y, iky * v.x);        // i ky v
             out[3 * q.M] = mk(d.x, d.y);
