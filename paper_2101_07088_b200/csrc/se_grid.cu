@@ -569,6 +569,7 @@ __global__ void __launch_bounds__(IW * 32, MINB) interp_kernel(InterpArgsT<T> a)
 #pragma unroll
         for (int c = 0; c < NF; ++c) acc[m][c] = T(0);
     const int Wx = xmax - xmin + SX, Wy = ymax - ymin + SY;
+    const int sx32 = 32 / Wy, sy32 = 32 - sx32 * Wy;
     const int64_t zstride = 4 * a.NXY;
     for (int zc = zlo; zc < zhi; zc += IZC) {
         const int nz = min(IZC, zhi - zc);
@@ -597,8 +598,19 @@ __global__ void __launch_bounds__(IW * 32, MINB) interp_kernel(InterpArgsT<T> a)
             }
             gi.sz0[lane] = sz0; gi.sz1[lane] = sz1;
         }
+        // fp64: (ux, uy) of this lane's column advanced by 32 columns per
+        // step without an integer division per column (3.51 -> 3.48 ms; the
+        // fp32 kernel keeps the division: 2.66 vs 2.69 ms)
+        int cux = lane / Wy, cuy = lane - cux * Wy;
         for (int p = lane; p < Wx * Wy; p += 32) {
-            const int ux = p / Wy, uy = p - ux * Wy;
+            int ux, uy;
+            if constexpr (sizeof(T) == sizeof(double)) {
+                ux = cux; uy = cuy;
+                cux += sx32; cuy += sy32;
+                if (cuy >= Wy) { cuy -= Wy; ++cux; }
+            } else {
+                ux = p / Wy; uy = p - ux * Wy;
+            }
             T wxy[IG];
             bool any = false;
 #pragma unroll
